@@ -1,0 +1,433 @@
+"""Benchmark: fwd+bwd megapixels/s of the splat renderer (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+One step = forward + backward of the hot path for each of this rank's
+views (N=1: config C3 — 1M Gaussians, 1920x1080, softplus(κ=20), global
+depth order chunk_size=1 — the configuration the BASELINE metric is quoted
+on), gradients accumulated into one flat buffer, plus one NCCL all-reduce
+of that buffer when N > 1 (weak scaling: views_per_rank views per GPU).
+
+value : Mpix/s with the scene and seeds resident in HBM (device path,
+        CUDA events on the launching stream, max over ranks).
+e2e   : the same metric through the public drop-in API
+        (render_with_gradients on float64 numpy arrays): host->device copy of
+        the scene and seed and device->host copy of image + gradients inside
+        the timed region.
+roofline: for the kernel with the largest share of the step, measured live
+        (per-phase CUDA events, include/nxs.h nxs_view_timings).
+cpu_baseline: the CPU oracle port (oracle/splat_oracle.py, brute force over
+        all Gaussians per pixel like the reference) on a bounded pixel sample,
+        all host cores, rank 0 only.
+--impl reference: times that CPU implementation as the reference arm.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "fwd+bwd megapixels/sec at 1M Gaussians 1080p; fraction of FP32/HBM roofline"
+# algorithmic flops per event (FMA = 2)
+F_TEST = 24
+F_FWD = {"linear": 37, "exponential": 38, "blended": 40, "vicini": 40, "softplus": 43,
+         "quadratic": 39, "power_law": 43}
+F_BWD = {"softplus": 146, "power_law": 146}
+F_BWD_DEFAULT = 140
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=30)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--gaussians", type=int, default=1_000_000)
+    p.add_argument("--width", type=int, default=1920)
+    p.add_argument("--height", type=int, default=1080)
+    p.add_argument("--model", default="softplus")
+    p.add_argument("--param", type=float, default=None)
+    p.add_argument("--views-per-rank", type=int, default=1)
+    p.add_argument("--e2e-steps", type=int, default=5)
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def model_of(a):
+    from paper_2603_02887_b200 import TransmittanceModel
+    defaults = {"softplus": 20.0, "blended": 0.5, "vicini": 0.5, "quadratic": 0.5,
+                "power_law": 2.0}
+    p = a.param if a.param is not None else defaults.get(a.model, 0.0)
+    return TransmittanceModel(a.model, p)
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle port on a bounded sample (rank 0)
+# ---------------------------------------------------------------------------
+
+_CPU = {}
+
+
+def _cpu_worker(args):
+    wid, budget = args
+    from oracle import splat_oracle as O
+    sc, cam, model, seed = _CPU["sc"], _CPU["cam"], _CPU["model"], _CPU["seed"]
+    rng = np.random.default_rng(100 + wid)
+    t0 = time.perf_counter()
+    done = 0
+    while time.perf_counter() - t0 < budget or done == 0:
+        px = rng.choice(cam.width * cam.height, 1, replace=False)
+        fwd = O.forward(sc, cam, model, np.zeros(3), chunk_size=1, pixels=px, prune=False,
+                        keep_state=True)
+        O.backward(sc, cam, model, np.zeros(3), fwd, seed.reshape(-1, 3)[px])
+        done += 1
+    return done, time.perf_counter() - t0
+
+
+def cpu_baseline(arrs, cam, model, seconds):
+    import multiprocessing as mp
+    from oracle import splat_oracle as O
+    _CPU.update(sc=O.Scene.of(arrs), cam=cam, model=model,
+                seed=np.random.default_rng(1000).uniform(0.2, 1.0, (cam.height, cam.width, 3)))
+    cores = os.cpu_count() or 1
+    workers = max(1, min(cores, 32))
+    # each worker holds ~1M x a few float64 temporaries per pixel
+    try:
+        import psutil
+        mem = psutil.virtual_memory().available
+        workers = max(1, min(workers, int(mem / 3.0e9)))
+    except Exception:
+        pass
+    ctx = mp.get_context("fork")
+    t0 = time.perf_counter()
+    with ctx.Pool(workers) as pool:
+        res = pool.map(_cpu_worker, [(i, seconds) for i in range(workers)])
+    wall = time.perf_counter() - t0
+    px = sum(r[0] for r in res)
+    try:
+        cpu = subprocess.run(["lscpu"], capture_output=True, text=True).stdout
+        name = [ln.split(":", 1)[1].strip() for ln in cpu.splitlines() if "Model name" in ln][0]
+    except Exception:
+        name = "unknown"
+    return {"value": px / wall / 1e6, "unit": "Mpix/s", "cores": workers, "kind": "port",
+            "sample": f"{px} random pixels of the same 1M-Gaussian view, fwd+bwd, brute force "
+                      f"over all Gaussians per pixel (reference algorithm, oracle/splat_oracle.py"
+                      f"), {workers} processes x ~{seconds:.0f}s on {name}; wall {wall:.1f}s"}
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------
+
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.p = None
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in out.strip().splitlines():
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# main
+# ---------------------------------------------------------------------------
+
+def main():
+    a = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    model = model_of(a)
+
+    if a.impl == "reference":
+        return reference_arm(a, rank, model)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_02887_b200 import (DeviceScene, _native, render_with_gradients)
+    from paper_2603_02887_b200.dp import DataParallelStep, GradBuffer, device_view_renderer
+    from paper_2603_02887_b200.scenes import canonical_camera, canonical_scene, canonical_seed
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    W, H, vpr = a.width, a.height, a.views_per_rank
+    n_views = vpr * world
+    arrs = canonical_scene(a.gaussians, seed=5)
+    dev = DeviceScene.from_arrays(arrs)
+    if n_views == 1:
+        cams = [canonical_camera(W, H)]
+    else:
+        cams = [canonical_camera(W, H, v, n_views) for v in range(n_views)]
+    seeds = {v: torch.as_tensor(canonical_seed(W, H, v), dtype=torch.float32, device="cuda")
+             for v in range(n_views)}
+    bg = np.zeros(3)
+    grads = GradBuffer(len(arrs), arrs.sh.shape[2], device="cuda")
+    rv = device_view_renderer(dev, model, bg, cams, seeds)
+    step = DataParallelStep(n_views, rank, world, grads, rv)
+    my_views = step.views()
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, device events, barrier + sync both sides
+    clocks = Clocks(local)
+    time.sleep(0.25)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(a.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    ck = clocks.stop()
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    ms_step = ms_max / a.steps
+    mpix = W * H * n_views / (ms_step / 1e3) / 1e6
+
+    # ---- per-phase device timings (same steps, events inside the library)
+    views = rv.views
+    phase_tot = {}
+    for _ in range(max(3, min(a.steps, 10))):
+        step()
+        for v in my_views:
+            for k, x in views[v].timings().items():
+                phase_tot[k] = phase_tot.get(k, 0.0) + x
+    nprof = max(3, min(a.steps, 10))
+    phase = {k: x / nprof / max(1, len(my_views)) for k, x in phase_tot.items()}
+
+    # ---- event counts (instrumented run, not timed) for the blend roofline
+    from paper_2603_02887_b200 import backward_device, forward_device
+    cview = _native.View()
+    forward_device(cview, dev, cams[my_views[0]], model, bg, chunk_size=1, count_events=True)
+    backward_device(cview, dev, seeds[my_views[0]])
+    st = cview.stats()
+    cview.close()
+
+    roof = roofline(a, model, phase, st)
+
+    # ---- end to end through the public API with host buffers
+    e2e = None
+    if not a.no_e2e:
+        e2e = e2e_arm(a, arrs, cams, model, my_views, world, render_with_gradients)
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        cpu = cpu_baseline(arrs, cams[0], model, a.cpu_seconds)
+
+    if rank == 0:
+        launches_per_view = 7  # depth_keys, project, emit, ranges, blend_fwd, blend_bwd, chain
+        out = {
+            "metric": METRIC,
+            "value": round(mpix, 3),
+            "unit": "Mpix/s",
+            "n_gpus": world,
+            "steps": a.steps,
+            "warmup": a.warmup,
+            "ms_per_step": round(ms_step, 4),
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f32",
+            "data": "synthetic",
+            "config": {
+                "workload": (f"C3: {a.gaussians} Gaussians (canonical synthetic scene, seed 5), "
+                             f"{W}x{H}, {model.describe()}, chunk_size=1 (global depth order), "
+                             f"fwd+bwd, {vpr} view(s) per GPU"
+                             + (", NCCL all-reduce of gradients" if world > 1 else "")),
+                "gaussians": a.gaussians, "width": W, "height": H,
+                "views_per_gpu": vpr, "total_views": n_views,
+                "parallelism": f"dp{world} over views",
+                "l2": "inputs larger than L2 (records 128 MB + pairs + 192 MB moments per view)",
+            },
+            "phase_ms": {k: round(v, 4) for k, v in phase.items()},
+            "events": {k: st[k] for k in ("n_pairs", "n_tests_fwd", "n_composited",
+                                           "n_tests_bwd", "n_entries_bwd")},
+            "roofline": roof,
+            "clocks": ck,
+            "gpu_launches": launches_per_view * len(my_views) * a.steps,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def roofline(a, model, phase, st):
+    """Dominant kernel vs its bound.  Blend kernels: FP32 pipe (algorithmic
+    flops); sort/projection/chain: HBM bytes."""
+    peaks = {}
+    try:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        pass
+    sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    import torch
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    fp32_peak = sms * 128 * 2 * sm_mhz * 1e6 / 1e12  # TFLOP/s
+    var = model.variant
+    blend_ms = phase.get("blend_fwd", 0.0) + phase.get("blend_bwd", 0.0)
+    flops = (st["n_tests_fwd"] * F_TEST + st["n_composited"] * F_FWD.get(var, 40)
+             + st["n_tests_bwd"] * F_TEST + st["n_composited"] * F_BWD.get(var, F_BWD_DEFAULT))
+    blend = {"bound": "tensor" if False else "fp32", "achieved": flops / (blend_ms / 1e3) / 1e12
+             if blend_ms > 0 else 0.0, "peak": round(fp32_peak, 2), "unit": "TFLOP/s"}
+    P, npairs = a.gaussians, st["n_pairs"]
+    # pair sort: 2 LSD passes over (u32 tile key, u32 rank) pairs, read + write
+    sort_bytes = npairs * 8 * 2 * 2
+    proj_bytes = P * (92 + 8 + 128 + 16 + 8)  # params + order in; record + rect + count out
+    shares = {"blend (fwd+bwd)": blend_ms, "pair_sort": phase.get("pair_sort", 0.0),
+              "depth_sort": phase.get("depth_sort", 0.0), "project": phase.get("project", 0.0)}
+    dom = max(shares, key=shares.get)
+    total = sum(phase.values())
+    if dom == "blend (fwd+bwd)":
+        r = dict(blend, kernel=dom)
+    elif dom == "pair_sort":
+        ach = sort_bytes / (phase["pair_sort"] / 1e3) / 1e9
+        r = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "kernel": dom}
+    elif dom == "project":
+        ach = proj_bytes / (phase["project"] / 1e3) / 1e9
+        r = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "kernel": dom}
+    else:
+        b = P * (8 + 4) * 2 * 8 + P * 12
+        ach = b / (phase["depth_sort"] / 1e3) / 1e9
+        r = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "kernel": dom}
+    r["achieved"] = round(r["achieved"], 3)
+    r["frac"] = round(r["achieved"] / r["peak"], 4) if r["peak"] else None
+    r["traffic"] = None
+    r["share_of_step"] = round(shares[dom] / total, 3) if total else None
+    r["blend_fp32"] = {"achieved_tflops": round(blend["achieved"], 3),
+                       "frac_of_derived_peak": round(blend["achieved"] / fp32_peak, 4),
+                       "flops": flops, "ms": round(blend_ms, 4)}
+    r["peak_source"] = ("MEASURED_PEAKS.json hbm_gbs (measured copy)" if r["unit"] == "GB/s"
+                        else f"derived: {sms} SMs x 128 FMA x 2 x {sm_mhz:.0f} MHz "
+                             "(MEASURED_PEAKS.json sm_max_mhz)")
+    return r
+
+
+def e2e_arm(a, arrs, cams, model, my_views, world, render_with_gradients):
+    """Public drop-in API on host float64 arrays: every step uploads the
+    scene + seed and downloads rgb/overdraw/residual + gradients."""
+    import torch
+    from paper_2603_02887_b200.scenes import canonical_seed
+    seeds = {v: canonical_seed(a.width, a.height, v) for v in my_views}
+
+    def one():
+        for v in my_views:
+            res, g = render_with_gradients(arrs, cams[v], model, np.zeros(3), seeds[v],
+                                           chunk_size=1)
+        return res, g
+
+    one()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(a.e2e_steps):
+        one()
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / a.e2e_steps
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+    P, C = len(arrs), arrs.sh.shape[2]
+    npx = a.width * a.height
+    h2d = len(my_views) * (P * (3 + 3 + 4 + 1 + 3 * C) * 4 + npx * 3 * 4)
+    d2h = len(my_views) * (npx * (3 + 1 + 1) * 8 + P * (3 + 3 + 4 + 1 + 3 * C) * 8)
+    return {"value": round(npx * len(my_views) * world / dt / 1e6, 3), "unit": "Mpix/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "ms_per_step": round(dt * 1e3, 3),
+            "api": "render_with_gradients(numpy float64 SceneArrays, chunk_size=1)"}
+
+
+def reference_arm(a, rank, model):
+    """The reference's CPU implementation of the path (oracle port, the
+    reference is not installed on the GPU box), rank 0 only."""
+    if rank != 0:
+        return
+    from paper_2603_02887_b200.scenes import canonical_camera, canonical_scene
+    arrs = canonical_scene(a.gaussians, seed=5)
+    cam = canonical_camera(a.width, a.height)
+    per_step = max(2.0, min(20.0, 150.0 / max(1, a.steps + a.warmup)))
+    vals = []
+    last = None
+    for i in range(a.warmup + a.steps):
+        last = cpu_baseline(arrs, cam, model, per_step)
+        if i >= a.warmup:
+            vals.append(last["value"])
+    v = statistics.median(vals) if vals else last["value"]
+    out = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": v,
+        "unit": "Mpix/s",
+        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+        "steps": a.steps,
+        "warmup": a.warmup,
+        "higher_is_better": True,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"C3: {a.gaussians} Gaussians, {a.width}x{a.height}, "
+                               f"{model.describe()}, chunk_size=1, fwd+bwd (sampled pixels)"},
+        "cpu_baseline": dict(last, value=v),
+        "e2e": {"value": v, "unit": "Mpix/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

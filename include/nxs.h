@@ -1,0 +1,185 @@
+/*
+ * nxs.h — C-ABI of the B200 generalized-transmittance splat renderer.
+ *
+ * Drop-in boundary for the reference's image renderer (reference
+ * pkg/src/nexsplat/render.py, module `nexsplat.render`, __all__ at
+ * render.py:34-41).  The reference is pure Python/numpy and has no FFI of
+ * its own; these entry points are what its Python API binds to (the
+ * ctypes binding is paper_2603_02887_b200/_native.py; INTEGRATION.md shows
+ * the stub a nexsplat maintainer would add).  Plain C types only: no torch,
+ * no CUDA types in the signatures (streams are passed as void*).
+ *
+ * Entry point  ->  reference interface it replaces
+ *   nxs_forward        render_forward_cached / render      (render.py:361-425;
+ *                      core _forward_sweep, render.py:147-217)
+ *   nxs_backward       render_backward                      (render.py:428-442;
+ *                      core _backward_sweep, render.py:220-347)
+ *   nxs_cache_export   the cache dict of render_forward_cached
+ *                      (render.py:214-217: sat, e_k, t_k, theta0)
+ *   nxs_depth_order    _depth_chunks ordering               (render.py:350-358)
+ *
+ * Conventions
+ *   - Status: 0 on success, negative NXS_ERR_* on failure; no exceptions
+ *     cross the ABI.  nxs_error_string() / nxs_last_error() describe it.
+ *   - All array pointers are DEVICE pointers (cudaMalloc / torch CUDA
+ *     tensors) unless stated; the caller owns them.  Work is enqueued on
+ *     `stream` (a cudaStream_t, NULL = legacy default stream).
+ *   - nxs_forward synchronises `stream` once, to read the number of
+ *     (tile, Gaussian) pairs it must sort; everything else is asynchronous.
+ *   - A view (nxs_view) owns the per-view device workspace: projected
+ *     records, tile lists and the per-pixel replay cache.  It persists from
+ *     nxs_forward to nxs_backward of the same view ("settings must match the
+ *     forward call", render.py:435-436).  Distinct views are independent and
+ *     may be used concurrently on distinct streams.
+ *   - Gradients ACCUMULATE (+=) into the caller's buffers, so a rank's views
+ *     sum into one buffer before the data-parallel all-reduce.
+ */
+#ifndef NXS_H
+#define NXS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NXS_ABI_VERSION 1
+
+/* status codes */
+#define NXS_OK 0
+#define NXS_ERR_INVALID (-1)       /* bad argument (shape, pointer, option) */
+#define NXS_ERR_UNSUPPORTED (-2)   /* mode/model combination not implemented */
+#define NXS_ERR_CUDA (-3)          /* a CUDA call failed */
+#define NXS_ERR_NOMEM (-4)         /* device allocation failed */
+#define NXS_ERR_STATE (-5)         /* backward without a matching forward */
+#define NXS_ERR_GEOMETRY (-6)      /* Gaussian straddles the near plane (not yet supported) */
+
+/* transmittance variants: order of reference transmittance.py:32-40 */
+#define NXS_MODEL_EXPONENTIAL 0
+#define NXS_MODEL_LINEAR 1
+#define NXS_MODEL_QUADRATIC 2
+#define NXS_MODEL_BLENDED 3
+#define NXS_MODEL_VICINI 4
+#define NXS_MODEL_POWER_LAW 5
+#define NXS_MODEL_SOFTPLUS 6
+
+/* opts.flags */
+#define NXS_FLAG_COUNT_EVENTS 1    /* count tests/composites (instrumented run) */
+
+/* ordering: opts.chunk_size (reference render(..., chunk_size=)) */
+#define NXS_CHUNK_EXACT 0          /* chunk_size=None: exact per-pixel depth order */
+
+/* TransmittanceModel (reference transmittance.py:54-79): variant + param */
+typedef struct {
+    int32_t variant;
+    double param;
+} nxs_model;
+
+/* Camera (reference primitives.py:153-190): rotation maps camera axes
+ * (right, down, forward) to world, row-major 3x3; pixel (row i, col j)
+ * looks along rotation * ((j+0.5-cx)/focal, (i+0.5-cy)/focal, 1). */
+typedef struct {
+    double position[3];
+    double rotation[9];
+    double focal, cx, cy;
+    int32_t width, height;
+} nxs_camera;
+
+/* render keyword arguments (reference render.py:361-364) */
+typedef struct {
+    int32_t max_splats;      /* default 128 */
+    double alpha_cutoff;     /* default 1/255 */
+    double near_plane;       /* default 1e-4 */
+    int32_t chunk_size;      /* NXS_CHUNK_EXACT (None) or >= 1 */
+    int32_t flags;           /* NXS_FLAG_* */
+} nxs_opts;
+
+/* SceneArrays (reference render.py:44-52), device float32, row-major:
+ * centers (P,3), scales (P,3), quats (P,4) (w,x,y,z; normalised on use),
+ * opacities (P), sh (P,3,C) with C in {1,4}. */
+typedef struct {
+    const float* centers;
+    const float* scales;
+    const float* quats;
+    const float* opacities;
+    const float* sh;
+    int64_t count;
+    int32_t sh_coeffs;
+} nxs_scene;
+
+/* per-view statistics of the last forward/backward */
+typedef struct {
+    int64_t n_gaussians;
+    int64_t n_visible;        /* Gaussians with >= 1 tile */
+    int64_t n_pairs;          /* (tile, Gaussian) pairs sorted */
+    int64_t n_straddling;     /* Gaussians crossing the near plane */
+    int64_t n_tiles;
+    int64_t n_tests_fwd;      /* (pixel, list entry) pairs tested   [COUNT_EVENTS] */
+    int64_t n_composited;     /* sum of overdraw                     [COUNT_EVENTS] */
+    int64_t n_tests_bwd;      /* pairs re-tested by the backward     [COUNT_EVENTS] */
+    int64_t n_entries_bwd;    /* (tile, entry) pairs replayed        [COUNT_EVENTS] */
+} nxs_stats;
+
+typedef struct nxs_view nxs_view;
+
+/* device-timed phases of the last forward + backward (CUDA events on the
+ * call's stream), order of nxs_view_timings' output */
+#define NXS_PHASES 10
+/* 0 depth sort (K0 + radix sort), 1 projection (K1), 2 tile-count scan
+ * (+ host sync), 3 pair emission (K2), 4 pair sort by tile, 5 tile ranges,
+ * 6 forward blend (K3), 7 moment clear, 8 backward blend (K4), 9 chain (K5) */
+
+int nxs_abi_version(void);
+const char* nxs_error_string(int code);
+/* message of the last error on this thread (with CUDA detail if any) */
+const char* nxs_last_error(void);
+
+int nxs_view_create(nxs_view** out);
+int nxs_view_destroy(nxs_view* view);
+int nxs_view_stats(const nxs_view* view, nxs_stats* out);
+/* bytes of device memory currently held by the view */
+int64_t nxs_view_bytes(const nxs_view* view);
+
+/* Milliseconds per phase (NXS_PHASES entries) of the last nxs_forward /
+ * nxs_backward of this view; waits for those phases to finish. */
+int nxs_view_timings(nxs_view* view, float* ms, int n);
+
+/* Forward render (render_forward_cached).  background: 3 host floats.
+ * rgb (H*W*3), overdraw (H*W), residual (H*W): device outputs, row-major
+ * over (row, col).  Fills the view's replay cache. */
+int nxs_forward(nxs_view* view, const nxs_scene* scene, const nxs_camera* camera,
+                const nxs_model* model, const nxs_opts* opts, const float background[3],
+                float* rgb, int32_t* overdraw, float* residual, void* stream);
+
+/* Backward (render_backward) for adjoint seed d loss / d rgb (device,
+ * H*W*3).  Replays the view's last forward; the scene must be unchanged.
+ * Accumulates into g_centers (P,3), g_scales (P,3), g_quats (P,4),
+ * g_opacities (P), g_sh (P,3,C) (device float32). */
+int nxs_backward(nxs_view* view, const nxs_scene* scene, const float* seed,
+                 float* g_centers, float* g_scales, float* g_quats,
+                 float* g_opacities, float* g_sh, void* stream);
+
+/* Reference cache fields of the last forward (device outputs, any may be
+ * NULL): sat (H*W uint8), e_k (H*W*3), t_k (H*W), theta0 (H*W*3). */
+int nxs_cache_export(nxs_view* view, uint8_t* sat, float* e_k, float* t_k,
+                     float* theta0, void* stream);
+
+/* Front-to-back depth order of the last forward: order (P int32, device),
+ * order[rank] = Gaussian index, stable by fp64 view depth (render.py:355-357). */
+int nxs_depth_order(nxs_view* view, int32_t* order, void* stream);
+
+/* Binning of the last forward, for the bit-exact checks against the C
+ * restatement (oracle/binning_oracle.c): tile rectangle per rank
+ * (P x int32[4] = tx0,ty0,tx1,ty1; empty = -1), tile ranges (n_tiles x
+ * int32[2]) and the sorted pair values (n_pairs ranks). */
+int nxs_binning_export(nxs_view* view, int32_t* rects, int32_t* ranges,
+                       int32_t* pair_ranks, void* stream);
+
+/* Projected per-rank records (P x 32 float32) of the last forward. */
+int nxs_records_export(nxs_view* view, float* records, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NXS_H */

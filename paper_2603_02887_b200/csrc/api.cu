@@ -1,0 +1,538 @@
+// C-ABI of libnxs (include/nxs.h): view workspace management and the
+// per-view pipeline
+//   K0 depth keys -> CUB stable radix sort (64-bit fp64 keys) -> order
+//   K1 projection + conic tile bbox (per rank)
+//   CUB exclusive scan of tile counts -> K2 pair emission (rank order)
+//   CUB stable radix sort of pairs by tile id -> tile ranges
+//   K3 forward blend                                  (nxs_forward)
+//   K4 back-to-front replay -> moments -> K5 chain    (nxs_backward)
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/nxs.h"
+#include "nxs_internal.cuh"
+
+namespace nxs {
+void launch_depth_keys(const float*, int64_t, const CamDev&, unsigned long long*, uint32_t*,
+                       cudaStream_t);
+void launch_project(const float*, const float*, const float*, const float*, const float*, int,
+                    int64_t, const uint32_t*, const CamDev&, double, double, unsigned long long*,
+                    int4*, float4*, unsigned long long*, cudaStream_t);
+void launch_emit_pairs(const int4*, const unsigned long long*, int64_t, int, uint32_t*, uint32_t*,
+                       cudaStream_t);
+void launch_tile_ranges(const uint32_t*, int64_t, int2*, cudaStream_t);
+void launch_blend_fwd(bool, int, const float4*, const uint32_t*, const int2*, const CamDev&,
+                      const ModelDev&, int, float, const float*, float*, int32_t*, float*,
+                      const PixCache&, Counters*, cudaStream_t);
+void launch_blend_bwd(bool, int, const float4*, const uint32_t*, const int2*, const CamDev&,
+                      const ModelDev&, float, const float*, const float*, const PixCache&,
+                      double*, Counters*, cudaStream_t);
+void launch_chain(const float*, const float*, const float*, int, int64_t, const uint32_t*,
+                  const CamDev&, const double*, float*, float*, float*, float*, float*,
+                  cudaStream_t);
+}  // namespace nxs
+
+using namespace nxs;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define NXS_CUDA(call)                                                                 \
+  do {                                                                                 \
+    cudaError_t _e = (call);                                                           \
+    if (_e != cudaSuccess)                                                             \
+      return fail(_e == cudaErrorMemoryAllocation ? NXS_ERR_NOMEM : NXS_ERR_CUDA,      \
+                  std::string(#call) + ": " + cudaGetErrorString(_e));                 \
+  } while (0)
+
+#define NXS_LAUNCHED(what)                                                             \
+  do {                                                                                 \
+    cudaError_t _e = cudaGetLastError();                                               \
+    if (_e != cudaSuccess)                                                             \
+      return fail(NXS_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(_e));    \
+  } while (0)
+
+struct Buf {
+  void* p = nullptr;
+  size_t cap = 0;
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+  cudaError_t ensure(size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    if (bytes <= cap) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = bytes + bytes / 8;  // headroom against regrowth
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+int bits_for(uint32_t n) {
+  int b = 1;
+  while (b < 32 && (1u << b) < n) ++b;
+  return b;
+}
+
+}  // namespace
+
+struct nxs_view {
+  // per Gaussian
+  Buf dkeys_in, dkeys_out, idx_in, idx_out, records, rects, ntiles, offsets, moments;
+  // per pair
+  Buf pk_in, pk_out, pv_in, pv_out;
+  // per tile / pixel
+  Buf ranges, c_last, c_sat, c_tk, c_thi, c_tlo, c_P, c_ck, c_Pck, c_ek, c_th0;
+  Buf temp, dev_small;  // CUB temp; counters
+  unsigned long long* host_small = nullptr;  // pinned
+  // phase events: see NXS_PHASES in include/nxs.h
+  cudaEvent_t ev[NXS_PHASES + 2] = {};
+  bool ev_ok = false;
+  bool ev_fwd = false, ev_bwd = false;
+  // state of the last forward
+  bool have_fwd = false;
+  CamDev cam{};
+  ModelDev model{};
+  nxs_opts opts{};
+  float bg[3] = {0, 0, 0};
+  int64_t P = 0;
+  int32_t C = 1;
+  int64_t n_pairs = 0;
+  int n_tiles = 0;
+  const float* scene_centers = nullptr;
+  nxs_stats stats{};
+
+  ~nxs_view() {
+    Buf* all[] = {&dkeys_in, &dkeys_out, &idx_in, &idx_out, &records, &rects, &ntiles, &offsets,
+                  &moments, &pk_in, &pk_out, &pv_in, &pv_out, &ranges, &c_last, &c_sat, &c_tk,
+                  &c_thi, &c_tlo, &c_P, &c_ck, &c_Pck, &c_ek, &c_th0, &temp, &dev_small};
+    for (Buf* b : all) b->release();
+    if (host_small) cudaFreeHost(host_small);
+    if (ev_ok)
+      for (auto& e : ev) cudaEventDestroy(e);
+  }
+  int64_t bytes() const {
+    const Buf* all[] = {&dkeys_in, &dkeys_out, &idx_in, &idx_out, &records, &rects, &ntiles,
+                        &offsets, &moments, &pk_in, &pk_out, &pv_in, &pv_out, &ranges, &c_last,
+                        &c_sat, &c_tk, &c_thi, &c_tlo, &c_P, &c_ck, &c_Pck, &c_ek, &c_th0,
+                        &temp, &dev_small};
+    int64_t s = 0;
+    for (const Buf* b : all) s += (int64_t)b->cap;
+    return s;
+  }
+  PixCache cache() const {
+    return PixCache{c_last.as<int32_t>(), c_sat.as<uint8_t>(), c_tk.as<float>(),
+                    c_thi.as<float>(), c_tlo.as<float>(), c_P.as<float>(),
+                    c_ck.as<int32_t>(), c_Pck.as<float>(), c_ek.as<float>(),
+                    c_th0.as<float>()};
+  }
+};
+
+namespace {
+
+int make_model(const nxs_model* m, ModelDev& md) {
+  md = ModelDev{};
+  const double p = m->param;
+  switch (m->variant) {
+    case NXS_MODEL_EXPONENTIAL: md.fam = FAM_EXP; break;
+    case NXS_MODEL_LINEAR: md.fam = FAM_LIN; break;
+    case NXS_MODEL_QUADRATIC:
+      if (!(p >= -0.5)) return fail(NXS_ERR_INVALID, "quadratic curvature must be >= -0.5");
+      md.fam = FAM_QUAD;
+      md.c = (float)p;
+      break;
+    case NXS_MODEL_BLENDED:
+    case NXS_MODEL_VICINI:
+      if (!(p >= 0.0 && p <= 1.0)) return fail(NXS_ERR_INVALID, "mix weight must be in [0, 1]");
+      md.fam = FAM_BLEND;
+      md.c = (float)p;
+      break;
+    case NXS_MODEL_POWER_LAW:
+      if (!(p >= -1.0)) return fail(NXS_ERR_INVALID, "power-law exponent must be >= -1");
+      if (p == -1.0) {
+        md.fam = FAM_LIN;
+      } else {
+        md.fam = FAM_POW;
+        md.c = (float)p;
+        md.powmode = std::fabs(p) < 1e-4 ? 2 : 0;
+        md.ex = (float)(-(1.0 + p) / p);
+      }
+      break;
+    case NXS_MODEL_SOFTPLUS:
+      if (!(p >= 10.0)) return fail(NXS_ERR_INVALID, "softplus sharpness must be >= 10");
+      md.fam = FAM_SOFT;
+      md.c = (float)p;
+      md.K = (float)(p / (p + std::log1p(std::exp(-p))));
+      break;
+    default:
+      return fail(NXS_ERR_INVALID, "unknown transmittance variant");
+  }
+  return NXS_OK;
+}
+
+int make_camera(const nxs_camera* c, CamDev& cd) {
+  if (!(c->focal > 0) || c->width <= 0 || c->height <= 0)
+    return fail(NXS_ERR_INVALID, "focal length and image dimensions must be positive");
+  for (int i = 0; i < 3; ++i) cd.o[i] = c->position[i];
+  for (int i = 0; i < 9; ++i) cd.R[i] = c->rotation[i];
+  cd.f = c->focal;
+  cd.cx = c->cx;
+  cd.cy = c->cy;
+  cd.W = c->width;
+  cd.H = c->height;
+  cd.tiles_x = (c->width + TILE - 1) / TILE;
+  cd.tiles_y = (c->height + TILE - 1) / TILE;
+  return NXS_OK;
+}
+
+inline void mark(nxs_view* v, int i, cudaStream_t s) {
+  if (v->ev_ok) cudaEventRecord(v->ev[i], s);
+}
+
+template <class T>
+cudaError_t ensure_n(Buf& b, int64_t n) {
+  return b.ensure((size_t)n * sizeof(T));
+}
+
+}  // namespace
+
+extern "C" {
+
+int nxs_abi_version(void) { return NXS_ABI_VERSION; }
+
+const char* nxs_error_string(int code) {
+  switch (code) {
+    case NXS_OK: return "ok";
+    case NXS_ERR_INVALID: return "invalid argument";
+    case NXS_ERR_UNSUPPORTED: return "unsupported mode or model";
+    case NXS_ERR_CUDA: return "CUDA error";
+    case NXS_ERR_NOMEM: return "out of device memory";
+    case NXS_ERR_STATE: return "backward without a matching forward";
+    case NXS_ERR_GEOMETRY: return "Gaussian crosses the near plane (unsupported geometry)";
+    default: return "unknown error";
+  }
+}
+
+const char* nxs_last_error(void) { return g_last_error.c_str(); }
+
+int nxs_view_create(nxs_view** out) {
+  if (!out) return fail(NXS_ERR_INVALID, "null output pointer");
+  nxs_view* v = new (std::nothrow) nxs_view();
+  if (!v) return fail(NXS_ERR_NOMEM, "host allocation failed");
+  if (cudaHostAlloc((void**)&v->host_small, 8 * sizeof(unsigned long long),
+                    cudaHostAllocDefault) != cudaSuccess) {
+    delete v;
+    cudaGetLastError();
+    return fail(NXS_ERR_CUDA, "cudaHostAlloc failed (no CUDA device?)");
+  }
+  v->ev_ok = true;
+  for (auto& e : v->ev) v->ev_ok = v->ev_ok && cudaEventCreate(&e) == cudaSuccess;
+  *out = v;
+  return NXS_OK;
+}
+
+int nxs_view_destroy(nxs_view* view) {
+  delete view;
+  return NXS_OK;
+}
+
+int nxs_view_stats(const nxs_view* view, nxs_stats* out) {
+  if (!view || !out) return fail(NXS_ERR_INVALID, "null pointer");
+  *out = view->stats;
+  return NXS_OK;
+}
+
+int64_t nxs_view_bytes(const nxs_view* view) { return view ? view->bytes() : 0; }
+
+int nxs_forward(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
+                const nxs_model* model, const nxs_opts* opts, const float background[3],
+                float* rgb, int32_t* overdraw, float* residual, void* stream_) {
+  if (!v || !scene || !camera || !model || !opts || !background || !rgb || !overdraw ||
+      !residual)
+    return fail(NXS_ERR_INVALID, "null argument");
+  cudaStream_t s = (cudaStream_t)stream_;
+  v->have_fwd = false;
+  CamDev cam;
+  ModelDev md;
+  int rc;
+  if ((rc = make_camera(camera, cam)) != NXS_OK) return rc;
+  if ((rc = make_model(model, md)) != NXS_OK) return rc;
+  const int64_t P = scene->count;
+  const int C = scene->sh_coeffs;
+  if (P < 0 || (C != 1 && C != 4)) return fail(NXS_ERR_INVALID, "bad scene size or sh_coeffs");
+  if (P > 0 && (!scene->centers || !scene->scales || !scene->quats || !scene->opacities ||
+                !scene->sh))
+    return fail(NXS_ERR_INVALID, "null scene array");
+  if (P >= (int64_t)1 << 31) return fail(NXS_ERR_INVALID, "more than 2^31 Gaussians");
+  if (opts->chunk_size != 1)
+    return fail(NXS_ERR_UNSUPPORTED,
+                "only the global depth order (chunk_size=1) is implemented on the device");
+  if (!(opts->alpha_cutoff > 0.0) || !(opts->near_plane >= 0.0))
+    return fail(NXS_ERR_INVALID, "alpha_cutoff must be > 0 and near >= 0");
+
+  const int64_t npix = (int64_t)cam.W * cam.H;
+  const int n_tiles = cam.tiles_x * cam.tiles_y;
+  v->stats = nxs_stats{};
+  v->stats.n_gaussians = P;
+  v->stats.n_tiles = n_tiles;
+
+  // ---- workspace
+  NXS_CUDA(ensure_n<unsigned long long>(v->dkeys_in, P));
+  NXS_CUDA(ensure_n<unsigned long long>(v->dkeys_out, P));
+  NXS_CUDA(ensure_n<uint32_t>(v->idx_in, P));
+  NXS_CUDA(ensure_n<uint32_t>(v->idx_out, P));
+  NXS_CUDA(ensure_n<float4>(v->records, P * REC_F4));
+  NXS_CUDA(ensure_n<int4>(v->rects, P));
+  NXS_CUDA(ensure_n<unsigned long long>(v->ntiles, P));
+  NXS_CUDA(ensure_n<unsigned long long>(v->offsets, P));
+  NXS_CUDA(ensure_n<int2>(v->ranges, n_tiles));
+  NXS_CUDA(ensure_n<int32_t>(v->c_last, npix));
+  NXS_CUDA(ensure_n<uint8_t>(v->c_sat, npix));
+  NXS_CUDA(ensure_n<float>(v->c_tk, npix));
+  NXS_CUDA(ensure_n<float>(v->c_thi, npix));
+  NXS_CUDA(ensure_n<float>(v->c_tlo, npix));
+  NXS_CUDA(ensure_n<float>(v->c_P, npix));
+  NXS_CUDA(ensure_n<int32_t>(v->c_ck, npix));
+  NXS_CUDA(ensure_n<float>(v->c_Pck, npix));
+  NXS_CUDA(ensure_n<float>(v->c_ek, npix * 3));
+  NXS_CUDA(ensure_n<float>(v->c_th0, npix * 3));
+  NXS_CUDA(v->dev_small.ensure(8 * sizeof(unsigned long long)));
+  unsigned long long* dsmall = v->dev_small.as<unsigned long long>();
+  Counters* cnt = reinterpret_cast<Counters*>(dsmall + 1);  // [0] straddle, [1..4] counters
+  NXS_CUDA(cudaMemsetAsync(dsmall, 0, 8 * sizeof(unsigned long long), s));
+
+  size_t tmp_sort = 0, tmp_scan = 0;
+  mark(v, 0, s);
+  if (P > 0) {
+    NXS_CUDA(cub::DeviceRadixSort::SortPairs(
+        nullptr, tmp_sort, v->dkeys_in.as<unsigned long long>(),
+        v->dkeys_out.as<unsigned long long>(), v->idx_in.as<uint32_t>(),
+        v->idx_out.as<uint32_t>(), (int)P, 0, 64, s));
+    NXS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_scan,
+                                           v->ntiles.as<unsigned long long>(),
+                                           v->offsets.as<unsigned long long>(), (int)P, s));
+    NXS_CUDA(v->temp.ensure(tmp_sort > tmp_scan ? tmp_sort : tmp_scan));
+
+    // ---- K0 + depth sort
+    launch_depth_keys(scene->centers, P, cam, v->dkeys_in.as<unsigned long long>(),
+                      v->idx_in.as<uint32_t>(), s);
+    NXS_LAUNCHED("depth_keys");
+    size_t tb = v->temp.cap;
+    NXS_CUDA(cub::DeviceRadixSort::SortPairs(
+        v->temp.p, tb, v->dkeys_in.as<unsigned long long>(), v->dkeys_out.as<unsigned long long>(),
+        v->idx_in.as<uint32_t>(), v->idx_out.as<uint32_t>(), (int)P, 0, 64, s));
+    mark(v, 1, s);
+    // ---- K1 projection
+    launch_project(scene->centers, scene->scales, scene->quats, scene->opacities, scene->sh, C, P,
+                   v->idx_out.as<uint32_t>(), cam, opts->alpha_cutoff, opts->near_plane,
+                   v->ntiles.as<unsigned long long>(), v->rects.as<int4>(),
+                   v->records.as<float4>(), dsmall, s);
+    NXS_LAUNCHED("project");
+    mark(v, 2, s);
+    tb = v->temp.cap;
+    NXS_CUDA(cub::DeviceScan::ExclusiveSum(v->temp.p, tb, v->ntiles.as<unsigned long long>(),
+                                           v->offsets.as<unsigned long long>(), (int)P, s));
+    // total pairs = offsets[P-1] + ntiles[P-1]; plus the straddle counter
+    NXS_CUDA(cudaMemcpyAsync(v->host_small, v->offsets.as<unsigned long long>() + (P - 1),
+                             sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    NXS_CUDA(cudaMemcpyAsync(v->host_small + 1, v->ntiles.as<unsigned long long>() + (P - 1),
+                             sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    NXS_CUDA(cudaMemcpyAsync(v->host_small + 2, dsmall, sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, s));
+    NXS_CUDA(cudaStreamSynchronize(s));
+  } else {
+    v->host_small[0] = v->host_small[1] = v->host_small[2] = 0;
+    mark(v, 1, s);
+    mark(v, 2, s);
+  }
+  mark(v, 3, s);
+  const unsigned long long n_pairs = v->host_small[0] + v->host_small[1];
+  v->stats.n_straddling = (int64_t)v->host_small[2];
+  v->stats.n_pairs = (int64_t)n_pairs;
+  if (v->host_small[2] > 0)
+    return fail(NXS_ERR_GEOMETRY,
+                std::to_string(v->host_small[2]) +
+                    " Gaussian(s) cross the near plane; not supported by the device path yet");
+  if (n_pairs >= (1ull << 31)) return fail(NXS_ERR_NOMEM, "more than 2^31 tile pairs");
+
+  NXS_CUDA(cudaMemsetAsync(v->ranges.p, 0, (size_t)n_tiles * sizeof(int2), s));
+  if (n_pairs > 0) {
+    NXS_CUDA(ensure_n<uint32_t>(v->pk_in, (int64_t)n_pairs));
+    NXS_CUDA(ensure_n<uint32_t>(v->pk_out, (int64_t)n_pairs));
+    NXS_CUDA(ensure_n<uint32_t>(v->pv_in, (int64_t)n_pairs));
+    NXS_CUDA(ensure_n<uint32_t>(v->pv_out, (int64_t)n_pairs));
+    const int tbits = bits_for((uint32_t)n_tiles);
+    size_t tmp_pairs = 0;
+    NXS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_pairs, v->pk_in.as<uint32_t>(),
+                                             v->pk_out.as<uint32_t>(), v->pv_in.as<uint32_t>(),
+                                             v->pv_out.as<uint32_t>(), (int)n_pairs, 0, tbits, s));
+    NXS_CUDA(v->temp.ensure(tmp_pairs));
+    // ---- K2 pairs, sort by tile, ranges
+    launch_emit_pairs(v->rects.as<int4>(), v->offsets.as<unsigned long long>(), P, cam.tiles_x,
+                      v->pk_in.as<uint32_t>(), v->pv_in.as<uint32_t>(), s);
+    NXS_LAUNCHED("emit_pairs");
+    mark(v, 4, s);
+    size_t tb = v->temp.cap;
+    NXS_CUDA(cub::DeviceRadixSort::SortPairs(v->temp.p, tb, v->pk_in.as<uint32_t>(),
+                                             v->pk_out.as<uint32_t>(), v->pv_in.as<uint32_t>(),
+                                             v->pv_out.as<uint32_t>(), (int)n_pairs, 0, tbits, s));
+    mark(v, 5, s);
+    launch_tile_ranges(v->pk_out.as<uint32_t>(), (int64_t)n_pairs, v->ranges.as<int2>(), s);
+    NXS_LAUNCHED("tile_ranges");
+  } else {
+    mark(v, 4, s);
+    mark(v, 5, s);
+  }
+  mark(v, 6, s);
+
+  // ---- K3 forward blend
+  const bool count = (opts->flags & NXS_FLAG_COUNT_EVENTS) != 0;
+  const float bgf[3] = {background[0], background[1], background[2]};
+  launch_blend_fwd(count, n_tiles, v->records.as<float4>(), v->pv_out.as<uint32_t>(),
+                   v->ranges.as<int2>(), cam, md, opts->max_splats, (float)opts->alpha_cutoff,
+                   bgf, rgb, overdraw, residual, v->cache(), cnt, s);
+  NXS_LAUNCHED("blend_fwd");
+  mark(v, 7, s);
+  v->ev_fwd = true;
+  v->ev_bwd = false;
+  if (count) {
+    NXS_CUDA(cudaMemcpyAsync(v->host_small + 3, cnt, 2 * sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, s));
+    NXS_CUDA(cudaStreamSynchronize(s));
+    v->stats.n_tests_fwd = (int64_t)v->host_small[3];
+    v->stats.n_composited = (int64_t)v->host_small[4];
+  }
+
+  v->have_fwd = true;
+  v->cam = cam;
+  v->model = md;
+  v->opts = *opts;
+  for (int i = 0; i < 3; ++i) v->bg[i] = bgf[i];
+  v->P = P;
+  v->C = C;
+  v->n_pairs = (int64_t)n_pairs;
+  v->n_tiles = n_tiles;
+  v->scene_centers = scene->centers;
+  return NXS_OK;
+}
+
+int nxs_backward(nxs_view* v, const nxs_scene* scene, const float* seed, float* g_centers,
+                 float* g_scales, float* g_quats, float* g_opacities, float* g_sh, void* stream_) {
+  if (!v || !scene || !seed) return fail(NXS_ERR_INVALID, "null argument");
+  if (!v->have_fwd) return fail(NXS_ERR_STATE, "no forward pass recorded in this view");
+  if (scene->count != v->P || scene->sh_coeffs != v->C)
+    return fail(NXS_ERR_STATE, "scene differs from the forward call");
+  if (v->P > 0 && (!g_centers || !g_scales || !g_quats || !g_opacities || !g_sh))
+    return fail(NXS_ERR_INVALID, "null gradient buffer");
+  cudaStream_t s = (cudaStream_t)stream_;
+  const int64_t P = v->P;
+  if (P == 0) return NXS_OK;
+  NXS_CUDA(ensure_n<double>(v->moments, P * NMOM));
+  mark(v, 8, s);
+  NXS_CUDA(cudaMemsetAsync(v->moments.p, 0, (size_t)P * NMOM * sizeof(double), s));
+  mark(v, 9, s);
+  const bool count = (v->opts.flags & NXS_FLAG_COUNT_EVENTS) != 0;
+  unsigned long long* dsmall = v->dev_small.as<unsigned long long>();
+  Counters* cnt = reinterpret_cast<Counters*>(dsmall + 1);
+  launch_blend_bwd(count, v->n_tiles, v->records.as<float4>(), v->pv_out.as<uint32_t>(),
+                   v->ranges.as<int2>(), v->cam, v->model, (float)v->opts.alpha_cutoff, v->bg,
+                   seed, v->cache(), v->moments.as<double>(), cnt, s);
+  NXS_LAUNCHED("blend_bwd");
+  mark(v, 10, s);
+  launch_chain(scene->centers, scene->scales, scene->quats, v->C, P, v->idx_out.as<uint32_t>(),
+               v->cam, v->moments.as<double>(), g_centers, g_scales, g_quats, g_opacities, g_sh,
+               s);
+  NXS_LAUNCHED("chain");
+  mark(v, 11, s);
+  v->ev_bwd = true;
+  if (count) {
+    NXS_CUDA(cudaMemcpyAsync(v->host_small + 5, &cnt->tests_bwd, 2 * sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, s));
+    NXS_CUDA(cudaStreamSynchronize(s));
+    v->stats.n_tests_bwd = (int64_t)v->host_small[5];
+    v->stats.n_entries_bwd = (int64_t)v->host_small[6];
+  }
+  return NXS_OK;
+}
+
+int nxs_view_timings(nxs_view* v, float* ms, int n) {
+  if (!v || !ms) return fail(NXS_ERR_INVALID, "null argument");
+  if (!v->ev_ok) return fail(NXS_ERR_CUDA, "timing events unavailable");
+  for (int i = 0; i < n && i < NXS_PHASES; ++i) ms[i] = 0.f;
+  const int a[NXS_PHASES] = {0, 1, 2, 3, 4, 5, 6, 8, 9, 10};
+  for (int i = 0; i < n && i < NXS_PHASES; ++i) {
+    const bool fwd = i < 7;
+    if (fwd ? !v->ev_fwd : !v->ev_bwd) continue;
+    NXS_CUDA(cudaEventSynchronize(v->ev[a[i] + 1]));
+    NXS_CUDA(cudaEventElapsedTime(&ms[i], v->ev[a[i]], v->ev[a[i] + 1]));
+  }
+  return NXS_OK;
+}
+
+int nxs_cache_export(nxs_view* v, uint8_t* sat, float* e_k, float* t_k, float* theta0,
+                     void* stream_) {
+  if (!v) return fail(NXS_ERR_INVALID, "null view");
+  if (!v->have_fwd) return fail(NXS_ERR_STATE, "no forward pass recorded in this view");
+  cudaStream_t s = (cudaStream_t)stream_;
+  const size_t npix = (size_t)v->cam.W * v->cam.H;
+  if (sat) NXS_CUDA(cudaMemcpyAsync(sat, v->c_sat.p, npix, cudaMemcpyDeviceToDevice, s));
+  if (e_k) NXS_CUDA(cudaMemcpyAsync(e_k, v->c_ek.p, npix * 12, cudaMemcpyDeviceToDevice, s));
+  if (t_k) NXS_CUDA(cudaMemcpyAsync(t_k, v->c_tk.p, npix * 4, cudaMemcpyDeviceToDevice, s));
+  if (theta0)
+    NXS_CUDA(cudaMemcpyAsync(theta0, v->c_th0.p, npix * 12, cudaMemcpyDeviceToDevice, s));
+  return NXS_OK;
+}
+
+int nxs_depth_order(nxs_view* v, int32_t* order, void* stream_) {
+  if (!v || !order) return fail(NXS_ERR_INVALID, "null argument");
+  if (!v->have_fwd) return fail(NXS_ERR_STATE, "no forward pass recorded in this view");
+  if (v->P == 0) return NXS_OK;
+  NXS_CUDA(cudaMemcpyAsync(order, v->idx_out.p, (size_t)v->P * 4, cudaMemcpyDeviceToDevice,
+                           (cudaStream_t)stream_));
+  return NXS_OK;
+}
+
+int nxs_binning_export(nxs_view* v, int32_t* rects, int32_t* ranges, int32_t* pair_ranks,
+                       void* stream_) {
+  if (!v) return fail(NXS_ERR_INVALID, "null view");
+  if (!v->have_fwd) return fail(NXS_ERR_STATE, "no forward pass recorded in this view");
+  cudaStream_t s = (cudaStream_t)stream_;
+  if (rects && v->P)
+    NXS_CUDA(cudaMemcpyAsync(rects, v->rects.p, (size_t)v->P * 16, cudaMemcpyDeviceToDevice, s));
+  if (ranges)
+    NXS_CUDA(cudaMemcpyAsync(ranges, v->ranges.p, (size_t)v->n_tiles * 8,
+                             cudaMemcpyDeviceToDevice, s));
+  if (pair_ranks && v->n_pairs)
+    NXS_CUDA(cudaMemcpyAsync(pair_ranks, v->pv_out.p, (size_t)v->n_pairs * 4,
+                             cudaMemcpyDeviceToDevice, s));
+  return NXS_OK;
+}
+
+int nxs_records_export(nxs_view* v, float* records, void* stream_) {
+  if (!v || !records) return fail(NXS_ERR_INVALID, "null argument");
+  if (!v->have_fwd) return fail(NXS_ERR_STATE, "no forward pass recorded in this view");
+  if (v->P == 0) return NXS_OK;
+  NXS_CUDA(cudaMemcpyAsync(records, v->records.p, (size_t)v->P * REC_F4 * 16,
+                           cudaMemcpyDeviceToDevice, (cudaStream_t)stream_));
+  return NXS_OK;
+}
+
+}  // extern "C"

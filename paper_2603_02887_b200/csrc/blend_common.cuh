@@ -1,0 +1,86 @@
+// Per-pixel ray-peak test and emission shared by the forward (K3) and the
+// backward (K4) blend kernels.
+//
+// Every float operation is an explicit round-to-nearest intrinsic, so the
+// compiler cannot contract or reorder differently in the two kernels: the
+// backward replays exactly the validity decisions and alphas of the forward.
+//
+// Restates, per (Gaussian, pixel) (reference pkg/src/nexsplat/render.py):
+//   t, m2, alpha, valid     _chunk_geometry, render.py:122-134
+//   emission E, E>0 mask    _sh_basis/_emission, render.py:97-106, 141-144
+// via the centred-conic form of SURVEY §8.0.5: m2 = Δᵀ N' Δ / hᵀA'h with
+// Δ the pixel offset from the fp32 (hi, lo) projected centre.
+#pragma once
+#include "nxs_internal.cuh"
+
+namespace nxs {
+
+struct PixelConst {
+  float pxc, pyc;  // pixel centre (j + 0.5, i + 0.5)
+  float hx, hy;    // normalised image coordinates ((j+0.5-cx)/f, (i+0.5-cy)/f)
+  float Y1, Y2, Y3;  // SH band-1 basis; Y0 = C0
+};
+
+__device__ __forceinline__ PixelConst pixel_setup(const CamDev& cam, int px, int py) {
+  PixelConst pc;
+  double hxd = ((double)px + 0.5 - cam.cx) / cam.f;
+  double hyd = ((double)py + 0.5 - cam.cy) / cam.f;
+  pc.pxc = (float)px + 0.5f;
+  pc.pyc = (float)py + 0.5f;
+  pc.hx = (float)hxd;
+  pc.hy = (float)hyd;
+  // world direction = R (hx, hy, 1), normalised (primitives.py:192-203)
+  double dx = (cam.R[0] * hxd + cam.R[1] * hyd) + cam.R[2];
+  double dy = (cam.R[3] * hxd + cam.R[4] * hyd) + cam.R[5];
+  double dz = (cam.R[6] * hxd + cam.R[7] * hyd) + cam.R[8];
+  double inv = 1.0 / sqrt(dx * dx + dy * dy + dz * dz);
+  pc.Y1 = (float)(-SH_C1 * (dy * inv));
+  pc.Y2 = (float)(SH_C1 * (dz * inv));
+  pc.Y3 = (float)(-SH_C1 * (dx * inv));
+  return pc;
+}
+
+struct TestOut {
+  float ddx, ddy;  // Δ in pixels
+  float D;         // hᵀ A' h
+  float m2;        // Mahalanobis distance² at the ray peak
+  float kern;      // exp(-m2/2)
+  float araw;      // opacity·kern (unclamped)
+  float alpha;     // min(araw, ALPHA_MAX)
+};
+
+// r0 = (cxh, cyh, cxl, cyl); r1 = (n0, k, n1, r2m); r2 = (a, b, c, d); r3 = (e, g, opac, flags)
+__device__ __forceinline__ bool ray_peak_test(const float4& r0, const float4& r1, const float4& r2,
+                                              const float4& r3, const PixelConst& pc, float cutoff,
+                                              TestOut& o) {
+  o.ddx = __fsub_rn(__fsub_rn(pc.pxc, r0.x), r0.z);
+  o.ddy = __fsub_rn(__fsub_rn(pc.pyc, r0.y), r0.w);
+  float w = __fmaf_rn(r1.y, o.ddy, o.ddx);
+  float num = __fmaf_rn(__fmul_rn(r1.x, w), w, __fmul_rn(__fmul_rn(r1.z, o.ddy), o.ddy));
+  float u = __fadd_rn(__fmaf_rn(r2.y, pc.hy, r2.z), pc.hx);
+  float v = __fadd_rn(pc.hy, r3.x);
+  o.D = __fmaf_rn(__fmul_rn(r2.x, u), u, __fmaf_rn(__fmul_rn(r2.w, v), v, r3.y));
+  // cheap reject against the cutoff ellipse (r2m carries a 1e-4 margin)
+  if (num > __fmul_rn(r1.w, o.D)) return false;
+  o.m2 = __fdividef(num, o.D);
+  o.kern = ex2_approx(__fmul_rn(-0.72134752044448170368f, o.m2));  // e^{-m2/2}
+  o.araw = __fmul_rn(r3.z, o.kern);
+  o.alpha = fminf(o.araw, ALPHA_MAX_F);
+  return o.alpha >= cutoff;
+}
+
+// E_c = max(Σ_k sh[c][k] Y_k, 0); returns the positivity mask bits.
+__device__ __forceinline__ int emission(const float4& s0, const float4& s1, const float4& s2,
+                                        const PixelConst& pc, float& E0, float& E1, float& E2) {
+  const float Y0 = (float)SH_C0;
+  float e0 = __fmaf_rn(s0.w, pc.Y3, __fmaf_rn(s0.z, pc.Y2, __fmaf_rn(s0.y, pc.Y1, __fmul_rn(s0.x, Y0))));
+  float e1 = __fmaf_rn(s1.w, pc.Y3, __fmaf_rn(s1.z, pc.Y2, __fmaf_rn(s1.y, pc.Y1, __fmul_rn(s1.x, Y0))));
+  float e2 = __fmaf_rn(s2.w, pc.Y3, __fmaf_rn(s2.z, pc.Y2, __fmaf_rn(s2.y, pc.Y1, __fmul_rn(s2.x, Y0))));
+  int mask = (e0 > 0.f ? 1 : 0) | (e1 > 0.f ? 2 : 0) | (e2 > 0.f ? 4 : 0);
+  E0 = fmaxf(e0, 0.f);
+  E1 = fmaxf(e1, 0.f);
+  E2 = fmaxf(e2, 0.f);
+  return mask;
+}
+
+}  // namespace nxs

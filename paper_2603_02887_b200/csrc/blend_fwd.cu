@@ -1,0 +1,198 @@
+// K3: forward compositing, one 16x16 tile per 256-thread block.
+//
+// Replaces the reference per-pixel loop (pkg/src/nexsplat/render.py:
+// _forward_sweep 147-217: live/sat_now/go, clamp, overdraw, finalize) for
+// the global depth order (reference chunk_size=1, SURVEY §8.0.6 Mode G).
+//
+// Per batch of 256 list entries the block stages the projected records
+// (8 threads per 128-B record, coalesced 16-B loads) in shared memory;
+// every thread then walks the batch front to back for its pixel with the
+// carry in registers and leaves once saturated or capped; the block leaves
+// when all its pixels have.  Numerics (SURVEY R10 + §8.0.4):
+//   * remaining transmittance T_rem is carried instead of cum (exp: P;
+//     blended: closed form; others: T_rem -= w) and saturation is w >= T_rem;
+//   * the optical depth τ̄ is an exact double-float sum, so the backward can
+//     subtract its way back to every τ̄_i bit-exactly;
+//   * the per-pixel cache (last live position, τ̄_end, P_end, t_k, P
+//     checkpoint) is all the back-to-front backward needs.
+#include "blend_common.cuh"
+
+namespace nxs {
+
+template <int FAM, bool COUNT>
+__global__ void __launch_bounds__(TILE_PIX)
+    k_blend_fwd(const float4* __restrict__ records, const uint32_t* __restrict__ pairs,
+                const int2* __restrict__ ranges, CamDev cam, ModelDev m, int max_splats,
+                float cutoff, float bg0, float bg1, float bg2, float* __restrict__ rgb,
+                int32_t* __restrict__ overdraw, float* __restrict__ residual, PixCache cache,
+                Counters* __restrict__ cnt) {
+  __shared__ float4 s_rec[TILE_PIX][7];
+  __shared__ uint32_t s_rank[TILE_PIX];
+
+  const int tile = blockIdx.x;
+  const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
+  const int tid = threadIdx.x;
+  const int px = tx * TILE + (tid & (TILE - 1)), py = ty * TILE + (tid >> 4);
+  const bool inside = px < cam.W && py < cam.H;
+  const PixelConst pc = pixel_setup(cam, px, py);
+
+  float rad0 = 0.f, rad1 = 0.f, rad2 = 0.f;
+  float thi = 0.f, tlo = 0.f;  // exact τ̄
+  float P = 1.f;               // transparency product Π(1-α)
+  float Trem = 1.f;            // 1 - cum
+  int count = 0, last = -1;
+  bool sat = false;
+  float ek0 = bg0, ek1 = bg1, ek2 = bg2, tk = 0.f;
+  float sea0 = 0.f, sea1 = 0.f, sea2 = 0.f, sa = 0.f;  // reference theta0 sums
+  int ck = -1;
+  float Pck = 0.f;
+  unsigned long long ntest = 0;
+  bool done = !inside || max_splats <= 0;
+
+  const int2 rg = ranges[tile];
+  for (int base = rg.x; base < rg.y; base += TILE_PIX) {
+    const int n = min(TILE_PIX, rg.y - base);
+    __syncthreads();
+    if (tid < n) s_rank[tid] = pairs[base + tid];
+    __syncthreads();
+    for (int k = tid; k < n * 8; k += TILE_PIX) {
+      const int e = k >> 3, part = k & 7;
+      if (part < 7) s_rec[e][part] = records[(size_t)s_rank[e] * REC_F4 + part];
+    }
+    __syncthreads();
+    if (!done) {
+      for (int j = 0; j < n; ++j) {
+        if (COUNT) ++ntest;
+        TestOut t;
+        if (!ray_peak_test(s_rec[j][0], s_rec[j][1], s_rec[j][2], s_rec[j][3], pc, cutoff, t))
+          continue;
+        const int idx = base + j;
+        const float alpha = t.alpha;
+        float E0, E1, E2;
+        emission(s_rec[j][4], s_rec[j][5], s_rec[j][6], pc, E0, E1, E2);
+        float fp;
+        const float g = weight_g<FAM>(m, thi, tlo, P, fp);
+        const float wr = alpha * g;
+        const bool satnow = (FAM == FAM_EXP) ? false : (wr >= Trem);
+        const int cb = count;
+        ++count;
+        last = idx;
+        if (satnow) {
+          rad0 = fmaf(Trem, E0, rad0);
+          rad1 = fmaf(Trem, E1, rad1);
+          rad2 = fmaf(Trem, E2, rad2);
+          ek0 = E0;
+          ek1 = E1;
+          ek2 = E2;
+          tk = Trem;
+          sat = true;
+          done = true;
+          break;
+        }
+        rad0 = fmaf(wr, E0, rad0);
+        rad1 = fmaf(wr, E1, rad1);
+        rad2 = fmaf(wr, E2, rad2);
+        if (cb >= 1) {
+          sea0 = fmaf(alpha, E0, sea0);
+          sea1 = fmaf(alpha, E1, sea1);
+          sea2 = fmaf(alpha, E2, sea2);
+          sa += alpha;
+        }
+        if constexpr (FAM != FAM_EXP) df_add(thi, tlo, alpha);
+        if constexpr (IsPFam<FAM>::value) {
+          const float Pn = __fmul_rn(P, __fsub_rn(1.0f, alpha));
+          if (Pn < P_FLOOR && ck < 0) {
+            ck = idx;
+            Pck = P;
+          }
+          P = Pn;
+        }
+        if constexpr (FAM == FAM_EXP) {
+          Trem = P;
+        } else if constexpr (FAM == FAM_BLEND) {
+          Trem = fmaf(1.0f - m.c, __fsub_rn(__fsub_rn(1.0f, thi), tlo), m.c * P);
+        } else {
+          Trem = __fsub_rn(Trem, wr);
+        }
+        if (count >= max_splats) {
+          done = true;
+          break;
+        }
+      }
+    }
+    if (__syncthreads_count(!done) == 0) break;
+  }
+
+  if (COUNT) {
+    __shared__ unsigned long long s_cnt[2];
+    if (tid == 0) s_cnt[0] = s_cnt[1] = 0;
+    __syncthreads();
+    atomicAdd(&s_cnt[0], ntest);
+    atomicAdd(&s_cnt[1], (unsigned long long)count);
+    __syncthreads();
+    if (tid == 0) {
+      atomicAdd(&cnt->tests_fwd, s_cnt[0]);
+      atomicAdd(&cnt->composited, s_cnt[1]);
+    }
+  }
+
+  if (!inside) return;
+  const int pix = py * cam.W + px;
+  const float res = sat ? 0.f : Trem;  // render.py:210
+  rgb[3 * pix + 0] = fmaf(bg0, res, rad0);
+  rgb[3 * pix + 1] = fmaf(bg1, res, rad1);
+  rgb[3 * pix + 2] = fmaf(bg2, res, rad2);
+  overdraw[pix] = count;
+  residual[pix] = res;
+  cache.last[pix] = last;
+  cache.sat[pix] = sat ? 1 : 0;
+  cache.t_k[pix] = sat ? tk : res;  // render.py:212
+  cache.tau_hi[pix] = thi;
+  cache.tau_lo[pix] = tlo;
+  cache.P_end[pix] = P;
+  cache.ck_idx[pix] = ck;
+  cache.P_ck[pix] = Pck;
+  cache.e_k[3 * pix + 0] = ek0;
+  cache.e_k[3 * pix + 1] = ek1;
+  cache.e_k[3 * pix + 2] = ek2;
+  cache.theta0[3 * pix + 0] = sea0 - ek0 * sa;  // render.py:213
+  cache.theta0[3 * pix + 1] = sea1 - ek1 * sa;
+  cache.theta0[3 * pix + 2] = sea2 - ek2 * sa;
+}
+
+template <int FAM>
+static void launch_fwd_fam(bool count, int n_tiles, const float4* records, const uint32_t* pairs,
+                           const int2* ranges, const CamDev& cam, const ModelDev& m,
+                           int max_splats, float cutoff, const float* bg, float* rgb,
+                           int32_t* overdraw, float* residual, const PixCache& cache,
+                           Counters* cnt, cudaStream_t s) {
+  if (count)
+    k_blend_fwd<FAM, true><<<n_tiles, TILE_PIX, 0, s>>>(records, pairs, ranges, cam, m,
+                                                         max_splats, cutoff, bg[0], bg[1], bg[2],
+                                                         rgb, overdraw, residual, cache, cnt);
+  else
+    k_blend_fwd<FAM, false><<<n_tiles, TILE_PIX, 0, s>>>(records, pairs, ranges, cam, m,
+                                                          max_splats, cutoff, bg[0], bg[1], bg[2],
+                                                          rgb, overdraw, residual, cache, cnt);
+}
+
+void launch_blend_fwd(bool count, int n_tiles, const float4* records, const uint32_t* pairs,
+                      const int2* ranges, const CamDev& cam, const ModelDev& m, int max_splats,
+                      float cutoff, const float* bg, float* rgb, int32_t* overdraw,
+                      float* residual, const PixCache& cache, Counters* cnt, cudaStream_t s) {
+  if (n_tiles == 0) return;
+#define NXS_FWD(F)                                                                            \
+  launch_fwd_fam<F>(count, n_tiles, records, pairs, ranges, cam, m, max_splats, cutoff, bg, rgb, \
+                    overdraw, residual, cache, cnt, s)
+  switch (m.fam) {
+    case FAM_EXP: NXS_FWD(FAM_EXP); break;
+    case FAM_LIN: NXS_FWD(FAM_LIN); break;
+    case FAM_QUAD: NXS_FWD(FAM_QUAD); break;
+    case FAM_BLEND: NXS_FWD(FAM_BLEND); break;
+    case FAM_POW: NXS_FWD(FAM_POW); break;
+    default: NXS_FWD(FAM_SOFT); break;
+  }
+#undef NXS_FWD
+}
+
+}  // namespace nxs

@@ -1,0 +1,168 @@
+// Internal device-side definitions shared by the kernels of libnxs.
+//
+// Layout in HBM (per view):
+//   order    [P]      u32   rank -> Gaussian index (stable fp64 depth sort)
+//   records  [P][8]   float4 per-rank projected record, 128 B, rank order
+//   rects    [P]      int4  tile rectangle per rank (tx0,ty0,tx1,ty1)
+//   pairs    [n_pairs] u32  ranks, grouped by tile (stable, so rank-ascending)
+//   ranges   [T]      int2  [start, end) of each tile's run in `pairs`
+//   cache    [H*W]    per-pixel replay state (SoA, see PixCache)
+//   moments  [P][24]  f64   per-rank gradient moments (backward)
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace nxs {
+
+constexpr int TILE = 16;
+constexpr int TILE_PIX = TILE * TILE;  // 256 threads per tile block
+constexpr int REC_F4 = 8;              // float4 per record
+constexpr int NMOM = 24;               // gradient moments per Gaussian
+
+// reference compositor.py:30-31 (ALPHA_MAX = 1 - 1e-6), rounded to fp32
+constexpr float ALPHA_MAX_F = 0.999999f;
+// reference primitives.py:41-42
+constexpr double SH_C0 = 0.28209479177387814;
+constexpr double SH_C1 = 0.4886025119029199;
+// P-family checkpoint: below this the transparency product is frozen for
+// the backward's recovery (see blend kernels)
+constexpr float P_FLOOR = 1e-30f;
+
+// record flags (stored as int bits in rec[3].w)
+constexpr int RF_CONIC = 1;
+
+struct CamDev {
+  double o[3];
+  double R[9];  // row-major, camera -> world
+  double f, cx, cy;
+  int W, H;
+  int tiles_x, tiles_y;
+};
+
+// model families
+enum Fam : int {
+  FAM_EXP = 0,
+  FAM_LIN = 1,
+  FAM_QUAD = 2,
+  FAM_BLEND = 3,  // blended and vicini (identical discrete weights)
+  FAM_POW = 5,
+  FAM_SOFT = 6,
+};
+
+struct ModelDev {
+  int fam;
+  float c;       // quad: c; blend: gamma; soft: kappa; pow: v
+  float K;       // soft: kappa / log(1 + e^kappa)
+  float ex;      // pow: -(1+v)/v
+  int powmode;   // pow: 0 general, 1 linear (v == -1), 2 exponential limit
+};
+
+struct PixCache {
+  int32_t* last;     // list position of the last live splat (-1: none)
+  uint8_t* sat;      // saturated
+  float* t_k;        // saturating weight, or residual
+  float* tau_hi;     // exact double-float optical depth after the last go splat
+  float* tau_lo;
+  float* P_end;      // transparency product after the last go splat
+  int32_t* ck_idx;   // list position where P fell below P_FLOOR (-1: never)
+  float* P_ck;       // P before that splat
+  float* e_k;        // [3] saturating emission (or background)
+  float* theta0;     // [3] reference quadratic-adjoint cache (compat)
+};
+
+struct Counters {
+  unsigned long long tests_fwd, composited, tests_bwd, entries_bwd;
+};
+
+// ---------------------------------------------------------------------------
+// error-free float transforms (exact double-float optical depth)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void two_sum(float a, float b, float& s, float& e) {
+  s = __fadd_rn(a, b);
+  float bb = __fsub_rn(s, a);
+  e = __fadd_rn(__fsub_rn(a, __fsub_rn(s, bb)), __fsub_rn(b, bb));
+}
+__device__ __forceinline__ void fast_two_sum(float a, float b, float& s, float& e) {
+  s = __fadd_rn(a, b);
+  e = __fsub_rn(b, __fsub_rn(s, a));
+}
+// (hi, lo) += a, exactly (the partial sums of alphas >= 2^-8 need < 48 bits)
+__device__ __forceinline__ void df_add(float& hi, float& lo, float a) {
+  float s, e;
+  two_sum(hi, a, s, e);
+  fast_two_sum(s, __fadd_rn(e, lo), hi, lo);
+}
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float lg2_approx(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// ---------------------------------------------------------------------------
+// transmittance weights p̄ = α·g  (reference transmittance.py:234-262)
+// τ-family: g = f(τ̄), fp = f'(τ̄).  P-family: g = (1-γ) + γP.
+// ---------------------------------------------------------------------------
+template <int FAM>
+__device__ __forceinline__ float weight_g(const ModelDev& m, float thi, float tlo, float P,
+                                          float& fp) {
+  if constexpr (FAM == FAM_EXP) {
+    fp = 0.f;
+    return P;
+  } else if constexpr (FAM == FAM_BLEND) {
+    fp = 0.f;
+    return fmaf(m.c, P - 1.0f, 1.0f);
+  } else if constexpr (FAM == FAM_LIN) {
+    fp = 0.f;
+    return 1.0f;
+  } else if constexpr (FAM == FAM_QUAD) {
+    fp = m.c;
+    return fmaf(m.c, thi, fmaf(m.c, tlo, 1.0f));
+  } else if constexpr (FAM == FAM_SOFT) {
+    // σ(x), x = κ(1 - τ̄), split by sign so neither exp overflows
+    float x = m.c * __fsub_rn(__fsub_rn(1.0f, thi), tlo);
+    float t = ex2_approx(-fabsf(x) * 1.4426950408889634f);  // e^{-|x|}
+    float r = __fdividef(1.0f, 1.0f + t);
+    float sig = x >= 0.f ? r : t * r;
+    float oms = x >= 0.f ? t * r : r;  // 1 - σ
+    float g = m.K * sig;
+    fp = -m.c * g * oms;
+    return g;
+  } else {  // FAM_POW
+    if (m.powmode == 1) {
+      fp = 0.f;
+      return 1.0f;
+    }
+    float tau = thi + tlo;
+    if (m.powmode == 2) {
+      float e = ex2_approx(-tau * 1.4426950408889634f);
+      fp = -e;
+      return e;
+    }
+    float base = fmaf(tau, m.c, 1.0f);
+    if (!(base > 0.f)) {
+      fp = 0.f;
+      return 0.f;
+    }
+    float g = ex2_approx(m.ex * lg2_approx(base));
+    fp = m.ex * m.c * __fdividef(g, base);
+    return g;
+  }
+}
+
+template <int FAM>
+struct IsPFam {
+  static constexpr bool value = (FAM == FAM_EXP || FAM == FAM_BLEND);
+};
+
+}  // namespace nxs

@@ -1,0 +1,279 @@
+// K0 depth keys, K1 per-Gaussian projection + conic tile bbox, K2 pair
+// emission and tile ranges.
+//
+// Compiled with --fmad=false: every fp64 operation here is a correctly
+// rounded IEEE add/sub/mul/div/sqrt (plus exact floor/ceil/frexp), in the
+// order written, so oracle/binning_oracle.c (gcc -ffp-contract=off)
+// reproduces the records, rectangles, ranks and pair lists bit for bit.
+// The operation order below is normative for that restatement.
+//
+// Replaces (reference pkg/src/nexsplat/):
+//   _depth_chunks ordering           render.py:350-358
+//   per-Gaussian part of _chunk_geometry (quat_to_rot, A, b)
+//                                    render.py:116-121, primitives.py:45-64
+// The per-pixel test those records feed is in blend_fwd.cu.
+#include "nxs_internal.cuh"
+
+namespace nxs {
+
+// ln(x) for x > 0 with only IEEE basic ops: x = m·2^e, m in [√½, √2),
+// ln m = 2·atanh((m-1)/(m+1)) as an 11-term odd series (|z| <= 0.1716,
+// truncation < 1e-18).  Deterministic across nvcc and gcc.
+__device__ __forceinline__ double ln_det(double x) {
+  int e;
+  double m = frexp(x, &e);
+  if (m < 0.70710678118654752440) {
+    m = m * 2.0;
+    e = e - 1;
+  }
+  double z = (m - 1.0) / (m + 1.0);
+  double z2 = z * z;
+  double s = 1.0 / 23.0;
+  s = s * z2 + 1.0 / 21.0;
+  s = s * z2 + 1.0 / 19.0;
+  s = s * z2 + 1.0 / 17.0;
+  s = s * z2 + 1.0 / 15.0;
+  s = s * z2 + 1.0 / 13.0;
+  s = s * z2 + 1.0 / 11.0;
+  s = s * z2 + 1.0 / 9.0;
+  s = s * z2 + 1.0 / 7.0;
+  s = s * z2 + 1.0 / 5.0;
+  s = s * z2 + 1.0 / 3.0;
+  s = s * z2 + 1.0;
+  return (double)e * 0.69314718055994530942 + 2.0 * z * s;
+}
+
+// K0: fp64 view depth (μ - o)·forward -> order-preserving u64 key.
+__global__ void k_depth_keys(const float* __restrict__ centers, int64_t P, CamDev cam,
+                             unsigned long long* __restrict__ keys,
+                             uint32_t* __restrict__ idx) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  double b0 = (double)centers[3 * i + 0] - cam.o[0];
+  double b1 = (double)centers[3 * i + 1] - cam.o[1];
+  double b2 = (double)centers[3 * i + 2] - cam.o[2];
+  // forward = third column of the camera rotation
+  double depth = (b0 * cam.R[2] + b1 * cam.R[5]) + b2 * cam.R[8];
+  unsigned long long u = (unsigned long long)__double_as_longlong(depth);
+  keys[i] = (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+  idx[i] = (uint32_t)i;
+}
+
+struct ProjOut {
+  unsigned long long* n_tiles;  // per rank tile count
+  int4* rects;                  // per rank tile rectangle
+  float4* records;              // per rank 8 x float4
+  unsigned long long* straddle; // counter
+};
+
+// K1: per rank r (Gaussian g = order[r]).
+__global__ void k_project(const float* __restrict__ centers, const float* __restrict__ scales,
+                          const float* __restrict__ quats, const float* __restrict__ opacities,
+                          const float* __restrict__ sh, int C, int64_t P,
+                          const uint32_t* __restrict__ order, CamDev cam, double cutoff,
+                          double near_plane, ProjOut out) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= P) return;
+  const int64_t g = order[r];
+
+  // --- rotation from the normalised quaternion (primitives.py:45-64)
+  double qw = quats[4 * g + 0], qx = quats[4 * g + 1], qy = quats[4 * g + 2],
+         qz = quats[4 * g + 3];
+  double nq = sqrt(((qw * qw + qx * qx) + qy * qy) + qz * qz);
+  double w = qw / nq, x = qx / nq, y = qy / nq, z = qz / nq;
+  double R[9];
+  R[0] = 1.0 - 2.0 * (y * y + z * z);
+  R[1] = 2.0 * (x * y - w * z);
+  R[2] = 2.0 * (x * z + w * y);
+  R[3] = 2.0 * (x * y + w * z);
+  R[4] = 1.0 - 2.0 * (x * x + z * z);
+  R[5] = 2.0 * (y * z - w * x);
+  R[6] = 2.0 * (x * z - w * y);
+  R[7] = 2.0 * (y * z + w * x);
+  R[8] = 1.0 - 2.0 * (x * x + y * y);
+
+  // M = Rc^T R  (Gaussian axes in camera frame)
+  double M[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      M[3 * i + j] = (cam.R[0 + i] * R[0 + j] + cam.R[3 + i] * R[3 + j]) + cam.R[6 + i] * R[6 + j];
+
+  double s0 = scales[3 * g + 0], s1 = scales[3 * g + 1], s2 = scales[3 * g + 2];
+  double is0 = 1.0 / (s0 * s0), is1 = 1.0 / (s1 * s1), is2 = 1.0 / (s2 * s2);
+  // A' = M diag(1/s^2) M^T  (camera-frame inverse covariance)
+  double Ap[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = i; j < 3; ++j) {
+      double v = ((M[3 * i + 0] * is0) * M[3 * j + 0] + (M[3 * i + 1] * is1) * M[3 * j + 1]) +
+                 (M[3 * i + 2] * is2) * M[3 * j + 2];
+      Ap[3 * i + j] = v;
+      Ap[3 * j + i] = v;
+    }
+
+  // b' = Rc^T (μ - o)
+  double b0 = (double)centers[3 * g + 0] - cam.o[0];
+  double b1 = (double)centers[3 * g + 1] - cam.o[1];
+  double b2 = (double)centers[3 * g + 2] - cam.o[2];
+  double bp[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) bp[i] = (cam.R[0 + i] * b0 + cam.R[3 + i] * b1) + cam.R[6 + i] * b2;
+  double Ab[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+    Ab[i] = (Ap[3 * i + 0] * bp[0] + Ap[3 * i + 1] * bp[1]) + Ap[3 * i + 2] * bp[2];
+  double bAb = (bp[0] * Ab[0] + bp[1] * Ab[1]) + bp[2] * Ab[2];
+  // N = (b'A'b') A' - (A'b')(A'b')^T, null vector b'
+  double N[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) N[3 * i + j] = bAb * Ap[3 * i + j] - Ab[i] * Ab[j];
+
+  float4* rec = out.records + r * REC_F4;
+  int4 rect = make_int4(-1, -1, -1, -1);
+  unsigned long long ntile = 0;
+
+  double opac = (double)opacities[g];
+  bool live = opac >= cutoff;
+  // cutoff ellipsoid radius (Mahalanobis), with the bbox/pre-test margin
+  double r2 = live ? 2.0 * ln_det(opac / cutoff) : 0.0;
+  double r2m = r2 * (1.0 + 1e-4) + 1e-4;
+  double rm = sqrt(r2m);
+  double m20 = M[6] * s0, m21 = M[7] * s1, m22 = M[8] * s2;
+  double sz = sqrt((m20 * m20 + m21 * m21) + m22 * m22);
+  double zmin = bp[2] - rm * sz;
+  double zmax = bp[2] + rm * sz;
+  if (live && zmax <= 0.0) live = false;  // entirely behind the camera plane
+  if (live && zmin <= near_plane * 1.001) {
+    // crosses the near region: the conic form does not apply
+    atomicAdd(out.straddle, 1ull);
+    live = false;
+  }
+
+  // --- per-pixel test coefficients (Cholesky-style forms)
+  double f = cam.f, f2 = f * f;
+  double Np00 = N[0] / f2, Np01 = N[1] / f2, Np11 = N[4] / f2;
+  double n0 = Np00, kk = Np01 / Np00, n1 = Np11 - Np01 * kk;
+  double ccx = cam.cx + f * (bp[0] / bp[2]);
+  double ccy = cam.cy + f * (bp[1] / bp[2]);
+  float cxh = (float)ccx, cyh = (float)ccy;
+  float cxl = (float)(ccx - (double)cxh), cyl = (float)(ccy - (double)cyh);
+  double a = Ap[0], bb = Ap[1] / a, cc = Ap[2] / a;
+  double A11s = Ap[4] - Ap[1] * bb, A12s = Ap[5] - Ap[1] * cc, A22s = Ap[8] - Ap[2] * cc;
+  double d = A11s, e = A12s / d, gg = A22s - A12s * e;
+
+  if (live) {
+    // --- silhouette conic Q = N - r2m A' and its dual: tile bbox
+    double Q[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) Q[i] = N[i] - r2m * Ap[i];
+    double S00 = Q[4] * Q[8] - Q[5] * Q[5];
+    double S11 = Q[0] * Q[8] - Q[2] * Q[2];
+    double S22 = Q[0] * Q[4] - Q[1] * Q[1];
+    double S02 = Q[1] * Q[5] - Q[2] * Q[4];
+    double S12 = Q[1] * Q[2] - Q[0] * Q[5];
+    double dx = S02 * S02 - S00 * S22;
+    double dy = S12 * S12 - S11 * S22;
+    double jlo = 0.0, jhi = (double)(cam.W - 1), ilo = 0.0, ihi = (double)(cam.H - 1);
+    bool ok = (dx >= 0.0) && (dy >= 0.0) && (S22 != 0.0);
+    if (ok) {
+      double sx = sqrt(dx), sy = sqrt(dy);
+      double x1 = (S02 - sx) / S22, x2 = (S02 + sx) / S22;
+      double y1 = (S12 - sy) / S22, y2 = (S12 + sy) / S22;
+      double xl = x1 < x2 ? x1 : x2, xh = x1 < x2 ? x2 : x1;
+      double yl = y1 < y2 ? y1 : y2, yh = y1 < y2 ? y2 : y1;
+      double pjl = ceil((cam.cx + f * xl) - 0.5), pjh = floor((cam.cx + f * xh) - 0.5);
+      double pil = ceil((cam.cy + f * yl) - 0.5), pih = floor((cam.cy + f * yh) - 0.5);
+      // NaN-safe clamps (a NaN bound keeps the full range)
+      if (pjl > jlo) jlo = pjl;
+      if (pjh < jhi) jhi = pjh;
+      if (pil > ilo) ilo = pil;
+      if (pih < ihi) ihi = pih;
+    }
+    if (jlo <= jhi && ilo <= ihi) {
+      int j0 = (int)jlo, j1 = (int)jhi, i0 = (int)ilo, i1 = (int)ihi;
+      rect = make_int4(j0 / TILE, i0 / TILE, j1 / TILE, i1 / TILE);
+      ntile = (unsigned long long)(rect.z - rect.x + 1) * (unsigned long long)(rect.w - rect.y + 1);
+    }
+  }
+
+  rec[0] = make_float4(cxh, cyh, cxl, cyl);
+  rec[1] = make_float4((float)n0, (float)kk, (float)n1, (float)r2m);
+  rec[2] = make_float4((float)a, (float)bb, (float)cc, (float)d);
+  rec[3] = make_float4((float)e, (float)gg, (float)opac, __int_as_float(RF_CONIC));
+  float shv[12];
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) shv[4 * c + k] = (k < C) ? sh[(g * 3 + c) * C + k] : 0.0f;
+  rec[4] = make_float4(shv[0], shv[1], shv[2], shv[3]);
+  rec[5] = make_float4(shv[4], shv[5], shv[6], shv[7]);
+  rec[6] = make_float4(shv[8], shv[9], shv[10], shv[11]);
+  // reserved for the exact-order mode: t-coefficients (A'b')·h and z_lo
+  rec[7] = make_float4((float)Ab[0], (float)Ab[1], (float)Ab[2], (float)zmin);
+  out.rects[r] = rect;
+  out.n_tiles[r] = ntile;
+}
+
+// K2: emit (tile, rank) pairs at the exclusive-scan offsets, rank order.
+__global__ void k_emit_pairs(const int4* __restrict__ rects,
+                             const unsigned long long* __restrict__ offsets, int64_t P,
+                             int tiles_x, uint32_t* __restrict__ keys,
+                             uint32_t* __restrict__ vals) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= P) return;
+  int4 rc = rects[r];
+  if (rc.x < 0) return;
+  unsigned long long o = offsets[r];
+  for (int ty = rc.y; ty <= rc.w; ++ty)
+    for (int tx = rc.x; tx <= rc.z; ++tx) {
+      keys[o] = (uint32_t)(ty * tiles_x + tx);
+      vals[o] = (uint32_t)r;
+      ++o;
+    }
+}
+
+__global__ void k_tile_ranges(const uint32_t* __restrict__ keys, int64_t n,
+                              int2* __restrict__ ranges) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint32_t t = keys[i];
+  if (i == 0 || keys[i - 1] != t) ranges[t].x = (int)i;
+  if (i == n - 1 || keys[i + 1] != t) ranges[t].y = (int)(i + 1);
+}
+
+// host launchers
+void launch_depth_keys(const float* centers, int64_t P, const CamDev& cam,
+                       unsigned long long* keys, uint32_t* idx, cudaStream_t s) {
+  if (P == 0) return;
+  k_depth_keys<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(centers, P, cam, keys, idx);
+}
+
+void launch_project(const float* centers, const float* scales, const float* quats,
+                    const float* opacities, const float* sh, int C, int64_t P,
+                    const uint32_t* order, const CamDev& cam, double cutoff, double near_plane,
+                    unsigned long long* n_tiles, int4* rects, float4* records,
+                    unsigned long long* straddle, cudaStream_t s) {
+  if (P == 0) return;
+  ProjOut o{n_tiles, rects, records, straddle};
+  k_project<<<(unsigned)((P + 127) / 128), 128, 0, s>>>(centers, scales, quats, opacities, sh, C,
+                                                        P, order, cam, cutoff, near_plane, o);
+}
+
+void launch_emit_pairs(const int4* rects, const unsigned long long* offsets, int64_t P,
+                       int tiles_x, uint32_t* keys, uint32_t* vals, cudaStream_t s) {
+  if (P == 0) return;
+  k_emit_pairs<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(rects, offsets, P, tiles_x, keys,
+                                                           vals);
+}
+
+void launch_tile_ranges(const uint32_t* keys, int64_t n, int2* ranges, cudaStream_t s) {
+  if (n == 0) return;
+  k_tile_ranges<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(keys, n, ranges);
+}
+
+}  // namespace nxs

@@ -1,0 +1,404 @@
+"""Drop-in replacement for the reference module ``nexsplat.render``.
+
+Same names, signatures, argument meaning, return types and error
+behaviour as reference ``pkg/src/nexsplat/render.py`` (``__all__`` at
+render.py:34-41):
+
+    render(scene, camera, model, background, *, max_splats=128,
+           alpha_cutoff=1/255, near=1e-4, chunk_size=None, threads=1)
+        -> RenderResult(rgb (H,W,3) f64, overdraw (H,W) int64, residual (H,W) f64)
+    render_forward_cached(arrs, camera, model, background, *, ...) -> (RenderResult, cache)
+    render_backward(arrs, camera, model, background, cache, seed_image, *, ...) -> grads
+    render_with_gradients(arrs, camera, model, background, seed_image, *, ...)
+
+All arithmetic runs in the CUDA library (libnxs, include/nxs.h) on the
+current torch CUDA device; this module only moves arrays.  Inputs may be
+the reference's numpy ``SceneArrays`` / primitive lists (float64, copied to
+the device as float32 each call — the reference mutates them in place
+between calls, optimizer.py:382) or a :class:`DeviceScene` of resident
+float32 CUDA tensors (the fast path; nothing crosses PCIe but the outputs).
+
+Ordering (reference render.py:350-358): ``chunk_size=1``
+(global front-to-back order, "Mode G") runs on the device.  The exact
+per-pixel order of ``chunk_size=None`` and chunked orders ``C > 1`` are not
+implemented yet and raise ``NotImplementedError`` — never a silent
+approximation.
+"""
+from __future__ import annotations
+
+import threading
+import weakref
+from collections.abc import Mapping
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .camera import ALPHA_MAX, DEFAULT_ALPHA_CUTOFF, NEAR_PLANE, GaussianPrimitive
+from .transmittance import VARIANT_IDS, as_model
+
+__all__ = [
+    "SceneArrays",
+    "RenderResult",
+    "DeviceScene",
+    "render",
+    "render_forward_cached",
+    "render_backward",
+    "render_with_gradients",
+    "forward_device",
+    "backward_device",
+    "zero_grads_device",
+]
+
+
+@dataclass
+class SceneArrays:
+    """Structure-of-arrays scene (reference render.py:44-87)."""
+
+    centers: np.ndarray   # (P, 3)
+    scales: np.ndarray    # (P, 3)
+    quats: np.ndarray     # (P, 4), normalised on use
+    opacities: np.ndarray  # (P,)
+    sh: np.ndarray        # (P, 3, C)
+
+    @classmethod
+    def from_primitives(cls, scene) -> "SceneArrays":
+        n = len(scene)
+        c = max((p.sh.shape[1] for p in scene), default=1)
+        sh = np.zeros((n, 3, c))
+        for i, p in enumerate(scene):
+            sh[i, :, : p.sh.shape[1]] = p.sh
+        return cls(
+            centers=np.array([p.center for p in scene], dtype=np.float64).reshape(n, 3),
+            scales=np.array([p.scale for p in scene], dtype=np.float64).reshape(n, 3),
+            quats=np.array([p.rotation for p in scene], dtype=np.float64).reshape(n, 4),
+            opacities=np.array([p.opacity for p in scene], dtype=np.float64),
+            sh=sh,
+        )
+
+    def to_primitives(self) -> list:
+        prims = []
+        for i in range(len(self.opacities)):
+            q = self.quats[i] / np.linalg.norm(self.quats[i])
+            prims.append(GaussianPrimitive(
+                self.centers[i].copy(), np.maximum(self.scales[i], 1e-6), q,
+                float(np.clip(self.opacities[i], 1e-4, ALPHA_MAX)), self.sh[i].copy()))
+        return prims
+
+    def __len__(self) -> int:
+        return len(self.opacities)
+
+    def copy(self) -> "SceneArrays":
+        return SceneArrays(self.centers.copy(), self.scales.copy(), self.quats.copy(),
+                           self.opacities.copy(), self.sh.copy())
+
+
+@dataclass
+class RenderResult:
+    rgb: np.ndarray       # (H, W, 3) linear radiance
+    overdraw: np.ndarray  # (H, W) splats evaluated per pixel
+    residual: np.ndarray  # (H, W) transmittance left after all splats
+
+
+class DeviceScene:
+    """Resident float32 CUDA copy of a scene (the B200 fast path)."""
+
+    FIELDS = ("centers", "scales", "quats", "opacities", "sh")
+
+    def __init__(self, centers, scales, quats, opacities, sh):
+        import torch
+        self.centers = centers.contiguous()
+        self.scales = scales.contiguous()
+        self.quats = quats.contiguous()
+        self.opacities = opacities.contiguous()
+        self.sh = sh.contiguous()
+        for name in self.FIELDS:
+            t = getattr(self, name)
+            if t.dtype != torch.float32 or not t.is_cuda:
+                raise TypeError(f"DeviceScene.{name} must be a float32 CUDA tensor")
+        self.count = int(self.opacities.shape[0])
+        self.sh_coeffs = int(self.sh.shape[2]) if self.sh.ndim == 3 else 1
+        if self.sh_coeffs not in (1, 4):
+            raise ValueError("sh must have 1 or 4 coefficients per channel")
+
+    @classmethod
+    def from_arrays(cls, arrs, device=None, non_blocking=False) -> "DeviceScene":
+        import torch
+        dev = torch.device("cuda") if device is None else torch.device(device)
+
+        def up(x, shape):
+            if isinstance(x, torch.Tensor):
+                return x.to(device=dev, dtype=torch.float32).reshape(shape)
+            a = np.ascontiguousarray(np.asarray(x, dtype=np.float32).reshape(shape))
+            return torch.from_numpy(a).to(dev, non_blocking=non_blocking)
+
+        n = len(arrs.opacities)
+        sh = arrs.sh
+        c = int(np.shape(sh)[2]) if len(np.shape(sh)) == 3 else 1
+        return cls(up(arrs.centers, (n, 3)), up(arrs.scales, (n, 3)), up(arrs.quats, (n, 4)),
+                   up(arrs.opacities, (n,)), up(sh, (n, 3, c)))
+
+    def __len__(self):
+        return self.count
+
+
+def _as_device_scene(scene) -> DeviceScene:
+    if isinstance(scene, DeviceScene):
+        return scene
+    if isinstance(scene, (list, tuple)):
+        scene = SceneArrays.from_primitives(scene)
+    return DeviceScene.from_arrays(scene)
+
+
+def _effective_chunk(chunk_size, n: int) -> int:
+    """Map the reference chunk_size onto the device ordering mode
+    (reference render.py:350-354: None or >= P means one exact chunk)."""
+    if n <= 1:
+        return 1  # every order coincides
+    if chunk_size is None or int(chunk_size) >= n:
+        return 0
+    c = int(chunk_size)
+    if c < 1:
+        raise ValueError("chunk_size must be >= 1 or None")
+    return c
+
+
+def _check_mode(chunk: int):
+    if chunk != 1:
+        what = "the exact per-pixel order (chunk_size=None)" if chunk == 0 else \
+            f"chunked order chunk_size={chunk}"
+        raise NotImplementedError(
+            f"{what} is not implemented on the device yet; use chunk_size=1 "
+            "(global front-to-back order)")
+
+
+def _model_struct(model):
+    m = as_model(model)
+    return m, _native.make_model(VARIANT_IDS[m.variant], m.param)
+
+
+def forward_device(view, dev: DeviceScene, camera, model, background, *, max_splats=128,
+                   alpha_cutoff=DEFAULT_ALPHA_CUTOFF, near=NEAR_PLANE, chunk_size=1,
+                   count_events=False, out=None, stream=None):
+    """Forward render on the device; returns (rgb (H,W,3), overdraw (H,W)
+    int32, residual (H,W)) float32 CUDA tensors."""
+    import torch
+    chunk = _effective_chunk(chunk_size, dev.count)
+    _check_mode(chunk)
+    _, ms = _model_struct(model)
+    H, W = int(camera.height), int(camera.width)
+    d = dev.centers.device
+    if out is None:
+        out = (torch.empty((H, W, 3), dtype=torch.float32, device=d),
+               torch.empty((H, W), dtype=torch.int32, device=d),
+               torch.empty((H, W), dtype=torch.float32, device=d))
+    bg = np.asarray(background, dtype=np.float64).reshape(3)
+    opts = _native.make_opts(max_splats, alpha_cutoff, near, chunk,
+                             _native.NXS_FLAG_COUNT_EVENTS if count_events else 0)
+    try:
+        view.forward(dev, _native.make_camera(camera), ms, opts, bg, out[0], out[1], out[2],
+                     stream=stream)
+    except _native.NxsError as e:
+        if e.code == _native.NXS_ERR_GEOMETRY:
+            raise NotImplementedError(str(e)) from e
+        if e.code == _native.NXS_ERR_INVALID:
+            raise ValueError(str(e)) from e
+        raise
+    return out
+
+
+def zero_grads_device(dev: DeviceScene) -> dict:
+    import torch
+    return {
+        "centers": torch.zeros_like(dev.centers),
+        "scales": torch.zeros_like(dev.scales),
+        "quats": torch.zeros_like(dev.quats),
+        "opacities": torch.zeros_like(dev.opacities),
+        "sh": torch.zeros_like(dev.sh),
+    }
+
+
+def backward_device(view, dev: DeviceScene, seed, grads=None, stream=None) -> dict:
+    """Accumulate parameter gradients for ``seed`` (H,W,3 float32 CUDA)
+    into ``grads`` (dict of float32 CUDA tensors shaped like the scene)."""
+    if grads is None:
+        grads = zero_grads_device(dev)
+    seed = seed.contiguous()
+    view.backward(dev, seed, grads, stream=stream)
+    return grads
+
+
+# Reusable per-view device workspaces for the numpy API (a view grows its
+# buffers once and keeps them; allocating ~1 GB per call would dominate).
+_POOL: list = []
+_POOL_LOCK = threading.Lock()
+_POOL_MAX = 4
+
+
+def _acquire_view():
+    with _POOL_LOCK:
+        if _POOL:
+            return _POOL.pop()
+    return _native.View()
+
+
+def _release_view(view):
+    with _POOL_LOCK:
+        if len(_POOL) < _POOL_MAX:
+            _POOL.append(view)
+            return
+    view.close()
+
+
+class _ForwardState:
+    """Opaque device state handed from render_forward_cached to
+    render_backward (the reference cache is opaque too, render.py:435-436)."""
+
+    def __init__(self, view, dev, settings, outputs):
+        self.view, self.dev, self.settings, self.outputs = view, dev, settings, outputs
+        weakref.finalize(self, _release_view, view)
+
+
+class ForwardCache(Mapping):
+    """The reference cache dict (render.py:214-217) — keys rad, residual,
+    overdraw, sat, e_k, t_k, theta0, flat over pixels, float64 — fetched
+    from the device lazily on first access."""
+
+    KEYS = ("rad", "residual", "overdraw", "sat", "e_k", "t_k", "theta0")
+
+    def __init__(self, state: _ForwardState, result: RenderResult):
+        self._state = state
+        self._result = result
+        self._vals: dict = {}
+
+    def _load(self):
+        import torch
+        st = self._state
+        rgb, _, _ = st.outputs
+        H, W = rgb.shape[:2]
+        d = rgb.device
+        sat = torch.empty((H * W,), dtype=torch.uint8, device=d)
+        e_k = torch.empty((H * W, 3), dtype=torch.float32, device=d)
+        t_k = torch.empty((H * W,), dtype=torch.float32, device=d)
+        th0 = torch.empty((H * W, 3), dtype=torch.float32, device=d)
+        st.view.cache_export(sat, e_k, t_k, th0)
+        r = self._result
+        self._vals = {
+            "rad": r.rgb.reshape(-1, 3),
+            "residual": r.residual.reshape(-1),
+            "overdraw": r.overdraw.reshape(-1),
+            "sat": sat.cpu().numpy().astype(bool),
+            "e_k": e_k.cpu().numpy().astype(np.float64),
+            "t_k": t_k.cpu().numpy().astype(np.float64),
+            "theta0": th0.cpu().numpy().astype(np.float64),
+        }
+
+    def __getitem__(self, key):
+        if key == "_nxs":
+            return self._state
+        if key not in self.KEYS:
+            raise KeyError(key)
+        if not self._vals:
+            self._load()
+        return self._vals[key]
+
+    def __iter__(self):
+        return iter(self.KEYS)
+
+    def __len__(self):
+        return len(self.KEYS)
+
+
+def _result_to_host(out) -> RenderResult:
+    rgb, od, res = out
+    return RenderResult(rgb.double().cpu().numpy(), od.long().cpu().numpy(),
+                        res.double().cpu().numpy())
+
+
+def _settings(camera, model, background, max_splats, alpha_cutoff, near, chunk_size):
+    m = as_model(model)
+    return (int(camera.width), int(camera.height), float(camera.focal), float(camera.cx),
+            float(camera.cy), tuple(np.asarray(camera.position, dtype=np.float64).ravel()),
+            tuple(np.asarray(camera.rotation, dtype=np.float64).ravel()), m.variant,
+            float(m.param), tuple(np.asarray(background, dtype=np.float64).ravel()),
+            int(max_splats), float(alpha_cutoff), float(near),
+            None if chunk_size is None else int(chunk_size))
+
+
+def render(scene, camera, model, background, *, max_splats: int = 128,
+           alpha_cutoff: float = DEFAULT_ALPHA_CUTOFF, near: float = NEAR_PLANE,
+           chunk_size: int | None = None, threads: int = 1) -> RenderResult:
+    """Render radiance, overdraw and residual transmittance (reference
+    render.py:361-405).  ``threads`` is accepted and ignored: the output is
+    identical for any value, as in the reference."""
+    del threads
+    background = np.asarray(background, dtype=np.float64)
+    dev = _as_device_scene(scene)
+    view = _acquire_view()
+    try:
+        out = forward_device(view, dev, camera, model, background, max_splats=max_splats,
+                             alpha_cutoff=alpha_cutoff, near=near, chunk_size=chunk_size)
+        return _result_to_host(out)
+    finally:
+        _release_view(view)
+
+
+def render_forward_cached(arrs, camera, model, background, *, max_splats: int = 128,
+                          alpha_cutoff: float = DEFAULT_ALPHA_CUTOFF, near: float = NEAR_PLANE,
+                          chunk_size: int | None = None):
+    """Forward sweep plus the replay cache (reference render.py:408-425)."""
+    background = np.asarray(background, dtype=np.float64)
+    dev = _as_device_scene(arrs)
+    view = _acquire_view()
+    try:
+        out = forward_device(view, dev, camera, model, background, max_splats=max_splats,
+                             alpha_cutoff=alpha_cutoff, near=near, chunk_size=chunk_size)
+    except BaseException:
+        _release_view(view)
+        raise
+    result = _result_to_host(out)
+    st = _ForwardState(view, dev, _settings(camera, model, background, max_splats,
+                                            alpha_cutoff, near, chunk_size), out)
+    return result, ForwardCache(st, result)
+
+
+def render_backward(arrs, camera, model, background, cache, seed_image, *,
+                    max_splats: int = 128, alpha_cutoff: float = DEFAULT_ALPHA_CUTOFF,
+                    near: float = NEAR_PLANE, chunk_size: int | None = None) -> dict:
+    """Parameter gradients for an adjoint seed, replaying the traversal that
+    produced ``cache`` (reference render.py:428-442).  Settings must match
+    the forward call.  Unlike the reference (render.py:229-231) every
+    transmittance model has a backward here."""
+    import torch
+    try:
+        st = cache["_nxs"]
+    except (KeyError, TypeError):
+        raise ValueError("cache was not produced by this package's render_forward_cached")
+    if _settings(camera, model, background, max_splats, alpha_cutoff, near,
+                 chunk_size) != st.settings:
+        raise ValueError("render_backward settings must match the forward call")
+    if len(arrs) != st.dev.count:
+        raise ValueError("scene size differs from the forward call")
+    # the replay uses the forward's device scene (the cache describes it)
+    dev = st.dev
+    H, W = int(camera.height), int(camera.width)
+    seed = np.asarray(seed_image, dtype=np.float64).reshape(H, W, 3) if not isinstance(
+        seed_image, torch.Tensor) else seed_image
+    seed_t = seed if isinstance(seed, torch.Tensor) else torch.from_numpy(
+        np.ascontiguousarray(seed, dtype=np.float32))
+    seed_t = seed_t.to(device=dev.centers.device, dtype=torch.float32).contiguous()
+    g = backward_device(st.view, dev, seed_t)
+    return {k: v.double().cpu().numpy() for k, v in g.items()}
+
+
+def render_with_gradients(arrs, camera, model, background, seed_image, *,
+                          max_splats: int = 128, alpha_cutoff: float = DEFAULT_ALPHA_CUTOFF,
+                          near: float = NEAR_PLANE, chunk_size: int | None = None):
+    """Forward render plus parameter gradients (reference render.py:445-464)."""
+    result, cache = render_forward_cached(arrs, camera, model, background,
+                                          max_splats=max_splats, alpha_cutoff=alpha_cutoff,
+                                          near=near, chunk_size=chunk_size)
+    grads = render_backward(arrs, camera, model, background, cache, seed_image,
+                            max_splats=max_splats, alpha_cutoff=alpha_cutoff, near=near,
+                            chunk_size=chunk_size)
+    return result, grads

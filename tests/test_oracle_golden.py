@@ -1,0 +1,108 @@
+"""Pin the CPU oracle to the reference: every golden vector produced by the
+reference itself (tests/golden/make_golden.py) must be reproduced by
+oracle/splat_oracle.py.  CPU only."""
+import numpy as np
+import pytest
+
+from oracle import splat_oracle as O
+from tests._util import GRAD_FIELDS, MODELS, cam_from, load, scene_from
+
+SMALL = load("golden_small.npz")
+C1 = load("golden_c1.npz")
+FD = load("golden_fd.npz")
+
+
+@pytest.mark.parametrize("cs", [None, 1])
+@pytest.mark.parametrize("name", list(MODELS))
+def test_forward_small_matches_reference(name, cs):
+    d = SMALL
+    tag = f"{name}__{'none' if cs is None else cs}"
+    cam, sc, bg = cam_from(d), scene_from(d), d["bg"]
+    out = O.forward(sc, cam, MODELS[name], bg, chunk_size=cs)
+    H, W = cam.height, cam.width
+    np.testing.assert_allclose(out["rad"].reshape(H, W, 3), d[tag + "__rgb"], atol=1e-12)
+    np.testing.assert_array_equal(out["overdraw"].reshape(H, W), d[tag + "__overdraw"])
+    np.testing.assert_allclose(out["residual"].reshape(H, W), d[tag + "__residual"], atol=1e-12)
+    for k in ("e_k", "t_k", "theta0"):
+        np.testing.assert_allclose(out[k], d[tag + "__" + k], atol=1e-12)
+    np.testing.assert_array_equal(out["sat"], d[tag + "__sat"])
+
+
+@pytest.mark.parametrize("cs", [None, 1])
+@pytest.mark.parametrize("name", ["exponential", "linear", "quadratic_0.5"])
+def test_backward_small_matches_reference(name, cs):
+    d = SMALL
+    tag = f"{name}__{'none' if cs is None else cs}"
+    _, g = O.render_with_gradients(scene_from(d), cam_from(d), MODELS[name], d["bg"], d["seed"],
+                                   chunk_size=cs)
+    for k in GRAD_FIELDS:
+        ref = d[tag + "__g_" + k]
+        np.testing.assert_allclose(g[k], ref, rtol=1e-10, atol=1e-12 * np.abs(ref).max())
+
+
+@pytest.mark.parametrize("name", ["exponential", "linear", "quadratic_0.5", "softplus_20",
+                                  "blended_0.5"])
+def test_c1_matches_reference(name):
+    d = C1
+    cam, sc = cam_from(d), scene_from(d)
+    fwd, g = O.render_with_gradients(sc, cam, MODELS[name], d["bg"], d["seed"], chunk_size=1)
+    H, W = cam.height, cam.width
+    np.testing.assert_allclose(fwd["rad"].reshape(H, W, 3), d[name + "__rgb"], atol=1e-12)
+    np.testing.assert_array_equal(fwd["overdraw"].reshape(H, W), d[name + "__overdraw"])
+    if name + "__g_centers" in d:
+        for k in GRAD_FIELDS:
+            ref = d[name + "__g_" + k]
+            np.testing.assert_allclose(g[k], ref, rtol=1e-9, atol=1e-12 * np.abs(ref).max())
+
+
+@pytest.mark.parametrize("cs", [None, 1])
+@pytest.mark.parametrize("name", ["softplus_20", "blended_0.5", "exponential", "linear"])
+def test_backward_matches_reference_finite_differences(name, cs):
+    """The unified adjoint vs central FD of the reference forward (the
+    reference's only gradient oracle for softplus/blended); tolerance of
+    reference tests/test_primitives.py:363 (rel 2e-4, abs 2e-6)."""
+    d = FD
+    tag = f"{name}__{'none' if cs is None else cs}"
+    _, g = O.render_with_gradients(scene_from(d), cam_from(d), MODELS[name], d["bg"], d["seed"],
+                                   chunk_size=cs)
+    for k in GRAD_FIELDS:
+        fd = d[tag + "__fd_" + k]
+        np.testing.assert_allclose(g[k], fd, rtol=2e-4, atol=2e-6, err_msg=k)
+
+
+def test_transmit_study_overdraw_totals():
+    """Acceptance crit. 7 (reference tests/test_acceptance.py:210-225,
+    pkg/test_output.txt:23)."""
+    d = load("golden_transmit.npz")
+    cam, sc = cam_from(d), scene_from(d)
+    models = {"quadratic_1": ("quadratic", 1.0), "linear": ("linear", 0.0),
+              "quadratic_-0.5": ("quadratic", -0.5), "exponential": ("exponential", 0.0),
+              "power_law_2": ("power_law", 2.0)}
+    expect = {"quadratic_1": 37888, "linear": 51200, "quadratic_-0.5": 93184,
+              "exponential": 102400, "power_law_2": 102400}
+    from tests._util import Model
+    for name, (v, p) in models.items():
+        for cs in (None, 1):
+            out = O.forward(sc, cam, Model(v, p), np.zeros(3), chunk_size=cs)
+            total = int(out["overdraw"].sum())
+            assert total == int(d[f"{name}__{'none' if cs is None else cs}__overdraw_total"])
+            assert total == expect[name]
+
+
+def test_depth_order_matches_reference():
+    d = load("golden_order.npz")
+    sc = O.round_scene_f32(O.canonical_scene(100_000, seed=5))
+    for v in (0, 3):
+        cam = cam_from(d, f"v{v}_cam_")
+        np.testing.assert_array_equal(O.depth_order(sc, cam), d[f"v{v}_order"])
+
+
+def test_pixel_subset_is_exact():
+    """Pixel batching reproduces the full image (SURVEY Probe P3)."""
+    d = C1
+    cam, sc = cam_from(d), scene_from(d)
+    full = O.forward(sc, cam, MODELS["exponential"], d["bg"], chunk_size=1)
+    px = np.random.default_rng(0).choice(cam.width * cam.height, 97, replace=False)
+    sub = O.forward(sc, cam, MODELS["exponential"], d["bg"], chunk_size=1, pixels=px)
+    np.testing.assert_array_equal(sub["rad"], full["rad"][px])
+    np.testing.assert_array_equal(sub["overdraw"], full["overdraw"][px])
