@@ -53,7 +53,7 @@ extern "C" {
 #define NXS_ERR_CUDA (-3)          /* a CUDA call failed */
 #define NXS_ERR_NOMEM (-4)         /* device allocation failed */
 #define NXS_ERR_STATE (-5)         /* backward without a matching forward */
-#define NXS_ERR_GEOMETRY (-6)      /* Gaussian straddles the near plane (not yet supported) */
+#define NXS_ERR_GEOMETRY (-6)      /* reserved: unsupported geometry */
 
 /* transmittance variants: order of reference transmittance.py:32-40 */
 #define NXS_MODEL_EXPONENTIAL 0

@@ -9,7 +9,10 @@
  * reference pkg/src/nexsplat/render.py:109-138); what it does define, and
  * what this file follows, is:
  *   - the global order: stable argsort of the float64 view depth
- *     (μ - o)·forward, reference render.py:350-358;
+ *     (μ - o)·forward, reference render.py:350-358 (evaluated as a
+ *     compensated dot product: numpy's `@` goes through OpenBLAS with a
+ *     CPU-dependent FMA order, so the reference's last bit is not
+ *     machine-independent; see test_binning_oracle.py for the tie rule);
  *   - the per-Gaussian frame: normalised quaternion -> R
  *     (primitives.py:45-64), A = R diag(s^-2) R^T, b = μ - o
  *     (render.py:116-121);
@@ -46,6 +49,24 @@ static double ln_series(double x) {
   double s = inv_odd[0];
   for (int k = 1; k < 12; ++k) s = s * z2 + inv_odd[k];
   return (double)e * 0.69314718055994530942 + 2.0 * z * s;
+}
+
+/* compensated dot product (Dot2), same op sequence as the device's K0 */
+static double dot3_compensated(double a0, double a1, double a2, double b0, double b1, double b2) {
+  double p = a0 * b0;
+  double s = fma(a0, b0, -p);
+  double h = a1 * b1, r = fma(a1, b1, -h);
+  double t = p + h, bb = t - p, q = (p - (t - bb)) + (h - bb);
+  p = t;
+  s = s + (q + r);
+  h = a2 * b2;
+  r = fma(a2, b2, -h);
+  t = p + h;
+  bb = t - p;
+  q = (p - (t - bb)) + (h - bb);
+  p = t;
+  s = s + (q + r);
+  return p + s;
 }
 
 static uint64_t depth_key(double d) {
@@ -92,7 +113,7 @@ int64_t nxs_oracle_binning(int64_t P, const float* centers, const float* scales,
     double b0 = (double)centers[3 * i + 0] - cam_o[0];
     double b1 = (double)centers[3 * i + 1] - cam_o[1];
     double b2 = (double)centers[3 * i + 2] - cam_o[2];
-    double depth = (b0 * cam_R[2] + b1 * cam_R[5]) + b2 * cam_R[8];
+    double depth = dot3_compensated(b0, b1, b2, cam_R[2], cam_R[5], cam_R[8]);
     key[i] = depth_key(depth);
     idx[i] = (uint32_t)i;
   }

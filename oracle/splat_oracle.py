@@ -73,7 +73,8 @@ class Scene:
         self.quats = np.asarray(quats, dtype=np.float64).reshape(-1, 4)
         self.opacities = np.asarray(opacities, dtype=np.float64).reshape(-1)
         sh = np.asarray(sh, dtype=np.float64)
-        self.sh = sh.reshape(len(self.opacities), 3, -1)
+        c = sh.shape[-1] if sh.ndim == 3 else max(1, sh.size // max(1, 3 * len(self.opacities)))
+        self.sh = sh.reshape(len(self.opacities), 3, c)
 
     @classmethod
     def of(cls, s) -> "Scene":

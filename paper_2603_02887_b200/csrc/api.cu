@@ -27,14 +27,14 @@ void launch_emit_pairs(const int4*, const unsigned long long*, int64_t, int, uin
                        cudaStream_t);
 void launch_tile_ranges(const uint32_t*, int64_t, int2*, cudaStream_t);
 void launch_blend_fwd(bool, int, const float4*, const uint32_t*, const int2*, const CamDev&,
-                      const ModelDev&, int, float, const float*, float*, int32_t*, float*,
-                      const PixCache&, Counters*, cudaStream_t);
+                      const ModelDev&, int, float, double, const float*, float*, int32_t*,
+                      float*, const PixCache&, Counters*, cudaStream_t);
 void launch_blend_bwd(bool, int, const float4*, const uint32_t*, const int2*, const CamDev&,
-                      const ModelDev&, float, const float*, const float*, const PixCache&,
-                      double*, Counters*, cudaStream_t);
+                      const ModelDev&, float, double, const float*, const float*,
+                      const PixCache&, double*, Counters*, cudaStream_t);
 void launch_chain(const float*, const float*, const float*, int, int64_t, const uint32_t*,
-                  const CamDev&, const double*, float*, float*, float*, float*, float*,
-                  cudaStream_t);
+                  const float4*, const CamDev&, const double*, float*, float*, float*, float*,
+                  float*, cudaStream_t);
 }  // namespace nxs
 
 using namespace nxs;
@@ -367,10 +367,6 @@ int nxs_forward(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
   const unsigned long long n_pairs = v->host_small[0] + v->host_small[1];
   v->stats.n_straddling = (int64_t)v->host_small[2];
   v->stats.n_pairs = (int64_t)n_pairs;
-  if (v->host_small[2] > 0)
-    return fail(NXS_ERR_GEOMETRY,
-                std::to_string(v->host_small[2]) +
-                    " Gaussian(s) cross the near plane; not supported by the device path yet");
   if (n_pairs >= (1ull << 31)) return fail(NXS_ERR_NOMEM, "more than 2^31 tile pairs");
 
   NXS_CUDA(cudaMemsetAsync(v->ranges.p, 0, (size_t)n_tiles * sizeof(int2), s));
@@ -408,7 +404,7 @@ int nxs_forward(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
   const float bgf[3] = {background[0], background[1], background[2]};
   launch_blend_fwd(count, n_tiles, v->records.as<float4>(), v->pv_out.as<uint32_t>(),
                    v->ranges.as<int2>(), cam, md, opts->max_splats, (float)opts->alpha_cutoff,
-                   bgf, rgb, overdraw, residual, v->cache(), cnt, s);
+                   opts->near_plane, bgf, rgb, overdraw, residual, v->cache(), cnt, s);
   NXS_LAUNCHED("blend_fwd");
   mark(v, 7, s);
   v->ev_fwd = true;
@@ -453,12 +449,12 @@ int nxs_backward(nxs_view* v, const nxs_scene* scene, const float* seed, float* 
   unsigned long long* dsmall = v->dev_small.as<unsigned long long>();
   Counters* cnt = reinterpret_cast<Counters*>(dsmall + 1);
   launch_blend_bwd(count, v->n_tiles, v->records.as<float4>(), v->pv_out.as<uint32_t>(),
-                   v->ranges.as<int2>(), v->cam, v->model, (float)v->opts.alpha_cutoff, v->bg,
-                   seed, v->cache(), v->moments.as<double>(), cnt, s);
+                   v->ranges.as<int2>(), v->cam, v->model, (float)v->opts.alpha_cutoff,
+                   v->opts.near_plane, v->bg, seed, v->cache(), v->moments.as<double>(), cnt, s);
   NXS_LAUNCHED("blend_bwd");
   mark(v, 10, s);
   launch_chain(scene->centers, scene->scales, scene->quats, v->C, P, v->idx_out.as<uint32_t>(),
-               v->cam, v->moments.as<double>(), g_centers, g_scales, g_quats, g_opacities, g_sh,
+               v->records.as<float4>(), v->cam, v->moments.as<double>(), g_centers, g_scales, g_quats, g_opacities, g_sh,
                s);
   NXS_LAUNCHED("chain");
   mark(v, 11, s);

@@ -45,10 +45,11 @@ __device__ __forceinline__ float transpose_reduce32(float (&v)[32], int lane) {
 template <int FAM, bool COUNT>
 __global__ void __launch_bounds__(TILE_PIX)
     k_blend_bwd(const float4* __restrict__ records, const uint32_t* __restrict__ pairs,
-                const int2* __restrict__ ranges, CamDev cam, ModelDev m, float cutoff, float bg0,
-                float bg1, float bg2, const float* __restrict__ seed, PixCache cache,
+                const int2* __restrict__ ranges, CamDev cam, ModelDev m, float cutoff,
+                double near_plane, float bg0, float bg1, float bg2,
+                const float* __restrict__ seed, PixCache cache,
                 double* __restrict__ moments, Counters* __restrict__ cnt) {
-  __shared__ float4 s_rec[BWD_BATCH][7];
+  __shared__ float4 s_rec[BWD_BATCH][REC_F4];
   __shared__ uint32_t s_rank[BWD_BATCH];
   __shared__ float s_acc[BWD_BATCH * NMOM];
   __shared__ int s_maxlast;
@@ -82,6 +83,7 @@ __global__ void __launch_bounds__(TILE_PIX)
   float ek0 = bg0, ek1 = bg1, ek2 = bg2;
   float carry = 0.f;  // Θ (τ-family) or U (P-family), seed-contracted
   const float gam = (FAM == FAM_EXP) ? 1.0f : m.c;
+  const float inv_f = (float)(1.0 / cam.f);
   unsigned long long ntest = 0, nent = 0;
 
   if (tid == 0) s_maxlast = -1;
@@ -100,7 +102,7 @@ __global__ void __launch_bounds__(TILE_PIX)
     __syncthreads();
     for (int k = tid; k < n * 8; k += TILE_PIX) {
       const int e = k >> 3, part = k & 7;
-      if (part < 7) s_rec[e][part] = records[(size_t)s_rank[e] * REC_F4 + part];
+      s_rec[e][part] = records[(size_t)s_rank[e] * REC_F4 + part];
     }
     __syncthreads();
     if (COUNT) nent += n;
@@ -114,7 +116,14 @@ __global__ void __launch_bounds__(TILE_PIX)
       if (idx <= last) {
         if (COUNT) ++ntest;
         TestOut t;
-        if (ray_peak_test(s_rec[j][0], s_rec[j][1], s_rec[j][2], s_rec[j][3], pc, cutoff, t)) {
+        const bool gen = (__float_as_int(s_rec[j][3].w) & RF_GENERAL) != 0;  // block-uniform
+        float gx = 0.f, gy = 0.f, gz = 0.f;
+        bool ok;
+        if (gen)
+          ok = general_test(s_rec[j], cam, px, py, cutoff, near_plane, t, gx, gy, gz);
+        else
+          ok = ray_peak_test(s_rec[j][0], s_rec[j][1], s_rec[j][2], s_rec[j][3], pc, cutoff, t);
+        if (ok) {
           contrib = true;
           const float alpha = t.alpha;
           float E0, E1, E2;
@@ -149,21 +158,37 @@ __global__ void __launch_bounds__(TILE_PIX)
             dE0 = s0 * w;
             dE1 = s1 * w;
             dE2 = s2 * w;
-            // chain to the conic moments (zero when α is clamped, render.py:327)
+            // chain moments (render.py:326-339 in the camera frame): by the
+            // envelope theorem ∂m2/∂A' = diff'diff'ᵀ and ∂m2/∂b' = -2A'diff',
+            // with the peak offset diff' = b'_z·e, e = δ - ε h, δ = Δ/f,
+            // ε = δᵀA'h / D — all O(|δ|) terms, no cancellation against b'
             const float dae = (t.araw >= ALPHA_MAX_F) ? 0.f : da;
-            const float q = __fdividef(-0.5f * alpha * dae, t.D);
-            v[0] = q * t.ddx * t.ddx;
-            v[1] = q * t.ddx * t.ddy;
-            v[2] = q * t.ddy * t.ddy;
-            v[3] = q * t.ddx;
-            v[4] = q * t.ddy;
-            const float qm = q * t.m2;
-            v[5] = qm * pc.hx * pc.hx;
-            v[6] = qm * pc.hx * pc.hy;
-            v[7] = qm * pc.hx;
-            v[8] = qm * pc.hy * pc.hy;
-            v[9] = qm * pc.hy;
-            v[10] = qm;
+            const float dm2 = -0.5f * alpha * dae;
+            float ex, ey, ez;
+            if (gen) {  // world-frame diff (K5 knows the record kind)
+              ex = gx;
+              ey = gy;
+              ez = gz;
+            } else {
+              const float4 r2 = s_rec[j][2];
+              const float dxn = t.ddx * inv_f, dyn = t.ddy * inv_f;
+              const float Ahx = r2.x * t.u;
+              const float Ahy = fmaf(r2.x * r2.y, t.u, r2.w * t.v);
+              const float eps = __fdividef(fmaf(dxn, Ahx, dyn * Ahy), t.D);
+              ex = fmaf(-eps, pc.hx, dxn);
+              ey = fmaf(-eps, pc.hy, dyn);
+              ez = -eps;
+            }
+            const float wx = dm2 * ex, wy = dm2 * ey, wz = dm2 * ez;
+            v[0] = wx * ex;
+            v[1] = wx * ey;
+            v[2] = wx * ez;
+            v[3] = wy * ey;
+            v[4] = wy * ez;
+            v[5] = wz * ez;
+            v[6] = wx;
+            v[7] = wy;
+            v[8] = wz;
             v[11] = dae * t.kern;
           }
           // SH moments dE_c·[E_c > 0]·Y_k (render.py:340-341)
@@ -217,26 +242,27 @@ __global__ void __launch_bounds__(TILE_PIX)
 template <int FAM>
 static void launch_bwd_fam(bool count, int n_tiles, const float4* records, const uint32_t* pairs,
                            const int2* ranges, const CamDev& cam, const ModelDev& m,
-                           float cutoff, const float* bg, const float* seed,
+                           float cutoff, double near_plane, const float* bg, const float* seed,
                            const PixCache& cache, double* moments, Counters* cnt,
                            cudaStream_t s) {
   if (count)
     k_blend_bwd<FAM, true><<<n_tiles, TILE_PIX, 0, s>>>(records, pairs, ranges, cam, m, cutoff,
-                                                         bg[0], bg[1], bg[2], seed, cache,
-                                                         moments, cnt);
+                                                         near_plane, bg[0], bg[1], bg[2], seed,
+                                                         cache, moments, cnt);
   else
     k_blend_bwd<FAM, false><<<n_tiles, TILE_PIX, 0, s>>>(records, pairs, ranges, cam, m, cutoff,
-                                                          bg[0], bg[1], bg[2], seed, cache,
-                                                          moments, cnt);
+                                                          near_plane, bg[0], bg[1], bg[2], seed,
+                                                          cache, moments, cnt);
 }
 
 void launch_blend_bwd(bool count, int n_tiles, const float4* records, const uint32_t* pairs,
                       const int2* ranges, const CamDev& cam, const ModelDev& m, float cutoff,
-                      const float* bg, const float* seed, const PixCache& cache, double* moments,
-                      Counters* cnt, cudaStream_t s) {
+                      double near_plane, const float* bg, const float* seed,
+                      const PixCache& cache, double* moments, Counters* cnt, cudaStream_t s) {
   if (n_tiles == 0) return;
 #define NXS_BWD(F) \
-  launch_bwd_fam<F>(count, n_tiles, records, pairs, ranges, cam, m, cutoff, bg, seed, cache, moments, cnt, s)
+  launch_bwd_fam<F>(count, n_tiles, records, pairs, ranges, cam, m, cutoff, near_plane, bg, seed, \
+                    cache, moments, cnt, s)
   switch (m.fam) {
     case FAM_EXP: NXS_BWD(FAM_EXP); break;
     case FAM_LIN: NXS_BWD(FAM_LIN); break;

@@ -43,6 +43,7 @@ __device__ __forceinline__ PixelConst pixel_setup(const CamDev& cam, int px, int
 struct TestOut {
   float ddx, ddy;  // Δ in pixels
   float D;         // hᵀ A' h
+  float u, v;      // D = a·u² + d·v² + g  (so (A'h)_x = a·u, (A'h)_y = a·b·u + d·v)
   float m2;        // Mahalanobis distance² at the ray peak
   float kern;      // exp(-m2/2)
   float araw;      // opacity·kern (unclamped)
@@ -57,8 +58,10 @@ __device__ __forceinline__ bool ray_peak_test(const float4& r0, const float4& r1
   o.ddy = __fsub_rn(__fsub_rn(pc.pyc, r0.y), r0.w);
   float w = __fmaf_rn(r1.y, o.ddy, o.ddx);
   float num = __fmaf_rn(__fmul_rn(r1.x, w), w, __fmul_rn(__fmul_rn(r1.z, o.ddy), o.ddy));
-  float u = __fadd_rn(__fmaf_rn(r2.y, pc.hy, r2.z), pc.hx);
-  float v = __fadd_rn(pc.hy, r3.x);
+  const float u = __fadd_rn(__fmaf_rn(r2.y, pc.hy, r2.z), pc.hx);
+  const float v = __fadd_rn(pc.hy, r3.x);
+  o.u = u;
+  o.v = v;
   o.D = __fmaf_rn(__fmul_rn(r2.x, u), u, __fmaf_rn(__fmul_rn(r2.w, v), v, r3.y));
   // cheap reject against the cutoff ellipse (r2m carries a 1e-4 margin)
   if (num > __fmul_rn(r1.w, o.D)) return false;
@@ -67,6 +70,53 @@ __device__ __forceinline__ bool ray_peak_test(const float4& r0, const float4& r1
   o.araw = __fmul_rn(r3.z, o.kern);
   o.alpha = fminf(o.araw, ALPHA_MAX_F);
   return o.alpha >= cutoff;
+}
+
+// General path (records flagged RF_GENERAL: the cutoff ellipsoid reaches
+// the near region, so the conic form and its implied t > near do not hold):
+// the reference's per-(Gaussian, pixel) formula, render.py:122-134, in fp64
+// with explicit IEEE ops (identical in the forward and backward kernels).
+// Outputs the world-frame peak offset diff = t·d - b for the chain.
+__device__ __forceinline__ bool general_test(const float4* rec, const CamDev& cam, int px, int py,
+                                             float cutoff, double near_plane, TestOut& o,
+                                             float& gdx, float& gdy, float& gdz) {
+  const double* dp = reinterpret_cast<const double*>(rec);
+  const double b0 = dp[0], b1 = dp[1], b2 = dp[2];
+  const double A00 = dp[3], A01 = dp[4], A02 = dp[5], A11 = dp[6], A12 = dp[14], A22 = dp[15];
+  const float opac = reinterpret_cast<const float*>(rec)[14];
+  // unit world direction through the pixel centre (primitives.py:192-203)
+  const double hx = __ddiv_rn(__dsub_rn(__dadd_rn((double)px, 0.5), cam.cx), cam.f);
+  const double hy = __ddiv_rn(__dsub_rn(__dadd_rn((double)py, 0.5), cam.cy), cam.f);
+  double d0 = __dadd_rn(__dadd_rn(__dmul_rn(hx, cam.R[0]), __dmul_rn(hy, cam.R[1])), cam.R[2]);
+  double d1 = __dadd_rn(__dadd_rn(__dmul_rn(hx, cam.R[3]), __dmul_rn(hy, cam.R[4])), cam.R[5]);
+  double d2 = __dadd_rn(__dadd_rn(__dmul_rn(hx, cam.R[6]), __dmul_rn(hy, cam.R[7])), cam.R[8]);
+  const double nd = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)),
+                                         __dmul_rn(d2, d2)));
+  d0 = __ddiv_rn(d0, nd);
+  d1 = __ddiv_rn(d1, nd);
+  d2 = __ddiv_rn(d2, nd);
+#define NXS_DOT3(a0, a1, a2, c0, c1, c2) \
+  __dadd_rn(__dadd_rn(__dmul_rn(a0, c0), __dmul_rn(a1, c1)), __dmul_rn(a2, c2))
+  const double Ad0 = NXS_DOT3(A00, A01, A02, d0, d1, d2);
+  const double Ad1 = NXS_DOT3(A01, A11, A12, d0, d1, d2);
+  const double Ad2 = NXS_DOT3(A02, A12, A22, d0, d1, d2);
+  const double dAd = NXS_DOT3(Ad0, Ad1, Ad2, d0, d1, d2);
+  const double bAd = NXS_DOT3(b0, b1, b2, Ad0, Ad1, Ad2);
+  const double t = __ddiv_rn(bAd, dAd);
+  const double x0 = __dsub_rn(__dmul_rn(t, d0), b0);
+  const double x1 = __dsub_rn(__dmul_rn(t, d1), b1);
+  const double x2 = __dsub_rn(__dmul_rn(t, d2), b2);
+  const double m2 = NXS_DOT3(x0, x1, x2, NXS_DOT3(A00, A01, A02, x0, x1, x2),
+                             NXS_DOT3(A01, A11, A12, x0, x1, x2), NXS_DOT3(A02, A12, A22, x0, x1, x2));
+#undef NXS_DOT3
+  o.m2 = (float)m2;
+  o.kern = ex2_approx(__fmul_rn(-0.72134752044448170368f, o.m2));
+  o.araw = __fmul_rn(opac, o.kern);
+  o.alpha = fminf(o.araw, ALPHA_MAX_F);
+  gdx = (float)x0;
+  gdy = (float)x1;
+  gdz = (float)x2;
+  return (t > near_plane) && (o.alpha >= cutoff);
 }
 
 // E_c = max(Σ_k sh[c][k] Y_k, 0); returns the positivity mask bits.

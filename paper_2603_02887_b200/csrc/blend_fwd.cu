@@ -23,10 +23,11 @@ template <int FAM, bool COUNT>
 __global__ void __launch_bounds__(TILE_PIX)
     k_blend_fwd(const float4* __restrict__ records, const uint32_t* __restrict__ pairs,
                 const int2* __restrict__ ranges, CamDev cam, ModelDev m, int max_splats,
-                float cutoff, float bg0, float bg1, float bg2, float* __restrict__ rgb,
+                float cutoff, double near_plane, float bg0, float bg1, float bg2,
+                float* __restrict__ rgb,
                 int32_t* __restrict__ overdraw, float* __restrict__ residual, PixCache cache,
                 Counters* __restrict__ cnt) {
-  __shared__ float4 s_rec[TILE_PIX][7];
+  __shared__ float4 s_rec[TILE_PIX][REC_F4];
   __shared__ uint32_t s_rank[TILE_PIX];
 
   const int tile = blockIdx.x;
@@ -57,15 +58,21 @@ __global__ void __launch_bounds__(TILE_PIX)
     __syncthreads();
     for (int k = tid; k < n * 8; k += TILE_PIX) {
       const int e = k >> 3, part = k & 7;
-      if (part < 7) s_rec[e][part] = records[(size_t)s_rank[e] * REC_F4 + part];
+      s_rec[e][part] = records[(size_t)s_rank[e] * REC_F4 + part];
     }
     __syncthreads();
     if (!done) {
       for (int j = 0; j < n; ++j) {
         if (COUNT) ++ntest;
         TestOut t;
-        if (!ray_peak_test(s_rec[j][0], s_rec[j][1], s_rec[j][2], s_rec[j][3], pc, cutoff, t))
-          continue;
+        bool ok;
+        if (__float_as_int(s_rec[j][3].w) & RF_GENERAL) {  // block-uniform branch
+          float gx, gy, gz;
+          ok = general_test(s_rec[j], cam, px, py, cutoff, near_plane, t, gx, gy, gz);
+        } else {
+          ok = ray_peak_test(s_rec[j][0], s_rec[j][1], s_rec[j][2], s_rec[j][3], pc, cutoff, t);
+        }
+        if (!ok) continue;
         const int idx = base + j;
         const float alpha = t.alpha;
         float E0, E1, E2;
@@ -163,27 +170,30 @@ __global__ void __launch_bounds__(TILE_PIX)
 template <int FAM>
 static void launch_fwd_fam(bool count, int n_tiles, const float4* records, const uint32_t* pairs,
                            const int2* ranges, const CamDev& cam, const ModelDev& m,
-                           int max_splats, float cutoff, const float* bg, float* rgb,
-                           int32_t* overdraw, float* residual, const PixCache& cache,
+                           int max_splats, float cutoff, double near_plane, const float* bg,
+                           float* rgb, int32_t* overdraw, float* residual, const PixCache& cache,
                            Counters* cnt, cudaStream_t s) {
   if (count)
     k_blend_fwd<FAM, true><<<n_tiles, TILE_PIX, 0, s>>>(records, pairs, ranges, cam, m,
-                                                         max_splats, cutoff, bg[0], bg[1], bg[2],
-                                                         rgb, overdraw, residual, cache, cnt);
+                                                         max_splats, cutoff, near_plane, bg[0],
+                                                         bg[1], bg[2], rgb, overdraw, residual,
+                                                         cache, cnt);
   else
     k_blend_fwd<FAM, false><<<n_tiles, TILE_PIX, 0, s>>>(records, pairs, ranges, cam, m,
-                                                          max_splats, cutoff, bg[0], bg[1], bg[2],
-                                                          rgb, overdraw, residual, cache, cnt);
+                                                          max_splats, cutoff, near_plane, bg[0],
+                                                          bg[1], bg[2], rgb, overdraw, residual,
+                                                          cache, cnt);
 }
 
 void launch_blend_fwd(bool count, int n_tiles, const float4* records, const uint32_t* pairs,
                       const int2* ranges, const CamDev& cam, const ModelDev& m, int max_splats,
-                      float cutoff, const float* bg, float* rgb, int32_t* overdraw,
-                      float* residual, const PixCache& cache, Counters* cnt, cudaStream_t s) {
+                      float cutoff, double near_plane, const float* bg, float* rgb,
+                      int32_t* overdraw, float* residual, const PixCache& cache, Counters* cnt,
+                      cudaStream_t s) {
   if (n_tiles == 0) return;
 #define NXS_FWD(F)                                                                            \
-  launch_fwd_fam<F>(count, n_tiles, records, pairs, ranges, cam, m, max_splats, cutoff, bg, rgb, \
-                    overdraw, residual, cache, cnt, s)
+  launch_fwd_fam<F>(count, n_tiles, records, pairs, ranges, cam, m, max_splats, cutoff,       \
+                    near_plane, bg, rgb, overdraw, residual, cache, cnt, s)
   switch (m.fam) {
     case FAM_EXP: NXS_FWD(FAM_EXP); break;
     case FAM_LIN: NXS_FWD(FAM_LIN); break;

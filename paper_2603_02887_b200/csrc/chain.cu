@@ -1,60 +1,27 @@
 // K5: per-Gaussian moments -> parameter gradients, fp64.
 //
 // Replaces the reference chain (pkg/src/nexsplat/render.py:326-341, with
-// quat_rot_jacobian primitives.py:67-93).  With m2 = ΔᵀN'Δ / hᵀA'h
-// (SURVEY §8.0.5/§8.0.7), for any parameter direction θ̇:
-//   Σ_px dm2 ∂m2/∂θ = Σ_ij Ṅ'_ij S_ij − 2 Σ_ij N'_ij ċ_i S_j − Σ_kl Ȧ'_kl H_kl
-// where S_ij = Σ dm2 Δ_iΔ_j/D, S_i = Σ dm2 Δ_i/D, H_kl = Σ dm2 m2 h_k h_l/D
-// are the moments K4 accumulated (dm2 = -½·α·dα).  Each parameter (μ 3,
-// s 3, q 4) is one forward-mode tangent through (A', b') -> (N', c).  The
-// quaternion gradient is projected orthogonally to the unit quaternion
+// quat_rot_jacobian primitives.py:67-93).  K4 accumulated, in the camera
+// frame and per rank,
+//     X = Σ_px dm2 · e eᵀ   (6 values, symmetric 3x3)
+//     Y = Σ_px dm2 · e      (3 values)
+// with dm2 = -½·α·dα (dα zeroed where α is clamped, render.py:327) and
+// e = diff'/b'_z the kernel-peak offset.  By the envelope theorem (the peak
+// depth's own dependence drops out, primitives.py:245-249)
+//     ∂m2/∂A' = diff' diff'ᵀ,   ∂m2/∂b' = -2 A' diff',
+// so for any parameter tangent (Ȧ', ḃ')
+//     Σ_px dm2 ∂m2/∂θ = b'_z² Σ_kl Ȧ'_kl X_kl − 2 b'_z ḃ'ᵀ A' Y.
+// μ moves b' (= Rcᵀ(μ − o)); s and q move A' (= Rcᵀ R diag(s⁻²) Rᵀ Rc).
+// The quaternion gradient is projected orthogonally to the unit quaternion
 // without a 1/|q| factor, exactly as render.py:339 does.
 #include "nxs_internal.cuh"
 
 namespace nxs {
 
-struct ChainGeo {
-  double M[9];    // Rc^T R
-  double Ap[9];   // camera-frame inverse covariance
-  double bp[3];   // camera-frame centre offset
-  double Ab[3];   // A' b'
-  double bAb;
-  double Np[3];   // N'00, N'01, N'11 (pixel units)
-};
-
-struct Mom {
-  double S00, S01, S11, Sx, Sy, H00, H01, H02, H11, H12, H22;
-};
-
-// contribution of one tangent (dAp symmetric 3x3, dbp 3-vector)
-__device__ __forceinline__ double tangent_contract(const ChainGeo& G, const Mom& mo,
-                                                   const double* dAp, const double* dbp,
-                                                   double f) {
-  double dAb[3];
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-    dAb[i] = dAp[3 * i + 0] * G.bp[0] + dAp[3 * i + 1] * G.bp[1] + dAp[3 * i + 2] * G.bp[2] +
-             G.Ap[3 * i + 0] * dbp[0] + G.Ap[3 * i + 1] * dbp[1] + G.Ap[3 * i + 2] * dbp[2];
-  const double dbAb = dbp[0] * G.Ab[0] + dbp[1] * G.Ab[1] + dbp[2] * G.Ab[2] +
-                      G.bp[0] * dAb[0] + G.bp[1] * dAb[1] + G.bp[2] * dAb[2];
-  const double if2 = 1.0 / (f * f);
-  const double dN00 = (dbAb * G.Ap[0] + G.bAb * dAp[0] - 2.0 * dAb[0] * G.Ab[0]) * if2;
-  const double dN01 =
-      (dbAb * G.Ap[1] + G.bAb * dAp[1] - dAb[0] * G.Ab[1] - G.Ab[0] * dAb[1]) * if2;
-  const double dN11 = (dbAb * G.Ap[4] + G.bAb * dAp[4] - 2.0 * dAb[1] * G.Ab[1]) * if2;
-  const double bz = G.bp[2];
-  const double dcx = f * (dbp[0] * bz - G.bp[0] * dbp[2]) / (bz * bz);
-  const double dcy = f * (dbp[1] * bz - G.bp[1] * dbp[2]) / (bz * bz);
-  double acc = dN00 * mo.S00 + 2.0 * dN01 * mo.S01 + dN11 * mo.S11;
-  acc -= 2.0 * ((G.Np[0] * dcx + G.Np[1] * dcy) * mo.Sx + (G.Np[1] * dcx + G.Np[2] * dcy) * mo.Sy);
-  acc -= dAp[0] * mo.H00 + 2.0 * dAp[1] * mo.H01 + 2.0 * dAp[2] * mo.H02 + dAp[4] * mo.H11 +
-         2.0 * dAp[5] * mo.H12 + dAp[8] * mo.H22;
-  return acc;
-}
-
 __global__ void k_chain(const float* __restrict__ centers, const float* __restrict__ scales,
                         const float* __restrict__ quats, int C, int64_t P,
-                        const uint32_t* __restrict__ order, CamDev cam,
+                        const uint32_t* __restrict__ order,
+                        const float4* __restrict__ records, CamDev cam,
                         const double* __restrict__ moments, float* __restrict__ g_centers,
                         float* __restrict__ g_scales, float* __restrict__ g_quats,
                         float* __restrict__ g_opac, float* __restrict__ g_sh) {
@@ -71,88 +38,95 @@ __global__ void k_chain(const float* __restrict__ centers, const float* __restri
   if (!any) return;
   const int64_t g = order[r];
 
-  // SH and opacity need no geometry
+  // opacity and SH need no geometry
   g_opac[g] += (float)mv[11];
   for (int c = 0; c < 3; ++c)
     for (int k = 0; k < C; ++k) g_sh[(g * 3 + c) * C + k] += (float)mv[12 + 4 * c + k];
 
-  const Mom mo{mv[0], mv[1], mv[2], mv[3], mv[4], mv[5], mv[6], mv[7], mv[8], mv[9], mv[10]};
-  if (mo.S00 == 0.0 && mo.S01 == 0.0 && mo.S11 == 0.0 && mo.Sx == 0.0 && mo.Sy == 0.0 &&
-      mo.H22 == 0.0)
-    return;
+  bool geo = false;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) geo |= (mv[k] != 0.0);
+  if (!geo) return;
+  // symmetric X, vector Y
+  const double X[9] = {mv[0], mv[1], mv[2], mv[1], mv[3], mv[4], mv[2], mv[4], mv[5]};
+  const double Y[3] = {mv[6], mv[7], mv[8]};
 
-  double qw = quats[4 * g + 0], qx = quats[4 * g + 1], qy = quats[4 * g + 2], qz = quats[4 * g + 3];
+  const double qw = quats[4 * g + 0], qx = quats[4 * g + 1], qy = quats[4 * g + 2],
+               qz = quats[4 * g + 3];
   const double nq = sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
   const double w = qw / nq, x = qx / nq, y = qy / nq, z = qz / nq;
-  double R[9] = {1.0 - 2.0 * (y * y + z * z), 2.0 * (x * y - w * z), 2.0 * (x * z + w * y),
-                 2.0 * (x * y + w * z), 1.0 - 2.0 * (x * x + z * z), 2.0 * (y * z - w * x),
-                 2.0 * (x * z - w * y), 2.0 * (y * z + w * x), 1.0 - 2.0 * (x * x + y * y)};
+  const double R[9] = {1.0 - 2.0 * (y * y + z * z), 2.0 * (x * y - w * z), 2.0 * (x * z + w * y),
+                       2.0 * (x * y + w * z), 1.0 - 2.0 * (x * x + z * z), 2.0 * (y * z - w * x),
+                       2.0 * (x * z - w * y), 2.0 * (y * z + w * x), 1.0 - 2.0 * (x * x + y * y)};
   const double s[3] = {scales[3 * g + 0], scales[3 * g + 1], scales[3 * g + 2]};
   const double is[3] = {1.0 / (s[0] * s[0]), 1.0 / (s[1] * s[1]), 1.0 / (s[2] * s[2])};
-  ChainGeo G;
+  // conic records: camera frame (F = Rc, M = Rcᵀ R, κ = b'_z);
+  // general records: world frame (F = I, M = R, κ = 1), moments of diff itself
+  const bool gen = (__float_as_int(records[r * REC_F4 + 3].w) & RF_GENERAL) != 0;
+  double F[9];
+  for (int i = 0; i < 9; ++i) F[i] = gen ? ((i % 4 == 0) ? 1.0 : 0.0) : cam.R[i];
+  double M[9], Ap[9];
   for (int i = 0; i < 3; ++i)
     for (int j = 0; j < 3; ++j)
-      G.M[3 * i + j] = cam.R[0 + i] * R[0 + j] + cam.R[3 + i] * R[3 + j] + cam.R[6 + i] * R[6 + j];
+      M[3 * i + j] = F[0 + i] * R[0 + j] + F[3 + i] * R[3 + j] + F[6 + i] * R[6 + j];
   for (int i = 0; i < 3; ++i)
     for (int j = 0; j < 3; ++j)
-      G.Ap[3 * i + j] = G.M[3 * i + 0] * is[0] * G.M[3 * j + 0] +
-                        G.M[3 * i + 1] * is[1] * G.M[3 * j + 1] +
-                        G.M[3 * i + 2] * is[2] * G.M[3 * j + 2];
-  const double b[3] = {(double)centers[3 * g + 0] - cam.o[0], (double)centers[3 * g + 1] - cam.o[1],
+      Ap[3 * i + j] = M[3 * i + 0] * is[0] * M[3 * j + 0] + M[3 * i + 1] * is[1] * M[3 * j + 1] +
+                      M[3 * i + 2] * is[2] * M[3 * j + 2];
+  const double b[3] = {(double)centers[3 * g + 0] - cam.o[0],
+                       (double)centers[3 * g + 1] - cam.o[1],
                        (double)centers[3 * g + 2] - cam.o[2]};
-  for (int i = 0; i < 3; ++i) G.bp[i] = cam.R[0 + i] * b[0] + cam.R[3 + i] * b[1] + cam.R[6 + i] * b[2];
-  for (int i = 0; i < 3; ++i)
-    G.Ab[i] = G.Ap[3 * i + 0] * G.bp[0] + G.Ap[3 * i + 1] * G.bp[1] + G.Ap[3 * i + 2] * G.bp[2];
-  G.bAb = G.bp[0] * G.Ab[0] + G.bp[1] * G.Ab[1] + G.bp[2] * G.Ab[2];
-  const double f = cam.f, if2 = 1.0 / (f * f);
-  G.Np[0] = (G.bAb * G.Ap[0] - G.Ab[0] * G.Ab[0]) * if2;
-  G.Np[1] = (G.bAb * G.Ap[1] - G.Ab[0] * G.Ab[1]) * if2;
-  G.Np[2] = (G.bAb * G.Ap[4] - G.Ab[1] * G.Ab[1]) * if2;
+  const double bz = gen ? 1.0 : cam.R[2] * b[0] + cam.R[5] * b[1] + cam.R[8] * b[2];
+  const double bz2 = bz * bz;
 
-  const double zero3[3] = {0.0, 0.0, 0.0};
-  double dAp[9];
-  // μ_k: b' moves along row k of Rc (b' = Rc^T (μ - o))
+  // μ: ∂L/∂b' = -2 b'_z A'Y, ∂L/∂μ = Rc ∂L/∂b'
+  double AY[3];
+  for (int i = 0; i < 3; ++i) AY[i] = Ap[3 * i + 0] * Y[0] + Ap[3 * i + 1] * Y[1] + Ap[3 * i + 2] * Y[2];
+  for (int k = 0; k < 3; ++k)
+    g_centers[3 * g + k] +=
+        (float)(-2.0 * bz * (F[3 * k + 0] * AY[0] + F[3 * k + 1] * AY[1] + F[3 * k + 2] * AY[2]));
+
+  // s_k: Ȧ' = -2/s_k³ M_k M_kᵀ  ->  b'_z² (-2/s_k³) M_kᵀ X M_k
   for (int k = 0; k < 3; ++k) {
-    for (int i = 0; i < 9; ++i) dAp[i] = 0.0;
-    const double dbp[3] = {cam.R[3 * k + 0], cam.R[3 * k + 1], cam.R[3 * k + 2]};
-    g_centers[3 * g + k] += (float)tangent_contract(G, mo, dAp, dbp, f);
-  }
-  // s_k: A' += -2/s_k^3 M[:,k] M[:,k]^T
-  for (int k = 0; k < 3; ++k) {
-    const double coef = -2.0 / (s[k] * s[k] * s[k]);
+    double Xm[3];
     for (int i = 0; i < 3; ++i)
-      for (int j = 0; j < 3; ++j) dAp[3 * i + j] = coef * G.M[3 * i + k] * G.M[3 * j + k];
-    g_scales[3 * g + k] += (float)tangent_contract(G, mo, dAp, zero3, f);
+      Xm[i] = X[3 * i + 0] * M[0 + k] + X[3 * i + 1] * M[3 + k] + X[3 * i + 2] * M[6 + k];
+    const double mXm = M[0 + k] * Xm[0] + M[3 + k] * Xm[1] + M[6 + k] * Xm[2];
+    g_scales[3 * g + k] += (float)(bz2 * (-2.0 / (s[k] * s[k] * s[k])) * mXm);
   }
-  // q_k: dR = J_k (primitives.py:67-93), dM = Rc^T dR, dA' = dM Λ M^T + M Λ dM^T
+
+  // q_k: Ṙ = J_k (primitives.py:67-93), Ṁ = Rcᵀ Ṙ, Ȧ' = Ṁ Λ Mᵀ + M Λ Ṁᵀ
+  //      Σ Ȧ'⊙X = 2 Σ_l is_l (Ṁ_{:,l})ᵀ X M_{:,l}
+  double XM[9];  // X M, column l = X M_{:,l}
+  for (int i = 0; i < 3; ++i)
+    for (int l = 0; l < 3; ++l)
+      XM[3 * i + l] = X[3 * i + 0] * M[0 + l] + X[3 * i + 1] * M[3 + l] + X[3 * i + 2] * M[6 + l];
   double gq[4];
   for (int k = 0; k < 4; ++k) {
-    double J[9];
+    double t[9];
     if (k == 0) {
-      const double t[9] = {0, -z, y, z, 0, -x, -y, x, 0};
-      for (int i = 0; i < 9; ++i) J[i] = 2.0 * t[i];
+      const double v[9] = {0, -z, y, z, 0, -x, -y, x, 0};
+      for (int i = 0; i < 9; ++i) t[i] = 2.0 * v[i];
     } else if (k == 1) {
-      const double t[9] = {0, y, z, y, -2 * x, -w, z, w, -2 * x};
-      for (int i = 0; i < 9; ++i) J[i] = 2.0 * t[i];
+      const double v[9] = {0, y, z, y, -2 * x, -w, z, w, -2 * x};
+      for (int i = 0; i < 9; ++i) t[i] = 2.0 * v[i];
     } else if (k == 2) {
-      const double t[9] = {-2 * y, x, w, x, 0, z, -w, z, -2 * y};
-      for (int i = 0; i < 9; ++i) J[i] = 2.0 * t[i];
+      const double v[9] = {-2 * y, x, w, x, 0, z, -w, z, -2 * y};
+      for (int i = 0; i < 9; ++i) t[i] = 2.0 * v[i];
     } else {
-      const double t[9] = {-2 * z, -w, x, w, -2 * z, y, x, y, 0};
-      for (int i = 0; i < 9; ++i) J[i] = 2.0 * t[i];
+      const double v[9] = {-2 * z, -w, x, w, -2 * z, y, x, y, 0};
+      for (int i = 0; i < 9; ++i) t[i] = 2.0 * v[i];
     }
-    double dM[9];
-    for (int i = 0; i < 3; ++i)
-      for (int j = 0; j < 3; ++j)
-        dM[3 * i + j] = cam.R[0 + i] * J[0 + j] + cam.R[3 + i] * J[3 + j] + cam.R[6 + i] * J[6 + j];
-    for (int i = 0; i < 3; ++i)
-      for (int j = 0; j < 3; ++j) {
-        double v = 0.0;
-        for (int l = 0; l < 3; ++l)
-          v += is[l] * (dM[3 * i + l] * G.M[3 * j + l] + G.M[3 * i + l] * dM[3 * j + l]);
-        dAp[3 * i + j] = v;
+    double acc = 0.0;
+    for (int l = 0; l < 3; ++l) {
+      double col = 0.0;  // (Ṁ_{:,l})ᵀ (X M)_{:,l}, Ṁ_il = Σ_k Rc_ki J_kl
+      for (int i = 0; i < 3; ++i) {
+        const double dMil = F[0 + i] * t[0 + l] + F[3 + i] * t[3 + l] + F[6 + i] * t[6 + l];
+        col += dMil * XM[3 * i + l];
       }
-    gq[k] = tangent_contract(G, mo, dAp, zero3, f);
+      acc += is[l] * col;
+    }
+    gq[k] = bz2 * 2.0 * acc;
   }
   const double dot = w * gq[0] + x * gq[1] + y * gq[2] + z * gq[3];
   g_quats[4 * g + 0] += (float)(gq[0] - w * dot);
@@ -162,12 +136,13 @@ __global__ void k_chain(const float* __restrict__ centers, const float* __restri
 }
 
 void launch_chain(const float* centers, const float* scales, const float* quats, int C, int64_t P,
-                  const uint32_t* order, const CamDev& cam, const double* moments,
+                  const uint32_t* order, const float4* records, const CamDev& cam,
+                  const double* moments,
                   float* g_centers, float* g_scales, float* g_quats, float* g_opac, float* g_sh,
                   cudaStream_t s) {
   if (P == 0) return;
-  k_chain<<<(unsigned)((P + 127) / 128), 128, 0, s>>>(centers, scales, quats, C, P, order, cam,
-                                                      moments, g_centers, g_scales, g_quats,
+  k_chain<<<(unsigned)((P + 127) / 128), 128, 0, s>>>(centers, scales, quats, C, P, order,
+                                                      records, cam, moments, g_centers, g_scales, g_quats,
                                                       g_opac, g_sh);
 }
 

@@ -29,7 +29,12 @@ constexpr double SH_C1 = 0.4886025119029199;
 constexpr float P_FLOOR = 1e-30f;
 
 // record flags (stored as int bits in rec[3].w)
-constexpr int RF_CONIC = 1;
+constexpr int RF_CONIC = 1;    // centred-conic fp32 evaluation
+constexpr int RF_GENERAL = 2;  // crosses the near region: fp64 reference diff-form
+// General-path record: fp64 world-frame b = μ - o and A = R diag(s⁻²) Rᵀ
+// (upper triangle) packed as doubles 0..6 = b0 b1 b2 A00 A01 A02 A11 (float
+// words 0..13) and doubles 14..15 = A12 A22 (float words 28..31); words 14
+// (opacity), 15 (flags) and 16..27 (SH) keep their conic-record meaning.
 
 struct CamDev {
   double o[3];

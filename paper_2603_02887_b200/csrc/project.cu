@@ -43,6 +43,31 @@ __device__ __forceinline__ double ln_det(double x) {
   return (double)e * 0.69314718055994530942 + 2.0 * z * s;
 }
 
+// Compensated 3-term dot product (Ogita-Rump-Oishi Dot2: TwoProd via fma,
+// TwoSum cascade).  The reference computes the depth with numpy's `@`,
+// which runs through OpenBLAS with a CPU-dependent FMA/summation order, so
+// its last bit is not machine-independent; Dot2 is as accurate as a
+// double-double evaluation rounded once, and deterministic on both nvcc and
+// gcc.  Orders can then differ from the reference only between Gaussians
+// whose depths agree to a few ulps (true ties up to rounding).
+__device__ __forceinline__ double dot3_compensated(double a0, double a1, double a2, double b0,
+                                                   double b1, double b2) {
+  double p = a0 * b0;
+  double s = __fma_rn(a0, b0, -p);
+  double h = a1 * b1, r = __fma_rn(a1, b1, -h);
+  double t = p + h, bb = t - p, q = (p - (t - bb)) + (h - bb);
+  p = t;
+  s = s + (q + r);
+  h = a2 * b2;
+  r = __fma_rn(a2, b2, -h);
+  t = p + h;
+  bb = t - p;
+  q = (p - (t - bb)) + (h - bb);
+  p = t;
+  s = s + (q + r);
+  return p + s;
+}
+
 // K0: fp64 view depth (μ - o)·forward -> order-preserving u64 key.
 __global__ void k_depth_keys(const float* __restrict__ centers, int64_t P, CamDev cam,
                              unsigned long long* __restrict__ keys,
@@ -53,7 +78,7 @@ __global__ void k_depth_keys(const float* __restrict__ centers, int64_t P, CamDe
   double b1 = (double)centers[3 * i + 1] - cam.o[1];
   double b2 = (double)centers[3 * i + 2] - cam.o[2];
   // forward = third column of the camera rotation
-  double depth = (b0 * cam.R[2] + b1 * cam.R[5]) + b2 * cam.R[8];
+  double depth = dot3_compensated(b0, b1, b2, cam.R[2], cam.R[5], cam.R[8]);
   unsigned long long u = (unsigned long long)__double_as_longlong(depth);
   keys[i] = (u >> 63) ? ~u : (u | 0x8000000000000000ull);
   idx[i] = (uint32_t)i;
@@ -148,10 +173,13 @@ __global__ void k_project(const float* __restrict__ centers, const float* __rest
   double zmin = bp[2] - rm * sz;
   double zmax = bp[2] + rm * sz;
   if (live && zmax <= 0.0) live = false;  // entirely behind the camera plane
+  bool general = false;
   if (live && zmin <= near_plane * 1.001) {
-    // crosses the near region: the conic form does not apply
+    // crosses the near region: the conic form (and its implied t > near)
+    // does not apply; evaluate the reference formula in fp64 per pixel over
+    // the whole screen
     atomicAdd(out.straddle, 1ull);
-    live = false;
+    general = true;
   }
 
   // --- per-pixel test coefficients (Cholesky-style forms)
@@ -166,7 +194,7 @@ __global__ void k_project(const float* __restrict__ centers, const float* __rest
   double A11s = Ap[4] - Ap[1] * bb, A12s = Ap[5] - Ap[1] * cc, A22s = Ap[8] - Ap[2] * cc;
   double d = A11s, e = A12s / d, gg = A22s - A12s * e;
 
-  if (live) {
+  if (live && !general) {
     // --- silhouette conic Q = N - r2m A' and its dual: tile bbox
     double Q[9];
 #pragma unroll
@@ -201,10 +229,36 @@ __global__ void k_project(const float* __restrict__ centers, const float* __rest
     }
   }
 
-  rec[0] = make_float4(cxh, cyh, cxl, cyl);
-  rec[1] = make_float4((float)n0, (float)kk, (float)n1, (float)r2m);
-  rec[2] = make_float4((float)a, (float)bb, (float)cc, (float)d);
-  rec[3] = make_float4((float)e, (float)gg, (float)opac, __int_as_float(RF_CONIC));
+  if (general) {
+    rect = make_int4(0, 0, cam.tiles_x - 1, cam.tiles_y - 1);
+    ntile = (unsigned long long)cam.tiles_x * (unsigned long long)cam.tiles_y;
+    // world-frame A = R diag(s^-2) R^T, b = μ - o (render.py:116-121)
+    double A[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = i; j < 3; ++j)
+        A[3 * i + j] = ((R[3 * i + 0] * is0) * R[3 * j + 0] + (R[3 * i + 1] * is1) * R[3 * j + 1]) +
+                       (R[3 * i + 2] * is2) * R[3 * j + 2];
+    double* dp = reinterpret_cast<double*>(rec);
+    dp[0] = b0;
+    dp[1] = b1;
+    dp[2] = b2;
+    dp[3] = A[0];
+    dp[4] = A[1];
+    dp[5] = A[2];
+    dp[6] = A[4];
+    dp[14] = A[5];
+    dp[15] = A[8];
+    float* fw = reinterpret_cast<float*>(rec);
+    fw[14] = (float)opac;
+    fw[15] = __int_as_float(RF_GENERAL);
+  } else {
+    rec[0] = make_float4(cxh, cyh, cxl, cyl);
+    rec[1] = make_float4((float)n0, (float)kk, (float)n1, (float)r2m);
+    rec[2] = make_float4((float)a, (float)bb, (float)cc, (float)d);
+    rec[3] = make_float4((float)e, (float)gg, (float)opac, __int_as_float(RF_CONIC));
+  }
   float shv[12];
 #pragma unroll
   for (int c = 0; c < 3; ++c)
@@ -213,8 +267,8 @@ __global__ void k_project(const float* __restrict__ centers, const float* __rest
   rec[4] = make_float4(shv[0], shv[1], shv[2], shv[3]);
   rec[5] = make_float4(shv[4], shv[5], shv[6], shv[7]);
   rec[6] = make_float4(shv[8], shv[9], shv[10], shv[11]);
-  // reserved for the exact-order mode: t-coefficients (A'b')·h and z_lo
-  rec[7] = make_float4((float)Ab[0], (float)Ab[1], (float)Ab[2], (float)zmin);
+  // conic: reserved for the exact-order mode (t-coefficients (A'b')·h, z_lo)
+  if (!general) rec[7] = make_float4((float)Ab[0], (float)Ab[1], (float)Ab[2], (float)zmin);
   out.rects[r] = rect;
   out.n_tiles[r] = ntile;
 }

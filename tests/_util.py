@@ -75,3 +75,25 @@ def grad_report(g, ref, mass=None):
         if mass is not None:
             mass_f += int((np.abs(a - b) > ATOL + RTOL * np.asarray(mass[k])).sum())
     return strict, mass_f, total
+
+
+def exact_depths(centers, cam):
+    """View depths (μ - o)·forward in 80-bit extended precision."""
+    c = np.asarray(centers, dtype=np.longdouble) - np.asarray(cam.position, dtype=np.longdouble)
+    f = np.asarray(cam.rotation, dtype=np.longdouble)[:, 2]
+    return (c * f).sum(axis=1)
+
+
+def assert_order_matches_up_to_ties(got, ref, depths, ulps=4):
+    """Orders must agree except between Gaussians whose depths agree to a
+    few ulps (the reference's own depth rounding is CPU-dependent)."""
+    got, ref = np.asarray(got), np.asarray(ref)
+    assert sorted(got.tolist()) == sorted(ref.tolist())
+    bad = np.nonzero(got != ref)[0]
+    if bad.size == 0:
+        return 0
+    dg = depths[got[bad]].astype(np.float64)
+    dr = depths[ref[bad]].astype(np.float64)
+    tol = ulps * np.spacing(np.abs(dr))
+    assert (np.abs(dg - dr) <= tol).all(), bad[np.abs(dg - dr) > tol][:10]
+    return int(bad.size)
