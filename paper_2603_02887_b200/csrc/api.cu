@@ -22,19 +22,18 @@ void launch_depth_keys(const float*, int64_t, const CamDev&, unsigned long long*
                        cudaStream_t);
 void launch_project(const float*, const float*, const float*, const float*, const float*, int,
                     int64_t, const uint32_t*, const CamDev&, double, double, unsigned long long*,
-                    int4*, float4*, unsigned long long*, cudaStream_t);
+                    int4*, float4*, float4*, unsigned long long*, cudaStream_t);
 void launch_emit_pairs(const int4*, const unsigned long long*, int64_t, int, uint32_t*, uint32_t*,
                        cudaStream_t);
 void launch_tile_ranges(const uint32_t*, int64_t, int2*, cudaStream_t);
 void launch_blend_fwd(bool, int, const float4*, const uint32_t*, const int2*, const CamDev&,
                       const ModelDev&, int, float, double, const float*, float*, int32_t*,
                       float*, const PixCache&, Counters*, cudaStream_t);
-void launch_blend_bwd(bool, int, const float4*, const uint32_t*, const int2*, const CamDev&,
-                      const ModelDev&, float, double, const float*, const float*,
+void launch_blend_bwd(bool, int, const float4*, const float4*, const uint32_t*, const int2*,
+                      const CamDev&, const ModelDev&, float, double, const float*, const float*,
                       const PixCache&, double*, Counters*, cudaStream_t);
-void launch_chain(const float*, const float*, const float*, int, int64_t, const uint32_t*,
-                  const float4*, const CamDev&, const double*, float*, float*, float*, float*,
-                  float*, cudaStream_t);
+void launch_chain(const float*, const float*, int, int64_t, const uint32_t*, const double*,
+                  float*, float*, float*, float*, float*, cudaStream_t);
 }  // namespace nxs
 
 using namespace nxs;
@@ -96,7 +95,7 @@ int bits_for(uint32_t n) {
 
 struct nxs_view {
   // per Gaussian
-  Buf dkeys_in, dkeys_out, idx_in, idx_out, records, rects, ntiles, offsets, moments;
+  Buf dkeys_in, dkeys_out, idx_in, idx_out, records, bframe, rects, ntiles, offsets, moments;
   // per pair
   Buf pk_in, pk_out, pv_in, pv_out;
   // per tile / pixel
@@ -121,7 +120,7 @@ struct nxs_view {
   nxs_stats stats{};
 
   ~nxs_view() {
-    Buf* all[] = {&dkeys_in, &dkeys_out, &idx_in, &idx_out, &records, &rects, &ntiles, &offsets,
+    Buf* all[] = {&dkeys_in, &dkeys_out, &idx_in, &idx_out, &records, &bframe, &rects, &ntiles, &offsets,
                   &moments, &pk_in, &pk_out, &pv_in, &pv_out, &ranges, &c_last, &c_sat, &c_tk,
                   &c_thi, &c_tlo, &c_P, &c_ck, &c_Pck, &c_ek, &c_th0, &temp, &dev_small};
     for (Buf* b : all) b->release();
@@ -130,7 +129,7 @@ struct nxs_view {
       for (auto& e : ev) cudaEventDestroy(e);
   }
   int64_t bytes() const {
-    const Buf* all[] = {&dkeys_in, &dkeys_out, &idx_in, &idx_out, &records, &rects, &ntiles,
+    const Buf* all[] = {&dkeys_in, &dkeys_out, &idx_in, &idx_out, &records, &bframe, &rects, &ntiles,
                         &offsets, &moments, &pk_in, &pk_out, &pv_in, &pv_out, &ranges, &c_last,
                         &c_sat, &c_tk, &c_thi, &c_tlo, &c_P, &c_ck, &c_Pck, &c_ek, &c_th0,
                         &temp, &dev_small};
@@ -300,6 +299,7 @@ int nxs_forward(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
   NXS_CUDA(ensure_n<uint32_t>(v->idx_in, P));
   NXS_CUDA(ensure_n<uint32_t>(v->idx_out, P));
   NXS_CUDA(ensure_n<float4>(v->records, P * REC_F4));
+  NXS_CUDA(ensure_n<float4>(v->bframe, P * 3));
   NXS_CUDA(ensure_n<int4>(v->rects, P));
   NXS_CUDA(ensure_n<unsigned long long>(v->ntiles, P));
   NXS_CUDA(ensure_n<unsigned long long>(v->offsets, P));
@@ -344,7 +344,7 @@ int nxs_forward(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
     launch_project(scene->centers, scene->scales, scene->quats, scene->opacities, scene->sh, C, P,
                    v->idx_out.as<uint32_t>(), cam, opts->alpha_cutoff, opts->near_plane,
                    v->ntiles.as<unsigned long long>(), v->rects.as<int4>(),
-                   v->records.as<float4>(), dsmall, s);
+                   v->records.as<float4>(), v->bframe.as<float4>(), dsmall, s);
     NXS_LAUNCHED("project");
     mark(v, 2, s);
     tb = v->temp.cap;
@@ -448,14 +448,14 @@ int nxs_backward(nxs_view* v, const nxs_scene* scene, const float* seed, float* 
   const bool count = (v->opts.flags & NXS_FLAG_COUNT_EVENTS) != 0;
   unsigned long long* dsmall = v->dev_small.as<unsigned long long>();
   Counters* cnt = reinterpret_cast<Counters*>(dsmall + 1);
-  launch_blend_bwd(count, v->n_tiles, v->records.as<float4>(), v->pv_out.as<uint32_t>(),
+  launch_blend_bwd(count, v->n_tiles, v->records.as<float4>(), v->bframe.as<float4>(),
+                   v->pv_out.as<uint32_t>(),
                    v->ranges.as<int2>(), v->cam, v->model, (float)v->opts.alpha_cutoff,
                    v->opts.near_plane, v->bg, seed, v->cache(), v->moments.as<double>(), cnt, s);
   NXS_LAUNCHED("blend_bwd");
   mark(v, 10, s);
-  launch_chain(scene->centers, scene->scales, scene->quats, v->C, P, v->idx_out.as<uint32_t>(),
-               v->records.as<float4>(), v->cam, v->moments.as<double>(), g_centers, g_scales, g_quats, g_opacities, g_sh,
-               s);
+  launch_chain(scene->scales, scene->quats, v->C, P, v->idx_out.as<uint32_t>(),
+               v->moments.as<double>(), g_centers, g_scales, g_quats, g_opacities, g_sh, s);
   NXS_LAUNCHED("chain");
   mark(v, 11, s);
   v->ev_bwd = true;

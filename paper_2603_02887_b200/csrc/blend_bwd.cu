@@ -17,41 +17,41 @@
 // saturating splat only receives dE = s·T̄_k (render.py:313-314).  No
 // per-sample state is stored.
 //
-// Reduction: per list entry each warp reduces its 32 pixels' 24 moments
-// with a transpose-reduce (31 shuffles), lanes 0..23 add into a per-entry
-// shared accumulator, and after each batch the block flushes the non-zero
-// sums with one fp64 atomic each into the per-rank moment buffer.
+// Reduction: per list entry each warp transposes its 32 pixels' 24 moments
+// through shared memory (24 column stores, 8 row loads, 31 adds), lanes
+// 0..23 add into a per-entry shared accumulator, and after each batch the
+// block flushes the non-zero sums with one fp64 atomic each into the
+// per-rank moment buffer.
 #include "blend_common.cuh"
 
 namespace nxs {
 
-constexpr int BWD_BATCH = 128;  // list entries staged per batch
+constexpr int BWD_BATCH = 64;  // list entries staged per batch
 
-// v[32] per lane -> returns Σ_lanes v[lane]
-__device__ __forceinline__ float transpose_reduce32(float (&v)[32], int lane) {
-#pragma unroll
-  for (int step = 16; step >= 1; step >>= 1) {
-    const bool upper = (lane & step) != 0;
-#pragma unroll
-    for (int k = 0; k < step; ++k) {
-      const float send = upper ? v[k] : v[k + step];
-      const float keep = upper ? v[k + step] : v[k];
-      v[k] = keep + __shfl_xor_sync(0xffffffffu, send, step);
-    }
-  }
-  return v[0];
-}
+// Shared-memory layout of one block (dynamic): staged records, their ranks,
+// per-entry moment accumulators, and one 24x36-float transpose scratch per
+// warp (row k = moment k of all 32 lanes; rows padded to 36 floats so the
+// column stores and the 16-B row loads are both bank-conflict free).
+constexpr int RED_STRIDE = 36;
+constexpr int RED_WARP = NMOM * RED_STRIDE;  // floats per warp
+constexpr size_t BWD_SMEM = sizeof(float4) * BWD_BATCH * (REC_F4 + 3) + sizeof(uint32_t) * BWD_BATCH +
+                            sizeof(float) * BWD_BATCH * NMOM +
+                            sizeof(float) * RED_WARP * (TILE_PIX / 32);
 
 template <int FAM, bool COUNT>
-__global__ void __launch_bounds__(TILE_PIX)
-    k_blend_bwd(const float4* __restrict__ records, const uint32_t* __restrict__ pairs,
+__global__ void __launch_bounds__(TILE_PIX, 3)
+    k_blend_bwd(const float4* __restrict__ records, const float4* __restrict__ bframe,
+                const uint32_t* __restrict__ pairs,
                 const int2* __restrict__ ranges, CamDev cam, ModelDev m, float cutoff,
                 double near_plane, float bg0, float bg1, float bg2,
                 const float* __restrict__ seed, PixCache cache,
                 double* __restrict__ moments, Counters* __restrict__ cnt) {
-  __shared__ float4 s_rec[BWD_BATCH][REC_F4];
-  __shared__ uint32_t s_rank[BWD_BATCH];
-  __shared__ float s_acc[BWD_BATCH * NMOM];
+  extern __shared__ float4 smem_dyn[];
+  float4(*s_rec)[REC_F4] = reinterpret_cast<float4(*)[REC_F4]>(smem_dyn);
+  float4(*s_bf)[3] = reinterpret_cast<float4(*)[3]>(smem_dyn + BWD_BATCH * REC_F4);
+  uint32_t* s_rank = reinterpret_cast<uint32_t*>(smem_dyn + BWD_BATCH * (REC_F4 + 3));
+  float* s_acc = reinterpret_cast<float*>(s_rank + BWD_BATCH);
+  float* s_red = s_acc + BWD_BATCH * NMOM;
   __shared__ int s_maxlast;
 
   const int tile = blockIdx.x;
@@ -61,6 +61,7 @@ __global__ void __launch_bounds__(TILE_PIX)
   const bool inside = px < cam.W && py < cam.H;
   const PixelConst pc = pixel_setup(cam, px, py);
   const int pix = py * cam.W + px;
+  float* red = s_red + (tid >> 5) * RED_WARP;
 
   int last = -1;
   bool sat = false;
@@ -84,6 +85,7 @@ __global__ void __launch_bounds__(TILE_PIX)
   float carry = 0.f;  // Θ (τ-family) or U (P-family), seed-contracted
   const float gam = (FAM == FAM_EXP) ? 1.0f : m.c;
   const float inv_f = (float)(1.0 / cam.f);
+  const float Y0 = (float)SH_C0;
   unsigned long long ntest = 0, nent = 0;
 
   if (tid == 0) s_maxlast = -1;
@@ -104,14 +106,19 @@ __global__ void __launch_bounds__(TILE_PIX)
       const int e = k >> 3, part = k & 7;
       s_rec[e][part] = records[(size_t)s_rank[e] * REC_F4 + part];
     }
+    for (int k = tid; k < n * 3; k += TILE_PIX) {
+      const int e = k / 3, part = k - 3 * (k / 3);
+      s_bf[e][part] = bframe[(size_t)s_rank[e] * 3 + part];
+    }
     __syncthreads();
     if (COUNT) nent += n;
 
     for (int j = n - 1; j >= 0; --j) {
       const int idx = base + j;
-      float v[32];
-#pragma unroll
-      for (int k = 0; k < 32; ++k) v[k] = 0.f;
+      // per-pixel contribution as a few scalars; all zero when this lane
+      // contributes nothing, so the 24 moments need no separate zeroing
+      float dm2 = 0.f, ex = 0.f, ey = 0.f, ez = 0.f, dak = 0.f;
+      float e0 = 0.f, e1 = 0.f, e2 = 0.f;
       bool contrib = false;
       if (idx <= last) {
         if (COUNT) ++ntest;
@@ -158,61 +165,84 @@ __global__ void __launch_bounds__(TILE_PIX)
             dE0 = s0 * w;
             dE1 = s1 * w;
             dE2 = s2 * w;
-            // chain moments (render.py:326-339 in the camera frame): by the
-            // envelope theorem ∂m2/∂A' = diff'diff'ᵀ and ∂m2/∂b' = -2A'diff',
-            // with the peak offset diff' = b'_z·e, e = δ - ε h, δ = Δ/f,
-            // ε = δᵀA'h / D — all O(|δ|) terms, no cancellation against b'
+            // chain moments (render.py:326-339): by the envelope theorem the
+            // kernel-peak offset u = Rᵀ(t·d - b) carries the whole chain
+            // (∂m2/∂μ = -2RΛu, ∂m2/∂s_k = -2u_k²/s_k³, ∂m2/∂R = 2 diff (Λu)ᵀ).
+            // u is built from the stable conic offset diff' = b'_z·e,
+            // e = δ - ε h, δ = Δ/f, ε = δᵀA'h/D (all O(|δ|), no cancellation
+            // against b'), rotated into the Gaussian frame per pixel so each
+            // moment term has the sign structure of the reference's terms
             const float dae = (t.araw >= ALPHA_MAX_F) ? 0.f : da;
-            const float dm2 = -0.5f * alpha * dae;
-            float ex, ey, ez;
-            if (gen) {  // world-frame diff (K5 knows the record kind)
-              ex = gx;
-              ey = gy;
-              ez = gz;
+            dm2 = -0.5f * alpha * dae;
+            dak = dae * t.kern;
+            float qx, qy, qz;  // peak offset e (conic: diff'/b'_z; general: diff)
+            if (gen) {
+              qx = gx;
+              qy = gy;
+              qz = gz;
             } else {
               const float4 r2 = s_rec[j][2];
               const float dxn = t.ddx * inv_f, dyn = t.ddy * inv_f;
               const float Ahx = r2.x * t.u;
               const float Ahy = fmaf(r2.x * r2.y, t.u, r2.w * t.v);
               const float eps = __fdividef(fmaf(dxn, Ahx, dyn * Ahy), t.D);
-              ex = fmaf(-eps, pc.hx, dxn);
-              ey = fmaf(-eps, pc.hy, dyn);
-              ez = -eps;
+              qx = fmaf(-eps, pc.hx, dxn);
+              qy = fmaf(-eps, pc.hy, dyn);
+              qz = -eps;
             }
-            const float wx = dm2 * ex, wy = dm2 * ey, wz = dm2 * ez;
-            v[0] = wx * ex;
-            v[1] = wx * ey;
-            v[2] = wx * ez;
-            v[3] = wy * ey;
-            v[4] = wy * ez;
-            v[5] = wz * ez;
-            v[6] = wx;
-            v[7] = wy;
-            v[8] = wz;
-            v[11] = dae * t.kern;
+            // Gaussian-frame offset u = Rᵀ diff = B e
+            const float4 B0 = s_bf[j][0], B1 = s_bf[j][1], B2 = s_bf[j][2];
+            ex = fmaf(B0.x, qx, fmaf(B0.y, qy, B0.z * qz));
+            ey = fmaf(B1.x, qx, fmaf(B1.y, qy, B1.z * qz));
+            ez = fmaf(B2.x, qx, fmaf(B2.y, qy, B2.z * qz));
           }
-          // SH moments dE_c·[E_c > 0]·Y_k (render.py:340-341)
-          const float Y0 = (float)SH_C0;
-          const float e0 = (mask & 1) ? dE0 : 0.f;
-          const float e1 = (mask & 2) ? dE1 : 0.f;
-          const float e2 = (mask & 4) ? dE2 : 0.f;
-          v[12] = e0 * Y0;
-          v[13] = e0 * pc.Y1;
-          v[14] = e0 * pc.Y2;
-          v[15] = e0 * pc.Y3;
-          v[16] = e1 * Y0;
-          v[17] = e1 * pc.Y1;
-          v[18] = e1 * pc.Y2;
-          v[19] = e1 * pc.Y3;
-          v[20] = e2 * Y0;
-          v[21] = e2 * pc.Y1;
-          v[22] = e2 * pc.Y2;
-          v[23] = e2 * pc.Y3;
+          // SH moments use dE_c·[E_c > 0] (render.py:340-341)
+          e0 = (mask & 1) ? dE0 : 0.f;
+          e1 = (mask & 2) ? dE1 : 0.f;
+          e2 = (mask & 4) ? dE2 : 0.f;
         }
       }
       if (__any_sync(0xffffffffu, contrib)) {
-        const float r = transpose_reduce32(v, lane);
-        if (lane < NMOM && r != 0.f) atomicAdd(&s_acc[j * NMOM + lane], r);
+        // warp transpose-reduce through shared memory: lane r writes its 24
+        // moments down column r, lane k < 24 then sums row k
+        const float wx = dm2 * ex, wy = dm2 * ey, wz = dm2 * ez;
+        float* col = red + lane;
+        col[0 * RED_STRIDE] = wx * ex;
+        col[1 * RED_STRIDE] = wx * ey;
+        col[2 * RED_STRIDE] = wx * ez;
+        col[3 * RED_STRIDE] = wy * ey;
+        col[4 * RED_STRIDE] = wy * ez;
+        col[5 * RED_STRIDE] = wz * ez;
+        col[6 * RED_STRIDE] = wx;
+        col[7 * RED_STRIDE] = wy;
+        col[8 * RED_STRIDE] = wz;
+        col[9 * RED_STRIDE] = 0.f;
+        col[10 * RED_STRIDE] = 0.f;
+        col[11 * RED_STRIDE] = dak;
+        col[12 * RED_STRIDE] = e0 * Y0;
+        col[13 * RED_STRIDE] = e0 * pc.Y1;
+        col[14 * RED_STRIDE] = e0 * pc.Y2;
+        col[15 * RED_STRIDE] = e0 * pc.Y3;
+        col[16 * RED_STRIDE] = e1 * Y0;
+        col[17 * RED_STRIDE] = e1 * pc.Y1;
+        col[18 * RED_STRIDE] = e1 * pc.Y2;
+        col[19 * RED_STRIDE] = e1 * pc.Y3;
+        col[20 * RED_STRIDE] = e2 * Y0;
+        col[21 * RED_STRIDE] = e2 * pc.Y1;
+        col[22 * RED_STRIDE] = e2 * pc.Y2;
+        col[23 * RED_STRIDE] = e2 * pc.Y3;
+        __syncwarp();
+        if (lane < NMOM && lane != 9 && lane != 10) {
+          const float4* row = reinterpret_cast<const float4*>(red + lane * RED_STRIDE);
+          float4 a = row[0], b = row[1], c = row[2], d = row[3];
+          float4 e = row[4], f = row[5], g = row[6], h = row[7];
+          const float s = (((a.x + a.y) + (a.z + a.w)) + ((b.x + b.y) + (b.z + b.w))) +
+                          (((c.x + c.y) + (c.z + c.w)) + ((d.x + d.y) + (d.z + d.w))) +
+                          ((((e.x + e.y) + (e.z + e.w)) + ((f.x + f.y) + (f.z + f.w))) +
+                           (((g.x + g.y) + (g.z + g.w)) + ((h.x + h.y) + (h.z + h.w))));
+          if (s != 0.f) atomicAdd(&s_acc[j * NMOM + lane], s);
+        }
+        __syncwarp();
       }
     }
     __syncthreads();
@@ -240,28 +270,42 @@ __global__ void __launch_bounds__(TILE_PIX)
 }
 
 template <int FAM>
-static void launch_bwd_fam(bool count, int n_tiles, const float4* records, const uint32_t* pairs,
+static void launch_bwd_fam(bool count, int n_tiles, const float4* records, const float4* bframe,
+                           const uint32_t* pairs,
                            const int2* ranges, const CamDev& cam, const ModelDev& m,
                            float cutoff, double near_plane, const float* bg, const float* seed,
                            const PixCache& cache, double* moments, Counters* cnt,
                            cudaStream_t s) {
+  static bool attr_set = false;  // host-side, once per instantiation
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_blend_bwd<FAM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)BWD_SMEM);
+    cudaFuncSetAttribute(k_blend_bwd<FAM, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)BWD_SMEM);
+    cudaFuncSetAttribute(k_blend_bwd<FAM, true>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(k_blend_bwd<FAM, false>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
+    attr_set = true;
+  }
   if (count)
-    k_blend_bwd<FAM, true><<<n_tiles, TILE_PIX, 0, s>>>(records, pairs, ranges, cam, m, cutoff,
+    k_blend_bwd<FAM, true><<<n_tiles, TILE_PIX, BWD_SMEM, s>>>(records, bframe, pairs, ranges, cam, m, cutoff,
                                                          near_plane, bg[0], bg[1], bg[2], seed,
                                                          cache, moments, cnt);
   else
-    k_blend_bwd<FAM, false><<<n_tiles, TILE_PIX, 0, s>>>(records, pairs, ranges, cam, m, cutoff,
+    k_blend_bwd<FAM, false><<<n_tiles, TILE_PIX, BWD_SMEM, s>>>(records, bframe, pairs, ranges, cam, m, cutoff,
                                                           near_plane, bg[0], bg[1], bg[2], seed,
                                                           cache, moments, cnt);
 }
 
-void launch_blend_bwd(bool count, int n_tiles, const float4* records, const uint32_t* pairs,
+void launch_blend_bwd(bool count, int n_tiles, const float4* records, const float4* bframe,
+                      const uint32_t* pairs,
                       const int2* ranges, const CamDev& cam, const ModelDev& m, float cutoff,
                       double near_plane, const float* bg, const float* seed,
                       const PixCache& cache, double* moments, Counters* cnt, cudaStream_t s) {
   if (n_tiles == 0) return;
 #define NXS_BWD(F) \
-  launch_bwd_fam<F>(count, n_tiles, records, pairs, ranges, cam, m, cutoff, near_plane, bg, seed, \
+  launch_bwd_fam<F>(count, n_tiles, records, bframe, pairs, ranges, cam, m, cutoff, near_plane, bg, seed, \
                     cache, moments, cnt, s)
   switch (m.fam) {
     case FAM_EXP: NXS_BWD(FAM_EXP); break;

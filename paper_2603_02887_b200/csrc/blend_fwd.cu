@@ -4,8 +4,9 @@
 // _forward_sweep 147-217: live/sat_now/go, clamp, overdraw, finalize) for
 // the global depth order (reference chunk_size=1, SURVEY §8.0.6 Mode G).
 //
-// Per batch of 256 list entries the block stages the projected records
-// (8 threads per 128-B record, coalesced 16-B loads) in shared memory;
+// Per batch of 64 list entries the block stages the projected records
+// (8 threads per 128-B record, coalesced 16-B cp.async copies, double
+// buffered so the next batch loads while this one is composited);
 // every thread then walks the batch front to back for its pixel with the
 // carry in registers and leaves once saturated or capped; the block leaves
 // when all its pixels have.  Numerics (SURVEY R10 + §8.0.4):
@@ -19,6 +20,8 @@
 
 namespace nxs {
 
+constexpr int FWD_BATCH = 64;  // list entries per staged batch
+
 template <int FAM, bool COUNT>
 __global__ void __launch_bounds__(TILE_PIX)
     k_blend_fwd(const float4* __restrict__ records, const uint32_t* __restrict__ pairs,
@@ -27,8 +30,9 @@ __global__ void __launch_bounds__(TILE_PIX)
                 float* __restrict__ rgb,
                 int32_t* __restrict__ overdraw, float* __restrict__ residual, PixCache cache,
                 Counters* __restrict__ cnt) {
-  __shared__ float4 s_rec[TILE_PIX][REC_F4];
-  __shared__ uint32_t s_rank[TILE_PIX];
+  // two 64-entry record buffers: the next batch streams in (cp.async)
+  // while the current one is composited
+  __shared__ float4 s_rec[2][FWD_BATCH][REC_F4];
 
   const int tile = blockIdx.x;
   const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
@@ -51,32 +55,42 @@ __global__ void __launch_bounds__(TILE_PIX)
   bool done = !inside || max_splats <= 0;
 
   const int2 rg = ranges[tile];
-  for (int base = rg.x; base < rg.y; base += TILE_PIX) {
-    const int n = min(TILE_PIX, rg.y - base);
-    __syncthreads();
-    if (tid < n) s_rank[tid] = pairs[base + tid];
-    __syncthreads();
-    for (int k = tid; k < n * 8; k += TILE_PIX) {
+  auto stage = [&](int buf, int base) {
+    const int n = min(FWD_BATCH, rg.y - base);
+    for (int k = tid; k < n * REC_F4; k += TILE_PIX) {
       const int e = k >> 3, part = k & 7;
-      s_rec[e][part] = records[(size_t)s_rank[e] * REC_F4 + part];
+      cp_async16(&s_rec[buf][e][part], records + (size_t)pairs[base + e] * REC_F4 + part);
+    }
+    cp_async_commit();
+  };
+  if (rg.x < rg.y) stage(0, rg.x);
+  int buf = 0;
+  for (int base = rg.x; base < rg.y; base += FWD_BATCH, buf ^= 1) {
+    const int n = min(FWD_BATCH, rg.y - base);
+    if (base + FWD_BATCH < rg.y) {
+      stage(buf ^ 1, base + FWD_BATCH);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncthreads();
+    float4(*s_cur)[REC_F4] = s_rec[buf];
     if (!done) {
       for (int j = 0; j < n; ++j) {
         if (COUNT) ++ntest;
         TestOut t;
         bool ok;
-        if (__float_as_int(s_rec[j][3].w) & RF_GENERAL) {  // block-uniform branch
+        if (__float_as_int(s_cur[j][3].w) & RF_GENERAL) {  // block-uniform branch
           float gx, gy, gz;
-          ok = general_test(s_rec[j], cam, px, py, cutoff, near_plane, t, gx, gy, gz);
+          ok = general_test(s_cur[j], cam, px, py, cutoff, near_plane, t, gx, gy, gz);
         } else {
-          ok = ray_peak_test(s_rec[j][0], s_rec[j][1], s_rec[j][2], s_rec[j][3], pc, cutoff, t);
+          ok = ray_peak_test(s_cur[j][0], s_cur[j][1], s_cur[j][2], s_cur[j][3], pc, cutoff, t);
         }
         if (!ok) continue;
         const int idx = base + j;
         const float alpha = t.alpha;
         float E0, E1, E2;
-        emission(s_rec[j][4], s_rec[j][5], s_rec[j][6], pc, E0, E1, E2);
+        emission(s_cur[j][4], s_cur[j][5], s_cur[j][6], pc, E0, E1, E2);
         float fp;
         const float g = weight_g<FAM>(m, thi, tlo, P, fp);
         const float wr = alpha * g;
@@ -127,8 +141,10 @@ __global__ void __launch_bounds__(TILE_PIX)
         }
       }
     }
+    // all threads are past buffer `buf` before the next iteration refills it
     if (__syncthreads_count(!done) == 0) break;
   }
+  cp_async_wait<0>();
 
   if (COUNT) {
     __shared__ unsigned long long s_cnt[2];

@@ -88,6 +88,7 @@ struct ProjOut {
   unsigned long long* n_tiles;  // per rank tile count
   int4* rects;                  // per rank tile rectangle
   float4* records;              // per rank 8 x float4
+  float4* bframe;               // per rank 3 x float4: rows of B (backward only)
   unsigned long long* straddle; // counter
 };
 
@@ -269,6 +270,18 @@ __global__ void k_project(const float* __restrict__ centers, const float* __rest
   rec[6] = make_float4(shv[8], shv[9], shv[10], shv[11]);
   // conic: reserved for the exact-order mode (t-coefficients (A'b')·h, z_lo)
   if (!general) rec[7] = make_float4((float)Ab[0], (float)Ab[1], (float)Ab[2], (float)zmin);
+  // B maps the per-pixel peak offset e (conic: camera-frame diff'/b'_z;
+  // general: world-frame diff) to the Gaussian frame, u = Rᵀ diff = B e:
+  // conic B = b'_z Mᵀ, general B = Rᵀ (used by the backward only)
+  float4* bf = out.bframe + r * 3;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    if (general)
+      bf[k] = make_float4((float)R[0 + k], (float)R[3 + k], (float)R[6 + k], 0.f);
+    else
+      bf[k] = make_float4((float)(bp[2] * M[0 + k]), (float)(bp[2] * M[3 + k]),
+                          (float)(bp[2] * M[6 + k]), 0.f);
+  }
   out.rects[r] = rect;
   out.n_tiles[r] = ntile;
 }
@@ -310,10 +323,10 @@ void launch_depth_keys(const float* centers, int64_t P, const CamDev& cam,
 void launch_project(const float* centers, const float* scales, const float* quats,
                     const float* opacities, const float* sh, int C, int64_t P,
                     const uint32_t* order, const CamDev& cam, double cutoff, double near_plane,
-                    unsigned long long* n_tiles, int4* rects, float4* records,
+                    unsigned long long* n_tiles, int4* rects, float4* records, float4* bframe,
                     unsigned long long* straddle, cudaStream_t s) {
   if (P == 0) return;
-  ProjOut o{n_tiles, rects, records, straddle};
+  ProjOut o{n_tiles, rects, records, bframe, straddle};
   k_project<<<(unsigned)((P + 127) / 128), 128, 0, s>>>(centers, scales, quats, opacities, sh, C,
                                                         P, order, cam, cutoff, near_plane, o);
 }
