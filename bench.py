@@ -62,6 +62,8 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--first-phase", type=int, default=0,
+                   help="ranks binned in the first depth phase (0 = automatic)")
     return p.parse_args()
 
 
@@ -207,7 +209,7 @@ def main():
              for v in range(n_views)}
     bg = np.zeros(3)
     grads = GradBuffer(len(arrs), arrs.sh.shape[2], device="cuda")
-    rv = device_view_renderer(dev, model, bg, cams, seeds)
+    rv = device_view_renderer(dev, model, bg, cams, seeds, first_phase_ranks=a.first_phase)
     step = DataParallelStep(n_views, rank, world, grads, rv)
     my_views = step.views()
 
@@ -248,11 +250,13 @@ def main():
                 phase_tot[k] = phase_tot.get(k, 0.0) + x
     nprof = max(3, min(a.steps, 10))
     phase = {k: x / nprof / max(1, len(my_views)) for k, x in phase_tot.items()}
+    n_depth_phases = phase.pop("n_depth_phases", None)
 
     # ---- event counts (instrumented run, not timed) for the blend roofline
     from paper_2603_02887_b200 import backward_device, forward_device
     cview = _native.View()
-    forward_device(cview, dev, cams[my_views[0]], model, bg, chunk_size=1, count_events=True)
+    forward_device(cview, dev, cams[my_views[0]], model, bg, chunk_size=1, count_events=True,
+                   first_phase_ranks=a.first_phase)
     backward_device(cview, dev, seeds[my_views[0]])
     st = cview.stats()
     cview.close()
@@ -294,6 +298,7 @@ def main():
                 "l2": "inputs larger than L2 (records 128 MB + pairs + 192 MB moments per view)",
             },
             "phase_ms": {k: round(v, 4) for k, v in phase.items()},
+            "depth_phases": n_depth_phases,
             "events": {k: st[k] for k in ("n_pairs", "n_tests_fwd", "n_composited",
                                            "n_tests_bwd", "n_entries_bwd")},
             "roofline": roof,
@@ -330,14 +335,14 @@ def roofline(a, model, phase, st):
     # pair sort: 2 LSD passes over (u32 tile key, u32 rank) pairs, read + write
     sort_bytes = npairs * 8 * 2 * 2
     proj_bytes = P * (92 + 8 + 128 + 16 + 8)  # params + order in; record + rect + count out
-    shares = {"blend (fwd+bwd)": blend_ms, "pair_sort": phase.get("pair_sort", 0.0),
+    shares = {"blend (fwd+bwd)": blend_ms, "binning": phase.get("binning", 0.0),
               "depth_sort": phase.get("depth_sort", 0.0), "project": phase.get("project", 0.0)}
     dom = max(shares, key=shares.get)
     total = sum(phase.values())
     if dom == "blend (fwd+bwd)":
         r = dict(blend, kernel=dom)
-    elif dom == "pair_sort":
-        ach = sort_bytes / (phase["pair_sort"] / 1e3) / 1e9
+    elif dom == "binning":
+        ach = sort_bytes / (phase["binning"] / 1e3) / 1e9
         r = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "kernel": dom}
     elif dom == "project":
         ach = proj_bytes / (phase["project"] / 1e3) / 1e9

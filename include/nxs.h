@@ -66,6 +66,7 @@ extern "C" {
 
 /* opts.flags */
 #define NXS_FLAG_COUNT_EVENTS 1    /* count tests/composites (instrumented run) */
+#define NXS_FLAG_FULL_BINNING 2    /* bin every rank in one phase (no progressive binning) */
 
 /* ordering: opts.chunk_size (reference render(..., chunk_size=)) */
 #define NXS_CHUNK_EXACT 0          /* chunk_size=None: exact per-pixel depth order */
@@ -93,6 +94,8 @@ typedef struct {
     double near_plane;       /* default 1e-4 */
     int32_t chunk_size;      /* NXS_CHUNK_EXACT (None) or >= 1 */
     int32_t flags;           /* NXS_FLAG_* */
+    int64_t first_phase_ranks; /* progressive binning: ranks in the first depth
+                                  phase (0 = automatic); later phases grow x8 */
 } nxs_opts;
 
 /* SceneArrays (reference render.py:44-52), device float32, row-major:
@@ -126,9 +129,11 @@ typedef struct nxs_view nxs_view;
 /* device-timed phases of the last forward + backward (CUDA events on the
  * call's stream), order of nxs_view_timings' output */
 #define NXS_PHASES 10
-/* 0 depth sort (K0 + radix sort), 1 projection (K1), 2 tile-count scan
- * (+ host sync), 3 pair emission (K2), 4 pair sort by tile, 5 tile ranges,
- * 6 forward blend (K3), 7 moment clear, 8 backward blend (K4), 9 chain (K5) */
+/* 0 depth sort (K0 + radix sort), 1 projection (K1), 2 tile binning over
+ * all depth phases (active-tile counts, scan + host sync, pair emission,
+ * sort by tile, ranges), 3 forward blend over all phases (K3), 4 number of
+ * depth phases run (a count, not ms), 5-6 unused, 7 moment clear,
+ * 8 backward blend (K4), 9 chain (K5) */
 
 int nxs_abi_version(void);
 const char* nxs_error_string(int code);
@@ -171,8 +176,9 @@ int nxs_depth_order(nxs_view* view, int32_t* order, void* stream);
 
 /* Binning of the last forward, for the bit-exact checks against the C
  * restatement (oracle/binning_oracle.c): tile rectangle per rank
- * (P x int32[4] = tx0,ty0,tx1,ty1; empty = -1), tile ranges (n_tiles x
- * int32[2]) and the sorted pair values (n_pairs ranks). */
+ * (P x int32[4] = tx0,ty0,tx1,ty1; empty = -1), and the FIRST depth
+ * phase's tile ranges (n_tiles x int32[2]) and sorted pair values; with
+ * NXS_FLAG_FULL_BINNING that phase holds every rank (n_pairs ranks). */
 int nxs_binning_export(nxs_view* view, int32_t* rects, int32_t* ranges,
                        int32_t* pair_ranks, void* stream);
 

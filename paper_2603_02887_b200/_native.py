@@ -48,6 +48,7 @@ NXS_ERR_GEOMETRY = -6
 NXS_ERR_UNSUPPORTED = -2
 NXS_ERR_INVALID = -1
 NXS_FLAG_COUNT_EVENTS = 1
+NXS_FLAG_FULL_BINNING = 2
 
 
 class NativeLibraryError(ImportError):
@@ -83,6 +84,7 @@ class Opts(C.Structure):
         ("near_plane", C.c_double),
         ("chunk_size", C.c_int32),
         ("flags", C.c_int32),
+        ("first_phase_ranks", C.c_int64),
     ]
 
 
@@ -169,9 +171,10 @@ def make_model(variant_id: int, param: float) -> Model:
     return Model(int(variant_id), float(param))
 
 
-def make_opts(max_splats, alpha_cutoff, near, chunk_size, flags=0) -> Opts:
+def make_opts(max_splats, alpha_cutoff, near, chunk_size, flags=0, first_phase_ranks=0) -> Opts:
     cs = 0 if chunk_size is None else int(chunk_size)
-    return Opts(int(max_splats), float(alpha_cutoff), float(near), cs, int(flags))
+    return Opts(int(max_splats), float(alpha_cutoff), float(near), cs, int(flags),
+                int(first_phase_ranks))
 
 
 def _ptr(t) -> int | None:
@@ -244,14 +247,14 @@ class View:
         _check(self._h.nxs_view_stats(self._p, C.byref(st)))
         return st.as_dict()
 
-    PHASES = ("depth_sort", "project", "scan_sync", "emit_pairs", "pair_sort", "tile_ranges",
-              "blend_fwd", "moment_clear", "blend_bwd", "chain")
+    PHASES = ("depth_sort", "project", "binning", "blend_fwd", "n_depth_phases", "_5", "_6",
+              "moment_clear", "blend_bwd", "chain")
 
     def timings(self) -> dict:
         """Device milliseconds per phase of the last forward/backward."""
         arr = (C.c_float * len(self.PHASES))()
         _check(self._h.nxs_view_timings(self._p, arr, len(self.PHASES)))
-        return {n: float(arr[i]) for i, n in enumerate(self.PHASES)}
+        return {n: float(arr[i]) for i, n in enumerate(self.PHASES) if not n.startswith("_")}
 
     def nbytes(self) -> int:
         return int(self._h.nxs_view_bytes(self._p))

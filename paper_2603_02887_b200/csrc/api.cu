@@ -9,6 +9,7 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -23,14 +24,15 @@ void launch_depth_keys(const float*, int64_t, const CamDev&, unsigned long long*
 void launch_project(const float*, const float*, const float*, const float*, const float*, int,
                     int64_t, const uint32_t*, const CamDev&, double, double, unsigned long long*,
                     int4*, float4*, float4*, unsigned long long*, cudaStream_t);
-void launch_emit_pairs(const int4*, const unsigned long long*, int64_t, int, uint32_t*, uint32_t*,
-                       cudaStream_t);
+void launch_count_active(const int4*, int64_t, int64_t, int, const uint8_t*, unsigned long long*,
+                         cudaStream_t);
+void launch_emit_pairs(const int4*, const unsigned long long*, int64_t, int64_t, int,
+                       const uint8_t*, uint32_t*, uint32_t*, cudaStream_t);
 void launch_tile_ranges(const uint32_t*, int64_t, int2*, cudaStream_t);
-void launch_blend_fwd(bool, int, const float4*, const uint32_t*, const int2*, const CamDev&,
-                      const ModelDev&, int, float, double, const float*, float*, int32_t*,
-                      float*, const PixCache&, Counters*, cudaStream_t);
-void launch_blend_bwd(bool, int, const float4*, const float4*, const uint32_t*, const int2*,
-                      const CamDev&, const ModelDev&, float, double, const float*, const float*,
+void launch_blend_fwd(bool, int, const FwdArgs&, const CamDev&, const ModelDev&, const PixCache&,
+                      const PixResume&, Counters*, cudaStream_t);
+void launch_blend_bwd(bool, int, const float4*, const float4*, const PhaseLists&, const CamDev&,
+                      const ModelDev&, float, double, const float*, const float*,
                       const PixCache&, double*, Counters*, cudaStream_t);
 void launch_chain(const float*, const float*, int, int64_t, const uint32_t*, const double*,
                   float*, float*, float*, float*, float*, cudaStream_t);
@@ -96,14 +98,19 @@ int bits_for(uint32_t n) {
 struct nxs_view {
   // per Gaussian
   Buf dkeys_in, dkeys_out, idx_in, idx_out, records, bframe, rects, ntiles, offsets, moments;
-  // per pair
-  Buf pk_in, pk_out, pv_in, pv_out;
-  // per tile / pixel
-  Buf ranges, c_last, c_sat, c_tk, c_thi, c_tlo, c_P, c_ck, c_Pck, c_ek, c_th0;
+  // per pair: sort scratch, and the sorted ranks of each depth phase
+  Buf pk_in, pk_out, pv_in, pv_ph[MAX_PHASES];
+  // per tile: phase ranges and virtual offsets, activity
+  Buf ranges_ph[MAX_PHASES], cum_ph[MAX_PHASES + 1], active;
+  // per pixel: replay cache and the forward carry between phases
+  Buf c_last, c_sat, c_tk, c_thi, c_tlo, c_P, c_ck, c_Pck, c_ek, c_th0;
+  Buf r_rad, r_trem, r_count, r_sea, r_sa;
   Buf temp, dev_small;  // CUB temp; counters
   unsigned long long* host_small = nullptr;  // pinned
   // phase events: see NXS_PHASES in include/nxs.h
   cudaEvent_t ev[NXS_PHASES + 2] = {};
+  // per depth phase: [0] start, [1] after sort+ranges, [2] after the forward kernel
+  cudaEvent_t evp[MAX_PHASES][3] = {};
   bool ev_ok = false;
   bool ev_fwd = false, ev_bwd = false;
   // state of the last forward
@@ -114,27 +121,39 @@ struct nxs_view {
   float bg[3] = {0, 0, 0};
   int64_t P = 0;
   int32_t C = 1;
-  int64_t n_pairs = 0;
+  int64_t n_pairs = 0;  // pairs emitted over all phases
+  int64_t ph_pairs[MAX_PHASES] = {0, 0, 0, 0};
+  int n_phases = 0;
   int n_tiles = 0;
   const float* scene_centers = nullptr;
   nxs_stats stats{};
 
-  ~nxs_view() {
-    Buf* all[] = {&dkeys_in, &dkeys_out, &idx_in, &idx_out, &records, &bframe, &rects, &ntiles, &offsets,
-                  &moments, &pk_in, &pk_out, &pv_in, &pv_out, &ranges, &c_last, &c_sat, &c_tk,
-                  &c_thi, &c_tlo, &c_P, &c_ck, &c_Pck, &c_ek, &c_th0, &temp, &dev_small};
-    for (Buf* b : all) b->release();
-    if (host_small) cudaFreeHost(host_small);
-    if (ev_ok)
-      for (auto& e : ev) cudaEventDestroy(e);
+  template <class F>
+  void for_each_buf(F f) {
+    Buf* all[] = {&dkeys_in, &dkeys_out, &idx_in,  &idx_out, &records, &bframe, &rects,
+                  &ntiles,   &offsets,   &moments, &pk_in,   &pk_out,  &pv_in,  &active,
+                  &c_last,   &c_sat,     &c_tk,    &c_thi,   &c_tlo,   &c_P,    &c_ck,
+                  &c_Pck,    &c_ek,      &c_th0,   &r_rad,   &r_trem,  &r_count, &r_sea,
+                  &r_sa,     &temp,      &dev_small};
+    for (Buf* b : all) f(*b);
+    for (int p = 0; p < MAX_PHASES; ++p) {
+      f(pv_ph[p]);
+      f(ranges_ph[p]);
+    }
+    for (int p = 0; p <= MAX_PHASES; ++p) f(cum_ph[p]);
   }
-  int64_t bytes() const {
-    const Buf* all[] = {&dkeys_in, &dkeys_out, &idx_in, &idx_out, &records, &bframe, &rects, &ntiles,
-                        &offsets, &moments, &pk_in, &pk_out, &pv_in, &pv_out, &ranges, &c_last,
-                        &c_sat, &c_tk, &c_thi, &c_tlo, &c_P, &c_ck, &c_Pck, &c_ek, &c_th0,
-                        &temp, &dev_small};
+  ~nxs_view() {
+    for_each_buf([](Buf& b) { b.release(); });
+    if (host_small) cudaFreeHost(host_small);
+    if (ev_ok) {
+      for (auto& e : ev) cudaEventDestroy(e);
+      for (auto& row : evp)
+        for (auto& e : row) cudaEventDestroy(e);
+    }
+  }
+  int64_t bytes() {
     int64_t s = 0;
-    for (const Buf* b : all) s += (int64_t)b->cap;
+    for_each_buf([&](Buf& b) { s += (int64_t)b.cap; });
     return s;
   }
   PixCache cache() const {
@@ -142,6 +161,10 @@ struct nxs_view {
                     c_thi.as<float>(), c_tlo.as<float>(), c_P.as<float>(),
                     c_ck.as<int32_t>(), c_Pck.as<float>(), c_ek.as<float>(),
                     c_th0.as<float>()};
+  }
+  PixResume resume() const {
+    return PixResume{r_rad.as<float>(), r_trem.as<float>(), r_count.as<int32_t>(),
+                     r_sea.as<float>(), r_sa.as<float>()};
   }
 };
 
@@ -244,6 +267,8 @@ int nxs_view_create(nxs_view** out) {
   }
   v->ev_ok = true;
   for (auto& e : v->ev) v->ev_ok = v->ev_ok && cudaEventCreate(&e) == cudaSuccess;
+  for (auto& row : v->evp)
+    for (auto& e : row) v->ev_ok = v->ev_ok && cudaEventCreate(&e) == cudaSuccess;
   *out = v;
   return NXS_OK;
 }
@@ -259,7 +284,9 @@ int nxs_view_stats(const nxs_view* view, nxs_stats* out) {
   return NXS_OK;
 }
 
-int64_t nxs_view_bytes(const nxs_view* view) { return view ? view->bytes() : 0; }
+int64_t nxs_view_bytes(const nxs_view* view) {
+  return view ? const_cast<nxs_view*>(view)->bytes() : 0;
+}
 
 int nxs_forward(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
                 const nxs_model* model, const nxs_opts* opts, const float background[3],
@@ -292,6 +319,7 @@ int nxs_forward(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
   v->stats = nxs_stats{};
   v->stats.n_gaussians = P;
   v->stats.n_tiles = n_tiles;
+  const bool count = (opts->flags & NXS_FLAG_COUNT_EVENTS) != 0;
 
   // ---- workspace
   NXS_CUDA(ensure_n<unsigned long long>(v->dkeys_in, P));
@@ -303,7 +331,7 @@ int nxs_forward(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
   NXS_CUDA(ensure_n<int4>(v->rects, P));
   NXS_CUDA(ensure_n<unsigned long long>(v->ntiles, P));
   NXS_CUDA(ensure_n<unsigned long long>(v->offsets, P));
-  NXS_CUDA(ensure_n<int2>(v->ranges, n_tiles));
+  NXS_CUDA(ensure_n<uint8_t>(v->active, n_tiles));
   NXS_CUDA(ensure_n<int32_t>(v->c_last, npix));
   NXS_CUDA(ensure_n<uint8_t>(v->c_sat, npix));
   NXS_CUDA(ensure_n<float>(v->c_tk, npix));
@@ -315,13 +343,39 @@ int nxs_forward(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
   NXS_CUDA(ensure_n<float>(v->c_ek, npix * 3));
   NXS_CUDA(ensure_n<float>(v->c_th0, npix * 3));
   NXS_CUDA(v->dev_small.ensure(8 * sizeof(unsigned long long)));
+  // dsmall: [0] straddle count, [1..4] event counters, [5] active tiles (u32)
   unsigned long long* dsmall = v->dev_small.as<unsigned long long>();
-  Counters* cnt = reinterpret_cast<Counters*>(dsmall + 1);  // [0] straddle, [1..4] counters
+  Counters* cnt = reinterpret_cast<Counters*>(dsmall + 1);
+  unsigned int* n_active = reinterpret_cast<unsigned int*>(dsmall + 5);
   NXS_CUDA(cudaMemsetAsync(dsmall, 0, 8 * sizeof(unsigned long long), s));
+  NXS_CUDA(cudaMemsetAsync(v->active.p, 1, (size_t)n_tiles, s));
 
-  size_t tmp_sort = 0, tmp_scan = 0;
+  // ---- depth phases [R_p, R_{p+1}): R_1 = first phase, then x8
+  int64_t R[MAX_PHASES + 1];
+  int n_ph = 0;
+  {
+    int64_t r1;
+    if (opts->flags & NXS_FLAG_FULL_BINNING)
+      r1 = P;
+    else if (opts->first_phase_ranks > 0)
+      r1 = opts->first_phase_ranks;
+    else  // measured at C3: saturating models finish every tile within P/32
+          // ranks; exp never saturates and runs to the 128 cap
+      r1 = (md.fam == FAM_EXP) ? P / 4 : P / 32;
+    r1 = std::max<int64_t>(r1, 4096);
+    R[0] = 0;
+    int64_t r = std::min(P, r1);
+    while (true) {
+      R[++n_ph] = r;
+      if (r >= P || n_ph == MAX_PHASES - 1) break;
+      r = std::min(P, r * 8);
+    }
+    if (R[n_ph] < P) R[++n_ph] = P;
+  }
+
   mark(v, 0, s);
   if (P > 0) {
+    size_t tmp_sort = 0, tmp_scan = 0;
     NXS_CUDA(cub::DeviceRadixSort::SortPairs(
         nullptr, tmp_sort, v->dkeys_in.as<unsigned long long>(),
         v->dkeys_out.as<unsigned long long>(), v->idx_in.as<uint32_t>(),
@@ -329,8 +383,7 @@ int nxs_forward(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
     NXS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_scan,
                                            v->ntiles.as<unsigned long long>(),
                                            v->offsets.as<unsigned long long>(), (int)P, s));
-    NXS_CUDA(v->temp.ensure(tmp_sort > tmp_scan ? tmp_sort : tmp_scan));
-
+    NXS_CUDA(v->temp.ensure(std::max(tmp_sort, tmp_scan)));
     // ---- K0 + depth sort
     launch_depth_keys(scene->centers, P, cam, v->dkeys_in.as<unsigned long long>(),
                       v->idx_in.as<uint32_t>(), s);
@@ -339,82 +392,120 @@ int nxs_forward(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
     NXS_CUDA(cub::DeviceRadixSort::SortPairs(
         v->temp.p, tb, v->dkeys_in.as<unsigned long long>(), v->dkeys_out.as<unsigned long long>(),
         v->idx_in.as<uint32_t>(), v->idx_out.as<uint32_t>(), (int)P, 0, 64, s));
-    mark(v, 1, s);
-    // ---- K1 projection
+  }
+  mark(v, 1, s);
+  if (P > 0) {
+    // ---- K1 projection (all ranks: records, tile rectangles)
     launch_project(scene->centers, scene->scales, scene->quats, scene->opacities, scene->sh, C, P,
                    v->idx_out.as<uint32_t>(), cam, opts->alpha_cutoff, opts->near_plane,
                    v->ntiles.as<unsigned long long>(), v->rects.as<int4>(),
                    v->records.as<float4>(), v->bframe.as<float4>(), dsmall, s);
     NXS_LAUNCHED("project");
-    mark(v, 2, s);
-    tb = v->temp.cap;
-    NXS_CUDA(cub::DeviceScan::ExclusiveSum(v->temp.p, tb, v->ntiles.as<unsigned long long>(),
-                                           v->offsets.as<unsigned long long>(), (int)P, s));
-    // total pairs = offsets[P-1] + ntiles[P-1]; plus the straddle counter
-    NXS_CUDA(cudaMemcpyAsync(v->host_small, v->offsets.as<unsigned long long>() + (P - 1),
-                             sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-    NXS_CUDA(cudaMemcpyAsync(v->host_small + 1, v->ntiles.as<unsigned long long>() + (P - 1),
-                             sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  }
+  mark(v, 2, s);
+
+  const float bgf[3] = {background[0], background[1], background[2]};
+  NXS_CUDA(ensure_n<int32_t>(v->cum_ph[0], n_tiles));
+  NXS_CUDA(cudaMemsetAsync(v->cum_ph[0].p, 0, (size_t)n_tiles * 4, s));
+  const int tbits = bits_for((uint32_t)std::max(n_tiles, 2));
+  int64_t total_pairs = 0;
+  int ph_done = 0;
+  for (int ph = 0; ph < n_ph; ++ph) {
+    const int64_t r0 = R[ph], r1 = R[ph + 1], nr = r1 - r0;
+    if (v->ev_ok) cudaEventRecord(v->evp[ph][0], s);
+    // ---- K2a counts over active tiles, scan, one host sync for the pair count
+    if (nr > 0) {
+      launch_count_active(v->rects.as<int4>(), r0, r1, cam.tiles_x, v->active.as<uint8_t>(),
+                          v->ntiles.as<unsigned long long>(), s);
+      NXS_LAUNCHED("count_active");
+      size_t tb = v->temp.cap;
+      NXS_CUDA(cub::DeviceScan::ExclusiveSum(v->temp.p, tb, v->ntiles.as<unsigned long long>(),
+                                             v->offsets.as<unsigned long long>(), (int)nr, s));
+      NXS_CUDA(cudaMemcpyAsync(v->host_small, v->offsets.as<unsigned long long>() + (nr - 1),
+                               sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+      NXS_CUDA(cudaMemcpyAsync(v->host_small + 1, v->ntiles.as<unsigned long long>() + (nr - 1),
+                               sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    } else {
+      NXS_CUDA(cudaMemsetAsync(v->host_small, 0, 2 * sizeof(unsigned long long), s));
+    }
     NXS_CUDA(cudaMemcpyAsync(v->host_small + 2, dsmall, sizeof(unsigned long long),
                              cudaMemcpyDeviceToHost, s));
+    NXS_CUDA(cudaMemcpyAsync(v->host_small + 3, n_active, sizeof(unsigned int),
+                             cudaMemcpyDeviceToHost, s));
     NXS_CUDA(cudaStreamSynchronize(s));
-  } else {
-    v->host_small[0] = v->host_small[1] = v->host_small[2] = 0;
-    mark(v, 1, s);
-    mark(v, 2, s);
-  }
-  mark(v, 3, s);
-  const unsigned long long n_pairs = v->host_small[0] + v->host_small[1];
-  v->stats.n_straddling = (int64_t)v->host_small[2];
-  v->stats.n_pairs = (int64_t)n_pairs;
-  if (n_pairs >= (1ull << 31)) return fail(NXS_ERR_NOMEM, "more than 2^31 tile pairs");
+    if (ph == 0) mark(v, 3, s);
+    const unsigned long long n_pairs = v->host_small[0] + v->host_small[1];
+    v->stats.n_straddling = (int64_t)v->host_small[2];
+    if (ph > 0 && (unsigned)v->host_small[3] == 0) break;  // every tile finished
+    if (n_pairs >= (1ull << 31)) return fail(NXS_ERR_NOMEM, "more than 2^31 tile pairs");
+    total_pairs += (int64_t)n_pairs;
+    v->ph_pairs[ph] = (int64_t)n_pairs;
 
-  NXS_CUDA(cudaMemsetAsync(v->ranges.p, 0, (size_t)n_tiles * sizeof(int2), s));
-  if (n_pairs > 0) {
-    NXS_CUDA(ensure_n<uint32_t>(v->pk_in, (int64_t)n_pairs));
-    NXS_CUDA(ensure_n<uint32_t>(v->pk_out, (int64_t)n_pairs));
-    NXS_CUDA(ensure_n<uint32_t>(v->pv_in, (int64_t)n_pairs));
-    NXS_CUDA(ensure_n<uint32_t>(v->pv_out, (int64_t)n_pairs));
-    const int tbits = bits_for((uint32_t)n_tiles);
-    size_t tmp_pairs = 0;
-    NXS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_pairs, v->pk_in.as<uint32_t>(),
-                                             v->pk_out.as<uint32_t>(), v->pv_in.as<uint32_t>(),
-                                             v->pv_out.as<uint32_t>(), (int)n_pairs, 0, tbits, s));
-    NXS_CUDA(v->temp.ensure(tmp_pairs));
-    // ---- K2 pairs, sort by tile, ranges
-    launch_emit_pairs(v->rects.as<int4>(), v->offsets.as<unsigned long long>(), P, cam.tiles_x,
-                      v->pk_in.as<uint32_t>(), v->pv_in.as<uint32_t>(), s);
-    NXS_LAUNCHED("emit_pairs");
-    mark(v, 4, s);
-    size_t tb = v->temp.cap;
-    NXS_CUDA(cub::DeviceRadixSort::SortPairs(v->temp.p, tb, v->pk_in.as<uint32_t>(),
-                                             v->pk_out.as<uint32_t>(), v->pv_in.as<uint32_t>(),
-                                             v->pv_out.as<uint32_t>(), (int)n_pairs, 0, tbits, s));
-    mark(v, 5, s);
-    launch_tile_ranges(v->pk_out.as<uint32_t>(), (int64_t)n_pairs, v->ranges.as<int2>(), s);
-    NXS_LAUNCHED("tile_ranges");
-  } else {
-    mark(v, 4, s);
-    mark(v, 5, s);
+    NXS_CUDA(ensure_n<int2>(v->ranges_ph[ph], n_tiles));
+    NXS_CUDA(ensure_n<int32_t>(v->cum_ph[ph + 1], n_tiles));
+    NXS_CUDA(ensure_n<uint32_t>(v->pv_ph[ph], std::max<int64_t>(1, (int64_t)n_pairs)));
+    NXS_CUDA(cudaMemsetAsync(v->ranges_ph[ph].p, 0, (size_t)n_tiles * sizeof(int2), s));
+    if (n_pairs > 0) {
+      NXS_CUDA(ensure_n<uint32_t>(v->pk_in, (int64_t)n_pairs));
+      NXS_CUDA(ensure_n<uint32_t>(v->pk_out, (int64_t)n_pairs));
+      NXS_CUDA(ensure_n<uint32_t>(v->pv_in, (int64_t)n_pairs));
+      size_t tmp_pairs = 0;
+      NXS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_pairs, v->pk_in.as<uint32_t>(),
+                                               v->pk_out.as<uint32_t>(), v->pv_in.as<uint32_t>(),
+                                               v->pv_ph[ph].as<uint32_t>(), (int)n_pairs, 0,
+                                               tbits, s));
+      NXS_CUDA(v->temp.ensure(tmp_pairs));
+      // ---- K2b pairs (rank order), stable sort by tile, ranges
+      launch_emit_pairs(v->rects.as<int4>(), v->offsets.as<unsigned long long>(), r0, r1,
+                        cam.tiles_x, v->active.as<uint8_t>(), v->pk_in.as<uint32_t>(),
+                        v->pv_in.as<uint32_t>(), s);
+      NXS_LAUNCHED("emit_pairs");
+      if (ph == 0) mark(v, 4, s);
+      size_t tb = v->temp.cap;
+      NXS_CUDA(cub::DeviceRadixSort::SortPairs(v->temp.p, tb, v->pk_in.as<uint32_t>(),
+                                               v->pk_out.as<uint32_t>(), v->pv_in.as<uint32_t>(),
+                                               v->pv_ph[ph].as<uint32_t>(), (int)n_pairs, 0,
+                                               tbits, s));
+      if (ph == 0) mark(v, 5, s);
+      launch_tile_ranges(v->pk_out.as<uint32_t>(), (int64_t)n_pairs,
+                         v->ranges_ph[ph].as<int2>(), s);
+      NXS_LAUNCHED("tile_ranges");
+    } else if (ph == 0) {
+      mark(v, 4, s);
+      mark(v, 5, s);
+    }
+    if (ph == 0) mark(v, 6, s);
+    if (v->ev_ok) cudaEventRecord(v->evp[ph][1], s);
+    if (ph == 1 || (ph == 0 && n_ph > 1)) {
+      // forward carry between phases (allocated only when a second phase exists)
+      NXS_CUDA(ensure_n<float>(v->r_rad, npix * 3));
+      NXS_CUDA(ensure_n<float>(v->r_trem, npix));
+      NXS_CUDA(ensure_n<int32_t>(v->r_count, npix));
+      NXS_CUDA(ensure_n<float>(v->r_sea, npix * 3));
+      NXS_CUDA(ensure_n<float>(v->r_sa, npix));
+    }
+    // ---- K3 forward blend of this phase (tiles still active)
+    NXS_CUDA(cudaMemsetAsync(n_active, 0, sizeof(unsigned int), s));
+    FwdArgs fa{v->records.as<float4>(), v->pv_ph[ph].as<uint32_t>(), v->ranges_ph[ph].as<int2>(),
+               v->cum_ph[ph].as<int32_t>(), v->cum_ph[ph + 1].as<int32_t>(),
+               v->active.as<uint8_t>(), n_active, ph > 0, ph + 1 < n_ph, opts->max_splats,
+               (float)opts->alpha_cutoff, opts->near_plane, {bgf[0], bgf[1], bgf[2]},
+               rgb, overdraw, residual};
+    launch_blend_fwd(count, n_tiles, fa, cam, md, v->cache(), v->resume(), cnt, s);
+    NXS_LAUNCHED("blend_fwd");
+    if (v->ev_ok) cudaEventRecord(v->evp[ph][2], s);
+    ph_done = ph + 1;
   }
-  mark(v, 6, s);
-
-  // ---- K3 forward blend
-  const bool count = (opts->flags & NXS_FLAG_COUNT_EVENTS) != 0;
-  const float bgf[3] = {background[0], background[1], background[2]};
-  launch_blend_fwd(count, n_tiles, v->records.as<float4>(), v->pv_out.as<uint32_t>(),
-                   v->ranges.as<int2>(), cam, md, opts->max_splats, (float)opts->alpha_cutoff,
-                   opts->near_plane, bgf, rgb, overdraw, residual, v->cache(), cnt, s);
-  NXS_LAUNCHED("blend_fwd");
   mark(v, 7, s);
   v->ev_fwd = true;
   v->ev_bwd = false;
+  v->stats.n_pairs = total_pairs;
   if (count) {
-    NXS_CUDA(cudaMemcpyAsync(v->host_small + 3, cnt, 2 * sizeof(unsigned long long),
+    NXS_CUDA(cudaMemcpyAsync(v->host_small + 4, cnt, 2 * sizeof(unsigned long long),
                              cudaMemcpyDeviceToHost, s));
     NXS_CUDA(cudaStreamSynchronize(s));
-    v->stats.n_tests_fwd = (int64_t)v->host_small[3];
-    v->stats.n_composited = (int64_t)v->host_small[4];
+    v->stats.n_tests_fwd = (int64_t)v->host_small[4];
+    v->stats.n_composited = (int64_t)v->host_small[5];
   }
 
   v->have_fwd = true;
@@ -424,7 +515,8 @@ int nxs_forward(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
   for (int i = 0; i < 3; ++i) v->bg[i] = bgf[i];
   v->P = P;
   v->C = C;
-  v->n_pairs = (int64_t)n_pairs;
+  v->n_pairs = total_pairs;
+  v->n_phases = ph_done;
   v->n_tiles = n_tiles;
   v->scene_centers = scene->centers;
   return NXS_OK;
@@ -448,10 +540,16 @@ int nxs_backward(nxs_view* v, const nxs_scene* scene, const float* seed, float* 
   const bool count = (v->opts.flags & NXS_FLAG_COUNT_EVENTS) != 0;
   unsigned long long* dsmall = v->dev_small.as<unsigned long long>();
   Counters* cnt = reinterpret_cast<Counters*>(dsmall + 1);
-  launch_blend_bwd(count, v->n_tiles, v->records.as<float4>(), v->bframe.as<float4>(),
-                   v->pv_out.as<uint32_t>(),
-                   v->ranges.as<int2>(), v->cam, v->model, (float)v->opts.alpha_cutoff,
-                   v->opts.near_plane, v->bg, seed, v->cache(), v->moments.as<double>(), cnt, s);
+  PhaseLists lists{};
+  lists.n = v->n_phases;
+  for (int p = 0; p < v->n_phases; ++p) {
+    lists.pairs[p] = v->pv_ph[p].as<uint32_t>();
+    lists.ranges[p] = v->ranges_ph[p].as<int2>();
+    lists.cum[p] = v->cum_ph[p].as<int32_t>();
+  }
+  launch_blend_bwd(count, v->n_tiles, v->records.as<float4>(), v->bframe.as<float4>(), lists,
+                   v->cam, v->model, (float)v->opts.alpha_cutoff, v->opts.near_plane, v->bg, seed,
+                   v->cache(), v->moments.as<double>(), cnt, s);
   NXS_LAUNCHED("blend_bwd");
   mark(v, 10, s);
   launch_chain(scene->scales, scene->quats, v->C, P, v->idx_out.as<uint32_t>(),
@@ -472,14 +570,30 @@ int nxs_backward(nxs_view* v, const nxs_scene* scene, const float* seed, float* 
 int nxs_view_timings(nxs_view* v, float* ms, int n) {
   if (!v || !ms) return fail(NXS_ERR_INVALID, "null argument");
   if (!v->ev_ok) return fail(NXS_ERR_CUDA, "timing events unavailable");
-  for (int i = 0; i < n && i < NXS_PHASES; ++i) ms[i] = 0.f;
-  const int a[NXS_PHASES] = {0, 1, 2, 3, 4, 5, 6, 8, 9, 10};
-  for (int i = 0; i < n && i < NXS_PHASES; ++i) {
-    const bool fwd = i < 7;
-    if (fwd ? !v->ev_fwd : !v->ev_bwd) continue;
-    NXS_CUDA(cudaEventSynchronize(v->ev[a[i] + 1]));
-    NXS_CUDA(cudaEventElapsedTime(&ms[i], v->ev[a[i]], v->ev[a[i] + 1]));
+  float t[NXS_PHASES] = {0};
+  auto el = [&](cudaEvent_t a, cudaEvent_t b, float& out) -> int {
+    NXS_CUDA(cudaEventSynchronize(b));
+    float x = 0.f;
+    NXS_CUDA(cudaEventElapsedTime(&x, a, b));
+    out += x;
+    return NXS_OK;
+  };
+  int rc;
+  if (v->ev_fwd) {
+    if ((rc = el(v->ev[0], v->ev[1], t[0]))) return rc;  // depth keys + sort
+    if ((rc = el(v->ev[1], v->ev[2], t[1]))) return rc;  // projection
+    for (int p = 0; p < v->n_phases; ++p) {
+      if ((rc = el(v->evp[p][0], v->evp[p][1], t[2]))) return rc;  // count+scan+sync+emit+sort+ranges
+      if ((rc = el(v->evp[p][1], v->evp[p][2], t[3]))) return rc;  // forward blend (+carry)
+    }
+    t[4] = (float)v->n_phases;
   }
+  if (v->ev_bwd) {
+    if ((rc = el(v->ev[8], v->ev[9], t[7]))) return rc;
+    if ((rc = el(v->ev[9], v->ev[10], t[8]))) return rc;
+    if ((rc = el(v->ev[10], v->ev[11], t[9]))) return rc;
+  }
+  for (int i = 0; i < n && i < NXS_PHASES; ++i) ms[i] = t[i];
   return NXS_OK;
 }
 
@@ -513,11 +627,12 @@ int nxs_binning_export(nxs_view* v, int32_t* rects, int32_t* ranges, int32_t* pa
   cudaStream_t s = (cudaStream_t)stream_;
   if (rects && v->P)
     NXS_CUDA(cudaMemcpyAsync(rects, v->rects.p, (size_t)v->P * 16, cudaMemcpyDeviceToDevice, s));
+  if (v->n_phases < 1) return NXS_OK;
   if (ranges)
-    NXS_CUDA(cudaMemcpyAsync(ranges, v->ranges.p, (size_t)v->n_tiles * 8,
+    NXS_CUDA(cudaMemcpyAsync(ranges, v->ranges_ph[0].p, (size_t)v->n_tiles * 8,
                              cudaMemcpyDeviceToDevice, s));
-  if (pair_ranks && v->n_pairs)
-    NXS_CUDA(cudaMemcpyAsync(pair_ranks, v->pv_out.p, (size_t)v->n_pairs * 4,
+  if (pair_ranks && v->ph_pairs[0])
+    NXS_CUDA(cudaMemcpyAsync(pair_ranks, v->pv_ph[0].p, (size_t)v->ph_pairs[0] * 4,
                              cudaMemcpyDeviceToDevice, s));
   return NXS_OK;
 }

@@ -41,10 +41,8 @@ constexpr size_t BWD_SMEM = sizeof(float4) * BWD_BATCH * (REC_F4 + 3) + sizeof(u
 template <int FAM, bool COUNT>
 __global__ void __launch_bounds__(TILE_PIX, 3)
     k_blend_bwd(const float4* __restrict__ records, const float4* __restrict__ bframe,
-                const uint32_t* __restrict__ pairs,
-                const int2* __restrict__ ranges, CamDev cam, ModelDev m, float cutoff,
-                double near_plane, float bg0, float bg1, float bg2,
-                const float* __restrict__ seed, PixCache cache,
+                PhaseLists lists, CamDev cam, ModelDev m, float cutoff, double near_plane,
+                float bg0, float bg1, float bg2, const float* __restrict__ seed, PixCache cache,
                 double* __restrict__ moments, Counters* __restrict__ cnt) {
   extern __shared__ float4 smem_dyn[];
   float4(*s_rec)[REC_F4] = reinterpret_cast<float4(*)[REC_F4]>(smem_dyn);
@@ -92,14 +90,19 @@ __global__ void __launch_bounds__(TILE_PIX, 3)
   __syncthreads();
   if (last >= 0) atomicMax(&s_maxlast, last);
   __syncthreads();
-  const int2 rg = ranges[tile];
-  const int hi_end = s_maxlast + 1;
+  const int vmax = s_maxlast + 1;  // virtual per-tile list positions [0, vmax) are replayed
 
-  for (int hi = hi_end; hi > rg.x; hi -= BWD_BATCH) {
-    const int base = max(rg.x, hi - BWD_BATCH);
+  // phases back to front, each phase's segment back to front
+  for (int ph = lists.n - 1; ph >= 0; --ph) {
+   const int2 seg = lists.ranges[ph][tile];
+   if (seg.y <= seg.x) continue;
+   const int c0 = lists.cum[ph][tile];  // virtual index of seg.x
+   const uint32_t* __restrict__ pairs = lists.pairs[ph];
+   for (int hi = min(c0 + (seg.y - seg.x), vmax); hi > c0; hi -= BWD_BATCH) {
+    const int base = max(c0, hi - BWD_BATCH);  // virtual
     const int n = hi - base;
     __syncthreads();
-    if (tid < n) s_rank[tid] = pairs[base + tid];
+    if (tid < n) s_rank[tid] = pairs[seg.x + (base - c0) + tid];
     for (int k = tid; k < n * NMOM; k += TILE_PIX) s_acc[k] = 0.f;
     __syncthreads();
     for (int k = tid; k < n * 8; k += TILE_PIX) {
@@ -253,6 +256,7 @@ __global__ void __launch_bounds__(TILE_PIX, 3)
         atomicAdd(&moments[(size_t)s_rank[e] * NMOM + (k - e * NMOM)], (double)val);
       }
     }
+   }
   }
 
   if (COUNT) {
@@ -271,41 +275,31 @@ __global__ void __launch_bounds__(TILE_PIX, 3)
 
 template <int FAM>
 static void launch_bwd_fam(bool count, int n_tiles, const float4* records, const float4* bframe,
-                           const uint32_t* pairs,
-                           const int2* ranges, const CamDev& cam, const ModelDev& m,
+                           const PhaseLists& lists, const CamDev& cam, const ModelDev& m,
                            float cutoff, double near_plane, const float* bg, const float* seed,
                            const PixCache& cache, double* moments, Counters* cnt,
                            cudaStream_t s) {
   static bool attr_set = false;  // host-side, once per instantiation
   if (!attr_set) {
-    cudaFuncSetAttribute(k_blend_bwd<FAM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)BWD_SMEM);
-    cudaFuncSetAttribute(k_blend_bwd<FAM, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)BWD_SMEM);
-    cudaFuncSetAttribute(k_blend_bwd<FAM, true>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         (int)cudaSharedmemCarveoutMaxShared);
-    cudaFuncSetAttribute(k_blend_bwd<FAM, false>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         (int)cudaSharedmemCarveoutMaxShared);
+    for (auto k : {k_blend_bwd<FAM, true>, k_blend_bwd<FAM, false>}) {
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BWD_SMEM);
+      cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           (int)cudaSharedmemCarveoutMaxShared);
+    }
     attr_set = true;
   }
-  if (count)
-    k_blend_bwd<FAM, true><<<n_tiles, TILE_PIX, BWD_SMEM, s>>>(records, bframe, pairs, ranges, cam, m, cutoff,
-                                                         near_plane, bg[0], bg[1], bg[2], seed,
-                                                         cache, moments, cnt);
-  else
-    k_blend_bwd<FAM, false><<<n_tiles, TILE_PIX, BWD_SMEM, s>>>(records, bframe, pairs, ranges, cam, m, cutoff,
-                                                          near_plane, bg[0], bg[1], bg[2], seed,
-                                                          cache, moments, cnt);
+  auto k = count ? k_blend_bwd<FAM, true> : k_blend_bwd<FAM, false>;
+  k<<<n_tiles, TILE_PIX, BWD_SMEM, s>>>(records, bframe, lists, cam, m, cutoff, near_plane, bg[0],
+                                        bg[1], bg[2], seed, cache, moments, cnt);
 }
 
 void launch_blend_bwd(bool count, int n_tiles, const float4* records, const float4* bframe,
-                      const uint32_t* pairs,
-                      const int2* ranges, const CamDev& cam, const ModelDev& m, float cutoff,
-                      double near_plane, const float* bg, const float* seed,
+                      const PhaseLists& lists, const CamDev& cam, const ModelDev& m,
+                      float cutoff, double near_plane, const float* bg, const float* seed,
                       const PixCache& cache, double* moments, Counters* cnt, cudaStream_t s) {
   if (n_tiles == 0) return;
 #define NXS_BWD(F) \
-  launch_bwd_fam<F>(count, n_tiles, records, bframe, pairs, ranges, cam, m, cutoff, near_plane, bg, seed, \
+  launch_bwd_fam<F>(count, n_tiles, records, bframe, lists, cam, m, cutoff, near_plane, bg, seed, \
                     cache, moments, cnt, s)
   switch (m.fam) {
     case FAM_EXP: NXS_BWD(FAM_EXP); break;

@@ -23,18 +23,22 @@ namespace nxs {
 constexpr int FWD_BATCH = 64;  // list entries per staged batch
 
 template <int FAM, bool COUNT>
-__global__ void __launch_bounds__(TILE_PIX)
+__global__ void __launch_bounds__(TILE_PIX, 3)
     k_blend_fwd(const float4* __restrict__ records, const uint32_t* __restrict__ pairs,
-                const int2* __restrict__ ranges, CamDev cam, ModelDev m, int max_splats,
-                float cutoff, double near_plane, float bg0, float bg1, float bg2,
-                float* __restrict__ rgb,
-                int32_t* __restrict__ overdraw, float* __restrict__ residual, PixCache cache,
+                const int2* __restrict__ ranges, const int32_t* __restrict__ cum_in,
+                int32_t* __restrict__ cum_out, uint8_t* __restrict__ active,
+                unsigned int* __restrict__ n_active, bool resume, bool save, CamDev cam,
+                ModelDev m,
+                int max_splats, float cutoff, double near_plane, float bg0, float bg1, float bg2,
+                float* __restrict__ rgb, int32_t* __restrict__ overdraw,
+                float* __restrict__ residual, PixCache cache, PixResume rs,
                 Counters* __restrict__ cnt) {
+  const int tile = blockIdx.x;
+  if (!active[tile]) return;  // every pixel of the tile finished in an earlier phase
   // two 64-entry record buffers: the next batch streams in (cp.async)
   // while the current one is composited
   __shared__ float4 s_rec[2][FWD_BATCH][REC_F4];
 
-  const int tile = blockIdx.x;
   const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
   const int tid = threadIdx.x;
   const int px = tx * TILE + (tid & (TILE - 1)), py = ty * TILE + (tid >> 4);
@@ -52,9 +56,34 @@ __global__ void __launch_bounds__(TILE_PIX)
   int ck = -1;
   float Pck = 0.f;
   unsigned long long ntest = 0;
-  bool done = !inside || max_splats <= 0;
+  const int pix = py * cam.W + px;
+  if (resume && inside) {  // carry of the previous depth phase
+    rad0 = rs.rad[3 * pix + 0];
+    rad1 = rs.rad[3 * pix + 1];
+    rad2 = rs.rad[3 * pix + 2];
+    Trem = rs.trem[pix];
+    count = rs.count[pix];
+    sea0 = rs.sea[3 * pix + 0];
+    sea1 = rs.sea[3 * pix + 1];
+    sea2 = rs.sea[3 * pix + 2];
+    sa = rs.sa[pix];
+    last = cache.last[pix];
+    sat = cache.sat[pix] != 0;
+    tk = cache.t_k[pix];
+    thi = cache.tau_hi[pix];
+    tlo = cache.tau_lo[pix];
+    P = cache.P_end[pix];
+    ck = cache.ck_idx[pix];
+    Pck = cache.P_ck[pix];
+    ek0 = cache.e_k[3 * pix + 0];
+    ek1 = cache.e_k[3 * pix + 1];
+    ek2 = cache.e_k[3 * pix + 2];
+  }
+  bool done = !inside || sat || count >= max_splats;
+  const int count0 = count;
 
   const int2 rg = ranges[tile];
+  const int vbase = cum_in[tile] - rg.x;  // list position -> virtual per-tile index
   auto stage = [&](int buf, int base) {
     const int n = min(FWD_BATCH, rg.y - base);
     for (int k = tid; k < n * REC_F4; k += TILE_PIX) {
@@ -87,7 +116,7 @@ __global__ void __launch_bounds__(TILE_PIX)
           ok = ray_peak_test(s_cur[j][0], s_cur[j][1], s_cur[j][2], s_cur[j][3], pc, cutoff, t);
         }
         if (!ok) continue;
-        const int idx = base + j;
+        const int idx = vbase + base + j;
         const float alpha = t.alpha;
         float E0, E1, E2;
         emission(s_cur[j][4], s_cur[j][5], s_cur[j][6], pc, E0, E1, E2);
@@ -145,13 +174,19 @@ __global__ void __launch_bounds__(TILE_PIX)
     if (__syncthreads_count(!done) == 0) break;
   }
   cp_async_wait<0>();
+  const int still = __syncthreads_count(!done);
+  if (tid == 0) {
+    active[tile] = still > 0 ? 1 : 0;
+    cum_out[tile] = cum_in[tile] + (rg.y - rg.x);
+    if (still > 0) atomicAdd(n_active, 1u);
+  }
 
   if (COUNT) {
     __shared__ unsigned long long s_cnt[2];
     if (tid == 0) s_cnt[0] = s_cnt[1] = 0;
     __syncthreads();
     atomicAdd(&s_cnt[0], ntest);
-    atomicAdd(&s_cnt[1], (unsigned long long)count);
+    atomicAdd(&s_cnt[1], (unsigned long long)(count - count0));
     __syncthreads();
     if (tid == 0) {
       atomicAdd(&cnt->tests_fwd, s_cnt[0]);
@@ -160,7 +195,6 @@ __global__ void __launch_bounds__(TILE_PIX)
   }
 
   if (!inside) return;
-  const int pix = py * cam.W + px;
   const float res = sat ? 0.f : Trem;  // render.py:210
   rgb[3 * pix + 0] = fmaf(bg0, res, rad0);
   rgb[3 * pix + 1] = fmaf(bg1, res, rad1);
@@ -181,44 +215,43 @@ __global__ void __launch_bounds__(TILE_PIX)
   cache.theta0[3 * pix + 0] = sea0 - ek0 * sa;  // render.py:213
   cache.theta0[3 * pix + 1] = sea1 - ek1 * sa;
   cache.theta0[3 * pix + 2] = sea2 - ek2 * sa;
+  if (save && still > 0) {  // the tile continues in the next depth phase
+    rs.rad[3 * pix + 0] = rad0;
+    rs.rad[3 * pix + 1] = rad1;
+    rs.rad[3 * pix + 2] = rad2;
+    rs.trem[pix] = Trem;
+    rs.count[pix] = count;
+    rs.sea[3 * pix + 0] = sea0;
+    rs.sea[3 * pix + 1] = sea1;
+    rs.sea[3 * pix + 2] = sea2;
+    rs.sa[pix] = sa;
+  }
 }
+
 
 template <int FAM>
-static void launch_fwd_fam(bool count, int n_tiles, const float4* records, const uint32_t* pairs,
-                           const int2* ranges, const CamDev& cam, const ModelDev& m,
-                           int max_splats, float cutoff, double near_plane, const float* bg,
-                           float* rgb, int32_t* overdraw, float* residual, const PixCache& cache,
+static void launch_fwd_fam(bool count, int n_tiles, const FwdArgs& a, const CamDev& cam,
+                           const ModelDev& m, const PixCache& cache, const PixResume& rs,
                            Counters* cnt, cudaStream_t s) {
-  if (count)
-    k_blend_fwd<FAM, true><<<n_tiles, TILE_PIX, 0, s>>>(records, pairs, ranges, cam, m,
-                                                         max_splats, cutoff, near_plane, bg[0],
-                                                         bg[1], bg[2], rgb, overdraw, residual,
-                                                         cache, cnt);
-  else
-    k_blend_fwd<FAM, false><<<n_tiles, TILE_PIX, 0, s>>>(records, pairs, ranges, cam, m,
-                                                          max_splats, cutoff, near_plane, bg[0],
-                                                          bg[1], bg[2], rgb, overdraw, residual,
-                                                          cache, cnt);
+  auto k = count ? k_blend_fwd<FAM, true> : k_blend_fwd<FAM, false>;
+  k<<<n_tiles, TILE_PIX, 0, s>>>(a.records, a.pairs, a.ranges, a.cum_in, a.cum_out, a.active,
+                                 a.n_active, a.resume, a.save, cam, m, a.max_splats, a.cutoff,
+                                 a.near_plane, a.bg[0], a.bg[1], a.bg[2], a.rgb, a.overdraw,
+                                 a.residual, cache, rs, cnt);
 }
 
-void launch_blend_fwd(bool count, int n_tiles, const float4* records, const uint32_t* pairs,
-                      const int2* ranges, const CamDev& cam, const ModelDev& m, int max_splats,
-                      float cutoff, double near_plane, const float* bg, float* rgb,
-                      int32_t* overdraw, float* residual, const PixCache& cache, Counters* cnt,
-                      cudaStream_t s) {
+void launch_blend_fwd(bool count, int n_tiles, const FwdArgs& a, const CamDev& cam,
+                      const ModelDev& m, const PixCache& cache, const PixResume& rs,
+                      Counters* cnt, cudaStream_t s) {
   if (n_tiles == 0) return;
-#define NXS_FWD(F)                                                                            \
-  launch_fwd_fam<F>(count, n_tiles, records, pairs, ranges, cam, m, max_splats, cutoff,       \
-                    near_plane, bg, rgb, overdraw, residual, cache, cnt, s)
   switch (m.fam) {
-    case FAM_EXP: NXS_FWD(FAM_EXP); break;
-    case FAM_LIN: NXS_FWD(FAM_LIN); break;
-    case FAM_QUAD: NXS_FWD(FAM_QUAD); break;
-    case FAM_BLEND: NXS_FWD(FAM_BLEND); break;
-    case FAM_POW: NXS_FWD(FAM_POW); break;
-    default: NXS_FWD(FAM_SOFT); break;
+    case FAM_EXP: launch_fwd_fam<FAM_EXP>(count, n_tiles, a, cam, m, cache, rs, cnt, s); break;
+    case FAM_LIN: launch_fwd_fam<FAM_LIN>(count, n_tiles, a, cam, m, cache, rs, cnt, s); break;
+    case FAM_QUAD: launch_fwd_fam<FAM_QUAD>(count, n_tiles, a, cam, m, cache, rs, cnt, s); break;
+    case FAM_BLEND: launch_fwd_fam<FAM_BLEND>(count, n_tiles, a, cam, m, cache, rs, cnt, s); break;
+    case FAM_POW: launch_fwd_fam<FAM_POW>(count, n_tiles, a, cam, m, cache, rs, cnt, s); break;
+    default: launch_fwd_fam<FAM_SOFT>(count, n_tiles, a, cam, m, cache, rs, cnt, s); break;
   }
-#undef NXS_FWD
 }
 
 }  // namespace nxs

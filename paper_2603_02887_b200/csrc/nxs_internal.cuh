@@ -4,8 +4,10 @@
 //   order    [P]      u32   rank -> Gaussian index (stable fp64 depth sort)
 //   records  [P][8]   float4 per-rank projected record, 128 B, rank order
 //   rects    [P]      int4  tile rectangle per rank (tx0,ty0,tx1,ty1)
-//   pairs    [n_pairs] u32  ranks, grouped by tile (stable, so rank-ascending)
-//   ranges   [T]      int2  [start, end) of each tile's run in `pairs`
+//   pairs    [p][n]   u32   per depth phase p: ranks grouped by tile (stable,
+//                          so rank-ascending); tiles still active only
+//   ranges   [p][T]   int2  [start, end) of each tile's run in pairs[p]
+//   cum      [p][T]   i32   virtual list index where tile's phase-p run starts
 //   cache    [H*W]    per-pixel replay state (SoA, see PixCache)
 //   moments  [P][24]  f64   per-rank gradient moments (backward)
 #pragma once
@@ -73,6 +75,46 @@ struct PixCache {
   float* P_ck;       // P before that splat
   float* e_k;        // [3] saturating emission (or background)
   float* theta0;     // [3] reference quadratic-adjoint cache (compat)
+};
+
+// Progressive binning: ranks are binned in depth phases [R_p, R_{p+1});
+// phase p only emits pairs for tiles with a pixel still neither saturated
+// nor capped, and the forward resumes its per-pixel carry across phases.
+constexpr int MAX_PHASES = 4;
+
+struct PixResume {  // forward carry kept between phases (besides PixCache)
+  float* rad;       // [3]
+  float* trem;
+  int32_t* count;
+  float* sea;       // [3]
+  float* sa;
+};
+
+struct PhaseLists {  // the per-tile virtual list = phase segments in order
+  const uint32_t* pairs[MAX_PHASES];  // sorted ranks of phase p
+  const int2* ranges[MAX_PHASES];     // per tile [start, end) in pairs[p]
+  const int32_t* cum[MAX_PHASES];     // per tile virtual index of the segment start
+  int n;
+};
+
+// arguments of one forward phase launch
+struct FwdArgs {
+  const float4* records;
+  const uint32_t* pairs;
+  const int2* ranges;
+  const int32_t* cum_in;
+  int32_t* cum_out;
+  uint8_t* active;
+  unsigned int* n_active;
+  bool resume;  // load the carry of the previous phase
+  bool save;    // another phase follows: keep the carry of unfinished tiles
+  int max_splats;
+  float cutoff;
+  double near_plane;
+  float bg[3];
+  float* rgb;
+  int32_t* overdraw;
+  float* residual;
 };
 
 struct Counters {

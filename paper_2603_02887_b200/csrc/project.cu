@@ -286,19 +286,36 @@ __global__ void k_project(const float* __restrict__ centers, const float* __rest
   out.n_tiles[r] = ntile;
 }
 
-// K2: emit (tile, rank) pairs at the exclusive-scan offsets, rank order.
+// K2a: per rank of [r0, r1), the number of still-active tiles in its rect.
+__global__ void k_count_active(const int4* __restrict__ rects, int64_t r0, int64_t r1,
+                               int tiles_x, const uint8_t* __restrict__ active,
+                               unsigned long long* __restrict__ counts) {
+  const int64_t r = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= r1) return;
+  const int4 rc = rects[r];
+  unsigned long long n = 0;
+  if (rc.x >= 0)
+    for (int ty = rc.y; ty <= rc.w; ++ty)
+      for (int tx = rc.x; tx <= rc.z; ++tx) n += active[ty * tiles_x + tx];
+  counts[r - r0] = n;
+}
+
+// K2b: emit (tile, rank) pairs of active tiles at the exclusive-scan
+// offsets, in rank order (so a stable sort by tile keeps ranks ascending).
 __global__ void k_emit_pairs(const int4* __restrict__ rects,
-                             const unsigned long long* __restrict__ offsets, int64_t P,
-                             int tiles_x, uint32_t* __restrict__ keys,
-                             uint32_t* __restrict__ vals) {
-  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= P) return;
-  int4 rc = rects[r];
+                             const unsigned long long* __restrict__ offsets, int64_t r0,
+                             int64_t r1, int tiles_x, const uint8_t* __restrict__ active,
+                             uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+  const int64_t r = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= r1) return;
+  const int4 rc = rects[r];
   if (rc.x < 0) return;
-  unsigned long long o = offsets[r];
+  unsigned long long o = offsets[r - r0];
   for (int ty = rc.y; ty <= rc.w; ++ty)
     for (int tx = rc.x; tx <= rc.z; ++tx) {
-      keys[o] = (uint32_t)(ty * tiles_x + tx);
+      const int t = ty * tiles_x + tx;
+      if (!active[t]) continue;
+      keys[o] = (uint32_t)t;
       vals[o] = (uint32_t)r;
       ++o;
     }
@@ -331,11 +348,19 @@ void launch_project(const float* centers, const float* scales, const float* quat
                                                         P, order, cam, cutoff, near_plane, o);
 }
 
-void launch_emit_pairs(const int4* rects, const unsigned long long* offsets, int64_t P,
-                       int tiles_x, uint32_t* keys, uint32_t* vals, cudaStream_t s) {
-  if (P == 0) return;
-  k_emit_pairs<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(rects, offsets, P, tiles_x, keys,
-                                                           vals);
+void launch_count_active(const int4* rects, int64_t r0, int64_t r1, int tiles_x,
+                         const uint8_t* active, unsigned long long* counts, cudaStream_t s) {
+  if (r1 <= r0) return;
+  k_count_active<<<(unsigned)((r1 - r0 + 255) / 256), 256, 0, s>>>(rects, r0, r1, tiles_x, active,
+                                                                   counts);
+}
+
+void launch_emit_pairs(const int4* rects, const unsigned long long* offsets, int64_t r0, int64_t r1,
+                       int tiles_x, const uint8_t* active, uint32_t* keys, uint32_t* vals,
+                       cudaStream_t s) {
+  if (r1 <= r0) return;
+  k_emit_pairs<<<(unsigned)((r1 - r0 + 255) / 256), 256, 0, s>>>(rects, offsets, r0, r1, tiles_x,
+                                                                 active, keys, vals);
 }
 
 void launch_tile_ranges(const uint32_t* keys, int64_t n, int2* ranges, cudaStream_t s) {

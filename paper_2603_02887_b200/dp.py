@@ -79,7 +79,7 @@ class DataParallelStep:
 
 
 def device_view_renderer(dev_scene, model, background, cameras, seeds, *, chunk_size=1,
-                         max_splats=128, views=None):
+                         max_splats=128, views=None, first_phase_ranks=0):
     """Per-view fwd+bwd through libnxs on the current CUDA device.
     ``cameras[v]`` / ``seeds[v]`` (H,W,3 float32 CUDA) for view v; each view
     index gets its own persistent ``nxs_view`` workspace."""
@@ -92,7 +92,7 @@ def device_view_renderer(dev_scene, model, background, cameras, seeds, *, chunk_
             views[v] = _native.View()
         cam = cameras[v]
         forward_device(views[v], dev_scene, cam, model, background, chunk_size=chunk_size,
-                       max_splats=max_splats)
+                       max_splats=max_splats, first_phase_ranks=first_phase_ranks)
         backward_device(views[v], dev_scene, seeds[v], grads.fields)
 
     render_view.views = views

@@ -179,7 +179,8 @@ def _model_struct(model):
 
 def forward_device(view, dev: DeviceScene, camera, model, background, *, max_splats=128,
                    alpha_cutoff=DEFAULT_ALPHA_CUTOFF, near=NEAR_PLANE, chunk_size=1,
-                   count_events=False, out=None, stream=None):
+                   count_events=False, full_binning=False, first_phase_ranks=0, out=None,
+                   stream=None):
     """Forward render on the device; returns (rgb (H,W,3), overdraw (H,W)
     int32, residual (H,W)) float32 CUDA tensors."""
     import torch
@@ -193,8 +194,9 @@ def forward_device(view, dev: DeviceScene, camera, model, background, *, max_spl
                torch.empty((H, W), dtype=torch.int32, device=d),
                torch.empty((H, W), dtype=torch.float32, device=d))
     bg = np.asarray(background, dtype=np.float64).reshape(3)
-    opts = _native.make_opts(max_splats, alpha_cutoff, near, chunk,
-                             _native.NXS_FLAG_COUNT_EVENTS if count_events else 0)
+    flags = (_native.NXS_FLAG_COUNT_EVENTS if count_events else 0) | \
+        (_native.NXS_FLAG_FULL_BINNING if full_binning else 0)
+    opts = _native.make_opts(max_splats, alpha_cutoff, near, chunk, flags, first_phase_ranks)
     try:
         view.forward(dev, _native.make_camera(camera), ms, opts, bg, out[0], out[1], out[2],
                      stream=stream)
