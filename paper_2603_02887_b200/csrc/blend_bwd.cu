@@ -1,4 +1,4 @@
-// K4: path-replay backward, one 16x16 tile per 256-thread block.
+// K4: path-replay backward, one 16x16 tile per 128-thread block (2 pixels per thread).
 //
 // Replaces the reference replay and closed-form adjoints
 // (pkg/src/nexsplat/render.py:_backward_sweep 220-324) and produces the
@@ -28,18 +28,152 @@ namespace nxs {
 
 constexpr int BWD_BATCH = 64;  // list entries staged per batch
 
-// Shared-memory layout of one block (dynamic): staged records, their ranks,
-// per-entry moment accumulators, and one 24x36-float transpose scratch per
-// warp (row k = moment k of all 32 lanes; rows padded to 36 floats so the
-// column stores and the 16-B row loads are both bank-conflict free).
+// Two pixels per thread: a 128-thread block covers the 16x16 tile, thread t
+// owning pixels t (rows 0-7) and t+128 (rows 8-15).  Each thread sums its
+// two pixels' moments in registers before the warp reduction, halving the
+// per-entry reductions, and the two independent pixel chains add ILP.
+constexpr int BWD_THREADS = TILE_PIX / 2;
+constexpr int BWD_WARPS = BWD_THREADS / 32;
+
+// Shared-memory layout of one block (dynamic): staged records + B frames,
+// their ranks, per-entry moment accumulators, and one 24x36-float transpose
+// scratch per warp (row k = moment k of all 32 lanes; rows padded to 36
+// floats so the column stores and the 16-B row loads are conflict free).
 constexpr int RED_STRIDE = 36;
 constexpr int RED_WARP = NMOM * RED_STRIDE;  // floats per warp
 constexpr size_t BWD_SMEM = sizeof(float4) * BWD_BATCH * (REC_F4 + 3) + sizeof(uint32_t) * BWD_BATCH +
-                            sizeof(float) * BWD_BATCH * NMOM +
-                            sizeof(float) * RED_WARP * (TILE_PIX / 32);
+                            sizeof(float) * BWD_BATCH * NMOM + sizeof(float) * RED_WARP * BWD_WARPS;
+
+// per-pixel back-to-front replay state
+struct BwdPix {
+  PixelConst pc;
+  int px, py, last, ck;
+  bool sat;
+  float tk, thi, tlo, P, Pck, s0, s1, s2, ek0, ek1, ek2, carry;
+};
+
+// one pixel's contribution of list entry (records rec, B frame bf) at
+// virtual position idx; returns false (and leaves the outputs at zero) when
+// the pixel does not replay this entry
+template <int FAM>
+__device__ __forceinline__ bool bwd_pixel(BwdPix& st, const float4* rec, const float4* bf, int idx,
+                                          const CamDev& cam, const ModelDev& m, float cutoff,
+                                          double near_plane, float inv_f, float gam, float& dm2,
+                                          float& ux, float& uy, float& uz, float& dak, float& e0,
+                                          float& e1, float& e2, unsigned long long& ntest,
+                                          bool count) {
+  if (idx > st.last) return false;
+  if (count) ++ntest;
+  TestOut t;
+  const bool gen = (__float_as_int(rec[3].w) & RF_GENERAL) != 0;  // block-uniform
+  float gx = 0.f, gy = 0.f, gz = 0.f;
+  const bool ok = gen ? general_test(rec, cam, st.px, st.py, cutoff, near_plane, t, gx, gy, gz)
+                      : ray_peak_test(rec[0], rec[1], rec[2], rec[3], st.pc, cutoff, t);
+  if (!ok) return false;
+  const float alpha = t.alpha;
+  float E0, E1, E2;
+  const int mask = emission(rec[4], rec[5], rec[6], st.pc, E0, E1, E2);
+  float dE0, dE1, dE2;
+  if (st.sat && idx == st.last) {
+    // saturating splat: moves the loss only through its emission (render.py:313-314)
+    st.ek0 = E0;
+    st.ek1 = E1;
+    st.ek2 = E2;
+    dE0 = st.s0 * st.tk;
+    dE1 = st.s1 * st.tk;
+    dE2 = st.s2 * st.tk;
+  } else {
+    // state in front of splat i, recovered back to front
+    if constexpr (FAM != FAM_EXP) df_add(st.thi, st.tlo, -alpha);
+    if constexpr (IsPFam<FAM>::value) {
+      st.P = (idx == st.ck) ? st.Pck : __fdiv_rn(st.P, __fsub_rn(1.0f, alpha));
+    }
+    float fp;
+    const float g = weight_g<FAM>(m, st.thi, st.tlo, st.P, fp);
+    const float w = alpha * g;
+    const float sdE = fmaf(st.s0, E0 - st.ek0, fmaf(st.s1, E1 - st.ek1, st.s2 * (E2 - st.ek2)));
+    float da;
+    if constexpr (IsPFam<FAM>::value) {
+      da = fmaf(sdE, g, -gam * st.P * st.carry);
+      st.carry = fmaf(1.0f - alpha, st.carry, sdE * alpha);
+    } else {
+      da = fmaf(sdE, g, st.carry);
+      st.carry = fmaf(sdE * alpha, fp, st.carry);
+    }
+    dE0 = st.s0 * w;
+    dE1 = st.s1 * w;
+    dE2 = st.s2 * w;
+    // chain moments (render.py:326-339): by the envelope theorem the
+    // kernel-peak offset u = Rᵀ(t·d - b) carries the whole chain
+    // (∂m2/∂μ = -2RΛu, ∂m2/∂s_k = -2u_k²/s_k³, ∂m2/∂R = 2 diff (Λu)ᵀ).
+    // u is built from the stable conic offset diff' = b'_z·e,
+    // e = δ - ε h, δ = Δ/f, ε = δᵀA'h/D (all O(|δ|), no cancellation
+    // against b'), rotated into the Gaussian frame per pixel so each
+    // moment term has the sign structure of the reference's terms
+    const float dae = (t.araw >= ALPHA_MAX_F) ? 0.f : da;
+    dm2 = -0.5f * alpha * dae;
+    dak = dae * t.kern;
+    float qx, qy, qz;  // peak offset e (conic: diff'/b'_z; general: diff)
+    if (gen) {
+      qx = gx;
+      qy = gy;
+      qz = gz;
+    } else {
+      const float4 r2 = rec[2];
+      const float dxn = t.ddx * inv_f, dyn = t.ddy * inv_f;
+      const float Ahx = r2.x * t.u;
+      const float Ahy = fmaf(r2.x * r2.y, t.u, r2.w * t.v);
+      const float eps = __fdividef(fmaf(dxn, Ahx, dyn * Ahy), t.D);
+      qx = fmaf(-eps, st.pc.hx, dxn);
+      qy = fmaf(-eps, st.pc.hy, dyn);
+      qz = -eps;
+    }
+    // Gaussian-frame offset u = Rᵀ diff = B e
+    ux = fmaf(bf[0].x, qx, fmaf(bf[0].y, qy, bf[0].z * qz));
+    uy = fmaf(bf[1].x, qx, fmaf(bf[1].y, qy, bf[1].z * qz));
+    uz = fmaf(bf[2].x, qx, fmaf(bf[2].y, qy, bf[2].z * qz));
+  }
+  // SH moments use dE_c·[E_c > 0] (render.py:340-341)
+  e0 = (mask & 1) ? dE0 : 0.f;
+  e1 = (mask & 2) ? dE1 : 0.f;
+  e2 = (mask & 4) ? dE2 : 0.f;
+  return true;
+}
+
+__device__ __forceinline__ void bwd_load(BwdPix& st, const CamDev& cam, int px, int py,
+                                         const PixCache& cache, const float* __restrict__ seed,
+                                         float bg0, float bg1, float bg2) {
+  st.px = px;
+  st.py = py;
+  st.pc = pixel_setup(cam, px, py);
+  st.last = -1;
+  st.sat = false;
+  st.tk = st.thi = st.tlo = st.Pck = 0.f;
+  st.P = 1.f;
+  st.ck = -1;
+  st.s0 = st.s1 = st.s2 = 0.f;
+  if (px < cam.W && py < cam.H) {
+    const int pix = py * cam.W + px;
+    st.last = cache.last[pix];
+    st.sat = cache.sat[pix] != 0;
+    st.tk = cache.t_k[pix];
+    st.thi = cache.tau_hi[pix];
+    st.tlo = cache.tau_lo[pix];
+    st.P = cache.P_end[pix];
+    st.ck = cache.ck_idx[pix];
+    st.Pck = cache.P_ck[pix];
+    st.s0 = seed[3 * pix + 0];
+    st.s1 = seed[3 * pix + 1];
+    st.s2 = seed[3 * pix + 2];
+  }
+  st.ek0 = bg0;
+  st.ek1 = bg1;
+  st.ek2 = bg2;
+  st.carry = 0.f;  // Θ (τ-family) or U (P-family), seed-contracted
+}
 
 template <int FAM, bool COUNT>
-__global__ void __launch_bounds__(TILE_PIX, 3)
+__global__ void __launch_bounds__(BWD_THREADS, 4)
     k_blend_bwd(const float4* __restrict__ records, const float4* __restrict__ bframe,
                 PhaseLists lists, CamDev cam, ModelDev m, float cutoff, double near_plane,
                 float bg0, float bg1, float bg2, const float* __restrict__ seed, PixCache cache,
@@ -55,32 +189,12 @@ __global__ void __launch_bounds__(TILE_PIX, 3)
   const int tile = blockIdx.x;
   const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
   const int tid = threadIdx.x, lane = tid & 31;
-  const int px = tx * TILE + (tid & (TILE - 1)), py = ty * TILE + (tid >> 4);
-  const bool inside = px < cam.W && py < cam.H;
-  const PixelConst pc = pixel_setup(cam, px, py);
-  const int pix = py * cam.W + px;
+  const int px = tx * TILE + (tid & (TILE - 1));
+  const int py0 = ty * TILE + (tid >> 4);
+  BwdPix st[2];
+  bwd_load(st[0], cam, px, py0, cache, seed, bg0, bg1, bg2);
+  bwd_load(st[1], cam, px, py0 + TILE / 2, cache, seed, bg0, bg1, bg2);
   float* red = s_red + (tid >> 5) * RED_WARP;
-
-  int last = -1;
-  bool sat = false;
-  float tk = 0.f, thi = 0.f, tlo = 0.f, P = 1.f, Pck = 0.f;
-  int ck = -1;
-  float s0 = 0.f, s1 = 0.f, s2 = 0.f;
-  if (inside) {
-    last = cache.last[pix];
-    sat = cache.sat[pix] != 0;
-    tk = cache.t_k[pix];
-    thi = cache.tau_hi[pix];
-    tlo = cache.tau_lo[pix];
-    P = cache.P_end[pix];
-    ck = cache.ck_idx[pix];
-    Pck = cache.P_ck[pix];
-    s0 = seed[3 * pix + 0];
-    s1 = seed[3 * pix + 1];
-    s2 = seed[3 * pix + 2];
-  }
-  float ek0 = bg0, ek1 = bg1, ek2 = bg2;
-  float carry = 0.f;  // Θ (τ-family) or U (P-family), seed-contracted
   const float gam = (FAM == FAM_EXP) ? 1.0f : m.c;
   const float inv_f = (float)(1.0 / cam.f);
   const float Y0 = (float)SH_C0;
@@ -88,175 +202,100 @@ __global__ void __launch_bounds__(TILE_PIX, 3)
 
   if (tid == 0) s_maxlast = -1;
   __syncthreads();
-  if (last >= 0) atomicMax(&s_maxlast, last);
+  const int mylast = max(st[0].last, st[1].last);
+  if (mylast >= 0) atomicMax(&s_maxlast, mylast);
   __syncthreads();
   const int vmax = s_maxlast + 1;  // virtual per-tile list positions [0, vmax) are replayed
 
   // phases back to front, each phase's segment back to front
   for (int ph = lists.n - 1; ph >= 0; --ph) {
-   const int2 seg = lists.ranges[ph][tile];
-   if (seg.y <= seg.x) continue;
-   const int c0 = lists.cum[ph][tile];  // virtual index of seg.x
-   const uint32_t* __restrict__ pairs = lists.pairs[ph];
-   for (int hi = min(c0 + (seg.y - seg.x), vmax); hi > c0; hi -= BWD_BATCH) {
-    const int base = max(c0, hi - BWD_BATCH);  // virtual
-    const int n = hi - base;
-    __syncthreads();
-    if (tid < n) s_rank[tid] = pairs[seg.x + (base - c0) + tid];
-    for (int k = tid; k < n * NMOM; k += TILE_PIX) s_acc[k] = 0.f;
-    __syncthreads();
-    for (int k = tid; k < n * 8; k += TILE_PIX) {
-      const int e = k >> 3, part = k & 7;
-      s_rec[e][part] = records[(size_t)s_rank[e] * REC_F4 + part];
-    }
-    for (int k = tid; k < n * 3; k += TILE_PIX) {
-      const int e = k / 3, part = k - 3 * (k / 3);
-      s_bf[e][part] = bframe[(size_t)s_rank[e] * 3 + part];
-    }
-    __syncthreads();
-    if (COUNT) nent += n;
+    const int2 seg = lists.ranges[ph][tile];
+    if (seg.y <= seg.x) continue;
+    const int c0 = lists.cum[ph][tile];  // virtual index of seg.x
+    const uint32_t* __restrict__ pairs = lists.pairs[ph];
+    for (int hi = min(c0 + (seg.y - seg.x), vmax); hi > c0; hi -= BWD_BATCH) {
+      const int base = max(c0, hi - BWD_BATCH);  // virtual
+      const int n = hi - base;
+      __syncthreads();
+      if (tid < n) s_rank[tid] = pairs[seg.x + (base - c0) + tid];
+      for (int k = tid; k < n * NMOM; k += BWD_THREADS) s_acc[k] = 0.f;
+      __syncthreads();
+      for (int k = tid; k < n * 8; k += BWD_THREADS) {
+        const int e = k >> 3, part = k & 7;
+        s_rec[e][part] = records[(size_t)s_rank[e] * REC_F4 + part];
+      }
+      for (int k = tid; k < n * 3; k += BWD_THREADS) {
+        const int e = k / 3, part = k - 3 * (k / 3);
+        s_bf[e][part] = bframe[(size_t)s_rank[e] * 3 + part];
+      }
+      __syncthreads();
+      if (COUNT) nent += n;
 
-    for (int j = n - 1; j >= 0; --j) {
-      const int idx = base + j;
-      // per-pixel contribution as a few scalars; all zero when this lane
-      // contributes nothing, so the 24 moments need no separate zeroing
-      float dm2 = 0.f, ex = 0.f, ey = 0.f, ez = 0.f, dak = 0.f;
-      float e0 = 0.f, e1 = 0.f, e2 = 0.f;
-      bool contrib = false;
-      if (idx <= last) {
-        if (COUNT) ++ntest;
-        TestOut t;
-        const bool gen = (__float_as_int(s_rec[j][3].w) & RF_GENERAL) != 0;  // block-uniform
-        float gx = 0.f, gy = 0.f, gz = 0.f;
-        bool ok;
-        if (gen)
-          ok = general_test(s_rec[j], cam, px, py, cutoff, near_plane, t, gx, gy, gz);
-        else
-          ok = ray_peak_test(s_rec[j][0], s_rec[j][1], s_rec[j][2], s_rec[j][3], pc, cutoff, t);
-        if (ok) {
-          contrib = true;
-          const float alpha = t.alpha;
-          float E0, E1, E2;
-          const int mask = emission(s_rec[j][4], s_rec[j][5], s_rec[j][6], pc, E0, E1, E2);
-          float dE0, dE1, dE2;
-          if (sat && idx == last) {
-            // saturating splat: moves the loss only through its emission
-            ek0 = E0;
-            ek1 = E1;
-            ek2 = E2;
-            dE0 = s0 * tk;
-            dE1 = s1 * tk;
-            dE2 = s2 * tk;
-          } else {
-            // state in front of splat i, recovered back to front
-            if constexpr (FAM != FAM_EXP) df_add(thi, tlo, -alpha);
-            if constexpr (IsPFam<FAM>::value) {
-              P = (idx == ck) ? Pck : __fdiv_rn(P, __fsub_rn(1.0f, alpha));
-            }
-            float fp;
-            const float g = weight_g<FAM>(m, thi, tlo, P, fp);
-            const float w = alpha * g;
-            const float sdE = fmaf(s0, E0 - ek0, fmaf(s1, E1 - ek1, s2 * (E2 - ek2)));
-            float da;
-            if constexpr (IsPFam<FAM>::value) {
-              da = fmaf(sdE, g, -gam * P * carry);
-              carry = fmaf(1.0f - alpha, carry, sdE * alpha);
-            } else {
-              da = fmaf(sdE, g, carry);
-              carry = fmaf(sdE * alpha, fp, carry);
-            }
-            dE0 = s0 * w;
-            dE1 = s1 * w;
-            dE2 = s2 * w;
-            // chain moments (render.py:326-339): by the envelope theorem the
-            // kernel-peak offset u = Rᵀ(t·d - b) carries the whole chain
-            // (∂m2/∂μ = -2RΛu, ∂m2/∂s_k = -2u_k²/s_k³, ∂m2/∂R = 2 diff (Λu)ᵀ).
-            // u is built from the stable conic offset diff' = b'_z·e,
-            // e = δ - ε h, δ = Δ/f, ε = δᵀA'h/D (all O(|δ|), no cancellation
-            // against b'), rotated into the Gaussian frame per pixel so each
-            // moment term has the sign structure of the reference's terms
-            const float dae = (t.araw >= ALPHA_MAX_F) ? 0.f : da;
-            dm2 = -0.5f * alpha * dae;
-            dak = dae * t.kern;
-            float qx, qy, qz;  // peak offset e (conic: diff'/b'_z; general: diff)
-            if (gen) {
-              qx = gx;
-              qy = gy;
-              qz = gz;
-            } else {
-              const float4 r2 = s_rec[j][2];
-              const float dxn = t.ddx * inv_f, dyn = t.ddy * inv_f;
-              const float Ahx = r2.x * t.u;
-              const float Ahy = fmaf(r2.x * r2.y, t.u, r2.w * t.v);
-              const float eps = __fdividef(fmaf(dxn, Ahx, dyn * Ahy), t.D);
-              qx = fmaf(-eps, pc.hx, dxn);
-              qy = fmaf(-eps, pc.hy, dyn);
-              qz = -eps;
-            }
-            // Gaussian-frame offset u = Rᵀ diff = B e
-            const float4 B0 = s_bf[j][0], B1 = s_bf[j][1], B2 = s_bf[j][2];
-            ex = fmaf(B0.x, qx, fmaf(B0.y, qy, B0.z * qz));
-            ey = fmaf(B1.x, qx, fmaf(B1.y, qy, B1.z * qz));
-            ez = fmaf(B2.x, qx, fmaf(B2.y, qy, B2.z * qz));
+      for (int j = n - 1; j >= 0; --j) {
+        const int idx = base + j;
+        // both pixels' contributions as a few scalars each; zero when a
+        // pixel does not contribute, so the moments need no separate zeroing
+        float dm2[2] = {0.f, 0.f}, ux[2] = {0.f, 0.f}, uy[2] = {0.f, 0.f}, uz[2] = {0.f, 0.f};
+        float dak[2] = {0.f, 0.f}, e0[2] = {0.f, 0.f}, e1[2] = {0.f, 0.f}, e2[2] = {0.f, 0.f};
+        bool contrib = false;
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+          contrib |= bwd_pixel<FAM>(st[q], s_rec[j], s_bf[j], idx, cam, m, cutoff, near_plane,
+                                    inv_f, gam, dm2[q], ux[q], uy[q], uz[q], dak[q], e0[q], e1[q],
+                                    e2[q], ntest, COUNT);
+        if (__any_sync(0xffffffffu, contrib)) {
+          // warp transpose-reduce through shared memory: lane r writes its
+          // (two-pixel) moments down column r, lane k < 24 then sums row k
+          const PixelConst& pa = st[0].pc;
+          const PixelConst& pb = st[1].pc;
+          const float ax = dm2[0] * ux[0], ay = dm2[0] * uy[0], az = dm2[0] * uz[0];
+          const float bx = dm2[1] * ux[1], by = dm2[1] * uy[1], bz = dm2[1] * uz[1];
+          float* col = red + lane;
+          col[0 * RED_STRIDE] = fmaf(ax, ux[0], bx * ux[1]);
+          col[1 * RED_STRIDE] = fmaf(ax, uy[0], bx * uy[1]);
+          col[2 * RED_STRIDE] = fmaf(ax, uz[0], bx * uz[1]);
+          col[3 * RED_STRIDE] = fmaf(ay, uy[0], by * uy[1]);
+          col[4 * RED_STRIDE] = fmaf(ay, uz[0], by * uz[1]);
+          col[5 * RED_STRIDE] = fmaf(az, uz[0], bz * uz[1]);
+          col[6 * RED_STRIDE] = ax + bx;
+          col[7 * RED_STRIDE] = ay + by;
+          col[8 * RED_STRIDE] = az + bz;
+          col[11 * RED_STRIDE] = dak[0] + dak[1];
+          col[12 * RED_STRIDE] = (e0[0] + e0[1]) * Y0;
+          col[13 * RED_STRIDE] = fmaf(e0[0], pa.Y1, e0[1] * pb.Y1);
+          col[14 * RED_STRIDE] = fmaf(e0[0], pa.Y2, e0[1] * pb.Y2);
+          col[15 * RED_STRIDE] = fmaf(e0[0], pa.Y3, e0[1] * pb.Y3);
+          col[16 * RED_STRIDE] = (e1[0] + e1[1]) * Y0;
+          col[17 * RED_STRIDE] = fmaf(e1[0], pa.Y1, e1[1] * pb.Y1);
+          col[18 * RED_STRIDE] = fmaf(e1[0], pa.Y2, e1[1] * pb.Y2);
+          col[19 * RED_STRIDE] = fmaf(e1[0], pa.Y3, e1[1] * pb.Y3);
+          col[20 * RED_STRIDE] = (e2[0] + e2[1]) * Y0;
+          col[21 * RED_STRIDE] = fmaf(e2[0], pa.Y1, e2[1] * pb.Y1);
+          col[22 * RED_STRIDE] = fmaf(e2[0], pa.Y2, e2[1] * pb.Y2);
+          col[23 * RED_STRIDE] = fmaf(e2[0], pa.Y3, e2[1] * pb.Y3);
+          __syncwarp();
+          if (lane < NMOM && lane != 9 && lane != 10) {
+            const float4* row = reinterpret_cast<const float4*>(red + lane * RED_STRIDE);
+            const float4 a = row[0], b = row[1], c = row[2], d = row[3];
+            const float4 e = row[4], f = row[5], g = row[6], h = row[7];
+            const float sum = (((a.x + a.y) + (a.z + a.w)) + ((b.x + b.y) + (b.z + b.w))) +
+                              (((c.x + c.y) + (c.z + c.w)) + ((d.x + d.y) + (d.z + d.w))) +
+                              ((((e.x + e.y) + (e.z + e.w)) + ((f.x + f.y) + (f.z + f.w))) +
+                               (((g.x + g.y) + (g.z + g.w)) + ((h.x + h.y) + (h.z + h.w))));
+            if (sum != 0.f) atomicAdd(&s_acc[j * NMOM + lane], sum);
           }
-          // SH moments use dE_c·[E_c > 0] (render.py:340-341)
-          e0 = (mask & 1) ? dE0 : 0.f;
-          e1 = (mask & 2) ? dE1 : 0.f;
-          e2 = (mask & 4) ? dE2 : 0.f;
+          __syncwarp();
         }
       }
-      if (__any_sync(0xffffffffu, contrib)) {
-        // warp transpose-reduce through shared memory: lane r writes its 24
-        // moments down column r, lane k < 24 then sums row k
-        const float wx = dm2 * ex, wy = dm2 * ey, wz = dm2 * ez;
-        float* col = red + lane;
-        col[0 * RED_STRIDE] = wx * ex;
-        col[1 * RED_STRIDE] = wx * ey;
-        col[2 * RED_STRIDE] = wx * ez;
-        col[3 * RED_STRIDE] = wy * ey;
-        col[4 * RED_STRIDE] = wy * ez;
-        col[5 * RED_STRIDE] = wz * ez;
-        col[6 * RED_STRIDE] = wx;
-        col[7 * RED_STRIDE] = wy;
-        col[8 * RED_STRIDE] = wz;
-        col[9 * RED_STRIDE] = 0.f;
-        col[10 * RED_STRIDE] = 0.f;
-        col[11 * RED_STRIDE] = dak;
-        col[12 * RED_STRIDE] = e0 * Y0;
-        col[13 * RED_STRIDE] = e0 * pc.Y1;
-        col[14 * RED_STRIDE] = e0 * pc.Y2;
-        col[15 * RED_STRIDE] = e0 * pc.Y3;
-        col[16 * RED_STRIDE] = e1 * Y0;
-        col[17 * RED_STRIDE] = e1 * pc.Y1;
-        col[18 * RED_STRIDE] = e1 * pc.Y2;
-        col[19 * RED_STRIDE] = e1 * pc.Y3;
-        col[20 * RED_STRIDE] = e2 * Y0;
-        col[21 * RED_STRIDE] = e2 * pc.Y1;
-        col[22 * RED_STRIDE] = e2 * pc.Y2;
-        col[23 * RED_STRIDE] = e2 * pc.Y3;
-        __syncwarp();
-        if (lane < NMOM && lane != 9 && lane != 10) {
-          const float4* row = reinterpret_cast<const float4*>(red + lane * RED_STRIDE);
-          float4 a = row[0], b = row[1], c = row[2], d = row[3];
-          float4 e = row[4], f = row[5], g = row[6], h = row[7];
-          const float s = (((a.x + a.y) + (a.z + a.w)) + ((b.x + b.y) + (b.z + b.w))) +
-                          (((c.x + c.y) + (c.z + c.w)) + ((d.x + d.y) + (d.z + d.w))) +
-                          ((((e.x + e.y) + (e.z + e.w)) + ((f.x + f.y) + (f.z + f.w))) +
-                           (((g.x + g.y) + (g.z + g.w)) + ((h.x + h.y) + (h.z + h.w))));
-          if (s != 0.f) atomicAdd(&s_acc[j * NMOM + lane], s);
+      __syncthreads();
+      for (int k = tid; k < n * NMOM; k += BWD_THREADS) {
+        const float val = s_acc[k];
+        if (val != 0.f) {
+          const int e = k / NMOM;
+          atomicAdd(&moments[(size_t)s_rank[e] * NMOM + (k - e * NMOM)], (double)val);
         }
-        __syncwarp();
       }
     }
-    __syncthreads();
-    for (int k = tid; k < n * NMOM; k += TILE_PIX) {
-      const float val = s_acc[k];
-      if (val != 0.f) {
-        const int e = k / NMOM;
-        atomicAdd(&moments[(size_t)s_rank[e] * NMOM + (k - e * NMOM)], (double)val);
-      }
-    }
-   }
   }
 
   if (COUNT) {
@@ -289,7 +328,7 @@ static void launch_bwd_fam(bool count, int n_tiles, const float4* records, const
     attr_set = true;
   }
   auto k = count ? k_blend_bwd<FAM, true> : k_blend_bwd<FAM, false>;
-  k<<<n_tiles, TILE_PIX, BWD_SMEM, s>>>(records, bframe, lists, cam, m, cutoff, near_plane, bg[0],
+  k<<<n_tiles, BWD_THREADS, BWD_SMEM, s>>>(records, bframe, lists, cam, m, cutoff, near_plane, bg[0],
                                         bg[1], bg[2], seed, cache, moments, cnt);
 }
 
