@@ -19,8 +19,12 @@
 #include "nxs_internal.cuh"
 
 namespace nxs {
-void launch_depth_keys(const float*, int64_t, const CamDev&, unsigned long long*, uint32_t*,
-                       cudaStream_t);
+void launch_depth(const float*, int64_t, const CamDev&, double*, unsigned long long*, uint32_t*,
+                  unsigned long long*, cudaStream_t);
+void launch_key32(const double*, int64_t, const unsigned long long*, uint32_t*, cudaStream_t);
+void launch_key_fixup(const uint32_t*, uint32_t*, const double*, int64_t, unsigned long long*,
+                      cudaStream_t);
+void launch_rank_of(const uint32_t*, int64_t, uint32_t*, cudaStream_t);
 void launch_project(const float*, const float*, const float*, const float*, const float*, int,
                     int64_t, const uint32_t*, const CamDev&, double, double, unsigned long long*,
                     int4*, float4*, float4*, unsigned long long*, cudaStream_t);
@@ -33,8 +37,8 @@ void launch_blend_fwd(bool, int, const FwdArgs&, const CamDev&, const ModelDev&,
                       const PixResume&, Counters*, cudaStream_t);
 void launch_blend_bwd(bool, int, const float4*, const float4*, const PhaseLists&, const CamDev&,
                       const ModelDev&, float, double, const float*, const float*,
-                      const PixCache&, double*, Counters*, cudaStream_t);
-void launch_chain(const float*, const float*, int, int64_t, const uint32_t*, const double*,
+                      const PixCache&, double*, uint8_t*, Counters*, cudaStream_t);
+void launch_chain(const float*, const float*, int, int64_t, const uint32_t*, double*, uint8_t*,
                   float*, float*, float*, float*, float*, cudaStream_t);
 }  // namespace nxs
 
@@ -97,7 +101,8 @@ int bits_for(uint32_t n) {
 
 struct nxs_view {
   // per Gaussian
-  Buf dkeys_in, dkeys_out, idx_in, idx_out, records, bframe, rects, ntiles, offsets, moments;
+  Buf dkeys_in, dkeys_out, idx_in, idx_out, records, bframe, rects, ntiles, offsets, moments,
+      touched, depth, k32a, k32b, rank_of;
   // per pair: sort scratch, and the sorted ranks of each depth phase
   Buf pk_in, pk_out, pv_in, pv_ph[MAX_PHASES];
   // per tile: phase ranges and virtual offsets, activity
@@ -131,7 +136,8 @@ struct nxs_view {
   template <class F>
   void for_each_buf(F f) {
     Buf* all[] = {&dkeys_in, &dkeys_out, &idx_in,  &idx_out, &records, &bframe, &rects,
-                  &ntiles,   &offsets,   &moments, &pk_in,   &pk_out,  &pv_in,  &active,
+                  &ntiles,   &offsets,   &moments, &touched, &pk_in,   &pk_out,  &pv_in,  &active,
+                  &depth,    &k32a,      &k32b,    &rank_of,
                   &c_last,   &c_sat,     &c_tk,    &c_thi,   &c_tlo,   &c_P,    &c_ck,
                   &c_Pck,    &c_ek,      &c_th0,   &r_rad,   &r_trem,  &r_count, &r_sea,
                   &r_sa,     &temp,      &dev_small};
@@ -324,6 +330,10 @@ int nxs_forward(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
   // ---- workspace
   NXS_CUDA(ensure_n<unsigned long long>(v->dkeys_in, P));
   NXS_CUDA(ensure_n<unsigned long long>(v->dkeys_out, P));
+  NXS_CUDA(ensure_n<double>(v->depth, P));
+  NXS_CUDA(ensure_n<uint32_t>(v->k32a, P));
+  NXS_CUDA(ensure_n<uint32_t>(v->k32b, P));
+  NXS_CUDA(ensure_n<uint32_t>(v->rank_of, P));
   NXS_CUDA(ensure_n<uint32_t>(v->idx_in, P));
   NXS_CUDA(ensure_n<uint32_t>(v->idx_out, P));
   NXS_CUDA(ensure_n<float4>(v->records, P * REC_F4));
@@ -342,12 +352,13 @@ int nxs_forward(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
   NXS_CUDA(ensure_n<float>(v->c_Pck, npix));
   NXS_CUDA(ensure_n<float>(v->c_ek, npix * 3));
   NXS_CUDA(ensure_n<float>(v->c_th0, npix * 3));
-  NXS_CUDA(v->dev_small.ensure(8 * sizeof(unsigned long long)));
-  // dsmall: [0] straddle count, [1..4] event counters, [5] active tiles (u32)
+  NXS_CUDA(v->dev_small.ensure(16 * sizeof(unsigned long long)));
+  // dsmall: [0] straddle count, [1..4] event counters, [5] active tiles (u32),
+  // [6] min depth key, [7] max depth key, [8] key-run overflow
   unsigned long long* dsmall = v->dev_small.as<unsigned long long>();
   Counters* cnt = reinterpret_cast<Counters*>(dsmall + 1);
   unsigned int* n_active = reinterpret_cast<unsigned int*>(dsmall + 5);
-  NXS_CUDA(cudaMemsetAsync(dsmall, 0, 8 * sizeof(unsigned long long), s));
+  NXS_CUDA(cudaMemsetAsync(dsmall, 0, 16 * sizeof(unsigned long long), s));
   NXS_CUDA(cudaMemsetAsync(v->active.p, 1, (size_t)n_tiles, s));
 
   // ---- depth phases [R_p, R_{p+1}): R_1 = first phase, then x8
@@ -373,31 +384,56 @@ int nxs_forward(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
     if (R[n_ph] < P) R[++n_ph] = P;
   }
 
+  // depth order: 32-bit monotone keys + exact fix-up of equal-key runs;
+  // the 64-bit sort is the fallback when a run is too long (retry below)
+  bool sort64 = false;
+retry_sort:
   mark(v, 0, s);
   if (P > 0) {
     size_t tmp_sort = 0, tmp_scan = 0;
-    NXS_CUDA(cub::DeviceRadixSort::SortPairs(
-        nullptr, tmp_sort, v->dkeys_in.as<unsigned long long>(),
-        v->dkeys_out.as<unsigned long long>(), v->idx_in.as<uint32_t>(),
-        v->idx_out.as<uint32_t>(), (int)P, 0, 64, s));
+    if (sort64)
+      NXS_CUDA(cub::DeviceRadixSort::SortPairs(
+          nullptr, tmp_sort, v->dkeys_in.as<unsigned long long>(),
+          v->dkeys_out.as<unsigned long long>(), v->idx_in.as<uint32_t>(),
+          v->idx_out.as<uint32_t>(), (int)P, 0, 64, s));
+    else
+      NXS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_sort, v->k32a.as<uint32_t>(),
+                                               v->k32b.as<uint32_t>(), v->idx_in.as<uint32_t>(),
+                                               v->idx_out.as<uint32_t>(), (int)P, 0, 32, s));
     NXS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_scan,
                                            v->ntiles.as<unsigned long long>(),
                                            v->offsets.as<unsigned long long>(), (int)P, s));
     NXS_CUDA(v->temp.ensure(std::max(tmp_sort, tmp_scan)));
-    // ---- K0 + depth sort
-    launch_depth_keys(scene->centers, P, cam, v->dkeys_in.as<unsigned long long>(),
-                      v->idx_in.as<uint32_t>(), s);
-    NXS_LAUNCHED("depth_keys");
+    // ---- K0 depth (+ min/max) and the stable depth sort
+    NXS_CUDA(cudaMemsetAsync(dsmall + 6, 0xff, sizeof(unsigned long long), s));
+    NXS_CUDA(cudaMemsetAsync(dsmall + 7, 0, 2 * sizeof(unsigned long long), s));
+    launch_depth(scene->centers, P, cam, v->depth.as<double>(),
+                 v->dkeys_in.as<unsigned long long>(), v->idx_in.as<uint32_t>(), dsmall + 6, s);
+    NXS_LAUNCHED("depth");
     size_t tb = v->temp.cap;
-    NXS_CUDA(cub::DeviceRadixSort::SortPairs(
-        v->temp.p, tb, v->dkeys_in.as<unsigned long long>(), v->dkeys_out.as<unsigned long long>(),
-        v->idx_in.as<uint32_t>(), v->idx_out.as<uint32_t>(), (int)P, 0, 64, s));
+    if (sort64) {
+      NXS_CUDA(cub::DeviceRadixSort::SortPairs(
+          v->temp.p, tb, v->dkeys_in.as<unsigned long long>(),
+          v->dkeys_out.as<unsigned long long>(), v->idx_in.as<uint32_t>(),
+          v->idx_out.as<uint32_t>(), (int)P, 0, 64, s));
+    } else {
+      launch_key32(v->depth.as<double>(), P, dsmall + 6, v->k32a.as<uint32_t>(), s);
+      NXS_LAUNCHED("key32");
+      NXS_CUDA(cub::DeviceRadixSort::SortPairs(v->temp.p, tb, v->k32a.as<uint32_t>(),
+                                               v->k32b.as<uint32_t>(), v->idx_in.as<uint32_t>(),
+                                               v->idx_out.as<uint32_t>(), (int)P, 0, 32, s));
+      launch_key_fixup(v->k32b.as<uint32_t>(), v->idx_out.as<uint32_t>(), v->depth.as<double>(),
+                       P, dsmall + 8, s);
+      NXS_LAUNCHED("key_fixup");
+    }
+    launch_rank_of(v->idx_out.as<uint32_t>(), P, v->rank_of.as<uint32_t>(), s);
+    NXS_LAUNCHED("rank_of");
   }
   mark(v, 1, s);
   if (P > 0) {
-    // ---- K1 projection (all ranks: records, tile rectangles)
+    // ---- K1 projection (all Gaussians, storage order; records land at their rank)
     launch_project(scene->centers, scene->scales, scene->quats, scene->opacities, scene->sh, C, P,
-                   v->idx_out.as<uint32_t>(), cam, opts->alpha_cutoff, opts->near_plane,
+                   v->rank_of.as<uint32_t>(), cam, opts->alpha_cutoff, opts->near_plane,
                    v->ntiles.as<unsigned long long>(), v->rects.as<int4>(),
                    v->records.as<float4>(), v->bframe.as<float4>(), dsmall, s);
     NXS_LAUNCHED("project");
@@ -432,7 +468,16 @@ int nxs_forward(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
                              cudaMemcpyDeviceToHost, s));
     NXS_CUDA(cudaMemcpyAsync(v->host_small + 3, n_active, sizeof(unsigned int),
                              cudaMemcpyDeviceToHost, s));
+    if (ph == 0)
+      NXS_CUDA(cudaMemcpyAsync(v->host_small + 6, dsmall + 8, sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, s));
     NXS_CUDA(cudaStreamSynchronize(s));
+    if (ph == 0 && !sort64 && v->host_small[6] != 0) {
+      // an equal-key run longer than the fix-up handles: redo with 64-bit keys
+      sort64 = true;
+      NXS_CUDA(cudaMemsetAsync(dsmall, 0, 16 * sizeof(unsigned long long), s));
+      goto retry_sort;
+    }
     if (ph == 0) mark(v, 3, s);
     const unsigned long long n_pairs = v->host_small[0] + v->host_small[1];
     v->stats.n_straddling = (int64_t)v->host_small[2];
@@ -533,9 +578,18 @@ int nxs_backward(nxs_view* v, const nxs_scene* scene, const float* seed, float* 
   cudaStream_t s = (cudaStream_t)stream_;
   const int64_t P = v->P;
   if (P == 0) return NXS_OK;
-  NXS_CUDA(ensure_n<double>(v->moments, P * NMOM));
   mark(v, 8, s);
-  NXS_CUDA(cudaMemsetAsync(v->moments.p, 0, (size_t)P * NMOM * sizeof(double), s));
+  {
+    // moments/touched stay zero between backwards (K5 re-zeroes what it
+    // reads); clear only freshly allocated buffers
+    void* mp = v->moments.p;
+    void* tp = v->touched.p;
+    NXS_CUDA(ensure_n<double>(v->moments, P * NMOM));
+    NXS_CUDA(ensure_n<uint8_t>(v->touched, P));
+    if (v->moments.p != mp)
+      NXS_CUDA(cudaMemsetAsync(v->moments.p, 0, v->moments.cap, s));
+    if (v->touched.p != tp) NXS_CUDA(cudaMemsetAsync(v->touched.p, 0, v->touched.cap, s));
+  }
   mark(v, 9, s);
   const bool count = (v->opts.flags & NXS_FLAG_COUNT_EVENTS) != 0;
   unsigned long long* dsmall = v->dev_small.as<unsigned long long>();
@@ -549,11 +603,12 @@ int nxs_backward(nxs_view* v, const nxs_scene* scene, const float* seed, float* 
   }
   launch_blend_bwd(count, v->n_tiles, v->records.as<float4>(), v->bframe.as<float4>(), lists,
                    v->cam, v->model, (float)v->opts.alpha_cutoff, v->opts.near_plane, v->bg, seed,
-                   v->cache(), v->moments.as<double>(), cnt, s);
+                   v->cache(), v->moments.as<double>(), v->touched.as<uint8_t>(), cnt, s);
   NXS_LAUNCHED("blend_bwd");
   mark(v, 10, s);
   launch_chain(scene->scales, scene->quats, v->C, P, v->idx_out.as<uint32_t>(),
-               v->moments.as<double>(), g_centers, g_scales, g_quats, g_opacities, g_sh, s);
+               v->moments.as<double>(), v->touched.as<uint8_t>(), g_centers, g_scales, g_quats,
+               g_opacities, g_sh, s);
   NXS_LAUNCHED("chain");
   mark(v, 11, s);
   v->ev_bwd = true;

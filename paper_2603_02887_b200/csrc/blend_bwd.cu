@@ -86,7 +86,7 @@ __device__ __forceinline__ bool bwd_pixel(BwdPix& st, const float4* rec, const f
     // state in front of splat i, recovered back to front
     if constexpr (FAM != FAM_EXP) df_add(st.thi, st.tlo, -alpha);
     if constexpr (IsPFam<FAM>::value) {
-      st.P = (idx == st.ck) ? st.Pck : __fdiv_rn(st.P, __fsub_rn(1.0f, alpha));
+      st.P = (idx == st.ck) ? st.Pck : div_newton(st.P, __fsub_rn(1.0f, alpha));
     }
     float fp;
     const float g = weight_g<FAM>(m, st.thi, st.tlo, st.P, fp);
@@ -123,7 +123,7 @@ __device__ __forceinline__ bool bwd_pixel(BwdPix& st, const float4* rec, const f
       const float dxn = t.ddx * inv_f, dyn = t.ddy * inv_f;
       const float Ahx = r2.x * t.u;
       const float Ahy = fmaf(r2.x * r2.y, t.u, r2.w * t.v);
-      const float eps = __fdividef(fmaf(dxn, Ahx, dyn * Ahy), t.D);
+      const float eps = fmaf(dxn, Ahx, dyn * Ahy) * t.rD;
       qx = fmaf(-eps, st.pc.hx, dxn);
       qy = fmaf(-eps, st.pc.hy, dyn);
       qz = -eps;
@@ -177,7 +177,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 4)
     k_blend_bwd(const float4* __restrict__ records, const float4* __restrict__ bframe,
                 PhaseLists lists, CamDev cam, ModelDev m, float cutoff, double near_plane,
                 float bg0, float bg1, float bg2, const float* __restrict__ seed, PixCache cache,
-                double* __restrict__ moments, Counters* __restrict__ cnt) {
+                double* __restrict__ moments, uint8_t* __restrict__ touched,
+                Counters* __restrict__ cnt) {
   extern __shared__ float4 smem_dyn[];
   float4(*s_rec)[REC_F4] = reinterpret_cast<float4(*)[REC_F4]>(smem_dyn);
   float4(*s_bf)[3] = reinterpret_cast<float4(*)[3]>(smem_dyn + BWD_BATCH * REC_F4);
@@ -293,6 +294,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 4)
         if (val != 0.f) {
           const int e = k / NMOM;
           atomicAdd(&moments[(size_t)s_rank[e] * NMOM + (k - e * NMOM)], (double)val);
+          touched[s_rank[e]] = 1;  // K5 reads (and re-zeroes) touched ranks only
         }
       }
     }
@@ -316,8 +318,8 @@ template <int FAM>
 static void launch_bwd_fam(bool count, int n_tiles, const float4* records, const float4* bframe,
                            const PhaseLists& lists, const CamDev& cam, const ModelDev& m,
                            float cutoff, double near_plane, const float* bg, const float* seed,
-                           const PixCache& cache, double* moments, Counters* cnt,
-                           cudaStream_t s) {
+                           const PixCache& cache, double* moments, uint8_t* touched,
+                           Counters* cnt, cudaStream_t s) {
   static bool attr_set = false;  // host-side, once per instantiation
   if (!attr_set) {
     for (auto k : {k_blend_bwd<FAM, true>, k_blend_bwd<FAM, false>}) {
@@ -329,17 +331,18 @@ static void launch_bwd_fam(bool count, int n_tiles, const float4* records, const
   }
   auto k = count ? k_blend_bwd<FAM, true> : k_blend_bwd<FAM, false>;
   k<<<n_tiles, BWD_THREADS, BWD_SMEM, s>>>(records, bframe, lists, cam, m, cutoff, near_plane, bg[0],
-                                        bg[1], bg[2], seed, cache, moments, cnt);
+                                        bg[1], bg[2], seed, cache, moments, touched, cnt);
 }
 
 void launch_blend_bwd(bool count, int n_tiles, const float4* records, const float4* bframe,
                       const PhaseLists& lists, const CamDev& cam, const ModelDev& m,
                       float cutoff, double near_plane, const float* bg, const float* seed,
-                      const PixCache& cache, double* moments, Counters* cnt, cudaStream_t s) {
+                      const PixCache& cache, double* moments, uint8_t* touched, Counters* cnt,
+                      cudaStream_t s) {
   if (n_tiles == 0) return;
 #define NXS_BWD(F) \
   launch_bwd_fam<F>(count, n_tiles, records, bframe, lists, cam, m, cutoff, near_plane, bg, seed, \
-                    cache, moments, cnt, s)
+                    cache, moments, touched, cnt, s)
   switch (m.fam) {
     case FAM_EXP: NXS_BWD(FAM_EXP); break;
     case FAM_LIN: NXS_BWD(FAM_LIN); break;

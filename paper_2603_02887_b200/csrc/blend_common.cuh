@@ -43,6 +43,7 @@ __device__ __forceinline__ PixelConst pixel_setup(const CamDev& cam, int px, int
 struct TestOut {
   float ddx, ddy;  // Δ in pixels
   float D;         // hᵀ A' h
+  float rD;        // rcp.approx(D), shared by m2 and the backward's ε
   float u, v;      // D = a·u² + d·v² + g  (so (A'h)_x = a·u, (A'h)_y = a·b·u + d·v)
   float m2;        // Mahalanobis distance² at the ray peak
   float kern;      // exp(-m2/2)
@@ -65,7 +66,8 @@ __device__ __forceinline__ bool ray_peak_test(const float4& r0, const float4& r1
   o.D = __fmaf_rn(__fmul_rn(r2.x, u), u, __fmaf_rn(__fmul_rn(r2.w, v), v, r3.y));
   // cheap reject against the cutoff ellipse (r2m carries a 1e-4 margin)
   if (num > __fmul_rn(r1.w, o.D)) return false;
-  o.m2 = __fdividef(num, o.D);
+  o.rD = rcp_approx(o.D);
+  o.m2 = __fmul_rn(num, o.rD);
   o.kern = ex2_approx(__fmul_rn(-0.72134752044448170368f, o.m2));  // e^{-m2/2}
   o.araw = __fmul_rn(r3.z, o.kern);
   o.alpha = fminf(o.araw, ALPHA_MAX_F);
@@ -110,6 +112,7 @@ __device__ __forceinline__ bool general_test(const float4* rec, const CamDev& ca
                              NXS_DOT3(A01, A11, A12, x0, x1, x2), NXS_DOT3(A02, A12, A22, x0, x1, x2));
 #undef NXS_DOT3
   o.m2 = (float)m2;
+  o.rD = 0.f;
   o.kern = ex2_approx(__fmul_rn(-0.72134752044448170368f, o.m2));
   o.araw = __fmul_rn(opac, o.kern);
   o.alpha = fminf(o.araw, ALPHA_MAX_F);

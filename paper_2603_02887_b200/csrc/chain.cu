@@ -1,4 +1,6 @@
-// K5: per-Gaussian moments -> parameter gradients, fp64.
+// K5: per-Gaussian moments -> parameter gradients, fp64.  Only ranks the
+// backward touched are read; their moments are re-zeroed here, so the
+// buffer is clean for the next backward without a separate clear.
 //
 // Replaces the reference chain (pkg/src/nexsplat/render.py:326-341, with
 // quat_rot_jacobian primitives.py:67-93).  K4 accumulated per rank, in the
@@ -19,20 +21,21 @@ namespace nxs {
 
 __global__ void k_chain(const float* __restrict__ scales, const float* __restrict__ quats, int C,
                         int64_t P, const uint32_t* __restrict__ order,
-                        const double* __restrict__ moments, float* __restrict__ g_centers,
+                        double* __restrict__ moments, uint8_t* __restrict__ touched,
+                        float* __restrict__ g_centers,
                         float* __restrict__ g_scales, float* __restrict__ g_quats,
                         float* __restrict__ g_opac, float* __restrict__ g_sh) {
   int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= P) return;
-  const double* mm = moments + r * NMOM;
+  if (r >= P || !touched[r]) return;
+  // read this rank's moments and leave the buffer zeroed for the next backward
+  double* mm = moments + r * NMOM;
   double mv[NMOM];
-  bool any = false;
 #pragma unroll
   for (int k = 0; k < NMOM; ++k) {
     mv[k] = mm[k];
-    any |= (mv[k] != 0.0);
+    mm[k] = 0.0;
   }
-  if (!any) return;
+  touched[r] = 0;
   const int64_t g = order[r];
 
   // opacity and SH need no geometry
@@ -95,10 +98,10 @@ __global__ void k_chain(const float* __restrict__ scales, const float* __restric
 }
 
 void launch_chain(const float* scales, const float* quats, int C, int64_t P, const uint32_t* order,
-                  const double* moments, float* g_centers, float* g_scales, float* g_quats,
-                  float* g_opac, float* g_sh, cudaStream_t s) {
+                  double* moments, uint8_t* touched, float* g_centers, float* g_scales,
+                  float* g_quats, float* g_opac, float* g_sh, cudaStream_t s) {
   if (P == 0) return;
-  k_chain<<<(unsigned)((P + 127) / 128), 128, 0, s>>>(scales, quats, C, P, order, moments,
+  k_chain<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(scales, quats, C, P, order, moments, touched,
                                                       g_centers, g_scales, g_quats, g_opac, g_sh);
 }
 

@@ -166,6 +166,13 @@ __device__ __forceinline__ float rcp_approx(float x) {
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// a / b within ~1 ulp: approximate reciprocal plus one Newton step on the
+// quotient (no IEEE-division slow path); b in normal range
+__device__ __forceinline__ float div_newton(float a, float b) {
+  const float r = rcp_approx(b);
+  const float q = a * r;
+  return fmaf(fmaf(-q, b, a), r, q);
+}
 
 // ---------------------------------------------------------------------------
 // transmittance weights p̄ = α·g  (reference transmittance.py:234-262)

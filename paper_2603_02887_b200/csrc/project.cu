@@ -68,20 +68,119 @@ __device__ __forceinline__ double dot3_compensated(double a0, double a1, double 
   return p + s;
 }
 
-// K0: fp64 view depth (μ - o)·forward -> order-preserving u64 key.
-__global__ void k_depth_keys(const float* __restrict__ centers, int64_t P, CamDev cam,
-                             unsigned long long* __restrict__ keys,
-                             uint32_t* __restrict__ idx) {
+__device__ __forceinline__ unsigned long long dkey(double d) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(d);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double dkey_inv(unsigned long long k) {
+  const unsigned long long u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double((long long)u);
+}
+
+// K0: fp64 view depth (μ - o)·forward (compensated), its order-preserving
+// u64 key (64-bit fallback sort), and the NaN-free min/max key of the batch.
+__global__ void k_depth(const float* __restrict__ centers, int64_t P, CamDev cam,
+                        double* __restrict__ depth, unsigned long long* __restrict__ key64,
+                        uint32_t* __restrict__ idx, unsigned long long* __restrict__ kminmax) {
+  __shared__ unsigned long long s_min[8], s_max[8];
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long kmin = ~0ull, kmax = 0ull;
+  if (i < P) {
+    double b0 = (double)centers[3 * i + 0] - cam.o[0];
+    double b1 = (double)centers[3 * i + 1] - cam.o[1];
+    double b2 = (double)centers[3 * i + 2] - cam.o[2];
+    // forward = third column of the camera rotation
+    const double d = dot3_compensated(b0, b1, b2, cam.R[2], cam.R[5], cam.R[8]);
+    depth[i] = d;
+    const unsigned long long k = dkey(d);
+    key64[i] = k;
+    idx[i] = (uint32_t)i;
+    if (d == d) {
+      kmin = k;
+      kmax = k;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+    kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    s_min[w] = kmin;
+    s_max[w] = kmax;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
+      kmin = min(kmin, s_min[k]);
+      kmax = max(kmax, s_max[k]);
+    }
+    if (kmin <= kmax) {
+      atomicMin(&kminmax[0], kmin);
+      atomicMax(&kminmax[1], kmax);
+    }
+  }
+}
+
+// 32-bit monotone key: floor((d - dmin) * (2^32 - 2) / (dmax - dmin)); NaN last.
+// d1 < d2 implies key(d1) <= key(d2); equal keys are re-ordered by k_key_fixup.
+__global__ void k_key32(const double* __restrict__ depth, int64_t P,
+                        const unsigned long long* __restrict__ kminmax,
+                        uint32_t* __restrict__ key) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P) return;
-  double b0 = (double)centers[3 * i + 0] - cam.o[0];
-  double b1 = (double)centers[3 * i + 1] - cam.o[1];
-  double b2 = (double)centers[3 * i + 2] - cam.o[2];
-  // forward = third column of the camera rotation
-  double depth = dot3_compensated(b0, b1, b2, cam.R[2], cam.R[5], cam.R[8]);
-  unsigned long long u = (unsigned long long)__double_as_longlong(depth);
-  keys[i] = (u >> 63) ? ~u : (u | 0x8000000000000000ull);
-  idx[i] = (uint32_t)i;
+  const double d = depth[i];
+  uint32_t k = 0u;
+  if (!(d == d)) {
+    k = 0xffffffffu;
+  } else if (kminmax[0] < kminmax[1]) {
+    const double lo = dkey_inv(kminmax[0]), hi = dkey_inv(kminmax[1]);
+    double x = (d - lo) * (4294967294.0 / (hi - lo));
+    x = x < 0.0 ? 0.0 : (x > 4294967294.0 ? 4294967294.0 : x);
+    k = (uint32_t)x;
+  }
+  key[i] = k;
+}
+
+// Runs of equal 32-bit keys come out of the stable sort in index order;
+// re-sort each run by (fp64 depth, index) — exactly the 64-bit order.
+// Runs longer than 256 raise `overflow` (the host then redoes the 64-bit sort).
+__global__ void k_key_fixup(const uint32_t* __restrict__ key, uint32_t* __restrict__ idx,
+                            const double* __restrict__ depth, int64_t P,
+                            unsigned long long* __restrict__ overflow) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  const uint32_t k = key[i];
+  if (i > 0 && key[i - 1] == k) return;         // not a run start
+  if (i + 1 >= P || key[i + 1] != k) return;    // singleton
+  int64_t e = i + 1;
+  while (e < P && key[e] == k && e - i <= 256) ++e;
+  if (e - i > 256) {
+    atomicAdd(overflow, 1ull);
+    return;
+  }
+  for (int64_t a = i + 1; a < e; ++a) {  // insertion sort, stable by index
+    const uint32_t v = idx[a];
+    const double dv = depth[v];
+    int64_t b = a - 1;
+    while (b >= i) {
+      const uint32_t w = idx[b];
+      const double dw = depth[w];
+      if (dw > dv || (dw == dv && w > v) || (!(dw == dw) && (dv == dv))) {
+        idx[b + 1] = w;
+        --b;
+      } else {
+        break;
+      }
+    }
+    idx[b + 1] = v;
+  }
+}
+
+__global__ void k_rank_of(const uint32_t* __restrict__ order, int64_t P,
+                          uint32_t* __restrict__ rank_of) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < P) rank_of[order[r]] = (uint32_t)r;
 }
 
 struct ProjOut {
@@ -96,11 +195,13 @@ struct ProjOut {
 __global__ void k_project(const float* __restrict__ centers, const float* __restrict__ scales,
                           const float* __restrict__ quats, const float* __restrict__ opacities,
                           const float* __restrict__ sh, int C, int64_t P,
-                          const uint32_t* __restrict__ order, CamDev cam, double cutoff,
+                          const uint32_t* __restrict__ rank_of, CamDev cam, double cutoff,
                           double near_plane, ProjOut out) {
-  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= P) return;
-  const int64_t g = order[r];
+  // one thread per Gaussian in storage order (coalesced parameter reads);
+  // the 128-B record is written to its depth-rank slot
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= P) return;
+  const int64_t r = rank_of[g];
 
   // --- rotation from the normalised quaternion (primitives.py:45-64)
   double qw = quats[4 * g + 0], qx = quats[4 * g + 1], qy = quats[4 * g + 2],
@@ -331,21 +432,36 @@ __global__ void k_tile_ranges(const uint32_t* __restrict__ keys, int64_t n,
 }
 
 // host launchers
-void launch_depth_keys(const float* centers, int64_t P, const CamDev& cam,
-                       unsigned long long* keys, uint32_t* idx, cudaStream_t s) {
+void launch_depth(const float* centers, int64_t P, const CamDev& cam, double* depth,
+                  unsigned long long* key64, uint32_t* idx, unsigned long long* kminmax,
+                  cudaStream_t s) {
   if (P == 0) return;
-  k_depth_keys<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(centers, P, cam, keys, idx);
+  k_depth<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(centers, P, cam, depth, key64, idx, kminmax);
+}
+void launch_key32(const double* depth, int64_t P, const unsigned long long* kminmax,
+                  uint32_t* key, cudaStream_t s) {
+  if (P == 0) return;
+  k_key32<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(depth, P, kminmax, key);
+}
+void launch_key_fixup(const uint32_t* key, uint32_t* idx, const double* depth, int64_t P,
+                      unsigned long long* overflow, cudaStream_t s) {
+  if (P == 0) return;
+  k_key_fixup<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(key, idx, depth, P, overflow);
+}
+void launch_rank_of(const uint32_t* order, int64_t P, uint32_t* rank_of, cudaStream_t s) {
+  if (P == 0) return;
+  k_rank_of<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(order, P, rank_of);
 }
 
 void launch_project(const float* centers, const float* scales, const float* quats,
                     const float* opacities, const float* sh, int C, int64_t P,
-                    const uint32_t* order, const CamDev& cam, double cutoff, double near_plane,
+                    const uint32_t* rank_of, const CamDev& cam, double cutoff, double near_plane,
                     unsigned long long* n_tiles, int4* rects, float4* records, float4* bframe,
                     unsigned long long* straddle, cudaStream_t s) {
   if (P == 0) return;
   ProjOut o{n_tiles, rects, records, bframe, straddle};
   k_project<<<(unsigned)((P + 127) / 128), 128, 0, s>>>(centers, scales, quats, opacities, sh, C,
-                                                        P, order, cam, cutoff, near_plane, o);
+                                                        P, rank_of, cam, cutoff, near_plane, o);
 }
 
 void launch_count_active(const int4* rects, int64_t r0, int64_t r1, int tiles_x,

@@ -383,3 +383,25 @@ def test_progressive_binning_is_bit_identical_to_full(name):
             np.testing.assert_allclose(prog["grads"][k], full["grads"][k], rtol=1e-5,
                                        atol=1e-7 * np.abs(full["grads"][k]).max())
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("case", ["equal_depths", "far_outlier", "negative"])
+def test_depth_order_edge_cases_match_c_restatement(case):
+    """32-bit depth keys + exact run fix-up (and the 64-bit fallback when a
+    far outlier collapses everything into one key) give exactly the
+    (fp64 depth, index) order of the C restatement."""
+    sc = O.round_scene_f32(O.canonical_scene(20_000, seed=3))
+    cen = sc.centers.copy()
+    if case == "equal_depths":
+        cen[::3, 2] = 4.0  # thousands of exactly equal depths, camera looks along +z
+    elif case == "far_outlier":
+        cen[7] = [0.0, 0.0, 1e30]
+    else:
+        cen[::5, 2] *= -1.0  # behind the camera
+    sc = O.Scene(np.asarray(cen, np.float32).astype(np.float64), sc.scales, sc.quats,
+                 sc.opacities, sc.sh)
+    cam = O.canonical_camera(128, 96)
+    got = gpu_run(sc, cam, MODELS["linear"], np.zeros(3))
+    order, *_ = _binning_of(got["view"], len(sc))
+    ref = oracle.binning(sc, cam)
+    np.testing.assert_array_equal(order, ref["order"])
