@@ -202,10 +202,29 @@ __global__ void k_project(const float* __restrict__ centers, const float* __rest
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= P) return;
   const int64_t r = rank_of[g];
+  // every parameter load is issued up front (16-B vector loads where the
+  // layout allows), before any record store could alias them
+  const float4 q4 = reinterpret_cast<const float4*>(quats)[g];
+  const float cx0 = centers[3 * g + 0], cx1 = centers[3 * g + 1], cx2 = centers[3 * g + 2];
+  const float sc0 = scales[3 * g + 0], sc1 = scales[3 * g + 1], sc2 = scales[3 * g + 2];
+  const float op = opacities[g];
+  float shv[12];
+  if (C == 4) {
+    const float4* s4 = reinterpret_cast<const float4*>(sh) + 3 * g;
+    const float4 a = s4[0], b = s4[1], c = s4[2];
+    shv[0] = a.x; shv[1] = a.y; shv[2] = a.z; shv[3] = a.w;
+    shv[4] = b.x; shv[5] = b.y; shv[6] = b.z; shv[7] = b.w;
+    shv[8] = c.x; shv[9] = c.y; shv[10] = c.z; shv[11] = c.w;
+  } else {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      shv[4 * c] = sh[3 * g + c];
+      shv[4 * c + 1] = shv[4 * c + 2] = shv[4 * c + 3] = 0.0f;
+    }
+  }
 
   // --- rotation from the normalised quaternion (primitives.py:45-64)
-  double qw = quats[4 * g + 0], qx = quats[4 * g + 1], qy = quats[4 * g + 2],
-         qz = quats[4 * g + 3];
+  double qw = q4.x, qx = q4.y, qy = q4.z, qz = q4.w;
   double nq = sqrt(((qw * qw + qx * qx) + qy * qy) + qz * qz);
   double w = qw / nq, x = qx / nq, y = qy / nq, z = qz / nq;
   double R[9];
@@ -227,7 +246,7 @@ __global__ void k_project(const float* __restrict__ centers, const float* __rest
     for (int j = 0; j < 3; ++j)
       M[3 * i + j] = (cam.R[0 + i] * R[0 + j] + cam.R[3 + i] * R[3 + j]) + cam.R[6 + i] * R[6 + j];
 
-  double s0 = scales[3 * g + 0], s1 = scales[3 * g + 1], s2 = scales[3 * g + 2];
+  double s0 = sc0, s1 = sc1, s2 = sc2;
   double is0 = 1.0 / (s0 * s0), is1 = 1.0 / (s1 * s1), is2 = 1.0 / (s2 * s2);
   // A' = M diag(1/s^2) M^T  (camera-frame inverse covariance)
   double Ap[9];
@@ -242,9 +261,9 @@ __global__ void k_project(const float* __restrict__ centers, const float* __rest
     }
 
   // b' = Rc^T (μ - o)
-  double b0 = (double)centers[3 * g + 0] - cam.o[0];
-  double b1 = (double)centers[3 * g + 1] - cam.o[1];
-  double b2 = (double)centers[3 * g + 2] - cam.o[2];
+  double b0 = (double)cx0 - cam.o[0];
+  double b1 = (double)cx1 - cam.o[1];
+  double b2 = (double)cx2 - cam.o[2];
   double bp[3];
 #pragma unroll
   for (int i = 0; i < 3; ++i) bp[i] = (cam.R[0 + i] * b0 + cam.R[3 + i] * b1) + cam.R[6 + i] * b2;
@@ -264,7 +283,7 @@ __global__ void k_project(const float* __restrict__ centers, const float* __rest
   int4 rect = make_int4(-1, -1, -1, -1);
   unsigned long long ntile = 0;
 
-  double opac = (double)opacities[g];
+  double opac = (double)op;
   bool live = opac >= cutoff;
   // cutoff ellipsoid radius (Mahalanobis), with the bbox/pre-test margin
   double r2 = live ? 2.0 * ln_det(opac / cutoff) : 0.0;
@@ -361,11 +380,6 @@ __global__ void k_project(const float* __restrict__ centers, const float* __rest
     rec[2] = make_float4((float)a, (float)bb, (float)cc, (float)d);
     rec[3] = make_float4((float)e, (float)gg, (float)opac, __int_as_float(RF_CONIC));
   }
-  float shv[12];
-#pragma unroll
-  for (int c = 0; c < 3; ++c)
-#pragma unroll
-    for (int k = 0; k < 4; ++k) shv[4 * c + k] = (k < C) ? sh[(g * 3 + c) * C + k] : 0.0f;
   rec[4] = make_float4(shv[0], shv[1], shv[2], shv[3]);
   rec[5] = make_float4(shv[4], shv[5], shv[6], shv[7]);
   rec[6] = make_float4(shv[8], shv[9], shv[10], shv[11]);

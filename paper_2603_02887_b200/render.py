@@ -129,8 +129,7 @@ class DeviceScene:
         def up(x, shape):
             if isinstance(x, torch.Tensor):
                 return x.to(device=dev, dtype=torch.float32).reshape(shape)
-            a = np.ascontiguousarray(np.asarray(x, dtype=np.float32).reshape(shape))
-            return torch.from_numpy(a).to(dev, non_blocking=non_blocking)
+            return _h2d_f32(np.asarray(x).reshape(shape), dev)
 
         n = len(arrs.opacities)
         sh = arrs.sh
@@ -140,6 +139,42 @@ class DeviceScene:
 
     def __len__(self):
         return self.count
+
+
+# --- host <-> device staging for the numpy API ------------------------------
+# float64 numpy in, float64 numpy out (the reference's types).  Conversions run
+# multi-threaded inside torch into cached page-locked float32 buffers, and the
+# PCIe copies are asynchronous from/to those buffers.
+_PINNED: dict = {}
+
+
+def _pinned(key, shape, dtype):
+    import torch
+    t = _PINNED.get(key)
+    if t is None or t.shape != tuple(shape) or t.dtype != dtype:
+        t = torch.empty(tuple(shape), dtype=dtype, pin_memory=True)
+        _PINNED[key] = t
+    return t
+
+
+def _h2d_f32(a: np.ndarray, dev):
+    import torch
+    src = torch.from_numpy(np.ascontiguousarray(a))
+    stage = _pinned(("h2d", a.shape), a.shape, torch.float32)
+    torch.cuda.current_stream(dev).synchronize()  # stage may still feed an earlier copy
+    stage.copy_(src)
+    return stage.to(dev, non_blocking=True)
+
+
+def _d2h_f64(t, key) -> np.ndarray:
+    """Fresh float64 numpy array from a device tensor (via pinned float32)."""
+    import torch
+    stage = _pinned(("d2h", key), t.shape, t.dtype)
+    stage.copy_(t, non_blocking=True)
+    torch.cuda.current_stream(t.device).synchronize()
+    out = torch.empty(t.shape, dtype=torch.float64 if t.is_floating_point() else torch.int64)
+    out.copy_(stage)
+    return out.numpy()
 
 
 def _as_device_scene(scene) -> DeviceScene:
@@ -313,8 +348,7 @@ class ForwardCache(Mapping):
 
 def _result_to_host(out) -> RenderResult:
     rgb, od, res = out
-    return RenderResult(rgb.double().cpu().numpy(), od.long().cpu().numpy(),
-                        res.double().cpu().numpy())
+    return RenderResult(_d2h_f64(rgb, "rgb"), _d2h_f64(od, "overdraw"), _d2h_f64(res, "residual"))
 
 
 def _settings(camera, model, background, max_splats, alpha_cutoff, near, chunk_size):
@@ -386,11 +420,12 @@ def render_backward(arrs, camera, model, background, cache, seed_image, *,
     H, W = int(camera.height), int(camera.width)
     seed = np.asarray(seed_image, dtype=np.float64).reshape(H, W, 3) if not isinstance(
         seed_image, torch.Tensor) else seed_image
-    seed_t = seed if isinstance(seed, torch.Tensor) else torch.from_numpy(
-        np.ascontiguousarray(seed, dtype=np.float32))
-    seed_t = seed_t.to(device=dev.centers.device, dtype=torch.float32).contiguous()
+    if isinstance(seed, torch.Tensor):
+        seed_t = seed.to(device=dev.centers.device, dtype=torch.float32).contiguous()
+    else:
+        seed_t = _h2d_f32(seed, dev.centers.device)
     g = backward_device(st.view, dev, seed_t)
-    return {k: v.double().cpu().numpy() for k, v in g.items()}
+    return {k: _d2h_f64(v, "g_" + k) for k, v in g.items()}
 
 
 def render_with_gradients(arrs, camera, model, background, seed_image, *,
