@@ -175,8 +175,8 @@ int nxs_cache_export(nxs_view* view, uint8_t* sat, float* e_k, float* t_k,
 int nxs_depth_order(nxs_view* view, int32_t* order, void* stream);
 
 /* Binning of the last forward, for the bit-exact checks against the C
- * restatement (oracle/binning_oracle.c): tile rectangle per rank
- * (P x int32[4] = tx0,ty0,tx1,ty1; empty = -1), and the FIRST depth
+ * restatement (oracle/binning_oracle.c): tile rectangle per Gaussian in
+ * storage order (P x int32[4] = tx0,ty0,tx1,ty1; empty = -1), and the FIRST depth
  * phase's tile ranges (n_tiles x int32[2]) and sorted pair values; with
  * NXS_FLAG_FULL_BINNING that phase holds every rank (n_pairs ranks). */
 int nxs_binning_export(nxs_view* view, int32_t* rects, int32_t* ranges,

@@ -125,7 +125,8 @@ int64_t nxs_oracle_binning(int64_t P, const float* centers, const float* scales,
     double qw = quats[4 * g + 0], qx = quats[4 * g + 1], qy = quats[4 * g + 2],
            qz = quats[4 * g + 3];
     double nq = sqrt(((qw * qw + qx * qx) + qy * qy) + qz * qz);
-    double w = qw / nq, x = qx / nq, y = qy / nq, z = qz / nq;
+    double inq = 1.0 / nq;
+    double w = qw * inq, x = qx * inq, y = qy * inq, z = qz * inq;
     double R[9] = {1.0 - 2.0 * (y * y + z * z), 2.0 * (x * y - w * z), 2.0 * (x * z + w * y),
                    2.0 * (x * y + w * z),       1.0 - 2.0 * (x * x + z * z), 2.0 * (y * z - w * x),
                    2.0 * (x * z - w * y),       2.0 * (y * z + w * x), 1.0 - 2.0 * (x * x + y * y)};
@@ -168,13 +169,15 @@ int64_t nxs_oracle_binning(int64_t P, const float* centers, const float* scales,
       live = 0;
     }
     double f2 = f * f;
-    double Np00 = N[0] / f2, Np01 = N[1] / f2, Np11 = N[4] / f2;
+    double if2 = 1.0 / f2;
+    double Np00 = N[0] * if2, Np01 = N[1] * if2, Np11 = N[4] * if2;
     double n0 = Np00, kk = Np01 / Np00, n1 = Np11 - Np01 * kk;
-    double ccx = cx + f * (bp[0] / bp[2]);
-    double ccy = cy + f * (bp[1] / bp[2]);
+    double ibz = 1.0 / bp[2];
+    double ccx = cx + f * (bp[0] * ibz);
+    double ccy = cy + f * (bp[1] * ibz);
     float cxh = (float)ccx, cyh = (float)ccy;
     float cxl = (float)(ccx - (double)cxh), cyl = (float)(ccy - (double)cyh);
-    double a = Ap[0], bb = Ap[1] / a, cc = Ap[2] / a;
+    double a = Ap[0], ia = 1.0 / a, bb = Ap[1] * ia, cc = Ap[2] * ia;
     double A11s = Ap[4] - Ap[1] * bb, A12s = Ap[5] - Ap[1] * cc, A22s = Ap[8] - Ap[2] * cc;
     double d = A11s, e = A12s / d, gg = A22s - A12s * e;
     if (live) {
@@ -190,8 +193,9 @@ int64_t nxs_oracle_binning(int64_t P, const float* centers, const float* scales,
       double jlo = 0.0, jhi = (double)(W - 1), ilo = 0.0, ihi = (double)(H - 1);
       if ((dx >= 0.0) && (dy >= 0.0) && (S22 != 0.0)) {
         double sx = sqrt(dx), sy = sqrt(dy);
-        double x1 = (S02 - sx) / S22, x2 = (S02 + sx) / S22;
-        double y1 = (S12 - sy) / S22, y2 = (S12 + sy) / S22;
+        double iS = 1.0 / S22;
+        double x1 = (S02 - sx) * iS, x2 = (S02 + sx) * iS;
+        double y1 = (S12 - sy) * iS, y2 = (S12 + sy) * iS;
         double xl = x1 < x2 ? x1 : x2, xh = x1 < x2 ? x2 : x1;
         double yl = y1 < y2 ? y1 : y2, yh = y1 < y2 ? y2 : y1;
         double pjl = ceil((cx + f * xl) - 0.5), pjh = floor((cx + f * xh) - 0.5);

@@ -28,10 +28,10 @@ void launch_rank_of(const uint32_t*, int64_t, uint32_t*, cudaStream_t);
 void launch_project(const float*, const float*, const float*, const float*, const float*, int,
                     int64_t, const uint32_t*, const CamDev&, double, double, unsigned long long*,
                     int4*, float4*, float4*, unsigned long long*, cudaStream_t);
-void launch_count_active(const int4*, int64_t, int64_t, int, const uint8_t*, unsigned long long*,
-                         cudaStream_t);
-void launch_emit_pairs(const int4*, const unsigned long long*, int64_t, int64_t, int,
-                       const uint8_t*, uint32_t*, uint32_t*, cudaStream_t);
+void launch_count_active(const int4*, const uint32_t*, int64_t, int64_t, int, const uint8_t*,
+                         unsigned long long*, cudaStream_t);
+void launch_emit_pairs(const int4*, const uint32_t*, const unsigned long long*, int64_t, int64_t,
+                       int, const uint8_t*, uint32_t*, uint32_t*, cudaStream_t);
 void launch_tile_ranges(const uint32_t*, int64_t, int2*, cudaStream_t);
 void launch_blend_fwd(bool, int, const FwdArgs&, const CamDev&, const ModelDev&, const PixCache&,
                       const PixResume&, Counters*, cudaStream_t);
@@ -451,8 +451,8 @@ retry_sort:
     if (v->ev_ok) cudaEventRecord(v->evp[ph][0], s);
     // ---- K2a counts over active tiles, scan, one host sync for the pair count
     if (nr > 0) {
-      launch_count_active(v->rects.as<int4>(), r0, r1, cam.tiles_x, v->active.as<uint8_t>(),
-                          v->ntiles.as<unsigned long long>(), s);
+      launch_count_active(v->rects.as<int4>(), v->idx_out.as<uint32_t>(), r0, r1, cam.tiles_x,
+                          v->active.as<uint8_t>(), v->ntiles.as<unsigned long long>(), s);
       NXS_LAUNCHED("count_active");
       size_t tb = v->temp.cap;
       NXS_CUDA(cub::DeviceScan::ExclusiveSum(v->temp.p, tb, v->ntiles.as<unsigned long long>(),
@@ -501,9 +501,10 @@ retry_sort:
                                                tbits, s));
       NXS_CUDA(v->temp.ensure(tmp_pairs));
       // ---- K2b pairs (rank order), stable sort by tile, ranges
-      launch_emit_pairs(v->rects.as<int4>(), v->offsets.as<unsigned long long>(), r0, r1,
-                        cam.tiles_x, v->active.as<uint8_t>(), v->pk_in.as<uint32_t>(),
-                        v->pv_in.as<uint32_t>(), s);
+      launch_emit_pairs(v->rects.as<int4>(), v->idx_out.as<uint32_t>(),
+                        v->offsets.as<unsigned long long>(), r0, r1, cam.tiles_x,
+                        v->active.as<uint8_t>(), v->pk_in.as<uint32_t>(), v->pv_in.as<uint32_t>(),
+                        s);
       NXS_LAUNCHED("emit_pairs");
       if (ph == 0) mark(v, 4, s);
       size_t tb = v->temp.cap;

@@ -23,20 +23,22 @@ struct PixelConst {
 
 __device__ __forceinline__ PixelConst pixel_setup(const CamDev& cam, int px, int py) {
   PixelConst pc;
-  double hxd = ((double)px + 0.5 - cam.cx) / cam.f;
-  double hyd = ((double)py + 0.5 - cam.cy) / cam.f;
+  const double inv_f = 1.0 / cam.f;  // uniform across the block
+  const double hxd = ((double)px + 0.5 - cam.cx) * inv_f;
+  const double hyd = ((double)py + 0.5 - cam.cy) * inv_f;
   pc.pxc = (float)px + 0.5f;
   pc.pyc = (float)py + 0.5f;
   pc.hx = (float)hxd;
   pc.hy = (float)hyd;
-  // world direction = R (hx, hy, 1), normalised (primitives.py:192-203)
-  double dx = (cam.R[0] * hxd + cam.R[1] * hyd) + cam.R[2];
-  double dy = (cam.R[3] * hxd + cam.R[4] * hyd) + cam.R[5];
-  double dz = (cam.R[6] * hxd + cam.R[7] * hyd) + cam.R[8];
-  double inv = 1.0 / sqrt(dx * dx + dy * dy + dz * dz);
-  pc.Y1 = (float)(-SH_C1 * (dy * inv));
-  pc.Y2 = (float)(SH_C1 * (dz * inv));
-  pc.Y3 = (float)(-SH_C1 * (dx * inv));
+  // world direction = R (hx, hy, 1), normalised (primitives.py:192-203); the
+  // SH basis only needs it to fp32 accuracy
+  const float dx = __fmaf_rn((float)cam.R[0], pc.hx, __fmaf_rn((float)cam.R[1], pc.hy, (float)cam.R[2]));
+  const float dy = __fmaf_rn((float)cam.R[3], pc.hx, __fmaf_rn((float)cam.R[4], pc.hy, (float)cam.R[5]));
+  const float dz = __fmaf_rn((float)cam.R[6], pc.hx, __fmaf_rn((float)cam.R[7], pc.hy, (float)cam.R[8]));
+  const float inv = rsqrtf(__fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz))));
+  pc.Y1 = (float)(-SH_C1) * (dy * inv);
+  pc.Y2 = (float)SH_C1 * (dz * inv);
+  pc.Y3 = (float)(-SH_C1) * (dx * inv);
   return pc;
 }
 

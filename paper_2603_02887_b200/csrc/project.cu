@@ -12,6 +12,8 @@
 //   per-Gaussian part of _chunk_geometry (quat_to_rot, A, b)
 //                                    render.py:116-121, primitives.py:45-64
 // The per-pixel test those records feed is in blend_fwd.cu.
+#include <algorithm>
+
 #include "nxs_internal.cuh"
 
 namespace nxs {
@@ -192,41 +194,28 @@ struct ProjOut {
 };
 
 // K1: per rank r (Gaussian g = order[r]).
-__global__ void k_project(const float* __restrict__ centers, const float* __restrict__ scales,
-                          const float* __restrict__ quats, const float* __restrict__ opacities,
-                          const float* __restrict__ sh, int C, int64_t P,
-                          const uint32_t* __restrict__ rank_of, CamDev cam, double cutoff,
-                          double near_plane, ProjOut out) {
-  // one thread per Gaussian in storage order (coalesced parameter reads);
-  // the 128-B record is written to its depth-rank slot
-  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= P) return;
-  const int64_t r = rank_of[g];
-  // every parameter load is issued up front (16-B vector loads where the
-  // layout allows), before any record store could alias them
-  const float4 q4 = reinterpret_cast<const float4*>(quats)[g];
-  const float cx0 = centers[3 * g + 0], cx1 = centers[3 * g + 1], cx2 = centers[3 * g + 2];
-  const float sc0 = scales[3 * g + 0], sc1 = scales[3 * g + 1], sc2 = scales[3 * g + 2];
-  const float op = opacities[g];
+// Per-Gaussian projection (g = storage index, r = depth rank), parameters
+// already in registers.
+struct GParams {
+  float4 q;
+  float c0, c1, c2, s0, s1, s2, op;
   float shv[12];
-  if (C == 4) {
-    const float4* s4 = reinterpret_cast<const float4*>(sh) + 3 * g;
-    const float4 a = s4[0], b = s4[1], c = s4[2];
-    shv[0] = a.x; shv[1] = a.y; shv[2] = a.z; shv[3] = a.w;
-    shv[4] = b.x; shv[5] = b.y; shv[6] = b.z; shv[7] = b.w;
-    shv[8] = c.x; shv[9] = c.y; shv[10] = c.z; shv[11] = c.w;
-  } else {
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      shv[4 * c] = sh[3 * g + c];
-      shv[4 * c + 1] = shv[4 * c + 2] = shv[4 * c + 3] = 0.0f;
-    }
-  }
+};
+
+__device__ __forceinline__ void project_one(const GParams& prm, int64_t g, const CamDev& cam,
+                                            double cutoff, double near_plane, const ProjOut& out,
+                                            float4* rec, float4* bf) {
+  const float cx0 = prm.c0, cx1 = prm.c1, cx2 = prm.c2;
+  const float sc0 = prm.s0, sc1 = prm.s1, sc2 = prm.s2;
+  const float op = prm.op;
+  const float* shv = prm.shv;
+  const float4 q4 = prm.q;
 
   // --- rotation from the normalised quaternion (primitives.py:45-64)
   double qw = q4.x, qx = q4.y, qy = q4.z, qz = q4.w;
   double nq = sqrt(((qw * qw + qx * qx) + qy * qy) + qz * qz);
-  double w = qw / nq, x = qx / nq, y = qy / nq, z = qz / nq;
+  double inq = 1.0 / nq;
+  double w = qw * inq, x = qx * inq, y = qy * inq, z = qz * inq;
   double R[9];
   R[0] = 1.0 - 2.0 * (y * y + z * z);
   R[1] = 2.0 * (x * y - w * z);
@@ -279,9 +268,7 @@ __global__ void k_project(const float* __restrict__ centers, const float* __rest
 #pragma unroll
     for (int j = 0; j < 3; ++j) N[3 * i + j] = bAb * Ap[3 * i + j] - Ab[i] * Ab[j];
 
-  float4* rec = out.records + r * REC_F4;
   int4 rect = make_int4(-1, -1, -1, -1);
-  unsigned long long ntile = 0;
 
   double opac = (double)op;
   bool live = opac >= cutoff;
@@ -305,13 +292,15 @@ __global__ void k_project(const float* __restrict__ centers, const float* __rest
 
   // --- per-pixel test coefficients (Cholesky-style forms)
   double f = cam.f, f2 = f * f;
-  double Np00 = N[0] / f2, Np01 = N[1] / f2, Np11 = N[4] / f2;
+  double if2 = 1.0 / f2;
+  double Np00 = N[0] * if2, Np01 = N[1] * if2, Np11 = N[4] * if2;
   double n0 = Np00, kk = Np01 / Np00, n1 = Np11 - Np01 * kk;
-  double ccx = cam.cx + f * (bp[0] / bp[2]);
-  double ccy = cam.cy + f * (bp[1] / bp[2]);
+  double ibz = 1.0 / bp[2];
+  double ccx = cam.cx + f * (bp[0] * ibz);
+  double ccy = cam.cy + f * (bp[1] * ibz);
   float cxh = (float)ccx, cyh = (float)ccy;
   float cxl = (float)(ccx - (double)cxh), cyl = (float)(ccy - (double)cyh);
-  double a = Ap[0], bb = Ap[1] / a, cc = Ap[2] / a;
+  double a = Ap[0], ia = 1.0 / a, bb = Ap[1] * ia, cc = Ap[2] * ia;
   double A11s = Ap[4] - Ap[1] * bb, A12s = Ap[5] - Ap[1] * cc, A22s = Ap[8] - Ap[2] * cc;
   double d = A11s, e = A12s / d, gg = A22s - A12s * e;
 
@@ -331,8 +320,9 @@ __global__ void k_project(const float* __restrict__ centers, const float* __rest
     bool ok = (dx >= 0.0) && (dy >= 0.0) && (S22 != 0.0);
     if (ok) {
       double sx = sqrt(dx), sy = sqrt(dy);
-      double x1 = (S02 - sx) / S22, x2 = (S02 + sx) / S22;
-      double y1 = (S12 - sy) / S22, y2 = (S12 + sy) / S22;
+      double iS = 1.0 / S22;
+      double x1 = (S02 - sx) * iS, x2 = (S02 + sx) * iS;
+      double y1 = (S12 - sy) * iS, y2 = (S12 + sy) * iS;
       double xl = x1 < x2 ? x1 : x2, xh = x1 < x2 ? x2 : x1;
       double yl = y1 < y2 ? y1 : y2, yh = y1 < y2 ? y2 : y1;
       double pjl = ceil((cam.cx + f * xl) - 0.5), pjh = floor((cam.cx + f * xh) - 0.5);
@@ -346,13 +336,11 @@ __global__ void k_project(const float* __restrict__ centers, const float* __rest
     if (jlo <= jhi && ilo <= ihi) {
       int j0 = (int)jlo, j1 = (int)jhi, i0 = (int)ilo, i1 = (int)ihi;
       rect = make_int4(j0 / TILE, i0 / TILE, j1 / TILE, i1 / TILE);
-      ntile = (unsigned long long)(rect.z - rect.x + 1) * (unsigned long long)(rect.w - rect.y + 1);
     }
   }
 
   if (general) {
     rect = make_int4(0, 0, cam.tiles_x - 1, cam.tiles_y - 1);
-    ntile = (unsigned long long)cam.tiles_x * (unsigned long long)cam.tiles_y;
     // world-frame A = R diag(s^-2) R^T, b = μ - o (render.py:116-121)
     double A[9];
 #pragma unroll
@@ -388,7 +376,6 @@ __global__ void k_project(const float* __restrict__ centers, const float* __rest
   // B maps the per-pixel peak offset e (conic: camera-frame diff'/b'_z;
   // general: world-frame diff) to the Gaussian frame, u = Rᵀ diff = B e:
   // conic B = b'_z Mᵀ, general B = Rᵀ (used by the backward only)
-  float4* bf = out.bframe + r * 3;
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     if (general)
@@ -397,17 +384,151 @@ __global__ void k_project(const float* __restrict__ centers, const float* __rest
       bf[k] = make_float4((float)(bp[2] * M[0 + k]), (float)(bp[2] * M[3 + k]),
                           (float)(bp[2] * M[6 + k]), 0.f);
   }
-  out.rects[r] = rect;
-  out.n_tiles[r] = ntile;
+  out.rects[g] = rect;  // storage order (coalesced); the binning gathers by rank
+}
+
+// K1: persistent blocks of 128 threads stream chunks of 128 Gaussians'
+// parameters (~12 KB) into shared memory with 16-B cp.async copies, double
+// buffered, so the fp64 projection of one chunk overlaps the loads of the
+// next; the 128-B records land at their depth-rank slots.
+constexpr int PROJ_CHUNK = 128;
+
+struct ProjStage {  // one chunk of parameters in shared memory
+  float4 q[PROJ_CHUNK];
+  float c[PROJ_CHUNK * 3];
+  float s[PROJ_CHUNK * 3];
+  float sh[PROJ_CHUNK * 12];
+  float op[PROJ_CHUNK];
+  uint32_t rank[PROJ_CHUNK];
+};
+
+struct ProjOutStage {  // one chunk of finished records, written out per warp
+  float4 rec[PROJ_CHUNK][REC_F4];
+  float4 bf[PROJ_CHUNK][3];
+  int64_t rank[PROJ_CHUNK];
+};
+
+__global__ void __launch_bounds__(PROJ_CHUNK)
+    k_project(const float* __restrict__ centers, const float* __restrict__ scales,
+              const float* __restrict__ quats, const float* __restrict__ opacities,
+              const float* __restrict__ sh, int C, int64_t P,
+              const uint32_t* __restrict__ rank_of, CamDev cam, double cutoff,
+              double near_plane, ProjOut out) {
+  __shared__ ProjStage st[2];
+  __shared__ ProjOutStage so;
+  const int tid = threadIdx.x, lane = tid & 31, wbase = tid & ~31;
+  const int64_t n_chunks = (P + PROJ_CHUNK - 1) / PROJ_CHUNK;
+  // full chunks stream through cp.async; a partial last chunk uses plain loads
+  auto stage = [&](int buf, int64_t ch) {
+    const int64_t g0 = ch * PROJ_CHUNK;
+    if (g0 + PROJ_CHUNK <= P) {
+      ProjStage& S = st[buf];
+      const char* src_q = reinterpret_cast<const char*>(quats + 4 * g0);
+      const char* src_c = reinterpret_cast<const char*>(centers + 3 * g0);
+      const char* src_s = reinterpret_cast<const char*>(scales + 3 * g0);
+      const char* src_o = reinterpret_cast<const char*>(opacities + g0);
+      const char* src_r = reinterpret_cast<const char*>(rank_of + g0);
+      const char* src_h = reinterpret_cast<const char*>(sh + (int64_t)3 * C * g0);
+      for (int k = tid; k < PROJ_CHUNK * 16 / 16; k += PROJ_CHUNK)
+        cp_async16(reinterpret_cast<char*>(S.q) + 16 * k, src_q + 16 * k);
+      for (int k = tid; k < PROJ_CHUNK * 12 / 16; k += PROJ_CHUNK) {
+        cp_async16(reinterpret_cast<char*>(S.c) + 16 * k, src_c + 16 * k);
+        cp_async16(reinterpret_cast<char*>(S.s) + 16 * k, src_s + 16 * k);
+      }
+      for (int k = tid; k < PROJ_CHUNK * 4 / 16; k += PROJ_CHUNK) {
+        cp_async16(reinterpret_cast<char*>(S.op) + 16 * k, src_o + 16 * k);
+        cp_async16(reinterpret_cast<char*>(S.rank) + 16 * k, src_r + 16 * k);
+      }
+      for (int k = tid; k < PROJ_CHUNK * 3 * C * 4 / 16; k += PROJ_CHUNK)  // 3*C floats each
+        cp_async16(reinterpret_cast<char*>(S.sh) + 16 * k, src_h + 16 * k);
+    }
+    cp_async_commit();
+  };
+  int buf = 0;
+  int64_t ch = blockIdx.x;
+  if (ch < n_chunks) stage(0, ch);
+  for (; ch < n_chunks; ch += gridDim.x, buf ^= 1) {
+    const int64_t nxt = ch + gridDim.x;
+    if (nxt < n_chunks) {
+      stage(buf ^ 1, nxt);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const int64_t g = ch * PROJ_CHUNK + tid;
+    if (g < P) {
+      GParams prm;
+      int64_t r;
+      const bool full = ch * PROJ_CHUNK + PROJ_CHUNK <= P;
+      if (full) {
+        const ProjStage& S = st[buf];
+        prm.q = S.q[tid];
+        prm.c0 = S.c[3 * tid + 0];
+        prm.c1 = S.c[3 * tid + 1];
+        prm.c2 = S.c[3 * tid + 2];
+        prm.s0 = S.s[3 * tid + 0];
+        prm.s1 = S.s[3 * tid + 1];
+        prm.s2 = S.s[3 * tid + 2];
+        prm.op = S.op[tid];
+        r = S.rank[tid];
+        if (C == 4) {
+#pragma unroll
+          for (int k = 0; k < 12; ++k) prm.shv[k] = S.sh[12 * tid + k];
+        } else {
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            prm.shv[4 * c] = S.sh[3 * tid + c];
+            prm.shv[4 * c + 1] = prm.shv[4 * c + 2] = prm.shv[4 * c + 3] = 0.0f;
+          }
+        }
+      } else {
+        prm.q = reinterpret_cast<const float4*>(quats)[g];
+        prm.c0 = centers[3 * g + 0];
+        prm.c1 = centers[3 * g + 1];
+        prm.c2 = centers[3 * g + 2];
+        prm.s0 = scales[3 * g + 0];
+        prm.s1 = scales[3 * g + 1];
+        prm.s2 = scales[3 * g + 2];
+        prm.op = opacities[g];
+        r = rank_of[g];
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) prm.shv[4 * c + k] = (k < C) ? sh[(g * 3 + c) * C + k] : 0.0f;
+      }
+      project_one(prm, g, cam, cutoff, near_plane, out, so.rec[tid], so.bf[tid]);
+      so.rank[tid] = r;
+    } else {
+      so.rank[tid] = -1;
+    }
+    __syncwarp();
+    // each store instruction writes 4 complete 128-B records (full lines)
+#pragma unroll
+    for (int i = 0; i < REC_F4; ++i) {
+      const int k = i * 32 + lane, t = wbase + (k >> 3), part = k & 7;
+      const int64_t rr = so.rank[t];
+      if (rr >= 0) out.records[rr * REC_F4 + part] = so.rec[t][part];
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const int k = i * 32 + lane, t = wbase + k / 3, part = k - 3 * (k / 3);
+      const int64_t rr = so.rank[t];
+      if (rr >= 0) out.bframe[rr * 3 + part] = so.bf[t][part];
+    }
+    __syncthreads();  // everyone is done with `buf` and `so` before they are refilled
+  }
+  cp_async_wait<0>();
 }
 
 // K2a: per rank of [r0, r1), the number of still-active tiles in its rect.
-__global__ void k_count_active(const int4* __restrict__ rects, int64_t r0, int64_t r1,
-                               int tiles_x, const uint8_t* __restrict__ active,
+__global__ void k_count_active(const int4* __restrict__ rects, const uint32_t* __restrict__ order,
+                               int64_t r0, int64_t r1, int tiles_x,
+                               const uint8_t* __restrict__ active,
                                unsigned long long* __restrict__ counts) {
   const int64_t r = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= r1) return;
-  const int4 rc = rects[r];
+  const int4 rc = rects[order[r]];
   unsigned long long n = 0;
   if (rc.x >= 0)
     for (int ty = rc.y; ty <= rc.w; ++ty)
@@ -417,13 +538,13 @@ __global__ void k_count_active(const int4* __restrict__ rects, int64_t r0, int64
 
 // K2b: emit (tile, rank) pairs of active tiles at the exclusive-scan
 // offsets, in rank order (so a stable sort by tile keeps ranks ascending).
-__global__ void k_emit_pairs(const int4* __restrict__ rects,
+__global__ void k_emit_pairs(const int4* __restrict__ rects, const uint32_t* __restrict__ order,
                              const unsigned long long* __restrict__ offsets, int64_t r0,
                              int64_t r1, int tiles_x, const uint8_t* __restrict__ active,
                              uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
   const int64_t r = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= r1) return;
-  const int4 rc = rects[r];
+  const int4 rc = rects[order[r]];
   if (rc.x < 0) return;
   unsigned long long o = offsets[r - r0];
   for (int ty = rc.y; ty <= rc.w; ++ty)
@@ -474,23 +595,29 @@ void launch_project(const float* centers, const float* scales, const float* quat
                     unsigned long long* straddle, cudaStream_t s) {
   if (P == 0) return;
   ProjOut o{n_tiles, rects, records, bframe, straddle};
-  k_project<<<(unsigned)((P + 127) / 128), 128, 0, s>>>(centers, scales, quats, opacities, sh, C,
-                                                        P, rank_of, cam, cutoff, near_plane, o);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t n_chunks = (P + PROJ_CHUNK - 1) / PROJ_CHUNK;
+  const unsigned grid = (unsigned)std::min<int64_t>(n_chunks, (int64_t)sms * 8);
+  k_project<<<grid, PROJ_CHUNK, 0, s>>>(centers, scales, quats, opacities, sh, C, P, rank_of, cam,
+                                         cutoff, near_plane, o);
 }
 
-void launch_count_active(const int4* rects, int64_t r0, int64_t r1, int tiles_x,
-                         const uint8_t* active, unsigned long long* counts, cudaStream_t s) {
+void launch_count_active(const int4* rects, const uint32_t* order, int64_t r0, int64_t r1,
+                         int tiles_x, const uint8_t* active, unsigned long long* counts,
+                         cudaStream_t s) {
   if (r1 <= r0) return;
-  k_count_active<<<(unsigned)((r1 - r0 + 255) / 256), 256, 0, s>>>(rects, r0, r1, tiles_x, active,
-                                                                   counts);
+  k_count_active<<<(unsigned)((r1 - r0 + 255) / 256), 256, 0, s>>>(rects, order, r0, r1, tiles_x,
+                                                                   active, counts);
 }
 
-void launch_emit_pairs(const int4* rects, const unsigned long long* offsets, int64_t r0, int64_t r1,
-                       int tiles_x, const uint8_t* active, uint32_t* keys, uint32_t* vals,
-                       cudaStream_t s) {
+void launch_emit_pairs(const int4* rects, const uint32_t* order, const unsigned long long* offsets,
+                       int64_t r0, int64_t r1, int tiles_x, const uint8_t* active, uint32_t* keys,
+                       uint32_t* vals, cudaStream_t s) {
   if (r1 <= r0) return;
-  k_emit_pairs<<<(unsigned)((r1 - r0 + 255) / 256), 256, 0, s>>>(rects, offsets, r0, r1, tiles_x,
-                                                                 active, keys, vals);
+  k_emit_pairs<<<(unsigned)((r1 - r0 + 255) / 256), 256, 0, s>>>(rects, order, offsets, r0, r1,
+                                                                 tiles_x, active, keys, vals);
 }
 
 void launch_tile_ranges(const uint32_t* keys, int64_t n, int2* ranges, cudaStream_t s) {

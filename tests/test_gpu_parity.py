@@ -183,7 +183,7 @@ def test_binning_bit_exact_vs_c_restatement(n, W, H, seed):
     order, rects, ranges, pairs, recs = _binning_of(got["view"], n, T, st["n_pairs"])
     np.testing.assert_array_equal(order, ref["order"])
     assert_order_matches_up_to_ties(order, O.depth_order(sc, cam), exact_depths(sc.centers, cam))
-    np.testing.assert_array_equal(rects, ref["rects"])
+    np.testing.assert_array_equal(rects[order], ref["rects"])  # exported per Gaussian
     np.testing.assert_array_equal(ranges, ref["ranges"])
     np.testing.assert_array_equal(pairs, ref["pairs"])
     # projected record words (centre hi/lo, conic, denominator, opacity) bitwise
@@ -215,7 +215,7 @@ def test_tile_lists_cover_reference_valid_pairs():
     rank[order] = np.arange(P)
     g = O._geometry(sc, np.arange(P), O.pixel_directions(cam), cam.position, 1e-4, 1 / 255)
     r_, m_ = np.nonzero(g["valid"])
-    rc = rects[rank[r_]]
+    rc = rects[r_]  # exported per Gaussian (storage order)
     tx, ty = (m_ % cam.width) // 16, (m_ // cam.width) // 16
     inside = (rc[:, 0] <= tx) & (tx <= rc[:, 2]) & (rc[:, 1] <= ty) & (ty <= rc[:, 3])
     assert inside.all()
