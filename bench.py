@@ -62,6 +62,8 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--chunk", default="1",
+                   help="ordering: 1 = global depth order (default), none = exact per-pixel order")
     p.add_argument("--first-phase", type=int, default=0,
                    help="ranks binned in the first depth phase (0 = automatic)")
     return p.parse_args()
@@ -183,6 +185,7 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     model = model_of(a)
+    a.chunk_size = None if str(a.chunk).lower() in ("none", "0", "exact") else int(a.chunk)
 
     if a.impl == "reference":
         return reference_arm(a, rank, model)
@@ -209,7 +212,8 @@ def main():
              for v in range(n_views)}
     bg = np.zeros(3)
     grads = GradBuffer(len(arrs), arrs.sh.shape[2], device="cuda")
-    rv = device_view_renderer(dev, model, bg, cams, seeds, first_phase_ranks=a.first_phase)
+    rv = device_view_renderer(dev, model, bg, cams, seeds, first_phase_ranks=a.first_phase,
+                              chunk_size=a.chunk_size)
     step = DataParallelStep(n_views, rank, world, grads, rv)
     my_views = step.views()
 
@@ -255,8 +259,8 @@ def main():
     # ---- event counts (instrumented run, not timed) for the blend roofline
     from paper_2603_02887_b200 import backward_device, forward_device
     cview = _native.View()
-    forward_device(cview, dev, cams[my_views[0]], model, bg, chunk_size=1, count_events=True,
-                   first_phase_ranks=a.first_phase)
+    forward_device(cview, dev, cams[my_views[0]], model, bg, chunk_size=a.chunk_size,
+                   count_events=True, first_phase_ranks=a.first_phase)
     backward_device(cview, dev, seeds[my_views[0]])
     st = cview.stats()
     cview.close()
@@ -289,8 +293,10 @@ def main():
             "data": "synthetic",
             "config": {
                 "workload": (f"C3: {a.gaussians} Gaussians (canonical synthetic scene, seed 5), "
-                             f"{W}x{H}, {model.describe()}, chunk_size=1 (global depth order), "
-                             f"fwd+bwd, {vpr} view(s) per GPU"
+                             f"{W}x{H}, {model.describe()}, "
+                             + ("chunk_size=1 (global depth order), " if a.chunk_size == 1 else
+                                "chunk_size=None (exact per-pixel order), ")
+                             + f"fwd+bwd, {vpr} view(s) per GPU"
                              + (", NCCL all-reduce of gradients" if world > 1 else "")),
                 "gaussians": a.gaussians, "width": W, "height": H,
                 "views_per_gpu": vpr, "total_views": n_views,
@@ -374,7 +380,7 @@ def e2e_arm(a, arrs, cams, model, my_views, world, render_with_gradients):
     def one():
         for v in my_views:
             res, g = render_with_gradients(arrs, cams[v], model, np.zeros(3), seeds[v],
-                                           chunk_size=1)
+                                           chunk_size=a.chunk_size)
         return res, g
 
     one()
@@ -396,7 +402,7 @@ def e2e_arm(a, arrs, cams, model, my_views, world, render_with_gradients):
     return {"value": round(npx * len(my_views) * world / dt / 1e6, 3), "unit": "Mpix/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "ms_per_step": round(dt * 1e3, 3),
-            "api": "render_with_gradients(numpy float64 SceneArrays, chunk_size=1)"}
+            "api": f"render_with_gradients(numpy float64 SceneArrays, chunk_size={a.chunk_size})"}
 
 
 def reference_arm(a, rank, model):

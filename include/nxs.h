@@ -54,6 +54,7 @@ extern "C" {
 #define NXS_ERR_NOMEM (-4)         /* device allocation failed */
 #define NXS_ERR_STATE (-5)         /* backward without a matching forward */
 #define NXS_ERR_GEOMETRY (-6)      /* reserved: unsupported geometry */
+#define NXS_ERR_OVERFLOW (-7)      /* exact order: a pixel's pending buffer overflowed */
 
 /* transmittance variants: order of reference transmittance.py:32-40 */
 #define NXS_MODEL_EXPONENTIAL 0
@@ -122,6 +123,7 @@ typedef struct {
     int64_t n_composited;     /* sum of overdraw                     [COUNT_EVENTS] */
     int64_t n_tests_bwd;      /* pairs re-tested by the backward     [COUNT_EVENTS] */
     int64_t n_entries_bwd;    /* (tile, entry) pairs replayed        [COUNT_EVENTS] */
+    int64_t n_overflow;       /* exact order: pending-buffer overflows (must be 0) */
 } nxs_stats;
 
 typedef struct nxs_view nxs_view;

@@ -350,6 +350,7 @@ def _forward_batch(scene, cam, model, bg, dirs, max_splats, cutoff, near,
     # ln α to ln cutoff, and of any live splat's raw weight to 1 - cum
     amargin = np.full(m, np.inf)
     smargin = np.full(m, np.inf)
+    tmargin = np.full(m, np.inf)
     if geo is not None:
         la = np.log(np.maximum(geo["alpha"], 1e-300))
         amargin = np.min(np.abs(la - np.log(cutoff)), axis=0)
@@ -384,13 +385,29 @@ def _forward_batch(scene, cam, model, bg, dirs, max_splats, cutoff, near,
             e_k = np.where(sat_now[:, None], e, e_k)
             t_k = np.where(sat_now, w, t_k)
             sat |= sat_now
+    if geo is not None and slots:
+        # relative gap between consecutive peak depths among the replayed
+        # prefix (orders that depend on t: chunk_size None or C > 1)
+        order = st["order"]
+        k = min(len(slots) + 1, order.shape[0])
+        cols = np.arange(m)
+        tt = geo["t"][order[:k], cols[None, :]]
+        vv = geo["valid"][order[:k], cols[None, :]]
+        gi = group[ids][order[:k]] if group is not None else None
+        if k >= 2:
+            gap = np.abs(np.diff(tt, axis=0)) / np.maximum(np.abs(tt[:-1]), 1e-300)
+            ok = vv[1:] & vv[:-1]
+            if gi is not None:
+                ok &= gi[1:] == gi[:-1]
+            gap = np.where(ok, gap, np.inf)
+            tmargin = gap.min(axis=0)
     residual = np.where(sat, 0.0, 1.0 - cum)
     rad += bg[None, :] * residual[:, None]
     t_k = np.where(sat, t_k, residual)
     theta0 = sea - e_k * sa[:, None]
     out = dict(rad=rad, residual=residual, overdraw=count, sat=sat, e_k=e_k,
                t_k=t_k, theta0=theta0, tau=tau, prod=prod, cum=cum,
-               amargin=amargin, smargin=smargin)
+               amargin=amargin, smargin=smargin, tmargin=tmargin)
     st["slots"] = slots
     return out, st
 
@@ -434,7 +451,7 @@ def forward(scene, cam, model, background, *, max_splats=128, alpha_cutoff=1.0 /
     dirs_all = pixel_directions(cam)
     group, tie = _group_keys(scene, cam, chunk_size)
     keys = ("rad", "residual", "overdraw", "sat", "e_k", "t_k", "theta0", "amargin",
-            "smargin")
+            "smargin", "tmargin")
     res = {k: None for k in keys}
     states = []
     pos = {int(p): i for i, p in enumerate(pixels)}
@@ -453,13 +470,13 @@ def forward(scene, cam, model, background, *, max_splats=128, alpha_cutoff=1.0 /
         for k in keys:
             res[k] = np.zeros((0, 3) if k in ("rad", "e_k", "theta0") else (0,))
     res["pixels"] = pixels
-    res["mask"] = margin_mask(res, model)
+    res["mask"] = margin_mask(res, model, t_order=(chunk_size != 1))
     if keep_state:
         res["_states"] = states
     return res
 
 
-def margin_mask(res, model, tol=1e-5):
+def margin_mask(res, model, tol=1e-5, t_order=False):
     """Pixels excluded from fp32-vs-fp64 parity because a decision sits on a
     threshold (the reference's own gradcheck excludes
     near-saturation rays the same way, adjoint.py:225-231).  True = masked."""
@@ -470,6 +487,8 @@ def margin_mask(res, model, tol=1e-5):
         m = m | res["sat"]
     else:
         m = m | (res["smargin"] < tol)
+    if t_order:  # candidates with |Δt| < 1e-6·t
+        m = m | (res["tmargin"] < 1e-6)
     return m
 
 

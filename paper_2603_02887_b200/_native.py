@@ -45,6 +45,7 @@ SYMBOLS = (
 )
 
 NXS_ERR_GEOMETRY = -6
+NXS_ERR_OVERFLOW = -7
 NXS_ERR_UNSUPPORTED = -2
 NXS_ERR_INVALID = -1
 NXS_FLAG_COUNT_EVENTS = 1
@@ -103,7 +104,7 @@ class Scene(C.Structure):
 class Stats(C.Structure):
     _fields_ = [(n, C.c_int64) for n in (
         "n_gaussians", "n_visible", "n_pairs", "n_straddling", "n_tiles", "n_tests_fwd",
-        "n_composited", "n_tests_bwd", "n_entries_bwd")]
+        "n_composited", "n_tests_bwd", "n_entries_bwd", "n_overflow")]
 
     def as_dict(self) -> dict:
         return {n: int(getattr(self, n)) for n, _ in self._fields_}

@@ -19,15 +19,20 @@
 #include "nxs_internal.cuh"
 
 namespace nxs {
-void launch_depth(const float*, int64_t, const CamDev&, double*, unsigned long long*, uint32_t*,
-                  unsigned long long*, cudaStream_t);
+void launch_depth(const float*, const float*, const float*, const float*, int64_t, const CamDev&,
+                  double, int, double*, unsigned long long*, uint32_t*, unsigned long long*,
+                  cudaStream_t);
 void launch_key32(const double*, int64_t, const unsigned long long*, uint32_t*, cudaStream_t);
 void launch_key_fixup(const uint32_t*, uint32_t*, const double*, int64_t, unsigned long long*,
                       cudaStream_t);
 void launch_rank_of(const uint32_t*, int64_t, uint32_t*, cudaStream_t);
 void launch_project(const float*, const float*, const float*, const float*, const float*, int,
-                    int64_t, const uint32_t*, const CamDev&, double, double, unsigned long long*,
-                    int4*, float4*, float4*, unsigned long long*, cudaStream_t);
+                    int64_t, const uint32_t*, const CamDev&, double, double, const double*,
+                    float*, int4*, float4*, float4*, unsigned long long*, cudaStream_t);
+void launch_blend_fwd_x(bool, int, const FwdXArgs&, const CamDev&, const ModelDev&,
+                        const PixCache&, Counters*, cudaStream_t);
+void launch_blend_bwd_x(bool, int, const BwdXArgs&, const CamDev&, const ModelDev&,
+                        const PixCache&, Counters*, cudaStream_t);
 void launch_count_active(const int4*, const uint32_t*, int64_t, int64_t, int, const uint8_t*,
                          unsigned long long*, cudaStream_t);
 void launch_emit_pairs(const int4*, const uint32_t*, const unsigned long long*, int64_t, int64_t,
@@ -102,7 +107,7 @@ int bits_for(uint32_t n) {
 struct nxs_view {
   // per Gaussian
   Buf dkeys_in, dkeys_out, idx_in, idx_out, records, bframe, rects, ntiles, offsets, moments,
-      touched, depth, k32a, k32b, rank_of;
+      touched, depth, k32a, k32b, rank_of, zlo_rank, seq;
   // per pair: sort scratch, and the sorted ranks of each depth phase
   Buf pk_in, pk_out, pv_in, pv_ph[MAX_PHASES];
   // per tile: phase ranges and virtual offsets, activity
@@ -137,7 +142,7 @@ struct nxs_view {
   void for_each_buf(F f) {
     Buf* all[] = {&dkeys_in, &dkeys_out, &idx_in,  &idx_out, &records, &bframe, &rects,
                   &ntiles,   &offsets,   &moments, &touched, &pk_in,   &pk_out,  &pv_in,  &active,
-                  &depth,    &k32a,      &k32b,    &rank_of,
+                  &depth,    &k32a,      &k32b,    &rank_of, &zlo_rank, &seq,
                   &c_last,   &c_sat,     &c_tk,    &c_thi,   &c_tlo,   &c_P,    &c_ck,
                   &c_Pck,    &c_ek,      &c_th0,   &r_rad,   &r_trem,  &r_count, &r_sea,
                   &r_sa,     &temp,      &dev_small};
@@ -254,7 +259,8 @@ const char* nxs_error_string(int code) {
     case NXS_ERR_CUDA: return "CUDA error";
     case NXS_ERR_NOMEM: return "out of device memory";
     case NXS_ERR_STATE: return "backward without a matching forward";
-    case NXS_ERR_GEOMETRY: return "Gaussian crosses the near plane (unsupported geometry)";
+    case NXS_ERR_GEOMETRY: return "unsupported geometry";
+    case NXS_ERR_OVERFLOW: return "exact-order pending buffer overflow";
     default: return "unknown error";
   }
 }
@@ -314,9 +320,12 @@ int nxs_forward(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
                 !scene->sh))
     return fail(NXS_ERR_INVALID, "null scene array");
   if (P >= (int64_t)1 << 31) return fail(NXS_ERR_INVALID, "more than 2^31 Gaussians");
-  if (opts->chunk_size != 1)
+  if (opts->chunk_size != 1 && opts->chunk_size != NXS_CHUNK_EXACT)
     return fail(NXS_ERR_UNSUPPORTED,
-                "only the global depth order (chunk_size=1) is implemented on the device");
+                "chunked order (chunk_size > 1) is not implemented on the device yet");
+  const bool exact = opts->chunk_size == NXS_CHUNK_EXACT;
+  if (exact && opts->max_splats > 4096)
+    return fail(NXS_ERR_INVALID, "exact order supports max_splats <= 4096");
   if (!(opts->alpha_cutoff > 0.0) || !(opts->near_plane >= 0.0))
     return fail(NXS_ERR_INVALID, "alpha_cutoff must be > 0 and near >= 0");
 
@@ -366,8 +375,8 @@ int nxs_forward(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
   int n_ph = 0;
   {
     int64_t r1;
-    if (opts->flags & NXS_FLAG_FULL_BINNING)
-      r1 = P;
+    if ((opts->flags & NXS_FLAG_FULL_BINNING) || exact)
+      r1 = P;  // the exact order keeps per-pixel pending state: one phase
     else if (opts->first_phase_ranks > 0)
       r1 = opts->first_phase_ranks;
     else  // measured at C3: saturating models finish every tile within P/32
@@ -407,7 +416,8 @@ retry_sort:
     // ---- K0 depth (+ min/max) and the stable depth sort
     NXS_CUDA(cudaMemsetAsync(dsmall + 6, 0xff, sizeof(unsigned long long), s));
     NXS_CUDA(cudaMemsetAsync(dsmall + 7, 0, 2 * sizeof(unsigned long long), s));
-    launch_depth(scene->centers, P, cam, v->depth.as<double>(),
+    launch_depth(scene->centers, scene->scales, scene->quats, scene->opacities, P, cam,
+                 opts->alpha_cutoff, exact ? 1 : 0, v->depth.as<double>(),
                  v->dkeys_in.as<unsigned long long>(), v->idx_in.as<uint32_t>(), dsmall + 6, s);
     NXS_LAUNCHED("depth");
     size_t tb = v->temp.cap;
@@ -432,9 +442,11 @@ retry_sort:
   mark(v, 1, s);
   if (P > 0) {
     // ---- K1 projection (all Gaussians, storage order; records land at their rank)
+    if (exact) NXS_CUDA(ensure_n<float>(v->zlo_rank, P));
     launch_project(scene->centers, scene->scales, scene->quats, scene->opacities, scene->sh, C, P,
                    v->rank_of.as<uint32_t>(), cam, opts->alpha_cutoff, opts->near_plane,
-                   v->ntiles.as<unsigned long long>(), v->rects.as<int4>(),
+                   exact ? v->depth.as<double>() : nullptr,
+                   exact ? v->zlo_rank.as<float>() : nullptr, v->rects.as<int4>(),
                    v->records.as<float4>(), v->bframe.as<float4>(), dsmall, s);
     NXS_LAUNCHED("project");
   }
@@ -530,6 +542,20 @@ retry_sort:
       NXS_CUDA(ensure_n<float>(v->r_sea, npix * 3));
       NXS_CUDA(ensure_n<float>(v->r_sa, npix));
     }
+    if (exact) {
+      // ---- K3x exact-order forward (single phase)
+      NXS_CUDA(ensure_n<int32_t>(v->seq, npix * std::max(1, opts->max_splats)));
+      FwdXArgs xa{v->records.as<float4>(), v->pv_ph[ph].as<uint32_t>(),
+                  v->ranges_ph[ph].as<int2>(), v->zlo_rank.as<float>(), v->idx_out.as<uint32_t>(),
+                  opts->max_splats, (float)opts->alpha_cutoff, opts->near_plane,
+                  {bgf[0], bgf[1], bgf[2]}, rgb, overdraw, residual, v->seq.as<int32_t>(),
+                  dsmall + 9};
+      launch_blend_fwd_x(count, n_tiles, xa, cam, md, v->cache(), cnt, s);
+      NXS_LAUNCHED("blend_fwd_x");
+      if (v->ev_ok) cudaEventRecord(v->evp[ph][2], s);
+      ph_done = ph + 1;
+      break;
+    }
     // ---- K3 forward blend of this phase (tiles still active)
     NXS_CUDA(cudaMemsetAsync(n_active, 0, sizeof(unsigned int), s));
     FwdArgs fa{v->records.as<float4>(), v->pv_ph[ph].as<uint32_t>(), v->ranges_ph[ph].as<int2>(),
@@ -546,6 +572,17 @@ retry_sort:
   v->ev_fwd = true;
   v->ev_bwd = false;
   v->stats.n_pairs = total_pairs;
+  if (exact) {
+    // pending-buffer overflow means the exact order was not guaranteed: report
+    NXS_CUDA(cudaMemcpyAsync(v->host_small + 7, dsmall + 9, sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, s));
+    NXS_CUDA(cudaStreamSynchronize(s));
+    v->stats.n_overflow = (int64_t)v->host_small[7];
+    if (v->host_small[7] > 0)
+      return fail(NXS_ERR_OVERFLOW, std::to_string(v->host_small[7]) +
+                                        " pixel-entries overflowed the exact-order pending "
+                                        "buffer; the per-pixel order is not guaranteed");
+  }
   if (count) {
     NXS_CUDA(cudaMemcpyAsync(v->host_small + 4, cnt, 2 * sizeof(unsigned long long),
                              cudaMemcpyDeviceToHost, s));
@@ -595,6 +632,13 @@ int nxs_backward(nxs_view* v, const nxs_scene* scene, const float* seed, float* 
   const bool count = (v->opts.flags & NXS_FLAG_COUNT_EVENTS) != 0;
   unsigned long long* dsmall = v->dev_small.as<unsigned long long>();
   Counters* cnt = reinterpret_cast<Counters*>(dsmall + 1);
+  if (v->opts.chunk_size == NXS_CHUNK_EXACT) {
+    BwdXArgs xa{v->records.as<float4>(), v->bframe.as<float4>(), v->pv_ph[0].as<uint32_t>(),
+                v->seq.as<int32_t>(), std::max(1, v->opts.max_splats),
+                (float)v->opts.alpha_cutoff, v->opts.near_plane, {v->bg[0], v->bg[1], v->bg[2]},
+                seed, v->moments.as<double>(), v->touched.as<uint8_t>()};
+    launch_blend_bwd_x(count, v->n_tiles, xa, v->cam, v->model, v->cache(), cnt, s);
+  } else {
   PhaseLists lists{};
   lists.n = v->n_phases;
   for (int p = 0; p < v->n_phases; ++p) {
@@ -605,6 +649,7 @@ int nxs_backward(nxs_view* v, const nxs_scene* scene, const float* seed, float* 
   launch_blend_bwd(count, v->n_tiles, v->records.as<float4>(), v->bframe.as<float4>(), lists,
                    v->cam, v->model, (float)v->opts.alpha_cutoff, v->opts.near_plane, v->bg, seed,
                    v->cache(), v->moments.as<double>(), v->touched.as<uint8_t>(), cnt, s);
+  }
   NXS_LAUNCHED("blend_bwd");
   mark(v, 10, s);
   launch_chain(scene->scales, scene->quats, v->C, P, v->idx_out.as<uint32_t>(),

@@ -83,7 +83,7 @@ __device__ __forceinline__ bool ray_peak_test(const float4& r0, const float4& r1
 // Outputs the world-frame peak offset diff = t·d - b for the chain.
 __device__ __forceinline__ bool general_test(const float4* rec, const CamDev& cam, int px, int py,
                                              float cutoff, double near_plane, TestOut& o,
-                                             float& gdx, float& gdy, float& gdz) {
+                                             float& gdx, float& gdy, float& gdz, float& tpk) {
   const double* dp = reinterpret_cast<const double*>(rec);
   const double b0 = dp[0], b1 = dp[1], b2 = dp[2];
   const double A00 = dp[3], A01 = dp[4], A02 = dp[5], A11 = dp[6], A12 = dp[14], A22 = dp[15];
@@ -121,6 +121,7 @@ __device__ __forceinline__ bool general_test(const float4* rec, const CamDev& ca
   gdx = (float)x0;
   gdy = (float)x1;
   gdz = (float)x2;
+  tpk = (float)t;
   return (t > near_plane) && (o.alpha >= cutoff);
 }
 

@@ -110,8 +110,8 @@ __global__ void __launch_bounds__(TILE_PIX, 3)
         TestOut t;
         bool ok;
         if (__float_as_int(s_cur[j][3].w) & RF_GENERAL) {  // block-uniform branch
-          float gx, gy, gz;
-          ok = general_test(s_cur[j], cam, px, py, cutoff, near_plane, t, gx, gy, gz);
+          float gx, gy, gz, tpk;
+          ok = general_test(s_cur[j], cam, px, py, cutoff, near_plane, t, gx, gy, gz, tpk);
         } else {
           ok = ray_peak_test(s_cur[j][0], s_cur[j][1], s_cur[j][2], s_cur[j][3], pc, cutoff, t);
         }

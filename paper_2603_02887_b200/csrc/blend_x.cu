@@ -1,0 +1,426 @@
+// K3x / K4x: exact per-pixel order — the reference's default traversal
+// (render(..., chunk_size=None): one chunk, every pixel stable-sorts its
+// valid splats by peak depth t, ties by storage index; reference
+// pkg/src/nexsplat/render.py:171, primitives.py:299).
+//
+// Tile lists are ordered by z_lo, a lower bound of t over every pixel where a
+// Gaussian can be valid (min camera-z of its cutoff ellipsoid; t >= z_lo·|h|).
+// K3x walks the list keeping, per pixel, a pending buffer of valid entries
+// sorted by (t, index) in shared memory: before testing the next entry it
+// commits (composites) every pending entry whose t is below that entry's
+// bound z_lo·|h| — no later entry can precede it — and at the end of the
+// list it commits the rest.  A full buffer is an overflow:
+// counted and reported by the API, never silently accepted.  Each pixel's
+// commit sequence (list positions) is stored for the backward.
+//
+// K4x replays every pixel's sequence back to front with the same unified
+// adjoint as K4 (bwd_common.cuh).  Lanes of a warp step together through
+// list positions (the warp processes the largest pending position each
+// step, pixels whose next entry it is take part), so the 24 moments still
+// reduce per warp through the shared-memory transpose before one fp64
+// atomic per moment.
+#include "bwd_common.cuh"
+
+namespace nxs {
+
+constexpr int XBUF = 32;     // pending entries per pixel
+constexpr int XBATCH = 64;   // list entries staged per batch
+constexpr size_t FWDX_SMEM = sizeof(float4) * XBATCH * REC_F4 + sizeof(uint32_t) * XBATCH +
+                             sizeof(float) * XBATCH + (sizeof(float) + sizeof(int)) * XBUF * TILE_PIX;
+
+struct FwdXPix {
+  float rad0, rad1, rad2, thi, tlo, P, Trem, ek0, ek1, ek2, tk, sea0, sea1, sea2, sa, Pck;
+  int count, ck;
+  bool sat, done;
+};
+
+// one front-to-back compositing step (reference render.py:181-203) for the
+// entry committed as the pixel's `count`-th live splat
+template <int FAM>
+__device__ __forceinline__ void composite(FwdXPix& s, const ModelDev& m, int max_splats,
+                                          float alpha, float E0, float E1, float E2) {
+  float fp;
+  const float g = weight_g<FAM>(m, s.thi, s.tlo, s.P, fp);
+  const float wr = alpha * g;
+  const bool satnow = (FAM == FAM_EXP) ? false : (wr >= s.Trem);
+  const int cb = s.count;
+  ++s.count;
+  if (satnow) {
+    s.rad0 = fmaf(s.Trem, E0, s.rad0);
+    s.rad1 = fmaf(s.Trem, E1, s.rad1);
+    s.rad2 = fmaf(s.Trem, E2, s.rad2);
+    s.ek0 = E0;
+    s.ek1 = E1;
+    s.ek2 = E2;
+    s.tk = s.Trem;
+    s.sat = true;
+    s.done = true;
+    return;
+  }
+  s.rad0 = fmaf(wr, E0, s.rad0);
+  s.rad1 = fmaf(wr, E1, s.rad1);
+  s.rad2 = fmaf(wr, E2, s.rad2);
+  if (cb >= 1) {
+    s.sea0 = fmaf(alpha, E0, s.sea0);
+    s.sea1 = fmaf(alpha, E1, s.sea1);
+    s.sea2 = fmaf(alpha, E2, s.sea2);
+    s.sa += alpha;
+  }
+  if constexpr (FAM != FAM_EXP) df_add(s.thi, s.tlo, alpha);
+  if constexpr (IsPFam<FAM>::value) {
+    const float Pn = __fmul_rn(s.P, __fsub_rn(1.0f, alpha));
+    if (Pn < P_FLOOR && s.ck < 0) {
+      s.ck = cb;
+      s.Pck = s.P;
+    }
+    s.P = Pn;
+  }
+  if constexpr (FAM == FAM_EXP) {
+    s.Trem = s.P;
+  } else if constexpr (FAM == FAM_BLEND) {
+    s.Trem = fmaf(1.0f - m.c, __fsub_rn(__fsub_rn(1.0f, s.thi), s.tlo), m.c * s.P);
+  } else {
+    s.Trem = __fsub_rn(s.Trem, wr);
+  }
+  if (s.count >= max_splats) s.done = true;
+}
+
+// ray-peak test of one record for this pixel, with the peak depth t
+__device__ __forceinline__ bool test_with_t(const float4* rec, const CamDev& cam, int px, int py,
+                                            const PixelConst& pc, float hnorm, float cutoff,
+                                            double near_plane, TestOut& t, float& tpk) {
+  if (__float_as_int(rec[3].w) & RF_GENERAL) {
+    float gx, gy, gz;
+    return general_test(rec, cam, px, py, cutoff, near_plane, t, gx, gy, gz, tpk);
+  }
+  if (!ray_peak_test(rec[0], rec[1], rec[2], rec[3], pc, cutoff, t)) return false;
+  // t = |h| (A'b')·h / hᵀA'h  (rec[7].xyz = A'b')
+  const float4 ab = rec[7];
+  tpk = hnorm * (__fmaf_rn(ab.x, pc.hx, __fmaf_rn(ab.y, pc.hy, ab.z)) * t.rD);
+  return true;
+}
+
+template <int FAM, bool COUNT>
+__global__ void __launch_bounds__(TILE_PIX)
+    k_blend_fwd_x(const float4* __restrict__ records, const uint32_t* __restrict__ pairs,
+                  const int2* __restrict__ ranges, const float* __restrict__ zlo_rank,
+                  const uint32_t* __restrict__ order, CamDev cam, ModelDev m, int max_splats,
+                  float cutoff, double near_plane, float bg0, float bg1, float bg2,
+                  float* __restrict__ rgb, int32_t* __restrict__ overdraw,
+                  float* __restrict__ residual, PixCache cache, int32_t* __restrict__ seq,
+                  unsigned long long* __restrict__ overflow, Counters* __restrict__ cnt) {
+  extern __shared__ float4 smem_dyn[];
+  float4(*s_rec)[REC_F4] = reinterpret_cast<float4(*)[REC_F4]>(smem_dyn);
+  uint32_t* s_rank = reinterpret_cast<uint32_t*>(smem_dyn + XBATCH * REC_F4);
+  float* s_zlo = reinterpret_cast<float*>(s_rank + XBATCH);
+  float* bt = s_zlo + XBATCH;                                 // [XBUF][TILE_PIX] pending t
+  int* bp = reinterpret_cast<int*>(bt + XBUF * TILE_PIX);     // [XBUF][TILE_PIX] list position
+
+  const int tile = blockIdx.x;
+  const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
+  const int tid = threadIdx.x;
+  const int px = tx * TILE + (tid & (TILE - 1)), py = ty * TILE + (tid >> 4);
+  const bool inside = px < cam.W && py < cam.H;
+  const PixelConst pc = pixel_setup(cam, px, py);
+  const float hnorm = sqrtf(__fmaf_rn(pc.hx, pc.hx, __fmaf_rn(pc.hy, pc.hy, 1.0f)));
+  const int pix = py * cam.W + px;
+  int32_t* myseq = seq + (size_t)(inside ? pix : 0) * max_splats;
+
+  FwdXPix s{};
+  s.P = 1.f;
+  s.Trem = 1.f;
+  s.ek0 = bg0;
+  s.ek1 = bg1;
+  s.ek2 = bg2;
+  s.ck = -1;
+  s.done = !inside || max_splats <= 0;
+  int nb = 0;  // pending entries: descending by (t, index), the next commit at nb-1
+  unsigned long long ntest = 0;
+
+  // commit the smallest pending entry: re-read its record (L1/L2; every
+  // pixel of the tile commits the same few entries) and composite it
+  auto commit_front = [&]() {
+    --nb;
+    const int pos = bp[nb * TILE_PIX + tid];
+    const float4* rec = records + (size_t)pairs[pos] * REC_F4;
+    float4 r[REC_F4];
+#pragma unroll
+    for (int k = 0; k < REC_F4; ++k) r[k] = __ldg(rec + k);
+    TestOut t;
+    float tpk;
+    test_with_t(r, cam, px, py, pc, hnorm, cutoff, near_plane, t, tpk);  // valid by construction
+    float E0, E1, E2;
+    emission(r[4], r[5], r[6], pc, E0, E1, E2);
+    myseq[s.count] = pos;
+    composite<FAM>(s, m, max_splats, t.alpha, E0, E1, E2);
+  };
+
+  const int2 rg = ranges[tile];
+  for (int base = rg.x; base < rg.y; base += XBATCH) {
+    const int n = min(XBATCH, rg.y - base);
+    __syncthreads();
+    if (tid < n) {
+      const uint32_t rk = pairs[base + tid];
+      s_rank[tid] = rk;
+      s_zlo[tid] = zlo_rank[rk];
+    }
+    __syncthreads();
+    for (int k = tid; k < n * REC_F4; k += TILE_PIX) {
+      const int e = k >> 3, part = k & 7;
+      s_rec[e][part] = records[(size_t)s_rank[e] * REC_F4 + part];
+    }
+    __syncthreads();
+    if (!s.done) {
+      for (int j = 0; j < n; ++j) {
+        // every remaining entry has t >= bound: pending entries below it are final
+        const float bound = s_zlo[j] * hnorm;
+        while (nb > 0 && bt[(nb - 1) * TILE_PIX + tid] < bound) {
+          commit_front();
+          if (s.done) break;
+        }
+        if (s.done) break;
+        if (COUNT) ++ntest;
+        TestOut t;
+        float tpk;
+        if (!test_with_t(s_rec[j], cam, px, py, pc, hnorm, cutoff, near_plane, t, tpk)) continue;
+        if (nb == XBUF) {
+          // overflow: the order is no longer guaranteed for this pixel
+          atomicAdd(overflow, 1ull);
+          commit_front();
+          if (s.done) break;
+        }
+        // insert (t, index) keeping the buffer descending
+        const int pos = base + j;
+        int k = nb;
+        uint32_t gid_new = 0xffffffffu;
+        while (k > 0) {
+          const float tk = bt[(k - 1) * TILE_PIX + tid];
+          bool smaller = tk < tpk;  // the element ahead commits after the new one
+          if (tk == tpk) {
+            if (gid_new == 0xffffffffu) gid_new = order[s_rank[j]];
+            smaller = order[pairs[bp[(k - 1) * TILE_PIX + tid]]] < gid_new;
+          }
+          if (!smaller) break;
+          bt[k * TILE_PIX + tid] = tk;
+          bp[k * TILE_PIX + tid] = bp[(k - 1) * TILE_PIX + tid];
+          --k;
+        }
+        bt[k * TILE_PIX + tid] = tpk;
+        bp[k * TILE_PIX + tid] = pos;
+        ++nb;
+      }
+    }
+    if (__syncthreads_count(!s.done && true) == 0) break;
+  }
+  // end of the list: everything pending is final, in order
+  while (nb > 0 && !s.done) commit_front();
+
+  if (COUNT) {
+    __shared__ unsigned long long s_cnt[2];
+    __syncthreads();
+    if (tid == 0) s_cnt[0] = s_cnt[1] = 0;
+    __syncthreads();
+    atomicAdd(&s_cnt[0], ntest);
+    atomicAdd(&s_cnt[1], (unsigned long long)s.count);
+    __syncthreads();
+    if (tid == 0) {
+      atomicAdd(&cnt->tests_fwd, s_cnt[0]);
+      atomicAdd(&cnt->composited, s_cnt[1]);
+    }
+  }
+  if (!inside) return;
+  const float res = s.sat ? 0.f : s.Trem;  // render.py:210
+  rgb[3 * pix + 0] = fmaf(bg0, res, s.rad0);
+  rgb[3 * pix + 1] = fmaf(bg1, res, s.rad1);
+  rgb[3 * pix + 2] = fmaf(bg2, res, s.rad2);
+  overdraw[pix] = s.count;
+  residual[pix] = res;
+  cache.last[pix] = s.count - 1;  // index into the commit sequence
+  cache.sat[pix] = s.sat ? 1 : 0;
+  cache.t_k[pix] = s.sat ? s.tk : res;
+  cache.tau_hi[pix] = s.thi;
+  cache.tau_lo[pix] = s.tlo;
+  cache.P_end[pix] = s.P;
+  cache.ck_idx[pix] = s.ck;
+  cache.P_ck[pix] = s.Pck;
+  cache.e_k[3 * pix + 0] = s.ek0;
+  cache.e_k[3 * pix + 1] = s.ek1;
+  cache.e_k[3 * pix + 2] = s.ek2;
+  cache.theta0[3 * pix + 0] = s.sea0 - s.ek0 * s.sa;
+  cache.theta0[3 * pix + 1] = s.sea1 - s.ek1 * s.sa;
+  cache.theta0[3 * pix + 2] = s.sea2 - s.ek2 * s.sa;
+}
+
+// ---------------------------------------------------------------------------
+// K4x
+// ---------------------------------------------------------------------------
+constexpr int XRED_STRIDE = 36;
+constexpr size_t BWDX_SMEM = sizeof(float) * NMOM * XRED_STRIDE * (TILE_PIX / 32);
+
+template <int FAM, bool COUNT>
+__global__ void __launch_bounds__(TILE_PIX)
+    k_blend_bwd_x(const float4* __restrict__ records, const float4* __restrict__ bframe,
+                  const uint32_t* __restrict__ pairs, const int32_t* __restrict__ seq,
+                  int max_splats, CamDev cam, ModelDev m, float cutoff, double near_plane,
+                  float bg0, float bg1, float bg2, const float* __restrict__ seed,
+                  PixCache cache, double* __restrict__ moments, uint8_t* __restrict__ touched,
+                  Counters* __restrict__ cnt) {
+  extern __shared__ float smem_red[];
+  const int tile = blockIdx.x;
+  const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int px = tx * TILE + (tid & (TILE - 1)), py = ty * TILE + (tid >> 4);
+  const bool inside = px < cam.W && py < cam.H;
+  BwdPix st;
+  bwd_load(st, cam, px, py, cache, seed, bg0, bg1, bg2);
+  const int32_t* myseq = seq + (size_t)(inside ? py * cam.W + px : 0) * max_splats;
+  float* red = smem_red + (tid >> 5) * NMOM * XRED_STRIDE;
+  const float gam = (FAM == FAM_EXP) ? 1.0f : m.c;
+  const float inv_f = (float)(1.0 / cam.f);
+  const float Y0 = (float)SH_C0;
+  unsigned long long ntest = 0, nent = 0;
+  int ptr = st.last;  // commit index, back to front
+
+  while (true) {
+    const int pos = ptr >= 0 ? myseq[ptr] : -1;
+    const int wpos = __reduce_max_sync(0xffffffffu, pos);
+    if (wpos < 0) break;
+    if (COUNT && lane == 0) ++nent;
+    const uint32_t rank = pairs[wpos];  // warp-uniform
+    float4 rec[REC_F4], bf[3];
+#pragma unroll
+    for (int k = 0; k < REC_F4; ++k) rec[k] = __ldg(records + (size_t)rank * REC_F4 + k);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) bf[k] = __ldg(bframe + (size_t)rank * 3 + k);
+    float dm2 = 0.f, ux = 0.f, uy = 0.f, uz = 0.f, dak = 0.f, e0 = 0.f, e1 = 0.f, e2 = 0.f;
+    if (pos == wpos) {
+      bwd_pixel<FAM>(st, rec, bf, ptr, cam, m, cutoff, near_plane, inv_f, gam, dm2, ux, uy, uz,
+                     dak, e0, e1, e2, ntest, COUNT);
+      --ptr;
+    }
+    const float ax = dm2 * ux, ay = dm2 * uy, az = dm2 * uz;
+    float* col = red + lane;
+    col[0 * XRED_STRIDE] = ax * ux;
+    col[1 * XRED_STRIDE] = ax * uy;
+    col[2 * XRED_STRIDE] = ax * uz;
+    col[3 * XRED_STRIDE] = ay * uy;
+    col[4 * XRED_STRIDE] = ay * uz;
+    col[5 * XRED_STRIDE] = az * uz;
+    col[6 * XRED_STRIDE] = ax;
+    col[7 * XRED_STRIDE] = ay;
+    col[8 * XRED_STRIDE] = az;
+    col[11 * XRED_STRIDE] = dak;
+    col[12 * XRED_STRIDE] = e0 * Y0;
+    col[13 * XRED_STRIDE] = e0 * st.pc.Y1;
+    col[14 * XRED_STRIDE] = e0 * st.pc.Y2;
+    col[15 * XRED_STRIDE] = e0 * st.pc.Y3;
+    col[16 * XRED_STRIDE] = e1 * Y0;
+    col[17 * XRED_STRIDE] = e1 * st.pc.Y1;
+    col[18 * XRED_STRIDE] = e1 * st.pc.Y2;
+    col[19 * XRED_STRIDE] = e1 * st.pc.Y3;
+    col[20 * XRED_STRIDE] = e2 * Y0;
+    col[21 * XRED_STRIDE] = e2 * st.pc.Y1;
+    col[22 * XRED_STRIDE] = e2 * st.pc.Y2;
+    col[23 * XRED_STRIDE] = e2 * st.pc.Y3;
+    __syncwarp();
+    if (lane < NMOM && lane != 9 && lane != 10) {
+      const float4* row = reinterpret_cast<const float4*>(red + lane * XRED_STRIDE);
+      const float4 a = row[0], b = row[1], c = row[2], d = row[3];
+      const float4 e = row[4], f = row[5], g = row[6], h = row[7];
+      const float sum = (((a.x + a.y) + (a.z + a.w)) + ((b.x + b.y) + (b.z + b.w))) +
+                        (((c.x + c.y) + (c.z + c.w)) + ((d.x + d.y) + (d.z + d.w))) +
+                        ((((e.x + e.y) + (e.z + e.w)) + ((f.x + f.y) + (f.z + f.w))) +
+                         (((g.x + g.y) + (g.z + g.w)) + ((h.x + h.y) + (h.z + h.w))));
+      if (sum != 0.f) {
+        atomicAdd(&moments[(size_t)rank * NMOM + lane], (double)sum);
+        touched[rank] = 1;
+      }
+    }
+    __syncwarp();
+  }
+
+  if (COUNT) {
+    __shared__ unsigned long long s_cnt[2];
+    __syncthreads();
+    if (tid == 0) s_cnt[0] = s_cnt[1] = 0;
+    __syncthreads();
+    atomicAdd(&s_cnt[0], ntest);
+    atomicAdd(&s_cnt[1], nent);
+    __syncthreads();
+    if (tid == 0) {
+      atomicAdd(&cnt->tests_bwd, s_cnt[0]);
+      atomicAdd(&cnt->entries_bwd, s_cnt[1]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+template <class K>
+static void set_smem(K k, size_t bytes) {
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       (int)cudaSharedmemCarveoutMaxShared);
+}
+
+template <int FAM>
+static void launch_fwd_x_fam(bool count, int n_tiles, const FwdXArgs& a, const CamDev& cam,
+                             const ModelDev& m, const PixCache& cache, Counters* cnt,
+                             cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    set_smem(k_blend_fwd_x<FAM, true>, FWDX_SMEM);
+    set_smem(k_blend_fwd_x<FAM, false>, FWDX_SMEM);
+    attr = true;
+  }
+  auto k = count ? k_blend_fwd_x<FAM, true> : k_blend_fwd_x<FAM, false>;
+  k<<<n_tiles, TILE_PIX, FWDX_SMEM, s>>>(a.records, a.pairs, a.ranges, a.zlo_rank, a.order, cam, m,
+                                         a.max_splats, a.cutoff, a.near_plane, a.bg[0], a.bg[1],
+                                         a.bg[2], a.rgb, a.overdraw, a.residual, cache, a.seq,
+                                         a.overflow, cnt);
+}
+
+void launch_blend_fwd_x(bool count, int n_tiles, const FwdXArgs& a, const CamDev& cam,
+                        const ModelDev& m, const PixCache& cache, Counters* cnt, cudaStream_t s) {
+  if (n_tiles == 0) return;
+  switch (m.fam) {
+    case FAM_EXP: launch_fwd_x_fam<FAM_EXP>(count, n_tiles, a, cam, m, cache, cnt, s); break;
+    case FAM_LIN: launch_fwd_x_fam<FAM_LIN>(count, n_tiles, a, cam, m, cache, cnt, s); break;
+    case FAM_QUAD: launch_fwd_x_fam<FAM_QUAD>(count, n_tiles, a, cam, m, cache, cnt, s); break;
+    case FAM_BLEND: launch_fwd_x_fam<FAM_BLEND>(count, n_tiles, a, cam, m, cache, cnt, s); break;
+    case FAM_POW: launch_fwd_x_fam<FAM_POW>(count, n_tiles, a, cam, m, cache, cnt, s); break;
+    default: launch_fwd_x_fam<FAM_SOFT>(count, n_tiles, a, cam, m, cache, cnt, s); break;
+  }
+}
+
+template <int FAM>
+static void launch_bwd_x_fam(bool count, int n_tiles, const BwdXArgs& a, const CamDev& cam,
+                             const ModelDev& m, const PixCache& cache, Counters* cnt,
+                             cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    set_smem(k_blend_bwd_x<FAM, true>, BWDX_SMEM);
+    set_smem(k_blend_bwd_x<FAM, false>, BWDX_SMEM);
+    attr = true;
+  }
+  auto k = count ? k_blend_bwd_x<FAM, true> : k_blend_bwd_x<FAM, false>;
+  k<<<n_tiles, TILE_PIX, BWDX_SMEM, s>>>(a.records, a.bframe, a.pairs, a.seq, a.max_splats, cam, m,
+                                         a.cutoff, a.near_plane, a.bg[0], a.bg[1], a.bg[2],
+                                         a.seed, cache, a.moments, a.touched, cnt);
+}
+
+void launch_blend_bwd_x(bool count, int n_tiles, const BwdXArgs& a, const CamDev& cam,
+                        const ModelDev& m, const PixCache& cache, Counters* cnt, cudaStream_t s) {
+  if (n_tiles == 0) return;
+  switch (m.fam) {
+    case FAM_EXP: launch_bwd_x_fam<FAM_EXP>(count, n_tiles, a, cam, m, cache, cnt, s); break;
+    case FAM_LIN: launch_bwd_x_fam<FAM_LIN>(count, n_tiles, a, cam, m, cache, cnt, s); break;
+    case FAM_QUAD: launch_bwd_x_fam<FAM_QUAD>(count, n_tiles, a, cam, m, cache, cnt, s); break;
+    case FAM_BLEND: launch_bwd_x_fam<FAM_BLEND>(count, n_tiles, a, cam, m, cache, cnt, s); break;
+    case FAM_POW: launch_bwd_x_fam<FAM_POW>(count, n_tiles, a, cam, m, cache, cnt, s); break;
+    default: launch_bwd_x_fam<FAM_SOFT>(count, n_tiles, a, cam, m, cache, cnt, s); break;
+  }
+}
+
+}  // namespace nxs

@@ -117,6 +117,37 @@ struct FwdArgs {
   float* residual;
 };
 
+// exact-order mode (K3x/K4x)
+struct FwdXArgs {
+  const float4* records;
+  const uint32_t* pairs;
+  const int2* ranges;
+  const float* zlo_rank;
+  const uint32_t* order;
+  int max_splats;
+  float cutoff;
+  double near_plane;
+  float bg[3];
+  float* rgb;
+  int32_t* overdraw;
+  float* residual;
+  int32_t* seq;
+  unsigned long long* overflow;
+};
+struct BwdXArgs {
+  const float4* records;
+  const float4* bframe;
+  const uint32_t* pairs;
+  const int32_t* seq;
+  int max_splats;
+  float cutoff;
+  double near_plane;
+  float bg[3];
+  const float* seed;
+  double* moments;
+  uint8_t* touched;
+};
+
 struct Counters {
   unsigned long long tests_fwd, composited, tests_bwd, entries_bwd;
 };

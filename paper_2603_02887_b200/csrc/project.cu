@@ -79,9 +79,73 @@ __device__ __forceinline__ double dkey_inv(unsigned long long k) {
   return __longlong_as_double((long long)u);
 }
 
+// Lower bound of the camera depth of the ray-peak point over every pixel where
+// the Gaussian can be valid; since x'_z = t·d'_z with d'_z = 1/|h|, every valid
+// pixel has t >= z_lo·|h| (exact-order mode).
+// Peak points x satisfy (x - b')ᵀA'x = 0: in A'-whitened coordinates y = Lx
+// they lie on the sphere |y - c| = |c|, c = Lb'/2, and validity (m2 <= r²)
+// keeps them within distance r of the sphere point 2c — a spherical cap.  The
+// depth x'_z = wᵀy (w = L⁻ᵀe_z, |w| = σ_z) is minimised over that cap in
+// closed form: z_lo = b'_z/2 + R σ_z cos(min(π, α + φ)), R = |c| = √(bᵀAb)/2,
+// cos α = (b'_z/2)/(R σ_z), cos φ = 1 - r²/(2R²).  Far tighter than the
+// ellipsoid's own minimum depth b'_z - r σ_z (used when R degenerates).
+__device__ __forceinline__ double z_lower(const float* __restrict__ centers,
+                                          const float* __restrict__ scales,
+                                          const float* __restrict__ quats,
+                                          const float* __restrict__ opacities, int64_t g,
+                                          const CamDev& cam, double cutoff) {
+  const float4 q4 = reinterpret_cast<const float4*>(quats)[g];
+  double qw = q4.x, qx = q4.y, qy = q4.z, qz = q4.w;
+  double nq = sqrt(((qw * qw + qx * qx) + qy * qy) + qz * qz);
+  double inq = 1.0 / nq;
+  double w = qw * inq, x = qx * inq, y = qy * inq, z = qz * inq;
+  const double R[9] = {1.0 - 2.0 * (y * y + z * z), 2.0 * (x * y - w * z), 2.0 * (x * z + w * y),
+                       2.0 * (x * y + w * z),       1.0 - 2.0 * (x * x + z * z), 2.0 * (y * z - w * x),
+                       2.0 * (x * z - w * y),       2.0 * (y * z + w * x), 1.0 - 2.0 * (x * x + y * y)};
+  const double s[3] = {(double)scales[3 * g + 0], (double)scales[3 * g + 1],
+                       (double)scales[3 * g + 2]};
+  const double b0 = (double)centers[3 * g + 0] - cam.o[0];
+  const double b1 = (double)centers[3 * g + 1] - cam.o[1];
+  const double b2 = (double)centers[3 * g + 2] - cam.o[2];
+  double szz = 0.0, bAb = 0.0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    // camera z of Gaussian axis k, and the offset's component along it
+    const double mk = (cam.R[2] * R[0 + k] + cam.R[5] * R[3 + k]) + cam.R[8] * R[6 + k];
+    const double uk = (b0 * R[0 + k] + b1 * R[3 + k]) + b2 * R[6 + k];
+    szz += (mk * s[k]) * (mk * s[k]);
+    bAb += (uk / s[k]) * (uk / s[k]);
+  }
+  const double sz = sqrt(szz);
+  const double op = (double)opacities[g];
+  const double r2 = (op >= cutoff ? 2.0 * ln_det(op / cutoff) : 0.0) * (1.0 + 1e-4) + 1e-4;
+  const double bz = (cam.R[2] * b0 + cam.R[5] * b1) + cam.R[8] * b2;
+  const double zell = bz - sqrt(r2) * sz;  // the ellipsoid's own minimum depth
+  const double Rs = 0.5 * sqrt(bAb);
+  if (!(Rs > 0.0) || !(sz > 0.0)) return zell;
+  double ca = (0.5 * bz) / (Rs * sz);
+  ca = ca > 1.0 ? 1.0 : (ca < -1.0 ? -1.0 : ca);
+  const double cf = 1.0 - r2 / (2.0 * Rs * Rs);
+  double caf;
+  if (cf <= -ca) {
+    caf = -1.0;  // the cap reaches the sphere's deepest point against w
+  } else {
+    const double sa = sqrt(fmax(0.0, 1.0 - ca * ca)), sf = sqrt(fmax(0.0, 1.0 - cf * cf));
+    caf = ca * cf - sa * sf;
+  }
+  const double zc = 0.5 * bz + Rs * sz * caf;
+  // guard rounding: never above the true bound by more than a few ulps
+  const double zlo = zc - 1e-9 * fabs(bz) - 1e-12;
+  return (zlo == zlo) ? fmax(zlo, zell) : zell;
+}
+
 // K0: fp64 view depth (μ - o)·forward (compensated), its order-preserving
 // u64 key (64-bit fallback sort), and the NaN-free min/max key of the batch.
-__global__ void k_depth(const float* __restrict__ centers, int64_t P, CamDev cam,
+// With `zmode` (exact-order mode) the sort key is z_lo instead of the
+// centre depth.
+__global__ void k_depth(const float* __restrict__ centers, const float* __restrict__ scales,
+                        const float* __restrict__ quats, const float* __restrict__ opacities,
+                        int64_t P, CamDev cam, double cutoff, int zmode,
                         double* __restrict__ depth, unsigned long long* __restrict__ key64,
                         uint32_t* __restrict__ idx, unsigned long long* __restrict__ kminmax) {
   __shared__ unsigned long long s_min[8], s_max[8];
@@ -92,7 +156,8 @@ __global__ void k_depth(const float* __restrict__ centers, int64_t P, CamDev cam
     double b1 = (double)centers[3 * i + 1] - cam.o[1];
     double b2 = (double)centers[3 * i + 2] - cam.o[2];
     // forward = third column of the camera rotation
-    const double d = dot3_compensated(b0, b1, b2, cam.R[2], cam.R[5], cam.R[8]);
+    const double d = zmode ? z_lower(centers, scales, quats, opacities, i, cam, cutoff)
+                           : dot3_compensated(b0, b1, b2, cam.R[2], cam.R[5], cam.R[8]);
     depth[i] = d;
     const unsigned long long k = dkey(d);
     key64[i] = k;
@@ -186,8 +251,9 @@ __global__ void k_rank_of(const uint32_t* __restrict__ order, int64_t P,
 }
 
 struct ProjOut {
-  unsigned long long* n_tiles;  // per rank tile count
-  int4* rects;                  // per rank tile rectangle
+  const double* zlo;            // exact-order mode: z_lo per Gaussian (sort key), else null
+  float* zlo_rank;              // exact-order mode: z_lo per rank, rounded down
+  int4* rects;                  // per Gaussian tile rectangle
   float4* records;              // per rank 8 x float4
   float4* bframe;               // per rank 3 x float4: rows of B (backward only)
   unsigned long long* straddle; // counter
@@ -499,6 +565,7 @@ __global__ void __launch_bounds__(PROJ_CHUNK)
       }
       project_one(prm, g, cam, cutoff, near_plane, out, so.rec[tid], so.bf[tid]);
       so.rank[tid] = r;
+      if (out.zlo_rank) out.zlo_rank[r] = __double2float_rd(out.zlo[g]);
     } else {
       so.rank[tid] = -1;
     }
@@ -567,11 +634,13 @@ __global__ void k_tile_ranges(const uint32_t* __restrict__ keys, int64_t n,
 }
 
 // host launchers
-void launch_depth(const float* centers, int64_t P, const CamDev& cam, double* depth,
-                  unsigned long long* key64, uint32_t* idx, unsigned long long* kminmax,
-                  cudaStream_t s) {
+void launch_depth(const float* centers, const float* scales, const float* quats,
+                  const float* opacities, int64_t P, const CamDev& cam, double cutoff, int zmode,
+                  double* depth, unsigned long long* key64, uint32_t* idx,
+                  unsigned long long* kminmax, cudaStream_t s) {
   if (P == 0) return;
-  k_depth<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(centers, P, cam, depth, key64, idx, kminmax);
+  k_depth<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(centers, scales, quats, opacities, P, cam,
+                                                      cutoff, zmode, depth, key64, idx, kminmax);
 }
 void launch_key32(const double* depth, int64_t P, const unsigned long long* kminmax,
                   uint32_t* key, cudaStream_t s) {
@@ -591,10 +660,10 @@ void launch_rank_of(const uint32_t* order, int64_t P, uint32_t* rank_of, cudaStr
 void launch_project(const float* centers, const float* scales, const float* quats,
                     const float* opacities, const float* sh, int C, int64_t P,
                     const uint32_t* rank_of, const CamDev& cam, double cutoff, double near_plane,
-                    unsigned long long* n_tiles, int4* rects, float4* records, float4* bframe,
-                    unsigned long long* straddle, cudaStream_t s) {
+                    const double* zlo, float* zlo_rank, int4* rects, float4* records,
+                    float4* bframe, unsigned long long* straddle, cudaStream_t s) {
   if (P == 0) return;
-  ProjOut o{n_tiles, rects, records, bframe, straddle};
+  ProjOut o{zlo, zlo_rank, rects, records, bframe, straddle};
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

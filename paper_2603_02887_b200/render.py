@@ -18,11 +18,11 @@ the device as float32 each call — the reference mutates them in place
 between calls, optimizer.py:382) or a :class:`DeviceScene` of resident
 float32 CUDA tensors (the fast path; nothing crosses PCIe but the outputs).
 
-Ordering (reference render.py:350-358): ``chunk_size=1``
-(global front-to-back order, "Mode G") runs on the device.  The exact
-per-pixel order of ``chunk_size=None`` and chunked orders ``C > 1`` are not
-implemented yet and raise ``NotImplementedError`` — never a silent
-approximation.
+Ordering (reference render.py:171, 350-358): the default
+``chunk_size=None`` (exact per-pixel order by peak depth, "Mode X") and
+``chunk_size=1`` (global front-to-back order, "Mode G") run on the device.
+Chunked orders ``C > 1`` are not implemented yet and raise
+``NotImplementedError`` — never a silent approximation.
 """
 from __future__ import annotations
 
@@ -199,12 +199,10 @@ def _effective_chunk(chunk_size, n: int) -> int:
 
 
 def _check_mode(chunk: int):
-    if chunk != 1:
-        what = "the exact per-pixel order (chunk_size=None)" if chunk == 0 else \
-            f"chunked order chunk_size={chunk}"
+    if chunk > 1:
         raise NotImplementedError(
-            f"{what} is not implemented on the device yet; use chunk_size=1 "
-            "(global front-to-back order)")
+            f"chunked order chunk_size={chunk} is not implemented on the device yet; use "
+            "chunk_size=None (exact per-pixel order) or chunk_size=1 (global depth order)")
 
 
 def _model_struct(model):
@@ -236,6 +234,8 @@ def forward_device(view, dev: DeviceScene, camera, model, background, *, max_spl
         view.forward(dev, _native.make_camera(camera), ms, opts, bg, out[0], out[1], out[2],
                      stream=stream)
     except _native.NxsError as e:
+        if e.code == _native.NXS_ERR_OVERFLOW:
+            raise RuntimeError(f"{e} (exact order could not be guaranteed)") from e
         if e.code == _native.NXS_ERR_GEOMETRY:
             raise NotImplementedError(str(e)) from e
         if e.code == _native.NXS_ERR_INVALID:

@@ -25,13 +25,13 @@ def _dev(sc):
     return DeviceScene.from_arrays(sc)
 
 
-def gpu_run(sc, cam, model, bg, seed=None, count=False, **kw):
+def gpu_run(sc, cam, model, bg, seed=None, count=False, chunk_size=1, **kw):
     import torch
     from paper_2603_02887_b200 import _native, backward_device, forward_device
     dev = _dev(sc)
     view = _native.View()
-    rgb, od, res = forward_device(view, dev, cam, model, bg, chunk_size=1, count_events=count,
-                                  **kw)
+    rgb, od, res = forward_device(view, dev, cam, model, bg, chunk_size=chunk_size,
+                                  count_events=count, **kw)
     out = {"rgb": rgb.double().cpu().numpy(), "overdraw": od.cpu().numpy(),
            "residual": res.double().cpu().numpy(), "view": view, "dev": dev}
     if seed is not None:
@@ -317,8 +317,13 @@ def test_dropin_api_shapes_and_cache():
     np.testing.assert_array_equal(cache["sat"], ref["sat"])
     assert close(cache["theta0"], ref["theta0"], rtol=1e-4, atol=1e-5).all()
     assert close(cache["e_k"], ref["e_k"]).all() and close(cache["t_k"], ref["t_k"]).all()
+    out = nx.render(arrs, cam, model, bg)  # default chunk_size=None: exact order
+    golden = d["softplus_20__none__rgb"]
+    ref = O.forward(sc, cam, MODELS["softplus_20"], bg, chunk_size=None)
+    keep = ~ref["mask"].reshape(16, 24)
+    assert close(out.rgb, golden).all(axis=2)[keep].all()
     with pytest.raises(NotImplementedError):
-        nx.render(arrs, cam, model, bg)  # chunk_size=None: exact order not on device yet
+        nx.render(arrs, cam, model, bg, chunk_size=3)
     with pytest.raises(ValueError):
         nx.render_backward(arrs, cam, model, bg, {"rad": 0}, d["seed"], chunk_size=1)
     # the reference's own objects are accepted (duck-typed)
@@ -405,3 +410,87 @@ def test_depth_order_edge_cases_match_c_restatement(case):
     order, *_ = _binning_of(got["view"], len(sc))
     ref = oracle.binning(sc, cam)
     np.testing.assert_array_equal(order, ref["order"])
+
+
+# ---------------------------------------------------------------------------
+# exact per-pixel order (reference default chunk_size=None, "Mode X")
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name", list(MODELS))
+def test_exact_order_small_scene_matches_reference_golden(name):
+    d = load("golden_small.npz")
+    cam, sc, bg = cam_from(d), scene_from(d), d["bg"]
+    tag = f"{name}__none"
+    got = gpu_run(sc, cam, MODELS[name], bg, chunk_size=None)
+    ref = O.forward(sc, cam, MODELS[name], bg, chunk_size=None)
+    golden = {"rad": d[tag + "__rgb"], "residual": d[tag + "__residual"],
+              "overdraw": d[tag + "__overdraw"]}
+    bad, kept = check_forward(got, golden, ref["mask"], cam.height, cam.width)
+    assert bad == 0 and kept > 0.9 * cam.width * cam.height, (bad, kept)
+    if name + "__none__g_centers" in d and not ref["mask"].any():
+        g = gpu_run(sc, cam, MODELS[name], bg, seed=d["seed"], chunk_size=None)
+        golden_g = {k: d[f"{name}__none__g_{k}"] for k in GRAD_FIELDS}
+        _, mass = O.render_with_gradients(sc, cam, MODELS[name], bg, d["seed"], chunk_size=None,
+                                          with_mass=True)[1]
+        strict, massf, total = grad_report(g["grads"], golden_g, mass)
+        assert massf == 0 and strict <= max(1, total // 1000), (strict, massf, total)
+
+
+@pytest.mark.parametrize("name", list(MODELS))
+def test_exact_order_c1_matches_oracle(name):
+    d = load("golden_c1.npz")
+    cam, sc, bg = cam_from(d), scene_from(d), d["bg"]
+    model = MODELS[name]
+    fwd = O.forward(sc, cam, model, bg, chunk_size=None, keep_state=True)
+    seed = d["seed"].reshape(-1, 3) * (~fwd["mask"])[:, None]
+    g_ref, mass = O.backward(sc, cam, model, bg, fwd, seed, with_mass=True)
+    got = gpu_run(sc, cam, model, bg, seed=seed.reshape(cam.height, cam.width, 3),
+                  chunk_size=None)
+    bad, kept = check_forward(got, fwd, fwd["mask"], cam.height, cam.width)
+    assert bad == 0 and kept >= 0.95 * cam.width * cam.height, (bad, kept)
+    strict, massf, total = grad_report(got["grads"], g_ref, mass)
+    assert massf == 0, (strict, massf, total)
+    assert strict <= max(2, total // 1000), (strict, massf, total)
+    assert got["stats"]["n_overflow"] == 0
+
+
+@pytest.mark.parametrize("name", ["exponential", "softplus_20", "blended_0.5"])
+def test_exact_order_c2_sampled_pixels_match_oracle(name):
+    sc = O.round_scene_f32(O.canonical_scene(100_000, seed=0))
+    cam = O.canonical_camera(512, 512)
+    bg = np.array([0.1, 0.05, 0.2], dtype=np.float32).astype(np.float64)
+    model = MODELS[name]
+    px = np.random.default_rng(12).choice(512 * 512, 128, replace=False)
+    fwd = O.forward(sc, cam, model, bg, chunk_size=None, pixels=px, keep_state=True, batch=16)
+    seed_px = O.canonical_seed(512, 512, 0).reshape(-1, 3)[px].astype(np.float32).astype(
+        np.float64) * (~fwd["mask"])[:, None]
+    g_ref, mass = O.backward(sc, cam, model, bg, fwd, seed_px, with_mass=True)
+    seed_full = np.zeros((512 * 512, 3))
+    seed_full[px] = seed_px
+    got = gpu_run(sc, cam, model, bg, seed=seed_full.reshape(512, 512, 3), chunk_size=None)
+    keep = ~fwd["mask"]
+    ok = close(got["rgb"].reshape(-1, 3)[px], fwd["rad"]).all(1) & \
+        (got["overdraw"].reshape(-1)[px] == fwd["overdraw"]) & \
+        close(got["residual"].reshape(-1)[px], fwd["residual"])
+    assert (keep & ~ok).sum() == 0, int((keep & ~ok).sum())
+    assert keep.sum() >= 0.8 * len(px), int(keep.sum())
+    strict, massf, total = grad_report(got["grads"], g_ref, mass)
+    assert massf == 0, (strict, massf, total)
+
+
+def test_exact_order_pending_overflow_is_reported():
+    """A column of Gaussians elongated along the view axis: z_lo far below
+    every peak depth, so more than 32 entries are pending at once."""
+    import paper_2603_02887_b200 as nx
+    k = 40
+    cen = np.column_stack([np.zeros(k), np.zeros(k), np.linspace(12.0, 13.0, k)])
+    sc = O.Scene(cen, np.tile([0.3, 0.3, 3.0], (k, 1)), np.tile([1.0, 0, 0, 0], (k, 1)),
+                 np.full(k, 0.05), np.ones((k, 3, 1)))
+    cam = O.look_at([0, 0, 0], [0, 0, 1], [0, 1, 0], 40.0, 16, 16)
+    with pytest.raises(RuntimeError, match="overflow"):
+        gpu_run(sc, cam, MODELS["exponential"], np.zeros(3), chunk_size=None)
+    # the global order has no pending state and renders it fine
+    gpu_run(sc, cam, MODELS["exponential"], np.zeros(3), chunk_size=1)
+    arrs = nx.SceneArrays(sc.centers, sc.scales, sc.quats, sc.opacities, sc.sh)
+    with pytest.raises(RuntimeError):
+        nx.render(arrs, cam, MODELS["exponential"], np.zeros(3))
