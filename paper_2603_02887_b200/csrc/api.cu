@@ -544,7 +544,7 @@ retry_sort:
     }
     if (exact) {
       // ---- K3x exact-order forward (single phase)
-      NXS_CUDA(ensure_n<int32_t>(v->seq, npix * std::max(1, opts->max_splats)));
+      NXS_CUDA(ensure_n<int32_t>(v->seq, npix * std::max(1, opts->max_splats)));  // [slot][pixel]
       FwdXArgs xa{v->records.as<float4>(), v->pv_ph[ph].as<uint32_t>(),
                   v->ranges_ph[ph].as<int2>(), v->zlo_rank.as<float>(), v->idx_out.as<uint32_t>(),
                   opts->max_splats, (float)opts->alpha_cutoff, opts->near_plane,

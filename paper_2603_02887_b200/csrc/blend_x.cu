@@ -25,7 +25,9 @@ namespace nxs {
 
 constexpr int XBUF = 32;     // pending entries per pixel
 constexpr int XBATCH = 64;   // list entries staged per batch
-constexpr size_t FWDX_SMEM = sizeof(float4) * XBATCH * REC_F4 + sizeof(uint32_t) * XBATCH +
+// records of the current and the previous batch stay staged (a ring of
+// 2*XBATCH): most commits are of recently tested entries
+constexpr size_t FWDX_SMEM = sizeof(float4) * 2 * XBATCH * REC_F4 + sizeof(uint32_t) * XBATCH +
                              sizeof(float) * XBATCH + (sizeof(float) + sizeof(int)) * XBUF * TILE_PIX;
 
 struct FwdXPix {
@@ -110,8 +112,8 @@ __global__ void __launch_bounds__(TILE_PIX)
                   float* __restrict__ residual, PixCache cache, int32_t* __restrict__ seq,
                   unsigned long long* __restrict__ overflow, Counters* __restrict__ cnt) {
   extern __shared__ float4 smem_dyn[];
-  float4(*s_rec)[REC_F4] = reinterpret_cast<float4(*)[REC_F4]>(smem_dyn);
-  uint32_t* s_rank = reinterpret_cast<uint32_t*>(smem_dyn + XBATCH * REC_F4);
+  float4(*s_ring)[REC_F4] = reinterpret_cast<float4(*)[REC_F4]>(smem_dyn);  // [2*XBATCH]
+  uint32_t* s_rank = reinterpret_cast<uint32_t*>(smem_dyn + 2 * XBATCH * REC_F4);
   float* s_zlo = reinterpret_cast<float*>(s_rank + XBATCH);
   float* bt = s_zlo + XBATCH;                                 // [XBUF][TILE_PIX] pending t
   int* bp = reinterpret_cast<int*>(bt + XBUF * TILE_PIX);     // [XBUF][TILE_PIX] list position
@@ -124,7 +126,8 @@ __global__ void __launch_bounds__(TILE_PIX)
   const PixelConst pc = pixel_setup(cam, px, py);
   const float hnorm = sqrtf(__fmaf_rn(pc.hx, pc.hx, __fmaf_rn(pc.hy, pc.hy, 1.0f)));
   const int pix = py * cam.W + px;
-  int32_t* myseq = seq + (size_t)(inside ? pix : 0) * max_splats;
+  const size_t npix = (size_t)cam.W * cam.H;
+  int32_t* myseq = seq + (inside ? pix : 0);  // [slot][pixel]: lanes read/write contiguously
 
   FwdXPix s{};
   s.P = 1.f;
@@ -134,24 +137,34 @@ __global__ void __launch_bounds__(TILE_PIX)
   s.ek2 = bg2;
   s.ck = -1;
   s.done = !inside || max_splats <= 0;
-  int nb = 0;  // pending entries: descending by (t, index), the next commit at nb-1
+  // pending entries: a ring of XBUF slots, ascending by (t, index) from the
+  // head; new entries (lists are in z_lo order) usually append at the tail
+  int nb = 0, head = 0;
   unsigned long long ntest = 0;
 
   // commit the smallest pending entry: re-read its record (L1/L2; every
   // pixel of the tile commits the same few entries) and composite it
+  int ring_lo = 0;  // list positions [ring_lo, current batch end) are staged
   auto commit_front = [&]() {
+    const int pos = bp[head * TILE_PIX + tid];
+    head = (head + 1) & (XBUF - 1);
     --nb;
-    const int pos = bp[nb * TILE_PIX + tid];
-    const float4* rec = records + (size_t)pairs[pos] * REC_F4;
     float4 r[REC_F4];
+    if (pos >= ring_lo) {
+      const float4* rec = s_ring[pos % (2 * XBATCH)];
 #pragma unroll
-    for (int k = 0; k < REC_F4; ++k) r[k] = __ldg(rec + k);
+      for (int k = 0; k < REC_F4; ++k) r[k] = rec[k];
+    } else {
+      const float4* rec = records + (size_t)pairs[pos] * REC_F4;
+#pragma unroll
+      for (int k = 0; k < REC_F4; ++k) r[k] = __ldg(rec + k);
+    }
     TestOut t;
     float tpk;
     test_with_t(r, cam, px, py, pc, hnorm, cutoff, near_plane, t, tpk);  // valid by construction
     float E0, E1, E2;
     emission(r[4], r[5], r[6], pc, E0, E1, E2);
-    myseq[s.count] = pos;
+    myseq[(size_t)s.count * npix] = pos;
     composite<FAM>(s, m, max_splats, t.alpha, E0, E1, E2);
   };
 
@@ -165,16 +178,19 @@ __global__ void __launch_bounds__(TILE_PIX)
       s_zlo[tid] = zlo_rank[rk];
     }
     __syncthreads();
+    // stage this batch into the ring slot it maps to (positions are consecutive)
     for (int k = tid; k < n * REC_F4; k += TILE_PIX) {
       const int e = k >> 3, part = k & 7;
-      s_rec[e][part] = records[(size_t)s_rank[e] * REC_F4 + part];
+      s_ring[(base + e) % (2 * XBATCH)][part] = records[(size_t)s_rank[e] * REC_F4 + part];
     }
+    ring_lo = max(rg.x, base - XBATCH);
     __syncthreads();
     if (!s.done) {
       for (int j = 0; j < n; ++j) {
+        const float4* s_rec_j = s_ring[(base + j) % (2 * XBATCH)];
         // every remaining entry has t >= bound: pending entries below it are final
         const float bound = s_zlo[j] * hnorm;
-        while (nb > 0 && bt[(nb - 1) * TILE_PIX + tid] < bound) {
+        while (nb > 0 && bt[head * TILE_PIX + tid] < bound) {
           commit_front();
           if (s.done) break;
         }
@@ -182,35 +198,38 @@ __global__ void __launch_bounds__(TILE_PIX)
         if (COUNT) ++ntest;
         TestOut t;
         float tpk;
-        if (!test_with_t(s_rec[j], cam, px, py, pc, hnorm, cutoff, near_plane, t, tpk)) continue;
+        if (!test_with_t(s_rec_j, cam, px, py, pc, hnorm, cutoff, near_plane, t, tpk)) continue;
         if (nb == XBUF) {
           // overflow: the order is no longer guaranteed for this pixel
           atomicAdd(overflow, 1ull);
           commit_front();
           if (s.done) break;
         }
-        // insert (t, index) keeping the buffer descending
+        // insert (t, index) keeping the ring ascending from the head
         const int pos = base + j;
-        int k = nb;
+        int i = nb;
         uint32_t gid_new = 0xffffffffu;
-        while (k > 0) {
-          const float tk = bt[(k - 1) * TILE_PIX + tid];
-          bool smaller = tk < tpk;  // the element ahead commits after the new one
-          if (tk == tpk) {
+        while (i > 0) {
+          const int e = (head + i - 1) & (XBUF - 1);
+          const float te = bt[e * TILE_PIX + tid];
+          bool later = te > tpk;  // the pending entry commits after the new one
+          if (te == tpk) {
             if (gid_new == 0xffffffffu) gid_new = order[s_rank[j]];
-            smaller = order[pairs[bp[(k - 1) * TILE_PIX + tid]]] < gid_new;
+            later = order[pairs[bp[e * TILE_PIX + tid]]] > gid_new;
           }
-          if (!smaller) break;
-          bt[k * TILE_PIX + tid] = tk;
-          bp[k * TILE_PIX + tid] = bp[(k - 1) * TILE_PIX + tid];
-          --k;
+          if (!later) break;
+          const int f = (head + i) & (XBUF - 1);
+          bt[f * TILE_PIX + tid] = te;
+          bp[f * TILE_PIX + tid] = bp[e * TILE_PIX + tid];
+          --i;
         }
-        bt[k * TILE_PIX + tid] = tpk;
-        bp[k * TILE_PIX + tid] = pos;
+        const int f = (head + i) & (XBUF - 1);
+        bt[f * TILE_PIX + tid] = tpk;
+        bp[f * TILE_PIX + tid] = pos;
         ++nb;
       }
     }
-    if (__syncthreads_count(!s.done && true) == 0) break;
+    if (__syncthreads_count(!s.done) == 0) break;
   }
   // end of the list: everything pending is final, in order
   while (nb > 0 && !s.done) commit_front();
@@ -273,7 +292,8 @@ __global__ void __launch_bounds__(TILE_PIX)
   const bool inside = px < cam.W && py < cam.H;
   BwdPix st;
   bwd_load(st, cam, px, py, cache, seed, bg0, bg1, bg2);
-  const int32_t* myseq = seq + (size_t)(inside ? py * cam.W + px : 0) * max_splats;
+  const size_t npix = (size_t)cam.W * cam.H;
+  const int32_t* myseq = seq + (inside ? py * cam.W + px : 0);  // [slot][pixel]
   float* red = smem_red + (tid >> 5) * NMOM * XRED_STRIDE;
   const float gam = (FAM == FAM_EXP) ? 1.0f : m.c;
   const float inv_f = (float)(1.0 / cam.f);
@@ -282,10 +302,11 @@ __global__ void __launch_bounds__(TILE_PIX)
   int ptr = st.last;  // commit index, back to front
 
   while (true) {
-    const int pos = ptr >= 0 ? myseq[ptr] : -1;
+    const int pos = ptr >= 0 ? myseq[(size_t)ptr * npix] : -1;
     const int wpos = __reduce_max_sync(0xffffffffu, pos);
     if (wpos < 0) break;
     if (COUNT && lane == 0) ++nent;
+    const bool mine = pos == wpos;
     const uint32_t rank = pairs[wpos];  // warp-uniform
     float4 rec[REC_F4], bf[3];
 #pragma unroll
@@ -293,7 +314,7 @@ __global__ void __launch_bounds__(TILE_PIX)
 #pragma unroll
     for (int k = 0; k < 3; ++k) bf[k] = __ldg(bframe + (size_t)rank * 3 + k);
     float dm2 = 0.f, ux = 0.f, uy = 0.f, uz = 0.f, dak = 0.f, e0 = 0.f, e1 = 0.f, e2 = 0.f;
-    if (pos == wpos) {
+    if (mine) {
       bwd_pixel<FAM>(st, rec, bf, ptr, cam, m, cutoff, near_plane, inv_f, gam, dm2, ux, uy, uz,
                      dak, e0, e1, e2, ntest, COUNT);
       --ptr;
