@@ -63,7 +63,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--chunk", default="1",
-                   help="ordering: 1 = global depth order (default), none = exact per-pixel order")
+                   help="ordering: 1 = global depth order (default), none = exact per-pixel order, "
+                        "C > 1 = chunked order")
     p.add_argument("--first-phase", type=int, default=0,
                    help="ranks binned in the first depth phase (0 = automatic)")
     return p.parse_args()
@@ -295,7 +296,8 @@ def main():
                 "workload": (f"C3: {a.gaussians} Gaussians (canonical synthetic scene, seed 5), "
                              f"{W}x{H}, {model.describe()}, "
                              + ("chunk_size=1 (global depth order), " if a.chunk_size == 1 else
-                                "chunk_size=None (exact per-pixel order), ")
+                                "chunk_size=None (exact per-pixel order), " if a.chunk_size is None
+                                else f"chunk_size={a.chunk_size} (chunked order), ")
                              + f"fwd+bwd, {vpr} view(s) per GPU"
                              + (", NCCL all-reduce of gradients" if world > 1 else "")),
                 "gaussians": a.gaussians, "width": W, "height": H,

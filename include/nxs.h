@@ -69,8 +69,11 @@ extern "C" {
 #define NXS_FLAG_COUNT_EVENTS 1    /* count tests/composites (instrumented run) */
 #define NXS_FLAG_FULL_BINNING 2    /* bin every rank in one phase (no progressive binning) */
 
-/* ordering: opts.chunk_size (reference render(..., chunk_size=)) */
-#define NXS_CHUNK_EXACT 0          /* chunk_size=None: exact per-pixel depth order */
+/* ordering: opts.chunk_size (reference render(..., chunk_size=), render.py:350-358)
+ *   NXS_CHUNK_EXACT (None) or C >= count: one chunk, exact per-pixel t order
+ *   1: global centre-depth order
+ *   1 < C < count: chunks of C in centre-depth order, per-pixel t order within */
+#define NXS_CHUNK_EXACT 0
 
 /* TransmittanceModel (reference transmittance.py:54-79): variant + param */
 typedef struct {
@@ -93,7 +96,7 @@ typedef struct {
     int32_t max_splats;      /* default 128 */
     double alpha_cutoff;     /* default 1/255 */
     double near_plane;       /* default 1e-4 */
-    int32_t chunk_size;      /* NXS_CHUNK_EXACT (None) or >= 1 */
+    int32_t chunk_size;      /* NXS_CHUNK_EXACT (None) or >= 1, see above */
     int32_t flags;           /* NXS_FLAG_* */
     int64_t first_phase_ranks; /* progressive binning: ranks in the first depth
                                   phase (0 = automatic); later phases grow x8 */

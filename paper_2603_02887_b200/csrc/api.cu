@@ -26,6 +26,9 @@ void launch_key32(const double*, int64_t, const unsigned long long*, uint32_t*, 
 void launch_key_fixup(const uint32_t*, uint32_t*, const double*, int64_t, unsigned long long*,
                       cudaStream_t);
 void launch_rank_of(const uint32_t*, int64_t, uint32_t*, cudaStream_t);
+void launch_chunk_key(const float*, const float*, const float*, const float*, int64_t,
+                      const CamDev&, double, const uint32_t*, int, double*, unsigned long long*,
+                      uint32_t*, cudaStream_t);
 void launch_project(const float*, const float*, const float*, const float*, const float*, int,
                     int64_t, const uint32_t*, const CamDev&, double, double, const double*,
                     float*, int4*, float4*, float4*, unsigned long long*, cudaStream_t);
@@ -107,7 +110,7 @@ int bits_for(uint32_t n) {
 struct nxs_view {
   // per Gaussian
   Buf dkeys_in, dkeys_out, idx_in, idx_out, records, bframe, rects, ntiles, offsets, moments,
-      touched, depth, k32a, k32b, rank_of, zlo_rank, seq;
+      touched, depth, k32a, k32b, rank_of, rank_c, zlo_rank, seq;
   // per pair: sort scratch, and the sorted ranks of each depth phase
   Buf pk_in, pk_out, pv_in, pv_ph[MAX_PHASES];
   // per tile: phase ranges and virtual offsets, activity
@@ -142,7 +145,7 @@ struct nxs_view {
   void for_each_buf(F f) {
     Buf* all[] = {&dkeys_in, &dkeys_out, &idx_in,  &idx_out, &records, &bframe, &rects,
                   &ntiles,   &offsets,   &moments, &touched, &pk_in,   &pk_out,  &pv_in,  &active,
-                  &depth,    &k32a,      &k32b,    &rank_of, &zlo_rank, &seq,
+                  &depth,    &k32a,      &k32b,    &rank_of, &rank_c, &zlo_rank, &seq,
                   &c_last,   &c_sat,     &c_tk,    &c_thi,   &c_tlo,   &c_P,    &c_ck,
                   &c_Pck,    &c_ek,      &c_th0,   &r_rad,   &r_trem,  &r_count, &r_sea,
                   &r_sa,     &temp,      &dev_small};
@@ -320,12 +323,14 @@ int nxs_forward(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
                 !scene->sh))
     return fail(NXS_ERR_INVALID, "null scene array");
   if (P >= (int64_t)1 << 31) return fail(NXS_ERR_INVALID, "more than 2^31 Gaussians");
-  if (opts->chunk_size != 1 && opts->chunk_size != NXS_CHUNK_EXACT)
-    return fail(NXS_ERR_UNSUPPORTED,
-                "chunked order (chunk_size > 1) is not implemented on the device yet");
-  const bool exact = opts->chunk_size == NXS_CHUNK_EXACT;
-  if (exact && opts->max_splats > 4096)
-    return fail(NXS_ERR_INVALID, "exact order supports max_splats <= 4096");
+  if (opts->chunk_size < 0) return fail(NXS_ERR_INVALID, "chunk_size must be >= 0");
+  // per-pixel t order within chunks: one chunk (exact, 0, or C >= P) or
+  // chunks of C > 1 in centre-depth order; chunk_size 1 is the global order
+  const bool chunked = opts->chunk_size > 1 && (int64_t)opts->chunk_size < P;
+  const bool exact = opts->chunk_size == NXS_CHUNK_EXACT || (opts->chunk_size > 1 && !chunked);
+  const bool torder = exact || chunked;
+  if (torder && opts->max_splats > 4096)
+    return fail(NXS_ERR_INVALID, "t-ordered modes support max_splats <= 4096");
   if (!(opts->alpha_cutoff > 0.0) || !(opts->near_plane >= 0.0))
     return fail(NXS_ERR_INVALID, "alpha_cutoff must be > 0 and near >= 0");
 
@@ -375,8 +380,8 @@ int nxs_forward(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
   int n_ph = 0;
   {
     int64_t r1;
-    if ((opts->flags & NXS_FLAG_FULL_BINNING) || exact)
-      r1 = P;  // the exact order keeps per-pixel pending state: one phase
+    if ((opts->flags & NXS_FLAG_FULL_BINNING) || torder)
+      r1 = P;  // t-ordered modes keep per-pixel pending state: one phase
     else if (opts->first_phase_ranks > 0)
       r1 = opts->first_phase_ranks;
     else  // measured at C3: saturating models finish every tile within P/32
@@ -412,6 +417,14 @@ retry_sort:
     NXS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_scan,
                                            v->ntiles.as<unsigned long long>(),
                                            v->offsets.as<unsigned long long>(), (int)P, s));
+    if (chunked) {
+      size_t tmp_chunk = 0;
+      NXS_CUDA(cub::DeviceRadixSort::SortPairs(
+          nullptr, tmp_chunk, v->dkeys_in.as<unsigned long long>(),
+          v->dkeys_out.as<unsigned long long>(), v->idx_in.as<uint32_t>(),
+          v->idx_out.as<uint32_t>(), (int)P, 0, 64, s));
+      tmp_sort = std::max(tmp_sort, tmp_chunk);
+    }
     NXS_CUDA(v->temp.ensure(std::max(tmp_sort, tmp_scan)));
     // ---- K0 depth (+ min/max) and the stable depth sort
     NXS_CUDA(cudaMemsetAsync(dsmall + 6, 0xff, sizeof(unsigned long long), s));
@@ -436,17 +449,35 @@ retry_sort:
                        P, dsmall + 8, s);
       NXS_LAUNCHED("key_fixup");
     }
+    if (chunked) {
+      // chunk = centre-depth rank / C; lists in (chunk, z_lo) order
+      NXS_CUDA(ensure_n<uint32_t>(v->rank_c, P));
+      launch_rank_of(v->idx_out.as<uint32_t>(), P, v->rank_c.as<uint32_t>(), s);
+      NXS_LAUNCHED("rank_of");
+      launch_chunk_key(scene->centers, scene->scales, scene->quats, scene->opacities, P, cam,
+                       opts->alpha_cutoff, v->rank_c.as<uint32_t>(), opts->chunk_size,
+                       v->depth.as<double>(), v->dkeys_in.as<unsigned long long>(),
+                       v->idx_in.as<uint32_t>(), s);
+      NXS_LAUNCHED("chunk_key");
+      const int n_chunks = (int)((P + opts->chunk_size - 1) / opts->chunk_size);
+      size_t tb = v->temp.cap;
+      NXS_CUDA(cub::DeviceRadixSort::SortPairs(
+          v->temp.p, tb, v->dkeys_in.as<unsigned long long>(),
+          v->dkeys_out.as<unsigned long long>(), v->idx_in.as<uint32_t>(),
+          v->idx_out.as<uint32_t>(), (int)P, 0, 32 + bits_for((uint32_t)std::max(n_chunks, 2)),
+          s));
+    }
     launch_rank_of(v->idx_out.as<uint32_t>(), P, v->rank_of.as<uint32_t>(), s);
     NXS_LAUNCHED("rank_of");
   }
   mark(v, 1, s);
   if (P > 0) {
     // ---- K1 projection (all Gaussians, storage order; records land at their rank)
-    if (exact) NXS_CUDA(ensure_n<float>(v->zlo_rank, P));
+    if (torder) NXS_CUDA(ensure_n<float>(v->zlo_rank, P));
     launch_project(scene->centers, scene->scales, scene->quats, scene->opacities, scene->sh, C, P,
                    v->rank_of.as<uint32_t>(), cam, opts->alpha_cutoff, opts->near_plane,
-                   exact ? v->depth.as<double>() : nullptr,
-                   exact ? v->zlo_rank.as<float>() : nullptr, v->rects.as<int4>(),
+                   torder ? v->depth.as<double>() : nullptr,
+                   torder ? v->zlo_rank.as<float>() : nullptr, v->rects.as<int4>(),
                    v->records.as<float4>(), v->bframe.as<float4>(), dsmall, s);
     NXS_LAUNCHED("project");
   }
@@ -542,11 +573,12 @@ retry_sort:
       NXS_CUDA(ensure_n<float>(v->r_sea, npix * 3));
       NXS_CUDA(ensure_n<float>(v->r_sa, npix));
     }
-    if (exact) {
-      // ---- K3x exact-order forward (single phase)
+    if (torder) {
+      // ---- K3x exact/chunked-order forward (single phase)
       NXS_CUDA(ensure_n<int32_t>(v->seq, npix * std::max(1, opts->max_splats)));  // [slot][pixel]
       FwdXArgs xa{v->records.as<float4>(), v->pv_ph[ph].as<uint32_t>(),
                   v->ranges_ph[ph].as<int2>(), v->zlo_rank.as<float>(), v->idx_out.as<uint32_t>(),
+                  chunked ? v->rank_c.as<uint32_t>() : nullptr, chunked ? opts->chunk_size : 0,
                   opts->max_splats, (float)opts->alpha_cutoff, opts->near_plane,
                   {bgf[0], bgf[1], bgf[2]}, rgb, overdraw, residual, v->seq.as<int32_t>(),
                   dsmall + 9};
@@ -572,7 +604,7 @@ retry_sort:
   v->ev_fwd = true;
   v->ev_bwd = false;
   v->stats.n_pairs = total_pairs;
-  if (exact) {
+  if (torder) {
     // pending-buffer overflow means the exact order was not guaranteed: report
     NXS_CUDA(cudaMemcpyAsync(v->host_small + 7, dsmall + 9, sizeof(unsigned long long),
                              cudaMemcpyDeviceToHost, s));
@@ -632,7 +664,7 @@ int nxs_backward(nxs_view* v, const nxs_scene* scene, const float* seed, float* 
   const bool count = (v->opts.flags & NXS_FLAG_COUNT_EVENTS) != 0;
   unsigned long long* dsmall = v->dev_small.as<unsigned long long>();
   Counters* cnt = reinterpret_cast<Counters*>(dsmall + 1);
-  if (v->opts.chunk_size == NXS_CHUNK_EXACT) {
+  if (v->opts.chunk_size != 1) {
     BwdXArgs xa{v->records.as<float4>(), v->bframe.as<float4>(), v->pv_ph[0].as<uint32_t>(),
                 v->seq.as<int32_t>(), std::max(1, v->opts.max_splats),
                 (float)v->opts.alpha_cutoff, v->opts.near_plane, {v->bg[0], v->bg[1], v->bg[2]},

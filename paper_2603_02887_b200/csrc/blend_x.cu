@@ -28,7 +28,8 @@ constexpr int XBATCH = 64;   // list entries staged per batch
 // records of the current and the previous batch stay staged (a ring of
 // 2*XBATCH): most commits are of recently tested entries
 constexpr size_t FWDX_SMEM = sizeof(float4) * 2 * XBATCH * REC_F4 + sizeof(uint32_t) * XBATCH +
-                             sizeof(float) * XBATCH + (sizeof(float) + sizeof(int)) * XBUF * TILE_PIX;
+                             sizeof(float) * XBATCH + sizeof(uint32_t) * XBATCH +
+                             (sizeof(float) + sizeof(int)) * XBUF * TILE_PIX;
 
 struct FwdXPix {
   float rad0, rad1, rad2, thi, tlo, P, Trem, ek0, ek1, ek2, tk, sea0, sea1, sea2, sa, Pck;
@@ -106,7 +107,8 @@ template <int FAM, bool COUNT>
 __global__ void __launch_bounds__(TILE_PIX)
     k_blend_fwd_x(const float4* __restrict__ records, const uint32_t* __restrict__ pairs,
                   const int2* __restrict__ ranges, const float* __restrict__ zlo_rank,
-                  const uint32_t* __restrict__ order, CamDev cam, ModelDev m, int max_splats,
+                  const uint32_t* __restrict__ order, const uint32_t* __restrict__ rank_c,
+                  int chunk, CamDev cam, ModelDev m, int max_splats,
                   float cutoff, double near_plane, float bg0, float bg1, float bg2,
                   float* __restrict__ rgb, int32_t* __restrict__ overdraw,
                   float* __restrict__ residual, PixCache cache, int32_t* __restrict__ seq,
@@ -115,7 +117,8 @@ __global__ void __launch_bounds__(TILE_PIX)
   float4(*s_ring)[REC_F4] = reinterpret_cast<float4(*)[REC_F4]>(smem_dyn);  // [2*XBATCH]
   uint32_t* s_rank = reinterpret_cast<uint32_t*>(smem_dyn + 2 * XBATCH * REC_F4);
   float* s_zlo = reinterpret_cast<float*>(s_rank + XBATCH);
-  float* bt = s_zlo + XBATCH;                                 // [XBUF][TILE_PIX] pending t
+  uint32_t* s_chunk = reinterpret_cast<uint32_t*>(s_zlo + XBATCH);
+  float* bt = reinterpret_cast<float*>(s_chunk + XBATCH);    // [XBUF][TILE_PIX] pending t
   int* bp = reinterpret_cast<int*>(bt + XBUF * TILE_PIX);     // [XBUF][TILE_PIX] list position
 
   const int tile = blockIdx.x;
@@ -140,7 +143,14 @@ __global__ void __launch_bounds__(TILE_PIX)
   // pending entries: a ring of XBUF slots, ascending by (t, index) from the
   // head; new entries (lists are in z_lo order) usually append at the tail
   int nb = 0, head = 0;
+  uint32_t cur_chunk = 0;  // chunk of the pending entries (chunked order)
   unsigned long long ntest = 0;
+  // ties in t: storage index (one chunk, reference argsort over arange(n)) or
+  // the centre-depth rank (chunked: stable argsort within the chunk's ids)
+  auto tie_key = [&](uint32_t rank) -> uint32_t {
+    const uint32_t g = order[rank];
+    return rank_c ? rank_c[g] : g;
+  };
 
   // commit the smallest pending entry: re-read its record (L1/L2; every
   // pixel of the tile commits the same few entries) and composite it
@@ -176,6 +186,7 @@ __global__ void __launch_bounds__(TILE_PIX)
       const uint32_t rk = pairs[base + tid];
       s_rank[tid] = rk;
       s_zlo[tid] = zlo_rank[rk];
+      s_chunk[tid] = chunk > 0 ? rank_c[order[rk]] / (uint32_t)chunk : 0u;
     }
     __syncthreads();
     // stage this batch into the ring slot it maps to (positions are consecutive)
@@ -188,13 +199,16 @@ __global__ void __launch_bounds__(TILE_PIX)
     if (!s.done) {
       for (int j = 0; j < n; ++j) {
         const float4* s_rec_j = s_ring[(base + j) % (2 * XBATCH)];
-        // every remaining entry has t >= bound: pending entries below it are final
+        // every remaining entry has t >= bound: pending entries below it are
+        // final; a new chunk makes every pending entry final
+        const bool next_chunk = s_chunk[j] != cur_chunk;
         const float bound = s_zlo[j] * hnorm;
-        while (nb > 0 && bt[head * TILE_PIX + tid] < bound) {
+        while (nb > 0 && (next_chunk || bt[head * TILE_PIX + tid] < bound)) {
           commit_front();
           if (s.done) break;
         }
         if (s.done) break;
+        cur_chunk = s_chunk[j];
         if (COUNT) ++ntest;
         TestOut t;
         float tpk;
@@ -214,8 +228,8 @@ __global__ void __launch_bounds__(TILE_PIX)
           const float te = bt[e * TILE_PIX + tid];
           bool later = te > tpk;  // the pending entry commits after the new one
           if (te == tpk) {
-            if (gid_new == 0xffffffffu) gid_new = order[s_rank[j]];
-            later = order[pairs[bp[e * TILE_PIX + tid]]] > gid_new;
+            if (gid_new == 0xffffffffu) gid_new = tie_key(s_rank[j]);
+            later = tie_key(pairs[bp[e * TILE_PIX + tid]]) > gid_new;
           }
           if (!later) break;
           const int f = (head + i) & (XBUF - 1);
@@ -396,8 +410,8 @@ static void launch_fwd_x_fam(bool count, int n_tiles, const FwdXArgs& a, const C
     attr = true;
   }
   auto k = count ? k_blend_fwd_x<FAM, true> : k_blend_fwd_x<FAM, false>;
-  k<<<n_tiles, TILE_PIX, FWDX_SMEM, s>>>(a.records, a.pairs, a.ranges, a.zlo_rank, a.order, cam, m,
-                                         a.max_splats, a.cutoff, a.near_plane, a.bg[0], a.bg[1],
+  k<<<n_tiles, TILE_PIX, FWDX_SMEM, s>>>(a.records, a.pairs, a.ranges, a.zlo_rank, a.order, a.rank_c,
+                                         a.chunk, cam, m, a.max_splats, a.cutoff, a.near_plane, a.bg[0], a.bg[1],
                                          a.bg[2], a.rgb, a.overdraw, a.residual, cache, a.seq,
                                          a.overflow, cnt);
 }

@@ -124,6 +124,8 @@ struct FwdXArgs {
   const int2* ranges;
   const float* zlo_rank;
   const uint32_t* order;
+  const uint32_t* rank_c;  // chunked order: centre-depth rank per Gaussian, else null
+  int chunk;               // chunked order: chunk size C, else 0 (one chunk)
   int max_splats;
   float cutoff;
   double near_plane;

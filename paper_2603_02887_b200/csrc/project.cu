@@ -250,6 +250,30 @@ __global__ void k_rank_of(const uint32_t* __restrict__ order, int64_t P,
   if (r < P) rank_of[order[r]] = (uint32_t)r;
 }
 
+// Chunked order (reference chunk_size = C > 1, render.py:350-358): the
+// chunks are consecutive runs of C Gaussians in centre-depth order; tile
+// lists are ordered by (chunk, z_lo) so the exact-order blend can commit
+// per chunk.  Key = chunk << 32 | monotone bits of float_rd(z_lo); z_lo
+// (fp64) goes to zlo for the projection's per-rank copy.  Ties in the key
+// need no fix-up: any order of equal z_lo within a chunk is a valid list
+// order (the per-pixel order comes from t and the centre-depth rank).
+__global__ void k_chunk_key(const float* __restrict__ centers, const float* __restrict__ scales,
+                            const float* __restrict__ quats, const float* __restrict__ opacities,
+                            int64_t P, CamDev cam, double cutoff,
+                            const uint32_t* __restrict__ rank_c, int chunk,
+                            double* __restrict__ zlo, unsigned long long* __restrict__ key64,
+                            uint32_t* __restrict__ idx) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= P) return;
+  const double z = z_lower(centers, scales, quats, opacities, g, cam, cutoff);
+  zlo[g] = z;
+  const float zf = __double2float_rd(z);
+  uint32_t b = __float_as_uint(zf);
+  b = (zf == zf) ? ((b & 0x80000000u) ? ~b : (b | 0x80000000u)) : 0xffffffffu;
+  key64[g] = ((unsigned long long)(rank_c[g] / (uint32_t)chunk) << 32) | b;
+  idx[g] = (uint32_t)g;
+}
+
 struct ProjOut {
   const double* zlo;            // exact-order mode: z_lo per Gaussian (sort key), else null
   float* zlo_rank;              // exact-order mode: z_lo per rank, rounded down
@@ -651,6 +675,15 @@ void launch_key_fixup(const uint32_t* key, uint32_t* idx, const double* depth, i
                       unsigned long long* overflow, cudaStream_t s) {
   if (P == 0) return;
   k_key_fixup<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(key, idx, depth, P, overflow);
+}
+void launch_chunk_key(const float* centers, const float* scales, const float* quats,
+                      const float* opacities, int64_t P, const CamDev& cam, double cutoff,
+                      const uint32_t* rank_c, int chunk, double* zlo, unsigned long long* key64,
+                      uint32_t* idx, cudaStream_t s) {
+  if (P == 0) return;
+  k_chunk_key<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(centers, scales, quats, opacities, P,
+                                                          cam, cutoff, rank_c, chunk, zlo, key64,
+                                                          idx);
 }
 void launch_rank_of(const uint32_t* order, int64_t P, uint32_t* rank_of, cudaStream_t s) {
   if (P == 0) return;

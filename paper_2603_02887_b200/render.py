@@ -18,11 +18,13 @@ the device as float32 each call — the reference mutates them in place
 between calls, optimizer.py:382) or a :class:`DeviceScene` of resident
 float32 CUDA tensors (the fast path; nothing crosses PCIe but the outputs).
 
-Ordering (reference render.py:171, 350-358): the default
-``chunk_size=None`` (exact per-pixel order by peak depth, "Mode X") and
-``chunk_size=1`` (global front-to-back order, "Mode G") run on the device.
-Chunked orders ``C > 1`` are not implemented yet and raise
-``NotImplementedError`` — never a silent approximation.
+Ordering (reference render.py:171, 350-358), all on the
+device: the default ``chunk_size=None`` (exact per-pixel order by peak
+depth, "Mode X"), ``chunk_size=1`` (global front-to-back order, "Mode G")
+and ``chunk_size=C`` (chunks of C Gaussians in centre-depth order, per-pixel
+peak-depth order within each chunk, "Mode C" — the training default
+C=128).  A pixel whose pending buffer overflows in the t-ordered modes makes
+the call raise ``RuntimeError`` rather than return an unguaranteed order.
 """
 from __future__ import annotations
 
@@ -199,10 +201,9 @@ def _effective_chunk(chunk_size, n: int) -> int:
 
 
 def _check_mode(chunk: int):
-    if chunk > 1:
-        raise NotImplementedError(
-            f"chunked order chunk_size={chunk} is not implemented on the device yet; use "
-            "chunk_size=None (exact per-pixel order) or chunk_size=1 (global depth order)")
+    """0: exact per-pixel order, 1: global depth order, C > 1: chunks of C."""
+    if chunk < 0:
+        raise ValueError("chunk_size must be >= 1 or None")
 
 
 def _model_struct(model):

@@ -20,6 +20,11 @@ Fixtures (all scenes are stored, so nothing is regenerated at test time):
   golden_transmit.npz transmittance-study overdraw totals (acceptance crit. 7,
                       tests/test_acceptance.py:210-225).
   golden_order.npz    _depth_chunks order of a 100k canonical scene, 2 views.
+  golden_chunk.npz    chunked order (Mode C): the small scene at chunk_size 3
+                      (7 models, + gradients for exp/linear/quadratic) and the
+                      C1 scene at chunk_size 128 (the TrainConfig default,
+                      reference optimizer.py:278) and 64, 5 models, gradients
+                      for exp/linear/quadratic(0.5).
 """
 from __future__ import annotations
 
@@ -188,8 +193,46 @@ def order():
     np.savez_compressed(OUT / "golden_order.npz", **d)
 
 
+def chunk():
+    d = {}
+    rng = np.random.default_rng(31)
+    scene = [random_prim(rng) for _ in range(8)]
+    arrs = rounded(SceneArrays.from_primitives(scene))
+    cam = Camera.from_look_at([0, 0, -3], [0, 0, 4], [0, 1, 0], 55.0, 24, 16)
+    bg = f32([0.05, 0.1, 0.15])
+    seed = f32(np.random.default_rng(7).uniform(0.2, 1.0, (16, 24, 3)))
+    for name, m in MODELS.items():
+        tag = f"small__{name}__3"
+        res = render(arrs, cam, m, bg, chunk_size=3)
+        d[tag + "__rgb"], d[tag + "__overdraw"], d[tag + "__residual"] = \
+            res.rgb, res.overdraw, res.residual
+        if name in BWD:
+            _, g = render_with_gradients(arrs, cam, m, bg, seed, chunk_size=3)
+            for k, v in g.items():
+                d[tag + "__g_" + k] = v
+    sc = O.round_scene_f32(O.canonical_scene(1000, seed=5))
+    arrs = SceneArrays(sc.centers, sc.scales, sc.quats, sc.opacities, sc.sh)
+    cam = Camera.from_look_at([0, 0, 0], [0, 0, 3.5], [0, 1, 0], 55.0, 64, 64)
+    bg = f32([0.1, 0.05, 0.2])
+    seed = f32(O.canonical_seed(64, 64, 0))
+    for cs in (128, 64):
+        for name in ("exponential", "linear", "quadratic_0.5", "softplus_20", "blended_0.5"):
+            m = MODELS[name]
+            tag = f"c1__{name}__{cs}"
+            if name in BWD:
+                res, g = render_with_gradients(arrs, cam, m, bg, seed, chunk_size=cs)
+                for k, v in g.items():
+                    d[tag + "__g_" + k] = v
+            else:
+                res = render(arrs, cam, m, bg, chunk_size=cs)
+            d[tag + "__rgb"], d[tag + "__overdraw"], d[tag + "__residual"] = \
+                res.rgb, res.overdraw, res.residual
+            print("chunk", cs, name, "mean overdraw", res.overdraw.mean())
+    np.savez_compressed(OUT / "golden_chunk.npz", **d)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["small", "c1", "fd", "transmit", "order"]
+    which = sys.argv[1:] or ["small", "c1", "fd", "transmit", "order", "chunk"]
     for w in which:
         globals()[w]()
         print("wrote", w)

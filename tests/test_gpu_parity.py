@@ -322,8 +322,11 @@ def test_dropin_api_shapes_and_cache():
     ref = O.forward(sc, cam, MODELS["softplus_20"], bg, chunk_size=None)
     keep = ~ref["mask"].reshape(16, 24)
     assert close(out.rgb, golden).all(axis=2)[keep].all()
-    with pytest.raises(NotImplementedError):
-        nx.render(arrs, cam, model, bg, chunk_size=3)
+    out = nx.render(arrs, cam, model, bg, chunk_size=3)  # chunked order (Mode C)
+    ref = O.forward(sc, cam, MODELS["softplus_20"], bg, chunk_size=3)
+    keep = ~ref["mask"].reshape(16, 24)
+    assert close(out.rgb, load("golden_chunk.npz")["small__softplus_20__3__rgb"]).all(
+        axis=2)[keep].all()
     with pytest.raises(ValueError):
         nx.render_backward(arrs, cam, model, bg, {"rad": 0}, d["seed"], chunk_size=1)
     # the reference's own objects are accepted (duck-typed)
@@ -494,3 +497,90 @@ def test_exact_order_pending_overflow_is_reported():
     arrs = nx.SceneArrays(sc.centers, sc.scales, sc.quats, sc.opacities, sc.sh)
     with pytest.raises(RuntimeError):
         nx.render(arrs, cam, MODELS["exponential"], np.zeros(3))
+
+
+# ---------------------------------------------------------------------------
+# chunked order (reference chunk_size=C > 1, "Mode C"; C=128 is the training
+# default, optimizer.py:278)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name", list(MODELS))
+def test_chunked_small_scene_matches_reference_golden(name):
+    d, ch = load("golden_small.npz"), load("golden_chunk.npz")
+    cam, sc, bg = cam_from(d), scene_from(d), d["bg"]
+    tag = f"small__{name}__3"
+    got = gpu_run(sc, cam, MODELS[name], bg, chunk_size=3)
+    ref = O.forward(sc, cam, MODELS[name], bg, chunk_size=3)
+    golden = {"rad": ch[tag + "__rgb"], "residual": ch[tag + "__residual"],
+              "overdraw": ch[tag + "__overdraw"]}
+    bad, kept = check_forward(got, golden, ref["mask"], cam.height, cam.width)
+    assert bad == 0 and kept > 0.9 * cam.width * cam.height, (bad, kept)
+    if tag + "__g_centers" in ch and not ref["mask"].any():
+        g = gpu_run(sc, cam, MODELS[name], bg, seed=d["seed"], chunk_size=3)
+        golden_g = {k: ch[f"{tag}__g_{k}"] for k in GRAD_FIELDS}
+        _, mass = O.render_with_gradients(sc, cam, MODELS[name], bg, d["seed"], chunk_size=3,
+                                          with_mass=True)[1]
+        strict, massf, total = grad_report(g["grads"], golden_g, mass)
+        assert massf == 0 and strict <= max(1, total // 1000), (strict, massf, total)
+
+
+@pytest.mark.parametrize("cs", [128, 64])
+@pytest.mark.parametrize("name", list(MODELS))
+def test_chunked_c1_matches_oracle(name, cs):
+    d, ch = load("golden_c1.npz"), load("golden_chunk.npz")
+    cam, sc, bg = cam_from(d), scene_from(d), d["bg"]
+    model = MODELS[name]
+    fwd = O.forward(sc, cam, model, bg, chunk_size=cs, keep_state=True)
+    seed = d["seed"].reshape(-1, 3) * (~fwd["mask"])[:, None]
+    g_ref, mass = O.backward(sc, cam, model, bg, fwd, seed, with_mass=True)
+    got = gpu_run(sc, cam, model, bg, seed=seed.reshape(cam.height, cam.width, 3),
+                  chunk_size=cs)
+    bad, kept = check_forward(got, fwd, fwd["mask"], cam.height, cam.width)
+    assert bad == 0 and kept >= 0.95 * cam.width * cam.height, (bad, kept)
+    tag = f"c1__{name}__{cs}"
+    if tag + "__rgb" in ch:  # the reference's own output, on the unmasked pixels
+        golden = {"rad": ch[tag + "__rgb"], "residual": ch[tag + "__residual"],
+                  "overdraw": ch[tag + "__overdraw"]}
+        bad, _ = check_forward(got, golden, fwd["mask"], cam.height, cam.width)
+        assert bad == 0, bad
+    strict, massf, total = grad_report(got["grads"], g_ref, mass)
+    assert massf == 0, (strict, massf, total)
+    assert strict <= max(2, total // 1000), (strict, massf, total)
+    assert got["stats"]["n_overflow"] == 0
+
+
+def test_chunk_at_least_count_is_the_exact_order():
+    """chunk_size >= P is one chunk (reference render.py:353-354): the
+    device takes the exact-order path with storage-index ties."""
+    d = load("golden_c1.npz")
+    cam, sc, bg = cam_from(d), scene_from(d), d["bg"]
+    a = gpu_run(sc, cam, MODELS["softplus_20"], bg, chunk_size=None)
+    b = gpu_run(sc, cam, MODELS["softplus_20"], bg, chunk_size=len(sc))
+    c = gpu_run(sc, cam, MODELS["softplus_20"], bg, chunk_size=len(sc) - 1)
+    for k in ("rgb", "overdraw", "residual"):
+        np.testing.assert_array_equal(a[k], b[k])
+    assert c["stats"]["n_overflow"] == 0  # two chunks: the chunked path proper
+
+
+@pytest.mark.parametrize("name", ["exponential", "softplus_20"])
+def test_chunked_c2_sampled_pixels_match_oracle(name):
+    sc = O.round_scene_f32(O.canonical_scene(100_000, seed=0))
+    cam = O.canonical_camera(512, 512)
+    bg = np.array([0.1, 0.05, 0.2], dtype=np.float32).astype(np.float64)
+    model = MODELS[name]
+    px = np.random.default_rng(13).choice(512 * 512, 128, replace=False)
+    fwd = O.forward(sc, cam, model, bg, chunk_size=128, pixels=px, keep_state=True, batch=16)
+    seed_px = O.canonical_seed(512, 512, 0).reshape(-1, 3)[px].astype(np.float32).astype(
+        np.float64) * (~fwd["mask"])[:, None]
+    g_ref, mass = O.backward(sc, cam, model, bg, fwd, seed_px, with_mass=True)
+    seed_full = np.zeros((512 * 512, 3))
+    seed_full[px] = seed_px
+    got = gpu_run(sc, cam, model, bg, seed=seed_full.reshape(512, 512, 3), chunk_size=128)
+    keep = ~fwd["mask"]
+    ok = close(got["rgb"].reshape(-1, 3)[px], fwd["rad"]).all(1) & \
+        (got["overdraw"].reshape(-1)[px] == fwd["overdraw"]) & \
+        close(got["residual"].reshape(-1)[px], fwd["residual"])
+    assert (keep & ~ok).sum() == 0, int((keep & ~ok).sum())
+    assert keep.sum() >= 0.8 * len(px), int(keep.sum())
+    strict, massf, total = grad_report(got["grads"], g_ref, mass)
+    assert massf == 0, (strict, massf, total)

@@ -89,15 +89,19 @@ def test_primitive_validation_and_scene_arrays():
     assert back[1].scale[1] == 2.0
 
 
-def test_chunk_mapping_and_unsupported_modes_fail_loudly():
+def test_chunk_mapping_and_invalid_modes_fail_loudly():
     from paper_2603_02887_b200.render import _check_mode, _effective_chunk
     assert _effective_chunk(None, 10) == 0
     assert _effective_chunk(10, 10) == 0 and _effective_chunk(1, 10) == 1
     assert _effective_chunk(None, 1) == 1
-    with pytest.raises(NotImplementedError):
-        _check_mode(7)
+    assert _effective_chunk(7, 10) == 7
+    with pytest.raises(ValueError):
+        _effective_chunk(0, 10)
+    with pytest.raises(ValueError):
+        _check_mode(-1)
     _check_mode(0)
     _check_mode(1)
+    _check_mode(7)
 
 
 def test_product_never_imports_oracle():

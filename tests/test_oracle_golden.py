@@ -106,3 +106,42 @@ def test_pixel_subset_is_exact():
     sub = O.forward(sc, cam, MODELS["exponential"], d["bg"], chunk_size=1, pixels=px)
     np.testing.assert_array_equal(sub["rad"], full["rad"][px])
     np.testing.assert_array_equal(sub["overdraw"], full["overdraw"][px])
+
+
+CHUNK = load("golden_chunk.npz")
+
+
+@pytest.mark.parametrize("name", list(MODELS))
+def test_chunked_small_matches_reference(name):
+    """chunk_size=3 over the 8-primitive scene: per-pixel t order inside
+    each chunk of 3 (reference render.py:350-358, 171)."""
+    d, tag = SMALL, f"small__{name}__3"
+    cam, sc, bg = cam_from(d), scene_from(d), d["bg"]
+    H, W = cam.height, cam.width
+    if tag + "__g_centers" in CHUNK:
+        fwd, g = O.render_with_gradients(sc, cam, MODELS[name], bg, d["seed"], chunk_size=3)
+        for k in GRAD_FIELDS:
+            ref = CHUNK[tag + "__g_" + k]
+            np.testing.assert_allclose(g[k], ref, rtol=1e-10, atol=1e-12 * np.abs(ref).max())
+    else:
+        fwd = O.forward(sc, cam, MODELS[name], bg, chunk_size=3)
+    np.testing.assert_allclose(fwd["rad"].reshape(H, W, 3), CHUNK[tag + "__rgb"], atol=1e-12)
+    np.testing.assert_array_equal(fwd["overdraw"].reshape(H, W), CHUNK[tag + "__overdraw"])
+    np.testing.assert_allclose(fwd["residual"].reshape(H, W), CHUNK[tag + "__residual"],
+                               atol=1e-12)
+
+
+@pytest.mark.parametrize("cs", [128, 64])
+@pytest.mark.parametrize("name", ["exponential", "linear", "quadratic_0.5", "softplus_20",
+                                  "blended_0.5"])
+def test_chunked_c1_matches_reference(name, cs):
+    d, tag = C1, f"c1__{name}__{cs}"
+    cam, sc = cam_from(d), scene_from(d)
+    H, W = cam.height, cam.width
+    fwd, g = O.render_with_gradients(sc, cam, MODELS[name], d["bg"], d["seed"], chunk_size=cs)
+    np.testing.assert_allclose(fwd["rad"].reshape(H, W, 3), CHUNK[tag + "__rgb"], atol=1e-12)
+    np.testing.assert_array_equal(fwd["overdraw"].reshape(H, W), CHUNK[tag + "__overdraw"])
+    if tag + "__g_centers" in CHUNK:
+        for k in GRAD_FIELDS:
+            ref = CHUNK[tag + "__g_" + k]
+            np.testing.assert_allclose(g[k], ref, rtol=1e-9, atol=1e-12 * np.abs(ref).max())
