@@ -29,11 +29,12 @@ void launch_rank_of(const uint32_t*, int64_t, uint32_t*, cudaStream_t);
 void launch_chunk_key(const float*, const float*, const float*, const float*, int64_t,
                       const CamDev&, double, const uint32_t*, int, double*, unsigned long long*,
                       uint32_t*, cudaStream_t);
+bool launch_chunk_sort(const uint32_t*, const double*, int64_t, int, uint32_t*, cudaStream_t);
 void launch_project(const float*, const float*, const float*, const float*, const float*, int,
                     int64_t, const uint32_t*, const CamDev&, double, double, const double*,
                     float*, int4*, float4*, float4*, unsigned long long*, cudaStream_t);
 void launch_blend_fwd_x(bool, int, const FwdXArgs&, const CamDev&, const ModelDev&,
-                        const PixCache&, Counters*, cudaStream_t);
+                        const PixCache&, const PixResume&, Counters*, cudaStream_t);
 void launch_blend_bwd_x(bool, int, const BwdXArgs&, const CamDev&, const ModelDev&,
                         const PixCache&, Counters*, cudaStream_t);
 void launch_count_active(const int4*, const uint32_t*, int64_t, int64_t, int, const uint8_t*,
@@ -375,25 +376,29 @@ int nxs_forward(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
   NXS_CUDA(cudaMemsetAsync(dsmall, 0, 16 * sizeof(unsigned long long), s));
   NXS_CUDA(cudaMemsetAsync(v->active.p, 1, (size_t)n_tiles, s));
 
-  // ---- depth phases [R_p, R_{p+1}): R_1 = first phase, then x8
+  // ---- depth phases [R_p, R_{p+1}): R_1 = first phase, then x8.  The
+  // chunked order cuts phases on chunk boundaries (nothing is pending
+  // there); the exact order keeps per-pixel pending state: one phase.
   int64_t R[MAX_PHASES + 1];
   int n_ph = 0;
   {
     int64_t r1;
-    if ((opts->flags & NXS_FLAG_FULL_BINNING) || torder)
-      r1 = P;  // t-ordered modes keep per-pixel pending state: one phase
+    if ((opts->flags & NXS_FLAG_FULL_BINNING) || exact)
+      r1 = P;
     else if (opts->first_phase_ranks > 0)
       r1 = opts->first_phase_ranks;
     else  // measured at C3: saturating models finish every tile within P/32
           // ranks; exp never saturates and runs to the 128 cap
       r1 = (md.fam == FAM_EXP) ? P / 4 : P / 32;
     r1 = std::max<int64_t>(r1, 4096);
+    const int64_t unit = chunked ? opts->chunk_size : 1;
+    auto up = [&](int64_t r) { return std::min(P, (r + unit - 1) / unit * unit); };
     R[0] = 0;
-    int64_t r = std::min(P, r1);
+    int64_t r = up(r1);
     while (true) {
       R[++n_ph] = r;
       if (r >= P || n_ph == MAX_PHASES - 1) break;
-      r = std::min(P, r * 8);
+      r = up(r * 8);
     }
     if (R[n_ph] < P) R[++n_ph] = P;
   }
@@ -417,7 +422,7 @@ retry_sort:
     NXS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_scan,
                                            v->ntiles.as<unsigned long long>(),
                                            v->offsets.as<unsigned long long>(), (int)P, s));
-    if (chunked) {
+    if (chunked && opts->chunk_size > 2048) {
       size_t tmp_chunk = 0;
       NXS_CUDA(cub::DeviceRadixSort::SortPairs(
           nullptr, tmp_chunk, v->dkeys_in.as<unsigned long long>(),
@@ -450,22 +455,34 @@ retry_sort:
       NXS_LAUNCHED("key_fixup");
     }
     if (chunked) {
-      // chunk = centre-depth rank / C; lists in (chunk, z_lo) order
+      // chunk = centre-depth rank / C; lists in (chunk, z_lo) order: one
+      // block radix sort per chunk, or a global 64-bit sort for huge chunks
       NXS_CUDA(ensure_n<uint32_t>(v->rank_c, P));
       launch_rank_of(v->idx_out.as<uint32_t>(), P, v->rank_c.as<uint32_t>(), s);
       NXS_LAUNCHED("rank_of");
+      const bool block_sort = opts->chunk_size <= 2048;
       launch_chunk_key(scene->centers, scene->scales, scene->quats, scene->opacities, P, cam,
                        opts->alpha_cutoff, v->rank_c.as<uint32_t>(), opts->chunk_size,
-                       v->depth.as<double>(), v->dkeys_in.as<unsigned long long>(),
+                       v->depth.as<double>(),
+                       block_sort ? nullptr : v->dkeys_in.as<unsigned long long>(),
                        v->idx_in.as<uint32_t>(), s);
       NXS_LAUNCHED("chunk_key");
-      const int n_chunks = (int)((P + opts->chunk_size - 1) / opts->chunk_size);
-      size_t tb = v->temp.cap;
-      NXS_CUDA(cub::DeviceRadixSort::SortPairs(
-          v->temp.p, tb, v->dkeys_in.as<unsigned long long>(),
-          v->dkeys_out.as<unsigned long long>(), v->idx_in.as<uint32_t>(),
-          v->idx_out.as<uint32_t>(), (int)P, 0, 32 + bits_for((uint32_t)std::max(n_chunks, 2)),
-          s));
+      if (block_sort) {
+        // centre order (idx_out) -> per-chunk z_lo order (idx_in) -> idx_out
+        launch_chunk_sort(v->idx_out.as<uint32_t>(), v->depth.as<double>(), P, opts->chunk_size,
+                          v->idx_in.as<uint32_t>(), s);
+        NXS_LAUNCHED("chunk_sort");
+        NXS_CUDA(cudaMemcpyAsync(v->idx_out.p, v->idx_in.p, (size_t)P * 4,
+                                 cudaMemcpyDeviceToDevice, s));
+      } else {
+        const int n_chunks = (int)((P + opts->chunk_size - 1) / opts->chunk_size);
+        size_t tb = v->temp.cap;
+        NXS_CUDA(cub::DeviceRadixSort::SortPairs(
+            v->temp.p, tb, v->dkeys_in.as<unsigned long long>(),
+            v->dkeys_out.as<unsigned long long>(), v->idx_in.as<uint32_t>(),
+            v->idx_out.as<uint32_t>(), (int)P, 0,
+            32 + bits_for((uint32_t)std::max(n_chunks, 2)), s));
+      }
     }
     launch_rank_of(v->idx_out.as<uint32_t>(), P, v->rank_of.as<uint32_t>(), s);
     NXS_LAUNCHED("rank_of");
@@ -574,19 +591,21 @@ retry_sort:
       NXS_CUDA(ensure_n<float>(v->r_sa, npix));
     }
     if (torder) {
-      // ---- K3x exact/chunked-order forward (single phase)
+      // ---- K3x exact/chunked-order forward of this phase
       NXS_CUDA(ensure_n<int32_t>(v->seq, npix * std::max(1, opts->max_splats)));  // [slot][pixel]
+      if (n_ph > 1) NXS_CUDA(cudaMemsetAsync(n_active, 0, sizeof(unsigned int), s));
       FwdXArgs xa{v->records.as<float4>(), v->pv_ph[ph].as<uint32_t>(),
                   v->ranges_ph[ph].as<int2>(), v->zlo_rank.as<float>(), v->idx_out.as<uint32_t>(),
                   chunked ? v->rank_c.as<uint32_t>() : nullptr, chunked ? opts->chunk_size : 0,
                   opts->max_splats, (float)opts->alpha_cutoff, opts->near_plane,
                   {bgf[0], bgf[1], bgf[2]}, rgb, overdraw, residual, v->seq.as<int32_t>(),
-                  dsmall + 9};
-      launch_blend_fwd_x(count, n_tiles, xa, cam, md, v->cache(), cnt, s);
+                  dsmall + 9, n_ph > 1 ? v->active.as<uint8_t>() : nullptr,
+                  n_ph > 1 ? n_active : nullptr, ph > 0, ph + 1 < n_ph};
+      launch_blend_fwd_x(count, n_tiles, xa, cam, md, v->cache(), v->resume(), cnt, s);
       NXS_LAUNCHED("blend_fwd_x");
       if (v->ev_ok) cudaEventRecord(v->evp[ph][2], s);
       ph_done = ph + 1;
-      break;
+      continue;
     }
     // ---- K3 forward blend of this phase (tiles still active)
     NXS_CUDA(cudaMemsetAsync(n_active, 0, sizeof(unsigned int), s));

@@ -27,7 +27,8 @@ constexpr int XBUF = 32;     // pending entries per pixel
 constexpr int XBATCH = 64;   // list entries staged per batch
 // records of the current and the previous batch stay staged (a ring of
 // 2*XBATCH): most commits are of recently tested entries
-constexpr size_t FWDX_SMEM = sizeof(float4) * 2 * XBATCH * REC_F4 + sizeof(uint32_t) * XBATCH +
+constexpr size_t FWDX_SMEM = sizeof(float4) * 2 * XBATCH * REC_F4 +
+                             sizeof(uint32_t) * 2 * XBATCH + sizeof(uint32_t) * XBATCH +
                              sizeof(float) * XBATCH + sizeof(uint32_t) * XBATCH +
                              (sizeof(float) + sizeof(int)) * XBUF * TILE_PIX;
 
@@ -111,17 +112,21 @@ __global__ void __launch_bounds__(TILE_PIX)
                   int chunk, CamDev cam, ModelDev m, int max_splats,
                   float cutoff, double near_plane, float bg0, float bg1, float bg2,
                   float* __restrict__ rgb, int32_t* __restrict__ overdraw,
-                  float* __restrict__ residual, PixCache cache, int32_t* __restrict__ seq,
-                  unsigned long long* __restrict__ overflow, Counters* __restrict__ cnt) {
+                  float* __restrict__ residual, PixCache cache, PixResume rs,
+                  int32_t* __restrict__ seq, unsigned long long* __restrict__ overflow,
+                  uint8_t* __restrict__ active, unsigned int* __restrict__ n_active, bool resume,
+                  bool save, Counters* __restrict__ cnt) {
+  const int tile = blockIdx.x;
+  if (active && !active[tile]) return;  // finished in an earlier depth phase
   extern __shared__ float4 smem_dyn[];
   float4(*s_ring)[REC_F4] = reinterpret_cast<float4(*)[REC_F4]>(smem_dyn);  // [2*XBATCH]
-  uint32_t* s_rank = reinterpret_cast<uint32_t*>(smem_dyn + 2 * XBATCH * REC_F4);
+  uint32_t* s_ring_rank = reinterpret_cast<uint32_t*>(smem_dyn + 2 * XBATCH * REC_F4);
+  uint32_t* s_rank = s_ring_rank + 2 * XBATCH;
   float* s_zlo = reinterpret_cast<float*>(s_rank + XBATCH);
   uint32_t* s_chunk = reinterpret_cast<uint32_t*>(s_zlo + XBATCH);
   float* bt = reinterpret_cast<float*>(s_chunk + XBATCH);    // [XBUF][TILE_PIX] pending t
   int* bp = reinterpret_cast<int*>(bt + XBUF * TILE_PIX);     // [XBUF][TILE_PIX] list position
 
-  const int tile = blockIdx.x;
   const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
   const int tid = threadIdx.x;
   const int px = tx * TILE + (tid & (TILE - 1)), py = ty * TILE + (tid >> 4);
@@ -139,7 +144,29 @@ __global__ void __launch_bounds__(TILE_PIX)
   s.ek1 = bg1;
   s.ek2 = bg2;
   s.ck = -1;
-  s.done = !inside || max_splats <= 0;
+  if (resume && inside) {  // carry of the previous depth phase
+    s.rad0 = rs.rad[3 * pix + 0];
+    s.rad1 = rs.rad[3 * pix + 1];
+    s.rad2 = rs.rad[3 * pix + 2];
+    s.Trem = rs.trem[pix];
+    s.count = rs.count[pix];
+    s.sea0 = rs.sea[3 * pix + 0];
+    s.sea1 = rs.sea[3 * pix + 1];
+    s.sea2 = rs.sea[3 * pix + 2];
+    s.sa = rs.sa[pix];
+    s.sat = cache.sat[pix] != 0;
+    s.tk = cache.t_k[pix];
+    s.thi = cache.tau_hi[pix];
+    s.tlo = cache.tau_lo[pix];
+    s.P = cache.P_end[pix];
+    s.ck = cache.ck_idx[pix];
+    s.Pck = cache.P_ck[pix];
+    s.ek0 = cache.e_k[3 * pix + 0];
+    s.ek1 = cache.e_k[3 * pix + 1];
+    s.ek2 = cache.e_k[3 * pix + 2];
+  }
+  s.done = !inside || s.sat || s.count >= max_splats;
+  const int count0 = s.count;
   // pending entries: a ring of XBUF slots, ascending by (t, index) from the
   // head; new entries (lists are in z_lo order) usually append at the tail
   int nb = 0, head = 0;
@@ -160,12 +187,15 @@ __global__ void __launch_bounds__(TILE_PIX)
     head = (head + 1) & (XBUF - 1);
     --nb;
     float4 r[REC_F4];
+    uint32_t rank;
     if (pos >= ring_lo) {
       const float4* rec = s_ring[pos % (2 * XBATCH)];
+      rank = s_ring_rank[pos % (2 * XBATCH)];
 #pragma unroll
       for (int k = 0; k < REC_F4; ++k) r[k] = rec[k];
     } else {
-      const float4* rec = records + (size_t)pairs[pos] * REC_F4;
+      rank = pairs[pos];
+      const float4* rec = records + (size_t)rank * REC_F4;
 #pragma unroll
       for (int k = 0; k < REC_F4; ++k) r[k] = __ldg(rec + k);
     }
@@ -174,7 +204,7 @@ __global__ void __launch_bounds__(TILE_PIX)
     test_with_t(r, cam, px, py, pc, hnorm, cutoff, near_plane, t, tpk);  // valid by construction
     float E0, E1, E2;
     emission(r[4], r[5], r[6], pc, E0, E1, E2);
-    myseq[(size_t)s.count * npix] = pos;
+    myseq[(size_t)s.count * npix] = (int32_t)rank;
     composite<FAM>(s, m, max_splats, t.alpha, E0, E1, E2);
   };
 
@@ -185,6 +215,7 @@ __global__ void __launch_bounds__(TILE_PIX)
     if (tid < n) {
       const uint32_t rk = pairs[base + tid];
       s_rank[tid] = rk;
+      s_ring_rank[(base + tid) % (2 * XBATCH)] = rk;
       s_zlo[tid] = zlo_rank[rk];
       s_chunk[tid] = chunk > 0 ? rank_c[order[rk]] / (uint32_t)chunk : 0u;
     }
@@ -245,8 +276,13 @@ __global__ void __launch_bounds__(TILE_PIX)
     }
     if (__syncthreads_count(!s.done) == 0) break;
   }
-  // end of the list: everything pending is final, in order
+  // end of the list (and of a chunk): everything pending is final, in order
   while (nb > 0 && !s.done) commit_front();
+  const int still = __syncthreads_count(!s.done);
+  if (active && tid == 0) {
+    active[tile] = still > 0 ? 1 : 0;
+    if (still > 0) atomicAdd(n_active, 1u);
+  }
 
   if (COUNT) {
     __shared__ unsigned long long s_cnt[2];
@@ -254,7 +290,7 @@ __global__ void __launch_bounds__(TILE_PIX)
     if (tid == 0) s_cnt[0] = s_cnt[1] = 0;
     __syncthreads();
     atomicAdd(&s_cnt[0], ntest);
-    atomicAdd(&s_cnt[1], (unsigned long long)s.count);
+    atomicAdd(&s_cnt[1], (unsigned long long)(s.count - count0));
     __syncthreads();
     if (tid == 0) {
       atomicAdd(&cnt->tests_fwd, s_cnt[0]);
@@ -262,6 +298,17 @@ __global__ void __launch_bounds__(TILE_PIX)
     }
   }
   if (!inside) return;
+  if (save && still > 0) {  // the tile continues in the next depth phase
+    rs.rad[3 * pix + 0] = s.rad0;
+    rs.rad[3 * pix + 1] = s.rad1;
+    rs.rad[3 * pix + 2] = s.rad2;
+    rs.trem[pix] = s.Trem;
+    rs.count[pix] = s.count;
+    rs.sea[3 * pix + 0] = s.sea0;
+    rs.sea[3 * pix + 1] = s.sea1;
+    rs.sea[3 * pix + 2] = s.sea2;
+    rs.sa[pix] = s.sa;
+  }
   const float res = s.sat ? 0.f : s.Trem;  // render.py:210
   rgb[3 * pix + 0] = fmaf(bg0, res, s.rad0);
   rgb[3 * pix + 1] = fmaf(bg1, res, s.rad1);
@@ -316,12 +363,12 @@ __global__ void __launch_bounds__(TILE_PIX)
   int ptr = st.last;  // commit index, back to front
 
   while (true) {
-    const int pos = ptr >= 0 ? myseq[(size_t)ptr * npix] : -1;
-    const int wpos = __reduce_max_sync(0xffffffffu, pos);
-    if (wpos < 0) break;
+    const int cur = ptr >= 0 ? myseq[(size_t)ptr * npix] : -1;  // rank
+    const int wcur = __reduce_max_sync(0xffffffffu, cur);
+    if (wcur < 0) break;
     if (COUNT && lane == 0) ++nent;
-    const bool mine = pos == wpos;
-    const uint32_t rank = pairs[wpos];  // warp-uniform
+    const bool mine = cur == wcur;
+    const uint32_t rank = (uint32_t)wcur;  // warp-uniform
     float4 rec[REC_F4], bf[3];
 #pragma unroll
     for (int k = 0; k < REC_F4; ++k) rec[k] = __ldg(records + (size_t)rank * REC_F4 + k);
@@ -401,8 +448,8 @@ static void set_smem(K k, size_t bytes) {
 
 template <int FAM>
 static void launch_fwd_x_fam(bool count, int n_tiles, const FwdXArgs& a, const CamDev& cam,
-                             const ModelDev& m, const PixCache& cache, Counters* cnt,
-                             cudaStream_t s) {
+                             const ModelDev& m, const PixCache& cache, const PixResume& rs,
+                             Counters* cnt, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
     set_smem(k_blend_fwd_x<FAM, true>, FWDX_SMEM);
@@ -412,20 +459,22 @@ static void launch_fwd_x_fam(bool count, int n_tiles, const FwdXArgs& a, const C
   auto k = count ? k_blend_fwd_x<FAM, true> : k_blend_fwd_x<FAM, false>;
   k<<<n_tiles, TILE_PIX, FWDX_SMEM, s>>>(a.records, a.pairs, a.ranges, a.zlo_rank, a.order, a.rank_c,
                                          a.chunk, cam, m, a.max_splats, a.cutoff, a.near_plane, a.bg[0], a.bg[1],
-                                         a.bg[2], a.rgb, a.overdraw, a.residual, cache, a.seq,
-                                         a.overflow, cnt);
+                                         a.bg[2], a.rgb, a.overdraw, a.residual, cache, rs,
+                                         a.seq, a.overflow, a.active, a.n_active, a.resume,
+                                         a.save, cnt);
 }
 
 void launch_blend_fwd_x(bool count, int n_tiles, const FwdXArgs& a, const CamDev& cam,
-                        const ModelDev& m, const PixCache& cache, Counters* cnt, cudaStream_t s) {
+                        const ModelDev& m, const PixCache& cache, const PixResume& rs,
+                        Counters* cnt, cudaStream_t s) {
   if (n_tiles == 0) return;
   switch (m.fam) {
-    case FAM_EXP: launch_fwd_x_fam<FAM_EXP>(count, n_tiles, a, cam, m, cache, cnt, s); break;
-    case FAM_LIN: launch_fwd_x_fam<FAM_LIN>(count, n_tiles, a, cam, m, cache, cnt, s); break;
-    case FAM_QUAD: launch_fwd_x_fam<FAM_QUAD>(count, n_tiles, a, cam, m, cache, cnt, s); break;
-    case FAM_BLEND: launch_fwd_x_fam<FAM_BLEND>(count, n_tiles, a, cam, m, cache, cnt, s); break;
-    case FAM_POW: launch_fwd_x_fam<FAM_POW>(count, n_tiles, a, cam, m, cache, cnt, s); break;
-    default: launch_fwd_x_fam<FAM_SOFT>(count, n_tiles, a, cam, m, cache, cnt, s); break;
+    case FAM_EXP: launch_fwd_x_fam<FAM_EXP>(count, n_tiles, a, cam, m, cache, rs, cnt, s); break;
+    case FAM_LIN: launch_fwd_x_fam<FAM_LIN>(count, n_tiles, a, cam, m, cache, rs, cnt, s); break;
+    case FAM_QUAD: launch_fwd_x_fam<FAM_QUAD>(count, n_tiles, a, cam, m, cache, rs, cnt, s); break;
+    case FAM_BLEND: launch_fwd_x_fam<FAM_BLEND>(count, n_tiles, a, cam, m, cache, rs, cnt, s); break;
+    case FAM_POW: launch_fwd_x_fam<FAM_POW>(count, n_tiles, a, cam, m, cache, rs, cnt, s); break;
+    default: launch_fwd_x_fam<FAM_SOFT>(count, n_tiles, a, cam, m, cache, rs, cnt, s); break;
   }
 }
 

@@ -133,8 +133,13 @@ struct FwdXArgs {
   float* rgb;
   int32_t* overdraw;
   float* residual;
-  int32_t* seq;
+  int32_t* seq;                // commit sequence [slot][pixel]: ranks
   unsigned long long* overflow;
+  // depth phases (chunked order; phases end on chunk boundaries, where no
+  // entry is pending, so the carry is the global-order one)
+  uint8_t* active;
+  unsigned int* n_active;
+  bool resume, save;
 };
 struct BwdXArgs {
   const float4* records;

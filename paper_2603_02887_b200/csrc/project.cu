@@ -14,6 +14,8 @@
 // The per-pixel test those records feed is in blend_fwd.cu.
 #include <algorithm>
 
+#include <cub/block/block_radix_sort.cuh>
+
 #include "nxs_internal.cuh"
 
 namespace nxs {
@@ -252,11 +254,19 @@ __global__ void k_rank_of(const uint32_t* __restrict__ order, int64_t P,
 
 // Chunked order (reference chunk_size = C > 1, render.py:350-358): the
 // chunks are consecutive runs of C Gaussians in centre-depth order; tile
-// lists are ordered by (chunk, z_lo) so the exact-order blend can commit
-// per chunk.  Key = chunk << 32 | monotone bits of float_rd(z_lo); z_lo
-// (fp64) goes to zlo for the projection's per-rank copy.  Ties in the key
-// need no fix-up: any order of equal z_lo within a chunk is a valid list
-// order (the per-pixel order comes from t and the centre-depth rank).
+// lists are ordered by (chunk, z_lo) so the exact-order blend can commit per
+// chunk.  Keys are the monotone bits of float_rd(z_lo) — the value the blend
+// bounds with — and ties need no fix-up: any order of equal z_lo within a
+// chunk is a valid list order (the per-pixel order comes from t and the
+// centre-depth rank).
+__device__ __forceinline__ uint32_t zlo_key(double z) {
+  const float zf = __double2float_rd(z);
+  const uint32_t b = __float_as_uint(zf);
+  return (zf == zf) ? ((b & 0x80000000u) ? ~b : (b | 0x80000000u)) : 0xffffffffu;
+}
+
+// z_lo per Gaussian; with key64 also the (chunk << 32 | z_lo key) sort key
+// of the global fallback for chunks too large for one block
 __global__ void k_chunk_key(const float* __restrict__ centers, const float* __restrict__ scales,
                             const float* __restrict__ quats, const float* __restrict__ opacities,
                             int64_t P, CamDev cam, double cutoff,
@@ -267,11 +277,41 @@ __global__ void k_chunk_key(const float* __restrict__ centers, const float* __re
   if (g >= P) return;
   const double z = z_lower(centers, scales, quats, opacities, g, cam, cutoff);
   zlo[g] = z;
-  const float zf = __double2float_rd(z);
-  uint32_t b = __float_as_uint(zf);
-  b = (zf == zf) ? ((b & 0x80000000u) ? ~b : (b | 0x80000000u)) : 0xffffffffu;
-  key64[g] = ((unsigned long long)(rank_c[g] / (uint32_t)chunk) << 32) | b;
-  idx[g] = (uint32_t)g;
+  if (key64) {
+    key64[g] = ((unsigned long long)(rank_c[g] / (uint32_t)chunk) << 32) | zlo_key(z);
+    idx[g] = (uint32_t)g;
+  }
+}
+
+// one block per chunk: stable block radix sort of the chunk's Gaussians
+// (centre-depth order in, (z_lo, centre rank) order out)
+template <int THREADS, int ITEMS>
+__global__ void __launch_bounds__(THREADS)
+    k_chunk_sort(const uint32_t* __restrict__ order_c, const double* __restrict__ zlo, int64_t P,
+                 int chunk, uint32_t* __restrict__ order_out) {
+  using Sort = cub::BlockRadixSort<uint32_t, THREADS, ITEMS, uint32_t>;
+  __shared__ typename Sort::TempStorage tmp;
+  const int64_t base = (int64_t)blockIdx.x * chunk;
+  const int n = (int)((P - base) < (int64_t)chunk ? (P - base) : (int64_t)chunk);
+  uint32_t keys[ITEMS], vals[ITEMS];
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int k = threadIdx.x * ITEMS + i;  // blocked: padding sorts after equal real keys
+    if (k < n) {
+      const uint32_t g = order_c[base + k];
+      keys[i] = zlo_key(zlo[g]);
+      vals[i] = g;
+    } else {
+      keys[i] = 0xffffffffu;
+      vals[i] = 0xffffffffu;
+    }
+  }
+  Sort(tmp).Sort(keys, vals);
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int k = threadIdx.x * ITEMS + i;
+    if (k < n) order_out[base + k] = vals[i];
+  }
 }
 
 struct ProjOut {
@@ -684,6 +724,21 @@ void launch_chunk_key(const float* centers, const float* scales, const float* qu
   k_chunk_key<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(centers, scales, quats, opacities, P,
                                                           cam, cutoff, rank_c, chunk, zlo, key64,
                                                           idx);
+}
+// false when the chunk is too large for one block (use the global sort)
+bool launch_chunk_sort(const uint32_t* order_c, const double* zlo, int64_t P, int chunk,
+                       uint32_t* order_out, cudaStream_t s) {
+  if (P == 0) return true;
+  const unsigned grid = (unsigned)((P + chunk - 1) / chunk);
+  if (chunk <= 128)
+    k_chunk_sort<128, 1><<<grid, 128, 0, s>>>(order_c, zlo, P, chunk, order_out);
+  else if (chunk <= 512)
+    k_chunk_sort<128, 4><<<grid, 128, 0, s>>>(order_c, zlo, P, chunk, order_out);
+  else if (chunk <= 2048)
+    k_chunk_sort<256, 8><<<grid, 256, 0, s>>>(order_c, zlo, P, chunk, order_out);
+  else
+    return false;
+  return true;
 }
 void launch_rank_of(const uint32_t* order, int64_t P, uint32_t* rank_of, cudaStream_t s) {
   if (P == 0) return;

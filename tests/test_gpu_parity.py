@@ -369,19 +369,21 @@ def test_near_plane_straddlers_match_oracle(name):
     assert massf == 0, (strict, massf, total)
 
 
+@pytest.mark.parametrize("cs", [1, 128])
 @pytest.mark.parametrize("name", ["exponential", "softplus_20", "blended_0.5"])
-def test_progressive_binning_is_bit_identical_to_full(name):
+def test_progressive_binning_is_bit_identical_to_full(name, cs):
     """Depth-phased binning (only still-active tiles get later ranks) must
-    replay exactly the same entries per pixel as binning everything at once."""
+    replay exactly the same entries per pixel as binning everything at once
+    (global order, and chunked order with phases cut on chunk boundaries)."""
     import torch
     sc = O.round_scene_f32(O.canonical_scene(100_000, seed=1))
     cam = O.canonical_camera(512, 384, 2, 8)
     bg = np.array([0.1, 0.05, 0.2])
     seed = O.canonical_seed(512, 384, 2)
     model = MODELS[name]
-    full = gpu_run(sc, cam, model, bg, seed=seed, full_binning=True)
+    full = gpu_run(sc, cam, model, bg, seed=seed, full_binning=True, chunk_size=cs)
     for first in (0, 5000, 20000):
-        prog = gpu_run(sc, cam, model, bg, seed=seed, first_phase_ranks=first)
+        prog = gpu_run(sc, cam, model, bg, seed=seed, first_phase_ranks=first, chunk_size=cs)
         assert np.array_equal(prog["rgb"], full["rgb"])
         assert np.array_equal(prog["overdraw"], full["overdraw"])
         assert np.array_equal(prog["residual"], full["residual"])
@@ -562,20 +564,21 @@ def test_chunk_at_least_count_is_the_exact_order():
     assert c["stats"]["n_overflow"] == 0  # two chunks: the chunked path proper
 
 
-@pytest.mark.parametrize("name", ["exponential", "softplus_20"])
-def test_chunked_c2_sampled_pixels_match_oracle(name):
+@pytest.mark.parametrize("name,cs", [("exponential", 128), ("softplus_20", 128),
+                                     ("softplus_20", 5000)])  # 5000: global-sort fallback
+def test_chunked_c2_sampled_pixels_match_oracle(name, cs):
     sc = O.round_scene_f32(O.canonical_scene(100_000, seed=0))
     cam = O.canonical_camera(512, 512)
     bg = np.array([0.1, 0.05, 0.2], dtype=np.float32).astype(np.float64)
     model = MODELS[name]
     px = np.random.default_rng(13).choice(512 * 512, 128, replace=False)
-    fwd = O.forward(sc, cam, model, bg, chunk_size=128, pixels=px, keep_state=True, batch=16)
+    fwd = O.forward(sc, cam, model, bg, chunk_size=cs, pixels=px, keep_state=True, batch=16)
     seed_px = O.canonical_seed(512, 512, 0).reshape(-1, 3)[px].astype(np.float32).astype(
         np.float64) * (~fwd["mask"])[:, None]
     g_ref, mass = O.backward(sc, cam, model, bg, fwd, seed_px, with_mass=True)
     seed_full = np.zeros((512 * 512, 3))
     seed_full[px] = seed_px
-    got = gpu_run(sc, cam, model, bg, seed=seed_full.reshape(512, 512, 3), chunk_size=128)
+    got = gpu_run(sc, cam, model, bg, seed=seed_full.reshape(512, 512, 3), chunk_size=cs)
     keep = ~fwd["mask"]
     ok = close(got["rgb"].reshape(-1, 3)[px], fwd["rad"]).all(1) & \
         (got["overdraw"].reshape(-1)[px] == fwd["overdraw"]) & \
