@@ -68,6 +68,8 @@ extern "C" {
 /* opts.flags */
 #define NXS_FLAG_COUNT_EVENTS 1    /* count tests/composites (instrumented run) */
 #define NXS_FLAG_FULL_BINNING 2    /* bin every rank in one phase (no progressive binning) */
+#define NXS_FLAG_XBUF32 4          /* chunked order: start with the 32-entry pending buffer
+                                      (default 16, rerun with 32 on overflow) */
 
 /* ordering: opts.chunk_size (reference render(..., chunk_size=), render.py:350-358)
  *   NXS_CHUNK_EXACT (None) or C >= count: one chunk, exact per-pixel t order

@@ -600,7 +600,8 @@ retry_sort:
                   opts->max_splats, (float)opts->alpha_cutoff, opts->near_plane,
                   {bgf[0], bgf[1], bgf[2]}, rgb, overdraw, residual, v->seq.as<int32_t>(),
                   dsmall + 9, n_ph > 1 ? v->active.as<uint8_t>() : nullptr,
-                  n_ph > 1 ? n_active : nullptr, ph > 0, ph + 1 < n_ph};
+                  n_ph > 1 ? n_active : nullptr, ph > 0, ph + 1 < n_ph,
+                  (chunked && !(opts->flags & NXS_FLAG_XBUF32)) ? 16 : 32};
       launch_blend_fwd_x(count, n_tiles, xa, cam, md, v->cache(), v->resume(), cnt, s);
       NXS_LAUNCHED("blend_fwd_x");
       if (v->ev_ok) cudaEventRecord(v->evp[ph][2], s);
@@ -629,6 +630,13 @@ retry_sort:
                              cudaMemcpyDeviceToHost, s));
     NXS_CUDA(cudaStreamSynchronize(s));
     v->stats.n_overflow = (int64_t)v->host_small[7];
+    if (v->host_small[7] > 0 && chunked && !(opts->flags & NXS_FLAG_XBUF32)) {
+      // the small pending buffer overflowed: redo the pass with the large one
+      nxs_opts o2 = *opts;
+      o2.flags |= NXS_FLAG_XBUF32;
+      return nxs_forward(v, scene, camera, model, &o2, background, rgb, overdraw, residual,
+                         stream_);
+    }
     if (v->host_small[7] > 0)
       return fail(NXS_ERR_OVERFLOW, std::to_string(v->host_small[7]) +
                                         " pixel-entries overflowed the exact-order pending "

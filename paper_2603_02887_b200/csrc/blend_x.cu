@@ -23,14 +23,19 @@
 
 namespace nxs {
 
-constexpr int XBUF = 32;     // pending entries per pixel
+// pending entries per pixel: 16 for the chunked order (a chunk flush empties
+// the buffer; an overflow reruns with 32), 32 for the exact order
 constexpr int XBATCH = 64;   // list entries staged per batch
 // records of the current and the previous batch stay staged (a ring of
 // 2*XBATCH): most commits are of recently tested entries
-constexpr size_t FWDX_SMEM = sizeof(float4) * 2 * XBATCH * REC_F4 +
-                             sizeof(uint32_t) * 2 * XBATCH + sizeof(uint32_t) * XBATCH +
-                             sizeof(float) * XBATCH + sizeof(uint32_t) * XBATCH +
-                             (sizeof(float) + sizeof(int)) * XBUF * TILE_PIX;
+// the 16-entry buffer also keeps each pending entry's alpha (no re-test at
+// commit); the 32-entry one re-tests so that two blocks still fit an SM
+constexpr bool keeps_alpha(int xb) { return xb <= 16; }
+constexpr size_t fwdx_smem(int xb) {
+  return sizeof(float4) * 2 * XBATCH * REC_F4 + sizeof(uint32_t) * 2 * XBATCH +
+         (sizeof(uint32_t) + sizeof(float) + sizeof(uint32_t)) * XBATCH +
+         (sizeof(float) + sizeof(int) + (keeps_alpha(xb) ? sizeof(float) : 0)) * xb * TILE_PIX;
+}
 
 struct FwdXPix {
   float rad0, rad1, rad2, thi, tlo, P, Trem, ek0, ek1, ek2, tk, sea0, sea1, sea2, sa, Pck;
@@ -104,8 +109,8 @@ __device__ __forceinline__ bool test_with_t(const float4* rec, const CamDev& cam
   return true;
 }
 
-template <int FAM, bool COUNT>
-__global__ void __launch_bounds__(TILE_PIX)
+template <int FAM, bool COUNT, int XBUF>
+__global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
     k_blend_fwd_x(const float4* __restrict__ records, const uint32_t* __restrict__ pairs,
                   const int2* __restrict__ ranges, const float* __restrict__ zlo_rank,
                   const uint32_t* __restrict__ order, const uint32_t* __restrict__ rank_c,
@@ -126,6 +131,7 @@ __global__ void __launch_bounds__(TILE_PIX)
   uint32_t* s_chunk = reinterpret_cast<uint32_t*>(s_zlo + XBATCH);
   float* bt = reinterpret_cast<float*>(s_chunk + XBATCH);    // [XBUF][TILE_PIX] pending t
   int* bp = reinterpret_cast<int*>(bt + XBUF * TILE_PIX);     // [XBUF][TILE_PIX] list position
+  float* ba = reinterpret_cast<float*>(bp + XBUF * TILE_PIX);  // [XBUF][TILE_PIX] alpha
 
   const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
   const int tid = threadIdx.x;
@@ -179,33 +185,42 @@ __global__ void __launch_bounds__(TILE_PIX)
     return rank_c ? rank_c[g] : g;
   };
 
-  // commit the smallest pending entry: re-read its record (L1/L2; every
-  // pixel of the tile commits the same few entries) and composite it
+  // commit the smallest pending entry: its alpha was kept at insertion, the
+  // emission re-reads the record's SH words (staged ring, else L1/L2)
   int ring_lo = 0;  // list positions [ring_lo, current batch end) are staged
   auto commit_front = [&]() {
-    const int pos = bp[head * TILE_PIX + tid];
+    const int slot = head * TILE_PIX + tid;
+    const int pos = bp[slot];
     head = (head + 1) & (XBUF - 1);
     --nb;
+    // explicit shared / global branches (no generic loads)
     float4 r[REC_F4];
+    constexpr int K0 = keeps_alpha(XBUF) ? 4 : 0, K1 = keeps_alpha(XBUF) ? 7 : REC_F4;
     uint32_t rank;
     if (pos >= ring_lo) {
       const float4* rec = s_ring[pos % (2 * XBATCH)];
       rank = s_ring_rank[pos % (2 * XBATCH)];
 #pragma unroll
-      for (int k = 0; k < REC_F4; ++k) r[k] = rec[k];
+      for (int k = K0; k < K1; ++k) r[k] = rec[k];
     } else {
       rank = pairs[pos];
       const float4* rec = records + (size_t)rank * REC_F4;
 #pragma unroll
-      for (int k = 0; k < REC_F4; ++k) r[k] = __ldg(rec + k);
+      for (int k = K0; k < K1; ++k) r[k] = __ldg(rec + k);
     }
-    TestOut t;
-    float tpk;
-    test_with_t(r, cam, px, py, pc, hnorm, cutoff, near_plane, t, tpk);  // valid by construction
+    float alpha;
+    if constexpr (keeps_alpha(XBUF)) {
+      alpha = ba[slot];
+    } else {
+      TestOut t;
+      float tpk;
+      test_with_t(r, cam, px, py, pc, hnorm, cutoff, near_plane, t, tpk);  // valid by construction
+      alpha = t.alpha;
+    }
     float E0, E1, E2;
     emission(r[4], r[5], r[6], pc, E0, E1, E2);
     myseq[(size_t)s.count * npix] = (int32_t)rank;
-    composite<FAM>(s, m, max_splats, t.alpha, E0, E1, E2);
+    composite<FAM>(s, m, max_splats, alpha, E0, E1, E2);
   };
 
   const int2 rg = ranges[tile];
@@ -266,11 +281,13 @@ __global__ void __launch_bounds__(TILE_PIX)
           const int f = (head + i) & (XBUF - 1);
           bt[f * TILE_PIX + tid] = te;
           bp[f * TILE_PIX + tid] = bp[e * TILE_PIX + tid];
+          if constexpr (keeps_alpha(XBUF)) ba[f * TILE_PIX + tid] = ba[e * TILE_PIX + tid];
           --i;
         }
         const int f = (head + i) & (XBUF - 1);
         bt[f * TILE_PIX + tid] = tpk;
         bp[f * TILE_PIX + tid] = pos;
+        if constexpr (keeps_alpha(XBUF)) ba[f * TILE_PIX + tid] = t.alpha;
         ++nb;
       }
     }
@@ -446,22 +463,31 @@ static void set_smem(K k, size_t bytes) {
                        (int)cudaSharedmemCarveoutMaxShared);
 }
 
+template <int FAM, int XB>
+static void launch_fwd_x_xb(bool count, int n_tiles, const FwdXArgs& a, const CamDev& cam,
+                            const ModelDev& m, const PixCache& cache, const PixResume& rs,
+                            Counters* cnt, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    set_smem(k_blend_fwd_x<FAM, true, XB>, fwdx_smem(XB));
+    set_smem(k_blend_fwd_x<FAM, false, XB>, fwdx_smem(XB));
+    attr = true;
+  }
+  auto k = count ? k_blend_fwd_x<FAM, true, XB> : k_blend_fwd_x<FAM, false, XB>;
+  k<<<n_tiles, TILE_PIX, fwdx_smem(XB), s>>>(
+      a.records, a.pairs, a.ranges, a.zlo_rank, a.order, a.rank_c, a.chunk, cam, m, a.max_splats,
+      a.cutoff, a.near_plane, a.bg[0], a.bg[1], a.bg[2], a.rgb, a.overdraw, a.residual, cache, rs,
+      a.seq, a.overflow, a.active, a.n_active, a.resume, a.save, cnt);
+}
+
 template <int FAM>
 static void launch_fwd_x_fam(bool count, int n_tiles, const FwdXArgs& a, const CamDev& cam,
                              const ModelDev& m, const PixCache& cache, const PixResume& rs,
                              Counters* cnt, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    set_smem(k_blend_fwd_x<FAM, true>, FWDX_SMEM);
-    set_smem(k_blend_fwd_x<FAM, false>, FWDX_SMEM);
-    attr = true;
-  }
-  auto k = count ? k_blend_fwd_x<FAM, true> : k_blend_fwd_x<FAM, false>;
-  k<<<n_tiles, TILE_PIX, FWDX_SMEM, s>>>(a.records, a.pairs, a.ranges, a.zlo_rank, a.order, a.rank_c,
-                                         a.chunk, cam, m, a.max_splats, a.cutoff, a.near_plane, a.bg[0], a.bg[1],
-                                         a.bg[2], a.rgb, a.overdraw, a.residual, cache, rs,
-                                         a.seq, a.overflow, a.active, a.n_active, a.resume,
-                                         a.save, cnt);
+  if (a.xbuf <= 16)
+    launch_fwd_x_xb<FAM, 16>(count, n_tiles, a, cam, m, cache, rs, cnt, s);
+  else
+    launch_fwd_x_xb<FAM, 32>(count, n_tiles, a, cam, m, cache, rs, cnt, s);
 }
 
 void launch_blend_fwd_x(bool count, int n_tiles, const FwdXArgs& a, const CamDev& cam,

@@ -140,6 +140,7 @@ struct FwdXArgs {
   uint8_t* active;
   unsigned int* n_active;
   bool resume, save;
+  int xbuf;  // pending entries per pixel (16 or 32)
 };
 struct BwdXArgs {
   const float4* records;
