@@ -38,7 +38,7 @@ void launch_blend_fwd_x(bool, int, const FwdXArgs&, const CamDev&, const ModelDe
 void launch_blend_bwd_x(bool, int, const BwdXArgs&, const CamDev&, const ModelDev&,
                         const PixCache&, Counters*, cudaStream_t);
 void launch_count_active(const int4*, const uint32_t*, int64_t, int64_t, int, const uint8_t*,
-                         unsigned long long*, cudaStream_t);
+                         const unsigned int*, unsigned long long*, cudaStream_t);
 void launch_emit_pairs(const int4*, const uint32_t*, const unsigned long long*, int64_t, int64_t,
                        int, const uint8_t*, uint32_t*, uint32_t*, cudaStream_t);
 void launch_tile_ranges(const uint32_t*, int64_t, int2*, cudaStream_t);
@@ -512,7 +512,8 @@ retry_sort:
     // ---- K2a counts over active tiles, scan, one host sync for the pair count
     if (nr > 0) {
       launch_count_active(v->rects.as<int4>(), v->idx_out.as<uint32_t>(), r0, r1, cam.tiles_x,
-                          v->active.as<uint8_t>(), v->ntiles.as<unsigned long long>(), s);
+                          v->active.as<uint8_t>(), ph > 0 ? n_active : nullptr,
+                          v->ntiles.as<unsigned long long>(), s);
       NXS_LAUNCHED("count_active");
       size_t tb = v->temp.cap;
       NXS_CUDA(cub::DeviceScan::ExclusiveSum(v->temp.p, tb, v->ntiles.as<unsigned long long>(),

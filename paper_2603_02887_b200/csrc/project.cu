@@ -656,7 +656,11 @@ __global__ void __launch_bounds__(PROJ_CHUNK)
 __global__ void k_count_active(const int4* __restrict__ rects, const uint32_t* __restrict__ order,
                                int64_t r0, int64_t r1, int tiles_x,
                                const uint8_t* __restrict__ active,
+                               const unsigned int* __restrict__ gate,
                                unsigned long long* __restrict__ counts) {
+  // later phases: nothing to count when the previous forward left no tile
+  // active (the host then stops before reading the counts)
+  if (gate && *gate == 0u) return;
   const int64_t r = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= r1) return;
   const int4 rc = rects[order[r]];
@@ -762,11 +766,11 @@ void launch_project(const float* centers, const float* scales, const float* quat
 }
 
 void launch_count_active(const int4* rects, const uint32_t* order, int64_t r0, int64_t r1,
-                         int tiles_x, const uint8_t* active, unsigned long long* counts,
-                         cudaStream_t s) {
+                         int tiles_x, const uint8_t* active, const unsigned int* gate,
+                         unsigned long long* counts, cudaStream_t s) {
   if (r1 <= r0) return;
   k_count_active<<<(unsigned)((r1 - r0 + 255) / 256), 256, 0, s>>>(rects, order, r0, r1, tiles_x,
-                                                                   active, counts);
+                                                                   active, gate, counts);
 }
 
 void launch_emit_pairs(const int4* rects, const uint32_t* order, const unsigned long long* offsets,
