@@ -192,6 +192,42 @@ int nxs_binning_export(nxs_view* view, int32_t* rects, int32_t* ranges,
 /* Projected per-rank records (P x 32 float32) of the last forward. */
 int nxs_records_export(nxs_view* view, float* records, void* stream);
 
+/* ---- train-step neighbours ---------------------------- */
+
+/* Image loss (reference optimizer.py:128-152 loss(), :68-111 ssim(),
+ * :114-118 mse()): (1 - lam) L1 + lam (1 - SSIM) in sRGB between the linear
+ * render and target (device float32, H*W*3, row-major), 11x11 Gaussian
+ * window (sigma 1.5) over fully-interior windows, computed in fp64.
+ * out (device, 4 doubles): total, L1, mean SSIM (0 when lam == 0), MSE of
+ * the clipped sRGB images.  seed (device H*W*3, may be NULL): d total /
+ * d render, the adjoint seed for nxs_backward.  With NXS_LOSS_SRGB_INPUT the
+ * inputs are already sRGB (the reference ssim(x, y) semantics) and seed is
+ * d total / d x.  workspace: nxs_loss_workspace_bytes(H, W) device bytes.
+ * lam > 0 needs H, W >= 11 (reference ValueError). */
+#define NXS_LOSS_SRGB_INPUT 1
+int64_t nxs_loss_workspace_bytes(int32_t height, int32_t width);
+int nxs_image_loss(const float* rendered, const float* target, int32_t height, int32_t width,
+                   double lam, int32_t flags, double* out, float* seed, void* workspace,
+                   void* stream);
+
+/* One bounded Adam step (reference optimizer.py:173-204 bounded_adam_step):
+ * groups[5] in the order centers, scales, quats, opacities, sh (device
+ * float32 param / grad / m / v of `count` elements; param NULL skips the
+ * group).  Non-finite gradients are zeroed and counted into *nan_skips
+ * (device u64); scales are floored at 1e-6, opacities clamped to
+ * [1e-4, 1 - 1e-6], quaternion rows renormalised.  step = Adam step t >= 1
+ * (after increment), betas 0.9 / 0.999, eps 1e-8. */
+typedef struct {
+    float* param;
+    const float* grad;
+    float* m;
+    float* v;
+    int64_t count;
+    double lr;
+} nxs_adam_group;
+int nxs_adam_step(const nxs_adam_group* groups, int64_t step, double lr_mult,
+                  unsigned long long* nan_skips, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -6,7 +6,9 @@ Drop-in for the reference package's image-renderer path (``nexsplat.render``:
 hand-written sm_100a CUDA library ``lib/libnxs.so`` (C-ABI: include/nxs.h).
 The host-side descriptors (``TransmittanceModel``, ``Camera``,
 ``GaussianPrimitive``) mirror the reference's so existing callers can switch
-imports; the reference's own objects are accepted as well.
+imports; the reference's own objects are accepted as well.  ``optim``
+holds the device loss / SSIM / bounded Adam of the reference optimizer
+(the train-step neighbours of the render path).
 """
 from .camera import (
     ALPHA_EPS,
@@ -32,6 +34,8 @@ from .render import (
     zero_grads_device,
 )
 from .transmittance import TransmittanceModel, model_from_config, model_to_config
+from . import optim
+from .optim import AdamState, bounded_adam_step, loss, mse, psnr, ssim
 
 __version__ = "0.1.0"
 
@@ -42,4 +46,5 @@ __all__ = [
     "render_backward", "render_with_gradients", "forward_device", "backward_device",
     "zero_grads_device",
     "TransmittanceModel", "model_from_config", "model_to_config",
+    "optim", "AdamState", "bounded_adam_step", "loss", "mse", "psnr", "ssim",
 ]

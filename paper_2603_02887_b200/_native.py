@@ -42,6 +42,9 @@ SYMBOLS = (
     "nxs_depth_order",
     "nxs_binning_export",
     "nxs_records_export",
+    "nxs_loss_workspace_bytes",
+    "nxs_image_loss",
+    "nxs_adam_step",
 )
 
 NXS_ERR_GEOMETRY = -6
@@ -50,6 +53,8 @@ NXS_ERR_UNSUPPORTED = -2
 NXS_ERR_INVALID = -1
 NXS_FLAG_COUNT_EVENTS = 1
 NXS_FLAG_FULL_BINNING = 2
+NXS_FLAG_XBUF32 = 4
+NXS_LOSS_SRGB_INPUT = 1
 
 
 class NativeLibraryError(ImportError):
@@ -101,6 +106,11 @@ class Scene(C.Structure):
     ]
 
 
+class AdamGroup(C.Structure):
+    _fields_ = [("param", C.c_void_p), ("grad", C.c_void_p), ("m", C.c_void_p),
+                ("v", C.c_void_p), ("count", C.c_int64), ("lr", C.c_double)]
+
+
 class Stats(C.Structure):
     _fields_ = [(n, C.c_int64) for n in (
         "n_gaussians", "n_visible", "n_pairs", "n_straddling", "n_tiles", "n_tests_fwd",
@@ -142,8 +152,13 @@ def lib():
     h.nxs_depth_order.argtypes = [vp, vp, vp]
     h.nxs_binning_export.argtypes = [vp, vp, vp, vp, vp]
     h.nxs_records_export.argtypes = [vp, vp, vp]
+    h.nxs_loss_workspace_bytes.argtypes = [i32, i32]
+    h.nxs_loss_workspace_bytes.restype = i64
+    h.nxs_image_loss.argtypes = [vp, vp, i32, i32, C.c_double, i32, vp, vp, vp, vp]
+    h.nxs_adam_step.argtypes = [C.POINTER(AdamGroup), i64, C.c_double, vp, vp]
     for name in SYMBOLS:
-        if name not in ("nxs_error_string", "nxs_last_error", "nxs_view_bytes"):
+        if name not in ("nxs_error_string", "nxs_last_error", "nxs_view_bytes",
+                        "nxs_loss_workspace_bytes"):
             getattr(h, name).restype = C.c_int
     if h.nxs_abi_version() != 1:
         raise NativeLibraryError("libnxs ABI version mismatch")

@@ -108,6 +108,11 @@ int bits_for(uint32_t n) {
 
 }  // namespace
 
+namespace nxs {
+// error reporting for entry points defined in other translation units
+int set_last_error(int code, const char* msg) { return fail(code, msg); }
+}  // namespace nxs
+
 struct nxs_view {
   // per Gaussian
   Buf dkeys_in, dkeys_out, idx_in, idx_out, records, bframe, rects, ntiles, offsets, moments,

@@ -25,6 +25,11 @@ Fixtures (all scenes are stored, so nothing is regenerated at test time):
                       C1 scene at chunk_size 128 (the TrainConfig default,
                       reference optimizer.py:278) and 64, 5 models, gradients
                       for exp/linear/quadratic(0.5).
+  golden_train.npz    train-step neighbours: loss() for lam 0 / 0.2 / 1 on
+                      fp32-rounded 37x53 images (values over and below the
+                      sRGB knee and above 1), ssim(x, y, with_grad=True),
+                      mse/psnr, and three bounded_adam_step() calls on a
+                      64-Gaussian parameter set (one gradient with NaN/inf).
 """
 from __future__ import annotations
 
@@ -231,8 +236,52 @@ def chunk():
     np.savez_compressed(OUT / "golden_chunk.npz", **d)
 
 
+def train():
+    from nexsplat.optimizer import AdamState, bounded_adam_step, loss, mse, psnr, ssim
+    rng = np.random.default_rng(17)
+    H, W = 37, 53
+    d = {}
+    ren = f32(np.clip(rng.normal(0.4, 0.35, (H, W, 3)), -0.05, 1.3))
+    ren[:3, :3] = 0.001  # below the sRGB knee
+    tgt = f32(np.clip(ren + rng.normal(0, 0.1, (H, W, 3)), 0.0, 1.2))
+    tgt[5, 5] = ren[5, 5]  # a zero difference (sign 0)
+    d["rendered"], d["target"] = ren, tgt
+    for lam in (0.0, 0.2, 1.0):
+        total, seed = loss(ren, tgt, lam)
+        d[f"loss_{lam}"] = total
+        d[f"seed_{lam}"] = seed
+    x, y = f32(rng.uniform(0, 1, (H, W, 3))), f32(rng.uniform(0, 1, (H, W, 3)))
+    d["ssim_x"], d["ssim_y"] = x, y
+    d["ssim_value"], d["ssim_grad"] = ssim(x, y, with_grad=True)
+    d["mse"], d["psnr"] = mse(ren, tgt), psnr(ren, tgt)
+    n = 64
+    params = {"centers": f32(rng.normal(0, 1, (n, 3))),
+              "scales": f32(rng.uniform(1e-6, 0.2, (n, 3))),
+              "quats": f32(rng.normal(0, 1, (n, 4))),
+              "opacities": f32(rng.uniform(0.0, 1.0, n)),
+              "sh": f32(rng.normal(0, 0.5, (n, 3, 4)))}
+    params["quats"] = f32(params["quats"] / np.linalg.norm(params["quats"], axis=1,
+                                                          keepdims=True))
+    for k, v in params.items():
+        d["p0_" + k] = v.copy()
+    state = AdamState.for_params(params)
+    lr = {"centers": 0.13, "scales": 0.08, "quats": 0.45, "opacities": 1.0, "sh": 2.0}
+    for step in range(3):
+        grads = {k: f32(rng.normal(0, 0.3, v.shape)) for k, v in params.items()}
+        if step == 1:
+            grads["centers"][2, 1] = np.nan
+            grads["sh"][5, 0, 0] = np.inf
+        for k, v in grads.items():
+            d[f"g{step}_{k}"] = v
+        bounded_adam_step(params, grads, state, lr, lr_mult=0.9)
+        for k, v in params.items():
+            d[f"p{step + 1}_{k}"] = v.copy()
+    d["nan_skips"] = state.nan_skips
+    np.savez_compressed(OUT / "golden_train.npz", **d)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["small", "c1", "fd", "transmit", "order", "chunk"]
+    which = sys.argv[1:] or ["small", "c1", "fd", "transmit", "order", "chunk", "train"]
     for w in which:
         globals()[w]()
         print("wrote", w)

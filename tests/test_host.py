@@ -120,3 +120,16 @@ def test_render_requires_device_no_cpu_fallback():
     cam = nx.Camera.from_look_at([0, 0, 0], [0, 0, 1], [0, 1, 0], 50.0, 8, 8)
     with pytest.raises(Exception):
         nx.render(arrs, cam, nx.TransmittanceModel.linear(), np.zeros(3), chunk_size=1)
+
+
+def test_optim_validation_matches_reference():
+    """reference optimizer.py:84-87, 134-138 (raised before any device work)"""
+    from paper_2603_02887_b200 import optim
+    a = np.zeros((16, 16, 3))
+    with pytest.raises(ValueError):
+        optim.loss(a, np.zeros((16, 15, 3)), 0.2)
+    with pytest.raises(ValueError):
+        optim.loss(a, a, 1.5)
+    with pytest.raises(ValueError):
+        optim.ssim(np.zeros((10, 20, 3)), np.zeros((10, 20, 3)))
+    assert optim.PARAM_GROUPS == ("centers", "scales", "quats", "opacities", "sh")

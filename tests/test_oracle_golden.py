@@ -145,3 +145,50 @@ def test_chunked_c1_matches_reference(name, cs):
         for k in GRAD_FIELDS:
             ref = CHUNK[tag + "__g_" + k]
             np.testing.assert_allclose(g[k], ref, rtol=1e-9, atol=1e-12 * np.abs(ref).max())
+
+
+# ---------------------------------------------------------------------------
+# train-step neighbours: oracle/train_oracle.py against
+# the reference's loss / ssim / mse / psnr / bounded_adam_step
+# ---------------------------------------------------------------------------
+TRAIN = load("golden_train.npz")
+
+
+@pytest.mark.parametrize("lam", [0.0, 0.2, 1.0])
+def test_train_oracle_loss_matches_reference(lam):
+    from oracle import train_oracle as T
+    total, seed = T.loss(TRAIN["rendered"], TRAIN["target"], lam)
+    assert total == pytest.approx(float(TRAIN[f"loss_{lam}"]), rel=1e-13)
+    np.testing.assert_allclose(seed, TRAIN[f"seed_{lam}"], rtol=1e-11,
+                               atol=1e-14 * np.abs(TRAIN[f"seed_{lam}"]).max())
+
+
+def test_train_oracle_ssim_mse_psnr_match_reference():
+    from oracle import train_oracle as T
+    v, g = T.ssim(TRAIN["ssim_x"], TRAIN["ssim_y"], with_grad=True)
+    assert v == pytest.approx(float(TRAIN["ssim_value"]), rel=1e-13)
+    np.testing.assert_allclose(g, TRAIN["ssim_grad"], rtol=1e-10,
+                               atol=1e-14 * np.abs(TRAIN["ssim_grad"]).max())
+    assert T.mse(TRAIN["rendered"], TRAIN["target"]) == pytest.approx(float(TRAIN["mse"]),
+                                                                        rel=1e-13)
+    assert T.psnr(TRAIN["rendered"], TRAIN["target"]) == pytest.approx(float(TRAIN["psnr"]),
+                                                                         rel=1e-13)
+    with pytest.raises(ValueError):
+        T.ssim(np.zeros((10, 20, 3)), np.zeros((10, 20, 3)))
+
+
+def test_train_oracle_adam_matches_reference():
+    from oracle import train_oracle as T
+    keys = ("centers", "scales", "quats", "opacities", "sh")
+    params = {k: TRAIN["p0_" + k].copy() for k in keys}
+    m = {k: np.zeros_like(v) for k, v in params.items()}
+    v = {k: np.zeros_like(x) for k, x in params.items()}
+    lr = {"centers": 0.13, "scales": 0.08, "quats": 0.45, "opacities": 1.0, "sh": 2.0}
+    skips = 0
+    for step in range(3):
+        grads = {k: TRAIN[f"g{step}_{k}"] for k in keys}
+        skips += T.bounded_adam_step(params, grads, m, v, step + 1, lr, 0.9)
+        for k in keys:
+            np.testing.assert_allclose(params[k], TRAIN[f"p{step + 1}_{k}"], rtol=1e-13,
+                                       atol=1e-15)
+    assert skips == int(TRAIN["nan_skips"]) == 2
