@@ -228,6 +228,21 @@ typedef struct {
 int nxs_adam_step(const nxs_adam_group* groups, int64_t step, double lr_mult,
                   unsigned long long* nan_skips, void* stream);
 
+/* ---- per-ray batched compositing --------------------- */
+
+/* composite_batch (reference compositor.py:84-171), fp64: R rays of N
+ * front-to-back samples.  alpha (R*N), emission (R*N*3), valid (R*N uint8,
+ * NULL = all valid; padding must be 0), background: 3 host doubles.
+ * Device outputs (only radiance is required): weights (R*N clamped
+ * extinction weights), radiance (R*3), residual (R), k0 (R, 0-based
+ * saturation index, N when none), overdraw (R), e_k (R*3), theta0 (R*3),
+ * t_k (R).  Backs finite_diff_gradients (adjoint.py:195-222). */
+int nxs_composite_batch(const nxs_model* model, const double* alpha, const double* emission,
+                        const uint8_t* valid, int64_t rays, int64_t samples,
+                        const double background[3], double* weights, double* radiance,
+                        double* residual, int64_t* k0, int64_t* overdraw, double* e_k,
+                        double* theta0, double* t_k, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

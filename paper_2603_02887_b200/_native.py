@@ -45,6 +45,7 @@ SYMBOLS = (
     "nxs_loss_workspace_bytes",
     "nxs_image_loss",
     "nxs_adam_step",
+    "nxs_composite_batch",
 )
 
 NXS_ERR_GEOMETRY = -6
@@ -156,6 +157,8 @@ def lib():
     h.nxs_loss_workspace_bytes.restype = i64
     h.nxs_image_loss.argtypes = [vp, vp, i32, i32, C.c_double, i32, vp, vp, vp, vp]
     h.nxs_adam_step.argtypes = [C.POINTER(AdamGroup), i64, C.c_double, vp, vp]
+    h.nxs_composite_batch.argtypes = [C.POINTER(Model), vp, vp, vp, i64, i64,
+                                      C.POINTER(C.c_double), vp, vp, vp, vp, vp, vp, vp, vp, vp]
     for name in SYMBOLS:
         if name not in ("nxs_error_string", "nxs_last_error", "nxs_view_bytes",
                         "nxs_loss_workspace_bytes"):

@@ -30,6 +30,10 @@ Fixtures (all scenes are stored, so nothing is regenerated at test time):
                       sRGB knee and above 1), ssim(x, y, with_grad=True),
                       mse/psnr, and three bounded_adam_step() calls on a
                       64-Gaussian parameter set (one gradient with NaN/inf).
+  golden_batch.npz    composite_batch() of 300 rays x 40 samples (ragged
+                      valid masks, saturating and non-saturating rays, an
+                      exactly-saturating ray) for the 7 models, N = 0, and
+                      finite_diff_gradients() of a 6-sample ray.
 """
 from __future__ import annotations
 
@@ -280,8 +284,44 @@ def train():
     np.savez_compressed(OUT / "golden_train.npz", **d)
 
 
+def batch():
+    from nexsplat.adjoint import finite_diff_gradients
+    from nexsplat.compositor import SplatSample, composite_batch
+    rng = np.random.default_rng(23)
+    R, N = 300, 40
+    alpha = rng.uniform(0.0, 0.35, (R, N))
+    alpha[:50] *= 0.1                      # rays that never saturate
+    alpha[50:60, :3] = 0.999999            # early saturation
+    alpha[60, :] = 0.0
+    alpha[60, :4] = 0.25                   # linear: cumulative weight exactly 1 at i = 3
+    emission = rng.uniform(0.0, 2.0, (R, N, 3))
+    lengths = rng.integers(0, N + 1, R)
+    valid = np.arange(N)[None, :] < lengths[:, None]
+    valid[61] = rng.uniform(size=N) < 0.5  # holes inside a ray
+    alpha = np.where(valid, alpha, 0.0)
+    bg = np.array([0.1, 0.2, 0.3])
+    d = {"alpha": alpha, "emission": emission, "valid": valid, "bg": bg}
+    for name, m in MODELS.items():
+        out = composite_batch(m, alpha, emission, bg, valid)
+        for k, v in out.items():
+            d[f"{name}__{k}"] = v
+    out0 = composite_batch(MODELS["linear"], np.zeros((3, 0)), np.zeros((3, 0, 3)), bg)
+    for k, v in out0.items():
+        d[f"empty__{k}"] = v
+    samples = [SplatSample(1.0 + i, float(a), tuple(float(x) for x in e))
+               for i, (a, e) in enumerate(zip(rng.uniform(0.05, 0.5, 6),
+                                              rng.uniform(0.1, 1.0, (6, 3))))]
+    d["fd_alpha"] = np.array([s.alpha for s in samples])
+    d["fd_emission"] = np.array([s.emission for s in samples])
+    for name in ("exponential", "linear", "softplus_20", "blended_0.5"):
+        g = finite_diff_gradients(MODELS[name], samples, bg, eps=1e-5, seed=(0.3, 1.0, 0.7))
+        d[f"fd__{name}__d_alpha"] = g.d_alpha
+        d[f"fd__{name}__d_emission"] = g.d_emission
+    np.savez_compressed(OUT / "golden_batch.npz", **d)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["small", "c1", "fd", "transmit", "order", "chunk", "train"]
+    which = sys.argv[1:] or ["small", "c1", "fd", "transmit", "order", "chunk", "train", "batch"]
     for w in which:
         globals()[w]()
         print("wrote", w)

@@ -133,3 +133,20 @@ def test_optim_validation_matches_reference():
     with pytest.raises(ValueError):
         optim.ssim(np.zeros((10, 20, 3)), np.zeros((10, 20, 3)))
     assert optim.PARAM_GROUPS == ("centers", "scales", "quats", "opacities", "sh")
+
+
+def test_batch_validation_matches_reference():
+    """compositor.py:36-50 sample validation; adjoint.py:200-201 eps check;
+    shape checks happen before any device work."""
+    from paper_2603_02887_b200 import batch
+    with pytest.raises(ValueError):
+        batch.SplatSample(1.0, 1.0, (0.1, 0.1, 0.1))
+    with pytest.raises(ValueError):
+        batch.SplatSample(1.0, 0.5, (-0.1, 0.1, 0.1))
+    with pytest.raises(ValueError):
+        batch.finite_diff_gradients(nx.TransmittanceModel.linear(), [], np.zeros(3), eps=0.0)
+    with pytest.raises(ValueError):
+        batch.composite_batch(nx.TransmittanceModel.linear(), np.zeros(4), np.zeros((4, 3)),
+                              np.zeros(3))
+    g = batch.finite_diff_gradients(nx.TransmittanceModel.linear(), [], np.zeros(3))
+    assert g.d_alpha.shape == (0,) and g.d_emission.shape == (0, 3)

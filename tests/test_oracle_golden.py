@@ -192,3 +192,35 @@ def test_train_oracle_adam_matches_reference():
             np.testing.assert_allclose(params[k], TRAIN[f"p{step + 1}_{k}"], rtol=1e-13,
                                        atol=1e-15)
     assert skips == int(TRAIN["nan_skips"]) == 2
+
+
+# ---------------------------------------------------------------------------
+# per-ray batched compositor: oracle/ray_oracle.py against
+# the reference's composite_batch / finite_diff_gradients
+# ---------------------------------------------------------------------------
+BATCH = load("golden_batch.npz")
+BATCH_KEYS = ("weights", "radiance", "residual", "k0", "overdraw", "e_k", "theta0", "t_k")
+
+
+@pytest.mark.parametrize("name", list(MODELS))
+def test_ray_oracle_composite_batch_matches_reference(name):
+    from oracle import ray_oracle as RO
+    m = MODELS[name]
+    out = RO.composite_batch(m.variant, m.param, BATCH["alpha"], BATCH["emission"], BATCH["bg"],
+                             BATCH["valid"])
+    for k in BATCH_KEYS:
+        np.testing.assert_allclose(out[k], BATCH[f"{name}__{k}"], rtol=1e-12, atol=1e-13,
+                                   err_msg=k)
+
+
+def test_ray_oracle_empty_and_finite_differences_match_reference():
+    from oracle import ray_oracle as RO
+    out = RO.composite_batch("linear", 0.0, np.zeros((3, 0)), np.zeros((3, 0, 3)), BATCH["bg"])
+    for k in BATCH_KEYS:
+        np.testing.assert_array_equal(out[k], BATCH[f"empty__{k}"], err_msg=k)
+    for name in ("exponential", "linear", "softplus_20", "blended_0.5"):
+        m = MODELS[name]
+        da, de = RO.finite_diff_gradients(m.variant, m.param, BATCH["fd_alpha"],
+                                          BATCH["fd_emission"], BATCH["bg"], 1e-5, (0.3, 1.0, 0.7))
+        np.testing.assert_allclose(da, BATCH[f"fd__{name}__d_alpha"], rtol=1e-9, atol=1e-10)
+        np.testing.assert_allclose(de, BATCH[f"fd__{name}__d_emission"], rtol=1e-9, atol=1e-10)
