@@ -128,55 +128,110 @@ class DeviceScene:
         import torch
         dev = torch.device("cuda") if device is None else torch.device(device)
 
-        def up(x, shape):
+        def up(x, shape, key):
             if isinstance(x, torch.Tensor):
                 return x.to(device=dev, dtype=torch.float32).reshape(shape)
-            return _h2d_f32(np.asarray(x).reshape(shape), dev)
+            return _h2d_f32(np.asarray(x).reshape(shape), dev, key)
 
         n = len(arrs.opacities)
         sh = arrs.sh
         c = int(np.shape(sh)[2]) if len(np.shape(sh)) == 3 else 1
-        return cls(up(arrs.centers, (n, 3)), up(arrs.scales, (n, 3)), up(arrs.quats, (n, 4)),
-                   up(arrs.opacities, (n,)), up(sh, (n, 3, c)))
+        return cls(up(arrs.centers, (n, 3), "centers"), up(arrs.scales, (n, 3), "scales"),
+                   up(arrs.quats, (n, 4), "quats"), up(arrs.opacities, (n,), "opacities"),
+                   up(sh, (n, 3, c), "sh"))
 
     def __len__(self):
         return self.count
 
 
 # --- host <-> device staging for the numpy API ------------------------------
-# float64 numpy in, float64 numpy out (the reference's types).  Conversions run
-# multi-threaded inside torch into cached page-locked float32 buffers, and the
-# PCIe copies are asynchronous from/to those buffers.
-_PINNED: dict = {}
+# float64 numpy in, float64 numpy out (the reference's types).  Transfers are
+# pipelined in pieces through cached page-locked buffers: the host converts
+# piece k+1 (multi-threaded torch copy) while the DMA engine moves piece k,
+# and downloads convert each piece as soon as its copy event fires.
+_PIECE = 1 << 22  # elements per pipelined piece (measured: 1M pieces cost 2x on downloads)
+_STAGES: dict = {}
 
 
-def _pinned(key, shape, dtype):
+class _Stage:
+    """A cached page-locked buffer and the event of the last copy using it."""
+
+    def __init__(self, n, dtype):
+        import torch
+        self.buf = torch.empty(n, dtype=dtype, pin_memory=True)
+        self.ev = torch.cuda.Event()
+        self.ev.record()
+
+
+def _stage(key, n, dtype) -> _Stage:
+    st = _STAGES.get(key)
+    if st is None or st.buf.numel() < n or st.buf.dtype != dtype:
+        st = _Stage(max(n, 1), dtype)
+        _STAGES[key] = st
+    return st
+
+
+def _h2d_f32(a: np.ndarray, dev, key):
+    """float64 (or float32) numpy array -> new float32 CUDA tensor."""
     import torch
-    t = _PINNED.get(key)
-    if t is None or t.shape != tuple(shape) or t.dtype != dtype:
-        t = torch.empty(tuple(shape), dtype=dtype, pin_memory=True)
-        _PINNED[key] = t
-    return t
+    src = torch.from_numpy(np.ascontiguousarray(a).reshape(-1))
+    n = src.numel()
+    out = torch.empty(n, dtype=torch.float32, device=dev)
+    st = _stage(("h2d", key), n, torch.float32)
+    st.ev.synchronize()  # the previous upload from this buffer has left it
+    for off in range(0, n, _PIECE):
+        end = min(n, off + _PIECE)
+        st.buf[off:end].copy_(src[off:end])
+        out[off:end].copy_(st.buf[off:end], non_blocking=True)
+    st.ev.record(torch.cuda.current_stream(dev))
+    return out.reshape(np.shape(a))
 
 
-def _h2d_f32(a: np.ndarray, dev):
+class _Download:
+    """Device -> host copies queued (in pieces) on the current stream; the
+    float64 / int64 numpy arrays are assembled by :meth:`result`."""
+
+    def __init__(self):
+        self.items = []
+
+    def add(self, t, key):
+        import torch
+        flat = t.reshape(-1)
+        n = flat.numel()
+        st = _stage(("d2h", key), n, t.dtype)
+        stream = torch.cuda.current_stream(t.device)
+        evs = []
+        for off in range(0, n, _PIECE):
+            end = min(n, off + _PIECE)
+            st.buf[off:end].copy_(flat[off:end], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            evs.append((off, end, ev))
+        self.items.append((tuple(t.shape), t.is_floating_point(), st, evs, t))
+
+    def result(self) -> list:
+        import torch
+        outs = []
+        for shape, is_float, st, evs, _ in self.items:
+            out = np.empty(int(np.prod(shape)), dtype=np.float64 if is_float else np.int64)
+            o = torch.from_numpy(out)
+            for off, end, ev in evs:
+                ev.synchronize()
+                o[off:end].copy_(st.buf[off:end])
+            outs.append(out.reshape(shape))
+        self.items = []
+        return outs
+
+
+_SIDE: dict = {}
+
+
+def _side_stream(dev):
     import torch
-    src = torch.from_numpy(np.ascontiguousarray(a))
-    stage = _pinned(("h2d", a.shape), a.shape, torch.float32)
-    torch.cuda.current_stream(dev).synchronize()  # stage may still feed an earlier copy
-    stage.copy_(src)
-    return stage.to(dev, non_blocking=True)
-
-
-def _d2h_f64(t, key) -> np.ndarray:
-    """Fresh float64 numpy array from a device tensor (via pinned float32)."""
-    import torch
-    stage = _pinned(("d2h", key), t.shape, t.dtype)
-    stage.copy_(t, non_blocking=True)
-    torch.cuda.current_stream(t.device).synchronize()
-    out = torch.empty(t.shape, dtype=torch.float64 if t.is_floating_point() else torch.int64)
-    out.copy_(stage)
-    return out.numpy()
+    s = _SIDE.get(dev)
+    if s is None:
+        s = _SIDE[dev] = torch.cuda.Stream(device=dev)
+    return s
 
 
 def _as_device_scene(scene) -> DeviceScene:
@@ -348,8 +403,10 @@ class ForwardCache(Mapping):
 
 
 def _result_to_host(out) -> RenderResult:
-    rgb, od, res = out
-    return RenderResult(_d2h_f64(rgb, "rgb"), _d2h_f64(od, "overdraw"), _d2h_f64(res, "residual"))
+    dl = _Download()
+    for t, k in zip(out, ("rgb", "overdraw", "residual")):
+        dl.add(t, k)
+    return RenderResult(*dl.result())
 
 
 def _settings(camera, model, background, max_splats, alpha_cutoff, near, chunk_size):
@@ -424,19 +481,55 @@ def render_backward(arrs, camera, model, background, cache, seed_image, *,
     if isinstance(seed, torch.Tensor):
         seed_t = seed.to(device=dev.centers.device, dtype=torch.float32).contiguous()
     else:
-        seed_t = _h2d_f32(seed, dev.centers.device)
+        seed_t = _h2d_f32(seed, dev.centers.device, "seed")
     g = backward_device(st.view, dev, seed_t)
-    return {k: _d2h_f64(v, "g_" + k) for k, v in g.items()}
+    dl = _Download()
+    for k, v in g.items():
+        dl.add(v, "g_" + k)
+    return dict(zip(g.keys(), dl.result()))
 
 
 def render_with_gradients(arrs, camera, model, background, seed_image, *,
                           max_splats: int = 128, alpha_cutoff: float = DEFAULT_ALPHA_CUTOFF,
                           near: float = NEAR_PLANE, chunk_size: int | None = None):
-    """Forward render plus parameter gradients (reference render.py:445-464)."""
-    result, cache = render_forward_cached(arrs, camera, model, background,
-                                          max_splats=max_splats, alpha_cutoff=alpha_cutoff,
-                                          near=near, chunk_size=chunk_size)
-    grads = render_backward(arrs, camera, model, background, cache, seed_image,
-                            max_splats=max_splats, alpha_cutoff=alpha_cutoff, near=near,
-                            chunk_size=chunk_size)
-    return result, grads
+    """Forward render plus parameter gradients (reference render.py:445-464).
+
+    One pass over the device: the seed upload is converted on the host while
+    the forward runs, the forward outputs are downloaded on a side stream
+    (and converted) while the backward runs, and the gradients download in
+    pieces converted as they land."""
+    import torch
+    background = np.asarray(background, dtype=np.float64)
+    H, W = int(camera.height), int(camera.width)
+    if isinstance(seed_image, torch.Tensor):
+        seed = seed_image
+    else:
+        seed = np.asarray(seed_image, dtype=np.float64).reshape(H, W, 3)
+    dev = _as_device_scene(arrs)
+    d = dev.centers.device
+    view = _acquire_view()
+    try:
+        out = forward_device(view, dev, camera, model, background, max_splats=max_splats,
+                             alpha_cutoff=alpha_cutoff, near=near, chunk_size=chunk_size)
+        fwd_done = torch.cuda.Event()
+        fwd_done.record(torch.cuda.current_stream(d))
+        if isinstance(seed, torch.Tensor):
+            seed_t = seed.to(device=d, dtype=torch.float32).reshape(H, W, 3).contiguous()
+        else:
+            seed_t = _h2d_f32(seed, d, "seed")
+        grads = backward_device(view, dev, seed_t)
+        side = _side_stream(d)
+        side.wait_event(fwd_done)
+        dl_fwd = _Download()
+        with torch.cuda.stream(side):
+            for t, k in zip(out, ("rgb", "overdraw", "residual")):
+                t.record_stream(side)
+                dl_fwd.add(t, k)
+        dl_g = _Download()
+        for k, v in grads.items():
+            dl_g.add(v, "g_" + k)
+        result = RenderResult(*dl_fwd.result())
+        g = dict(zip(grads.keys(), dl_g.result()))
+    finally:
+        _release_view(view)
+    return result, g
