@@ -8,6 +8,8 @@
 //   K4 back-to-front replay -> moments -> K5 chain    (nxs_backward)
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
 
 #include <algorithm>
 #include <cmath>
@@ -24,8 +26,18 @@ void launch_depth(const float*, const float*, const float*, const float*, int64_
                   cudaStream_t);
 void launch_key32(const double*, int64_t, const unsigned long long*, uint32_t*, cudaStream_t);
 void launch_key_fixup(const uint32_t*, uint32_t*, const double*, int64_t, unsigned long long*,
-                      cudaStream_t);
+                      cudaStream_t, int shift = 0);
 void launch_rank_of(const uint32_t*, int64_t, uint32_t*, cudaStream_t);
+void launch_rank_of_range(const uint32_t*, int64_t, int64_t, uint32_t*, cudaStream_t);
+void launch_key_hist(const uint32_t*, int64_t, unsigned int*, cudaStream_t);
+void launch_phase_select(const unsigned int*, const int64_t*, int, int64_t, long long*,
+                         cudaStream_t);
+void launch_project_ranks(const float*, const float*, const float*, const float*, const float*,
+                          int, int64_t, int64_t, const uint32_t*, const CamDev&, double, double,
+                          int4*, float4*, float4*, unsigned long long*, cudaStream_t);
+void launch_gather_keys(const uint32_t*, const uint32_t*, int64_t, uint32_t*, cudaStream_t);
+void launch_clear_rects(const uint32_t*, int64_t, int64_t, int4*, cudaStream_t);
+void launch_iota(uint32_t*, int64_t, cudaStream_t);
 void launch_chunk_key(const float*, const float*, const float*, const float*, int64_t,
                       const CamDev&, double, const uint32_t*, int, double*, unsigned long long*,
                       uint32_t*, cudaStream_t);
@@ -109,6 +121,15 @@ int bits_for(uint32_t n) {
 }  // namespace
 
 namespace nxs {
+// lazy depth phases: Gaussians whose 32-bit key falls in bins [lo, hi]
+struct BinRange {
+  const uint32_t* key;
+  int lo, hi;
+  __host__ __device__ bool operator()(const uint32_t& i) const {
+    const int b = (int)(key[i] >> 20);
+    return b >= lo && b <= hi;
+  }
+};
 // error reporting for entry points defined in other translation units
 int set_last_error(int code, const char* msg) { return fail(code, msg); }
 }  // namespace nxs
@@ -116,7 +137,7 @@ int set_last_error(int code, const char* msg) { return fail(code, msg); }
 struct nxs_view {
   // per Gaussian
   Buf dkeys_in, dkeys_out, idx_in, idx_out, records, bframe, rects, ntiles, offsets, moments,
-      touched, depth, k32a, k32b, rank_of, rank_c, zlo_rank, seq;
+      touched, depth, k32a, k32b, k32c, rank_of, rank_c, zlo_rank, seq, ph_hist, ph_sel;
   // per pair: sort scratch, and the sorted ranks of each depth phase
   Buf pk_in, pk_out, pv_in, pv_ph[MAX_PHASES];
   // per tile: phase ranges and virtual offsets, activity
@@ -129,7 +150,9 @@ struct nxs_view {
   // phase events: see NXS_PHASES in include/nxs.h
   cudaEvent_t ev[NXS_PHASES + 2] = {};
   // per depth phase: [0] start, [1] after sort+ranges, [2] after the forward kernel
-  cudaEvent_t evp[MAX_PHASES][3] = {};
+  // [0] start, [1] after the phase's depth sort, [2] after its projection
+  // (both lazy phases only), [3] after binning, [4] after the forward blend
+  cudaEvent_t evp[MAX_PHASES][5] = {};
   bool ev_ok = false;
   bool ev_fwd = false, ev_bwd = false;
   // state of the last forward
@@ -144,6 +167,11 @@ struct nxs_view {
   int64_t ph_pairs[MAX_PHASES] = {0, 0, 0, 0};
   int n_phases = 0;
   int n_tiles = 0;
+  // lazy depth phases: ranks [0, sorted_end) are sorted (and, for processed
+  // phases, projected); key bins [0, bin_done] are consumed
+  bool lazy = false;
+  int64_t sorted_end = 0, proj_end = 0;
+  int bin_done = -1;
   const float* scene_centers = nullptr;
   nxs_stats stats{};
 
@@ -151,7 +179,8 @@ struct nxs_view {
   void for_each_buf(F f) {
     Buf* all[] = {&dkeys_in, &dkeys_out, &idx_in,  &idx_out, &records, &bframe, &rects,
                   &ntiles,   &offsets,   &moments, &touched, &pk_in,   &pk_out,  &pv_in,  &active,
-                  &depth,    &k32a,      &k32b,    &rank_of, &rank_c, &zlo_rank, &seq,
+                  &depth,    &k32a,      &k32b,    &k32c,    &rank_of, &rank_c, &zlo_rank, &seq, &ph_hist,
+                  &ph_sel,
                   &c_last,   &c_sat,     &c_tk,    &c_thi,   &c_tlo,   &c_P,    &c_ck,
                   &c_Pck,    &c_ek,      &c_th0,   &r_rad,   &r_trem,  &r_count, &r_sea,
                   &r_sa,     &temp,      &dev_small};
@@ -254,6 +283,59 @@ cudaError_t ensure_n(Buf& b, int64_t n) {
   return b.ensure((size_t)n * sizeof(T));
 }
 
+// Lazy depth phases leave the ranks past the last processed phase unsorted;
+// the exports complete the order (sort + fix-up of the remaining key bins)
+// and mark the unprojected Gaussians' tile rectangles empty.
+int complete_order(nxs_view* v, cudaStream_t s) {
+  if (!v->lazy || v->sorted_end >= v->P) return NXS_OK;
+  const int64_t r0 = v->sorted_end, n = v->P - r0;
+  unsigned long long* dsmall = v->dev_small.as<unsigned long long>();
+  size_t tbs = v->temp.cap;
+  NXS_CUDA(cub::DeviceSelect::If(v->temp.p, tbs, cub::CountingInputIterator<uint32_t>(0),
+                                 v->idx_in.as<uint32_t>(),
+                                 reinterpret_cast<int*>(v->ph_sel.as<long long>() + 48),
+                                 (int)v->P, BinRange{v->k32a.as<uint32_t>(), v->bin_done + 1, 4095},
+                                 s));
+  launch_gather_keys(v->idx_in.as<uint32_t>(), v->k32a.as<uint32_t>(), n, v->k32c.as<uint32_t>(),
+                     s);
+  NXS_LAUNCHED("gather_keys");
+  size_t tb = v->temp.cap;
+  NXS_CUDA(cub::DeviceRadixSort::SortPairs(v->temp.p, tb, v->k32c.as<uint32_t>(),
+                                           v->k32b.as<uint32_t>() + r0, v->idx_in.as<uint32_t>(),
+                                           v->idx_out.as<uint32_t>() + r0, (int)n, 0, 32, s));
+  NXS_CUDA(cudaMemsetAsync(dsmall + 8, 0, sizeof(unsigned long long), s));
+  launch_key_fixup(v->k32b.as<uint32_t>() + r0, v->idx_out.as<uint32_t>() + r0,
+                   v->depth.as<double>(), n, dsmall + 8, s);
+  NXS_LAUNCHED("key_fixup");
+  NXS_CUDA(cudaMemcpyAsync(v->host_small + 6, dsmall + 8, sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, s));
+  NXS_CUDA(cudaStreamSynchronize(s));
+  if (v->host_small[6] != 0) {
+    // a long equal-key run in the tail: the 64-bit sort of everything (its
+    // prefix is the order the processed phases already used)
+    launch_iota(v->idx_in.as<uint32_t>(), v->P, s);
+    NXS_LAUNCHED("iota");
+    size_t tb64 = 0;
+    NXS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb64, v->dkeys_in.as<unsigned long long>(),
+                                             v->dkeys_out.as<unsigned long long>(),
+                                             v->idx_in.as<uint32_t>(), v->idx_out.as<uint32_t>(),
+                                             (int)v->P, 0, 64, s));
+    NXS_CUDA(v->temp.ensure(tb64));
+    tb64 = v->temp.cap;
+    NXS_CUDA(cub::DeviceRadixSort::SortPairs(v->temp.p, tb64, v->dkeys_in.as<unsigned long long>(),
+                                             v->dkeys_out.as<unsigned long long>(),
+                                             v->idx_in.as<uint32_t>(), v->idx_out.as<uint32_t>(),
+                                             (int)v->P, 0, 64, s));
+  }
+  launch_rank_of_range(v->idx_out.as<uint32_t>(), r0, v->P, v->rank_of.as<uint32_t>(), s);
+  NXS_LAUNCHED("rank_of");
+  launch_clear_rects(v->idx_out.as<uint32_t>(), v->proj_end, v->P, v->rects.as<int4>(), s);
+  NXS_LAUNCHED("clear_rects");
+  v->sorted_end = v->P;
+  v->bin_done = 4095;
+  return NXS_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -280,7 +362,7 @@ int nxs_view_create(nxs_view** out) {
   if (!out) return fail(NXS_ERR_INVALID, "null output pointer");
   nxs_view* v = new (std::nothrow) nxs_view();
   if (!v) return fail(NXS_ERR_NOMEM, "host allocation failed");
-  if (cudaHostAlloc((void**)&v->host_small, 8 * sizeof(unsigned long long),
+  if (cudaHostAlloc((void**)&v->host_small, 32 * sizeof(unsigned long long),
                     cudaHostAllocDefault) != cudaSuccess) {
     delete v;
     cudaGetLastError();
@@ -409,9 +491,24 @@ int nxs_forward(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
   }
 
   // depth order: 32-bit monotone keys + exact fix-up of equal-key runs;
-  // the 64-bit sort is the fallback when a run is too long (retry below)
+  // the 64-bit sort is the fallback when a run is too long (retry below).
+  // The global order sorts and projects lazily, one depth phase at a time
+  // (only the phases the image needs); the t-ordered modes, full binning
+  // and the 64-bit fallback sort and project everything up front.
   bool sort64 = false;
+  int64_t Rplan[MAX_PHASES + 1];
+  const int n_ph_plan = n_ph;
+  for (int i = 0; i <= n_ph; ++i) Rplan[i] = R[i];
+  int ph_bin[MAX_PHASES] = {0, 0, 0, 0};  // last key bin of each lazy phase
+  bool phase_full[MAX_PHASES] = {false, false, false, false};  // lazy phase sorted on 32 bits
+  int phase_shift[MAX_PHASES] = {0, 0, 0, 0};
 retry_sort:
+  n_ph = n_ph_plan;
+  for (int i = 0; i <= n_ph; ++i) R[i] = Rplan[i];
+  v->lazy = !torder && !sort64 && !(opts->flags & NXS_FLAG_FULL_BINNING) && P > 0;
+  v->sorted_end = 0;
+  v->proj_end = 0;
+  v->bin_done = -1;
   mark(v, 0, s);
   if (P > 0) {
     size_t tmp_sort = 0, tmp_scan = 0;
@@ -435,6 +532,13 @@ retry_sort:
           v->idx_out.as<uint32_t>(), (int)P, 0, 64, s));
       tmp_sort = std::max(tmp_sort, tmp_chunk);
     }
+    if (v->lazy) {
+      size_t tmp_sel = 0;
+      NXS_CUDA(cub::DeviceSelect::If(nullptr, tmp_sel, cub::CountingInputIterator<uint32_t>(0),
+                                     v->idx_in.as<uint32_t>(), v->ph_sel.as<int>(), (int)P,
+                                     BinRange{nullptr, 0, 0}, s));
+      tmp_sort = std::max(tmp_sort, tmp_sel);
+    }
     NXS_CUDA(v->temp.ensure(std::max(tmp_sort, tmp_scan)));
     // ---- K0 depth (+ min/max) and the stable depth sort
     NXS_CUDA(cudaMemsetAsync(dsmall + 6, 0xff, sizeof(unsigned long long), s));
@@ -449,6 +553,38 @@ retry_sort:
           v->temp.p, tb, v->dkeys_in.as<unsigned long long>(),
           v->dkeys_out.as<unsigned long long>(), v->idx_in.as<uint32_t>(),
           v->idx_out.as<uint32_t>(), (int)P, 0, 64, s));
+    } else if (v->lazy) {
+      // phase boundaries on whole key bins: one host sync for their ranks
+      launch_key32(v->depth.as<double>(), P, dsmall + 6, v->k32a.as<uint32_t>(), s);
+      NXS_LAUNCHED("key32");
+      NXS_CUDA(v->ph_hist.ensure(4096 * sizeof(unsigned int)));
+      NXS_CUDA(v->ph_sel.ensure(64 * sizeof(long long)));
+      launch_key_hist(v->k32a.as<uint32_t>(), P, v->ph_hist.as<unsigned int>(), s);
+      NXS_LAUNCHED("key_hist");
+      int64_t* tgt = reinterpret_cast<int64_t*>(v->host_small + 8);
+      for (int p = 1; p < n_ph; ++p) tgt[p - 1] = R[p];
+      long long* dsel = v->ph_sel.as<long long>();
+      NXS_CUDA(cudaMemcpyAsync(dsel + 32, tgt, sizeof(int64_t) * (n_ph - 1 > 0 ? n_ph - 1 : 1),
+                               cudaMemcpyHostToDevice, s));
+      launch_phase_select(v->ph_hist.as<unsigned int>(), reinterpret_cast<int64_t*>(dsel + 32),
+                          n_ph - 1, P, dsel, s);
+      NXS_LAUNCHED("phase_select");
+      long long* hsel = reinterpret_cast<long long*>(v->host_small + 16);
+      NXS_CUDA(cudaMemcpyAsync(hsel, dsel, sizeof(long long) * 2 * n_ph, cudaMemcpyDeviceToHost,
+                               s));
+      NXS_CUDA(cudaStreamSynchronize(s));
+      // phases = bins (prev, ph_bin]; drop phases that came out empty
+      int m = 0;
+      int64_t last = 0;
+      for (int p = 0; p < n_ph; ++p) {
+        const int64_t end = hsel[2 * p + 1];
+        if (end <= last && m > 0) continue;
+        ph_bin[m] = (int)hsel[2 * p];
+        R[++m] = std::max(end, last);
+        last = R[m];
+      }
+      n_ph = m;
+      R[0] = 0;
     } else {
       launch_key32(v->depth.as<double>(), P, dsmall + 6, v->k32a.as<uint32_t>(), s);
       NXS_LAUNCHED("key32");
@@ -489,11 +625,14 @@ retry_sort:
             32 + bits_for((uint32_t)std::max(n_chunks, 2)), s));
       }
     }
-    launch_rank_of(v->idx_out.as<uint32_t>(), P, v->rank_of.as<uint32_t>(), s);
-    NXS_LAUNCHED("rank_of");
+    if (!v->lazy) {
+      launch_rank_of(v->idx_out.as<uint32_t>(), P, v->rank_of.as<uint32_t>(), s);
+      NXS_LAUNCHED("rank_of");
+      v->sorted_end = v->proj_end = P;
+    }
   }
   mark(v, 1, s);
-  if (P > 0) {
+  if (P > 0 && !v->lazy) {
     // ---- K1 projection (all Gaussians, storage order; records land at their rank)
     if (torder) NXS_CUDA(ensure_n<float>(v->zlo_rank, P));
     launch_project(scene->centers, scene->scales, scene->quats, scene->opacities, scene->sh, C, P,
@@ -514,6 +653,61 @@ retry_sort:
   for (int ph = 0; ph < n_ph; ++ph) {
     const int64_t r0 = R[ph], r1 = R[ph + 1], nr = r1 - r0;
     if (v->ev_ok) cudaEventRecord(v->evp[ph][0], s);
+    if (v->lazy) {
+      if (ph > 0) {
+        // the previous phase's forward decides whether this one is needed
+        NXS_CUDA(cudaMemcpyAsync(v->host_small + 3, n_active, sizeof(unsigned int),
+                                 cudaMemcpyDeviceToHost, s));
+        NXS_CUDA(cudaStreamSynchronize(s));
+        if ((unsigned)v->host_small[3] == 0) break;  // every tile finished
+      }
+      if (nr > 0) {
+        // ---- this phase's Gaussians (key bins (prev, ph_bin]) in storage
+        // order, 32-bit sort + fix-up into ranks [r0, r1), projection
+        const int lo = ph == 0 ? 0 : ph_bin[ph - 1] + 1, hi = ph_bin[ph];
+        size_t tbs = v->temp.cap;
+        NXS_CUDA(cub::DeviceSelect::If(v->temp.p, tbs, cub::CountingInputIterator<uint32_t>(0),
+                                       v->idx_in.as<uint32_t>(),
+                                       reinterpret_cast<int*>(v->ph_sel.as<long long>() + 48),
+                                       (int)P, BinRange{v->k32a.as<uint32_t>(), lo, hi}, s));
+        NXS_CUDA(ensure_n<uint32_t>(v->k32c, P));
+        launch_gather_keys(v->idx_in.as<uint32_t>(), v->k32a.as<uint32_t>(), nr,
+                           v->k32c.as<uint32_t>(), s);
+        NXS_LAUNCHED("gather_keys");
+        // two radix passes over the top 16 significant key bits of the
+        // phase; the fix-up re-sorts equal truncated keys exactly (a run
+        // over 256 redoes the phase on all 32 bits)
+        const int end_bit = std::min(32, 20 + bits_for((uint32_t)hi + 1));
+        const int shift = phase_full[ph] ? 0 : std::max(0, end_bit - 16);
+        size_t tb = v->temp.cap;
+        NXS_CUDA(cub::DeviceRadixSort::SortPairs(v->temp.p, tb, v->k32c.as<uint32_t>(),
+                                                 v->k32b.as<uint32_t>() + r0,
+                                                 v->idx_in.as<uint32_t>(),
+                                                 v->idx_out.as<uint32_t>() + r0, (int)nr, shift,
+                                                 shift ? end_bit : 32, s));
+        launch_key_fixup(v->k32b.as<uint32_t>() + r0, v->idx_out.as<uint32_t>() + r0,
+                         v->depth.as<double>(), nr, dsmall + 8, s, shift);
+        phase_shift[ph] = shift;
+        NXS_LAUNCHED("key_fixup");
+        launch_rank_of_range(v->idx_out.as<uint32_t>(), r0, r1, v->rank_of.as<uint32_t>(), s);
+        NXS_LAUNCHED("rank_of");
+        v->sorted_end = r1;
+        v->bin_done = hi;
+        if (v->ev_ok) cudaEventRecord(v->evp[ph][1], s);
+        launch_project_ranks(scene->centers, scene->scales, scene->quats, scene->opacities,
+                             scene->sh, C, r0, r1, v->idx_out.as<uint32_t>(), cam,
+                             opts->alpha_cutoff, opts->near_plane, v->rects.as<int4>(),
+                             v->records.as<float4>(), v->bframe.as<float4>(), dsmall, s);
+        NXS_LAUNCHED("project_ranks");
+        v->proj_end = r1;
+      } else if (v->ev_ok) {
+        cudaEventRecord(v->evp[ph][1], s);
+      }
+      if (v->ev_ok) cudaEventRecord(v->evp[ph][2], s);
+    } else if (v->ev_ok) {
+      cudaEventRecord(v->evp[ph][1], s);
+      cudaEventRecord(v->evp[ph][2], s);
+    }
     // ---- K2a counts over active tiles, scan, one host sync for the pair count
     if (nr > 0) {
       launch_count_active(v->rects.as<int4>(), v->idx_out.as<uint32_t>(), r0, r1, cam.tiles_x,
@@ -534,11 +728,18 @@ retry_sort:
                              cudaMemcpyDeviceToHost, s));
     NXS_CUDA(cudaMemcpyAsync(v->host_small + 3, n_active, sizeof(unsigned int),
                              cudaMemcpyDeviceToHost, s));
-    if (ph == 0)
+    if (ph == 0 || v->lazy)
       NXS_CUDA(cudaMemcpyAsync(v->host_small + 6, dsmall + 8, sizeof(unsigned long long),
                                cudaMemcpyDeviceToHost, s));
     NXS_CUDA(cudaStreamSynchronize(s));
-    if (ph == 0 && !sort64 && v->host_small[6] != 0) {
+    if (v->lazy && v->host_small[6] != 0 && phase_shift[ph] > 0) {
+      // a long run of equal truncated keys: redo this phase on all 32 bits
+      phase_full[ph] = true;
+      NXS_CUDA(cudaMemsetAsync(dsmall + 8, 0, sizeof(unsigned long long), s));
+      --ph;
+      continue;
+    }
+    if ((ph == 0 || v->lazy) && !sort64 && v->host_small[6] != 0) {
       // an equal-key run longer than the fix-up handles: redo with 64-bit keys
       sort64 = true;
       NXS_CUDA(cudaMemsetAsync(dsmall, 0, 16 * sizeof(unsigned long long), s));
@@ -547,7 +748,7 @@ retry_sort:
     if (ph == 0) mark(v, 3, s);
     const unsigned long long n_pairs = v->host_small[0] + v->host_small[1];
     v->stats.n_straddling = (int64_t)v->host_small[2];
-    if (ph > 0 && (unsigned)v->host_small[3] == 0) break;  // every tile finished
+    if (ph > 0 && !v->lazy && (unsigned)v->host_small[3] == 0) break;  // every tile finished
     if (n_pairs >= (1ull << 31)) return fail(NXS_ERR_NOMEM, "more than 2^31 tile pairs");
     total_pairs += (int64_t)n_pairs;
     v->ph_pairs[ph] = (int64_t)n_pairs;
@@ -587,7 +788,7 @@ retry_sort:
       mark(v, 5, s);
     }
     if (ph == 0) mark(v, 6, s);
-    if (v->ev_ok) cudaEventRecord(v->evp[ph][1], s);
+    if (v->ev_ok) cudaEventRecord(v->evp[ph][3], s);
     if (ph == 1 || (ph == 0 && n_ph > 1)) {
       // forward carry between phases (allocated only when a second phase exists)
       NXS_CUDA(ensure_n<float>(v->r_rad, npix * 3));
@@ -610,7 +811,7 @@ retry_sort:
                   (chunked && !(opts->flags & NXS_FLAG_XBUF32)) ? 16 : 32};
       launch_blend_fwd_x(count, n_tiles, xa, cam, md, v->cache(), v->resume(), cnt, s);
       NXS_LAUNCHED("blend_fwd_x");
-      if (v->ev_ok) cudaEventRecord(v->evp[ph][2], s);
+      if (v->ev_ok) cudaEventRecord(v->evp[ph][4], s);
       ph_done = ph + 1;
       continue;
     }
@@ -623,7 +824,7 @@ retry_sort:
                rgb, overdraw, residual};
     launch_blend_fwd(count, n_tiles, fa, cam, md, v->cache(), v->resume(), cnt, s);
     NXS_LAUNCHED("blend_fwd");
-    if (v->ev_ok) cudaEventRecord(v->evp[ph][2], s);
+    if (v->ev_ok) cudaEventRecord(v->evp[ph][4], s);
     ph_done = ph + 1;
   }
   mark(v, 7, s);
@@ -749,8 +950,10 @@ int nxs_view_timings(nxs_view* v, float* ms, int n) {
     if ((rc = el(v->ev[0], v->ev[1], t[0]))) return rc;  // depth keys + sort
     if ((rc = el(v->ev[1], v->ev[2], t[1]))) return rc;  // projection
     for (int p = 0; p < v->n_phases; ++p) {
-      if ((rc = el(v->evp[p][0], v->evp[p][1], t[2]))) return rc;  // count+scan+sync+emit+sort+ranges
-      if ((rc = el(v->evp[p][1], v->evp[p][2], t[3]))) return rc;  // forward blend (+carry)
+      if ((rc = el(v->evp[p][0], v->evp[p][1], t[0]))) return rc;  // lazy phase: depth sort
+      if ((rc = el(v->evp[p][1], v->evp[p][2], t[1]))) return rc;  // lazy phase: projection
+      if ((rc = el(v->evp[p][2], v->evp[p][3], t[2]))) return rc;  // count+scan+sync+emit+sort+ranges
+      if ((rc = el(v->evp[p][3], v->evp[p][4], t[3]))) return rc;  // forward blend (+carry)
     }
     t[4] = (float)v->n_phases;
   }
@@ -781,6 +984,8 @@ int nxs_depth_order(nxs_view* v, int32_t* order, void* stream_) {
   if (!v || !order) return fail(NXS_ERR_INVALID, "null argument");
   if (!v->have_fwd) return fail(NXS_ERR_STATE, "no forward pass recorded in this view");
   if (v->P == 0) return NXS_OK;
+  int rc;
+  if ((rc = complete_order(v, (cudaStream_t)stream_)) != NXS_OK) return rc;
   NXS_CUDA(cudaMemcpyAsync(order, v->idx_out.p, (size_t)v->P * 4, cudaMemcpyDeviceToDevice,
                            (cudaStream_t)stream_));
   return NXS_OK;
@@ -791,6 +996,8 @@ int nxs_binning_export(nxs_view* v, int32_t* rects, int32_t* ranges, int32_t* pa
   if (!v) return fail(NXS_ERR_INVALID, "null view");
   if (!v->have_fwd) return fail(NXS_ERR_STATE, "no forward pass recorded in this view");
   cudaStream_t s = (cudaStream_t)stream_;
+  int rc;
+  if (v->P && (rc = complete_order(v, s)) != NXS_OK) return rc;
   if (rects && v->P)
     NXS_CUDA(cudaMemcpyAsync(rects, v->rects.p, (size_t)v->P * 16, cudaMemcpyDeviceToDevice, s));
   if (v->n_phases < 1) return NXS_OK;

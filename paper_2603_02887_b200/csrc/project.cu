@@ -214,16 +214,18 @@ __global__ void k_key32(const double* __restrict__ depth, int64_t P,
 // Runs of equal 32-bit keys come out of the stable sort in index order;
 // re-sort each run by (fp64 depth, index) — exactly the 64-bit order.
 // Runs longer than 256 raise `overflow` (the host then redoes the 64-bit sort).
+// With `shift`, the keys were sorted on their bits >= shift only: runs are
+// equal key >> shift, and the same re-sort makes the order exact.
 __global__ void k_key_fixup(const uint32_t* __restrict__ key, uint32_t* __restrict__ idx,
-                            const double* __restrict__ depth, int64_t P,
+                            const double* __restrict__ depth, int64_t P, int shift,
                             unsigned long long* __restrict__ overflow) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P) return;
-  const uint32_t k = key[i];
-  if (i > 0 && key[i - 1] == k) return;         // not a run start
-  if (i + 1 >= P || key[i + 1] != k) return;    // singleton
+  const uint32_t k = key[i] >> shift;
+  if (i > 0 && (key[i - 1] >> shift) == k) return;         // not a run start
+  if (i + 1 >= P || (key[i + 1] >> shift) != k) return;    // singleton
   int64_t e = i + 1;
-  while (e < P && key[e] == k && e - i <= 256) ++e;
+  while (e < P && (key[e] >> shift) == k && e - i <= 256) ++e;
   if (e - i > 256) {
     atomicAdd(overflow, 1ull);
     return;
@@ -246,10 +248,84 @@ __global__ void k_key_fixup(const uint32_t* __restrict__ key, uint32_t* __restri
   }
 }
 
-__global__ void k_rank_of(const uint32_t* __restrict__ order, int64_t P,
+__global__ void k_rank_of(const uint32_t* __restrict__ order, int64_t r0, int64_t r1,
                           uint32_t* __restrict__ rank_of) {
-  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r < P) rank_of[order[r]] = (uint32_t)r;
+  int64_t r = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < r1) rank_of[order[r]] = (uint32_t)r;
+}
+
+// ---- lazy depth phases (global order): only the ranks a phase needs are
+// sorted and projected.  The 32-bit keys are histogrammed by their top 12
+// bits; phase p takes the bins up to the first one whose cumulative count
+// reaches its target rank, so phases are unions of whole key bins (ties
+// never straddle a boundary) and concatenating the phases' sorted ranks is
+// exactly the full order.
+constexpr int PH_BINS = 4096;
+
+__global__ void k_key_hist(const uint32_t* __restrict__ key, int64_t P,
+                           unsigned int* __restrict__ hist) {
+  __shared__ unsigned int sh[PH_BINS];
+  for (int b = threadIdx.x; b < PH_BINS; b += blockDim.x) sh[b] = 0u;
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P;
+       i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&sh[key[i] >> 20], 1u);
+  __syncthreads();
+  for (int b = threadIdx.x; b < PH_BINS; b += blockDim.x)
+    if (sh[b]) atomicAdd(&hist[b], sh[b]);
+}
+
+// one block: inclusive scan of the histogram; for each target rank T_p the
+// first bin whose cumulative count reaches it.  out[2p] = last bin of phase
+// p, out[2p+1] = its end rank; the last phase ends at bin PH_BINS-1, rank P.
+__global__ void __launch_bounds__(1024) k_phase_select(const unsigned int* __restrict__ hist,
+                                                       const int64_t* __restrict__ targets,
+                                                       int n_targets, int64_t P,
+                                                       long long* __restrict__ out) {
+  __shared__ unsigned long long cum[PH_BINS];
+  __shared__ unsigned long long wsum[32];
+  constexpr int PER = PH_BINS / 1024;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  unsigned long long loc[PER], run = 0;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    run += hist[t * PER + k];
+    loc[k] = run;
+  }
+  unsigned long long x = run;
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    unsigned long long v = wsum[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += y;
+    }
+    wsum[lane] = v;
+  }
+  __syncthreads();
+  const unsigned long long base = x - run + (w > 0 ? wsum[w - 1] : 0ull);
+#pragma unroll
+  for (int k = 0; k < PER; ++k) cum[t * PER + k] = base + loc[k];
+  __syncthreads();
+  if (t < n_targets) {
+    const unsigned long long T = (unsigned long long)targets[t];
+    int lo = 0, hi = PH_BINS - 1;  // first bin with cum >= T
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (cum[mid] >= T) hi = mid; else lo = mid + 1;
+    }
+    out[2 * t] = lo;
+    out[2 * t + 1] = (long long)cum[lo];
+  }
+  if (t == 0) {
+    out[2 * n_targets] = PH_BINS - 1;
+    out[2 * n_targets + 1] = P;
+  }
 }
 
 // Chunked order (reference chunk_size = C > 1, render.py:350-358): the
@@ -652,6 +728,66 @@ __global__ void __launch_bounds__(PROJ_CHUNK)
   cp_async_wait<0>();
 }
 
+// K1 for one lazy depth phase: ranks [r0, r1) in rank order (Gaussian
+// g = order[r], parameters gathered), records written as full lines at
+// consecutive ranks.
+__global__ void __launch_bounds__(PROJ_CHUNK)
+    k_project_ranks(const float* __restrict__ centers, const float* __restrict__ scales,
+                    const float* __restrict__ quats, const float* __restrict__ opacities,
+                    const float* __restrict__ sh, int C, int64_t r0, int64_t r1,
+                    const uint32_t* __restrict__ order, CamDev cam, double cutoff,
+                    double near_plane, ProjOut out) {
+  __shared__ ProjOutStage so;
+  const int tid = threadIdx.x, lane = tid & 31, wbase = tid & ~31;
+  const int64_t r = r0 + (int64_t)blockIdx.x * PROJ_CHUNK + tid;
+  if (r < r1) {
+    const int64_t g = order[r];
+    GParams prm;
+    prm.q = reinterpret_cast<const float4*>(quats)[g];
+    prm.c0 = centers[3 * g + 0];
+    prm.c1 = centers[3 * g + 1];
+    prm.c2 = centers[3 * g + 2];
+    prm.s0 = scales[3 * g + 0];
+    prm.s1 = scales[3 * g + 1];
+    prm.s2 = scales[3 * g + 2];
+    prm.op = opacities[g];
+    if (C == 4) {
+      const float4* h = reinterpret_cast<const float4*>(sh + g * 12);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const float4 v = h[c];
+        prm.shv[4 * c] = v.x;
+        prm.shv[4 * c + 1] = v.y;
+        prm.shv[4 * c + 2] = v.z;
+        prm.shv[4 * c + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        prm.shv[4 * c] = sh[g * 3 + c];
+        prm.shv[4 * c + 1] = prm.shv[4 * c + 2] = prm.shv[4 * c + 3] = 0.0f;
+      }
+    }
+    project_one(prm, g, cam, cutoff, near_plane, out, so.rec[tid], so.bf[tid]);
+    so.rank[tid] = r;
+  } else {
+    so.rank[tid] = -1;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < REC_F4; ++i) {
+    const int k = i * 32 + lane, t = wbase + (k >> 3), part = k & 7;
+    const int64_t rr = so.rank[t];
+    if (rr >= 0) out.records[rr * REC_F4 + part] = so.rec[t][part];
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const int k = i * 32 + lane, t = wbase + k / 3, part = k - 3 * (k / 3);
+    const int64_t rr = so.rank[t];
+    if (rr >= 0) out.bframe[rr * 3 + part] = so.bf[t][part];
+  }
+}
+
 // K2a: per rank of [r0, r1), the number of still-active tiles in its rect.
 __global__ void k_count_active(const int4* __restrict__ rects, const uint32_t* __restrict__ order,
                                int64_t r0, int64_t r1, int tiles_x,
@@ -716,9 +852,9 @@ void launch_key32(const double* depth, int64_t P, const unsigned long long* kmin
   k_key32<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(depth, P, kminmax, key);
 }
 void launch_key_fixup(const uint32_t* key, uint32_t* idx, const double* depth, int64_t P,
-                      unsigned long long* overflow, cudaStream_t s) {
+                      unsigned long long* overflow, cudaStream_t s, int shift) {
   if (P == 0) return;
-  k_key_fixup<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(key, idx, depth, P, overflow);
+  k_key_fixup<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(key, idx, depth, P, shift, overflow);
 }
 void launch_chunk_key(const float* centers, const float* scales, const float* quats,
                       const float* opacities, int64_t P, const CamDev& cam, double cutoff,
@@ -746,7 +882,63 @@ bool launch_chunk_sort(const uint32_t* order_c, const double* zlo, int64_t P, in
 }
 void launch_rank_of(const uint32_t* order, int64_t P, uint32_t* rank_of, cudaStream_t s) {
   if (P == 0) return;
-  k_rank_of<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(order, P, rank_of);
+  k_rank_of<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(order, 0, P, rank_of);
+}
+void launch_rank_of_range(const uint32_t* order, int64_t r0, int64_t r1, uint32_t* rank_of,
+                          cudaStream_t s) {
+  if (r1 <= r0) return;
+  k_rank_of<<<(unsigned)((r1 - r0 + 255) / 256), 256, 0, s>>>(order, r0, r1, rank_of);
+}
+__global__ void k_gather_keys(const uint32_t* __restrict__ idx, const uint32_t* __restrict__ key,
+                              int64_t n, uint32_t* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = key[idx[i]];
+}
+__global__ void k_clear_rects(const uint32_t* __restrict__ order, int64_t r0, int64_t r1,
+                              int4* __restrict__ rects) {
+  const int64_t r = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < r1) rects[order[r]] = make_int4(-1, -1, -1, -1);
+}
+__global__ void k_iota(uint32_t* __restrict__ a, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) a[i] = (uint32_t)i;
+}
+void launch_iota(uint32_t* a, int64_t n, cudaStream_t s) {
+  if (n <= 0) return;
+  k_iota<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a, n);
+}
+void launch_gather_keys(const uint32_t* idx, const uint32_t* key, int64_t n, uint32_t* out,
+                        cudaStream_t s) {
+  if (n <= 0) return;
+  k_gather_keys<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(idx, key, n, out);
+}
+void launch_clear_rects(const uint32_t* order, int64_t r0, int64_t r1, int4* rects,
+                        cudaStream_t s) {
+  if (r1 <= r0) return;
+  k_clear_rects<<<(unsigned)((r1 - r0 + 255) / 256), 256, 0, s>>>(order, r0, r1, rects);
+}
+void launch_key_hist(const uint32_t* key, int64_t P, unsigned int* hist, cudaStream_t s) {
+  cudaMemsetAsync(hist, 0, PH_BINS * sizeof(unsigned int), s);
+  if (P == 0) return;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned grid = (unsigned)std::min<int64_t>((P + 1023) / 1024, (int64_t)sms * 2);
+  k_key_hist<<<grid, 1024, 0, s>>>(key, P, hist);
+}
+void launch_phase_select(const unsigned int* hist, const int64_t* targets, int n_targets,
+                         int64_t P, long long* out, cudaStream_t s) {
+  k_phase_select<<<1, 1024, 0, s>>>(hist, targets, n_targets, P, out);
+}
+void launch_project_ranks(const float* centers, const float* scales, const float* quats,
+                          const float* opacities, const float* sh, int C, int64_t r0, int64_t r1,
+                          const uint32_t* order, const CamDev& cam, double cutoff,
+                          double near_plane, int4* rects, float4* records, float4* bframe,
+                          unsigned long long* straddle, cudaStream_t s) {
+  if (r1 <= r0) return;
+  ProjOut o{nullptr, nullptr, rects, records, bframe, straddle};
+  k_project_ranks<<<(unsigned)((r1 - r0 + PROJ_CHUNK - 1) / PROJ_CHUNK), PROJ_CHUNK, 0, s>>>(
+      centers, scales, quats, opacities, sh, C, r0, r1, order, cam, cutoff, near_plane, o);
 }
 
 void launch_project(const float* centers, const float* scales, const float* quats,
