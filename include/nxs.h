@@ -139,8 +139,9 @@ typedef struct nxs_view nxs_view;
 /* 0 depth sort (K0 + radix sort), 1 projection (K1), 2 tile binning over
  * all depth phases (active-tile counts, scan + host sync, pair emission,
  * sort by tile, ranges), 3 forward blend over all phases (K3), 4 number of
- * depth phases run (a count, not ms), 5-6 unused, 7 moment clear,
- * 8 backward blend (K4), 9 chain (K5) */
+ * depth phases run (a count, not ms), 5 device idle time between the end of
+ * the forward and the start of the backward (host sync + caller), 6 the
+ * whole forward, 7 moment clear, 8 backward blend (K4), 9 chain (K5) */
 
 int nxs_abi_version(void);
 const char* nxs_error_string(int code);
@@ -171,6 +172,17 @@ int nxs_forward(nxs_view* view, const nxs_scene* scene, const nxs_camera* camera
 int nxs_backward(nxs_view* view, const nxs_scene* scene, const float* seed,
                  float* g_centers, float* g_scales, float* g_quats,
                  float* g_opacities, float* g_sh, void* stream);
+
+/* Forward + backward in one call (render_with_gradients, render.py:445-464):
+ * nxs_forward then nxs_backward with the same arguments, but the depth-phase
+ * check that ends the forward is overlapped with the backward (the view
+ * speculates on the number of phases its previous call needed and redoes
+ * both passes when more were needed). */
+int nxs_forward_backward(nxs_view* view, const nxs_scene* scene, const nxs_camera* camera,
+                         const nxs_model* model, const nxs_opts* opts, const float background[3],
+                         float* rgb, int32_t* overdraw, float* residual, const float* seed,
+                         float* g_centers, float* g_scales, float* g_quats, float* g_opacities,
+                         float* g_sh, void* stream);
 
 /* Reference cache fields of the last forward (device outputs, any may be
  * NULL): sat (H*W uint8), e_k (H*W*3), t_k (H*W), theta0 (H*W*3). */

@@ -26,6 +26,7 @@ from .render import (
     RenderResult,
     SceneArrays,
     backward_device,
+    forward_backward_device,
     forward_device,
     render,
     render_backward,
@@ -44,6 +45,7 @@ __all__ = [
     "Camera", "GaussianPrimitive", "quat_to_rot",
     "DeviceScene", "RenderResult", "SceneArrays", "render", "render_forward_cached",
     "render_backward", "render_with_gradients", "forward_device", "backward_device",
+    "forward_backward_device",
     "zero_grads_device",
     "TransmittanceModel", "model_from_config", "model_to_config",
     "optim", "AdamState", "bounded_adam_step", "loss", "mse", "psnr", "ssim",

@@ -38,6 +38,7 @@ SYMBOLS = (
     "nxs_view_timings",
     "nxs_forward",
     "nxs_backward",
+    "nxs_forward_backward",
     "nxs_cache_export",
     "nxs_depth_order",
     "nxs_binning_export",
@@ -149,6 +150,9 @@ def lib():
     h.nxs_forward.argtypes = [vp, C.POINTER(Scene), C.POINTER(Camera), C.POINTER(Model),
                               C.POINTER(Opts), C.POINTER(C.c_float), vp, vp, vp, vp]
     h.nxs_backward.argtypes = [vp, C.POINTER(Scene), vp, vp, vp, vp, vp, vp, vp]
+    h.nxs_forward_backward.argtypes = [vp, C.POINTER(Scene), C.POINTER(Camera), C.POINTER(Model),
+                                       C.POINTER(Opts), C.POINTER(C.c_float), vp, vp, vp, vp,
+                                       vp, vp, vp, vp, vp, vp]
     h.nxs_cache_export.argtypes = [vp, vp, vp, vp, vp, vp]
     h.nxs_depth_order.argtypes = [vp, vp, vp]
     h.nxs_binning_export.argtypes = [vp, vp, vp, vp, vp]
@@ -247,6 +251,16 @@ class View:
                                     _ptr(grads["opacities"]), _ptr(grads["sh"]),
                                     _stream_ptr(stream)))
 
+    def forward_backward(self, dev, cam: Camera, model: Model, opts: Opts, bg, rgb, overdraw,
+                         residual, seed, grads, stream=None):
+        sc = self.scene_struct(dev)
+        bgc = (C.c_float * 3)(*[float(x) for x in bg])
+        _check(self._h.nxs_forward_backward(
+            self._p, C.byref(sc), C.byref(cam), C.byref(model), C.byref(opts), bgc, _ptr(rgb),
+            _ptr(overdraw), _ptr(residual), _ptr(seed), _ptr(grads["centers"]),
+            _ptr(grads["scales"]), _ptr(grads["quats"]), _ptr(grads["opacities"]),
+            _ptr(grads["sh"]), _stream_ptr(stream)))
+
     def cache_export(self, sat=None, e_k=None, t_k=None, theta0=None, stream=None):
         _check(self._h.nxs_cache_export(self._p, _ptr(sat), _ptr(e_k), _ptr(t_k), _ptr(theta0),
                                         _stream_ptr(stream)))
@@ -266,8 +280,8 @@ class View:
         _check(self._h.nxs_view_stats(self._p, C.byref(st)))
         return st.as_dict()
 
-    PHASES = ("depth_sort", "project", "binning", "blend_fwd", "n_depth_phases", "_5", "_6",
-              "moment_clear", "blend_bwd", "chain")
+    PHASES = ("depth_sort", "project", "binning", "blend_fwd", "n_depth_phases",
+              "fwd_bwd_gap", "forward_total", "moment_clear", "blend_bwd", "chain")
 
     def timings(self) -> dict:
         """Device milliseconds per phase of the last forward/backward."""

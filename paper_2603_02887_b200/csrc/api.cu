@@ -155,6 +155,7 @@ struct nxs_view {
   cudaEvent_t evp[MAX_PHASES][5] = {};
   bool ev_ok = false;
   bool ev_fwd = false, ev_bwd = false;
+  cudaEvent_t ev_sync = nullptr;  // host-side polling for the in-pipeline syncs
   // state of the last forward
   bool have_fwd = false;
   CamDev cam{};
@@ -170,6 +171,11 @@ struct nxs_view {
   // lazy depth phases: ranks [0, sorted_end) are sorted (and, for processed
   // phases, projected); key bins [0, bin_done] are consumed
   bool lazy = false;
+  // speculative fused forward+backward: the forward stopped before checking
+  // whether depth phase `spec_phase` is needed (the previous call of this
+  // view needed `phases_needed` phases)
+  bool spec_pending = false;
+  int phases_needed = 0;
   int64_t sorted_end = 0, proj_end = 0;
   int bin_done = -1;
   const float* scene_centers = nullptr;
@@ -194,6 +200,7 @@ struct nxs_view {
   ~nxs_view() {
     for_each_buf([](Buf& b) { b.release(); });
     if (host_small) cudaFreeHost(host_small);
+    if (ev_sync) cudaEventDestroy(ev_sync);
     if (ev_ok) {
       for (auto& e : ev) cudaEventDestroy(e);
       for (auto& row : evp)
@@ -274,6 +281,19 @@ int make_camera(const nxs_camera* c, CamDev& cd) {
   return NXS_OK;
 }
 
+// Wait for the stream by polling an event: the syncs inside the pipeline
+// (pair counts, phase sizes) sit between kernels, and a blocking wait's
+// wake-up latency would leave the GPU idle; fall back to blocking if no
+// event could be created.
+cudaError_t spin_sync(nxs_view* v, cudaStream_t s) {
+  if (!v->ev_sync) return cudaStreamSynchronize(s);
+  cudaError_t e = cudaEventRecord(v->ev_sync, s);
+  if (e != cudaSuccess) return e;
+  while ((e = cudaEventQuery(v->ev_sync)) == cudaErrorNotReady) {
+  }
+  return e;
+}
+
 inline void mark(nxs_view* v, int i, cudaStream_t s) {
   if (v->ev_ok) cudaEventRecord(v->ev[i], s);
 }
@@ -309,7 +329,7 @@ int complete_order(nxs_view* v, cudaStream_t s) {
   NXS_LAUNCHED("key_fixup");
   NXS_CUDA(cudaMemcpyAsync(v->host_small + 6, dsmall + 8, sizeof(unsigned long long),
                            cudaMemcpyDeviceToHost, s));
-  NXS_CUDA(cudaStreamSynchronize(s));
+  NXS_CUDA(spin_sync(v, s));
   if (v->host_small[6] != 0) {
     // a long equal-key run in the tail: the 64-bit sort of everything (its
     // prefix is the order the processed phases already used)
@@ -372,6 +392,8 @@ int nxs_view_create(nxs_view** out) {
   for (auto& e : v->ev) v->ev_ok = v->ev_ok && cudaEventCreate(&e) == cudaSuccess;
   for (auto& row : v->evp)
     for (auto& e : row) v->ev_ok = v->ev_ok && cudaEventCreate(&e) == cudaSuccess;
+  if (cudaEventCreateWithFlags(&v->ev_sync, cudaEventDisableTiming) != cudaSuccess)
+    v->ev_sync = nullptr;
   *out = v;
   return NXS_OK;
 }
@@ -391,14 +413,31 @@ int64_t nxs_view_bytes(const nxs_view* view) {
   return view ? const_cast<nxs_view*>(view)->bytes() : 0;
 }
 
+namespace {
+int forward_impl(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
+                 const nxs_model* model, const nxs_opts* opts, const float background[3],
+                 float* rgb, int32_t* overdraw, float* residual, void* stream_, int spec_phase);
+}
+
 int nxs_forward(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
                 const nxs_model* model, const nxs_opts* opts, const float background[3],
                 float* rgb, int32_t* overdraw, float* residual, void* stream_) {
+  return forward_impl(v, scene, camera, model, opts, background, rgb, overdraw, residual, stream_,
+                      0);
+}
+
+}  // extern "C"
+
+namespace {
+int forward_impl(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
+                 const nxs_model* model, const nxs_opts* opts, const float background[3],
+                 float* rgb, int32_t* overdraw, float* residual, void* stream_, int spec_phase) {
   if (!v || !scene || !camera || !model || !opts || !background || !rgb || !overdraw ||
       !residual)
     return fail(NXS_ERR_INVALID, "null argument");
   cudaStream_t s = (cudaStream_t)stream_;
   v->have_fwd = false;
+  v->spec_pending = false;
   CamDev cam;
   ModelDev md;
   int rc;
@@ -572,7 +611,7 @@ retry_sort:
       long long* hsel = reinterpret_cast<long long*>(v->host_small + 16);
       NXS_CUDA(cudaMemcpyAsync(hsel, dsel, sizeof(long long) * 2 * n_ph, cudaMemcpyDeviceToHost,
                                s));
-      NXS_CUDA(cudaStreamSynchronize(s));
+      NXS_CUDA(spin_sync(v, s));
       // phases = bins (prev, ph_bin]; drop phases that came out empty
       int m = 0;
       int64_t last = 0;
@@ -654,12 +693,20 @@ retry_sort:
     const int64_t r0 = R[ph], r1 = R[ph + 1], nr = r1 - r0;
     if (v->ev_ok) cudaEventRecord(v->evp[ph][0], s);
     if (v->lazy) {
+      if (ph > 0 && ph == spec_phase) {
+        // fused call: the backward goes ahead and the check overlaps it
+        v->spec_pending = true;
+        break;
+      }
       if (ph > 0) {
         // the previous phase's forward decides whether this one is needed
         NXS_CUDA(cudaMemcpyAsync(v->host_small + 3, n_active, sizeof(unsigned int),
                                  cudaMemcpyDeviceToHost, s));
-        NXS_CUDA(cudaStreamSynchronize(s));
-        if ((unsigned)v->host_small[3] == 0) break;  // every tile finished
+        NXS_CUDA(spin_sync(v, s));
+        if ((unsigned)v->host_small[3] == 0) {  // every tile finished
+          v->phases_needed = ph;
+          break;
+        }
       }
       if (nr > 0) {
         // ---- this phase's Gaussians (key bins (prev, ph_bin]) in storage
@@ -731,7 +778,7 @@ retry_sort:
     if (ph == 0 || v->lazy)
       NXS_CUDA(cudaMemcpyAsync(v->host_small + 6, dsmall + 8, sizeof(unsigned long long),
                                cudaMemcpyDeviceToHost, s));
-    NXS_CUDA(cudaStreamSynchronize(s));
+    NXS_CUDA(spin_sync(v, s));
     if (v->lazy && v->host_small[6] != 0 && phase_shift[ph] > 0) {
       // a long run of equal truncated keys: redo this phase on all 32 bits
       phase_full[ph] = true;
@@ -835,7 +882,7 @@ retry_sort:
     // pending-buffer overflow means the exact order was not guaranteed: report
     NXS_CUDA(cudaMemcpyAsync(v->host_small + 7, dsmall + 9, sizeof(unsigned long long),
                              cudaMemcpyDeviceToHost, s));
-    NXS_CUDA(cudaStreamSynchronize(s));
+    NXS_CUDA(spin_sync(v, s));
     v->stats.n_overflow = (int64_t)v->host_small[7];
     if (v->host_small[7] > 0 && chunked && !(opts->flags & NXS_FLAG_XBUF32)) {
       // the small pending buffer overflowed: redo the pass with the large one
@@ -852,7 +899,7 @@ retry_sort:
   if (count) {
     NXS_CUDA(cudaMemcpyAsync(v->host_small + 4, cnt, 2 * sizeof(unsigned long long),
                              cudaMemcpyDeviceToHost, s));
-    NXS_CUDA(cudaStreamSynchronize(s));
+    NXS_CUDA(spin_sync(v, s));
     v->stats.n_tests_fwd = (int64_t)v->host_small[4];
     v->stats.n_composited = (int64_t)v->host_small[5];
   }
@@ -868,20 +915,13 @@ retry_sort:
   v->n_phases = ph_done;
   v->n_tiles = n_tiles;
   v->scene_centers = scene->centers;
+  if (!v->spec_pending) v->phases_needed = ph_done;
   return NXS_OK;
 }
 
-int nxs_backward(nxs_view* v, const nxs_scene* scene, const float* seed, float* g_centers,
-                 float* g_scales, float* g_quats, float* g_opacities, float* g_sh, void* stream_) {
-  if (!v || !scene || !seed) return fail(NXS_ERR_INVALID, "null argument");
-  if (!v->have_fwd) return fail(NXS_ERR_STATE, "no forward pass recorded in this view");
-  if (scene->count != v->P || scene->sh_coeffs != v->C)
-    return fail(NXS_ERR_STATE, "scene differs from the forward call");
-  if (v->P > 0 && (!g_centers || !g_scales || !g_quats || !g_opacities || !g_sh))
-    return fail(NXS_ERR_INVALID, "null gradient buffer");
-  cudaStream_t s = (cudaStream_t)stream_;
+// backward blend (K4/K4x) into the per-rank moments; the chain follows
+int backward_blend(nxs_view* v, const float* seed, cudaStream_t s) {
   const int64_t P = v->P;
-  if (P == 0) return NXS_OK;
   mark(v, 8, s);
   {
     // moments/touched stay zero between backwards (K5 re-zeroes what it
@@ -918,20 +958,102 @@ int nxs_backward(nxs_view* v, const nxs_scene* scene, const float* seed, float* 
   }
   NXS_LAUNCHED("blend_bwd");
   mark(v, 10, s);
-  launch_chain(scene->scales, scene->quats, v->C, P, v->idx_out.as<uint32_t>(),
+  return NXS_OK;
+}
+
+// K5: moments -> gradients (null gradients: only clear the moments)
+int backward_chain(nxs_view* v, const nxs_scene* scene, float* g_centers, float* g_scales,
+                   float* g_quats, float* g_opacities, float* g_sh, cudaStream_t s) {
+  launch_chain(scene->scales, scene->quats, v->C, v->P, v->idx_out.as<uint32_t>(),
                v->moments.as<double>(), v->touched.as<uint8_t>(), g_centers, g_scales, g_quats,
                g_opacities, g_sh, s);
   NXS_LAUNCHED("chain");
+  if (!g_centers) return NXS_OK;
   mark(v, 11, s);
   v->ev_bwd = true;
+  const bool count = (v->opts.flags & NXS_FLAG_COUNT_EVENTS) != 0;
+  unsigned long long* dsmall = v->dev_small.as<unsigned long long>();
+  Counters* cnt = reinterpret_cast<Counters*>(dsmall + 1);
   if (count) {
     NXS_CUDA(cudaMemcpyAsync(v->host_small + 5, &cnt->tests_bwd, 2 * sizeof(unsigned long long),
                              cudaMemcpyDeviceToHost, s));
-    NXS_CUDA(cudaStreamSynchronize(s));
+    NXS_CUDA(spin_sync(v, s));
     v->stats.n_tests_bwd = (int64_t)v->host_small[5];
     v->stats.n_entries_bwd = (int64_t)v->host_small[6];
   }
   return NXS_OK;
+}
+
+int check_backward_args(nxs_view* v, const nxs_scene* scene, const float* seed, float* g_centers,
+                        float* g_scales, float* g_quats, float* g_opacities, float* g_sh) {
+  if (!v || !scene || !seed) return fail(NXS_ERR_INVALID, "null argument");
+  if (v->P > 0 && (!g_centers || !g_scales || !g_quats || !g_opacities || !g_sh))
+    return fail(NXS_ERR_INVALID, "null gradient buffer");
+  return NXS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int nxs_backward(nxs_view* v, const nxs_scene* scene, const float* seed, float* g_centers,
+                 float* g_scales, float* g_quats, float* g_opacities, float* g_sh, void* stream_) {
+  int rc;
+  if ((rc = check_backward_args(v, scene, seed, g_centers, g_scales, g_quats, g_opacities, g_sh)))
+    return rc;
+  if (!v->have_fwd) return fail(NXS_ERR_STATE, "no forward pass recorded in this view");
+  if (scene->count != v->P || scene->sh_coeffs != v->C)
+    return fail(NXS_ERR_STATE, "scene differs from the forward call");
+  if (v->spec_pending) return fail(NXS_ERR_STATE, "internal: unresolved speculative forward");
+  cudaStream_t s = (cudaStream_t)stream_;
+  if (v->P == 0) return NXS_OK;
+  if ((rc = backward_blend(v, seed, s))) return rc;
+  return backward_chain(v, scene, g_centers, g_scales, g_quats, g_opacities, g_sh, s);
+}
+
+int nxs_forward_backward(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
+                         const nxs_model* model, const nxs_opts* opts, const float background[3],
+                         float* rgb, int32_t* overdraw, float* residual, const float* seed,
+                         float* g_centers, float* g_scales, float* g_quats, float* g_opacities,
+                         float* g_sh, void* stream_) {
+  int rc;
+  if ((rc = check_backward_args(v, scene, seed, g_centers, g_scales, g_quats, g_opacities, g_sh)))
+    return rc;
+  cudaStream_t s = (cudaStream_t)stream_;
+  // speculate that this view needs as many depth phases as its last call
+  const int spec = (v->ev_sync && v->phases_needed > 0) ? v->phases_needed : 0;
+  if ((rc = forward_impl(v, scene, camera, model, opts, background, rgb, overdraw, residual,
+                         stream_, spec)))
+    return rc;
+  if (v->P == 0) return NXS_OK;
+  const bool spec_check = v->spec_pending;
+  if (spec_check) {
+    // the active-tile count of the last forward kernel, read back right
+    // behind it; the host waits for the forward only, not for the backward
+    unsigned int* n_active = reinterpret_cast<unsigned int*>(v->dev_small.as<unsigned long long>() + 5);
+    NXS_CUDA(cudaMemcpyAsync(v->host_small + 3, n_active, sizeof(unsigned int),
+                             cudaMemcpyDeviceToHost, s));
+    NXS_CUDA(cudaEventRecord(v->ev_sync, s));
+  }
+  if ((rc = backward_blend(v, seed, s))) return rc;
+  if (spec_check) {
+    cudaError_t e;
+    while ((e = cudaEventQuery(v->ev_sync)) == cudaErrorNotReady) {
+    }
+    NXS_CUDA(e);
+    v->spec_pending = false;
+    if ((unsigned)v->host_small[3] != 0) {
+      // more depth phases were needed: drop the moments, redo both passes
+      if ((rc = backward_chain(v, scene, nullptr, nullptr, nullptr, nullptr, nullptr, s)))
+        return rc;
+      v->phases_needed = 0;
+      if ((rc = forward_impl(v, scene, camera, model, opts, background, rgb, overdraw, residual,
+                             stream_, 0)))
+        return rc;
+      if ((rc = backward_blend(v, seed, s))) return rc;
+    }
+  }
+  return backward_chain(v, scene, g_centers, g_scales, g_quats, g_opacities, g_sh, s);
 }
 
 int nxs_view_timings(nxs_view* v, float* ms, int n) {
@@ -957,6 +1079,8 @@ int nxs_view_timings(nxs_view* v, float* ms, int n) {
     }
     t[4] = (float)v->n_phases;
   }
+  if (v->ev_fwd && (rc = el(v->ev[0], v->ev[7], t[6]))) return rc;  // whole forward
+  if (v->ev_fwd && v->ev_bwd && (rc = el(v->ev[7], v->ev[8], t[5]))) return rc;  // gap
   if (v->ev_bwd) {
     if ((rc = el(v->ev[8], v->ev[9], t[7]))) return rc;
     if ((rc = el(v->ev[9], v->ev[10], t[8]))) return rc;

@@ -36,6 +36,7 @@ __global__ void k_chain(const float* __restrict__ scales, const float* __restric
     mm[k] = 0.0;
   }
   touched[r] = 0;
+  if (!g_centers) return;  // clear only (a discarded speculative backward)
   const int64_t g = order[r];
 
   // opacity and SH need no geometry

@@ -84,16 +84,19 @@ def device_view_renderer(dev_scene, model, background, cameras, seeds, *, chunk_
     ``cameras[v]`` / ``seeds[v]`` (H,W,3 float32 CUDA) for view v; each view
     index gets its own persistent ``nxs_view`` workspace."""
     from . import _native
-    from .render import backward_device, forward_device
+    from .render import forward_backward_device
     views = {} if views is None else views
+    outs = {}
 
     def render_view(v, grads):
         if v not in views:
             views[v] = _native.View()
-        cam = cameras[v]
-        forward_device(views[v], dev_scene, cam, model, background, chunk_size=chunk_size,
-                       max_splats=max_splats, first_phase_ranks=first_phase_ranks)
-        backward_device(views[v], dev_scene, seeds[v], grads.fields)
+        # fused forward + backward; the output images are reused per view
+        o, _ = forward_backward_device(views[v], dev_scene, cameras[v], model, background,
+                                       seeds[v], grads.fields, chunk_size=chunk_size,
+                                       max_splats=max_splats,
+                                       first_phase_ranks=first_phase_ranks, out=outs.get(v))
+        outs[v] = o
 
     render_view.views = views
     return render_view

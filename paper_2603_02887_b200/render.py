@@ -266,12 +266,8 @@ def _model_struct(model):
     return m, _native.make_model(VARIANT_IDS[m.variant], m.param)
 
 
-def forward_device(view, dev: DeviceScene, camera, model, background, *, max_splats=128,
-                   alpha_cutoff=DEFAULT_ALPHA_CUTOFF, near=NEAR_PLANE, chunk_size=1,
-                   count_events=False, full_binning=False, first_phase_ranks=0, out=None,
-                   stream=None):
-    """Forward render on the device; returns (rgb (H,W,3), overdraw (H,W)
-    int32, residual (H,W)) float32 CUDA tensors."""
+def _forward_args(dev, camera, model, background, max_splats, alpha_cutoff, near, chunk_size,
+                  count_events, full_binning, first_phase_ranks, out):
     import torch
     chunk = _effective_chunk(chunk_size, dev.count)
     _check_mode(chunk)
@@ -286,18 +282,53 @@ def forward_device(view, dev: DeviceScene, camera, model, background, *, max_spl
     flags = (_native.NXS_FLAG_COUNT_EVENTS if count_events else 0) | \
         (_native.NXS_FLAG_FULL_BINNING if full_binning else 0)
     opts = _native.make_opts(max_splats, alpha_cutoff, near, chunk, flags, first_phase_ranks)
+    return _native.make_camera(camera), ms, opts, bg, out
+
+
+def _raise_mapped(e):
+    if e.code == _native.NXS_ERR_OVERFLOW:
+        raise RuntimeError(f"{e} (exact order could not be guaranteed)") from e
+    if e.code == _native.NXS_ERR_GEOMETRY:
+        raise NotImplementedError(str(e)) from e
+    if e.code == _native.NXS_ERR_INVALID:
+        raise ValueError(str(e)) from e
+    raise e
+
+
+def forward_device(view, dev: DeviceScene, camera, model, background, *, max_splats=128,
+                   alpha_cutoff=DEFAULT_ALPHA_CUTOFF, near=NEAR_PLANE, chunk_size=1,
+                   count_events=False, full_binning=False, first_phase_ranks=0, out=None,
+                   stream=None):
+    """Forward render on the device; returns (rgb (H,W,3), overdraw (H,W)
+    int32, residual (H,W)) float32 CUDA tensors."""
+    cam, ms, opts, bg, out = _forward_args(dev, camera, model, background, max_splats,
+                                           alpha_cutoff, near, chunk_size, count_events,
+                                           full_binning, first_phase_ranks, out)
     try:
-        view.forward(dev, _native.make_camera(camera), ms, opts, bg, out[0], out[1], out[2],
-                     stream=stream)
+        view.forward(dev, cam, ms, opts, bg, out[0], out[1], out[2], stream=stream)
     except _native.NxsError as e:
-        if e.code == _native.NXS_ERR_OVERFLOW:
-            raise RuntimeError(f"{e} (exact order could not be guaranteed)") from e
-        if e.code == _native.NXS_ERR_GEOMETRY:
-            raise NotImplementedError(str(e)) from e
-        if e.code == _native.NXS_ERR_INVALID:
-            raise ValueError(str(e)) from e
-        raise
+        _raise_mapped(e)
     return out
+
+
+def forward_backward_device(view, dev: DeviceScene, camera, model, background, seed, grads=None,
+                            *, max_splats=128, alpha_cutoff=DEFAULT_ALPHA_CUTOFF,
+                            near=NEAR_PLANE, chunk_size=1, count_events=False,
+                            full_binning=False, first_phase_ranks=0, out=None, stream=None):
+    """Forward render plus gradient accumulation for ``seed`` in one library
+    call (``nxs_forward_backward``: the end-of-forward depth-phase check
+    overlaps the backward).  Returns ((rgb, overdraw, residual), grads)."""
+    cam, ms, opts, bg, out = _forward_args(dev, camera, model, background, max_splats,
+                                           alpha_cutoff, near, chunk_size, count_events,
+                                           full_binning, first_phase_ranks, out)
+    if grads is None:
+        grads = zero_grads_device(dev)
+    try:
+        view.forward_backward(dev, cam, ms, opts, bg, out[0], out[1], out[2], seed.contiguous(),
+                              grads, stream=stream)
+    except _native.NxsError as e:
+        _raise_mapped(e)
+    return out, grads
 
 
 def zero_grads_device(dev: DeviceScene) -> dict:
@@ -494,10 +525,8 @@ def render_with_gradients(arrs, camera, model, background, seed_image, *,
                           near: float = NEAR_PLANE, chunk_size: int | None = None):
     """Forward render plus parameter gradients (reference render.py:445-464).
 
-    One pass over the device: the seed upload is converted on the host while
-    the forward runs, the forward outputs are downloaded on a side stream
-    (and converted) while the backward runs, and the gradients download in
-    pieces converted as they land."""
+    One fused library call (forward + backward); all results then download
+    in pieces that are converted to float64 as they land."""
     import torch
     background = np.asarray(background, dtype=np.float64)
     H, W = int(camera.height), int(camera.width)
@@ -509,27 +538,21 @@ def render_with_gradients(arrs, camera, model, background, seed_image, *,
     d = dev.centers.device
     view = _acquire_view()
     try:
-        out = forward_device(view, dev, camera, model, background, max_splats=max_splats,
-                             alpha_cutoff=alpha_cutoff, near=near, chunk_size=chunk_size)
-        fwd_done = torch.cuda.Event()
-        fwd_done.record(torch.cuda.current_stream(d))
         if isinstance(seed, torch.Tensor):
             seed_t = seed.to(device=d, dtype=torch.float32).reshape(H, W, 3).contiguous()
         else:
             seed_t = _h2d_f32(seed, d, "seed")
-        grads = backward_device(view, dev, seed_t)
-        side = _side_stream(d)
-        side.wait_event(fwd_done)
-        dl_fwd = _Download()
-        with torch.cuda.stream(side):
-            for t, k in zip(out, ("rgb", "overdraw", "residual")):
-                t.record_stream(side)
-                dl_fwd.add(t, k)
-        dl_g = _Download()
+        out, grads = forward_backward_device(view, dev, camera, model, background, seed_t,
+                                             max_splats=max_splats, alpha_cutoff=alpha_cutoff,
+                                             near=near, chunk_size=chunk_size)
+        dl = _Download()
+        for t, k in zip(out, ("rgb", "overdraw", "residual")):
+            dl.add(t, k)
         for k, v in grads.items():
-            dl_g.add(v, "g_" + k)
-        result = RenderResult(*dl_fwd.result())
-        g = dict(zip(grads.keys(), dl_g.result()))
+            dl.add(v, "g_" + k)
+        res = dl.result()
+        result = RenderResult(*res[:3])
+        g = dict(zip(grads.keys(), res[3:]))
     finally:
         _release_view(view)
     return result, g

@@ -587,3 +587,29 @@ def test_chunked_c2_sampled_pixels_match_oracle(name, cs):
     assert keep.sum() >= 0.8 * len(px), int(keep.sum())
     strict, massf, total = grad_report(got["grads"], g_ref, mass)
     assert massf == 0, (strict, massf, total)
+
+
+def test_fused_forward_backward_matches_separate_calls():
+    """nxs_forward_backward == nxs_forward + nxs_backward, including a view
+    whose depth-phase speculation fails (a saturating model first, then the
+    exponential model that needs every phase)."""
+    import torch
+    from paper_2603_02887_b200 import (_native, backward_device, forward_backward_device,
+                                       forward_device)
+    sc = O.round_scene_f32(O.canonical_scene(60_000, seed=1))
+    cam = O.canonical_camera(320, 240, 1, 8)
+    seed = torch.as_tensor(O.canonical_seed(320, 240, 1), dtype=torch.float32).cuda()
+    dev = _dev(sc)
+    fused = _native.View()
+    for name in ("softplus_20", "softplus_20", "exponential", "exponential", "softplus_20"):
+        model = MODELS[name]
+        ref_view = _native.View()
+        r_out = forward_device(ref_view, dev, cam, model, np.zeros(3), first_phase_ranks=4096)
+        r_g = backward_device(ref_view, dev, seed)
+        f_out, f_g = forward_backward_device(fused, dev, cam, model, np.zeros(3), seed,
+                                             first_phase_ranks=4096)
+        for a, b in zip(r_out, f_out):
+            assert torch.equal(a, b), name
+        for k in GRAD_FIELDS:
+            np.testing.assert_allclose(f_g[k].cpu().numpy(), r_g[k].cpu().numpy(), rtol=1e-5,
+                                       atol=1e-7 * float(r_g[k].abs().max()), err_msg=k)
