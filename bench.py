@@ -346,7 +346,7 @@ def roofline(a, model, phase, st):
     shares = {"blend (fwd+bwd)": blend_ms, "binning": phase.get("binning", 0.0),
               "depth_sort": phase.get("depth_sort", 0.0), "project": phase.get("project", 0.0)}
     dom = max(shares, key=shares.get)
-    total = sum(phase.values())
+    total = sum(x for k, x in phase.items() if k not in ("forward_total", "fwd_bwd_gap"))
     if dom == "blend (fwd+bwd)":
         r = dict(blend, kernel=dom)
     elif dom == "binning":
@@ -362,6 +362,20 @@ def roofline(a, model, phase, st):
     r["achieved"] = round(r["achieved"], 3)
     r["frac"] = round(r["achieved"] / r["peak"], 4) if r["peak"] else None
     r["traffic"] = None
+    # DRAM bytes and FP32-pipe utilisation of the blend kernels from the
+    # committed ncu capture of this workload (profiles/r01_blend_traffic.json)
+    try:
+        cap = json.loads((ROOT / "profiles" / "r01_blend_traffic.json").read_text())
+        k = cap["per_step"]
+        if dom == "blend (fwd+bwd)" and model.variant == "softplus" and a.chunk_size == 1 \
+                and a.gaussians == 1_000_000 and (a.width, a.height) == (1920, 1080):
+            r["traffic"] = sum(v["dram_read_bytes"] + v["dram_write_bytes"] for v in k.values())
+            r["traffic_unit"] = "bytes per step (fwd + bwd launches)"
+            r["ncu_fma_pipe_pct"] = {n: v["fma_pipe_pct"] for n, v in k.items()}
+            r["ncu_issue_active_pct"] = {n: v["issue_active_pct"] for n, v in k.items()}
+            r["ncu_source"] = "profiles/r01_blend_traffic.json"
+    except Exception:
+        pass
     r["share_of_step"] = round(shares[dom] / total, 3) if total else None
     r["blend_fp32"] = {"achieved_tflops": round(blend["achieved"], 3),
                        "frac_of_derived_peak": round(blend["achieved"] / fp32_peak, 4),
