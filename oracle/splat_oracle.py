@@ -559,10 +559,17 @@ def _backward_batch(scene, cam, model, bg, out, st, seed, grads, mass):
     grads["quats"][ids] += t_q.sum(1)
     grads["sh"][ids] += t_sh.sum(1)
     if mass is not None:
+        # parity scale of each gradient entry: Σ over pixels of the term's
+        # magnitude.  The geometric groups use the norm of the per-pixel
+        # term VECTOR (normwise): a component that is small next to its
+        # siblings (e.g. the thin-axis scale of a needle, or the ray-ward
+        # centre component) is only defined to fp32 precision of the whole
+        # per-pixel vector, which any fp32 evaluation of the peak offset
+        # inherits
         mass["opacities"][ids] += np.abs(t_op).sum(1)
-        mass["centers"][ids] += np.abs(t_c).sum(1)
-        mass["scales"][ids] += np.abs(t_s).sum(1)
-        mass["quats"][ids] += np.abs(t_q).sum(1)
+        mass["centers"][ids] += np.linalg.norm(t_c, axis=2).sum(1)[:, None]
+        mass["scales"][ids] += np.linalg.norm(t_s, axis=2).sum(1)[:, None]
+        mass["quats"][ids] += np.linalg.norm(t_q, axis=2).sum(1)[:, None]
         mass["sh"][ids] += np.abs(t_sh).sum(1)
 
 

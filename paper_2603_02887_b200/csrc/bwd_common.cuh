@@ -67,33 +67,54 @@ __device__ __forceinline__ bool bwd_pixel(BwdPix& st, const float4* rec, const f
     dE2 = st.s2 * w;
     // chain moments (render.py:326-339): by the envelope theorem the
     // kernel-peak offset u = Rᵀ(t·d - b) carries the whole chain
-    // (∂m2/∂μ = -2RΛu, ∂m2/∂s_k = -2u_k²/s_k³, ∂m2/∂R = 2 diff (Λu)ᵀ).
-    // u is built from the stable conic offset diff' = b'_z·e,
-    // e = δ - ε h, δ = Δ/f, ε = δᵀA'h/D (all O(|δ|), no cancellation
-    // against b'), rotated into the Gaussian frame per pixel so each
-    // moment term has the sign structure of the reference's terms
+    // (∂m2/∂μ = -2RΛu, ∂m2/∂s_k = -2u_k²/s_k³, ∂m2/∂R = 2 diff (Λu)ᵀ)
     const float dae = (t.araw >= ALPHA_MAX_F) ? 0.f : da;
     dm2 = -0.5f * alpha * dae;
     dak = dae * t.kern;
-    float qx, qy, qz;  // peak offset e (conic: diff'/b'_z; general: diff)
-    if (gen) {
-      qx = gx;
-      qy = gy;
-      qz = gz;
-    } else {
-      const float4 r2 = rec[2];
+    // Whitened Gaussian-frame peak offset y = Λ^{1/2} u (u = Rᵀ diff; the
+    // chain rescales by s in fp64), with the whitened B̃ = Λ^{1/2} B of K1.
+    // Conic records: y = B̃ e with the stable conic offset e = δ - ε h
+    // (δ = Δ/f, ε = δᵀA'h/D, all O(|δ|)).  For a thin Gaussian the
+    // thin-axis component of B̃ e cancels (error ~1e-7 x the aspect ratio);
+    // those records (RF_ANISO) use the cross-product form
+    // y = b'_z (a × v)/|a|², a = B̃ h, v_k = s_k² [B̃ (Δ × c)]_k / (s0 s1 s2),
+    // c = the centre's normalised image point: every input is O(1)-accurate.
+    const int rflags = __float_as_int(rec[3].w);
+    if (!gen && (rflags & RF_ANISO)) {
       const float dxn = t.ddx * inv_f, dyn = t.ddy * inv_f;
-      const float Ahx = r2.x * t.u;
-      const float Ahy = fmaf(r2.x * r2.y, t.u, r2.w * t.v);
-      const float eps = fmaf(dxn, Ahx, dyn * Ahy) * t.rD;
-      qx = fmaf(-eps, st.pc.hx, dxn);
-      qy = fmaf(-eps, st.pc.hy, dyn);
-      qz = -eps;
+      const float ccx = st.pc.hx - dxn, ccy = st.pc.hy - dyn;
+      const float w0 = dyn, w1 = -dxn, w2 = fmaf(dxn, ccy, -dyn * ccx);  // Δ × c
+      const float ax = fmaf(bf[0].x, st.pc.hx, fmaf(bf[0].y, st.pc.hy, bf[0].z));
+      const float ay = fmaf(bf[1].x, st.pc.hx, fmaf(bf[1].y, st.pc.hy, bf[1].z));
+      const float az = fmaf(bf[2].x, st.pc.hx, fmaf(bf[2].y, st.pc.hy, bf[2].z));
+      const float ip3 = 1.0f / (bf[0].w * bf[1].w * bf[2].w);
+      const float v0 = fmaf(bf[0].x, w0, fmaf(bf[0].y, w1, bf[0].z * w2)) * (bf[0].w * bf[0].w * ip3);
+      const float v1 = fmaf(bf[1].x, w0, fmaf(bf[1].y, w1, bf[1].z * w2)) * (bf[1].w * bf[1].w * ip3);
+      const float v2 = fmaf(bf[2].x, w0, fmaf(bf[2].y, w1, bf[2].z * w2)) * (bf[2].w * bf[2].w * ip3);
+      const float sc = rec[7].w / fmaf(ax, ax, fmaf(ay, ay, az * az));
+      ux = fmaf(ay, v2, -az * v1) * sc;
+      uy = fmaf(az, v0, -ax * v2) * sc;
+      uz = fmaf(ax, v1, -ay * v0) * sc;
+    } else {
+      float qx, qy, qz;  // peak offset e (conic: diff'/b'_z; general: diff)
+      if (gen) {
+        qx = gx;
+        qy = gy;
+        qz = gz;
+      } else {
+        const float4 r2 = rec[2];
+        const float dxn = t.ddx * inv_f, dyn = t.ddy * inv_f;
+        const float Ahx = r2.x * t.u;
+        const float Ahy = fmaf(r2.x * r2.y, t.u, r2.w * t.v);
+        const float eps = fmaf(dxn, Ahx, dyn * Ahy) * t.rD;
+        qx = fmaf(-eps, st.pc.hx, dxn);
+        qy = fmaf(-eps, st.pc.hy, dyn);
+        qz = -eps;
+      }
+      ux = fmaf(bf[0].x, qx, fmaf(bf[0].y, qy, bf[0].z * qz));
+      uy = fmaf(bf[1].x, qx, fmaf(bf[1].y, qy, bf[1].z * qz));
+      uz = fmaf(bf[2].x, qx, fmaf(bf[2].y, qy, bf[2].z * qz));
     }
-    // Gaussian-frame offset u = Rᵀ diff = B e
-    ux = fmaf(bf[0].x, qx, fmaf(bf[0].y, qy, bf[0].z * qz));
-    uy = fmaf(bf[1].x, qx, fmaf(bf[1].y, qy, bf[1].z * qz));
-    uz = fmaf(bf[2].x, qx, fmaf(bf[2].y, qy, bf[2].z * qz));
   }
   // SH moments use dE_c·[E_c > 0] (render.py:340-341)
   e0 = (mask & 1) ? dE0 : 0.f;

@@ -4,9 +4,10 @@
 //
 // Replaces the reference chain (pkg/src/nexsplat/render.py:326-341, with
 // quat_rot_jacobian primitives.py:67-93).  K4 accumulated per rank, in the
-// Gaussian's own frame (u = Rᵀ(t·d − b), the kernel-peak offset),
-//     U = Σ_px dm2 · u uᵀ   (6 values, symmetric 3x3)
-//     V = Σ_px dm2 · u      (3 values)
+// Gaussian's own whitened frame (y = Λ^{1/2} u, u = Rᵀ(t·d − b) the
+// kernel-peak offset), U' = Σ_px dm2 · y yᵀ and V' = Σ_px dm2 · y; here
+//     U = S U' S = Σ_px dm2 · u uᵀ   (6 values, symmetric 3x3)
+//     V = S V'   = Σ_px dm2 · u      (3 values)
 // with dm2 = -½·α·dα (dα zeroed where α is clamped, render.py:327).  By the
 // envelope theorem (primitives.py:245-249) m2 = diffᵀ A diff differentiated
 // at fixed peak depth, so with Λ = diag(s⁻²):
@@ -48,8 +49,12 @@ __global__ void k_chain(const float* __restrict__ scales, const float* __restric
 #pragma unroll
   for (int k = 0; k < 9; ++k) geo |= (mv[k] != 0.0);
   if (!geo) return;
-  const double U[9] = {mv[0], mv[1], mv[2], mv[1], mv[3], mv[4], mv[2], mv[4], mv[5]};
-  const double V[3] = {mv[6], mv[7], mv[8]};
+  // K4 accumulated the whitened offset y = Λ^{1/2} u: U = S U' S, V = S V'
+  const double s[3] = {scales[3 * g + 0], scales[3 * g + 1], scales[3 * g + 2]};
+  const double U[9] = {mv[0] * s[0] * s[0], mv[1] * s[0] * s[1], mv[2] * s[0] * s[2],
+                       mv[1] * s[0] * s[1], mv[3] * s[1] * s[1], mv[4] * s[1] * s[2],
+                       mv[2] * s[0] * s[2], mv[4] * s[1] * s[2], mv[5] * s[2] * s[2]};
+  const double V[3] = {mv[6] * s[0], mv[7] * s[1], mv[8] * s[2]};
 
   const double qw = quats[4 * g + 0], qx = quats[4 * g + 1], qy = quats[4 * g + 2],
                qz = quats[4 * g + 3];
@@ -58,7 +63,6 @@ __global__ void k_chain(const float* __restrict__ scales, const float* __restric
   const double R[9] = {1.0 - 2.0 * (y * y + z * z), 2.0 * (x * y - w * z), 2.0 * (x * z + w * y),
                        2.0 * (x * y + w * z), 1.0 - 2.0 * (x * x + z * z), 2.0 * (y * z - w * x),
                        2.0 * (x * z - w * y), 2.0 * (y * z + w * x), 1.0 - 2.0 * (x * x + y * y)};
-  const double s[3] = {scales[3 * g + 0], scales[3 * g + 1], scales[3 * g + 2]};
   const double L[3] = {1.0 / (s[0] * s[0]), 1.0 / (s[1] * s[1]), 1.0 / (s[2] * s[2])};
 
   const double LV[3] = {L[0] * V[0], L[1] * V[1], L[2] * V[2]};

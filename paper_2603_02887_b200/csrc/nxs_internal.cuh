@@ -33,6 +33,8 @@ constexpr float P_FLOOR = 1e-30f;
 // record flags (stored as int bits in rec[3].w)
 constexpr int RF_CONIC = 1;    // centred-conic fp32 evaluation
 constexpr int RF_GENERAL = 2;  // crosses the near region: fp64 reference diff-form
+constexpr int RF_ANISO = 4;    // conic record of a Gaussian with max/min scale > 4: the
+                               // backward uses the cancellation-free peak offset
 // General-path record: fp64 world-frame b = μ - o and A = R diag(s⁻²) Rᵀ
 // (upper triangle) packed as doubles 0..6 = b0 b1 b2 A00 A01 A02 A11 (float
 // words 0..13) and doubles 14..15 = A12 A22 (float words 28..31); words 14

@@ -572,23 +572,30 @@ __device__ __forceinline__ void project_one(const GParams& prm, int64_t g, const
     rec[0] = make_float4(cxh, cyh, cxl, cyl);
     rec[1] = make_float4((float)n0, (float)kk, (float)n1, (float)r2m);
     rec[2] = make_float4((float)a, (float)bb, (float)cc, (float)d);
-    rec[3] = make_float4((float)e, (float)gg, (float)opac, __int_as_float(RF_CONIC));
+    const double smx = fmax(s0, fmax(s1, s2)), smn = fmin(s0, fmin(s1, s2));
+    rec[3] = make_float4((float)e, (float)gg, (float)opac,
+                         __int_as_float(RF_CONIC | (smx > 4.0 * smn ? RF_ANISO : 0)));
   }
   rec[4] = make_float4(shv[0], shv[1], shv[2], shv[3]);
   rec[5] = make_float4(shv[4], shv[5], shv[6], shv[7]);
   rec[6] = make_float4(shv[8], shv[9], shv[10], shv[11]);
-  // conic: reserved for the exact-order mode (t-coefficients (A'b')·h, z_lo)
-  if (!general) rec[7] = make_float4((float)Ab[0], (float)Ab[1], (float)Ab[2], (float)zmin);
+  // conic: t coefficients (A'b')·h of the exact-order mode, and b'_z (the
+  // backward's cancellation-free peak offset)
+  if (!general) rec[7] = make_float4((float)Ab[0], (float)Ab[1], (float)Ab[2], (float)bp[2]);
   // B maps the per-pixel peak offset e (conic: camera-frame diff'/b'_z;
   // general: world-frame diff) to the Gaussian frame, u = Rᵀ diff = B e:
-  // conic B = b'_z Mᵀ, general B = Rᵀ (used by the backward only)
+  // conic B = b'_z Mᵀ, general B = Rᵀ; stored whitened (row k / s_k, so
+  // B̃ e = Λ^{1/2} u directly) with .w = s_k (used by the backward only)
+  const double sk[3] = {s0, s1, s2};
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
+    const double ik = 1.0 / sk[k];
     if (general)
-      bf[k] = make_float4((float)R[0 + k], (float)R[3 + k], (float)R[6 + k], 0.f);
+      bf[k] = make_float4((float)(R[0 + k] * ik), (float)(R[3 + k] * ik), (float)(R[6 + k] * ik),
+                          (float)sk[k]);
     else
-      bf[k] = make_float4((float)(bp[2] * M[0 + k]), (float)(bp[2] * M[3 + k]),
-                          (float)(bp[2] * M[6 + k]), 0.f);
+      bf[k] = make_float4((float)(bp[2] * M[0 + k] * ik), (float)(bp[2] * M[3 + k] * ik),
+                          (float)(bp[2] * M[6 + k] * ik), (float)sk[k]);
   }
   out.rects[g] = rect;  // storage order (coalesced); the binning gathers by rank
 }
