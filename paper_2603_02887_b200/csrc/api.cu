@@ -26,15 +26,23 @@ void launch_depth(const float*, const float*, const float*, const float*, int64_
                   cudaStream_t);
 void launch_key32(const double*, int64_t, const unsigned long long*, uint32_t*, cudaStream_t);
 void launch_key_fixup(const uint32_t*, uint32_t*, const double*, int64_t, unsigned long long*,
-                      cudaStream_t, int shift = 0);
+                      cudaStream_t, int shift = 0, const int* nd = nullptr);
 void launch_rank_of(const uint32_t*, int64_t, uint32_t*, cudaStream_t);
-void launch_rank_of_range(const uint32_t*, int64_t, int64_t, uint32_t*, cudaStream_t);
+void launch_rank_of_range(const uint32_t*, int64_t, int64_t, uint32_t*, cudaStream_t,
+                          const int* nd = nullptr);
 void launch_key_hist(const uint32_t*, int64_t, unsigned int*, cudaStream_t);
 void launch_phase_select(const unsigned int*, const int64_t*, int, int64_t, long long*,
-                         cudaStream_t);
+                         cudaStream_t, int max_bin0 = -1, unsigned long long* overflow = nullptr);
 void launch_project_ranks(const float*, const float*, const float*, const float*, const float*,
                           int, int64_t, int64_t, const uint32_t*, const CamDev&, double, double,
-                          int4*, float4*, float4*, unsigned long long*, cudaStream_t);
+                          int4*, float4*, float4*, unsigned long long*, cudaStream_t,
+                          const int* nd = nullptr);
+void launch_gather_keys_pad(uint32_t*, const uint32_t*, const int*, int64_t, uint32_t*,
+                            cudaStream_t);
+void launch_pairs_total(const unsigned long long*, const unsigned long long*, int64_t,
+                        unsigned long long, unsigned long long*, unsigned long long*,
+                        cudaStream_t);
+void launch_pad_keys(uint32_t*, int64_t, const unsigned long long*, cudaStream_t);
 void launch_gather_keys(const uint32_t*, const uint32_t*, int64_t, uint32_t*, cudaStream_t);
 void launch_clear_rects(const uint32_t*, int64_t, int64_t, int4*, cudaStream_t);
 void launch_iota(uint32_t*, int64_t, cudaStream_t);
@@ -50,9 +58,11 @@ void launch_blend_fwd_x(bool, int, const FwdXArgs&, const CamDev&, const ModelDe
 void launch_blend_bwd_x(bool, int, const BwdXArgs&, const CamDev&, const ModelDev&,
                         const PixCache&, Counters*, cudaStream_t);
 void launch_count_active(const int4*, const uint32_t*, int64_t, int64_t, int, const uint8_t*,
-                         const unsigned int*, unsigned long long*, cudaStream_t);
+                         const unsigned int*, unsigned long long*, cudaStream_t,
+                         const int* nd = nullptr);
 void launch_emit_pairs(const int4*, const uint32_t*, const unsigned long long*, int64_t, int64_t,
-                       int, const uint8_t*, uint32_t*, uint32_t*, cudaStream_t);
+                       int, const uint8_t*, uint32_t*, uint32_t*, cudaStream_t,
+                       const int* nd = nullptr, unsigned long long cap = ~0ull);
 void launch_tile_ranges(const uint32_t*, int64_t, int2*, cudaStream_t);
 void launch_blend_fwd(bool, int, const FwdArgs&, const CamDev&, const ModelDev&, const PixCache&,
                       const PixResume&, Counters*, cudaStream_t);
@@ -125,9 +135,10 @@ namespace nxs {
 struct BinRange {
   const uint32_t* key;
   int lo, hi;
+  const long long* dev_hi = nullptr;  // device-sized phase 0: last bin from k_phase_select
   __host__ __device__ bool operator()(const uint32_t& i) const {
     const int b = (int)(key[i] >> 20);
-    return b >= lo && b <= hi;
+    return b >= lo && b <= (dev_hi ? (int)*dev_hi : hi);
   }
 };
 // error reporting for entry points defined in other translation units
@@ -176,6 +187,13 @@ struct nxs_view {
   // view needed `phases_needed` phases)
   bool spec_pending = false;
   int phases_needed = 0;
+  // device-sized first phase: sizes of this view's last call (ranks, pairs,
+  // last key bin); valid after a call whose phase 0 was sized exactly
+  int64_t est_n0 = 0, est_pairs = 0;
+  int est_bin0 = -1;
+  bool async_pending = false;  // phase 0 ran device-sized, not yet verified
+  int n_phases_plan = 0;       // planned depth phases of the last forward
+  int64_t async_cap0 = 0, async_capp = 0;
   int64_t sorted_end = 0, proj_end = 0;
   int bin_done = -1;
   const float* scene_centers = nullptr;
@@ -429,6 +447,57 @@ int nxs_forward(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
 }  // extern "C"
 
 namespace {
+// Read back and check a device-sized phase 0 (behind its forward kernel):
+// host_small[3] = active tiles, [16..) = phase bounds (bin, end rank) of
+// k_phase_select, [24] = phase-0 Gaussians, [25] = overflow flags, [26] =
+// pair total.  The copies are enqueued (and v->ev_sync recorded) by
+// enqueue_async_check; finish_async_check waits for them: ok == false means
+// some capacity was exceeded and the pass must be redone with exact sizes.
+int enqueue_async_check(nxs_view* v, int n_ph, cudaStream_t s) {
+  unsigned long long* dsmall = v->dev_small.as<unsigned long long>();
+  long long* dsel = v->ph_sel.as<long long>();
+  v->host_small[24] = 0;
+  NXS_CUDA(cudaMemcpyAsync(v->host_small + 3, dsmall + 5, sizeof(unsigned int),
+                           cudaMemcpyDeviceToHost, s));
+  NXS_CUDA(cudaMemcpyAsync(v->host_small + 16, dsel, sizeof(long long) * 2 * n_ph,
+                           cudaMemcpyDeviceToHost, s));
+  NXS_CUDA(cudaMemcpyAsync(v->host_small + 24, dsel + 48, sizeof(int), cudaMemcpyDeviceToHost, s));
+  NXS_CUDA(cudaMemcpyAsync(v->host_small + 25, dsmall + 10, 2 * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, s));
+  NXS_CUDA(cudaMemcpyAsync(v->host_small + 2, dsmall, sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, s));
+  NXS_CUDA(cudaEventRecord(v->ev_sync, s));
+  return NXS_OK;
+}
+
+int finish_async_check(nxs_view* v, bool& ok) {
+  cudaError_t e;
+  while ((e = cudaEventQuery(v->ev_sync)) == cudaErrorNotReady) {
+  }
+  NXS_CUDA(e);
+  const int64_t n0 = (int64_t)(int)(uint32_t)v->host_small[24];
+  const uint64_t pairs = v->host_small[26];
+  ok = v->host_small[25] == 0 && n0 <= v->async_cap0 && (int64_t)pairs <= v->async_capp;
+  v->async_pending = false;
+  if (!ok) {
+    v->est_n0 = 0;  // the next pass sizes phase 0 exactly again
+    return NXS_OK;
+  }
+  const long long* hsel = reinterpret_cast<const long long*>(v->host_small + 16);
+  v->est_n0 = n0;
+  v->est_pairs = (int64_t)pairs;
+  v->est_bin0 = (int)hsel[0];
+  v->ph_pairs[0] = (int64_t)pairs;
+  v->n_pairs = (int64_t)pairs;
+  v->stats.n_pairs = (int64_t)pairs;
+  v->stats.n_straddling = (int64_t)v->host_small[2];
+  v->sorted_end = v->proj_end = n0;
+  v->bin_done = (int)hsel[0];
+  return NXS_OK;
+}
+}  // namespace
+
+namespace {
 int forward_impl(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
                  const nxs_model* model, const nxs_opts* opts, const float background[3],
                  float* rgb, int32_t* overdraw, float* residual, void* stream_, int spec_phase) {
@@ -535,13 +604,20 @@ int forward_impl(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
   // (only the phases the image needs); the t-ordered modes, full binning
   // and the 64-bit fallback sort and project everything up front.
   bool sort64 = false;
+  v->n_phases_plan = n_ph;
   int64_t Rplan[MAX_PHASES + 1];
   const int n_ph_plan = n_ph;
   for (int i = 0; i <= n_ph; ++i) Rplan[i] = R[i];
   int ph_bin[MAX_PHASES] = {0, 0, 0, 0};  // last key bin of each lazy phase
+  // device-sized phase 0 (no host sync before the first forward): needs
+  // estimates from this view's previous call and a later phase to verify at
+  bool async0 = v->est_n0 > 0 && v->est_pairs >= 0 && v->est_bin0 >= 0 && n_ph >= 2 &&
+                spec_phase >= 0;
   bool phase_full[MAX_PHASES] = {false, false, false, false};  // lazy phase sorted on 32 bits
   int phase_shift[MAX_PHASES] = {0, 0, 0, 0};
 retry_sort:
+  if (sort64) async0 = false;
+  v->async_pending = false;
   n_ph = n_ph_plan;
   for (int i = 0; i <= n_ph; ++i) R[i] = Rplan[i];
   v->lazy = !torder && !sort64 && !(opts->flags & NXS_FLAG_FULL_BINNING) && P > 0;
@@ -605,6 +681,22 @@ retry_sort:
       long long* dsel = v->ph_sel.as<long long>();
       NXS_CUDA(cudaMemcpyAsync(dsel + 32, tgt, sizeof(int64_t) * (n_ph - 1 > 0 ? n_ph - 1 : 1),
                                cudaMemcpyHostToDevice, s));
+      if (async0) {
+        // phase 0 sized from the previous call; the last bin it may use is
+        // checked on the device (k_phase_select) and verified later
+        NXS_CUDA(cudaMemsetAsync(dsmall + 10, 0, 2 * sizeof(unsigned long long), s));
+        ph_bin[0] = std::min(4095, v->est_bin0 + 2);
+        launch_phase_select(v->ph_hist.as<unsigned int>(), reinterpret_cast<int64_t*>(dsel + 32),
+                            n_ph - 1, P, dsel, s, ph_bin[0], dsmall + 10);
+        NXS_LAUNCHED("phase_select");
+        v->async_cap0 = std::min<int64_t>(P, v->est_n0 + v->est_n0 / 8 + 2048);
+        v->async_capp = v->est_pairs + v->est_pairs / 8 + 8192;
+        R[0] = 0;
+        R[1] = v->async_cap0;  // ranks phase 0 may occupy; later bounds come with the check
+      }
+    }
+    if (v->lazy && !async0) {
+      long long* dsel = v->ph_sel.as<long long>();
       launch_phase_select(v->ph_hist.as<unsigned int>(), reinterpret_cast<int64_t*>(dsel + 32),
                           n_ph - 1, P, dsel, s);
       NXS_LAUNCHED("phase_select");
@@ -624,7 +716,7 @@ retry_sort:
       }
       n_ph = m;
       R[0] = 0;
-    } else {
+    } else if (!v->lazy && !sort64) {
       launch_key32(v->depth.as<double>(), P, dsmall + 6, v->k32a.as<uint32_t>(), s);
       NXS_LAUNCHED("key32");
       NXS_CUDA(cub::DeviceRadixSort::SortPairs(v->temp.p, tb, v->k32a.as<uint32_t>(),
@@ -690,152 +782,267 @@ retry_sort:
   int64_t total_pairs = 0;
   int ph_done = 0;
   for (int ph = 0; ph < n_ph; ++ph) {
-    const int64_t r0 = R[ph], r1 = R[ph + 1], nr = r1 - r0;
+    int64_t r0 = R[ph], r1 = R[ph + 1], nr = r1 - r0;
     if (v->ev_ok) cudaEventRecord(v->evp[ph][0], s);
-    if (v->lazy) {
-      if (ph > 0 && ph == spec_phase) {
-        // fused call: the backward goes ahead and the check overlaps it
-        v->spec_pending = true;
+    if (v->async_pending && ph > 0 && ph != spec_phase) {
+      // verify the device-sized phase 0 and learn the real phase bounds
+      bool ok = false;
+      int rc2;
+      if ((rc2 = enqueue_async_check(v, n_ph, s))) return rc2;
+      if ((rc2 = finish_async_check(v, ok))) return rc2;
+      if (!ok) {
+        async0 = false;
+        NXS_CUDA(cudaMemsetAsync(dsmall, 0, 16 * sizeof(unsigned long long), s));
+        NXS_CUDA(cudaMemsetAsync(v->active.p, 1, (size_t)n_tiles, s));
+        goto retry_sort;
+      }
+      total_pairs += v->ph_pairs[0];
+      const long long* hsel = reinterpret_cast<const long long*>(v->host_small + 16);
+      int m = 0;
+      int64_t last = 0;
+      for (int p = 0; p < n_ph; ++p) {
+        const int64_t end = hsel[2 * p + 1];
+        if (end <= last && m > 0) continue;
+        ph_bin[m] = (int)hsel[2 * p];
+        R[++m] = std::max(end, last);
+        last = R[m];
+      }
+      n_ph = m;
+      R[0] = 0;
+      if ((unsigned)v->host_small[3] == 0 || ph >= n_ph) {  // every tile finished
+        v->phases_needed = 1;
         break;
       }
-      if (ph > 0) {
-        // the previous phase's forward decides whether this one is needed
-        NXS_CUDA(cudaMemcpyAsync(v->host_small + 3, n_active, sizeof(unsigned int),
-                                 cudaMemcpyDeviceToHost, s));
-        NXS_CUDA(spin_sync(v, s));
-        if ((unsigned)v->host_small[3] == 0) {  // every tile finished
-          v->phases_needed = ph;
-          break;
-        }
-      }
-      if (nr > 0) {
-        // ---- this phase's Gaussians (key bins (prev, ph_bin]) in storage
-        // order, 32-bit sort + fix-up into ranks [r0, r1), projection
-        const int lo = ph == 0 ? 0 : ph_bin[ph - 1] + 1, hi = ph_bin[ph];
-        size_t tbs = v->temp.cap;
-        NXS_CUDA(cub::DeviceSelect::If(v->temp.p, tbs, cub::CountingInputIterator<uint32_t>(0),
-                                       v->idx_in.as<uint32_t>(),
-                                       reinterpret_cast<int*>(v->ph_sel.as<long long>() + 48),
-                                       (int)P, BinRange{v->k32a.as<uint32_t>(), lo, hi}, s));
-        NXS_CUDA(ensure_n<uint32_t>(v->k32c, P));
-        launch_gather_keys(v->idx_in.as<uint32_t>(), v->k32a.as<uint32_t>(), nr,
-                           v->k32c.as<uint32_t>(), s);
-        NXS_LAUNCHED("gather_keys");
-        // two radix passes over the top 16 significant key bits of the
-        // phase; the fix-up re-sorts equal truncated keys exactly (a run
-        // over 256 redoes the phase on all 32 bits)
-        const int end_bit = std::min(32, 20 + bits_for((uint32_t)hi + 1));
-        const int shift = phase_full[ph] ? 0 : std::max(0, end_bit - 16);
-        size_t tb = v->temp.cap;
-        NXS_CUDA(cub::DeviceRadixSort::SortPairs(v->temp.p, tb, v->k32c.as<uint32_t>(),
-                                                 v->k32b.as<uint32_t>() + r0,
-                                                 v->idx_in.as<uint32_t>(),
-                                                 v->idx_out.as<uint32_t>() + r0, (int)nr, shift,
-                                                 shift ? end_bit : 32, s));
-        launch_key_fixup(v->k32b.as<uint32_t>() + r0, v->idx_out.as<uint32_t>() + r0,
-                         v->depth.as<double>(), nr, dsmall + 8, s, shift);
-        phase_shift[ph] = shift;
-        NXS_LAUNCHED("key_fixup");
-        launch_rank_of_range(v->idx_out.as<uint32_t>(), r0, r1, v->rank_of.as<uint32_t>(), s);
-        NXS_LAUNCHED("rank_of");
-        v->sorted_end = r1;
-        v->bin_done = hi;
-        if (v->ev_ok) cudaEventRecord(v->evp[ph][1], s);
-        launch_project_ranks(scene->centers, scene->scales, scene->quats, scene->opacities,
-                             scene->sh, C, r0, r1, v->idx_out.as<uint32_t>(), cam,
-                             opts->alpha_cutoff, opts->near_plane, v->rects.as<int4>(),
-                             v->records.as<float4>(), v->bframe.as<float4>(), dsmall, s);
-        NXS_LAUNCHED("project_ranks");
-        v->proj_end = r1;
-      } else if (v->ev_ok) {
-        cudaEventRecord(v->evp[ph][1], s);
-      }
-      if (v->ev_ok) cudaEventRecord(v->evp[ph][2], s);
-    } else if (v->ev_ok) {
-      cudaEventRecord(v->evp[ph][1], s);
-      cudaEventRecord(v->evp[ph][2], s);
+      r0 = R[ph];
+      r1 = R[ph + 1];
+      nr = r1 - r0;
     }
-    // ---- K2a counts over active tiles, scan, one host sync for the pair count
-    if (nr > 0) {
-      launch_count_active(v->rects.as<int4>(), v->idx_out.as<uint32_t>(), r0, r1, cam.tiles_x,
-                          v->active.as<uint8_t>(), ph > 0 ? n_active : nullptr,
-                          v->ntiles.as<unsigned long long>(), s);
-      NXS_LAUNCHED("count_active");
+    if (async0 && ph == 0) {
+      // ---- device-sized phase 0: every size below is an upper bound from
+      // this view's previous call; the real counts stay on the device
+      // (n_sel, pair total) and are verified behind the forward
+      const int64_t cap0 = v->async_cap0, capp = v->async_capp;
+      int* n_sel = reinterpret_cast<int*>(v->ph_sel.as<long long>() + 48);
+      long long* dsel = v->ph_sel.as<long long>();
+      size_t tbs = v->temp.cap;
+      NXS_CUDA(cub::DeviceSelect::If(v->temp.p, tbs, cub::CountingInputIterator<uint32_t>(0),
+                                     v->idx_in.as<uint32_t>(), n_sel, (int)P,
+                                     BinRange{v->k32a.as<uint32_t>(), 0, 0, dsel}, s));
+      NXS_CUDA(ensure_n<uint32_t>(v->k32c, P));
+      launch_gather_keys_pad(v->idx_in.as<uint32_t>(), v->k32a.as<uint32_t>(), n_sel, cap0,
+                             v->k32c.as<uint32_t>(), s);
+      NXS_LAUNCHED("gather_keys_pad");
+      const int end_bit = std::min(32, 20 + bits_for((uint32_t)ph_bin[0] + 1));
+      const int shift = std::max(0, end_bit - 16);
       size_t tb = v->temp.cap;
-      NXS_CUDA(cub::DeviceScan::ExclusiveSum(v->temp.p, tb, v->ntiles.as<unsigned long long>(),
-                                             v->offsets.as<unsigned long long>(), (int)nr, s));
-      NXS_CUDA(cudaMemcpyAsync(v->host_small, v->offsets.as<unsigned long long>() + (nr - 1),
-                               sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-      NXS_CUDA(cudaMemcpyAsync(v->host_small + 1, v->ntiles.as<unsigned long long>() + (nr - 1),
-                               sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-    } else {
-      NXS_CUDA(cudaMemsetAsync(v->host_small, 0, 2 * sizeof(unsigned long long), s));
-    }
-    NXS_CUDA(cudaMemcpyAsync(v->host_small + 2, dsmall, sizeof(unsigned long long),
-                             cudaMemcpyDeviceToHost, s));
-    NXS_CUDA(cudaMemcpyAsync(v->host_small + 3, n_active, sizeof(unsigned int),
-                             cudaMemcpyDeviceToHost, s));
-    if (ph == 0 || v->lazy)
-      NXS_CUDA(cudaMemcpyAsync(v->host_small + 6, dsmall + 8, sizeof(unsigned long long),
-                               cudaMemcpyDeviceToHost, s));
-    NXS_CUDA(spin_sync(v, s));
-    if (v->lazy && v->host_small[6] != 0 && phase_shift[ph] > 0) {
-      // a long run of equal truncated keys: redo this phase on all 32 bits
-      phase_full[ph] = true;
-      NXS_CUDA(cudaMemsetAsync(dsmall + 8, 0, sizeof(unsigned long long), s));
-      --ph;
-      continue;
-    }
-    if ((ph == 0 || v->lazy) && !sort64 && v->host_small[6] != 0) {
-      // an equal-key run longer than the fix-up handles: redo with 64-bit keys
-      sort64 = true;
-      NXS_CUDA(cudaMemsetAsync(dsmall, 0, 16 * sizeof(unsigned long long), s));
-      goto retry_sort;
-    }
-    if (ph == 0) mark(v, 3, s);
-    const unsigned long long n_pairs = v->host_small[0] + v->host_small[1];
-    v->stats.n_straddling = (int64_t)v->host_small[2];
-    if (ph > 0 && !v->lazy && (unsigned)v->host_small[3] == 0) break;  // every tile finished
-    if (n_pairs >= (1ull << 31)) return fail(NXS_ERR_NOMEM, "more than 2^31 tile pairs");
-    total_pairs += (int64_t)n_pairs;
-    v->ph_pairs[ph] = (int64_t)n_pairs;
-
-    NXS_CUDA(ensure_n<int2>(v->ranges_ph[ph], n_tiles));
-    NXS_CUDA(ensure_n<int32_t>(v->cum_ph[ph + 1], n_tiles));
-    NXS_CUDA(ensure_n<uint32_t>(v->pv_ph[ph], std::max<int64_t>(1, (int64_t)n_pairs)));
-    NXS_CUDA(cudaMemsetAsync(v->ranges_ph[ph].p, 0, (size_t)n_tiles * sizeof(int2), s));
-    if (n_pairs > 0) {
-      NXS_CUDA(ensure_n<uint32_t>(v->pk_in, (int64_t)n_pairs));
-      NXS_CUDA(ensure_n<uint32_t>(v->pk_out, (int64_t)n_pairs));
-      NXS_CUDA(ensure_n<uint32_t>(v->pv_in, (int64_t)n_pairs));
+      NXS_CUDA(cub::DeviceRadixSort::SortPairs(v->temp.p, tb, v->k32c.as<uint32_t>(),
+                                               v->k32b.as<uint32_t>(), v->idx_in.as<uint32_t>(),
+                                               v->idx_out.as<uint32_t>(), (int)cap0, shift,
+                                               shift ? end_bit : 32, s));
+      launch_key_fixup(v->k32b.as<uint32_t>(), v->idx_out.as<uint32_t>(), v->depth.as<double>(),
+                       cap0, dsmall + 8, s, shift, n_sel);
+      NXS_LAUNCHED("key_fixup");
+      launch_rank_of_range(v->idx_out.as<uint32_t>(), 0, cap0, v->rank_of.as<uint32_t>(), s,
+                           n_sel);
+      NXS_LAUNCHED("rank_of");
+      if (v->ev_ok) cudaEventRecord(v->evp[0][1], s);
+      launch_project_ranks(scene->centers, scene->scales, scene->quats, scene->opacities,
+                           scene->sh, C, 0, cap0, v->idx_out.as<uint32_t>(), cam,
+                           opts->alpha_cutoff, opts->near_plane, v->rects.as<int4>(),
+                           v->records.as<float4>(), v->bframe.as<float4>(), dsmall, s, n_sel);
+      NXS_LAUNCHED("project_ranks");
+      if (v->ev_ok) cudaEventRecord(v->evp[0][2], s);
+      launch_count_active(v->rects.as<int4>(), v->idx_out.as<uint32_t>(), 0, cap0, cam.tiles_x,
+                          v->active.as<uint8_t>(), nullptr, v->ntiles.as<unsigned long long>(),
+                          s, n_sel);
+      NXS_LAUNCHED("count_active");
+      size_t tbc = v->temp.cap;
+      NXS_CUDA(cub::DeviceScan::ExclusiveSum(v->temp.p, tbc, v->ntiles.as<unsigned long long>(),
+                                             v->offsets.as<unsigned long long>(), (int)cap0, s));
+      launch_pairs_total(v->offsets.as<unsigned long long>(), v->ntiles.as<unsigned long long>(),
+                         cap0, (unsigned long long)capp, dsmall + 11, dsmall + 10, s);
+      NXS_LAUNCHED("pairs_total");
+      NXS_CUDA(ensure_n<int2>(v->ranges_ph[0], n_tiles));
+      NXS_CUDA(ensure_n<int32_t>(v->cum_ph[1], n_tiles));
+      NXS_CUDA(ensure_n<uint32_t>(v->pv_ph[0], capp));
+      NXS_CUDA(ensure_n<uint32_t>(v->pk_in, capp));
+      NXS_CUDA(ensure_n<uint32_t>(v->pk_out, capp));
+      NXS_CUDA(ensure_n<uint32_t>(v->pv_in, capp));
+      NXS_CUDA(cudaMemsetAsync(v->ranges_ph[0].p, 0, (size_t)n_tiles * sizeof(int2), s));
+      const int tbits_pad = bits_for((uint32_t)n_tiles + 1);  // the padding key sorts last
       size_t tmp_pairs = 0;
       NXS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_pairs, v->pk_in.as<uint32_t>(),
                                                v->pk_out.as<uint32_t>(), v->pv_in.as<uint32_t>(),
-                                               v->pv_ph[ph].as<uint32_t>(), (int)n_pairs, 0,
-                                               tbits, s));
+                                               v->pv_ph[0].as<uint32_t>(), (int)capp, 0,
+                                               tbits_pad, s));
       NXS_CUDA(v->temp.ensure(tmp_pairs));
-      // ---- K2b pairs (rank order), stable sort by tile, ranges
       launch_emit_pairs(v->rects.as<int4>(), v->idx_out.as<uint32_t>(),
-                        v->offsets.as<unsigned long long>(), r0, r1, cam.tiles_x,
+                        v->offsets.as<unsigned long long>(), 0, cap0, cam.tiles_x,
                         v->active.as<uint8_t>(), v->pk_in.as<uint32_t>(), v->pv_in.as<uint32_t>(),
-                        s);
+                        s, n_sel, (unsigned long long)capp);
       NXS_LAUNCHED("emit_pairs");
-      if (ph == 0) mark(v, 4, s);
-      size_t tb = v->temp.cap;
-      NXS_CUDA(cub::DeviceRadixSort::SortPairs(v->temp.p, tb, v->pk_in.as<uint32_t>(),
-                                               v->pk_out.as<uint32_t>(), v->pv_in.as<uint32_t>(),
-                                               v->pv_ph[ph].as<uint32_t>(), (int)n_pairs, 0,
-                                               tbits, s));
-      if (ph == 0) mark(v, 5, s);
-      launch_tile_ranges(v->pk_out.as<uint32_t>(), (int64_t)n_pairs,
-                         v->ranges_ph[ph].as<int2>(), s);
-      NXS_LAUNCHED("tile_ranges");
-    } else if (ph == 0) {
+      launch_pad_keys(v->pk_in.as<uint32_t>(), capp, dsmall + 11, s);
+      NXS_LAUNCHED("pad_keys");
+      mark(v, 3, s);
       mark(v, 4, s);
+      size_t tbp = v->temp.cap;
+      NXS_CUDA(cub::DeviceRadixSort::SortPairs(v->temp.p, tbp, v->pk_in.as<uint32_t>(),
+                                               v->pk_out.as<uint32_t>(), v->pv_in.as<uint32_t>(),
+                                               v->pv_ph[0].as<uint32_t>(), (int)capp, 0,
+                                               tbits_pad, s));
       mark(v, 5, s);
+      launch_tile_ranges(v->pk_out.as<uint32_t>(), capp, v->ranges_ph[0].as<int2>(), s);
+      NXS_LAUNCHED("tile_ranges");
+      mark(v, 6, s);
+      if (v->ev_ok) cudaEventRecord(v->evp[0][3], s);
+      v->async_pending = true;
+      v->ph_pairs[0] = capp;  // capacity; the real count comes with the check
+    } else {
+      if (v->lazy) {
+        if (ph > 0 && ph == spec_phase) {
+          // fused call: the backward goes ahead and the check overlaps it
+          v->spec_pending = true;
+          break;
+        }
+        if (ph > 0 && !(ph == 1 && async0)) {
+          // the previous phase's forward decides whether this one is needed
+          NXS_CUDA(cudaMemcpyAsync(v->host_small + 3, n_active, sizeof(unsigned int),
+                                   cudaMemcpyDeviceToHost, s));
+          NXS_CUDA(spin_sync(v, s));
+          if ((unsigned)v->host_small[3] == 0) {  // every tile finished
+            v->phases_needed = ph;
+            break;
+          }
+        }
+        if (nr > 0) {
+          // ---- this phase's Gaussians (key bins (prev, ph_bin]) in storage
+          // order, 32-bit sort + fix-up into ranks [r0, r1), projection
+          const int lo = ph == 0 ? 0 : ph_bin[ph - 1] + 1, hi = ph_bin[ph];
+          size_t tbs = v->temp.cap;
+          NXS_CUDA(cub::DeviceSelect::If(v->temp.p, tbs, cub::CountingInputIterator<uint32_t>(0),
+                                         v->idx_in.as<uint32_t>(),
+                                         reinterpret_cast<int*>(v->ph_sel.as<long long>() + 48),
+                                         (int)P, BinRange{v->k32a.as<uint32_t>(), lo, hi}, s));
+          NXS_CUDA(ensure_n<uint32_t>(v->k32c, P));
+          launch_gather_keys(v->idx_in.as<uint32_t>(), v->k32a.as<uint32_t>(), nr,
+                             v->k32c.as<uint32_t>(), s);
+          NXS_LAUNCHED("gather_keys");
+          // two radix passes over the top 16 significant key bits of the
+          // phase; the fix-up re-sorts equal truncated keys exactly (a run
+          // over 256 redoes the phase on all 32 bits)
+          const int end_bit = std::min(32, 20 + bits_for((uint32_t)hi + 1));
+          const int shift = phase_full[ph] ? 0 : std::max(0, end_bit - 16);
+          size_t tb = v->temp.cap;
+          NXS_CUDA(cub::DeviceRadixSort::SortPairs(v->temp.p, tb, v->k32c.as<uint32_t>(),
+                                                   v->k32b.as<uint32_t>() + r0,
+                                                   v->idx_in.as<uint32_t>(),
+                                                   v->idx_out.as<uint32_t>() + r0, (int)nr, shift,
+                                                   shift ? end_bit : 32, s));
+          launch_key_fixup(v->k32b.as<uint32_t>() + r0, v->idx_out.as<uint32_t>() + r0,
+                           v->depth.as<double>(), nr, dsmall + 8, s, shift);
+          phase_shift[ph] = shift;
+          NXS_LAUNCHED("key_fixup");
+          launch_rank_of_range(v->idx_out.as<uint32_t>(), r0, r1, v->rank_of.as<uint32_t>(), s);
+          NXS_LAUNCHED("rank_of");
+          v->sorted_end = r1;
+          v->bin_done = hi;
+          if (v->ev_ok) cudaEventRecord(v->evp[ph][1], s);
+          launch_project_ranks(scene->centers, scene->scales, scene->quats, scene->opacities,
+                               scene->sh, C, r0, r1, v->idx_out.as<uint32_t>(), cam,
+                               opts->alpha_cutoff, opts->near_plane, v->rects.as<int4>(),
+                               v->records.as<float4>(), v->bframe.as<float4>(), dsmall, s);
+          NXS_LAUNCHED("project_ranks");
+          v->proj_end = r1;
+        } else if (v->ev_ok) {
+          cudaEventRecord(v->evp[ph][1], s);
+        }
+        if (v->ev_ok) cudaEventRecord(v->evp[ph][2], s);
+      } else if (v->ev_ok) {
+        cudaEventRecord(v->evp[ph][1], s);
+        cudaEventRecord(v->evp[ph][2], s);
+      }
+      // ---- K2a counts over active tiles, scan, one host sync for the pair count
+      if (nr > 0) {
+        launch_count_active(v->rects.as<int4>(), v->idx_out.as<uint32_t>(), r0, r1, cam.tiles_x,
+                            v->active.as<uint8_t>(), ph > 0 ? n_active : nullptr,
+                            v->ntiles.as<unsigned long long>(), s);
+        NXS_LAUNCHED("count_active");
+        size_t tb = v->temp.cap;
+        NXS_CUDA(cub::DeviceScan::ExclusiveSum(v->temp.p, tb, v->ntiles.as<unsigned long long>(),
+                                               v->offsets.as<unsigned long long>(), (int)nr, s));
+        NXS_CUDA(cudaMemcpyAsync(v->host_small, v->offsets.as<unsigned long long>() + (nr - 1),
+                                 sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+        NXS_CUDA(cudaMemcpyAsync(v->host_small + 1, v->ntiles.as<unsigned long long>() + (nr - 1),
+                                 sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+      } else {
+        NXS_CUDA(cudaMemsetAsync(v->host_small, 0, 2 * sizeof(unsigned long long), s));
+      }
+      NXS_CUDA(cudaMemcpyAsync(v->host_small + 2, dsmall, sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, s));
+      NXS_CUDA(cudaMemcpyAsync(v->host_small + 3, n_active, sizeof(unsigned int),
+                               cudaMemcpyDeviceToHost, s));
+      if (ph == 0 || v->lazy)
+        NXS_CUDA(cudaMemcpyAsync(v->host_small + 6, dsmall + 8, sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, s));
+      NXS_CUDA(spin_sync(v, s));
+      if (v->lazy && v->host_small[6] != 0 && phase_shift[ph] > 0) {
+        // a long run of equal truncated keys: redo this phase on all 32 bits
+        phase_full[ph] = true;
+        NXS_CUDA(cudaMemsetAsync(dsmall + 8, 0, sizeof(unsigned long long), s));
+        --ph;
+        continue;
+      }
+      if ((ph == 0 || v->lazy) && !sort64 && v->host_small[6] != 0) {
+        // an equal-key run longer than the fix-up handles: redo with 64-bit keys
+        sort64 = true;
+        NXS_CUDA(cudaMemsetAsync(dsmall, 0, 16 * sizeof(unsigned long long), s));
+        goto retry_sort;
+      }
+      if (ph == 0) mark(v, 3, s);
+      const unsigned long long n_pairs = v->host_small[0] + v->host_small[1];
+      v->stats.n_straddling = (int64_t)v->host_small[2];
+      if (ph > 0 && !v->lazy && (unsigned)v->host_small[3] == 0) break;  // every tile finished
+      if (n_pairs >= (1ull << 31)) return fail(NXS_ERR_NOMEM, "more than 2^31 tile pairs");
+      total_pairs += (int64_t)n_pairs;
+      v->ph_pairs[ph] = (int64_t)n_pairs;
+
+      NXS_CUDA(ensure_n<int2>(v->ranges_ph[ph], n_tiles));
+      NXS_CUDA(ensure_n<int32_t>(v->cum_ph[ph + 1], n_tiles));
+      NXS_CUDA(ensure_n<uint32_t>(v->pv_ph[ph], std::max<int64_t>(1, (int64_t)n_pairs)));
+      NXS_CUDA(cudaMemsetAsync(v->ranges_ph[ph].p, 0, (size_t)n_tiles * sizeof(int2), s));
+      if (n_pairs > 0) {
+        NXS_CUDA(ensure_n<uint32_t>(v->pk_in, (int64_t)n_pairs));
+        NXS_CUDA(ensure_n<uint32_t>(v->pk_out, (int64_t)n_pairs));
+        NXS_CUDA(ensure_n<uint32_t>(v->pv_in, (int64_t)n_pairs));
+        size_t tmp_pairs = 0;
+        NXS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_pairs, v->pk_in.as<uint32_t>(),
+                                                 v->pk_out.as<uint32_t>(), v->pv_in.as<uint32_t>(),
+                                                 v->pv_ph[ph].as<uint32_t>(), (int)n_pairs, 0,
+                                                 tbits, s));
+        NXS_CUDA(v->temp.ensure(tmp_pairs));
+        // ---- K2b pairs (rank order), stable sort by tile, ranges
+        launch_emit_pairs(v->rects.as<int4>(), v->idx_out.as<uint32_t>(),
+                          v->offsets.as<unsigned long long>(), r0, r1, cam.tiles_x,
+                          v->active.as<uint8_t>(), v->pk_in.as<uint32_t>(), v->pv_in.as<uint32_t>(),
+                          s);
+        NXS_LAUNCHED("emit_pairs");
+        if (ph == 0) mark(v, 4, s);
+        size_t tb = v->temp.cap;
+        NXS_CUDA(cub::DeviceRadixSort::SortPairs(v->temp.p, tb, v->pk_in.as<uint32_t>(),
+                                                 v->pk_out.as<uint32_t>(), v->pv_in.as<uint32_t>(),
+                                                 v->pv_ph[ph].as<uint32_t>(), (int)n_pairs, 0,
+                                                 tbits, s));
+        if (ph == 0) mark(v, 5, s);
+        launch_tile_ranges(v->pk_out.as<uint32_t>(), (int64_t)n_pairs,
+                           v->ranges_ph[ph].as<int2>(), s);
+        NXS_LAUNCHED("tile_ranges");
+      } else if (ph == 0) {
+        mark(v, 4, s);
+        mark(v, 5, s);
+      }
+      if (ph == 0) mark(v, 6, s);
+      if (v->ev_ok) cudaEventRecord(v->evp[ph][3], s);
     }
-    if (ph == 0) mark(v, 6, s);
-    if (v->ev_ok) cudaEventRecord(v->evp[ph][3], s);
     if (ph == 1 || (ph == 0 && n_ph > 1)) {
       // forward carry between phases (allocated only when a second phase exists)
       NXS_CUDA(ensure_n<float>(v->r_rad, npix * 3));
@@ -916,6 +1123,11 @@ retry_sort:
   v->n_tiles = n_tiles;
   v->scene_centers = scene->centers;
   if (!v->spec_pending) v->phases_needed = ph_done;
+  if (v->lazy && !async0 && ph_done >= 1) {  // exact phase 0: sizes for the next call
+    v->est_n0 = R[1];
+    v->est_pairs = v->ph_pairs[0];
+    v->est_bin0 = ph_bin[0];
+  }
   return NXS_OK;
 }
 
@@ -1027,22 +1239,34 @@ int nxs_forward_backward(nxs_view* v, const nxs_scene* scene, const nxs_camera* 
     return rc;
   if (v->P == 0) return NXS_OK;
   const bool spec_check = v->spec_pending;
+  const bool async_check = v->async_pending;
   if (spec_check) {
-    // the active-tile count of the last forward kernel, read back right
-    // behind it; the host waits for the forward only, not for the backward
-    unsigned int* n_active = reinterpret_cast<unsigned int*>(v->dev_small.as<unsigned long long>() + 5);
-    NXS_CUDA(cudaMemcpyAsync(v->host_small + 3, n_active, sizeof(unsigned int),
-                             cudaMemcpyDeviceToHost, s));
-    NXS_CUDA(cudaEventRecord(v->ev_sync, s));
+    // the active-tile count of the last forward kernel (and, for a
+    // device-sized phase 0, its sizes), read back right behind it; the host
+    // waits for the forward only, not for the backward
+    if (async_check) {
+      if ((rc = enqueue_async_check(v, v->n_phases_plan, s))) return rc;
+    } else {
+      unsigned int* n_active =
+          reinterpret_cast<unsigned int*>(v->dev_small.as<unsigned long long>() + 5);
+      NXS_CUDA(cudaMemcpyAsync(v->host_small + 3, n_active, sizeof(unsigned int),
+                               cudaMemcpyDeviceToHost, s));
+      NXS_CUDA(cudaEventRecord(v->ev_sync, s));
+    }
   }
   if ((rc = backward_blend(v, seed, s))) return rc;
   if (spec_check) {
-    cudaError_t e;
-    while ((e = cudaEventQuery(v->ev_sync)) == cudaErrorNotReady) {
+    bool ok = true;
+    if (async_check) {
+      if ((rc = finish_async_check(v, ok))) return rc;
+    } else {
+      cudaError_t e;
+      while ((e = cudaEventQuery(v->ev_sync)) == cudaErrorNotReady) {
+      }
+      NXS_CUDA(e);
     }
-    NXS_CUDA(e);
     v->spec_pending = false;
-    if ((unsigned)v->host_small[3] != 0) {
+    if (!ok || (unsigned)v->host_small[3] != 0) {
       // more depth phases were needed: drop the moments, redo both passes
       if ((rc = backward_chain(v, scene, nullptr, nullptr, nullptr, nullptr, nullptr, s)))
         return rc;

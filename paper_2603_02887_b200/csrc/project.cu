@@ -218,7 +218,9 @@ __global__ void k_key32(const double* __restrict__ depth, int64_t P,
 // equal key >> shift, and the same re-sort makes the order exact.
 __global__ void k_key_fixup(const uint32_t* __restrict__ key, uint32_t* __restrict__ idx,
                             const double* __restrict__ depth, int64_t P, int shift,
-                            unsigned long long* __restrict__ overflow) {
+                            unsigned long long* __restrict__ overflow,
+                            const int* __restrict__ nd) {
+  if (nd) P = min(P, (int64_t)*nd);  // device-sized phase: real items only
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P) return;
   const uint32_t k = key[i] >> shift;
@@ -249,7 +251,8 @@ __global__ void k_key_fixup(const uint32_t* __restrict__ key, uint32_t* __restri
 }
 
 __global__ void k_rank_of(const uint32_t* __restrict__ order, int64_t r0, int64_t r1,
-                          uint32_t* __restrict__ rank_of) {
+                          uint32_t* __restrict__ rank_of, const int* __restrict__ nd) {
+  if (nd) r1 = min(r1, r0 + (int64_t)*nd);
   int64_t r = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r < r1) rank_of[order[r]] = (uint32_t)r;
 }
@@ -281,7 +284,9 @@ __global__ void k_key_hist(const uint32_t* __restrict__ key, int64_t P,
 __global__ void __launch_bounds__(1024) k_phase_select(const unsigned int* __restrict__ hist,
                                                        const int64_t* __restrict__ targets,
                                                        int n_targets, int64_t P,
-                                                       long long* __restrict__ out) {
+                                                       long long* __restrict__ out,
+                                                       int max_bin0,
+                                                       unsigned long long* __restrict__ overflow) {
   __shared__ unsigned long long cum[PH_BINS];
   __shared__ unsigned long long wsum[32];
   constexpr int PER = PH_BINS / 1024;
@@ -321,10 +326,13 @@ __global__ void __launch_bounds__(1024) k_phase_select(const unsigned int* __res
     }
     out[2 * t] = lo;
     out[2 * t + 1] = (long long)cum[lo];
+    // device-sized phase 0 sorted only the key bits below max_bin0's
+    if (t == 0 && max_bin0 >= 0 && lo > max_bin0) atomicAdd(overflow, 1ull);
   }
   if (t == 0) {
     out[2 * n_targets] = PH_BINS - 1;
     out[2 * n_targets + 1] = P;
+    if (n_targets == 0 && max_bin0 >= 0 && max_bin0 < PH_BINS - 1) atomicAdd(overflow, 1ull);
   }
 }
 
@@ -743,8 +751,9 @@ __global__ void __launch_bounds__(PROJ_CHUNK)
                     const float* __restrict__ quats, const float* __restrict__ opacities,
                     const float* __restrict__ sh, int C, int64_t r0, int64_t r1,
                     const uint32_t* __restrict__ order, CamDev cam, double cutoff,
-                    double near_plane, ProjOut out) {
+                    double near_plane, ProjOut out, const int* __restrict__ nd) {
   __shared__ ProjOutStage so;
+  if (nd) r1 = min(r1, r0 + (int64_t)*nd);
   const int tid = threadIdx.x, lane = tid & 31, wbase = tid & ~31;
   const int64_t r = r0 + (int64_t)blockIdx.x * PROJ_CHUNK + tid;
   if (r < r1) {
@@ -800,12 +809,17 @@ __global__ void k_count_active(const int4* __restrict__ rects, const uint32_t* _
                                int64_t r0, int64_t r1, int tiles_x,
                                const uint8_t* __restrict__ active,
                                const unsigned int* __restrict__ gate,
-                               unsigned long long* __restrict__ counts) {
+                               unsigned long long* __restrict__ counts,
+                               const int* __restrict__ nd) {
   // later phases: nothing to count when the previous forward left no tile
   // active (the host then stops before reading the counts)
   if (gate && *gate == 0u) return;
   const int64_t r = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= r1) return;
+  if (nd && r >= r0 + *nd) {  // device-sized phase: padding ranks count 0
+    counts[r - r0] = 0;
+    return;
+  }
   const int4 rc = rects[order[r]];
   unsigned long long n = 0;
   if (rc.x >= 0)
@@ -819,7 +833,9 @@ __global__ void k_count_active(const int4* __restrict__ rects, const uint32_t* _
 __global__ void k_emit_pairs(const int4* __restrict__ rects, const uint32_t* __restrict__ order,
                              const unsigned long long* __restrict__ offsets, int64_t r0,
                              int64_t r1, int tiles_x, const uint8_t* __restrict__ active,
-                             uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+                             uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                             const int* __restrict__ nd, unsigned long long cap) {
+  if (nd) r1 = min(r1, r0 + (int64_t)*nd);
   const int64_t r = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= r1) return;
   const int4 rc = rects[order[r]];
@@ -829,10 +845,27 @@ __global__ void k_emit_pairs(const int4* __restrict__ rects, const uint32_t* __r
     for (int tx = rc.x; tx <= rc.z; ++tx) {
       const int t = ty * tiles_x + tx;
       if (!active[t]) continue;
+      if (o >= cap) return;  // device-sized pair buffer too small (flagged by k_pairs_total)
       keys[o] = (uint32_t)t;
       vals[o] = (uint32_t)r;
       ++o;
     }
+}
+
+// device-sized binning: total pair count of the scan, the capacity check,
+// and max-key padding of the pair buffer beyond it
+__global__ void k_pairs_total(const unsigned long long* __restrict__ offsets,
+                              const unsigned long long* __restrict__ counts, int64_t n,
+                              unsigned long long cap, unsigned long long* __restrict__ total,
+                              unsigned long long* __restrict__ overflow) {
+  const unsigned long long t = n > 0 ? offsets[n - 1] + counts[n - 1] : 0ull;
+  *total = t;
+  if (t > cap) atomicAdd(overflow, 1ull);
+}
+__global__ void k_pad_keys(uint32_t* __restrict__ keys, int64_t cap,
+                           const unsigned long long* __restrict__ total) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < cap && (unsigned long long)i >= *total) keys[i] = 0xffffffffu;
 }
 
 __global__ void k_tile_ranges(const uint32_t* __restrict__ keys, int64_t n,
@@ -840,6 +873,7 @@ __global__ void k_tile_ranges(const uint32_t* __restrict__ keys, int64_t n,
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   uint32_t t = keys[i];
+  if (t == 0xffffffffu) return;  // padding of a device-sized pair buffer (sorted last)
   if (i == 0 || keys[i - 1] != t) ranges[t].x = (int)i;
   if (i == n - 1 || keys[i + 1] != t) ranges[t].y = (int)(i + 1);
 }
@@ -859,9 +893,10 @@ void launch_key32(const double* depth, int64_t P, const unsigned long long* kmin
   k_key32<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(depth, P, kminmax, key);
 }
 void launch_key_fixup(const uint32_t* key, uint32_t* idx, const double* depth, int64_t P,
-                      unsigned long long* overflow, cudaStream_t s, int shift) {
+                      unsigned long long* overflow, cudaStream_t s, int shift, const int* nd) {
   if (P == 0) return;
-  k_key_fixup<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(key, idx, depth, P, shift, overflow);
+  k_key_fixup<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(key, idx, depth, P, shift, overflow,
+                                                          nd);
 }
 void launch_chunk_key(const float* centers, const float* scales, const float* quats,
                       const float* opacities, int64_t P, const CamDev& cam, double cutoff,
@@ -889,17 +924,29 @@ bool launch_chunk_sort(const uint32_t* order_c, const double* zlo, int64_t P, in
 }
 void launch_rank_of(const uint32_t* order, int64_t P, uint32_t* rank_of, cudaStream_t s) {
   if (P == 0) return;
-  k_rank_of<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(order, 0, P, rank_of);
+  k_rank_of<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(order, 0, P, rank_of, nullptr);
 }
 void launch_rank_of_range(const uint32_t* order, int64_t r0, int64_t r1, uint32_t* rank_of,
-                          cudaStream_t s) {
+                          cudaStream_t s, const int* nd) {
   if (r1 <= r0) return;
-  k_rank_of<<<(unsigned)((r1 - r0 + 255) / 256), 256, 0, s>>>(order, r0, r1, rank_of);
+  k_rank_of<<<(unsigned)((r1 - r0 + 255) / 256), 256, 0, s>>>(order, r0, r1, rank_of, nd);
 }
 __global__ void k_gather_keys(const uint32_t* __restrict__ idx, const uint32_t* __restrict__ key,
                               int64_t n, uint32_t* __restrict__ out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = key[idx[i]];
+}
+__global__ void k_gather_keys_pad(uint32_t* __restrict__ idx, const uint32_t* __restrict__ key,
+                                  const int* __restrict__ nd, int64_t cap,
+                                  uint32_t* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= cap) return;
+  if (i < *nd) {
+    out[i] = key[idx[i]];
+  } else {  // padding: sorts after every real key (max key, max index)
+    out[i] = 0xffffffffu;
+    idx[i] = 0xffffffffu;
+  }
 }
 __global__ void k_clear_rects(const uint32_t* __restrict__ order, int64_t r0, int64_t r1,
                               int4* __restrict__ rects) {
@@ -919,6 +966,11 @@ void launch_gather_keys(const uint32_t* idx, const uint32_t* key, int64_t n, uin
   if (n <= 0) return;
   k_gather_keys<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(idx, key, n, out);
 }
+void launch_gather_keys_pad(uint32_t* idx, const uint32_t* key, const int* nd, int64_t cap,
+                            uint32_t* out, cudaStream_t s) {
+  if (cap <= 0) return;
+  k_gather_keys_pad<<<(unsigned)((cap + 255) / 256), 256, 0, s>>>(idx, key, nd, cap, out);
+}
 void launch_clear_rects(const uint32_t* order, int64_t r0, int64_t r1, int4* rects,
                         cudaStream_t s) {
   if (r1 <= r0) return;
@@ -934,18 +986,19 @@ void launch_key_hist(const uint32_t* key, int64_t P, unsigned int* hist, cudaStr
   k_key_hist<<<grid, 1024, 0, s>>>(key, P, hist);
 }
 void launch_phase_select(const unsigned int* hist, const int64_t* targets, int n_targets,
-                         int64_t P, long long* out, cudaStream_t s) {
-  k_phase_select<<<1, 1024, 0, s>>>(hist, targets, n_targets, P, out);
+                         int64_t P, long long* out, cudaStream_t s, int max_bin0,
+                         unsigned long long* overflow) {
+  k_phase_select<<<1, 1024, 0, s>>>(hist, targets, n_targets, P, out, max_bin0, overflow);
 }
 void launch_project_ranks(const float* centers, const float* scales, const float* quats,
                           const float* opacities, const float* sh, int C, int64_t r0, int64_t r1,
                           const uint32_t* order, const CamDev& cam, double cutoff,
                           double near_plane, int4* rects, float4* records, float4* bframe,
-                          unsigned long long* straddle, cudaStream_t s) {
+                          unsigned long long* straddle, cudaStream_t s, const int* nd) {
   if (r1 <= r0) return;
   ProjOut o{nullptr, nullptr, rects, records, bframe, straddle};
   k_project_ranks<<<(unsigned)((r1 - r0 + PROJ_CHUNK - 1) / PROJ_CHUNK), PROJ_CHUNK, 0, s>>>(
-      centers, scales, quats, opacities, sh, C, r0, r1, order, cam, cutoff, near_plane, o);
+      centers, scales, quats, opacities, sh, C, r0, r1, order, cam, cutoff, near_plane, o, nd);
 }
 
 void launch_project(const float* centers, const float* scales, const float* quats,
@@ -966,18 +1019,28 @@ void launch_project(const float* centers, const float* scales, const float* quat
 
 void launch_count_active(const int4* rects, const uint32_t* order, int64_t r0, int64_t r1,
                          int tiles_x, const uint8_t* active, const unsigned int* gate,
-                         unsigned long long* counts, cudaStream_t s) {
+                         unsigned long long* counts, cudaStream_t s, const int* nd) {
   if (r1 <= r0) return;
   k_count_active<<<(unsigned)((r1 - r0 + 255) / 256), 256, 0, s>>>(rects, order, r0, r1, tiles_x,
-                                                                   active, gate, counts);
+                                                                   active, gate, counts, nd);
 }
 
 void launch_emit_pairs(const int4* rects, const uint32_t* order, const unsigned long long* offsets,
                        int64_t r0, int64_t r1, int tiles_x, const uint8_t* active, uint32_t* keys,
-                       uint32_t* vals, cudaStream_t s) {
+                       uint32_t* vals, cudaStream_t s, const int* nd, unsigned long long cap) {
   if (r1 <= r0) return;
-  k_emit_pairs<<<(unsigned)((r1 - r0 + 255) / 256), 256, 0, s>>>(rects, order, offsets, r0, r1,
-                                                                 tiles_x, active, keys, vals);
+  k_emit_pairs<<<(unsigned)((r1 - r0 + 255) / 256), 256, 0, s>>>(
+      rects, order, offsets, r0, r1, tiles_x, active, keys, vals, nd, cap);
+}
+void launch_pairs_total(const unsigned long long* offsets, const unsigned long long* counts,
+                        int64_t n, unsigned long long cap, unsigned long long* total,
+                        unsigned long long* overflow, cudaStream_t s) {
+  k_pairs_total<<<1, 1, 0, s>>>(offsets, counts, n, cap, total, overflow);
+}
+void launch_pad_keys(uint32_t* keys, int64_t cap, const unsigned long long* total,
+                     cudaStream_t s) {
+  if (cap <= 0) return;
+  k_pad_keys<<<(unsigned)((cap + 255) / 256), 256, 0, s>>>(keys, cap, total);
 }
 
 void launch_tile_ranges(const uint32_t* keys, int64_t n, int2* ranges, cudaStream_t s) {

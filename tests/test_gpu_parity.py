@@ -613,3 +613,41 @@ def test_fused_forward_backward_matches_separate_calls():
         for k in GRAD_FIELDS:
             np.testing.assert_allclose(f_g[k].cpu().numpy(), r_g[k].cpu().numpy(), rtol=1e-5,
                                        atol=1e-7 * float(r_g[k].abs().max()), err_msg=k)
+
+
+def test_device_sized_first_phase_matches_fresh_views():
+    """A view sizes its first depth phase from its previous call (no host
+    sync before the first forward) and verifies behind it.  Repeated calls
+    on one view — same camera, a camera needing more pairs, a larger scene,
+    a different model — must equal fresh-view results bit for bit."""
+    import torch
+    from paper_2603_02887_b200 import (_native, backward_device, forward_backward_device,
+                                       forward_device)
+    sc_a = O.round_scene_f32(O.canonical_scene(60_000, seed=2))
+    sc_b = O.round_scene_f32(O.canonical_scene(90_000, seed=3))
+    cams = [O.canonical_camera(320, 240, v, 8) for v in (0, 0, 3)]
+    wide = O.look_at([0, 0, -1.0], [0, 0, 4.0], [0, 1, 0], 80.0, 320, 240)  # many more pairs
+    seed = torch.as_tensor(O.canonical_seed(320, 240, 0), dtype=torch.float32).cuda()
+    dev_a, dev_b = _dev(sc_a), _dev(sc_b)
+    plan = [(dev_a, cams[0], "softplus_20"), (dev_a, cams[1], "softplus_20"),
+            (dev_a, wide, "softplus_20"), (dev_a, cams[2], "softplus_20"),
+            (dev_b, cams[2], "softplus_20"), (dev_b, cams[2], "linear"),
+            (dev_a, cams[0], "exponential"), (dev_a, cams[0], "softplus_20")]
+    for fused in (False, True):
+        view = _native.View()
+        for dev, cam, name in plan:
+            model = MODELS[name]
+            ref_view = _native.View()
+            r_out = forward_device(ref_view, dev, cam, model, np.zeros(3))
+            r_g = backward_device(ref_view, dev, seed)
+            if fused:
+                out, g = forward_backward_device(view, dev, cam, model, np.zeros(3), seed)
+            else:
+                out = forward_device(view, dev, cam, model, np.zeros(3))
+                g = backward_device(view, dev, seed)
+            for a, b in zip(r_out, out):
+                assert torch.equal(a, b), (fused, name)
+            for k in GRAD_FIELDS:
+                np.testing.assert_allclose(g[k].cpu().numpy(), r_g[k].cpu().numpy(), rtol=1e-5,
+                                           atol=1e-7 * float(r_g[k].abs().max()), err_msg=k)
+            assert view.stats()["n_pairs"] == ref_view.stats()["n_pairs"], (fused, name)
