@@ -192,6 +192,9 @@ struct nxs_view {
   int64_t est_n0 = 0, est_pairs = 0;
   int est_bin0 = -1;
   bool async_pending = false;  // phase 0 ran device-sized, not yet verified
+  cudaGraphExec_t gexec = nullptr;  // the device-sized phase 0, replayed as one graph
+  cudaStream_t cap_stream = nullptr;  // capture happens on this (non-default) stream
+  bool capturing = false;
   int n_phases_plan = 0;       // planned depth phases of the last forward
   int64_t async_cap0 = 0, async_capp = 0;
   int64_t sorted_end = 0, proj_end = 0;
@@ -219,6 +222,8 @@ struct nxs_view {
     for_each_buf([](Buf& b) { b.release(); });
     if (host_small) cudaFreeHost(host_small);
     if (ev_sync) cudaEventDestroy(ev_sync);
+    if (gexec) cudaGraphExecDestroy(gexec);
+    if (cap_stream) cudaStreamDestroy(cap_stream);
     if (ev_ok) {
       for (auto& e : ev) cudaEventDestroy(e);
       for (auto& row : evp)
@@ -299,6 +304,26 @@ int make_camera(const nxs_camera* c, CamDev& cd) {
   return NXS_OK;
 }
 
+// Stream capture of the device-sized first phase: its ~30 launches (sort,
+// projection, binning, forward) run as one CUDA graph, which removes the
+// per-launch gaps between the many short kernels.  The host code runs as
+// usual every call (all host-side state stays current); only the launches
+// are recorded, and the executable graph is updated in place.
+struct CaptureGuard {
+  cudaStream_t s = nullptr;
+  bool on = false;
+  bool* flag = nullptr;
+  ~CaptureGuard() {  // an error path left the capture open: close and drop it
+    if (flag) *flag = false;
+    if (on) {
+      cudaGraph_t g = nullptr;
+      cudaStreamEndCapture(s, &g);
+      if (g) cudaGraphDestroy(g);
+      cudaGetLastError();
+    }
+  }
+};
+
 // Wait for the stream by polling an event: the syncs inside the pipeline
 // (pair counts, phase sizes) sit between kernels, and a blocking wait's
 // wake-up latency would leave the GPU idle; fall back to blocking if no
@@ -312,8 +337,17 @@ cudaError_t spin_sync(nxs_view* v, cudaStream_t s) {
   return e;
 }
 
+// timing events: inside a stream capture they must be external event
+// nodes to stay observable from the host
+inline void rec_event(nxs_view* v, cudaEvent_t e, cudaStream_t s) {
+  if (v->capturing)
+    cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+  else
+    cudaEventRecord(e, s);
+}
+
 inline void mark(nxs_view* v, int i, cudaStream_t s) {
-  if (v->ev_ok) cudaEventRecord(v->ev[i], s);
+  if (v->ev_ok) rec_event(v, v->ev[i], s);
 }
 
 template <class T>
@@ -609,6 +643,9 @@ int forward_impl(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
   const int n_ph_plan = n_ph;
   for (int i = 0; i <= n_ph; ++i) Rplan[i] = R[i];
   int ph_bin[MAX_PHASES] = {0, 0, 0, 0};  // last key bin of each lazy phase
+  CaptureGuard cap;
+  cap.flag = &v->capturing;
+  const cudaStream_t s_caller = s;
   // device-sized phase 0 (no host sync before the first forward): needs
   // estimates from this view's previous call and a later phase to verify at
   bool async0 = v->est_n0 > 0 && v->est_pairs >= 0 && v->est_bin0 >= 0 && n_ph >= 2 &&
@@ -618,6 +655,16 @@ int forward_impl(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
 retry_sort:
   if (sort64) async0 = false;
   v->async_pending = false;
+  if (async0 && !getenv("NXS_NO_GRAPH")) {
+    // record on the view's own stream (the caller's may be the legacy default
+    // stream, which cannot capture); the graph is launched on the caller's
+    if (!v->cap_stream) NXS_CUDA(cudaStreamCreateWithFlags(&v->cap_stream, cudaStreamNonBlocking));
+    s = v->cap_stream;
+    NXS_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+    cap.s = s;
+    cap.on = true;
+    v->capturing = true;
+  }
   n_ph = n_ph_plan;
   for (int i = 0; i <= n_ph; ++i) R[i] = Rplan[i];
   v->lazy = !torder && !sort64 && !(opts->flags & NXS_FLAG_FULL_BINNING) && P > 0;
@@ -783,7 +830,7 @@ retry_sort:
   int ph_done = 0;
   for (int ph = 0; ph < n_ph; ++ph) {
     int64_t r0 = R[ph], r1 = R[ph + 1], nr = r1 - r0;
-    if (v->ev_ok) cudaEventRecord(v->evp[ph][0], s);
+    if (v->ev_ok) rec_event(v, v->evp[ph][0], s);
     if (v->async_pending && ph > 0 && ph != spec_phase) {
       // verify the device-sized phase 0 and learn the real phase bounds
       bool ok = false;
@@ -845,13 +892,13 @@ retry_sort:
       launch_rank_of_range(v->idx_out.as<uint32_t>(), 0, cap0, v->rank_of.as<uint32_t>(), s,
                            n_sel);
       NXS_LAUNCHED("rank_of");
-      if (v->ev_ok) cudaEventRecord(v->evp[0][1], s);
+      if (v->ev_ok) rec_event(v, v->evp[0][1], s);
       launch_project_ranks(scene->centers, scene->scales, scene->quats, scene->opacities,
                            scene->sh, C, 0, cap0, v->idx_out.as<uint32_t>(), cam,
                            opts->alpha_cutoff, opts->near_plane, v->rects.as<int4>(),
                            v->records.as<float4>(), v->bframe.as<float4>(), dsmall, s, n_sel);
       NXS_LAUNCHED("project_ranks");
-      if (v->ev_ok) cudaEventRecord(v->evp[0][2], s);
+      if (v->ev_ok) rec_event(v, v->evp[0][2], s);
       launch_count_active(v->rects.as<int4>(), v->idx_out.as<uint32_t>(), 0, cap0, cam.tiles_x,
                           v->active.as<uint8_t>(), nullptr, v->ntiles.as<unsigned long long>(),
                           s, n_sel);
@@ -894,7 +941,7 @@ retry_sort:
       launch_tile_ranges(v->pk_out.as<uint32_t>(), capp, v->ranges_ph[0].as<int2>(), s);
       NXS_LAUNCHED("tile_ranges");
       mark(v, 6, s);
-      if (v->ev_ok) cudaEventRecord(v->evp[0][3], s);
+      if (v->ev_ok) rec_event(v, v->evp[0][3], s);
       v->async_pending = true;
       v->ph_pairs[0] = capp;  // capacity; the real count comes with the check
     } else {
@@ -946,7 +993,7 @@ retry_sort:
           NXS_LAUNCHED("rank_of");
           v->sorted_end = r1;
           v->bin_done = hi;
-          if (v->ev_ok) cudaEventRecord(v->evp[ph][1], s);
+          if (v->ev_ok) rec_event(v, v->evp[ph][1], s);
           launch_project_ranks(scene->centers, scene->scales, scene->quats, scene->opacities,
                                scene->sh, C, r0, r1, v->idx_out.as<uint32_t>(), cam,
                                opts->alpha_cutoff, opts->near_plane, v->rects.as<int4>(),
@@ -954,12 +1001,12 @@ retry_sort:
           NXS_LAUNCHED("project_ranks");
           v->proj_end = r1;
         } else if (v->ev_ok) {
-          cudaEventRecord(v->evp[ph][1], s);
+          rec_event(v, v->evp[ph][1], s);
         }
-        if (v->ev_ok) cudaEventRecord(v->evp[ph][2], s);
+        if (v->ev_ok) rec_event(v, v->evp[ph][2], s);
       } else if (v->ev_ok) {
-        cudaEventRecord(v->evp[ph][1], s);
-        cudaEventRecord(v->evp[ph][2], s);
+        rec_event(v, v->evp[ph][1], s);
+        rec_event(v, v->evp[ph][2], s);
       }
       // ---- K2a counts over active tiles, scan, one host sync for the pair count
       if (nr > 0) {
@@ -1041,7 +1088,7 @@ retry_sort:
         mark(v, 5, s);
       }
       if (ph == 0) mark(v, 6, s);
-      if (v->ev_ok) cudaEventRecord(v->evp[ph][3], s);
+      if (v->ev_ok) rec_event(v, v->evp[ph][3], s);
     }
     if (ph == 1 || (ph == 0 && n_ph > 1)) {
       // forward carry between phases (allocated only when a second phase exists)
@@ -1065,7 +1112,7 @@ retry_sort:
                   (chunked && !(opts->flags & NXS_FLAG_XBUF32)) ? 16 : 32};
       launch_blend_fwd_x(count, n_tiles, xa, cam, md, v->cache(), v->resume(), cnt, s);
       NXS_LAUNCHED("blend_fwd_x");
-      if (v->ev_ok) cudaEventRecord(v->evp[ph][4], s);
+      if (v->ev_ok) rec_event(v, v->evp[ph][4], s);
       ph_done = ph + 1;
       continue;
     }
@@ -1078,8 +1125,29 @@ retry_sort:
                rgb, overdraw, residual};
     launch_blend_fwd(count, n_tiles, fa, cam, md, v->cache(), v->resume(), cnt, s);
     NXS_LAUNCHED("blend_fwd");
-    if (v->ev_ok) cudaEventRecord(v->evp[ph][4], s);
+    if (v->ev_ok) rec_event(v, v->evp[ph][4], s);
     ph_done = ph + 1;
+    if (cap.on && ph == 0) {
+      cudaGraph_t g = nullptr;
+      cap.on = false;
+      v->capturing = false;
+      NXS_CUDA(cudaStreamEndCapture(s, &g));
+      s = s_caller;
+      cudaGraphExecUpdateResultInfo info;
+      if (!v->gexec || cudaGraphExecUpdate(v->gexec, g, &info) != cudaSuccess) {
+        cudaGetLastError();
+        if (v->gexec) cudaGraphExecDestroy(v->gexec);
+        v->gexec = nullptr;
+        const cudaError_t e = cudaGraphInstantiate(&v->gexec, g, 0);
+        if (e != cudaSuccess) {
+          cudaGraphDestroy(g);
+          v->gexec = nullptr;
+          return fail(NXS_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+        }
+      }
+      cudaGraphDestroy(g);
+      NXS_CUDA(cudaGraphLaunch(v->gexec, s));
+    }
   }
   mark(v, 7, s);
   v->ev_fwd = true;
