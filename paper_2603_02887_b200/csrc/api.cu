@@ -46,6 +46,8 @@ void launch_pad_keys(uint32_t*, int64_t, const unsigned long long*, cudaStream_t
 void launch_gather_keys(const uint32_t*, const uint32_t*, int64_t, uint32_t*, cudaStream_t);
 void launch_clear_rects(const uint32_t*, int64_t, int64_t, int4*, cudaStream_t);
 void launch_iota(uint32_t*, int64_t, cudaStream_t);
+void launch_pack_check(const unsigned long long*, const long long*, int, unsigned long long*,
+                       cudaStream_t);
 void launch_chunk_key(const float*, const float*, const float*, const float*, int64_t,
                       const CamDev&, double, const uint32_t*, int, double*, unsigned long long*,
                       uint32_t*, cudaStream_t);
@@ -488,17 +490,13 @@ namespace {
 // enqueue_async_check; finish_async_check waits for them: ok == false means
 // some capacity was exceeded and the pass must be redone with exact sizes.
 int enqueue_async_check(nxs_view* v, int n_ph, cudaStream_t s) {
+  // one small kernel packs the values into host_small's layout, one copy
   unsigned long long* dsmall = v->dev_small.as<unsigned long long>();
   long long* dsel = v->ph_sel.as<long long>();
-  v->host_small[24] = 0;
-  NXS_CUDA(cudaMemcpyAsync(v->host_small + 3, dsmall + 5, sizeof(unsigned int),
-                           cudaMemcpyDeviceToHost, s));
-  NXS_CUDA(cudaMemcpyAsync(v->host_small + 16, dsel, sizeof(long long) * 2 * n_ph,
-                           cudaMemcpyDeviceToHost, s));
-  NXS_CUDA(cudaMemcpyAsync(v->host_small + 24, dsel + 48, sizeof(int), cudaMemcpyDeviceToHost, s));
-  NXS_CUDA(cudaMemcpyAsync(v->host_small + 25, dsmall + 10, 2 * sizeof(unsigned long long),
-                           cudaMemcpyDeviceToHost, s));
-  NXS_CUDA(cudaMemcpyAsync(v->host_small + 2, dsmall, sizeof(unsigned long long),
+  unsigned long long* pack = reinterpret_cast<unsigned long long*>(dsel + 56);
+  launch_pack_check(dsmall, dsel, n_ph, pack, s);
+  NXS_LAUNCHED("pack_check");
+  NXS_CUDA(cudaMemcpyAsync(v->host_small, pack, 27 * sizeof(unsigned long long),
                            cudaMemcpyDeviceToHost, s));
   NXS_CUDA(cudaEventRecord(v->ev_sync, s));
   return NXS_OK;
@@ -720,7 +718,7 @@ retry_sort:
       launch_key32(v->depth.as<double>(), P, dsmall + 6, v->k32a.as<uint32_t>(), s);
       NXS_LAUNCHED("key32");
       NXS_CUDA(v->ph_hist.ensure(4096 * sizeof(unsigned int)));
-      NXS_CUDA(v->ph_sel.ensure(64 * sizeof(long long)));
+      NXS_CUDA(v->ph_sel.ensure(96 * sizeof(long long)));
       launch_key_hist(v->k32a.as<uint32_t>(), P, v->ph_hist.as<unsigned int>(), s);
       NXS_LAUNCHED("key_hist");
       int64_t* tgt = reinterpret_cast<int64_t*>(v->host_small + 8);

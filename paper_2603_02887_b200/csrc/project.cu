@@ -957,6 +957,27 @@ __global__ void k_iota(uint32_t* __restrict__ a, int64_t n) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) a[i] = (uint32_t)i;
 }
+// the device-sized phase-0 check, packed in host_small's layout:
+// [2] straddle, [3] active tiles, [16..) phase bounds, [24] phase-0
+// Gaussians, [25] overflow flags, [26] pair total
+__global__ void k_pack_check(const unsigned long long* __restrict__ dsmall,
+                             const long long* __restrict__ dsel, int n_ph,
+                             unsigned long long* __restrict__ out) {
+  const int i = threadIdx.x;
+  if (i >= 27) return;
+  unsigned long long v = 0ull;
+  if (i == 2) v = dsmall[0];
+  else if (i == 3) v = (unsigned int)(dsmall[5] & 0xffffffffull);
+  else if (i >= 16 && i < 16 + 2 * n_ph) v = (unsigned long long)dsel[i - 16];
+  else if (i == 24) v = (unsigned int)*reinterpret_cast<const int*>(dsel + 48);
+  else if (i == 25) v = dsmall[10];
+  else if (i == 26) v = dsmall[11];
+  out[i] = v;
+}
+void launch_pack_check(const unsigned long long* dsmall, const long long* dsel, int n_ph,
+                       unsigned long long* out, cudaStream_t s) {
+  k_pack_check<<<1, 32, 0, s>>>(dsmall, dsel, n_ph, out);
+}
 void launch_iota(uint32_t* a, int64_t n, cudaStream_t s) {
   if (n <= 0) return;
   k_iota<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a, n);
