@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "../../include/nxs.h"
 #include "nxs_internal.cuh"
@@ -653,6 +654,45 @@ int forward_impl(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
 retry_sort:
   if (sort64) async0 = false;
   v->async_pending = false;
+  if (async0) {
+    // every buffer the device-sized phase 0 touches is sized up front: no
+    // allocation may move a buffer once its pointer is in the captured graph
+    const int64_t cap0 = std::min<int64_t>(P, v->est_n0 + v->est_n0 / 8 + 2048);
+    const int64_t capp = v->est_pairs + v->est_pairs / 8 + 8192;
+    const int tbits_pad = bits_for((uint32_t)n_tiles + 1);
+    size_t t_sort = 0, t_scan = 0, t_pairs = 0, t_sel = 0, t_full = 0;
+    NXS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t_full, v->k32a.as<uint32_t>(),
+                                             v->k32b.as<uint32_t>(), v->idx_in.as<uint32_t>(),
+                                             v->idx_out.as<uint32_t>(), (int)P, 0, 32, s));
+    NXS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t_sort, v->k32c.as<uint32_t>(),
+                                             v->k32b.as<uint32_t>(), v->idx_in.as<uint32_t>(),
+                                             v->idx_out.as<uint32_t>(), (int)cap0, 0, 32, s));
+    NXS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t_scan, v->ntiles.as<unsigned long long>(),
+                                           v->offsets.as<unsigned long long>(), (int)P, s));
+    NXS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t_pairs, v->pk_in.as<uint32_t>(),
+                                             v->pk_out.as<uint32_t>(), v->pv_in.as<uint32_t>(),
+                                             v->pv_ph[0].as<uint32_t>(), (int)capp, 0, tbits_pad,
+                                             s));
+    NXS_CUDA(cub::DeviceSelect::If(nullptr, t_sel, cub::CountingInputIterator<uint32_t>(0),
+                                   v->idx_in.as<uint32_t>(), v->ph_sel.as<int>(), (int)P,
+                                   BinRange{nullptr, 0, 0}, s));
+    NXS_CUDA(v->temp.ensure(std::max({t_full, t_sort, t_scan, t_pairs, t_sel})));
+    NXS_CUDA(v->ph_hist.ensure(4096 * sizeof(unsigned int)));
+    NXS_CUDA(v->ph_sel.ensure(96 * sizeof(long long)));
+    NXS_CUDA(ensure_n<uint32_t>(v->k32c, P));
+    NXS_CUDA(ensure_n<uint32_t>(v->pv_ph[0], capp));
+    NXS_CUDA(ensure_n<uint32_t>(v->pk_in, capp));
+    NXS_CUDA(ensure_n<uint32_t>(v->pk_out, capp));
+    NXS_CUDA(ensure_n<uint32_t>(v->pv_in, capp));
+    NXS_CUDA(ensure_n<int2>(v->ranges_ph[0], n_tiles));
+    NXS_CUDA(ensure_n<int32_t>(v->cum_ph[0], n_tiles));
+    NXS_CUDA(ensure_n<int32_t>(v->cum_ph[1], n_tiles));
+    NXS_CUDA(ensure_n<float>(v->r_rad, npix * 3));
+    NXS_CUDA(ensure_n<float>(v->r_trem, npix));
+    NXS_CUDA(ensure_n<int32_t>(v->r_count, npix));
+    NXS_CUDA(ensure_n<float>(v->r_sea, npix * 3));
+    NXS_CUDA(ensure_n<float>(v->r_sa, npix));
+  }
   if (async0 && !getenv("NXS_NO_GRAPH")) {
     // record on the view's own stream (the caller's may be the legacy default
     // stream, which cannot capture); the graph is launched on the caller's

@@ -632,7 +632,9 @@ def test_device_sized_first_phase_matches_fresh_views():
     plan = [(dev_a, cams[0], "softplus_20"), (dev_a, cams[1], "softplus_20"),
             (dev_a, wide, "softplus_20"), (dev_a, cams[2], "softplus_20"),
             (dev_b, cams[2], "softplus_20"), (dev_b, cams[2], "linear"),
-            (dev_a, cams[0], "exponential"), (dev_a, cams[0], "softplus_20")]
+            (dev_a, cams[0], "exponential"), (dev_a, cams[0], "exponential"),
+            (dev_a, cams[0], "exponential"), (dev_a, cams[0], "softplus_20"),
+            (dev_a, cams[0], "softplus_20")]
     for fused in (False, True):
         view = _native.View()
         for dev, cam, name in plan:
