@@ -89,6 +89,41 @@ static void msort(uint32_t* idx, uint32_t* tmp, const uint64_t* key, int64_t n) 
   }
 }
 
+/* Exact tile culling (csrc/project.cu tile_hit): does the silhouette
+ * ellipse q(X, Y) = Hᵀ Q H <= 0 meet the tile's pixel-centre rectangle?
+ * t = (q00, q01, q11, q02, q12, q22, c0, c1), c = the projected centre (inside). */
+static int tile_hit(const double* t, int tx, int ty, double cx, double cy, double f, int W,
+                    int H) {
+  const double q00 = t[0];
+  if (!(q00 == q00)) return 1;
+  const double q01 = t[1], q11 = t[2], q02 = t[3], q12 = t[4], q22 = t[5];
+  const double c0 = t[6], c1 = t[7], h00 = t[8], h11 = t[9];
+  const int jx0 = tx * TILE, iy0 = ty * TILE;
+  const int jx1 = jx0 + TILE - 1 < W - 1 ? jx0 + TILE - 1 : W - 1;
+  const int iy1 = iy0 + TILE - 1 < H - 1 ? iy0 + TILE - 1 : H - 1;
+  const double inv_f = 1.0 / f;
+  const double x0 = (((double)jx0 + 0.5) - cx) * inv_f, x1 = (((double)jx1 + 0.5) - cx) * inv_f;
+  const double y0 = (((double)iy0 + 0.5) - cy) * inv_f, y1 = (((double)iy1 + 0.5) - cy) * inv_f;
+  if (c0 >= x0 && c0 <= x1 && c1 >= y0 && c1 <= y1) return 1;
+  for (int k = 0; k < 2; ++k) {
+    const double xe = k ? x1 : x0;
+    const double b = 2.0 * (q01 * xe + q12);
+    const double c = (q00 * xe * xe + 2.0 * q02 * xe) + q22;
+    double yv = -b * h11;
+    yv = yv < y0 ? y0 : (yv > y1 ? y1 : yv);
+    if ((q11 * yv + b) * yv + c <= 0.0) return 1;
+  }
+  for (int k = 0; k < 2; ++k) {
+    const double ye = k ? y1 : y0;
+    const double b = 2.0 * (q01 * ye + q02);
+    const double c = (q11 * ye * ye + 2.0 * q12 * ye) + q22;
+    double xv = -b * h00;
+    xv = xv < x0 ? x0 : (xv > x1 ? x1 : xv);
+    if ((q00 * xv + b) * xv + c <= 0.0) return 1;
+  }
+  return 0;
+}
+
 /*
  * Outputs (caller-allocated):
  *   order[P]       rank -> Gaussian index
@@ -119,6 +154,7 @@ int64_t nxs_oracle_binning(int64_t P, const float* centers, const float* scales,
   }
   msort(idx, tmp, key, P);
   int64_t* count = (int64_t*)calloc((size_t)(P > 0 ? P : 1), sizeof(int64_t));
+  double* tq = (double*)malloc(sizeof(double) * 10 * (size_t)(P > 0 ? P : 1));
   for (int64_t r = 0; r < P; ++r) {
     const int64_t g = idx[r];
     order[r] = (int32_t)g;
@@ -191,7 +227,8 @@ int64_t nxs_oracle_binning(int64_t P, const float* centers, const float* scales,
       double dx = S02 * S02 - S00 * S22;
       double dy = S12 * S12 - S11 * S22;
       double jlo = 0.0, jhi = (double)(W - 1), ilo = 0.0, ihi = (double)(H - 1);
-      if ((dx >= 0.0) && (dy >= 0.0) && (S22 != 0.0)) {
+      const int ok = (dx >= 0.0) && (dy >= 0.0) && (S22 != 0.0);
+      if (ok) {
         double sx = sqrt(dx), sy = sqrt(dy);
         double iS = 1.0 / S22;
         double x1 = (S02 - sx) * iS, x2 = (S02 + sx) * iS;
@@ -205,13 +242,29 @@ int64_t nxs_oracle_binning(int64_t P, const float* centers, const float* scales,
         if (pil > ilo) ilo = pil;
         if (pih < ihi) ihi = pih;
       }
+      tq[10 * r] = NAN;
       if (jlo <= jhi && ilo <= ihi) {
         int j0 = (int)jlo, j1 = (int)jhi, i0 = (int)ilo, i1 = (int)ihi;
         rect[0] = j0 / TILE;
         rect[1] = i0 / TILE;
         rect[2] = j1 / TILE;
         rect[3] = i1 / TILE;
-        ntile = (int64_t)(rect[2] - rect[0] + 1) * (int64_t)(rect[3] - rect[1] + 1);
+        if (ok) {
+          double* t = tq + 10 * r;
+          t[0] = Q[0];
+          t[1] = Q[1];
+          t[2] = Q[4];
+          t[3] = Q[2];
+          t[4] = Q[5];
+          t[5] = Q[8];
+          t[6] = bp[0] * ibz;
+          t[7] = bp[1] * ibz;
+          t[8] = 0.5 / Q[0];
+          t[9] = 0.5 / Q[4];
+        }
+        for (int ty = rect[1]; ty <= rect[3]; ++ty)
+          for (int tx = rect[0]; tx <= rect[2]; ++tx)
+            ntile += tile_hit(tq + 10 * r, tx, ty, cx, cy, f, W, H);
       }
     }
     float* rec = records + r * 32;
@@ -237,7 +290,8 @@ int64_t nxs_oracle_binning(int64_t P, const float* centers, const float* scales,
     const int32_t* rc = rects + 4 * r;
     if (rc[0] < 0) continue;
     for (int ty = rc[1]; ty <= rc[3]; ++ty)
-      for (int tx = rc[0]; tx <= rc[2]; ++tx) tcount[ty * tiles_x + tx + 1]++;
+      for (int tx = rc[0]; tx <= rc[2]; ++tx)
+        if (tile_hit(tq + 10 * r, tx, ty, cx, cy, f, W, H)) tcount[ty * tiles_x + tx + 1]++;
   }
   for (int t = 0; t < T; ++t) tcount[t + 1] += tcount[t];
   for (int t = 0; t < T; ++t) {
@@ -253,12 +307,15 @@ int64_t nxs_oracle_binning(int64_t P, const float* centers, const float* scales,
       const int32_t* rc = rects + 4 * r;
       if (rc[0] < 0) continue;
       for (int ty = rc[1]; ty <= rc[3]; ++ty)
-        for (int tx = rc[0]; tx <= rc[2]; ++tx) pairs[fill[ty * tiles_x + tx]++] = (int32_t)r;
+        for (int tx = rc[0]; tx <= rc[2]; ++tx)
+          if (tile_hit(tq + 10 * r, tx, ty, cx, cy, f, W, H))
+            pairs[fill[ty * tiles_x + tx]++] = (int32_t)r;
     }
     free(fill);
   }
   free(tcount);
   free(count);
+  free(tq);
   free(key);
   free(idx);
   free(tmp);

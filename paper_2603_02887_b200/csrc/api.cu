@@ -36,7 +36,7 @@ void launch_phase_select(const unsigned int*, const int64_t*, int, int64_t, long
                          cudaStream_t, int max_bin0 = -1, unsigned long long* overflow = nullptr);
 void launch_project_ranks(const float*, const float*, const float*, const float*, const float*,
                           int, int64_t, int64_t, const uint32_t*, const CamDev&, double, double,
-                          int4*, float4*, float4*, unsigned long long*, cudaStream_t,
+                          int4*, float4*, float4*, unsigned long long*, double*, cudaStream_t,
                           const int* nd = nullptr);
 void launch_gather_keys_pad(uint32_t*, const uint32_t*, const int*, int64_t, uint32_t*,
                             cudaStream_t);
@@ -55,17 +55,17 @@ void launch_chunk_key(const float*, const float*, const float*, const float*, in
 bool launch_chunk_sort(const uint32_t*, const double*, int64_t, int, uint32_t*, cudaStream_t);
 void launch_project(const float*, const float*, const float*, const float*, const float*, int,
                     int64_t, const uint32_t*, const CamDev&, double, double, const double*,
-                    float*, int4*, float4*, float4*, unsigned long long*, cudaStream_t);
+                    float*, int4*, float4*, float4*, unsigned long long*, double*, cudaStream_t);
 void launch_blend_fwd_x(bool, int, const FwdXArgs&, const CamDev&, const ModelDev&,
                         const PixCache&, const PixResume&, Counters*, cudaStream_t);
 void launch_blend_bwd_x(bool, int, const BwdXArgs&, const CamDev&, const ModelDev&,
                         const PixCache&, Counters*, cudaStream_t);
 void launch_count_active(const int4*, const uint32_t*, int64_t, int64_t, int, const uint8_t*,
-                         const unsigned int*, unsigned long long*, cudaStream_t,
-                         const int* nd = nullptr);
+                         const unsigned int*, unsigned long long*, const double*, const CamDev&,
+                         cudaStream_t, const int* nd = nullptr);
 void launch_emit_pairs(const int4*, const uint32_t*, const unsigned long long*, int64_t, int64_t,
-                       int, const uint8_t*, uint32_t*, uint32_t*, cudaStream_t,
-                       const int* nd = nullptr, unsigned long long cap = ~0ull);
+                       int, const uint8_t*, uint32_t*, uint32_t*, const double*, const CamDev&,
+                       cudaStream_t, const int* nd = nullptr, unsigned long long cap = ~0ull);
 void launch_tile_ranges(const uint32_t*, int64_t, int2*, cudaStream_t);
 void launch_blend_fwd(bool, int, const FwdArgs&, const CamDev&, const ModelDev&, const PixCache&,
                       const PixResume&, Counters*, cudaStream_t);
@@ -151,7 +151,7 @@ int set_last_error(int code, const char* msg) { return fail(code, msg); }
 struct nxs_view {
   // per Gaussian
   Buf dkeys_in, dkeys_out, idx_in, idx_out, records, bframe, rects, ntiles, offsets, moments,
-      touched, depth, k32a, k32b, k32c, rank_of, rank_c, zlo_rank, seq, ph_hist, ph_sel;
+      touched, depth, k32a, k32b, k32c, rank_of, rank_c, zlo_rank, seq, ph_hist, ph_sel, tq;
   // per pair: sort scratch, and the sorted ranks of each depth phase
   Buf pk_in, pk_out, pv_in, pv_ph[MAX_PHASES];
   // per tile: phase ranges and virtual offsets, activity
@@ -210,7 +210,7 @@ struct nxs_view {
     Buf* all[] = {&dkeys_in, &dkeys_out, &idx_in,  &idx_out, &records, &bframe, &rects,
                   &ntiles,   &offsets,   &moments, &touched, &pk_in,   &pk_out,  &pv_in,  &active,
                   &depth,    &k32a,      &k32b,    &k32c,    &rank_of, &rank_c, &zlo_rank, &seq, &ph_hist,
-                  &ph_sel,
+                  &ph_sel,   &tq,
                   &c_last,   &c_sat,     &c_tk,    &c_thi,   &c_tlo,   &c_P,    &c_ck,
                   &c_Pck,    &c_ek,      &c_th0,   &r_rad,   &r_trem,  &r_count, &r_sea,
                   &r_sa,     &temp,      &dev_small};
@@ -582,6 +582,7 @@ int forward_impl(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
   NXS_CUDA(ensure_n<float4>(v->records, P * REC_F4));
   NXS_CUDA(ensure_n<float4>(v->bframe, P * 3));
   NXS_CUDA(ensure_n<int4>(v->rects, P));
+  NXS_CUDA(ensure_n<double>(v->tq, P * 10));
   NXS_CUDA(ensure_n<unsigned long long>(v->ntiles, P));
   NXS_CUDA(ensure_n<unsigned long long>(v->offsets, P));
   NXS_CUDA(ensure_n<uint8_t>(v->active, n_tiles));
@@ -855,7 +856,7 @@ retry_sort:
                    v->rank_of.as<uint32_t>(), cam, opts->alpha_cutoff, opts->near_plane,
                    torder ? v->depth.as<double>() : nullptr,
                    torder ? v->zlo_rank.as<float>() : nullptr, v->rects.as<int4>(),
-                   v->records.as<float4>(), v->bframe.as<float4>(), dsmall, s);
+                   v->records.as<float4>(), v->bframe.as<float4>(), dsmall, v->tq.as<double>(), s);
     NXS_LAUNCHED("project");
   }
   mark(v, 2, s);
@@ -934,12 +935,13 @@ retry_sort:
       launch_project_ranks(scene->centers, scene->scales, scene->quats, scene->opacities,
                            scene->sh, C, 0, cap0, v->idx_out.as<uint32_t>(), cam,
                            opts->alpha_cutoff, opts->near_plane, v->rects.as<int4>(),
-                           v->records.as<float4>(), v->bframe.as<float4>(), dsmall, s, n_sel);
+                           v->records.as<float4>(), v->bframe.as<float4>(), dsmall,
+                           v->tq.as<double>(), s, n_sel);
       NXS_LAUNCHED("project_ranks");
       if (v->ev_ok) rec_event(v, v->evp[0][2], s);
       launch_count_active(v->rects.as<int4>(), v->idx_out.as<uint32_t>(), 0, cap0, cam.tiles_x,
                           v->active.as<uint8_t>(), nullptr, v->ntiles.as<unsigned long long>(),
-                          s, n_sel);
+                          v->tq.as<double>(), cam, s, n_sel);
       NXS_LAUNCHED("count_active");
       size_t tbc = v->temp.cap;
       NXS_CUDA(cub::DeviceScan::ExclusiveSum(v->temp.p, tbc, v->ntiles.as<unsigned long long>(),
@@ -964,7 +966,7 @@ retry_sort:
       launch_emit_pairs(v->rects.as<int4>(), v->idx_out.as<uint32_t>(),
                         v->offsets.as<unsigned long long>(), 0, cap0, cam.tiles_x,
                         v->active.as<uint8_t>(), v->pk_in.as<uint32_t>(), v->pv_in.as<uint32_t>(),
-                        s, n_sel, (unsigned long long)capp);
+                        v->tq.as<double>(), cam, s, n_sel, (unsigned long long)capp);
       NXS_LAUNCHED("emit_pairs");
       launch_pad_keys(v->pk_in.as<uint32_t>(), capp, dsmall + 11, s);
       NXS_LAUNCHED("pad_keys");
@@ -1035,7 +1037,8 @@ retry_sort:
           launch_project_ranks(scene->centers, scene->scales, scene->quats, scene->opacities,
                                scene->sh, C, r0, r1, v->idx_out.as<uint32_t>(), cam,
                                opts->alpha_cutoff, opts->near_plane, v->rects.as<int4>(),
-                               v->records.as<float4>(), v->bframe.as<float4>(), dsmall, s);
+                               v->records.as<float4>(), v->bframe.as<float4>(), dsmall,
+                               v->tq.as<double>(), s);
           NXS_LAUNCHED("project_ranks");
           v->proj_end = r1;
         } else if (v->ev_ok) {
@@ -1050,7 +1053,7 @@ retry_sort:
       if (nr > 0) {
         launch_count_active(v->rects.as<int4>(), v->idx_out.as<uint32_t>(), r0, r1, cam.tiles_x,
                             v->active.as<uint8_t>(), ph > 0 ? n_active : nullptr,
-                            v->ntiles.as<unsigned long long>(), s);
+                            v->ntiles.as<unsigned long long>(), v->tq.as<double>(), cam, s);
         NXS_LAUNCHED("count_active");
         size_t tb = v->temp.cap;
         NXS_CUDA(cub::DeviceScan::ExclusiveSum(v->temp.p, tb, v->ntiles.as<unsigned long long>(),
@@ -1109,7 +1112,7 @@ retry_sort:
         launch_emit_pairs(v->rects.as<int4>(), v->idx_out.as<uint32_t>(),
                           v->offsets.as<unsigned long long>(), r0, r1, cam.tiles_x,
                           v->active.as<uint8_t>(), v->pk_in.as<uint32_t>(), v->pv_in.as<uint32_t>(),
-                          s);
+                          v->tq.as<double>(), cam, s);
         NXS_LAUNCHED("emit_pairs");
         if (ph == 0) mark(v, 4, s);
         size_t tb = v->temp.cap;

@@ -405,6 +405,7 @@ struct ProjOut {
   float4* records;              // per rank 8 x float4
   float4* bframe;               // per rank 3 x float4: rows of B (backward only)
   unsigned long long* straddle; // counter
+  double* tq;                   // per Gaussian: silhouette conic + an inside point (8)
 };
 
 // K1: per rank r (Gaussian g = order[r]).
@@ -550,11 +551,29 @@ __device__ __forceinline__ void project_one(const GParams& prm, int64_t g, const
     if (jlo <= jhi && ilo <= ihi) {
       int j0 = (int)jlo, j1 = (int)jhi, i0 = (int)ilo, i1 = (int)ihi;
       rect = make_int4(j0 / TILE, i0 / TILE, j1 / TILE, i1 / TILE);
+      if (ok && out.tq) {
+        // exact tile test data: the silhouette conic q(X, Y) = Hᵀ Q H and
+        // the projected centre (inside it: q = -r2m·D there)
+        double* t = out.tq + 10 * g;
+        t[0] = Q[0];
+        t[1] = Q[1];
+        t[2] = Q[4];
+        t[3] = Q[2];
+        t[4] = Q[5];
+        t[5] = Q[8];
+        t[6] = bp[0] * ibz;
+        t[7] = bp[1] * ibz;
+        t[8] = 0.5 / Q[0];
+        t[9] = 0.5 / Q[4];
+      } else if (out.tq) {
+        out.tq[10 * g] = __longlong_as_double(0x7ff8000000000000ll);  // NaN: no exact test
+      }
     }
   }
 
   if (general) {
     rect = make_int4(0, 0, cam.tiles_x - 1, cam.tiles_y - 1);
+    if (out.tq) out.tq[10 * g] = __longlong_as_double(0x7ff8000000000000ll);  // every tile
     // world-frame A = R diag(s^-2) R^T, b = μ - o (render.py:116-121)
     double A[9];
 #pragma unroll
@@ -804,52 +823,113 @@ __global__ void __launch_bounds__(PROJ_CHUNK)
   }
 }
 
+// Exact tile culling: does the silhouette ellipse q <= 0 meet the tile's
+// pixel-centre rectangle (normalised coordinates)?  The projected centre is
+// inside the ellipse, so it meets the (convex) rectangle iff the centre is
+// in it or q <= 0 somewhere on one of its edges (the minimum of q along an
+// edge line is the clamped vertex of a convex quadratic).  Conservative:
+// every valid pixel lies strictly inside the margin ellipse (r2m).  fp64,
+// IEEE op by op (this file is built with --fmad=false), restated in
+// oracle/binning_oracle.c.
+__device__ __forceinline__ bool tile_hit(const double* __restrict__ tq, int64_t g, int tx, int ty,
+                                         const CamDev& cam, double inv_f) {
+  const double* t = tq + 10 * g;
+  const double q00 = t[0];
+  if (!(q00 == q00)) return true;  // no exact test for this Gaussian
+  const double q01 = t[1], q11 = t[2], q02 = t[3], q12 = t[4], q22 = t[5];
+  const double c0 = t[6], c1 = t[7], h00 = t[8], h11 = t[9];
+  const int jx0 = tx * TILE, iy0 = ty * TILE;
+  const int jx1 = min(jx0 + TILE - 1, cam.W - 1), iy1 = min(iy0 + TILE - 1, cam.H - 1);
+  const double x0 = (((double)jx0 + 0.5) - cam.cx) * inv_f, x1 = (((double)jx1 + 0.5) - cam.cx) * inv_f;
+  const double y0 = (((double)iy0 + 0.5) - cam.cy) * inv_f, y1 = (((double)iy1 + 0.5) - cam.cy) * inv_f;
+  if (c0 >= x0 && c0 <= x1 && c1 >= y0 && c1 <= y1) return true;
+  for (int k = 0; k < 2; ++k) {  // vertical edges X = xe: q(Y) = q11 Y² + b Y + c
+    const double xe = k ? x1 : x0;
+    const double b = 2.0 * (q01 * xe + q12);
+    const double c = (q00 * xe * xe + 2.0 * q02 * xe) + q22;
+    double yv = -b * h11;
+    yv = yv < y0 ? y0 : (yv > y1 ? y1 : yv);
+    if ((q11 * yv + b) * yv + c <= 0.0) return true;
+  }
+  for (int k = 0; k < 2; ++k) {  // horizontal edges Y = ye: q(X) = q00 X² + b X + c
+    const double ye = k ? y1 : y0;
+    const double b = 2.0 * (q01 * ye + q02);
+    const double c = (q11 * ye * ye + 2.0 * q12 * ye) + q22;
+    double xv = -b * h00;
+    xv = xv < x0 ? x0 : (xv > x1 ? x1 : xv);
+    if ((q00 * xv + b) * xv + c <= 0.0) return true;
+  }
+  return false;
+}
+
 // K2a: per rank of [r0, r1), the number of still-active tiles in its rect.
-__global__ void k_count_active(const int4* __restrict__ rects, const uint32_t* __restrict__ order,
-                               int64_t r0, int64_t r1, int tiles_x,
-                               const uint8_t* __restrict__ active,
-                               const unsigned int* __restrict__ gate,
-                               unsigned long long* __restrict__ counts,
-                               const int* __restrict__ nd) {
+// One warp per rank: lanes stride over the candidate tiles of its rect
+// (the exact tile test is fp64 work per tile; a thread per rank would leave
+// the SMs nearly empty at a phase of a few 10^4 ranks).
+__global__ void __launch_bounds__(256)
+    k_count_active(const int4* __restrict__ rects, const uint32_t* __restrict__ order,
+                   int64_t r0, int64_t r1, int tiles_x, const uint8_t* __restrict__ active,
+                   const unsigned int* __restrict__ gate, unsigned long long* __restrict__ counts,
+                   const int* __restrict__ nd, const double* __restrict__ tq, CamDev cam) {
   // later phases: nothing to count when the previous forward left no tile
   // active (the host then stops before reading the counts)
   if (gate && *gate == 0u) return;
-  const int64_t r = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t r = r0 + (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= r1) return;
   if (nd && r >= r0 + *nd) {  // device-sized phase: padding ranks count 0
-    counts[r - r0] = 0;
+    if (lane == 0) counts[r - r0] = 0;
     return;
   }
-  const int4 rc = rects[order[r]];
-  unsigned long long n = 0;
-  if (rc.x >= 0)
-    for (int ty = rc.y; ty <= rc.w; ++ty)
-      for (int tx = rc.x; tx <= rc.z; ++tx) n += active[ty * tiles_x + tx];
-  counts[r - r0] = n;
+  const int64_t g = order[r];
+  const int4 rc = rects[g];
+  const double inv_f = 1.0 / cam.f;
+  unsigned n = 0;
+  if (rc.x >= 0) {
+    const int w = rc.z - rc.x + 1, nt = w * (rc.w - rc.y + 1);
+    for (int k = lane; k < nt; k += 32) {
+      const int tx = rc.x + k % w, ty = rc.y + k / w;
+      n += (active[ty * tiles_x + tx] && tile_hit(tq, g, tx, ty, cam, inv_f)) ? 1u : 0u;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+  if (lane == 0) counts[r - r0] = n;
 }
 
 // K2b: emit (tile, rank) pairs of active tiles at the exclusive-scan
-// offsets, in rank order (so a stable sort by tile keeps ranks ascending).
-__global__ void k_emit_pairs(const int4* __restrict__ rects, const uint32_t* __restrict__ order,
-                             const unsigned long long* __restrict__ offsets, int64_t r0,
-                             int64_t r1, int tiles_x, const uint8_t* __restrict__ active,
-                             uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                             const int* __restrict__ nd, unsigned long long cap) {
+// offsets, in rank order (so a stable sort by tile keeps ranks ascending);
+// one warp per rank, a ballot orders each 32-tile group.
+__global__ void __launch_bounds__(256)
+    k_emit_pairs(const int4* __restrict__ rects, const uint32_t* __restrict__ order,
+                 const unsigned long long* __restrict__ offsets, int64_t r0, int64_t r1,
+                 int tiles_x, const uint8_t* __restrict__ active, uint32_t* __restrict__ keys,
+                 uint32_t* __restrict__ vals, const int* __restrict__ nd, unsigned long long cap,
+                 const double* __restrict__ tq, CamDev cam) {
   if (nd) r1 = min(r1, r0 + (int64_t)*nd);
-  const int64_t r = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t r = r0 + (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= r1) return;
-  const int4 rc = rects[order[r]];
+  const int64_t g = order[r];
+  const int4 rc = rects[g];
   if (rc.x < 0) return;
+  const double inv_f = 1.0 / cam.f;
   unsigned long long o = offsets[r - r0];
-  for (int ty = rc.y; ty <= rc.w; ++ty)
-    for (int tx = rc.x; tx <= rc.z; ++tx) {
-      const int t = ty * tiles_x + tx;
-      if (!active[t]) continue;
-      if (o >= cap) return;  // device-sized pair buffer too small (flagged by k_pairs_total)
-      keys[o] = (uint32_t)t;
-      vals[o] = (uint32_t)r;
-      ++o;
+  const int w = rc.z - rc.x + 1, nt = w * (rc.w - rc.y + 1);
+  for (int base = 0; base < nt; base += 32) {
+    const int k = base + lane;
+    const int tx = rc.x + k % w, ty = rc.y + k / w;
+    const int t = ty * tiles_x + tx;
+    const bool hit = k < nt && active[t] && tile_hit(tq, g, tx, ty, cam, inv_f);
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    if (hit) {
+      const unsigned long long q = o + __popc(m & ((1u << lane) - 1u));
+      if (q < cap) {  // device-sized pair buffer too small: flagged by k_pairs_total
+        keys[q] = (uint32_t)t;
+        vals[q] = (uint32_t)r;
+      }
     }
+    o += __popc(m);
+  }
 }
 
 // device-sized binning: total pair count of the scan, the capacity check,
@@ -1015,9 +1095,10 @@ void launch_project_ranks(const float* centers, const float* scales, const float
                           const float* opacities, const float* sh, int C, int64_t r0, int64_t r1,
                           const uint32_t* order, const CamDev& cam, double cutoff,
                           double near_plane, int4* rects, float4* records, float4* bframe,
-                          unsigned long long* straddle, cudaStream_t s, const int* nd) {
+                          unsigned long long* straddle, double* tq, cudaStream_t s,
+                          const int* nd) {
   if (r1 <= r0) return;
-  ProjOut o{nullptr, nullptr, rects, records, bframe, straddle};
+  ProjOut o{nullptr, nullptr, rects, records, bframe, straddle, tq};
   k_project_ranks<<<(unsigned)((r1 - r0 + PROJ_CHUNK - 1) / PROJ_CHUNK), PROJ_CHUNK, 0, s>>>(
       centers, scales, quats, opacities, sh, C, r0, r1, order, cam, cutoff, near_plane, o, nd);
 }
@@ -1026,9 +1107,9 @@ void launch_project(const float* centers, const float* scales, const float* quat
                     const float* opacities, const float* sh, int C, int64_t P,
                     const uint32_t* rank_of, const CamDev& cam, double cutoff, double near_plane,
                     const double* zlo, float* zlo_rank, int4* rects, float4* records,
-                    float4* bframe, unsigned long long* straddle, cudaStream_t s) {
+                    float4* bframe, unsigned long long* straddle, double* tq, cudaStream_t s) {
   if (P == 0) return;
-  ProjOut o{zlo, zlo_rank, rects, records, bframe, straddle};
+  ProjOut o{zlo, zlo_rank, rects, records, bframe, straddle, tq};
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1040,18 +1121,20 @@ void launch_project(const float* centers, const float* scales, const float* quat
 
 void launch_count_active(const int4* rects, const uint32_t* order, int64_t r0, int64_t r1,
                          int tiles_x, const uint8_t* active, const unsigned int* gate,
-                         unsigned long long* counts, cudaStream_t s, const int* nd) {
+                         unsigned long long* counts, const double* tq, const CamDev& cam,
+                         cudaStream_t s, const int* nd) {
   if (r1 <= r0) return;
-  k_count_active<<<(unsigned)((r1 - r0 + 255) / 256), 256, 0, s>>>(rects, order, r0, r1, tiles_x,
-                                                                   active, gate, counts, nd);
+  k_count_active<<<(unsigned)((r1 - r0 + 7) / 8), 256, 0, s>>>(
+      rects, order, r0, r1, tiles_x, active, gate, counts, nd, tq, cam);
 }
 
 void launch_emit_pairs(const int4* rects, const uint32_t* order, const unsigned long long* offsets,
                        int64_t r0, int64_t r1, int tiles_x, const uint8_t* active, uint32_t* keys,
-                       uint32_t* vals, cudaStream_t s, const int* nd, unsigned long long cap) {
+                       uint32_t* vals, const double* tq, const CamDev& cam, cudaStream_t s,
+                       const int* nd, unsigned long long cap) {
   if (r1 <= r0) return;
-  k_emit_pairs<<<(unsigned)((r1 - r0 + 255) / 256), 256, 0, s>>>(
-      rects, order, offsets, r0, r1, tiles_x, active, keys, vals, nd, cap);
+  k_emit_pairs<<<(unsigned)((r1 - r0 + 7) / 8), 256, 0, s>>>(
+      rects, order, offsets, r0, r1, tiles_x, active, keys, vals, nd, cap, tq, cam);
 }
 void launch_pairs_total(const unsigned long long* offsets, const unsigned long long* counts,
                         int64_t n, unsigned long long cap, unsigned long long* total,
