@@ -57,7 +57,7 @@ def _view_grads(v, n_views):
     return g
 
 
-def _worker(rank, world, port, n_views, out):
+def _worker(rank, world, port, n_views, out, sparse=True):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     sc = _scene()
@@ -68,19 +68,20 @@ def _worker(rank, world, port, n_views, out):
         for k, t in gb.fields.items():
             t += torch.from_numpy(np.ascontiguousarray(g[k]).reshape(t.shape))
 
-    step = DataParallelStep(n_views, rank, world, grads, render_view)
+    step = DataParallelStep(n_views, rank, world, grads, render_view, sparse=sparse)
     step()
     out[rank] = grads.flat.numpy().copy()
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("sparse", [True, False])
 @pytest.mark.parametrize("n_views", [2, 3])
-def test_allreduce_equals_sum_of_per_view_gradients(n_views):
+def test_allreduce_equals_sum_of_per_view_gradients(n_views, sparse):
     world = 2
     port = _free_port()
     with mp.Manager() as mgr:
         out = mgr.dict()
-        mp.spawn(_worker, args=(world, port, n_views, out), nprocs=world, join=True)
+        mp.spawn(_worker, args=(world, port, n_views, out, sparse), nprocs=world, join=True)
         res = dict(out)
     assert np.array_equal(res[0], res[1])
     sc = _scene()
@@ -90,3 +91,34 @@ def test_allreduce_equals_sum_of_per_view_gradients(n_views):
         for k, t in expect.fields.items():
             t += torch.from_numpy(np.ascontiguousarray(g[k]).reshape(t.shape))
     np.testing.assert_allclose(res[0], expect.flat.numpy(), rtol=1e-12, atol=1e-15)
+
+
+def _sparse_worker(rank, world, port, out):
+    """Disjoint and overlapping touched sets, and an all-zero rank."""
+    from paper_2603_02887_b200.dp import sparse_allreduce
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g = GradBuffer(10, 4, dtype=torch.float64)
+    rng = np.random.default_rng(rank)
+    rows = [1, 4, 7] if rank == 0 else [4, 5]
+    for k, t in g.fields.items():
+        r = t.reshape(10, -1)
+        for i in rows:
+            r[i] = torch.from_numpy(rng.normal(size=r.shape[1]))
+    before = g.flat.clone()
+    m = sparse_allreduce(g)
+    out[rank] = (g.flat.numpy().copy(), before.numpy(), m)
+    dist.destroy_process_group()
+
+
+def test_sparse_allreduce_equals_dense_sum():
+    world = 2
+    port = _free_port()
+    with mp.Manager() as mgr:
+        out = mgr.dict()
+        mp.spawn(_sparse_worker, args=(world, port, out), nprocs=world, join=True)
+        res = dict(out)
+    total = res[0][1] + res[1][1]
+    np.testing.assert_allclose(res[0][0], total, rtol=1e-15, atol=0)
+    np.testing.assert_array_equal(res[0][0], res[1][0])
+    assert res[0][2] == 4  # rows 1, 4, 5, 7
