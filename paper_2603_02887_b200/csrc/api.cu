@@ -47,6 +47,12 @@ void launch_pad_keys(uint32_t*, int64_t, const unsigned long long*, cudaStream_t
 void launch_gather_keys(const uint32_t*, const uint32_t*, int64_t, uint32_t*, cudaStream_t);
 void launch_clear_rects(const uint32_t*, int64_t, int64_t, int4*, cudaStream_t);
 void launch_iota(uint32_t*, int64_t, cudaStream_t);
+void launch_zlo_ranks(const float*, const float*, const float*, const float*, const uint32_t*,
+                      int64_t, int64_t, const CamDev&, double, double*, cudaStream_t);
+void launch_project_ranks_z(const float*, const float*, const float*, const float*, const float*,
+                            int, int64_t, int64_t, const uint32_t*, const CamDev&, double, double,
+                            const double*, float*, int4*, float4*, float4*, unsigned long long*,
+                            double*, cudaStream_t);
 void launch_pack_check(const unsigned long long*, const long long*, int, unsigned long long*,
                        cudaStream_t);
 void launch_chunk_key(const float*, const float*, const float*, const float*, int64_t,
@@ -151,7 +157,7 @@ int set_last_error(int code, const char* msg) { return fail(code, msg); }
 struct nxs_view {
   // per Gaussian
   Buf dkeys_in, dkeys_out, idx_in, idx_out, records, bframe, rects, ntiles, offsets, moments,
-      touched, depth, k32a, k32b, k32c, rank_of, rank_c, zlo_rank, seq, ph_hist, ph_sel, tq;
+      touched, depth, k32a, k32b, k32c, rank_of, rank_c, zlo_rank, seq, ph_hist, ph_sel, tq, zlo64;
   // per pair: sort scratch, and the sorted ranks of each depth phase
   Buf pk_in, pk_out, pv_in, pv_ph[MAX_PHASES];
   // per tile: phase ranges and virtual offsets, activity
@@ -210,7 +216,7 @@ struct nxs_view {
     Buf* all[] = {&dkeys_in, &dkeys_out, &idx_in,  &idx_out, &records, &bframe, &rects,
                   &ntiles,   &offsets,   &moments, &touched, &pk_in,   &pk_out,  &pv_in,  &active,
                   &depth,    &k32a,      &k32b,    &k32c,    &rank_of, &rank_c, &zlo_rank, &seq, &ph_hist,
-                  &ph_sel,   &tq,
+                  &ph_sel,   &tq,      &zlo64,
                   &c_last,   &c_sat,     &c_tk,    &c_thi,   &c_tlo,   &c_P,    &c_ck,
                   &c_Pck,    &c_ek,      &c_th0,   &r_rad,   &r_trem,  &r_count, &r_sea,
                   &r_sa,     &temp,      &dev_small};
@@ -649,7 +655,8 @@ int forward_impl(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
   // device-sized phase 0 (no host sync before the first forward): needs
   // estimates from this view's previous call and a later phase to verify at
   bool async0 = v->est_n0 > 0 && v->est_pairs >= 0 && v->est_bin0 >= 0 && n_ph >= 2 &&
-                spec_phase >= 0;
+                spec_phase >= 0 && !chunked;
+  int64_t proc_end = 0;  // chunked lazy phases: ranks [0, proc_end) are processed
   bool phase_full[MAX_PHASES] = {false, false, false, false};  // lazy phase sorted on 32 bits
   int phase_shift[MAX_PHASES] = {0, 0, 0, 0};
 retry_sort:
@@ -706,10 +713,14 @@ retry_sort:
   }
   n_ph = n_ph_plan;
   for (int i = 0; i <= n_ph; ++i) R[i] = Rplan[i];
-  v->lazy = !torder && !sort64 && !(opts->flags & NXS_FLAG_FULL_BINNING) && P > 0;
+  // lazy depth phases: the global order, and the chunked order (phases end
+  // on chunk boundaries; each phase's chunks are z_lo-sorted when complete)
+  v->lazy = (!torder || (chunked && opts->chunk_size <= 2048)) && !sort64 &&
+            !(opts->flags & NXS_FLAG_FULL_BINNING) && P > 0;
   v->sorted_end = 0;
   v->proj_end = 0;
   v->bin_done = -1;
+  proc_end = 0;
   mark(v, 0, s);
   if (P > 0) {
     size_t tmp_sort = 0, tmp_scan = 0;
@@ -812,7 +823,7 @@ retry_sort:
                        P, dsmall + 8, s);
       NXS_LAUNCHED("key_fixup");
     }
-    if (chunked) {
+    if (chunked && !v->lazy) {
       // chunk = centre-depth rank / C; lists in (chunk, z_lo) order: one
       // block radix sort per chunk, or a global 64-bit sort for huge chunks
       NXS_CUDA(ensure_n<uint32_t>(v->rank_c, P));
@@ -1029,18 +1040,59 @@ retry_sort:
                            v->depth.as<double>(), nr, dsmall + 8, s, shift);
           phase_shift[ph] = shift;
           NXS_LAUNCHED("key_fixup");
-          launch_rank_of_range(v->idx_out.as<uint32_t>(), r0, r1, v->rank_of.as<uint32_t>(), s);
-          NXS_LAUNCHED("rank_of");
           v->sorted_end = r1;
           v->bin_done = hi;
-          if (v->ev_ok) rec_event(v, v->evp[ph][1], s);
-          launch_project_ranks(scene->centers, scene->scales, scene->quats, scene->opacities,
-                               scene->sh, C, r0, r1, v->idx_out.as<uint32_t>(), cam,
-                               opts->alpha_cutoff, opts->near_plane, v->rects.as<int4>(),
-                               v->records.as<float4>(), v->bframe.as<float4>(), dsmall,
-                               v->tq.as<double>(), s);
-          NXS_LAUNCHED("project_ranks");
-          v->proj_end = r1;
+          if (chunked) {
+            // centre-depth ranks of this phase, then the complete chunks it
+            // finishes, [proc_end, p1), sorted by z_lo and processed
+            NXS_CUDA(ensure_n<uint32_t>(v->rank_c, P));
+            NXS_CUDA(ensure_n<double>(v->zlo64, P));
+            NXS_CUDA(ensure_n<float>(v->zlo_rank, P));
+            launch_rank_of_range(v->idx_out.as<uint32_t>(), r0, r1, v->rank_c.as<uint32_t>(), s);
+            NXS_LAUNCHED("rank_c");
+            const int64_t Cc = opts->chunk_size;
+            const int64_t p0 = proc_end, p1 = (r1 >= P) ? P : (r1 / Cc) * Cc;
+            if (v->ev_ok) rec_event(v, v->evp[ph][1], s);
+            if (p1 > p0) {
+              launch_zlo_ranks(scene->centers, scene->scales, scene->quats, scene->opacities,
+                               v->idx_out.as<uint32_t>(), p0, p1, cam, opts->alpha_cutoff,
+                               v->zlo64.as<double>(), s);
+              NXS_LAUNCHED("zlo_ranks");
+              launch_chunk_sort(v->idx_out.as<uint32_t>() + p0, v->zlo64.as<double>(), p1 - p0,
+                                (int)Cc, v->idx_in.as<uint32_t>() + p0, s);
+              NXS_LAUNCHED("chunk_sort");
+              NXS_CUDA(cudaMemcpyAsync(v->idx_out.as<uint32_t>() + p0,
+                                       v->idx_in.as<uint32_t>() + p0, (size_t)(p1 - p0) * 4,
+                                       cudaMemcpyDeviceToDevice, s));
+              launch_rank_of_range(v->idx_out.as<uint32_t>(), p0, p1, v->rank_of.as<uint32_t>(), s);
+              NXS_LAUNCHED("rank_of");
+              launch_project_ranks_z(scene->centers, scene->scales, scene->quats,
+                                     scene->opacities, scene->sh, C, p0, p1,
+                                     v->idx_out.as<uint32_t>(), cam, opts->alpha_cutoff,
+                                     opts->near_plane, v->zlo64.as<double>(),
+                                     v->zlo_rank.as<float>(), v->rects.as<int4>(),
+                                     v->records.as<float4>(), v->bframe.as<float4>(), dsmall,
+                                     v->tq.as<double>(), s);
+              NXS_LAUNCHED("project_ranks");
+            }
+            proc_end = p1;
+            v->proj_end = p1;
+            r0 = p0;  // the rest of the phase works on the processed ranks
+            r1 = p1;
+            nr = p1 - p0;
+          } else {
+            launch_rank_of_range(v->idx_out.as<uint32_t>(), r0, r1, v->rank_of.as<uint32_t>(),
+                                 s);
+            NXS_LAUNCHED("rank_of");
+            if (v->ev_ok) rec_event(v, v->evp[ph][1], s);
+            launch_project_ranks(scene->centers, scene->scales, scene->quats, scene->opacities,
+                                 scene->sh, C, r0, r1, v->idx_out.as<uint32_t>(), cam,
+                                 opts->alpha_cutoff, opts->near_plane, v->rects.as<int4>(),
+                                 v->records.as<float4>(), v->bframe.as<float4>(), dsmall,
+                                 v->tq.as<double>(), s);
+            NXS_LAUNCHED("project_ranks");
+            v->proj_end = r1;
+          }
         } else if (v->ev_ok) {
           rec_event(v, v->evp[ph][1], s);
         }

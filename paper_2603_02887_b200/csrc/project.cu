@@ -804,6 +804,7 @@ __global__ void __launch_bounds__(PROJ_CHUNK)
       }
     }
     project_one(prm, g, cam, cutoff, near_plane, out, so.rec[tid], so.bf[tid]);
+    if (out.zlo_rank) out.zlo_rank[r] = __double2float_rd(out.zlo[g]);
     so.rank[tid] = r;
   } else {
     so.rank[tid] = -1;
@@ -1066,6 +1067,36 @@ void launch_gather_keys(const uint32_t* idx, const uint32_t* key, int64_t n, uin
                         cudaStream_t s) {
   if (n <= 0) return;
   k_gather_keys<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(idx, key, n, out);
+}
+// chunked lazy phases: z_lo of the Gaussians at ranks [r0, r1)
+__global__ void k_zlo_ranks(const float* __restrict__ centers, const float* __restrict__ scales,
+                            const float* __restrict__ quats, const float* __restrict__ opacities,
+                            const uint32_t* __restrict__ order, int64_t r0, int64_t r1,
+                            CamDev cam, double cutoff, double* __restrict__ zlo) {
+  const int64_t r = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= r1) return;
+  const int64_t g = order[r];
+  zlo[g] = z_lower(centers, scales, quats, opacities, g, cam, cutoff);
+}
+void launch_zlo_ranks(const float* centers, const float* scales, const float* quats,
+                      const float* opacities, const uint32_t* order, int64_t r0, int64_t r1,
+                      const CamDev& cam, double cutoff, double* zlo, cudaStream_t s) {
+  if (r1 <= r0) return;
+  k_zlo_ranks<<<(unsigned)((r1 - r0 + 255) / 256), 256, 0, s>>>(centers, scales, quats,
+                                                                opacities, order, r0, r1, cam,
+                                                                cutoff, zlo);
+}
+void launch_project_ranks_z(const float* centers, const float* scales, const float* quats,
+                            const float* opacities, const float* sh, int C, int64_t r0,
+                            int64_t r1, const uint32_t* order, const CamDev& cam, double cutoff,
+                            double near_plane, const double* zlo, float* zlo_rank, int4* rects,
+                            float4* records, float4* bframe, unsigned long long* straddle,
+                            double* tq, cudaStream_t s) {
+  if (r1 <= r0) return;
+  ProjOut o{zlo, zlo_rank, rects, records, bframe, straddle, tq};
+  k_project_ranks<<<(unsigned)((r1 - r0 + PROJ_CHUNK - 1) / PROJ_CHUNK), PROJ_CHUNK, 0, s>>>(
+      centers, scales, quats, opacities, sh, C, r0, r1, order, cam, cutoff, near_plane, o,
+      nullptr);
 }
 void launch_gather_keys_pad(uint32_t* idx, const uint32_t* key, const int* nd, int64_t cap,
                             uint32_t* out, cudaStream_t s) {
