@@ -952,7 +952,7 @@ retry_sort:
       if (v->ev_ok) rec_event(v, v->evp[0][2], s);
       launch_count_active(v->rects.as<int4>(), v->idx_out.as<uint32_t>(), 0, cap0, cam.tiles_x,
                           v->active.as<uint8_t>(), nullptr, v->ntiles.as<unsigned long long>(),
-                          v->tq.as<double>(), cam, s, n_sel);
+                          exact ? nullptr : v->tq.as<double>(), cam, s, n_sel);
       NXS_LAUNCHED("count_active");
       size_t tbc = v->temp.cap;
       NXS_CUDA(cub::DeviceScan::ExclusiveSum(v->temp.p, tbc, v->ntiles.as<unsigned long long>(),
@@ -977,7 +977,7 @@ retry_sort:
       launch_emit_pairs(v->rects.as<int4>(), v->idx_out.as<uint32_t>(),
                         v->offsets.as<unsigned long long>(), 0, cap0, cam.tiles_x,
                         v->active.as<uint8_t>(), v->pk_in.as<uint32_t>(), v->pv_in.as<uint32_t>(),
-                        v->tq.as<double>(), cam, s, n_sel, (unsigned long long)capp);
+                        exact ? nullptr : v->tq.as<double>(), cam, s, n_sel, (unsigned long long)capp);
       NXS_LAUNCHED("emit_pairs");
       launch_pad_keys(v->pk_in.as<uint32_t>(), capp, dsmall + 11, s);
       NXS_LAUNCHED("pad_keys");
@@ -1105,7 +1105,7 @@ retry_sort:
       if (nr > 0) {
         launch_count_active(v->rects.as<int4>(), v->idx_out.as<uint32_t>(), r0, r1, cam.tiles_x,
                             v->active.as<uint8_t>(), ph > 0 ? n_active : nullptr,
-                            v->ntiles.as<unsigned long long>(), v->tq.as<double>(), cam, s);
+                            v->ntiles.as<unsigned long long>(), exact ? nullptr : v->tq.as<double>(), cam, s);
         NXS_LAUNCHED("count_active");
         size_t tb = v->temp.cap;
         NXS_CUDA(cub::DeviceScan::ExclusiveSum(v->temp.p, tb, v->ntiles.as<unsigned long long>(),
@@ -1164,7 +1164,7 @@ retry_sort:
         launch_emit_pairs(v->rects.as<int4>(), v->idx_out.as<uint32_t>(),
                           v->offsets.as<unsigned long long>(), r0, r1, cam.tiles_x,
                           v->active.as<uint8_t>(), v->pk_in.as<uint32_t>(), v->pv_in.as<uint32_t>(),
-                          v->tq.as<double>(), cam, s);
+                          exact ? nullptr : v->tq.as<double>(), cam, s);
         NXS_LAUNCHED("emit_pairs");
         if (ph == 0) mark(v, 4, s);
         size_t tb = v->temp.cap;

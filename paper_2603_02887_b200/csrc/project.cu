@@ -834,6 +834,7 @@ __global__ void __launch_bounds__(PROJ_CHUNK)
 // oracle/binning_oracle.c.
 __device__ __forceinline__ bool tile_hit(const double* __restrict__ tq, int64_t g, int tx, int ty,
                                          const CamDev& cam, double inv_f) {
+  if (!tq) return true;  // culling off (exact order: full binning, bbox tiles)
   const double* t = tq + 10 * g;
   const double q00 = t[0];
   if (!(q00 == q00)) return true;  // no exact test for this Gaussian
@@ -864,9 +865,11 @@ __device__ __forceinline__ bool tile_hit(const double* __restrict__ tq, int64_t 
 }
 
 // K2a: per rank of [r0, r1), the number of still-active tiles in its rect.
-// One warp per rank: lanes stride over the candidate tiles of its rect
-// (the exact tile test is fp64 work per tile; a thread per rank would leave
-// the SMs nearly empty at a phase of a few 10^4 ranks).
+// KSUB lanes per rank: lanes stride over the candidate tiles of the rect,
+// so the fp64 exact tile tests of big rects run in parallel.  A depth phase
+// of a few 10^4 near (big) Gaussians uses a warp per rank; a full binning of
+// all ranks (mostly small rects) eight lanes.
+template <int KSUB>
 __global__ void __launch_bounds__(256)
     k_count_active(const int4* __restrict__ rects, const uint32_t* __restrict__ order,
                    int64_t r0, int64_t r1, int tiles_x, const uint8_t* __restrict__ active,
@@ -875,31 +878,31 @@ __global__ void __launch_bounds__(256)
   // later phases: nothing to count when the previous forward left no tile
   // active (the host then stops before reading the counts)
   if (gate && *gate == 0u) return;
-  const int lane = threadIdx.x & 31;
-  const int64_t r = r0 + (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (r >= r1) return;
-  if (nd && r >= r0 + *nd) {  // device-sized phase: padding ranks count 0
-    if (lane == 0) counts[r - r0] = 0;
-    return;
-  }
-  const int64_t g = order[r];
-  const int4 rc = rects[g];
-  const double inv_f = 1.0 / cam.f;
+  const int lane = threadIdx.x & 31, sl = lane & (KSUB - 1);
+  const int64_t r = r0 + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / KSUB;
+  const int64_t rn = nd ? min(r1, r0 + (int64_t)*nd) : r1;
+  const bool live = r < rn;
   unsigned n = 0;
-  if (rc.x >= 0) {
-    const int w = rc.z - rc.x + 1, nt = w * (rc.w - rc.y + 1);
-    for (int k = lane; k < nt; k += 32) {
-      const int tx = rc.x + k % w, ty = rc.y + k / w;
-      n += (active[ty * tiles_x + tx] && tile_hit(tq, g, tx, ty, cam, inv_f)) ? 1u : 0u;
+  if (live) {
+    const int64_t g = order[r];
+    const int4 rc = rects[g];
+    if (rc.x >= 0) {
+      const double inv_f = 1.0 / cam.f;
+      const int w = rc.z - rc.x + 1, nt = w * (rc.w - rc.y + 1);
+      for (int k = sl; k < nt; k += KSUB) {
+        const int tx = rc.x + k % w, ty = rc.y + k / w;
+        n += (active[ty * tiles_x + tx] && tile_hit(tq, g, tx, ty, cam, inv_f)) ? 1u : 0u;
+      }
     }
   }
-  for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
-  if (lane == 0) counts[r - r0] = n;
+  for (int o = KSUB / 2; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+  if (sl == 0 && r < r1) counts[r - r0] = live ? n : 0ull;  // padding ranks count 0
 }
 
 // K2b: emit (tile, rank) pairs of active tiles at the exclusive-scan
 // offsets, in rank order (so a stable sort by tile keeps ranks ascending);
-// one warp per rank, a ballot orders each 32-tile group.
+// KSUB lanes per rank, a ballot orders each KSUB-tile group.
+template <int KSUB>
 __global__ void __launch_bounds__(256)
     k_emit_pairs(const int4* __restrict__ rects, const uint32_t* __restrict__ order,
                  const unsigned long long* __restrict__ offsets, int64_t r0, int64_t r1,
@@ -907,23 +910,30 @@ __global__ void __launch_bounds__(256)
                  uint32_t* __restrict__ vals, const int* __restrict__ nd, unsigned long long cap,
                  const double* __restrict__ tq, CamDev cam) {
   if (nd) r1 = min(r1, r0 + (int64_t)*nd);
-  const int lane = threadIdx.x & 31;
-  const int64_t r = r0 + (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (r >= r1) return;
-  const int64_t g = order[r];
-  const int4 rc = rects[g];
-  if (rc.x < 0) return;
+  const int lane = threadIdx.x & 31, sl = lane & (KSUB - 1), grp = lane / KSUB;
+  const int64_t r = r0 + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / KSUB;
+  int64_t g = 0;
+  int4 rc = make_int4(-1, -1, -1, -1);
+  if (r < r1) {
+    g = order[r];
+    rc = rects[g];
+  }
+  const int w = rc.z - rc.x + 1;
+  const int nt = rc.x >= 0 ? w * (rc.w - rc.y + 1) : 0;
+  int nmax = nt;  // the warp loops to its largest rect (ballots need every lane)
+  for (int o = 16; o > 0; o >>= 1) nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
   const double inv_f = 1.0 / cam.f;
-  unsigned long long o = offsets[r - r0];
-  const int w = rc.z - rc.x + 1, nt = w * (rc.w - rc.y + 1);
-  for (int base = 0; base < nt; base += 32) {
-    const int k = base + lane;
-    const int tx = rc.x + k % w, ty = rc.y + k / w;
+  unsigned long long o = nt > 0 ? offsets[r - r0] : 0ull;
+  for (int base = 0; base < nmax; base += KSUB) {
+    const int k = base + sl;
+    const int tx = rc.x + (w > 0 ? k % w : 0), ty = rc.y + (w > 0 ? k / w : 0);
     const int t = ty * tiles_x + tx;
     const bool hit = k < nt && active[t] && tile_hit(tq, g, tx, ty, cam, inv_f);
-    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    const unsigned m = KSUB == 32 ? __ballot_sync(0xffffffffu, hit)
+                                  : (__ballot_sync(0xffffffffu, hit) >> (grp * KSUB)) &
+                                        ((1u << KSUB) - 1u);
     if (hit) {
-      const unsigned long long q = o + __popc(m & ((1u << lane) - 1u));
+      const unsigned long long q = o + __popc(m & ((1u << sl) - 1u));
       if (q < cap) {  // device-sized pair buffer too small: flagged by k_pairs_total
         keys[q] = (uint32_t)t;
         vals[q] = (uint32_t)r;
@@ -1155,8 +1165,12 @@ void launch_count_active(const int4* rects, const uint32_t* order, int64_t r0, i
                          unsigned long long* counts, const double* tq, const CamDev& cam,
                          cudaStream_t s, const int* nd) {
   if (r1 <= r0) return;
-  k_count_active<<<(unsigned)((r1 - r0 + 7) / 8), 256, 0, s>>>(
-      rects, order, r0, r1, tiles_x, active, gate, counts, nd, tq, cam);
+  if (r1 - r0 <= 262144)
+    k_count_active<32><<<(unsigned)((r1 - r0 + 7) / 8), 256, 0, s>>>(
+        rects, order, r0, r1, tiles_x, active, gate, counts, nd, tq, cam);
+  else
+    k_count_active<8><<<(unsigned)((r1 - r0 + 31) / 32), 256, 0, s>>>(
+        rects, order, r0, r1, tiles_x, active, gate, counts, nd, tq, cam);
 }
 
 void launch_emit_pairs(const int4* rects, const uint32_t* order, const unsigned long long* offsets,
@@ -1164,8 +1178,12 @@ void launch_emit_pairs(const int4* rects, const uint32_t* order, const unsigned 
                        uint32_t* vals, const double* tq, const CamDev& cam, cudaStream_t s,
                        const int* nd, unsigned long long cap) {
   if (r1 <= r0) return;
-  k_emit_pairs<<<(unsigned)((r1 - r0 + 7) / 8), 256, 0, s>>>(
-      rects, order, offsets, r0, r1, tiles_x, active, keys, vals, nd, cap, tq, cam);
+  if (r1 - r0 <= 262144)
+    k_emit_pairs<32><<<(unsigned)((r1 - r0 + 7) / 8), 256, 0, s>>>(
+        rects, order, offsets, r0, r1, tiles_x, active, keys, vals, nd, cap, tq, cam);
+  else
+    k_emit_pairs<8><<<(unsigned)((r1 - r0 + 31) / 32), 256, 0, s>>>(
+        rects, order, offsets, r0, r1, tiles_x, active, keys, vals, nd, cap, tq, cam);
 }
 void launch_pairs_total(const unsigned long long* offsets, const unsigned long long* counts,
                         int64_t n, unsigned long long cap, unsigned long long* total,
