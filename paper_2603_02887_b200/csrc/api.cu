@@ -47,6 +47,7 @@ void launch_pad_keys(uint32_t*, int64_t, const unsigned long long*, cudaStream_t
 void launch_gather_keys(const uint32_t*, const uint32_t*, int64_t, uint32_t*, cudaStream_t);
 void launch_clear_rects(const uint32_t*, int64_t, int64_t, int4*, cudaStream_t);
 void launch_iota(uint32_t*, int64_t, cudaStream_t);
+void launch_phase_bound(const unsigned long long*, int, float*, cudaStream_t);
 void launch_zlo_ranks(const float*, const float*, const float*, const float*, const uint32_t*,
                       int64_t, int64_t, const CamDev&, double, double*, cudaStream_t);
 void launch_project_ranks_z(const float*, const float*, const float*, const float*, const float*,
@@ -157,7 +158,8 @@ int set_last_error(int code, const char* msg) { return fail(code, msg); }
 struct nxs_view {
   // per Gaussian
   Buf dkeys_in, dkeys_out, idx_in, idx_out, records, bframe, rects, ntiles, offsets, moments,
-      touched, depth, k32a, k32b, k32c, rank_of, rank_c, zlo_rank, seq, ph_hist, ph_sel, tq, zlo64;
+      touched, depth, k32a, k32b, k32c, rank_of, rank_c, zlo_rank, seq, ph_hist, ph_sel, tq, zlo64,
+      xc_t, xc_r, xc_n;
   // per pair: sort scratch, and the sorted ranks of each depth phase
   Buf pk_in, pk_out, pv_in, pv_ph[MAX_PHASES];
   // per tile: phase ranges and virtual offsets, activity
@@ -216,7 +218,7 @@ struct nxs_view {
     Buf* all[] = {&dkeys_in, &dkeys_out, &idx_in,  &idx_out, &records, &bframe, &rects,
                   &ntiles,   &offsets,   &moments, &touched, &pk_in,   &pk_out,  &pv_in,  &active,
                   &depth,    &k32a,      &k32b,    &k32c,    &rank_of, &rank_c, &zlo_rank, &seq, &ph_hist,
-                  &ph_sel,   &tq,      &zlo64,
+                  &ph_sel,   &tq,      &zlo64,  &xc_t, &xc_r, &xc_n,
                   &c_last,   &c_sat,     &c_tk,    &c_thi,   &c_tlo,   &c_P,    &c_ck,
                   &c_Pck,    &c_ek,      &c_th0,   &r_rad,   &r_trem,  &r_count, &r_sea,
                   &r_sa,     &temp,      &dev_small};
@@ -618,13 +620,14 @@ int forward_impl(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
   int n_ph = 0;
   {
     int64_t r1;
-    if ((opts->flags & NXS_FLAG_FULL_BINNING) || exact)
+    if (opts->flags & NXS_FLAG_FULL_BINNING)
       r1 = P;
     else if (opts->first_phase_ranks > 0)
       r1 = opts->first_phase_ranks;
     else  // measured at C3: saturating models finish every tile within P/32
-          // ranks; exp never saturates and runs to the 128 cap
-      r1 = (md.fam == FAM_EXP) ? P / 4 : P / 32;
+          // ranks (P/16 by z_lo, the looser exact-order key); exp never
+          // saturates and runs to the 128 cap
+      r1 = (md.fam == FAM_EXP) ? P / 4 : (exact ? P / 16 : P / 32);
     r1 = std::max<int64_t>(r1, 4096);
     const int64_t unit = chunked ? opts->chunk_size : 1;
     auto up = [&](int64_t r) { return std::min(P, (r + unit - 1) / unit * unit); };
@@ -655,7 +658,7 @@ int forward_impl(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
   // device-sized phase 0 (no host sync before the first forward): needs
   // estimates from this view's previous call and a later phase to verify at
   bool async0 = v->est_n0 > 0 && v->est_pairs >= 0 && v->est_bin0 >= 0 && n_ph >= 2 &&
-                spec_phase >= 0 && !chunked;
+                spec_phase >= 0 && !chunked && !exact;
   int64_t proc_end = 0;  // chunked lazy phases: ranks [0, proc_end) are processed
   bool phase_full[MAX_PHASES] = {false, false, false, false};  // lazy phase sorted on 32 bits
   int phase_shift[MAX_PHASES] = {0, 0, 0, 0};
@@ -715,12 +718,16 @@ retry_sort:
   for (int i = 0; i <= n_ph; ++i) R[i] = Rplan[i];
   // lazy depth phases: the global order, and the chunked order (phases end
   // on chunk boundaries; each phase's chunks are z_lo-sorted when complete)
-  v->lazy = (!torder || (chunked && opts->chunk_size <= 2048)) && !sort64 &&
+  v->lazy = (!torder || exact || (chunked && opts->chunk_size <= 2048)) && !sort64 &&
             !(opts->flags & NXS_FLAG_FULL_BINNING) && P > 0;
   v->sorted_end = 0;
   v->proj_end = 0;
   v->bin_done = -1;
   proc_end = 0;
+  if (exact && !v->lazy) {  // the exact order phases only lazily (pending carry)
+    n_ph = 1;
+    R[1] = P;
+  }
   mark(v, 0, s);
   if (P > 0) {
     size_t tmp_sort = 0, tmp_scan = 0;
@@ -1085,11 +1092,22 @@ retry_sort:
                                  s);
             NXS_LAUNCHED("rank_of");
             if (v->ev_ok) rec_event(v, v->evp[ph][1], s);
-            launch_project_ranks(scene->centers, scene->scales, scene->quats, scene->opacities,
-                                 scene->sh, C, r0, r1, v->idx_out.as<uint32_t>(), cam,
-                                 opts->alpha_cutoff, opts->near_plane, v->rects.as<int4>(),
-                                 v->records.as<float4>(), v->bframe.as<float4>(), dsmall,
-                                 v->tq.as<double>(), s);
+            if (exact) {  // z_lo per rank for the pending-buffer bounds
+              NXS_CUDA(ensure_n<float>(v->zlo_rank, P));
+              launch_project_ranks_z(scene->centers, scene->scales, scene->quats,
+                                     scene->opacities, scene->sh, C, r0, r1,
+                                     v->idx_out.as<uint32_t>(), cam, opts->alpha_cutoff,
+                                     opts->near_plane, v->depth.as<double>(),
+                                     v->zlo_rank.as<float>(), v->rects.as<int4>(),
+                                     v->records.as<float4>(), v->bframe.as<float4>(), dsmall,
+                                     v->tq.as<double>(), s);
+            } else {
+              launch_project_ranks(scene->centers, scene->scales, scene->quats, scene->opacities,
+                                   scene->sh, C, r0, r1, v->idx_out.as<uint32_t>(), cam,
+                                   opts->alpha_cutoff, opts->near_plane, v->rects.as<int4>(),
+                                   v->records.as<float4>(), v->bframe.as<float4>(), dsmall,
+                                   v->tq.as<double>(), s);
+            }
             NXS_LAUNCHED("project_ranks");
             v->proj_end = r1;
           }
@@ -1195,6 +1213,19 @@ retry_sort:
       // ---- K3x exact/chunked-order forward of this phase
       NXS_CUDA(ensure_n<int32_t>(v->seq, npix * std::max(1, opts->max_splats)));  // [slot][pixel]
       if (n_ph > 1) NXS_CUDA(cudaMemsetAsync(n_active, 0, sizeof(unsigned int), s));
+      // exact order over several phases: pending entries cross the phase end
+      const bool xcarry = exact && n_ph > 1;
+      float* ebound = nullptr;
+      if (xcarry) {
+        NXS_CUDA(ensure_n<float>(v->xc_t, (int64_t)32 * npix));
+        NXS_CUDA(ensure_n<int32_t>(v->xc_r, (int64_t)32 * npix));
+        NXS_CUDA(ensure_n<int32_t>(v->xc_n, npix));
+        if (ph + 1 < n_ph) {
+          ebound = reinterpret_cast<float*>(v->ph_sel.as<long long>() + 90);
+          launch_phase_bound(dsmall + 6, ph_bin[ph], ebound, s);
+          NXS_LAUNCHED("phase_bound");
+        }
+      }
       FwdXArgs xa{v->records.as<float4>(), v->pv_ph[ph].as<uint32_t>(),
                   v->ranges_ph[ph].as<int2>(), v->zlo_rank.as<float>(), v->idx_out.as<uint32_t>(),
                   chunked ? v->rank_c.as<uint32_t>() : nullptr, chunked ? opts->chunk_size : 0,
@@ -1202,7 +1233,10 @@ retry_sort:
                   {bgf[0], bgf[1], bgf[2]}, rgb, overdraw, residual, v->seq.as<int32_t>(),
                   dsmall + 9, n_ph > 1 ? v->active.as<uint8_t>() : nullptr,
                   n_ph > 1 ? n_active : nullptr, ph > 0, ph + 1 < n_ph,
-                  (chunked && !(opts->flags & NXS_FLAG_XBUF32)) ? 16 : 32};
+                  (chunked && !(opts->flags & NXS_FLAG_XBUF32)) ? 16 : 32,
+                  xcarry ? v->xc_t.as<float>() : nullptr,
+                  xcarry ? v->xc_r.as<int32_t>() : nullptr,
+                  xcarry ? v->xc_n.as<int32_t>() : nullptr, ebound};
       launch_blend_fwd_x(count, n_tiles, xa, cam, md, v->cache(), v->resume(), cnt, s);
       NXS_LAUNCHED("blend_fwd_x");
       if (v->ev_ok) rec_event(v, v->evp[ph][4], s);

@@ -120,7 +120,9 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
                   float* __restrict__ residual, PixCache cache, PixResume rs,
                   int32_t* __restrict__ seq, unsigned long long* __restrict__ overflow,
                   uint8_t* __restrict__ active, unsigned int* __restrict__ n_active, bool resume,
-                  bool save, Counters* __restrict__ cnt) {
+                  bool save, float* __restrict__ carry_t, int32_t* __restrict__ carry_r,
+                  int32_t* __restrict__ carry_n, const float* __restrict__ end_bound,
+                  Counters* __restrict__ cnt) {
   const int tile = blockIdx.x;
   if (active && !active[tile]) return;  // finished in an earlier depth phase
   extern __shared__ float4 smem_dyn[];
@@ -176,6 +178,15 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
   // pending entries: a ring of XBUF slots, ascending by (t, index) from the
   // head; new entries (lists are in z_lo order) usually append at the tail
   int nb = 0, head = 0;
+  if (resume && inside && carry_n && !s.done) {
+    // pending entries carried over the phase end: list positions encode
+    // ranks as -1 - rank (their records are read from global memory)
+    nb = carry_n[pix];
+    for (int i = 0; i < nb; ++i) {
+      bt[i * TILE_PIX + tid] = carry_t[(size_t)i * npix + pix];
+      bp[i * TILE_PIX + tid] = -1 - carry_r[(size_t)i * npix + pix];
+    }
+  }
   uint32_t cur_chunk = 0;  // chunk of the pending entries (chunked order)
   unsigned long long ntest = 0;
   // ties in t: storage index (one chunk, reference argsort over arange(n)) or
@@ -197,13 +208,13 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
     float4 r[REC_F4];
     constexpr int K0 = keeps_alpha(XBUF) ? 4 : 0, K1 = keeps_alpha(XBUF) ? 7 : REC_F4;
     uint32_t rank;
-    if (pos >= ring_lo) {
+    if (pos >= ring_lo) {  // (carried entries have pos < 0 and take the global path)
       const float4* rec = s_ring[pos % (2 * XBATCH)];
       rank = s_ring_rank[pos % (2 * XBATCH)];
 #pragma unroll
       for (int k = K0; k < K1; ++k) r[k] = rec[k];
     } else {
-      rank = pairs[pos];
+      rank = pos < 0 ? (uint32_t)(-1 - pos) : pairs[pos];
       const float4* rec = records + (size_t)rank * REC_F4;
 #pragma unroll
       for (int k = K0; k < K1; ++k) r[k] = __ldg(rec + k);
@@ -275,7 +286,8 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
           bool later = te > tpk;  // the pending entry commits after the new one
           if (te == tpk) {
             if (gid_new == 0xffffffffu) gid_new = tie_key(s_rank[j]);
-            later = tie_key(pairs[bp[e * TILE_PIX + tid]]) > gid_new;
+            const int pe = bp[e * TILE_PIX + tid];
+            later = tie_key(pe < 0 ? (uint32_t)(-1 - pe) : pairs[pe]) > gid_new;
           }
           if (!later) break;
           const int f = (head + i) & (XBUF - 1);
@@ -293,8 +305,24 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
     }
     if (__syncthreads_count(!s.done) == 0) break;
   }
-  // end of the list (and of a chunk): everything pending is final, in order
-  while (nb > 0 && !s.done) commit_front();
+  // end of the list: everything pending is final, in order (one chunk, the
+  // end of a chunk, or the last depth phase) — or, with a later phase, only
+  // what lies in front of that phase's first z_lo; the rest is carried
+  if (end_bound && save) {
+    const float bound = *end_bound * hnorm;
+    while (nb > 0 && !s.done && bt[head * TILE_PIX + tid] < bound) commit_front();
+    if (inside && !s.done) {
+      carry_n[pix] = nb;
+      for (int i = 0; i < nb; ++i) {
+        const int e = (head + i) & (XBUF - 1);
+        const int pe = bp[e * TILE_PIX + tid];
+        carry_t[(size_t)i * npix + pix] = bt[e * TILE_PIX + tid];
+        carry_r[(size_t)i * npix + pix] = pe < 0 ? -1 - pe : (int32_t)pairs[pe];
+      }
+    }
+  } else {
+    while (nb > 0 && !s.done) commit_front();
+  }
   const int still = __syncthreads_count(!s.done);
   if (active && tid == 0) {
     active[tile] = still > 0 ? 1 : 0;
@@ -477,7 +505,8 @@ static void launch_fwd_x_xb(bool count, int n_tiles, const FwdXArgs& a, const Ca
   k<<<n_tiles, TILE_PIX, fwdx_smem(XB), s>>>(
       a.records, a.pairs, a.ranges, a.zlo_rank, a.order, a.rank_c, a.chunk, cam, m, a.max_splats,
       a.cutoff, a.near_plane, a.bg[0], a.bg[1], a.bg[2], a.rgb, a.overdraw, a.residual, cache, rs,
-      a.seq, a.overflow, a.active, a.n_active, a.resume, a.save, cnt);
+      a.seq, a.overflow, a.active, a.n_active, a.resume, a.save, a.carry_t, a.carry_r,
+      a.carry_n, a.end_bound, cnt);
 }
 
 template <int FAM>

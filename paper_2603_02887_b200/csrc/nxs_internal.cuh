@@ -143,6 +143,13 @@ struct FwdXArgs {
   unsigned int* n_active;
   bool resume, save;
   int xbuf;  // pending entries per pixel (16 or 32)
+  // exact order over depth phases: the pending entries of unfinished pixels
+  // cross the phase end ([slot][pixel] t and rank, per-pixel count), and
+  // *end_bound is a lower bound of every later phase's z_lo (null: commit all)
+  float* carry_t;
+  int32_t* carry_r;
+  int32_t* carry_n;
+  const float* end_bound;
 };
 struct BwdXArgs {
   const float4* records;

@@ -1069,6 +1069,23 @@ void launch_pack_check(const unsigned long long* dsmall, const long long* dsel, 
                        unsigned long long* out, cudaStream_t s) {
   k_pack_check<<<1, 32, 0, s>>>(dsmall, dsel, n_ph, out);
 }
+// exact order over depth phases: a lower bound of the depth key (z_lo) of
+// every Gaussian in the key bins after `bin` (the k_key32 map inverted, with
+// a relative safety margin; smaller is always safe), as float rounded down
+__global__ void k_phase_bound(const unsigned long long* __restrict__ kminmax, int bin,
+                              float* __restrict__ out) {
+  if (kminmax[0] < kminmax[1]) {
+    const double lo = dkey_inv(kminmax[0]), hi = dkey_inv(kminmax[1]);
+    const double step = (double)((unsigned long long)(bin + 1) << 20) / (4294967294.0 / (hi - lo));
+    const double b = (lo + step) - 1e-6 * (fabs(lo) + fabs(step));
+    *out = __double2float_rd(b);
+  } else {
+    *out = __int_as_float(0xff800000);  // -inf: nothing is final at the phase end
+  }
+}
+void launch_phase_bound(const unsigned long long* kminmax, int bin, float* out, cudaStream_t s) {
+  k_phase_bound<<<1, 1, 0, s>>>(kminmax, bin, out);
+}
 void launch_iota(uint32_t* a, int64_t n, cudaStream_t s) {
   if (n <= 0) return;
   k_iota<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a, n);

@@ -369,12 +369,13 @@ def test_near_plane_straddlers_match_oracle(name):
     assert massf == 0, (strict, massf, total)
 
 
-@pytest.mark.parametrize("cs", [1, 128])
+@pytest.mark.parametrize("cs", [1, 128, None])
 @pytest.mark.parametrize("name", ["exponential", "softplus_20", "blended_0.5"])
 def test_progressive_binning_is_bit_identical_to_full(name, cs):
     """Depth-phased binning (only still-active tiles get later ranks) must
     replay exactly the same entries per pixel as binning everything at once
-    (global order, and chunked order with phases cut on chunk boundaries)."""
+    (global order, chunked order with phases cut on chunk boundaries, and
+    the exact order with its pending entries carried over phase ends)."""
     import torch
     sc = O.round_scene_f32(O.canonical_scene(100_000, seed=1))
     cam = O.canonical_camera(512, 384, 2, 8)
