@@ -380,10 +380,15 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
 // K4x
 // ---------------------------------------------------------------------------
 constexpr int XRED_STRIDE = 36;
-constexpr size_t BWDX_SMEM = sizeof(float) * NMOM * XRED_STRIDE * (TILE_PIX / 32);
+constexpr size_t BWDX_SMEM = sizeof(float) * NMOM * XRED_STRIDE * (TILE_PIX / 2 / 32);
+
+// Two pixels per thread (rows r and r + 8, a 128-thread block per tile, as
+// K4): each warp step serves the largest pending rank over its 64 pixels,
+// and a thread adds both of its pixels' moments before the warp reduction.
+constexpr int BWDX_THREADS = TILE_PIX / 2;
 
 template <int FAM, bool COUNT>
-__global__ void __launch_bounds__(TILE_PIX)
+__global__ void __launch_bounds__(BWDX_THREADS)
     k_blend_bwd_x(const float4* __restrict__ records, const float4* __restrict__ bframe,
                   const uint32_t* __restrict__ pairs, const int32_t* __restrict__ seq,
                   int max_splats, CamDev cam, ModelDev m, float cutoff, double near_plane,
@@ -394,61 +399,76 @@ __global__ void __launch_bounds__(TILE_PIX)
   const int tile = blockIdx.x;
   const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
   const int tid = threadIdx.x, lane = tid & 31;
-  const int px = tx * TILE + (tid & (TILE - 1)), py = ty * TILE + (tid >> 4);
-  const bool inside = px < cam.W && py < cam.H;
-  BwdPix st;
-  bwd_load(st, cam, px, py, cache, seed, bg0, bg1, bg2);
+  const int px = tx * TILE + (tid & (TILE - 1)), py0 = ty * TILE + (tid >> 4);
+  BwdPix st[2];
+  const int32_t* myseq[2];
+  int ptr[2];
   const size_t npix = (size_t)cam.W * cam.H;
-  const int32_t* myseq = seq + (inside ? py * cam.W + px : 0);  // [slot][pixel]
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int py = py0 + q * (TILE / 2);
+    bwd_load(st[q], cam, px, py, cache, seed, bg0, bg1, bg2);
+    const bool inside = px < cam.W && py < cam.H;
+    myseq[q] = seq + (inside ? (size_t)py * cam.W + px : 0);  // [slot][pixel]
+    ptr[q] = st[q].last;  // commit index, back to front
+  }
   float* red = smem_red + (tid >> 5) * NMOM * XRED_STRIDE;
   const float gam = (FAM == FAM_EXP) ? 1.0f : m.c;
   const float inv_f = (float)(1.0 / cam.f);
   const float Y0 = (float)SH_C0;
   unsigned long long ntest = 0, nent = 0;
-  int ptr = st.last;  // commit index, back to front
+  int cur[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) cur[q] = ptr[q] >= 0 ? myseq[q][(size_t)ptr[q] * npix] : -1;
 
   while (true) {
-    const int cur = ptr >= 0 ? myseq[(size_t)ptr * npix] : -1;  // rank
-    const int wcur = __reduce_max_sync(0xffffffffu, cur);
+    const int wcur = __reduce_max_sync(0xffffffffu, max(cur[0], cur[1]));
     if (wcur < 0) break;
     if (COUNT && lane == 0) ++nent;
-    const bool mine = cur == wcur;
     const uint32_t rank = (uint32_t)wcur;  // warp-uniform
     float4 rec[REC_F4], bf[3];
 #pragma unroll
     for (int k = 0; k < REC_F4; ++k) rec[k] = __ldg(records + (size_t)rank * REC_F4 + k);
 #pragma unroll
     for (int k = 0; k < 3; ++k) bf[k] = __ldg(bframe + (size_t)rank * 3 + k);
-    float dm2 = 0.f, ux = 0.f, uy = 0.f, uz = 0.f, dak = 0.f, e0 = 0.f, e1 = 0.f, e2 = 0.f;
-    if (mine) {
-      bwd_pixel<FAM>(st, rec, bf, ptr, cam, m, cutoff, near_plane, inv_f, gam, dm2, ux, uy, uz,
-                     dak, e0, e1, e2, ntest, COUNT);
-      --ptr;
+    float dm2[2] = {0.f, 0.f}, ux[2] = {0.f, 0.f}, uy[2] = {0.f, 0.f}, uz[2] = {0.f, 0.f};
+    float dak[2] = {0.f, 0.f}, e0[2] = {0.f, 0.f}, e1[2] = {0.f, 0.f}, e2[2] = {0.f, 0.f};
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      if (cur[q] == wcur) {
+        bwd_pixel<FAM>(st[q], rec, bf, ptr[q], cam, m, cutoff, near_plane, inv_f, gam, dm2[q],
+                       ux[q], uy[q], uz[q], dak[q], e0[q], e1[q], e2[q], ntest, COUNT);
+        --ptr[q];
+        cur[q] = ptr[q] >= 0 ? myseq[q][(size_t)ptr[q] * npix] : -1;
+      }
     }
-    const float ax = dm2 * ux, ay = dm2 * uy, az = dm2 * uz;
+    const PixelConst& pa = st[0].pc;
+    const PixelConst& pb = st[1].pc;
+    const float ax = dm2[0] * ux[0], ay = dm2[0] * uy[0], az = dm2[0] * uz[0];
+    const float bx = dm2[1] * ux[1], by = dm2[1] * uy[1], bz = dm2[1] * uz[1];
     float* col = red + lane;
-    col[0 * XRED_STRIDE] = ax * ux;
-    col[1 * XRED_STRIDE] = ax * uy;
-    col[2 * XRED_STRIDE] = ax * uz;
-    col[3 * XRED_STRIDE] = ay * uy;
-    col[4 * XRED_STRIDE] = ay * uz;
-    col[5 * XRED_STRIDE] = az * uz;
-    col[6 * XRED_STRIDE] = ax;
-    col[7 * XRED_STRIDE] = ay;
-    col[8 * XRED_STRIDE] = az;
-    col[11 * XRED_STRIDE] = dak;
-    col[12 * XRED_STRIDE] = e0 * Y0;
-    col[13 * XRED_STRIDE] = e0 * st.pc.Y1;
-    col[14 * XRED_STRIDE] = e0 * st.pc.Y2;
-    col[15 * XRED_STRIDE] = e0 * st.pc.Y3;
-    col[16 * XRED_STRIDE] = e1 * Y0;
-    col[17 * XRED_STRIDE] = e1 * st.pc.Y1;
-    col[18 * XRED_STRIDE] = e1 * st.pc.Y2;
-    col[19 * XRED_STRIDE] = e1 * st.pc.Y3;
-    col[20 * XRED_STRIDE] = e2 * Y0;
-    col[21 * XRED_STRIDE] = e2 * st.pc.Y1;
-    col[22 * XRED_STRIDE] = e2 * st.pc.Y2;
-    col[23 * XRED_STRIDE] = e2 * st.pc.Y3;
+    col[0 * XRED_STRIDE] = fmaf(ax, ux[0], bx * ux[1]);
+    col[1 * XRED_STRIDE] = fmaf(ax, uy[0], bx * uy[1]);
+    col[2 * XRED_STRIDE] = fmaf(ax, uz[0], bx * uz[1]);
+    col[3 * XRED_STRIDE] = fmaf(ay, uy[0], by * uy[1]);
+    col[4 * XRED_STRIDE] = fmaf(ay, uz[0], by * uz[1]);
+    col[5 * XRED_STRIDE] = fmaf(az, uz[0], bz * uz[1]);
+    col[6 * XRED_STRIDE] = ax + bx;
+    col[7 * XRED_STRIDE] = ay + by;
+    col[8 * XRED_STRIDE] = az + bz;
+    col[11 * XRED_STRIDE] = dak[0] + dak[1];
+    col[12 * XRED_STRIDE] = (e0[0] + e0[1]) * Y0;
+    col[13 * XRED_STRIDE] = fmaf(e0[0], pa.Y1, e0[1] * pb.Y1);
+    col[14 * XRED_STRIDE] = fmaf(e0[0], pa.Y2, e0[1] * pb.Y2);
+    col[15 * XRED_STRIDE] = fmaf(e0[0], pa.Y3, e0[1] * pb.Y3);
+    col[16 * XRED_STRIDE] = (e1[0] + e1[1]) * Y0;
+    col[17 * XRED_STRIDE] = fmaf(e1[0], pa.Y1, e1[1] * pb.Y1);
+    col[18 * XRED_STRIDE] = fmaf(e1[0], pa.Y2, e1[1] * pb.Y2);
+    col[19 * XRED_STRIDE] = fmaf(e1[0], pa.Y3, e1[1] * pb.Y3);
+    col[20 * XRED_STRIDE] = (e2[0] + e2[1]) * Y0;
+    col[21 * XRED_STRIDE] = fmaf(e2[0], pa.Y1, e2[1] * pb.Y1);
+    col[22 * XRED_STRIDE] = fmaf(e2[0], pa.Y2, e2[1] * pb.Y2);
+    col[23 * XRED_STRIDE] = fmaf(e2[0], pa.Y3, e2[1] * pb.Y3);
     __syncwarp();
     if (lane < NMOM && lane != 9 && lane != 10) {
       const float4* row = reinterpret_cast<const float4*>(red + lane * XRED_STRIDE);
@@ -544,7 +564,7 @@ static void launch_bwd_x_fam(bool count, int n_tiles, const BwdXArgs& a, const C
     attr = true;
   }
   auto k = count ? k_blend_bwd_x<FAM, true> : k_blend_bwd_x<FAM, false>;
-  k<<<n_tiles, TILE_PIX, BWDX_SMEM, s>>>(a.records, a.bframe, a.pairs, a.seq, a.max_splats, cam, m,
+  k<<<n_tiles, BWDX_THREADS, BWDX_SMEM, s>>>(a.records, a.bframe, a.pairs, a.seq, a.max_splats, cam, m,
                                          a.cutoff, a.near_plane, a.bg[0], a.bg[1], a.bg[2],
                                          a.seed, cache, a.moments, a.touched, cnt);
 }
