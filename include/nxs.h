@@ -190,18 +190,24 @@ int nxs_cache_export(nxs_view* view, uint8_t* sat, float* e_k, float* t_k,
                      float* theta0, void* stream);
 
 /* Front-to-back depth order of the last forward: order (P int32, device),
- * order[rank] = Gaussian index, stable by fp64 view depth (render.py:355-357). */
+ * order[rank] = Gaussian index, stable by fp64 view depth (render.py:355-357).
+ * The global order sorts lazily (only the depth phases the image needed);
+ * this call completes the order of the remaining ranks first.  (Chunked and
+ * exact orders: the ranks of the list order the blend used.) */
 int nxs_depth_order(nxs_view* view, int32_t* order, void* stream);
 
 /* Binning of the last forward, for the bit-exact checks against the C
  * restatement (oracle/binning_oracle.c): tile rectangle per Gaussian in
- * storage order (P x int32[4] = tx0,ty0,tx1,ty1; empty = -1), and the FIRST depth
+ * storage order (P x int32[4] = tx0,ty0,tx1,ty1; empty = -1; Gaussians
+ * outside the projected depth phases read empty), and the FIRST depth
  * phase's tile ranges (n_tiles x int32[2]) and sorted pair values; with
  * NXS_FLAG_FULL_BINNING that phase holds every rank (n_pairs ranks). */
 int nxs_binning_export(nxs_view* view, int32_t* rects, int32_t* ranges,
                        int32_t* pair_ranks, void* stream);
 
-/* Projected per-rank records (P x 32 float32) of the last forward. */
+/* Projected per-rank records (P x 32 float32) of the last forward; only the
+ * ranks of the processed depth phases are defined (NXS_FLAG_FULL_BINNING
+ * projects every rank). */
 int nxs_records_export(nxs_view* view, float* records, void* stream);
 
 /* ---- train-step neighbours ---------------------------- */
