@@ -451,6 +451,7 @@ int nxs_view_create(nxs_view** out) {
     cudaGetLastError();
     return fail(NXS_ERR_CUDA, "cudaHostAlloc failed (no CUDA device?)");
   }
+  std::memset(v->host_small, 0, 32 * sizeof(unsigned long long));
   v->ev_ok = true;
   for (auto& e : v->ev) v->ev_ok = v->ev_ok && cudaEventCreate(&e) == cudaSuccess;
   for (auto& row : v->evp)
@@ -606,7 +607,8 @@ int forward_impl(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
   NXS_CUDA(ensure_n<float>(v->c_th0, npix * 3));
   NXS_CUDA(v->dev_small.ensure(16 * sizeof(unsigned long long)));
   // dsmall: [0] straddle count, [1..4] event counters, [5] active tiles (u32),
-  // [6] min depth key, [7] max depth key, [8] key-run overflow
+  // [6] min depth key, [7] max depth key, [8] key-run overflow, [12] last
+  // rank the finished tiles needed (global order)
   unsigned long long* dsmall = v->dev_small.as<unsigned long long>();
   Counters* cnt = reinterpret_cast<Counters*>(dsmall + 1);
   unsigned int* n_active = reinterpret_cast<unsigned int*>(dsmall + 5);
@@ -628,6 +630,17 @@ int forward_impl(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
           // ranks (P/16 by z_lo, the looser exact-order key); exp never
           // saturates and runs to the 128 cap
       r1 = (md.fam == FAM_EXP) ? P / 4 : (exact ? P / 16 : P / 32);
+    if (!(opts->flags & NXS_FLAG_FULL_BINNING) && opts->first_phase_ranks <= 0 && !chunked &&
+        !exact) {
+      // global order: this view's previous call reported the last rank its
+      // finished tiles needed (host_small[30], copied behind that forward);
+      // a first phase covering it (plus headroom) avoids a second phase.
+      // The hint only moves phase boundaries, never the result.
+      const int64_t need = (int64_t)v->host_small[30];
+      if (need > 0 && need < P && need + 1 > r1) r1 = need + 1 + need / 8 + 4096;
+      // device-sized phase-0 estimates that fell short: size exactly again
+      if (need > 0 && v->est_n0 > 0 && need >= v->est_n0) v->est_n0 = 0;
+    }
     r1 = std::max<int64_t>(r1, 4096);
     const int64_t unit = chunked ? opts->chunk_size : 1;
     auto up = [&](int64_t r) { return std::min(P, (r + unit - 1) / unit * unit); };
@@ -1249,7 +1262,7 @@ retry_sort:
                v->cum_ph[ph].as<int32_t>(), v->cum_ph[ph + 1].as<int32_t>(),
                v->active.as<uint8_t>(), n_active, ph > 0, ph + 1 < n_ph, opts->max_splats,
                (float)opts->alpha_cutoff, opts->near_plane, {bgf[0], bgf[1], bgf[2]},
-               rgb, overdraw, residual};
+               rgb, overdraw, residual, v->lazy ? dsmall + 12 : nullptr};
     launch_blend_fwd(count, n_tiles, fa, cam, md, v->cache(), v->resume(), cnt, s);
     NXS_LAUNCHED("blend_fwd");
     if (v->ev_ok) rec_event(v, v->evp[ph][4], s);
@@ -1277,6 +1290,9 @@ retry_sort:
     }
   }
   mark(v, 7, s);
+  if (v->lazy && !torder)  // the next call's first-phase hint (read without a sync)
+    NXS_CUDA(cudaMemcpyAsync(v->host_small + 30, dsmall + 12, sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, s));
   v->ev_fwd = true;
   v->ev_bwd = false;
   v->stats.n_pairs = total_pairs;

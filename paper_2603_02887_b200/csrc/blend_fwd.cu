@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(TILE_PIX, 3)
                 int max_splats, float cutoff, double near_plane, float bg0, float bg1, float bg2,
                 float* __restrict__ rgb, int32_t* __restrict__ overdraw,
                 float* __restrict__ residual, PixCache cache, PixResume rs,
-                Counters* __restrict__ cnt) {
+                unsigned long long* __restrict__ need_rank, Counters* __restrict__ cnt) {
   const int tile = blockIdx.x;
   if (!active[tile]) return;  // every pixel of the tile finished in an earlier phase
   // two 64-entry record buffers: the next batch streams in (cp.async)
@@ -94,6 +94,7 @@ __global__ void __launch_bounds__(TILE_PIX, 3)
   };
   if (rg.x < rg.y) stage(0, rg.x);
   int buf = 0;
+  int dpos = -1;  // list position of the entry that finished this pixel
   for (int base = rg.x; base < rg.y; base += FWD_BATCH, buf ^= 1) {
     const int n = min(FWD_BATCH, rg.y - base);
     if (base + FWD_BATCH < rg.y) {
@@ -137,6 +138,7 @@ __global__ void __launch_bounds__(TILE_PIX, 3)
           tk = Trem;
           sat = true;
           done = true;
+          dpos = base + j;
           break;
         }
         rad0 = fmaf(wr, E0, rad0);
@@ -166,6 +168,7 @@ __global__ void __launch_bounds__(TILE_PIX, 3)
         }
         if (count >= max_splats) {
           done = true;
+          dpos = base + j;
           break;
         }
       }
@@ -174,11 +177,17 @@ __global__ void __launch_bounds__(TILE_PIX, 3)
     if (__syncthreads_count(!done) == 0) break;
   }
   cp_async_wait<0>();
+  __shared__ int s_dpos;
+  if (tid == 0) s_dpos = -1;
   const int still = __syncthreads_count(!done);
+  if (still == 0 && need_rank && dpos >= 0) atomicMax(&s_dpos, dpos);
+  __syncthreads();
   if (tid == 0) {
     active[tile] = still > 0 ? 1 : 0;
     cum_out[tile] = cum_in[tile] + (rg.y - rg.x);
     if (still > 0) atomicAdd(n_active, 1u);
+    // the last rank this finished tile needed (the list is in rank order)
+    else if (need_rank && s_dpos >= 0) atomicMax(need_rank, (unsigned long long)pairs[s_dpos]);
   }
 
   if (COUNT) {
@@ -237,7 +246,7 @@ static void launch_fwd_fam(bool count, int n_tiles, const FwdArgs& a, const CamD
   k<<<n_tiles, TILE_PIX, 0, s>>>(a.records, a.pairs, a.ranges, a.cum_in, a.cum_out, a.active,
                                  a.n_active, a.resume, a.save, cam, m, a.max_splats, a.cutoff,
                                  a.near_plane, a.bg[0], a.bg[1], a.bg[2], a.rgb, a.overdraw,
-                                 a.residual, cache, rs, cnt);
+                                 a.residual, cache, rs, a.need_rank, cnt);
 }
 
 void launch_blend_fwd(bool count, int n_tiles, const FwdArgs& a, const CamDev& cam,

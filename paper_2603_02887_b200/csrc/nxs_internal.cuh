@@ -117,6 +117,9 @@ struct FwdArgs {
   float* rgb;
   int32_t* overdraw;
   float* residual;
+  // max over the tiles finishing in this pass of the last rank their list
+  // needed (the view's first-phase hint for its next call), or null
+  unsigned long long* need_rank;
 };
 
 // exact-order mode (K3x/K4x)
