@@ -630,10 +630,9 @@ int forward_impl(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
           // ranks (P/16 by z_lo, the looser exact-order key); exp never
           // saturates and runs to the 128 cap
       r1 = (md.fam == FAM_EXP) ? P / 4 : (exact ? P / 16 : P / 32);
-    if (!(opts->flags & NXS_FLAG_FULL_BINNING) && opts->first_phase_ranks <= 0 && !chunked &&
-        !exact) {
-      // global order: this view's previous call reported the last rank its
-      // finished tiles needed (host_small[30], copied behind that forward);
+    if (!(opts->flags & NXS_FLAG_FULL_BINNING) && opts->first_phase_ranks <= 0) {
+      // this view's previous call reported the last rank its finished tiles
+      // needed (host_small[30], copied behind that forward);
       // a first phase covering it (plus headroom) avoids a second phase.
       // The hint only moves phase boundaries, never the result.
       const int64_t need = (int64_t)v->host_small[30];
@@ -1249,7 +1248,8 @@ retry_sort:
                   (chunked && !(opts->flags & NXS_FLAG_XBUF32)) ? 16 : 32,
                   xcarry ? v->xc_t.as<float>() : nullptr,
                   xcarry ? v->xc_r.as<int32_t>() : nullptr,
-                  xcarry ? v->xc_n.as<int32_t>() : nullptr, ebound};
+                  xcarry ? v->xc_n.as<int32_t>() : nullptr, ebound,
+                  v->lazy ? dsmall + 12 : nullptr};
       launch_blend_fwd_x(count, n_tiles, xa, cam, md, v->cache(), v->resume(), cnt, s);
       NXS_LAUNCHED("blend_fwd_x");
       if (v->ev_ok) rec_event(v, v->evp[ph][4], s);
@@ -1290,7 +1290,7 @@ retry_sort:
     }
   }
   mark(v, 7, s);
-  if (v->lazy && !torder)  // the next call's first-phase hint (read without a sync)
+  if (v->lazy)  // the next call's first-phase hint (read without a sync)
     NXS_CUDA(cudaMemcpyAsync(v->host_small + 30, dsmall + 12, sizeof(unsigned long long),
                              cudaMemcpyDeviceToHost, s));
   v->ev_fwd = true;

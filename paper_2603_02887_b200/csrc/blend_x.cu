@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
                   uint8_t* __restrict__ active, unsigned int* __restrict__ n_active, bool resume,
                   bool save, float* __restrict__ carry_t, int32_t* __restrict__ carry_r,
                   int32_t* __restrict__ carry_n, const float* __restrict__ end_bound,
-                  Counters* __restrict__ cnt) {
+                  unsigned long long* __restrict__ need_rank, Counters* __restrict__ cnt) {
   const int tile = blockIdx.x;
   if (active && !active[tile]) return;  // finished in an earlier depth phase
   extern __shared__ float4 smem_dyn[];
@@ -174,6 +174,8 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
     s.ek2 = cache.e_k[3 * pix + 2];
   }
   s.done = !inside || s.sat || s.count >= max_splats;
+  const bool done0 = s.done;
+  int dpos = -1;  // list position being examined when the pixel finished
   const int count0 = s.count;
   // pending entries: a ring of XBUF slots, ascending by (t, index) from the
   // head; new entries (lists are in z_lo order) usually append at the tail
@@ -264,7 +266,10 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
           commit_front();
           if (s.done) break;
         }
-        if (s.done) break;
+        if (s.done) {
+          dpos = base + j;
+          break;
+        }
         cur_chunk = s_chunk[j];
         if (COUNT) ++ntest;
         TestOut t;
@@ -274,7 +279,10 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
           // overflow: the order is no longer guaranteed for this pixel
           atomicAdd(overflow, 1ull);
           commit_front();
-          if (s.done) break;
+          if (s.done) {
+            dpos = base + j;
+            break;
+          }
         }
         // insert (t, index) keeping the ring ascending from the head
         const int pos = base + j;
@@ -323,10 +331,21 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
   } else {
     while (nb > 0 && !s.done) commit_front();
   }
+  // finished by the commits at the list end: it needed the whole list
+  if (s.done && !done0 && dpos < 0 && rg.y > rg.x) dpos = rg.y - 1;
+  __shared__ int s_dpos;
+  if (tid == 0) s_dpos = -1;
   const int still = __syncthreads_count(!s.done);
-  if (active && tid == 0) {
-    active[tile] = still > 0 ? 1 : 0;
-    if (still > 0) atomicAdd(n_active, 1u);
+  if (still == 0 && need_rank && dpos >= 0) atomicMax(&s_dpos, dpos);
+  __syncthreads();
+  if (tid == 0) {
+    if (active) {
+      active[tile] = still > 0 ? 1 : 0;
+      if (still > 0) atomicAdd(n_active, 1u);
+    }
+    // the last rank this finished tile needed (lists are in rank order)
+    if (still == 0 && need_rank && s_dpos >= 0)
+      atomicMax(need_rank, (unsigned long long)pairs[s_dpos]);
   }
 
   if (COUNT) {
@@ -526,7 +545,7 @@ static void launch_fwd_x_xb(bool count, int n_tiles, const FwdXArgs& a, const Ca
       a.records, a.pairs, a.ranges, a.zlo_rank, a.order, a.rank_c, a.chunk, cam, m, a.max_splats,
       a.cutoff, a.near_plane, a.bg[0], a.bg[1], a.bg[2], a.rgb, a.overdraw, a.residual, cache, rs,
       a.seq, a.overflow, a.active, a.n_active, a.resume, a.save, a.carry_t, a.carry_r,
-      a.carry_n, a.end_bound, cnt);
+      a.carry_n, a.end_bound, a.need_rank, cnt);
 }
 
 template <int FAM>

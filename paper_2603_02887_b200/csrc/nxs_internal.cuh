@@ -153,6 +153,7 @@ struct FwdXArgs {
   int32_t* carry_r;
   int32_t* carry_n;
   const float* end_bound;
+  unsigned long long* need_rank;  // as FwdArgs::need_rank
 };
 struct BwdXArgs {
   const float4* records;
