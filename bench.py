@@ -247,7 +247,10 @@ def main():
 
     # ---- per-phase device timings (same steps, events inside the library)
     views = rv.views
+    for v in my_views:  # phase events only here (they cost the pipeline a few us)
+        views[v].set_timing(True)
     phase_tot = {}
+    step()
     for _ in range(max(3, min(a.steps, 10))):
         step()
         for v in my_views:

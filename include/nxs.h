@@ -154,8 +154,12 @@ int nxs_view_stats(const nxs_view* view, nxs_stats* out);
 /* bytes of device memory currently held by the view */
 int64_t nxs_view_bytes(const nxs_view* view);
 
+/* Phase timing (CUDA events between the pipeline's phases) is off by
+ * default: each event costs the device pipeline a few microseconds.  on != 0
+ * records them from the next call on. */
+int nxs_view_set_timing(nxs_view* view, int on);
 /* Milliseconds per phase (NXS_PHASES entries) of the last nxs_forward /
- * nxs_backward of this view; waits for those phases to finish. */
+ * nxs_backward of this view (timing on); waits for those phases to finish. */
 int nxs_view_timings(nxs_view* view, float* ms, int n);
 
 /* Forward render (render_forward_cached).  background: 3 host floats.

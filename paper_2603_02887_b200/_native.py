@@ -36,6 +36,7 @@ SYMBOLS = (
     "nxs_view_stats",
     "nxs_view_bytes",
     "nxs_view_timings",
+    "nxs_view_set_timing",
     "nxs_forward",
     "nxs_backward",
     "nxs_forward_backward",
@@ -147,6 +148,7 @@ def lib():
     h.nxs_view_bytes.argtypes = [vp]
     h.nxs_view_bytes.restype = i64
     h.nxs_view_timings.argtypes = [vp, C.POINTER(C.c_float), C.c_int]
+    h.nxs_view_set_timing.argtypes = [vp, C.c_int]
     h.nxs_forward.argtypes = [vp, C.POINTER(Scene), C.POINTER(Camera), C.POINTER(Model),
                               C.POINTER(Opts), C.POINTER(C.c_float), vp, vp, vp, vp]
     h.nxs_backward.argtypes = [vp, C.POINTER(Scene), vp, vp, vp, vp, vp, vp, vp]
@@ -283,8 +285,15 @@ class View:
     PHASES = ("depth_sort", "project", "binning", "blend_fwd", "n_depth_phases",
               "fwd_bwd_gap", "forward_total", "moment_clear", "blend_bwd", "chain")
 
+    def set_timing(self, on: bool = True) -> "View":
+        """Record per-phase CUDA events from the next call on (off by
+        default: every event costs the device pipeline a few microseconds)."""
+        _check(self._h.nxs_view_set_timing(self._p, 1 if on else 0))
+        return self
+
     def timings(self) -> dict:
-        """Device milliseconds per phase of the last forward/backward."""
+        """Device milliseconds per phase of the last forward/backward
+        (needs :meth:`set_timing`)."""
         arr = (C.c_float * len(self.PHASES))()
         _check(self._h.nxs_view_timings(self._p, arr, len(self.PHASES)))
         return {n: float(arr[i]) for i, n in enumerate(self.PHASES) if not n.startswith("_")}

@@ -14,9 +14,36 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
+#include <chrono>
+
+// NXS_HOST_TIMING=1: host-side time between points of one fused call,
+// printed to stderr (diagnostics only)
+namespace {
+struct HostTimer {
+  bool on = std::getenv("NXS_HOST_TIMING") != nullptr;
+  int n = 0;
+  const char* lab[32];
+  std::chrono::steady_clock::time_point t[32];
+  void mark(const char* l) {
+    if (!on || n >= 32) return;
+    lab[n] = l;
+    t[n++] = std::chrono::steady_clock::now();
+  }
+  void dump() {
+    if (!on) return;
+    for (int i = 1; i < n; ++i)
+      std::fprintf(stderr, "%s %.1f | ", lab[i],
+                   std::chrono::duration<double, std::micro>(t[i] - t[i - 1]).count());
+    std::fprintf(stderr, "\n");
+    n = 0;
+  }
+};
+HostTimer g_ht;
+}  // namespace
 
 #include "../../include/nxs.h"
 #include "nxs_internal.cuh"
@@ -56,6 +83,8 @@ void launch_project_ranks_z(const float*, const float*, const float*, const floa
                             double*, cudaStream_t);
 void launch_pack_check(const unsigned long long*, const long long*, int, unsigned long long*,
                        cudaStream_t);
+void launch_call_init(unsigned long long*, uint8_t*, int32_t*, int2*, int, long long*,
+                      const int64_t*, int, cudaStream_t);
 void launch_chunk_key(const float*, const float*, const float*, const float*, int64_t,
                       const CamDev&, double, const uint32_t*, int, double*, unsigned long long*,
                       uint32_t*, cudaStream_t);
@@ -176,6 +205,7 @@ struct nxs_view {
   // (both lazy phases only), [3] after binning, [4] after the forward blend
   cudaEvent_t evp[MAX_PHASES][5] = {};
   bool ev_ok = false;
+  bool timing = false;  // record the phase events (nxs_view_set_timing)
   bool ev_fwd = false, ev_bwd = false;
   cudaEvent_t ev_sync = nullptr;  // host-side polling for the in-pipeline syncs
   // state of the last forward
@@ -205,6 +235,10 @@ struct nxs_view {
   bool async_pending = false;  // phase 0 ran device-sized, not yet verified
   cudaGraphExec_t gexec = nullptr;  // the device-sized phase 0, replayed as one graph
   cudaStream_t cap_stream = nullptr;  // capture happens on this (non-default) stream
+  // small device->host reads that must not sit between two pipeline kernels
+  // run on this stream, ordered after the work they read by ev_side
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_side = nullptr;
   bool capturing = false;
   int n_phases_plan = 0;       // planned depth phases of the last forward
   int64_t async_cap0 = 0, async_capp = 0;
@@ -235,6 +269,8 @@ struct nxs_view {
     if (ev_sync) cudaEventDestroy(ev_sync);
     if (gexec) cudaGraphExecDestroy(gexec);
     if (cap_stream) cudaStreamDestroy(cap_stream);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
+    if (ev_side) cudaEventDestroy(ev_side);
     if (ev_ok) {
       for (auto& e : ev) cudaEventDestroy(e);
       for (auto& row : evp)
@@ -351,6 +387,7 @@ cudaError_t spin_sync(nxs_view* v, cudaStream_t s) {
 // timing events: inside a stream capture they must be external event
 // nodes to stay observable from the host
 inline void rec_event(nxs_view* v, cudaEvent_t e, cudaStream_t s) {
+  if (!v->timing) return;  // (an event node costs the pipeline a few us)
   if (v->capturing)
     cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
   else
@@ -358,7 +395,7 @@ inline void rec_event(nxs_view* v, cudaEvent_t e, cudaStream_t s) {
 }
 
 inline void mark(nxs_view* v, int i, cudaStream_t s) {
-  if (v->ev_ok) rec_event(v, v->ev[i], s);
+  if (v->ev_ok && v->timing) rec_event(v, v->ev[i], s);
 }
 
 template <class T>
@@ -499,16 +536,41 @@ namespace {
 // pair total.  The copies are enqueued (and v->ev_sync recorded) by
 // enqueue_async_check; finish_async_check waits for them: ok == false means
 // some capacity was exceeded and the pass must be redone with exact sizes.
+// the copy stream, ordered after everything enqueued on s so far (s itself
+// when the side stream cannot be created)
+cudaError_t side_after(nxs_view* v, cudaStream_t s, cudaStream_t& out) {
+  out = s;
+  if (v->capturing) return cudaSuccess;
+  if (!v->copy_stream &&
+      cudaStreamCreateWithFlags(&v->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    v->copy_stream = nullptr;
+    return cudaGetLastError(), cudaSuccess;
+  }
+  if (!v->ev_side &&
+      cudaEventCreateWithFlags(&v->ev_side, cudaEventDisableTiming) != cudaSuccess) {
+    v->ev_side = nullptr;
+    return cudaGetLastError(), cudaSuccess;
+  }
+  cudaError_t e = cudaEventRecord(v->ev_side, s);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(v->copy_stream, v->ev_side, 0);
+  if (e == cudaSuccess) out = v->copy_stream;
+  return e;
+}
+
 int enqueue_async_check(nxs_view* v, int n_ph, cudaStream_t s) {
-  // one small kernel packs the values into host_small's layout, one copy
+  // one small kernel packs the values into host_small's layout (in the
+  // pipeline, ahead of the backward that would hold every SM), one copy on
+  // the side stream (the backward does not wait for it)
   unsigned long long* dsmall = v->dev_small.as<unsigned long long>();
   long long* dsel = v->ph_sel.as<long long>();
   unsigned long long* pack = reinterpret_cast<unsigned long long*>(dsel + 56);
   launch_pack_check(dsmall, dsel, n_ph, pack, s);
   NXS_LAUNCHED("pack_check");
+  cudaStream_t cs;
+  NXS_CUDA(side_after(v, s, cs));
   NXS_CUDA(cudaMemcpyAsync(v->host_small, pack, 27 * sizeof(unsigned long long),
-                           cudaMemcpyDeviceToHost, s));
-  NXS_CUDA(cudaEventRecord(v->ev_sync, s));
+                           cudaMemcpyDeviceToHost, cs));
+  NXS_CUDA(cudaEventRecord(v->ev_sync, cs));
   return NXS_OK;
 }
 
@@ -612,8 +674,16 @@ int forward_impl(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
   unsigned long long* dsmall = v->dev_small.as<unsigned long long>();
   Counters* cnt = reinterpret_cast<Counters*>(dsmall + 1);
   unsigned int* n_active = reinterpret_cast<unsigned int*>(dsmall + 5);
-  NXS_CUDA(cudaMemsetAsync(dsmall, 0, 16 * sizeof(unsigned long long), s));
-  NXS_CUDA(cudaMemsetAsync(v->active.p, 1, (size_t)n_tiles, s));
+  NXS_CUDA(ensure_n<int2>(v->ranges_ph[0], n_tiles));
+  NXS_CUDA(ensure_n<int32_t>(v->cum_ph[0], n_tiles));
+  NXS_CUDA(v->ph_hist.ensure(4096 * sizeof(unsigned int)));
+  NXS_CUDA(v->ph_sel.ensure(96 * sizeof(long long)));
+  if (P == 0) {  // (P > 0: k_call_init below, in the pipeline)
+    NXS_CUDA(cudaMemsetAsync(dsmall, 0, 16 * sizeof(unsigned long long), s));
+    NXS_CUDA(cudaMemsetAsync(v->active.p, 1, (size_t)n_tiles, s));
+    NXS_CUDA(cudaMemsetAsync(v->cum_ph[0].p, 0, (size_t)n_tiles * 4, s));
+    NXS_CUDA(cudaMemsetAsync(v->ranges_ph[0].p, 0, (size_t)n_tiles * sizeof(int2), s));
+  }
 
   // ---- depth phases [R_p, R_{p+1}): R_1 = first phase, then x8.  The
   // chunked order cuts phases on chunk boundaries (nothing is pending
@@ -674,6 +744,7 @@ int forward_impl(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
   int64_t proc_end = 0;  // chunked lazy phases: ranks [0, proc_end) are processed
   bool phase_full[MAX_PHASES] = {false, false, false, false};  // lazy phase sorted on 32 bits
   int phase_shift[MAX_PHASES] = {0, 0, 0, 0};
+  g_ht.mark("setup");
 retry_sort:
   if (sort64) async0 = false;
   v->async_pending = false;
@@ -721,6 +792,7 @@ retry_sort:
     // stream, which cannot capture); the graph is launched on the caller's
     if (!v->cap_stream) NXS_CUDA(cudaStreamCreateWithFlags(&v->cap_stream, cudaStreamNonBlocking));
     s = v->cap_stream;
+    g_ht.mark("presize");
     NXS_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
     cap.s = s;
     cap.on = true;
@@ -771,9 +843,16 @@ retry_sort:
       tmp_sort = std::max(tmp_sort, tmp_sel);
     }
     NXS_CUDA(v->temp.ensure(std::max(tmp_sort, tmp_scan)));
+    // ---- counters, tile flags, phase-0 ranges/carry and the phase targets
+    {
+      int64_t tgt[4] = {0, 0, 0, 0};
+      for (int p = 1; p < n_ph && p <= 4; ++p) tgt[p - 1] = R[p];
+      launch_call_init(dsmall, v->active.as<uint8_t>(), v->cum_ph[0].as<int32_t>(),
+                       v->ranges_ph[0].as<int2>(), n_tiles,
+                       v->lazy ? v->ph_sel.as<long long>() + 32 : nullptr, tgt, n_ph - 1, s);
+      NXS_LAUNCHED("call_init");
+    }
     // ---- K0 depth (+ min/max) and the stable depth sort
-    NXS_CUDA(cudaMemsetAsync(dsmall + 6, 0xff, sizeof(unsigned long long), s));
-    NXS_CUDA(cudaMemsetAsync(dsmall + 7, 0, 2 * sizeof(unsigned long long), s));
     launch_depth(scene->centers, scene->scales, scene->quats, scene->opacities, P, cam,
                  opts->alpha_cutoff, exact ? 1 : 0, v->depth.as<double>(),
                  v->dkeys_in.as<unsigned long long>(), v->idx_in.as<uint32_t>(), dsmall + 6, s);
@@ -788,19 +867,12 @@ retry_sort:
       // phase boundaries on whole key bins: one host sync for their ranks
       launch_key32(v->depth.as<double>(), P, dsmall + 6, v->k32a.as<uint32_t>(), s);
       NXS_LAUNCHED("key32");
-      NXS_CUDA(v->ph_hist.ensure(4096 * sizeof(unsigned int)));
-      NXS_CUDA(v->ph_sel.ensure(96 * sizeof(long long)));
       launch_key_hist(v->k32a.as<uint32_t>(), P, v->ph_hist.as<unsigned int>(), s);
       NXS_LAUNCHED("key_hist");
-      int64_t* tgt = reinterpret_cast<int64_t*>(v->host_small + 8);
-      for (int p = 1; p < n_ph; ++p) tgt[p - 1] = R[p];
-      long long* dsel = v->ph_sel.as<long long>();
-      NXS_CUDA(cudaMemcpyAsync(dsel + 32, tgt, sizeof(int64_t) * (n_ph - 1 > 0 ? n_ph - 1 : 1),
-                               cudaMemcpyHostToDevice, s));
+      long long* dsel = v->ph_sel.as<long long>();  // [32..) phase targets (k_call_init)
       if (async0) {
         // phase 0 sized from the previous call; the last bin it may use is
         // checked on the device (k_phase_select) and verified later
-        NXS_CUDA(cudaMemsetAsync(dsmall + 10, 0, 2 * sizeof(unsigned long long), s));
         ph_bin[0] = std::min(4095, v->est_bin0 + 2);
         launch_phase_select(v->ph_hist.as<unsigned int>(), reinterpret_cast<int64_t*>(dsel + 32),
                             n_ph - 1, P, dsel, s, ph_bin[0], dsmall + 10);
@@ -892,8 +964,6 @@ retry_sort:
   mark(v, 2, s);
 
   const float bgf[3] = {background[0], background[1], background[2]};
-  NXS_CUDA(ensure_n<int32_t>(v->cum_ph[0], n_tiles));
-  NXS_CUDA(cudaMemsetAsync(v->cum_ph[0].p, 0, (size_t)n_tiles * 4, s));
   const int tbits = bits_for((uint32_t)std::max(n_tiles, 2));
   int64_t total_pairs = 0;
   int ph_done = 0;
@@ -985,7 +1055,7 @@ retry_sort:
       NXS_CUDA(ensure_n<uint32_t>(v->pk_in, capp));
       NXS_CUDA(ensure_n<uint32_t>(v->pk_out, capp));
       NXS_CUDA(ensure_n<uint32_t>(v->pv_in, capp));
-      NXS_CUDA(cudaMemsetAsync(v->ranges_ph[0].p, 0, (size_t)n_tiles * sizeof(int2), s));
+      // (ranges_ph[0] was cleared by k_call_init)
       const int tbits_pad = bits_for((uint32_t)n_tiles + 1);  // the padding key sorts last
       size_t tmp_pairs = 0;
       NXS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_pairs, v->pk_in.as<uint32_t>(),
@@ -1179,7 +1249,8 @@ retry_sort:
       NXS_CUDA(ensure_n<int2>(v->ranges_ph[ph], n_tiles));
       NXS_CUDA(ensure_n<int32_t>(v->cum_ph[ph + 1], n_tiles));
       NXS_CUDA(ensure_n<uint32_t>(v->pv_ph[ph], std::max<int64_t>(1, (int64_t)n_pairs)));
-      NXS_CUDA(cudaMemsetAsync(v->ranges_ph[ph].p, 0, (size_t)n_tiles * sizeof(int2), s));
+      if (ph > 0)  // (phase 0: cleared by k_call_init)
+        NXS_CUDA(cudaMemsetAsync(v->ranges_ph[ph].p, 0, (size_t)n_tiles * sizeof(int2), s));
       if (n_pairs > 0) {
         NXS_CUDA(ensure_n<uint32_t>(v->pk_in, (int64_t)n_pairs));
         NXS_CUDA(ensure_n<uint32_t>(v->pk_out, (int64_t)n_pairs));
@@ -1224,7 +1295,7 @@ retry_sort:
     if (torder) {
       // ---- K3x exact/chunked-order forward of this phase
       NXS_CUDA(ensure_n<int32_t>(v->seq, npix * std::max(1, opts->max_splats)));  // [slot][pixel]
-      if (n_ph > 1) NXS_CUDA(cudaMemsetAsync(n_active, 0, sizeof(unsigned int), s));
+      if (n_ph > 1 && ph > 0) NXS_CUDA(cudaMemsetAsync(n_active, 0, sizeof(unsigned int), s));
       // exact order over several phases: pending entries cross the phase end
       const bool xcarry = exact && n_ph > 1;
       float* ebound = nullptr;
@@ -1256,14 +1327,16 @@ retry_sort:
       ph_done = ph + 1;
       continue;
     }
-    // ---- K3 forward blend of this phase (tiles still active)
-    NXS_CUDA(cudaMemsetAsync(n_active, 0, sizeof(unsigned int), s));
+    // ---- K3 forward blend of this phase (tiles still active; phase 0's
+    // count was cleared by k_call_init)
+    if (ph > 0) NXS_CUDA(cudaMemsetAsync(n_active, 0, sizeof(unsigned int), s));
     FwdArgs fa{v->records.as<float4>(), v->pv_ph[ph].as<uint32_t>(), v->ranges_ph[ph].as<int2>(),
                v->cum_ph[ph].as<int32_t>(), v->cum_ph[ph + 1].as<int32_t>(),
                v->active.as<uint8_t>(), n_active, ph > 0, ph + 1 < n_ph, opts->max_splats,
                (float)opts->alpha_cutoff, opts->near_plane, {bgf[0], bgf[1], bgf[2]},
                rgb, overdraw, residual, v->lazy ? dsmall + 12 : nullptr};
     launch_blend_fwd(count, n_tiles, fa, cam, md, v->cache(), v->resume(), cnt, s);
+    g_ht.mark("fwd_enq");
     NXS_LAUNCHED("blend_fwd");
     if (v->ev_ok) rec_event(v, v->evp[ph][4], s);
     ph_done = ph + 1;
@@ -1287,12 +1360,16 @@ retry_sort:
       }
       cudaGraphDestroy(g);
       NXS_CUDA(cudaGraphLaunch(v->gexec, s));
+      g_ht.mark("graph");
     }
   }
   mark(v, 7, s);
-  if (v->lazy)  // the next call's first-phase hint (read without a sync)
+  if (v->lazy) {  // the next call's first-phase hint (read without a sync)
+    cudaStream_t cs;
+    NXS_CUDA(side_after(v, s, cs));
     NXS_CUDA(cudaMemcpyAsync(v->host_small + 30, dsmall + 12, sizeof(unsigned long long),
-                             cudaMemcpyDeviceToHost, s));
+                             cudaMemcpyDeviceToHost, cs));
+  }
   v->ev_fwd = true;
   v->ev_bwd = false;
   v->stats.n_pairs = total_pairs;
@@ -1443,6 +1520,7 @@ int nxs_forward_backward(nxs_view* v, const nxs_scene* scene, const nxs_camera* 
   if ((rc = check_backward_args(v, scene, seed, g_centers, g_scales, g_quats, g_opacities, g_sh)))
     return rc;
   cudaStream_t s = (cudaStream_t)stream_;
+  g_ht.mark("start");
   // speculate that this view needs as many depth phases as its last call
   const int spec = (v->ev_sync && v->phases_needed > 0) ? v->phases_needed : 0;
   if ((rc = forward_impl(v, scene, camera, model, opts, background, rgb, overdraw, residual,
@@ -1460,12 +1538,16 @@ int nxs_forward_backward(nxs_view* v, const nxs_scene* scene, const nxs_camera* 
     } else {
       unsigned int* n_active =
           reinterpret_cast<unsigned int*>(v->dev_small.as<unsigned long long>() + 5);
+      cudaStream_t cs;
+      NXS_CUDA(side_after(v, s, cs));
       NXS_CUDA(cudaMemcpyAsync(v->host_small + 3, n_active, sizeof(unsigned int),
-                               cudaMemcpyDeviceToHost, s));
-      NXS_CUDA(cudaEventRecord(v->ev_sync, s));
+                               cudaMemcpyDeviceToHost, cs));
+      NXS_CUDA(cudaEventRecord(v->ev_sync, cs));
     }
   }
+  g_ht.mark("check_enq");
   if ((rc = backward_blend(v, seed, s))) return rc;
+  g_ht.mark("bwd_enq");
   if (spec_check) {
     bool ok = true;
     if (async_check) {
@@ -1477,6 +1559,7 @@ int nxs_forward_backward(nxs_view* v, const nxs_scene* scene, const nxs_camera* 
       NXS_CUDA(e);
     }
     v->spec_pending = false;
+    g_ht.mark("spin");
     if (!ok || (unsigned)v->host_small[3] != 0) {
       // more depth phases were needed: drop the moments, redo both passes
       if ((rc = backward_chain(v, scene, nullptr, nullptr, nullptr, nullptr, nullptr, s)))
@@ -1488,12 +1571,23 @@ int nxs_forward_backward(nxs_view* v, const nxs_scene* scene, const nxs_camera* 
       if ((rc = backward_blend(v, seed, s))) return rc;
     }
   }
-  return backward_chain(v, scene, g_centers, g_scales, g_quats, g_opacities, g_sh, s);
+  rc = backward_chain(v, scene, g_centers, g_scales, g_quats, g_opacities, g_sh, s);
+  g_ht.mark("chain_enq");
+  g_ht.dump();
+  return rc;
+}
+
+int nxs_view_set_timing(nxs_view* v, int on) {
+  if (!v) return fail(NXS_ERR_INVALID, "null view");
+  v->timing = on != 0;
+  return NXS_OK;
 }
 
 int nxs_view_timings(nxs_view* v, float* ms, int n) {
   if (!v || !ms) return fail(NXS_ERR_INVALID, "null argument");
   if (!v->ev_ok) return fail(NXS_ERR_CUDA, "timing events unavailable");
+  if (!v->timing)
+    return fail(NXS_ERR_STATE, "phase timing is off for this view (nxs_view_set_timing)");
   float t[NXS_PHASES] = {0};
   auto el = [&](cudaEvent_t a, cudaEvent_t b, float& out) -> int {
     NXS_CUDA(cudaEventSynchronize(b));

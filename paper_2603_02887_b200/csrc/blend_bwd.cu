@@ -41,7 +41,10 @@ constexpr int BWD_WARPS = BWD_THREADS / 32;
 // floats so the column stores and the 16-B row loads are conflict free).
 constexpr int RED_STRIDE = 36;
 constexpr int RED_WARP = NMOM * RED_STRIDE;  // floats per warp
-constexpr size_t BWD_SMEM = sizeof(float4) * BWD_BATCH * (REC_F4 + 3) + sizeof(uint32_t) * BWD_BATCH +
+// Records, B frames and ranks are double-buffered: the next batch streams
+// in with cp.async while the current one is replayed.
+constexpr size_t BWD_SMEM = 2 * (sizeof(float4) * BWD_BATCH * (REC_F4 + 3) +
+                                 sizeof(uint32_t) * BWD_BATCH) +
                             sizeof(float) * BWD_BATCH * NMOM + sizeof(float) * RED_WARP * BWD_WARPS;
 
 template <int FAM, bool COUNT>
@@ -52,10 +55,13 @@ __global__ void __launch_bounds__(BWD_THREADS, 4)
                 double* __restrict__ moments, uint8_t* __restrict__ touched,
                 Counters* __restrict__ cnt) {
   extern __shared__ float4 smem_dyn[];
-  float4(*s_rec)[REC_F4] = reinterpret_cast<float4(*)[REC_F4]>(smem_dyn);
-  float4(*s_bf)[3] = reinterpret_cast<float4(*)[3]>(smem_dyn + BWD_BATCH * REC_F4);
-  uint32_t* s_rank = reinterpret_cast<uint32_t*>(smem_dyn + BWD_BATCH * (REC_F4 + 3));
-  float* s_acc = reinterpret_cast<float*>(s_rank + BWD_BATCH);
+  // [buffer][entry][part]
+  float4(*s_rec2)[BWD_BATCH][REC_F4] = reinterpret_cast<float4(*)[BWD_BATCH][REC_F4]>(smem_dyn);
+  float4(*s_bf2)[BWD_BATCH][3] =
+      reinterpret_cast<float4(*)[BWD_BATCH][3]>(smem_dyn + 2 * BWD_BATCH * REC_F4);
+  uint32_t(*s_rank2)[BWD_BATCH] =
+      reinterpret_cast<uint32_t(*)[BWD_BATCH]>(smem_dyn + 2 * BWD_BATCH * (REC_F4 + 3));
+  float* s_acc = reinterpret_cast<float*>(s_rank2 + 2);
   float* s_red = s_acc + BWD_BATCH * NMOM;
   __shared__ int s_maxlast;
 
@@ -80,29 +86,71 @@ __global__ void __launch_bounds__(BWD_THREADS, 4)
   __syncthreads();
   const int vmax = s_maxlast + 1;  // virtual per-tile list positions [0, vmax) are replayed
 
-  // phases back to front, each phase's segment back to front
-  for (int ph = lists.n - 1; ph >= 0; --ph) {
+  // phases back to front, each phase's segment back to front, in batches of
+  // BWD_BATCH virtual positions [base, hi); batch (ph, hi) -> the next one
+  auto seg_end = [&](int ph) {  // first batch end of phase ph (<= c0: empty)
     const int2 seg = lists.ranges[ph][tile];
-    if (seg.y <= seg.x) continue;
-    const int c0 = lists.cum[ph][tile];  // virtual index of seg.x
-    const uint32_t* __restrict__ pairs = lists.pairs[ph];
-    for (int hi = min(c0 + (seg.y - seg.x), vmax); hi > c0; hi -= BWD_BATCH) {
-      const int base = max(c0, hi - BWD_BATCH);  // virtual
-      const int n = hi - base;
-      __syncthreads();
-      if (tid < n) s_rank[tid] = pairs[seg.x + (base - c0) + tid];
-      for (int k = tid; k < n * NMOM; k += BWD_THREADS) s_acc[k] = 0.f;
-      __syncthreads();
-      for (int k = tid; k < n * 8; k += BWD_THREADS) {
-        const int e = k >> 3, part = k & 7;
-        s_rec[e][part] = records[(size_t)s_rank[e] * REC_F4 + part];
-      }
-      for (int k = tid; k < n * 3; k += BWD_THREADS) {
-        const int e = k / 3, part = k - 3 * (k / 3);
-        s_bf[e][part] = bframe[(size_t)s_rank[e] * 3 + part];
-      }
-      __syncthreads();
-      if (COUNT) nent += n;
+    const int c0 = lists.cum[ph][tile];
+    return seg.y > seg.x ? min(c0 + (seg.y - seg.x), vmax) : c0;
+  };
+  auto next_batch = [&](int& ph, int& hi) -> bool {  // from (ph, hi) (hi: current end)
+    const int c0 = lists.cum[ph][tile];
+    const int base = max(c0, hi - BWD_BATCH);
+    if (base > c0) {
+      hi = base;
+      return true;
+    }
+    for (--ph; ph >= 0; --ph) {
+      hi = seg_end(ph);
+      if (hi > lists.cum[ph][tile]) return true;
+    }
+    return false;
+  };
+  auto stage = [&](int b, int ph, int hi) {
+    const int c0 = lists.cum[ph][tile];
+    const int base = max(c0, hi - BWD_BATCH);
+    const int n = hi - base;
+    const uint32_t* __restrict__ pr = lists.pairs[ph] + lists.ranges[ph][tile].x + (base - c0);
+    for (int k = tid; k < n * 8; k += BWD_THREADS) {
+      const int e = k >> 3, part = k & 7;
+      const uint32_t rk = __ldg(pr + e);
+      if (part == 0) s_rank2[b][e] = rk;
+      cp_async16(&s_rec2[b][e][part], records + (size_t)rk * REC_F4 + part);
+    }
+    for (int k = tid; k < n * 3; k += BWD_THREADS) {
+      const int e = k / 3, part = k - 3 * (k / 3);
+      cp_async16(&s_bf2[b][e][part], bframe + (size_t)__ldg(pr + e) * 3 + part);
+    }
+    cp_async_commit();
+  };
+
+  int ph = lists.n - 1, hi = 0;
+  bool have = false;
+  for (; ph >= 0; --ph) {
+    hi = seg_end(ph);
+    if (hi > lists.cum[ph][tile]) {
+      have = true;
+      break;
+    }
+  }
+  if (have) stage(0, ph, hi);
+  int buf = 0;
+  while (have) {
+    const int c0 = lists.cum[ph][tile];
+    const int base = max(c0, hi - BWD_BATCH);  // virtual
+    const int n = hi - base;
+    int nph = ph, nhi = hi;
+    const bool more = next_batch(nph, nhi);
+    __syncthreads();  // every thread is past the previous batch's flush
+    if (more) stage(buf ^ 1, nph, nhi);
+    for (int k = tid; k < n * NMOM; k += BWD_THREADS) s_acc[k] = 0.f;
+    if (more) cp_async_wait<1>();
+    else cp_async_wait<0>();
+    __syncthreads();
+    float4(*s_rec)[REC_F4] = s_rec2[buf];
+    float4(*s_bf)[3] = s_bf2[buf];
+    const uint32_t* s_rank = s_rank2[buf];
+    if (COUNT) nent += n;
 
       for (int j = n - 1; j >= 0; --j) {
         const int idx = base + j;
@@ -169,7 +217,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 4)
           touched[s_rank[e]] = 1;  // K5 reads (and re-zeroes) touched ranks only
         }
       }
-    }
+    ph = nph;
+    hi = nhi;
+    have = more;
+    buf ^= 1;
   }
 
   if (COUNT) {

@@ -1065,6 +1065,32 @@ __global__ void k_pack_check(const unsigned long long* __restrict__ dsmall,
   else if (i == 26) v = dsmall[11];
   out[i] = v;
 }
+// start of a forward: the small counters (dsmall; [6] = min-key init), every
+// tile active, the phase-0 carry/ranges cleared and the phase targets — one
+// launch instead of a string of memsets and a host copy
+struct PhaseTargets {
+  long long v[4];
+};
+__global__ void k_call_init(unsigned long long* __restrict__ dsmall, uint8_t* __restrict__ active,
+                            int32_t* __restrict__ cum0, int2* __restrict__ ranges0, int n_tiles,
+                            long long* __restrict__ dtgt, PhaseTargets tgt, int n_tgt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < 16) dsmall[i] = (i == 6) ? ~0ull : 0ull;
+  if (dtgt && i < n_tgt) dtgt[i] = tgt.v[i];
+  if (i < n_tiles) {
+    active[i] = 1;
+    cum0[i] = 0;
+    ranges0[i] = make_int2(0, 0);
+  }
+}
+void launch_call_init(unsigned long long* dsmall, uint8_t* active, int32_t* cum0, int2* ranges0,
+                      int n_tiles, long long* dtgt, const int64_t* tgt, int n_tgt, cudaStream_t s) {
+  PhaseTargets t{};
+  for (int i = 0; i < n_tgt && i < 4; ++i) t.v[i] = tgt[i];
+  const int n = std::max(n_tiles, 16);
+  k_call_init<<<(n + 255) / 256, 256, 0, s>>>(dsmall, active, cum0, ranges0, n_tiles, dtgt, t,
+                                              std::min(n_tgt, 4));
+}
 void launch_pack_check(const unsigned long long* dsmall, const long long* dsel, int n_ph,
                        unsigned long long* out, cudaStream_t s) {
   k_pack_check<<<1, 32, 0, s>>>(dsmall, dsel, n_ph, out);

@@ -22,7 +22,7 @@ model = TransmittanceModel.softplus(20.0)
 cams = [canonical_camera(1920, 1080, v, n_views) for v in range(n_views)]
 seeds = [torch.as_tensor(canonical_seed(1920, 1080, v), dtype=torch.float32, device="cuda")
          for v in range(n_views)]
-views = [_native.View() for _ in range(n_views)]
+views = [_native.View().set_timing(True) for _ in range(n_views)]
 for rep in range(5):
     line = []
     for v in range(n_views):
