@@ -83,8 +83,18 @@ void launch_project_ranks_z(const float*, const float*, const float*, const floa
                             double*, cudaStream_t);
 void launch_pack_check(const unsigned long long*, const long long*, int, unsigned long long*,
                        cudaStream_t);
-void launch_call_init(unsigned long long*, uint8_t*, int32_t*, int2*, int, long long*,
-                      const int64_t*, int, cudaStream_t);
+void launch_call_init(unsigned long long*, uint8_t*, int32_t*, int2*, unsigned int*, int,
+                      long long*, const int64_t*, int, cudaStream_t);
+void launch_count_tiles(const int4*, const uint32_t*, int64_t, int64_t, int, const uint8_t*,
+                        const unsigned int*, unsigned int*, const double*, const CamDev&,
+                        cudaStream_t, const int* nd = nullptr);
+void launch_tile_scan(unsigned int*, int, int2*, unsigned long long*, unsigned long long*,
+                      unsigned long long, unsigned long long*, cudaStream_t);
+void launch_emit_tiles(const int4*, const uint32_t*, int64_t, int64_t, int, const uint8_t*,
+                       const int2*, unsigned int*, uint32_t*, const double*, const CamDev&,
+                       cudaStream_t, const int* nd, unsigned long long cap);
+void launch_seg_sort(uint32_t*, const int2*, unsigned int*, int, unsigned long long,
+                     cudaStream_t);
 void launch_chunk_key(const float*, const float*, const float*, const float*, int64_t,
                       const CamDev&, double, const uint32_t*, int, double*, unsigned long long*,
                       uint32_t*, cudaStream_t);
@@ -192,7 +202,7 @@ struct nxs_view {
   // per pair: sort scratch, and the sorted ranks of each depth phase
   Buf pk_in, pk_out, pv_in, pv_ph[MAX_PHASES];
   // per tile: phase ranges and virtual offsets, activity
-  Buf ranges_ph[MAX_PHASES], cum_ph[MAX_PHASES + 1], active;
+  Buf ranges_ph[MAX_PHASES], cum_ph[MAX_PHASES + 1], active, tile_cnt;
   // per pixel: replay cache and the forward carry between phases
   Buf c_last, c_sat, c_tk, c_thi, c_tlo, c_P, c_ck, c_Pck, c_ek, c_th0;
   Buf r_rad, r_trem, r_count, r_sea, r_sa;
@@ -251,6 +261,7 @@ struct nxs_view {
   void for_each_buf(F f) {
     Buf* all[] = {&dkeys_in, &dkeys_out, &idx_in,  &idx_out, &records, &bframe, &rects,
                   &ntiles,   &offsets,   &moments, &touched, &pk_in,   &pk_out,  &pv_in,  &active,
+                  &tile_cnt,
                   &depth,    &k32a,      &k32b,    &k32c,    &rank_of, &rank_c, &zlo_rank, &seq, &ph_hist,
                   &ph_sel,   &tq,      &zlo64,  &xc_t, &xc_r, &xc_n,
                   &c_last,   &c_sat,     &c_tk,    &c_thi,   &c_tlo,   &c_P,    &c_ck,
@@ -669,13 +680,15 @@ int forward_impl(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
   NXS_CUDA(ensure_n<float>(v->c_th0, npix * 3));
   NXS_CUDA(v->dev_small.ensure(16 * sizeof(unsigned long long)));
   // dsmall: [0] straddle count, [1..4] event counters, [5] active tiles (u32),
-  // [6] min depth key, [7] max depth key, [8] key-run overflow, [12] last
-  // rank the finished tiles needed (global order)
+  // [6] min depth key, [7] max depth key, [8] key-run overflow, [9] pending
+  // overflow, [10]/[11] device-sized overflow/pairs, [12] last rank the
+  // finished tiles needed, [13]/[14] pair total / longest tile list
   unsigned long long* dsmall = v->dev_small.as<unsigned long long>();
   Counters* cnt = reinterpret_cast<Counters*>(dsmall + 1);
   unsigned int* n_active = reinterpret_cast<unsigned int*>(dsmall + 5);
   NXS_CUDA(ensure_n<int2>(v->ranges_ph[0], n_tiles));
   NXS_CUDA(ensure_n<int32_t>(v->cum_ph[0], n_tiles));
+  NXS_CUDA(ensure_n<uint32_t>(v->tile_cnt, n_tiles));
   NXS_CUDA(v->ph_hist.ensure(4096 * sizeof(unsigned int)));
   NXS_CUDA(v->ph_sel.ensure(96 * sizeof(long long)));
   if (P == 0) {  // (P > 0: k_call_init below, in the pipeline)
@@ -683,6 +696,7 @@ int forward_impl(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
     NXS_CUDA(cudaMemsetAsync(v->active.p, 1, (size_t)n_tiles, s));
     NXS_CUDA(cudaMemsetAsync(v->cum_ph[0].p, 0, (size_t)n_tiles * 4, s));
     NXS_CUDA(cudaMemsetAsync(v->ranges_ph[0].p, 0, (size_t)n_tiles * sizeof(int2), s));
+    NXS_CUDA(cudaMemsetAsync(v->tile_cnt.p, 0, (size_t)n_tiles * 4, s));
   }
 
   // ---- depth phases [R_p, R_{p+1}): R_1 = first phase, then x8.  The
@@ -848,7 +862,7 @@ retry_sort:
       int64_t tgt[4] = {0, 0, 0, 0};
       for (int p = 1; p < n_ph && p <= 4; ++p) tgt[p - 1] = R[p];
       launch_call_init(dsmall, v->active.as<uint8_t>(), v->cum_ph[0].as<int32_t>(),
-                       v->ranges_ph[0].as<int2>(), n_tiles,
+                       v->ranges_ph[0].as<int2>(), v->tile_cnt.as<uint32_t>(), n_tiles,
                        v->lazy ? v->ph_sel.as<long long>() + 32 : nullptr, tgt, n_ph - 1, s);
       NXS_LAUNCHED("call_init");
     }
@@ -1039,47 +1053,31 @@ retry_sort:
                            v->tq.as<double>(), s, n_sel);
       NXS_LAUNCHED("project_ranks");
       if (v->ev_ok) rec_event(v, v->evp[0][2], s);
-      launch_count_active(v->rects.as<int4>(), v->idx_out.as<uint32_t>(), 0, cap0, cam.tiles_x,
-                          v->active.as<uint8_t>(), nullptr, v->ntiles.as<unsigned long long>(),
-                          exact ? nullptr : v->tq.as<double>(), cam, s, n_sel);
-      NXS_LAUNCHED("count_active");
-      size_t tbc = v->temp.cap;
-      NXS_CUDA(cub::DeviceScan::ExclusiveSum(v->temp.p, tbc, v->ntiles.as<unsigned long long>(),
-                                             v->offsets.as<unsigned long long>(), (int)cap0, s));
-      launch_pairs_total(v->offsets.as<unsigned long long>(), v->ntiles.as<unsigned long long>(),
-                         cap0, (unsigned long long)capp, dsmall + 11, dsmall + 10, s);
-      NXS_LAUNCHED("pairs_total");
+      // ---- tile-major binning: per-tile counts, one scan over the tiles
+      // (ranges, total vs capacity, longest list), emission at per-tile
+      // cursors, per-tile sort by rank
+      launch_count_tiles(v->rects.as<int4>(), v->idx_out.as<uint32_t>(), 0, cap0, cam.tiles_x,
+                         v->active.as<uint8_t>(), nullptr, v->tile_cnt.as<uint32_t>(),
+                         exact ? nullptr : v->tq.as<double>(), cam, s, n_sel);
+      NXS_LAUNCHED("count_tiles");
       NXS_CUDA(ensure_n<int2>(v->ranges_ph[0], n_tiles));
       NXS_CUDA(ensure_n<int32_t>(v->cum_ph[1], n_tiles));
       NXS_CUDA(ensure_n<uint32_t>(v->pv_ph[0], capp));
-      NXS_CUDA(ensure_n<uint32_t>(v->pk_in, capp));
-      NXS_CUDA(ensure_n<uint32_t>(v->pk_out, capp));
-      NXS_CUDA(ensure_n<uint32_t>(v->pv_in, capp));
-      // (ranges_ph[0] was cleared by k_call_init)
-      const int tbits_pad = bits_for((uint32_t)n_tiles + 1);  // the padding key sorts last
-      size_t tmp_pairs = 0;
-      NXS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_pairs, v->pk_in.as<uint32_t>(),
-                                               v->pk_out.as<uint32_t>(), v->pv_in.as<uint32_t>(),
-                                               v->pv_ph[0].as<uint32_t>(), (int)capp, 0,
-                                               tbits_pad, s));
-      NXS_CUDA(v->temp.ensure(tmp_pairs));
-      launch_emit_pairs(v->rects.as<int4>(), v->idx_out.as<uint32_t>(),
-                        v->offsets.as<unsigned long long>(), 0, cap0, cam.tiles_x,
-                        v->active.as<uint8_t>(), v->pk_in.as<uint32_t>(), v->pv_in.as<uint32_t>(),
-                        exact ? nullptr : v->tq.as<double>(), cam, s, n_sel, (unsigned long long)capp);
-      NXS_LAUNCHED("emit_pairs");
-      launch_pad_keys(v->pk_in.as<uint32_t>(), capp, dsmall + 11, s);
-      NXS_LAUNCHED("pad_keys");
       mark(v, 3, s);
+      launch_tile_scan(v->tile_cnt.as<uint32_t>(), n_tiles, v->ranges_ph[0].as<int2>(),
+                       dsmall + 11, dsmall + 14, (unsigned long long)capp, dsmall + 10, s);
+      NXS_LAUNCHED("tile_scan");
+      launch_emit_tiles(v->rects.as<int4>(), v->idx_out.as<uint32_t>(), 0, cap0, cam.tiles_x,
+                        v->active.as<uint8_t>(), v->ranges_ph[0].as<int2>(),
+                        v->tile_cnt.as<uint32_t>(), v->pv_ph[0].as<uint32_t>(),
+                        exact ? nullptr : v->tq.as<double>(), cam, s, n_sel,
+                        (unsigned long long)capp);
+      NXS_LAUNCHED("emit_tiles");
       mark(v, 4, s);
-      size_t tbp = v->temp.cap;
-      NXS_CUDA(cub::DeviceRadixSort::SortPairs(v->temp.p, tbp, v->pk_in.as<uint32_t>(),
-                                               v->pk_out.as<uint32_t>(), v->pv_in.as<uint32_t>(),
-                                               v->pv_ph[0].as<uint32_t>(), (int)capp, 0,
-                                               tbits_pad, s));
+      launch_seg_sort(v->pv_ph[0].as<uint32_t>(), v->ranges_ph[0].as<int2>(),
+                      v->tile_cnt.as<uint32_t>(), n_tiles, (unsigned long long)capp, s);
+      NXS_LAUNCHED("seg_sort");
       mark(v, 5, s);
-      launch_tile_ranges(v->pk_out.as<uint32_t>(), capp, v->ranges_ph[0].as<int2>(), s);
-      NXS_LAUNCHED("tile_ranges");
       mark(v, 6, s);
       if (v->ev_ok) rec_event(v, v->evp[0][3], s);
       v->async_pending = true;
@@ -1202,18 +1200,19 @@ retry_sort:
         rec_event(v, v->evp[ph][2], s);
       }
       // ---- K2a counts over active tiles, scan, one host sync for the pair count
+      NXS_CUDA(ensure_n<int2>(v->ranges_ph[ph], n_tiles));
       if (nr > 0) {
-        launch_count_active(v->rects.as<int4>(), v->idx_out.as<uint32_t>(), r0, r1, cam.tiles_x,
-                            v->active.as<uint8_t>(), ph > 0 ? n_active : nullptr,
-                            v->ntiles.as<unsigned long long>(), exact ? nullptr : v->tq.as<double>(), cam, s);
-        NXS_LAUNCHED("count_active");
-        size_t tb = v->temp.cap;
-        NXS_CUDA(cub::DeviceScan::ExclusiveSum(v->temp.p, tb, v->ntiles.as<unsigned long long>(),
-                                               v->offsets.as<unsigned long long>(), (int)nr, s));
-        NXS_CUDA(cudaMemcpyAsync(v->host_small, v->offsets.as<unsigned long long>() + (nr - 1),
-                                 sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-        NXS_CUDA(cudaMemcpyAsync(v->host_small + 1, v->ntiles.as<unsigned long long>() + (nr - 1),
-                                 sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+        // per-tile counts and one scan over the tiles: ranges, total, longest list
+        launch_count_tiles(v->rects.as<int4>(), v->idx_out.as<uint32_t>(), r0, r1, cam.tiles_x,
+                           v->active.as<uint8_t>(), ph > 0 ? n_active : nullptr,
+                           v->tile_cnt.as<uint32_t>(), exact ? nullptr : v->tq.as<double>(), cam,
+                           s);
+        NXS_LAUNCHED("count_tiles");
+        launch_tile_scan(v->tile_cnt.as<uint32_t>(), n_tiles, v->ranges_ph[ph].as<int2>(),
+                         dsmall + 13, dsmall + 14, ~0ull, nullptr, s);
+        NXS_LAUNCHED("tile_scan");
+        NXS_CUDA(cudaMemcpyAsync(v->host_small, dsmall + 13, 2 * sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, s));
       } else {
         NXS_CUDA(cudaMemsetAsync(v->host_small, 0, 2 * sizeof(unsigned long long), s));
       }
@@ -1239,19 +1238,40 @@ retry_sort:
         goto retry_sort;
       }
       if (ph == 0) mark(v, 3, s);
-      const unsigned long long n_pairs = v->host_small[0] + v->host_small[1];
+      const unsigned long long n_pairs = v->host_small[0];
+      const unsigned long long max_seg = v->host_small[1];
       v->stats.n_straddling = (int64_t)v->host_small[2];
       if (ph > 0 && !v->lazy && (unsigned)v->host_small[3] == 0) break;  // every tile finished
       if (n_pairs >= (1ull << 31)) return fail(NXS_ERR_NOMEM, "more than 2^31 tile pairs");
       total_pairs += (int64_t)n_pairs;
       v->ph_pairs[ph] = (int64_t)n_pairs;
 
-      NXS_CUDA(ensure_n<int2>(v->ranges_ph[ph], n_tiles));
       NXS_CUDA(ensure_n<int32_t>(v->cum_ph[ph + 1], n_tiles));
       NXS_CUDA(ensure_n<uint32_t>(v->pv_ph[ph], std::max<int64_t>(1, (int64_t)n_pairs)));
-      if (ph > 0)  // (phase 0: cleared by k_call_init)
+      if (n_pairs > 0 && max_seg <= (unsigned long long)SEG_MAX) {
+        // ---- K2b emission at the per-tile cursors, per-tile sort by rank
+        launch_emit_tiles(v->rects.as<int4>(), v->idx_out.as<uint32_t>(), r0, r1, cam.tiles_x,
+                          v->active.as<uint8_t>(), v->ranges_ph[ph].as<int2>(),
+                          v->tile_cnt.as<uint32_t>(), v->pv_ph[ph].as<uint32_t>(),
+                          exact ? nullptr : v->tq.as<double>(), cam, s, nullptr, n_pairs);
+        NXS_LAUNCHED("emit_tiles");
+        if (ph == 0) mark(v, 4, s);
+        launch_seg_sort(v->pv_ph[ph].as<uint32_t>(), v->ranges_ph[ph].as<int2>(),
+                        v->tile_cnt.as<uint32_t>(), n_tiles, n_pairs, s);
+        NXS_LAUNCHED("seg_sort");
+        if (ph == 0) mark(v, 5, s);
+      } else if (n_pairs > 0) {
+        // a tile list longer than the per-tile sort takes: per-rank counts,
+        // emission in rank order and a stable radix sort by tile
+        NXS_CUDA(cudaMemsetAsync(v->tile_cnt.p, 0, (size_t)n_tiles * 4, s));
+        launch_count_active(v->rects.as<int4>(), v->idx_out.as<uint32_t>(), r0, r1, cam.tiles_x,
+                            v->active.as<uint8_t>(), nullptr, v->ntiles.as<unsigned long long>(),
+                            exact ? nullptr : v->tq.as<double>(), cam, s);
+        NXS_LAUNCHED("count_active");
+        size_t tbo = v->temp.cap;
+        NXS_CUDA(cub::DeviceScan::ExclusiveSum(v->temp.p, tbo, v->ntiles.as<unsigned long long>(),
+                                               v->offsets.as<unsigned long long>(), (int)nr, s));
         NXS_CUDA(cudaMemsetAsync(v->ranges_ph[ph].p, 0, (size_t)n_tiles * sizeof(int2), s));
-      if (n_pairs > 0) {
         NXS_CUDA(ensure_n<uint32_t>(v->pk_in, (int64_t)n_pairs));
         NXS_CUDA(ensure_n<uint32_t>(v->pk_out, (int64_t)n_pairs));
         NXS_CUDA(ensure_n<uint32_t>(v->pv_in, (int64_t)n_pairs));
@@ -1261,7 +1281,6 @@ retry_sort:
                                                  v->pv_ph[ph].as<uint32_t>(), (int)n_pairs, 0,
                                                  tbits, s));
         NXS_CUDA(v->temp.ensure(tmp_pairs));
-        // ---- K2b pairs (rank order), stable sort by tile, ranges
         launch_emit_pairs(v->rects.as<int4>(), v->idx_out.as<uint32_t>(),
                           v->offsets.as<unsigned long long>(), r0, r1, cam.tiles_x,
                           v->active.as<uint8_t>(), v->pk_in.as<uint32_t>(), v->pv_in.as<uint32_t>(),

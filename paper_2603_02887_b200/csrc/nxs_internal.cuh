@@ -18,6 +18,7 @@ namespace nxs {
 
 constexpr int TILE = 16;
 constexpr int TILE_PIX = TILE * TILE;  // 256 threads per tile block
+constexpr int SEG_MAX = 4096;  // longest tile list the per-tile sort handles (else radix sort)
 constexpr int REC_F4 = 8;              // float4 per record
 constexpr int NMOM = 24;               // gradient moments per Gaussian
 

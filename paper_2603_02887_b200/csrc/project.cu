@@ -15,6 +15,7 @@
 #include <algorithm>
 
 #include <cub/block/block_radix_sort.cuh>
+#include <cub/block/block_scan.cuh>
 
 #include "nxs_internal.cuh"
 
@@ -943,6 +944,183 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Tile-major binning (counting sort by tile): per-tile hit counts, one scan
+// over the tiles (ranges, total, largest list), emission at per-tile atomic
+// cursors, and a per-tile sort of each list by rank.  Replaces the per-rank
+// scan + the radix sort of (tile, rank) pairs by tile: a rank order is
+// unique, so the sorted lists equal the stable sort's bit for bit.
+// ---------------------------------------------------------------------------
+template <int KSUB>
+__global__ void __launch_bounds__(256)
+    k_count_tiles(const int4* __restrict__ rects, const uint32_t* __restrict__ order,
+                  int64_t r0, int64_t r1, int tiles_x, const uint8_t* __restrict__ active,
+                  const unsigned int* __restrict__ gate, unsigned int* __restrict__ tile_cnt,
+                  const int* __restrict__ nd, const double* __restrict__ tq, CamDev cam) {
+  if (gate && *gate == 0u) return;
+  const int sl = threadIdx.x & (KSUB - 1);
+  const int64_t r = r0 + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / KSUB;
+  const int64_t rn = nd ? min(r1, r0 + (int64_t)*nd) : r1;
+  if (r >= rn) return;
+  const int64_t g = order[r];
+  const int4 rc = rects[g];
+  if (rc.x < 0) return;
+  const double inv_f = 1.0 / cam.f;
+  const int w = rc.z - rc.x + 1, nt = w * (rc.w - rc.y + 1);
+  for (int k = sl; k < nt; k += KSUB) {
+    const int tx = rc.x + k % w, ty = rc.y + k / w;
+    const int t = ty * tiles_x + tx;
+    if (active[t] && tile_hit(tq, g, tx, ty, cam, inv_f)) atomicAdd(&tile_cnt[t], 1u);
+  }
+}
+
+// one block: exclusive scan of the tile counts -> ranges [off, off + cnt),
+// the total (and whether it exceeds cap), the longest list; the counts are
+// reset to zero to serve as the emission cursors
+constexpr int TSCAN_THREADS = 1024;
+__global__ void __launch_bounds__(TSCAN_THREADS)
+    k_tile_scan(unsigned int* __restrict__ tile_cnt, int n_tiles, int2* __restrict__ ranges,
+                unsigned long long* __restrict__ total, unsigned long long* __restrict__ maxseg,
+                unsigned long long cap, unsigned long long* __restrict__ overflow, int seg_max) {
+  typedef cub::BlockScan<unsigned long long, TSCAN_THREADS> Scan;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ unsigned int s_max;
+  const int per = (n_tiles + TSCAN_THREADS - 1) / TSCAN_THREADS;
+  const int lo = min(n_tiles, (int)threadIdx.x * per), hi = min(n_tiles, lo + per);
+  unsigned long long sum = 0;
+  unsigned int mx = 0;
+  for (int t = lo; t < hi; ++t) {
+    const unsigned int c = tile_cnt[t];
+    sum += c;
+    mx = max(mx, c);
+  }
+  if (threadIdx.x == 0) s_max = 0;
+  unsigned long long off, all;
+  Scan(tmp).ExclusiveSum(sum, off, all);
+  __syncthreads();
+  atomicMax(&s_max, mx);
+  for (int t = lo; t < hi; ++t) {
+    const unsigned int c = tile_cnt[t];
+    ranges[t] = make_int2((int)off, (int)(off + c));
+    off += c;
+    tile_cnt[t] = 0u;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *total = all;
+    *maxseg = s_max;
+    if (overflow && (all > cap || (int)s_max > seg_max)) atomicAdd(overflow, 1ull);
+  }
+}
+
+template <int KSUB>
+__global__ void __launch_bounds__(256)
+    k_emit_tiles(const int4* __restrict__ rects, const uint32_t* __restrict__ order, int64_t r0,
+                 int64_t r1, int tiles_x, const uint8_t* __restrict__ active,
+                 const int2* __restrict__ ranges, unsigned int* __restrict__ cursor,
+                 uint32_t* __restrict__ vals, const int* __restrict__ nd, unsigned long long cap,
+                 const double* __restrict__ tq, CamDev cam) {
+  const int sl = threadIdx.x & (KSUB - 1);
+  const int64_t r = r0 + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / KSUB;
+  const int64_t rn = nd ? min(r1, r0 + (int64_t)*nd) : r1;
+  if (r >= rn) return;
+  const int64_t g = order[r];
+  const int4 rc = rects[g];
+  if (rc.x < 0) return;
+  const double inv_f = 1.0 / cam.f;
+  const int w = rc.z - rc.x + 1, nt = w * (rc.w - rc.y + 1);
+  for (int k = sl; k < nt; k += KSUB) {
+    const int tx = rc.x + k % w, ty = rc.y + k / w;
+    const int t = ty * tiles_x + tx;
+    if (active[t] && tile_hit(tq, g, tx, ty, cam, inv_f)) {
+      const unsigned long long q = (unsigned long long)ranges[t].x + atomicAdd(&cursor[t], 1u);
+      if (q < cap) vals[q] = (uint32_t)r;  // (a device-sized buffer too small is flagged)
+    }
+  }
+}
+
+// one block per tile: sort its list (distinct ranks) ascending in shared
+// memory — rank counting for short lists, a bitonic network up to SEG_MAX;
+// zeroes the tile's cursor for the next phase
+constexpr int SEG_THREADS = 256;
+__global__ void __launch_bounds__(SEG_THREADS)
+    k_seg_sort(uint32_t* __restrict__ vals, const int2* __restrict__ ranges,
+               unsigned int* __restrict__ cursor, unsigned long long cap) {
+  __shared__ uint32_t s_k[SEG_MAX];
+  const int t = blockIdx.x, tid = threadIdx.x;
+  const int2 rg = ranges[t];
+  if (tid == 0) cursor[t] = 0u;
+  const int n = rg.y - rg.x;
+  if (n <= 1 || n > SEG_MAX || (unsigned long long)rg.y > cap) return;
+  uint32_t* v = vals + rg.x;
+  if (n <= SEG_THREADS) {
+    const uint32_t k = tid < n ? v[tid] : 0u;
+    if (tid < n) s_k[tid] = k;
+    __syncthreads();
+    if (tid < n) {
+      int pos = 0;
+      for (int j = 0; j < n; ++j) pos += s_k[j] < k ? 1 : 0;
+      v[pos] = k;
+    }
+    return;
+  }
+  int p2 = SEG_THREADS * 2;
+  while (p2 < n) p2 <<= 1;
+  for (int i = tid; i < p2; i += SEG_THREADS) s_k[i] = i < n ? v[i] : 0xffffffffu;
+  __syncthreads();
+  for (int size = 2; size <= p2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = tid; i < (p2 >> 1); i += SEG_THREADS) {
+        const int a = 2 * i - (i & (stride - 1)), b = a + stride;
+        const bool up = (a & size) == 0;
+        const uint32_t x = s_k[a], y = s_k[b];
+        if ((x > y) == up) {
+          s_k[a] = y;
+          s_k[b] = x;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = tid; i < n; i += SEG_THREADS) v[i] = s_k[i];
+}
+
+void launch_count_tiles(const int4* rects, const uint32_t* order, int64_t r0, int64_t r1,
+                        int tiles_x, const uint8_t* active, const unsigned int* gate,
+                        unsigned int* tile_cnt, const double* tq, const CamDev& cam,
+                        cudaStream_t s, const int* nd) {
+  if (r1 <= r0) return;
+  if (r1 - r0 <= 262144)
+    k_count_tiles<32><<<(unsigned)((r1 - r0 + 7) / 8), 256, 0, s>>>(
+        rects, order, r0, r1, tiles_x, active, gate, tile_cnt, nd, tq, cam);
+  else
+    k_count_tiles<8><<<(unsigned)((r1 - r0 + 31) / 32), 256, 0, s>>>(
+        rects, order, r0, r1, tiles_x, active, gate, tile_cnt, nd, tq, cam);
+}
+void launch_tile_scan(unsigned int* tile_cnt, int n_tiles, int2* ranges, unsigned long long* total,
+                      unsigned long long* maxseg, unsigned long long cap,
+                      unsigned long long* overflow, cudaStream_t s) {
+  k_tile_scan<<<1, TSCAN_THREADS, 0, s>>>(tile_cnt, n_tiles, ranges, total, maxseg, cap, overflow,
+                                          SEG_MAX);
+}
+void launch_emit_tiles(const int4* rects, const uint32_t* order, int64_t r0, int64_t r1,
+                       int tiles_x, const uint8_t* active, const int2* ranges,
+                       unsigned int* cursor, uint32_t* vals, const double* tq, const CamDev& cam,
+                       cudaStream_t s, const int* nd, unsigned long long cap) {
+  if (r1 <= r0) return;
+  if (r1 - r0 <= 262144)
+    k_emit_tiles<32><<<(unsigned)((r1 - r0 + 7) / 8), 256, 0, s>>>(
+        rects, order, r0, r1, tiles_x, active, ranges, cursor, vals, nd, cap, tq, cam);
+  else
+    k_emit_tiles<8><<<(unsigned)((r1 - r0 + 31) / 32), 256, 0, s>>>(
+        rects, order, r0, r1, tiles_x, active, ranges, cursor, vals, nd, cap, tq, cam);
+}
+void launch_seg_sort(uint32_t* vals, const int2* ranges, unsigned int* cursor, int n_tiles,
+                     unsigned long long cap, cudaStream_t s) {
+  if (n_tiles <= 0) return;
+  k_seg_sort<<<n_tiles, SEG_THREADS, 0, s>>>(vals, ranges, cursor, cap);
+}
+
 // device-sized binning: total pair count of the scan, the capacity check,
 // and max-key padding of the pair buffer beyond it
 __global__ void k_pairs_total(const unsigned long long* __restrict__ offsets,
@@ -1072,7 +1250,8 @@ struct PhaseTargets {
   long long v[4];
 };
 __global__ void k_call_init(unsigned long long* __restrict__ dsmall, uint8_t* __restrict__ active,
-                            int32_t* __restrict__ cum0, int2* __restrict__ ranges0, int n_tiles,
+                            int32_t* __restrict__ cum0, int2* __restrict__ ranges0,
+                            unsigned int* __restrict__ tile_cnt, int n_tiles,
                             long long* __restrict__ dtgt, PhaseTargets tgt, int n_tgt) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < 16) dsmall[i] = (i == 6) ? ~0ull : 0ull;
@@ -1081,14 +1260,16 @@ __global__ void k_call_init(unsigned long long* __restrict__ dsmall, uint8_t* __
     active[i] = 1;
     cum0[i] = 0;
     ranges0[i] = make_int2(0, 0);
+    tile_cnt[i] = 0u;
   }
 }
 void launch_call_init(unsigned long long* dsmall, uint8_t* active, int32_t* cum0, int2* ranges0,
-                      int n_tiles, long long* dtgt, const int64_t* tgt, int n_tgt, cudaStream_t s) {
+                      unsigned int* tile_cnt, int n_tiles, long long* dtgt, const int64_t* tgt,
+                      int n_tgt, cudaStream_t s) {
   PhaseTargets t{};
   for (int i = 0; i < n_tgt && i < 4; ++i) t.v[i] = tgt[i];
   const int n = std::max(n_tiles, 16);
-  k_call_init<<<(n + 255) / 256, 256, 0, s>>>(dsmall, active, cum0, ranges0, n_tiles, dtgt, t,
+  k_call_init<<<(n + 255) / 256, 256, 0, s>>>(dsmall, active, cum0, ranges0, tile_cnt, n_tiles, dtgt, t,
                                               std::min(n_tgt, 4));
 }
 void launch_pack_check(const unsigned long long* dsmall, const long long* dsel, int n_ph,
