@@ -60,7 +60,12 @@ void launch_rank_of_range(const uint32_t*, int64_t, int64_t, uint32_t*, cudaStre
                           const int* nd = nullptr);
 void launch_key_hist(const uint32_t*, int64_t, unsigned int*, cudaStream_t);
 void launch_phase_select(const unsigned int*, const int64_t*, int, int64_t, long long*,
-                         cudaStream_t, int max_bin0 = -1, unsigned long long* overflow = nullptr);
+                         cudaStream_t, int max_bin0 = -1, unsigned long long* overflow = nullptr,
+                         unsigned int* bin_pos = nullptr, int* n_sel = nullptr);
+void launch_bin_scatter(const uint32_t*, int64_t, int, int, const long long*, unsigned int*,
+                        uint32_t*, cudaStream_t);
+void launch_bin_sort(uint32_t*, const double*, const unsigned int*, const unsigned int*, int, int,
+                     const long long*, uint32_t*, unsigned long long*, cudaStream_t);
 void launch_project_ranks(const float*, const float*, const float*, const float*, const float*,
                           int, int64_t, int64_t, const uint32_t*, const CamDev&, double, double,
                           int4*, float4*, float4*, unsigned long long*, double*, cudaStream_t,
@@ -203,6 +208,7 @@ struct nxs_view {
   Buf pk_in, pk_out, pv_in, pv_ph[MAX_PHASES];
   // per tile: phase ranges and virtual offsets, activity
   Buf ranges_ph[MAX_PHASES], cum_ph[MAX_PHASES + 1], active, tile_cnt;
+  Buf bin_pos;  // per depth-key bin: first rank, then the scatter cursor
   // per pixel: replay cache and the forward carry between phases
   Buf c_last, c_sat, c_tk, c_thi, c_tlo, c_P, c_ck, c_Pck, c_ek, c_th0;
   Buf r_rad, r_trem, r_count, r_sea, r_sa;
@@ -261,7 +267,7 @@ struct nxs_view {
   void for_each_buf(F f) {
     Buf* all[] = {&dkeys_in, &dkeys_out, &idx_in,  &idx_out, &records, &bframe, &rects,
                   &ntiles,   &offsets,   &moments, &touched, &pk_in,   &pk_out,  &pv_in,  &active,
-                  &tile_cnt,
+                  &tile_cnt, &bin_pos,
                   &depth,    &k32a,      &k32b,    &k32c,    &rank_of, &rank_c, &zlo_rank, &seq, &ph_hist,
                   &ph_sel,   &tq,      &zlo64,  &xc_t, &xc_r, &xc_n,
                   &c_last,   &c_sat,     &c_tk,    &c_thi,   &c_tlo,   &c_P,    &c_ck,
@@ -275,6 +281,10 @@ struct nxs_view {
     for (int p = 0; p <= MAX_PHASES; ++p) f(cum_ph[p]);
   }
   ~nxs_view() {
+    // work of this view may still be queued (the caller's stream, the side
+    // stream's readbacks into host_small): let it drain before freeing
+    cudaDeviceSynchronize();
+    cudaGetLastError();
     for_each_buf([](Buf& b) { b.release(); });
     if (host_small) cudaFreeHost(host_small);
     if (ev_sync) cudaEventDestroy(ev_sync);
@@ -421,6 +431,8 @@ int complete_order(nxs_view* v, cudaStream_t s) {
   if (!v->lazy || v->sorted_end >= v->P) return NXS_OK;
   const int64_t r0 = v->sorted_end, n = v->P - r0;
   unsigned long long* dsmall = v->dev_small.as<unsigned long long>();
+  NXS_CUDA(ensure_n<uint32_t>(v->k32c, v->P));
+  NXS_CUDA(ensure_n<uint32_t>(v->k32b, v->P));
   size_t tbs = v->temp.cap;
   NXS_CUDA(cub::DeviceSelect::If(v->temp.p, tbs, cub::CountingInputIterator<uint32_t>(0),
                                  v->idx_in.as<uint32_t>(),
@@ -689,6 +701,7 @@ int forward_impl(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
   NXS_CUDA(ensure_n<int2>(v->ranges_ph[0], n_tiles));
   NXS_CUDA(ensure_n<int32_t>(v->cum_ph[0], n_tiles));
   NXS_CUDA(ensure_n<uint32_t>(v->tile_cnt, n_tiles));
+  NXS_CUDA(ensure_n<uint32_t>(v->bin_pos, 4096));
   NXS_CUDA(v->ph_hist.ensure(4096 * sizeof(unsigned int)));
   NXS_CUDA(v->ph_sel.ensure(96 * sizeof(long long)));
   if (P == 0) {  // (P > 0: k_call_init below, in the pipeline)
@@ -755,6 +768,10 @@ int forward_impl(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
   // estimates from this view's previous call and a later phase to verify at
   bool async0 = v->est_n0 > 0 && v->est_pairs >= 0 && v->est_bin0 >= 0 && n_ph >= 2 &&
                 spec_phase >= 0 && !chunked && !exact;
+  if (std::getenv("NXS_DEBUG_PLAN"))
+    std::fprintf(stderr, "plan P=%lld n_ph=%d R1=%lld async0=%d est_n0=%lld est_bin0=%d hint=%llu\n",
+                 (long long)P, n_ph, (long long)R[1], (int)async0, (long long)v->est_n0,
+                 v->est_bin0, (unsigned long long)v->host_small[30]);
   int64_t proc_end = 0;  // chunked lazy phases: ranks [0, proc_end) are processed
   bool phase_full[MAX_PHASES] = {false, false, false, false};  // lazy phase sorted on 32 bits
   int phase_shift[MAX_PHASES] = {0, 0, 0, 0};
@@ -889,7 +906,8 @@ retry_sort:
         // checked on the device (k_phase_select) and verified later
         ph_bin[0] = std::min(4095, v->est_bin0 + 2);
         launch_phase_select(v->ph_hist.as<unsigned int>(), reinterpret_cast<int64_t*>(dsel + 32),
-                            n_ph - 1, P, dsel, s, ph_bin[0], dsmall + 10);
+                            n_ph - 1, P, dsel, s, ph_bin[0], dsmall + 10,
+                            v->bin_pos.as<uint32_t>(), reinterpret_cast<int*>(dsel + 48));
         NXS_LAUNCHED("phase_select");
         v->async_cap0 = std::min<int64_t>(P, v->est_n0 + v->est_n0 / 8 + 2048);
         v->async_capp = v->est_pairs + v->est_pairs / 8 + 8192;
@@ -900,7 +918,7 @@ retry_sort:
     if (v->lazy && !async0) {
       long long* dsel = v->ph_sel.as<long long>();
       launch_phase_select(v->ph_hist.as<unsigned int>(), reinterpret_cast<int64_t*>(dsel + 32),
-                          n_ph - 1, P, dsel, s);
+                          n_ph - 1, P, dsel, s, -1, nullptr, v->bin_pos.as<uint32_t>());
       NXS_LAUNCHED("phase_select");
       long long* hsel = reinterpret_cast<long long*>(v->host_small + 16);
       NXS_CUDA(cudaMemcpyAsync(hsel, dsel, sizeof(long long) * 2 * n_ph, cudaMemcpyDeviceToHost,
@@ -1022,29 +1040,17 @@ retry_sort:
       // this view's previous call; the real counts stay on the device
       // (n_sel, pair total) and are verified behind the forward
       const int64_t cap0 = v->async_cap0, capp = v->async_capp;
-      int* n_sel = reinterpret_cast<int*>(v->ph_sel.as<long long>() + 48);
+      int* n_sel = reinterpret_cast<int*>(v->ph_sel.as<long long>() + 48);  // (k_phase_select)
       long long* dsel = v->ph_sel.as<long long>();
-      size_t tbs = v->temp.cap;
-      NXS_CUDA(cub::DeviceSelect::If(v->temp.p, tbs, cub::CountingInputIterator<uint32_t>(0),
-                                     v->idx_in.as<uint32_t>(), n_sel, (int)P,
-                                     BinRange{v->k32a.as<uint32_t>(), 0, 0, dsel}, s));
-      NXS_CUDA(ensure_n<uint32_t>(v->k32c, P));
-      launch_gather_keys_pad(v->idx_in.as<uint32_t>(), v->k32a.as<uint32_t>(), n_sel, cap0,
-                             v->k32c.as<uint32_t>(), s);
-      NXS_LAUNCHED("gather_keys_pad");
-      const int end_bit = std::min(32, 20 + bits_for((uint32_t)ph_bin[0] + 1));
-      const int shift = std::max(0, end_bit - 16);
-      size_t tb = v->temp.cap;
-      NXS_CUDA(cub::DeviceRadixSort::SortPairs(v->temp.p, tb, v->k32c.as<uint32_t>(),
-                                               v->k32b.as<uint32_t>(), v->idx_in.as<uint32_t>(),
-                                               v->idx_out.as<uint32_t>(), (int)cap0, shift,
-                                               shift ? end_bit : 32, s));
-      launch_key_fixup(v->k32b.as<uint32_t>(), v->idx_out.as<uint32_t>(), v->depth.as<double>(),
-                       cap0, dsmall + 8, s, shift, n_sel);
-      NXS_LAUNCHED("key_fixup");
-      launch_rank_of_range(v->idx_out.as<uint32_t>(), 0, cap0, v->rank_of.as<uint32_t>(), s,
-                           n_sel);
-      NXS_LAUNCHED("rank_of");
+      // exact order of phase 0's key bins [0, dsel[0]]: scatter into the
+      // bins' rank ranges, per-bin sort by (depth, index), ranks
+      launch_bin_scatter(v->k32a.as<uint32_t>(), P, 0, 0, dsel, v->bin_pos.as<uint32_t>(),
+                         v->idx_out.as<uint32_t>(), s);
+      NXS_LAUNCHED("bin_scatter");
+      launch_bin_sort(v->idx_out.as<uint32_t>(), v->depth.as<double>(),
+                      v->ph_hist.as<unsigned int>(), v->bin_pos.as<uint32_t>(), 0, ph_bin[0], dsel,
+                      v->rank_of.as<uint32_t>(), dsmall + 10, s);
+      NXS_LAUNCHED("bin_sort");
       if (v->ev_ok) rec_event(v, v->evp[0][1], s);
       launch_project_ranks(scene->centers, scene->scales, scene->quats, scene->opacities,
                            scene->sh, C, 0, cap0, v->idx_out.as<uint32_t>(), cam,
@@ -1103,30 +1109,46 @@ retry_sort:
           // ---- this phase's Gaussians (key bins (prev, ph_bin]) in storage
           // order, 32-bit sort + fix-up into ranks [r0, r1), projection
           const int lo = ph == 0 ? 0 : ph_bin[ph - 1] + 1, hi = ph_bin[ph];
-          size_t tbs = v->temp.cap;
-          NXS_CUDA(cub::DeviceSelect::If(v->temp.p, tbs, cub::CountingInputIterator<uint32_t>(0),
-                                         v->idx_in.as<uint32_t>(),
-                                         reinterpret_cast<int*>(v->ph_sel.as<long long>() + 48),
-                                         (int)P, BinRange{v->k32a.as<uint32_t>(), lo, hi}, s));
-          NXS_CUDA(ensure_n<uint32_t>(v->k32c, P));
-          launch_gather_keys(v->idx_in.as<uint32_t>(), v->k32a.as<uint32_t>(), nr,
-                             v->k32c.as<uint32_t>(), s);
-          NXS_LAUNCHED("gather_keys");
-          // two radix passes over the top 16 significant key bits of the
-          // phase; the fix-up re-sorts equal truncated keys exactly (a run
-          // over 256 redoes the phase on all 32 bits)
-          const int end_bit = std::min(32, 20 + bits_for((uint32_t)hi + 1));
-          const int shift = phase_full[ph] ? 0 : std::max(0, end_bit - 16);
-          size_t tb = v->temp.cap;
-          NXS_CUDA(cub::DeviceRadixSort::SortPairs(v->temp.p, tb, v->k32c.as<uint32_t>(),
-                                                   v->k32b.as<uint32_t>() + r0,
-                                                   v->idx_in.as<uint32_t>(),
-                                                   v->idx_out.as<uint32_t>() + r0, (int)nr, shift,
-                                                   shift ? end_bit : 32, s));
-          launch_key_fixup(v->k32b.as<uint32_t>() + r0, v->idx_out.as<uint32_t>() + r0,
-                           v->depth.as<double>(), nr, dsmall + 8, s, shift);
-          phase_shift[ph] = shift;
-          NXS_LAUNCHED("key_fixup");
+          if (!phase_full[ph]) {
+            // scatter into the bins' rank ranges, per-bin exact sort, ranks
+            // (a bin too long for one block redoes the phase with the sort)
+            NXS_CUDA(ensure_n<uint32_t>(chunked ? v->rank_c : v->rank_of, P));
+            launch_bin_scatter(v->k32a.as<uint32_t>(), P, lo, hi, nullptr,
+                               v->bin_pos.as<uint32_t>(), v->idx_out.as<uint32_t>(), s);
+            NXS_LAUNCHED("bin_scatter");
+            launch_bin_sort(v->idx_out.as<uint32_t>(), v->depth.as<double>(),
+                            v->ph_hist.as<unsigned int>(), v->bin_pos.as<uint32_t>(), lo, hi,
+                            nullptr, chunked ? v->rank_c.as<uint32_t>() : v->rank_of.as<uint32_t>(),
+                            dsmall + 8, s);
+            NXS_LAUNCHED("bin_sort");
+            phase_shift[ph] = 1;  // (an overflow redoes the phase with the radix sort)
+          } else {
+            size_t tbs = v->temp.cap;
+            NXS_CUDA(cub::DeviceSelect::If(v->temp.p, tbs, cub::CountingInputIterator<uint32_t>(0),
+                                           v->idx_in.as<uint32_t>(),
+                                           reinterpret_cast<int*>(v->ph_sel.as<long long>() + 48),
+                                           (int)P, BinRange{v->k32a.as<uint32_t>(), lo, hi}, s));
+            NXS_CUDA(ensure_n<uint32_t>(v->k32c, P));
+            launch_gather_keys(v->idx_in.as<uint32_t>(), v->k32a.as<uint32_t>(), nr,
+                               v->k32c.as<uint32_t>(), s);
+            NXS_LAUNCHED("gather_keys");
+            // 32-bit radix sort; the fix-up re-sorts equal keys exactly (a
+            // run over 256 falls back to the 64-bit sort)
+            size_t tb = v->temp.cap;
+            NXS_CUDA(cub::DeviceRadixSort::SortPairs(v->temp.p, tb, v->k32c.as<uint32_t>(),
+                                                     v->k32b.as<uint32_t>() + r0,
+                                                     v->idx_in.as<uint32_t>(),
+                                                     v->idx_out.as<uint32_t>() + r0, (int)nr, 0,
+                                                     32, s));
+            launch_key_fixup(v->k32b.as<uint32_t>() + r0, v->idx_out.as<uint32_t>() + r0,
+                             v->depth.as<double>(), nr, dsmall + 8, s, 0);
+            NXS_LAUNCHED("key_fixup");
+            phase_shift[ph] = 0;
+            NXS_CUDA(ensure_n<uint32_t>(chunked ? v->rank_c : v->rank_of, P));
+            launch_rank_of_range(v->idx_out.as<uint32_t>(), r0, r1,
+                                 chunked ? v->rank_c.as<uint32_t>() : v->rank_of.as<uint32_t>(), s);
+            NXS_LAUNCHED("rank_of");
+          }
           v->sorted_end = r1;
           v->bin_done = hi;
           if (chunked) {
@@ -1135,8 +1157,7 @@ retry_sort:
             NXS_CUDA(ensure_n<uint32_t>(v->rank_c, P));
             NXS_CUDA(ensure_n<double>(v->zlo64, P));
             NXS_CUDA(ensure_n<float>(v->zlo_rank, P));
-            launch_rank_of_range(v->idx_out.as<uint32_t>(), r0, r1, v->rank_c.as<uint32_t>(), s);
-            NXS_LAUNCHED("rank_c");
+            // (rank_c of this phase was written with the sort)
             const int64_t Cc = opts->chunk_size;
             const int64_t p0 = proc_end, p1 = (r1 >= P) ? P : (r1 / Cc) * Cc;
             if (v->ev_ok) rec_event(v, v->evp[ph][1], s);
@@ -1168,9 +1189,7 @@ retry_sort:
             r1 = p1;
             nr = p1 - p0;
           } else {
-            launch_rank_of_range(v->idx_out.as<uint32_t>(), r0, r1, v->rank_of.as<uint32_t>(),
-                                 s);
-            NXS_LAUNCHED("rank_of");
+            // (rank_of of this phase was written with the sort)
             if (v->ev_ok) rec_event(v, v->evp[ph][1], s);
             if (exact) {  // z_lo per rank for the pending-buffer bounds
               NXS_CUDA(ensure_n<float>(v->zlo_rank, P));

@@ -287,7 +287,9 @@ __global__ void __launch_bounds__(1024) k_phase_select(const unsigned int* __res
                                                        int n_targets, int64_t P,
                                                        long long* __restrict__ out,
                                                        int max_bin0,
-                                                       unsigned long long* __restrict__ overflow) {
+                                                       unsigned long long* __restrict__ overflow,
+                                                       unsigned int* __restrict__ bin_pos,
+                                                       int* __restrict__ n_sel) {
   __shared__ unsigned long long cum[PH_BINS];
   __shared__ unsigned long long wsum[32];
   constexpr int PER = PH_BINS / 1024;
@@ -316,7 +318,11 @@ __global__ void __launch_bounds__(1024) k_phase_select(const unsigned int* __res
   __syncthreads();
   const unsigned long long base = x - run + (w > 0 ? wsum[w - 1] : 0ull);
 #pragma unroll
-  for (int k = 0; k < PER; ++k) cum[t * PER + k] = base + loc[k];
+  for (int k = 0; k < PER; ++k) {
+    cum[t * PER + k] = base + loc[k];
+    // each bin's first rank: the scatter's cursor (k_bin_scatter)
+    if (bin_pos) bin_pos[t * PER + k] = (unsigned int)(base + loc[k] - hist[t * PER + k]);
+  }
   __syncthreads();
   if (t < n_targets) {
     const unsigned long long T = (unsigned long long)targets[t];
@@ -334,6 +340,104 @@ __global__ void __launch_bounds__(1024) k_phase_select(const unsigned int* __res
     out[2 * n_targets] = PH_BINS - 1;
     out[2 * n_targets + 1] = P;
     if (n_targets == 0 && max_bin0 >= 0 && max_bin0 < PH_BINS - 1) atomicAdd(overflow, 1ull);
+    if (n_sel) *n_sel = (int)out[1];  // Gaussians of phase 0
+  }
+}
+
+// ---- one depth phase in exact order without a global sort: the phase's
+// key bins are contiguous rank ranges (k_phase_select's bin_pos), each
+// Gaussian is scattered into its bin (any order), then each bin is sorted
+// exactly by (depth, index) — NaN last — in shared memory, which is the
+// order the 32-bit sort + fix-up produces.  Ranks are written alongside.
+__global__ void k_bin_scatter(const uint32_t* __restrict__ key, int64_t P, int lo, int hi,
+                              const long long* __restrict__ hi_dev,
+                              unsigned int* __restrict__ bin_pos, uint32_t* __restrict__ order) {
+  if (hi_dev) hi = (int)hi_dev[0];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int b = (int)(key[i] >> 20);
+    if (b >= lo && b <= hi) order[atomicAdd(&bin_pos[b], 1u)] = (uint32_t)i;
+  }
+}
+
+__device__ __forceinline__ bool depth_before(double da, uint32_t ia, double db, uint32_t ib) {
+  const bool na = !(da == da), nb = !(db == db);
+  if (na != nb) return nb;  // numbers before NaN
+  if (!na && da != db) return da < db;
+  return ia < ib;
+}
+
+constexpr int BIN_THREADS = 256;
+constexpr int BIN_MAX = 2048;  // longest bin sorted in shared memory
+__global__ void __launch_bounds__(BIN_THREADS)
+    k_bin_sort(uint32_t* __restrict__ order, const double* __restrict__ depth,
+               const unsigned int* __restrict__ hist, const unsigned int* __restrict__ bin_end,
+               int lo, int hi, const long long* __restrict__ hi_dev,
+               uint32_t* __restrict__ rank_out, unsigned long long* __restrict__ overflow) {
+  __shared__ double s_d[BIN_MAX];
+  __shared__ uint32_t s_i[BIN_MAX];
+  if (hi_dev) hi = (int)hi_dev[0];
+  const int b = lo + blockIdx.x, tid = threadIdx.x;
+  if (b > hi) return;
+  const int n = (int)hist[b];
+  if (n == 0) return;
+  const int start = (int)bin_end[b] - n;
+  uint32_t* v = order + start;
+  if (n > BIN_MAX) {
+    if (tid == 0) atomicAdd(overflow, 1ull);
+    return;
+  }
+  if (n <= BIN_THREADS) {  // rank counting
+    uint32_t mi = 0u;
+    double md = 0.0;
+    if (tid < n) {
+      mi = v[tid];
+      md = depth[mi];
+      s_i[tid] = mi;
+      s_d[tid] = md;
+    }
+    __syncthreads();
+    if (tid < n) {
+      int pos = 0;
+      for (int j = 0; j < n; ++j) pos += depth_before(s_d[j], s_i[j], md, mi) ? 1 : 0;
+      v[pos] = mi;
+      if (rank_out) rank_out[mi] = (uint32_t)(start + pos);
+    }
+    return;
+  }
+  int p2 = BIN_THREADS * 2;
+  while (p2 < n) p2 <<= 1;
+  for (int i = tid; i < p2; i += BIN_THREADS) {
+    if (i < n) {
+      const uint32_t g = v[i];
+      s_i[i] = g;
+      s_d[i] = depth[g];
+    } else {
+      s_i[i] = 0xffffffffu;
+      s_d[i] = __longlong_as_double(0x7ff8000000000000ll);  // NaN, index max: last
+    }
+  }
+  __syncthreads();
+  for (int size = 2; size <= p2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = tid; i < (p2 >> 1); i += BIN_THREADS) {
+        const int a = 2 * i - (i & (stride - 1)), c = a + stride;
+        const bool up = (a & size) == 0;
+        const double da = s_d[a], dc = s_d[c];
+        const uint32_t ia = s_i[a], ic = s_i[c];
+        if (depth_before(dc, ic, da, ia) == up) {
+          s_d[a] = dc;
+          s_d[c] = da;
+          s_i[a] = ic;
+          s_i[c] = ia;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = tid; i < n; i += BIN_THREADS) {
+    v[i] = s_i[i];
+    if (rank_out) rank_out[s_i[i]] = (uint32_t)(start + i);
   }
 }
 
@@ -1001,7 +1105,9 @@ __global__ void __launch_bounds__(TSCAN_THREADS)
   atomicMax(&s_max, mx);
   for (int t = lo; t < hi; ++t) {
     const unsigned int c = tile_cnt[t];
-    ranges[t] = make_int2((int)off, (int)(off + c));
+    // (a device-sized buffer too small: lists clamped to it, the pass is
+    // flagged and redone — no list may reach past the buffer meanwhile)
+    ranges[t] = make_int2((int)min(off, cap), (int)min(off + c, cap));
     off += c;
     tile_cnt[t] = 0u;
   }
@@ -1353,8 +1459,25 @@ void launch_key_hist(const uint32_t* key, int64_t P, unsigned int* hist, cudaStr
 }
 void launch_phase_select(const unsigned int* hist, const int64_t* targets, int n_targets,
                          int64_t P, long long* out, cudaStream_t s, int max_bin0,
-                         unsigned long long* overflow) {
-  k_phase_select<<<1, 1024, 0, s>>>(hist, targets, n_targets, P, out, max_bin0, overflow);
+                         unsigned long long* overflow, unsigned int* bin_pos, int* n_sel) {
+  k_phase_select<<<1, 1024, 0, s>>>(hist, targets, n_targets, P, out, max_bin0, overflow,
+                                    bin_pos, n_sel);
+}
+void launch_bin_scatter(const uint32_t* key, int64_t P, int lo, int hi, const long long* hi_dev,
+                        unsigned int* bin_pos, uint32_t* order, cudaStream_t s) {
+  if (P <= 0) return;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned grid = (unsigned)std::min<int64_t>((P + 255) / 256, (int64_t)sms * 8);
+  k_bin_scatter<<<grid, 256, 0, s>>>(key, P, lo, hi, hi_dev, bin_pos, order);
+}
+void launch_bin_sort(uint32_t* order, const double* depth, const unsigned int* hist,
+                     const unsigned int* bin_end, int lo, int hi, const long long* hi_dev,
+                     uint32_t* rank_out, unsigned long long* overflow, cudaStream_t s) {
+  if (hi < lo) return;
+  k_bin_sort<<<hi - lo + 1, BIN_THREADS, 0, s>>>(order, depth, hist, bin_end, lo, hi, hi_dev,
+                                                 rank_out, overflow);
 }
 void launch_project_ranks(const float* centers, const float* scales, const float* quats,
                           const float* opacities, const float* sh, int C, int64_t r0, int64_t r1,
