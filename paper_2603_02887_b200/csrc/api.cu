@@ -89,7 +89,10 @@ void launch_project_ranks_z(const float*, const float*, const float*, const floa
 void launch_pack_check(const unsigned long long*, const long long*, int, unsigned long long*,
                        cudaStream_t);
 void launch_call_init(unsigned long long*, uint8_t*, int32_t*, int2*, unsigned int*, int,
-                      long long*, const int64_t*, int, cudaStream_t);
+                      long long*, const int64_t*, int, unsigned int*, cudaStream_t);
+void launch_key32_hist(const double*, int64_t, const unsigned long long*, uint32_t*,
+                       unsigned int*, cudaStream_t);
+void launch_dkeys(const double*, int64_t, unsigned long long*, cudaStream_t);
 void launch_count_tiles(const int4*, const uint32_t*, int64_t, int64_t, int, const uint8_t*,
                         const unsigned int*, unsigned int*, const double*, const CamDev&,
                         cudaStream_t, const int* nd = nullptr);
@@ -458,6 +461,8 @@ int complete_order(nxs_view* v, cudaStream_t s) {
     // prefix is the order the processed phases already used)
     launch_iota(v->idx_in.as<uint32_t>(), v->P, s);
     NXS_LAUNCHED("iota");
+    launch_dkeys(v->depth.as<double>(), v->P, v->dkeys_in.as<unsigned long long>(), s);
+    NXS_LAUNCHED("dkeys");
     size_t tb64 = 0;
     NXS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb64, v->dkeys_in.as<unsigned long long>(),
                                              v->dkeys_out.as<unsigned long long>(),
@@ -880,13 +885,16 @@ retry_sort:
       for (int p = 1; p < n_ph && p <= 4; ++p) tgt[p - 1] = R[p];
       launch_call_init(dsmall, v->active.as<uint8_t>(), v->cum_ph[0].as<int32_t>(),
                        v->ranges_ph[0].as<int2>(), v->tile_cnt.as<uint32_t>(), n_tiles,
-                       v->lazy ? v->ph_sel.as<long long>() + 32 : nullptr, tgt, n_ph - 1, s);
+                       v->lazy ? v->ph_sel.as<long long>() + 32 : nullptr, tgt, n_ph - 1,
+                       v->ph_hist.as<unsigned int>(), s);
       NXS_LAUNCHED("call_init");
     }
     // ---- K0 depth (+ min/max) and the stable depth sort
+    const bool keys64 = sort64 || !v->lazy;  // lazy phases need only the depths
     launch_depth(scene->centers, scene->scales, scene->quats, scene->opacities, P, cam,
                  opts->alpha_cutoff, exact ? 1 : 0, v->depth.as<double>(),
-                 v->dkeys_in.as<unsigned long long>(), v->idx_in.as<uint32_t>(), dsmall + 6, s);
+                 keys64 ? v->dkeys_in.as<unsigned long long>() : nullptr,
+                 keys64 ? v->idx_in.as<uint32_t>() : nullptr, dsmall + 6, s);
     NXS_LAUNCHED("depth");
     size_t tb = v->temp.cap;
     if (sort64) {
@@ -896,10 +904,9 @@ retry_sort:
           v->idx_out.as<uint32_t>(), (int)P, 0, 64, s));
     } else if (v->lazy) {
       // phase boundaries on whole key bins: one host sync for their ranks
-      launch_key32(v->depth.as<double>(), P, dsmall + 6, v->k32a.as<uint32_t>(), s);
-      NXS_LAUNCHED("key32");
-      launch_key_hist(v->k32a.as<uint32_t>(), P, v->ph_hist.as<unsigned int>(), s);
-      NXS_LAUNCHED("key_hist");
+      launch_key32_hist(v->depth.as<double>(), P, dsmall + 6, v->k32a.as<uint32_t>(),
+                        v->ph_hist.as<unsigned int>(), s);
+      NXS_LAUNCHED("key32_hist");
       long long* dsel = v->ph_sel.as<long long>();  // [32..) phase targets (k_call_init)
       if (async0) {
         // phase 0 sized from the previous call; the last bin it may use is

@@ -163,8 +163,10 @@ __global__ void k_depth(const float* __restrict__ centers, const float* __restri
                            : dot3_compensated(b0, b1, b2, cam.R[2], cam.R[5], cam.R[8]);
     depth[i] = d;
     const unsigned long long k = dkey(d);
-    key64[i] = k;
-    idx[i] = (uint32_t)i;
+    if (key64) {  // (the 64-bit sort's keys and values; lazy phases need neither)
+      key64[i] = k;
+      idx[i] = (uint32_t)i;
+    }
     if (d == d) {
       kmin = k;
       kmax = k;
@@ -194,22 +196,50 @@ __global__ void k_depth(const float* __restrict__ centers, const float* __restri
 
 // 32-bit monotone key: floor((d - dmin) * (2^32 - 2) / (dmax - dmin)); NaN last.
 // d1 < d2 implies key(d1) <= key(d2); equal keys are re-ordered by k_key_fixup.
+__device__ __forceinline__ uint32_t key32_of(double d, double lo, double scale, bool spread) {
+  if (!(d == d)) return 0xffffffffu;
+  if (!spread) return 0u;
+  double x = (d - lo) * scale;
+  x = x < 0.0 ? 0.0 : (x > 4294967294.0 ? 4294967294.0 : x);
+  return (uint32_t)x;
+}
 __global__ void k_key32(const double* __restrict__ depth, int64_t P,
                         const unsigned long long* __restrict__ kminmax,
                         uint32_t* __restrict__ key) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P) return;
-  const double d = depth[i];
-  uint32_t k = 0u;
-  if (!(d == d)) {
-    k = 0xffffffffu;
-  } else if (kminmax[0] < kminmax[1]) {
-    const double lo = dkey_inv(kminmax[0]), hi = dkey_inv(kminmax[1]);
-    double x = (d - lo) * (4294967294.0 / (hi - lo));
-    x = x < 0.0 ? 0.0 : (x > 4294967294.0 ? 4294967294.0 : x);
-    k = (uint32_t)x;
+  const bool spread = kminmax[0] < kminmax[1];
+  const double lo = dkey_inv(kminmax[0]), hi = dkey_inv(kminmax[1]);
+  key[i] = key32_of(depth[i], lo, 4294967294.0 / (hi - lo), spread);
+}
+// the same keys and, in one pass, their histogram over the top 12 bits
+// (k_key_hist's; hist is zeroed by k_call_init)
+constexpr int PH_BINS_ = 4096;
+__global__ void __launch_bounds__(1024)
+    k_key32_hist(const double* __restrict__ depth, int64_t P,
+                 const unsigned long long* __restrict__ kminmax, uint32_t* __restrict__ key,
+                 unsigned int* __restrict__ hist) {
+  __shared__ unsigned int sh[PH_BINS_];
+  for (int b = threadIdx.x; b < PH_BINS_; b += blockDim.x) sh[b] = 0u;
+  const bool spread = kminmax[0] < kminmax[1];
+  const double lo = dkey_inv(kminmax[0]), hi = dkey_inv(kminmax[1]);
+  const double scale = 4294967294.0 / (hi - lo);
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = key32_of(depth[i], lo, scale, spread);
+    key[i] = k;
+    atomicAdd(&sh[k >> 20], 1u);
   }
-  key[i] = k;
+  __syncthreads();
+  for (int b = threadIdx.x; b < PH_BINS_; b += blockDim.x)
+    if (sh[b]) atomicAdd(&hist[b], sh[b]);
+}
+// 64-bit keys of the fallback sort from the depths (lazy phases skip them in K0)
+__global__ void k_dkeys(const double* __restrict__ depth, int64_t P,
+                        unsigned long long* __restrict__ key64) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < P) key64[i] = dkey(depth[i]);
 }
 
 // Runs of equal 32-bit keys come out of the stable sort in index order;
@@ -1267,6 +1297,19 @@ void launch_key32(const double* depth, int64_t P, const unsigned long long* kmin
   if (P == 0) return;
   k_key32<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(depth, P, kminmax, key);
 }
+void launch_key32_hist(const double* depth, int64_t P, const unsigned long long* kminmax,
+                       uint32_t* key, unsigned int* hist, cudaStream_t s) {
+  if (P == 0) return;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned grid = (unsigned)std::min<int64_t>((P + 1023) / 1024, (int64_t)sms * 2);
+  k_key32_hist<<<grid, 1024, 0, s>>>(depth, P, kminmax, key, hist);
+}
+void launch_dkeys(const double* depth, int64_t P, unsigned long long* key64, cudaStream_t s) {
+  if (P == 0) return;
+  k_dkeys<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(depth, P, key64);
+}
 void launch_key_fixup(const uint32_t* key, uint32_t* idx, const double* depth, int64_t P,
                       unsigned long long* overflow, cudaStream_t s, int shift, const int* nd) {
   if (P == 0) return;
@@ -1358,8 +1401,10 @@ struct PhaseTargets {
 __global__ void k_call_init(unsigned long long* __restrict__ dsmall, uint8_t* __restrict__ active,
                             int32_t* __restrict__ cum0, int2* __restrict__ ranges0,
                             unsigned int* __restrict__ tile_cnt, int n_tiles,
-                            long long* __restrict__ dtgt, PhaseTargets tgt, int n_tgt) {
+                            long long* __restrict__ dtgt, PhaseTargets tgt, int n_tgt,
+                            unsigned int* __restrict__ hist) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (hist && i < 4096) hist[i] = 0u;
   if (i < 16) dsmall[i] = (i == 6) ? ~0ull : 0ull;
   if (dtgt && i < n_tgt) dtgt[i] = tgt.v[i];
   if (i < n_tiles) {
@@ -1371,12 +1416,12 @@ __global__ void k_call_init(unsigned long long* __restrict__ dsmall, uint8_t* __
 }
 void launch_call_init(unsigned long long* dsmall, uint8_t* active, int32_t* cum0, int2* ranges0,
                       unsigned int* tile_cnt, int n_tiles, long long* dtgt, const int64_t* tgt,
-                      int n_tgt, cudaStream_t s) {
+                      int n_tgt, unsigned int* hist, cudaStream_t s) {
   PhaseTargets t{};
   for (int i = 0; i < n_tgt && i < 4; ++i) t.v[i] = tgt[i];
-  const int n = std::max(n_tiles, 16);
+  const int n = std::max(n_tiles, 4096);
   k_call_init<<<(n + 255) / 256, 256, 0, s>>>(dsmall, active, cum0, ranges0, tile_cnt, n_tiles, dtgt, t,
-                                              std::min(n_tgt, 4));
+                                              std::min(n_tgt, 4), hist);
 }
 void launch_pack_check(const unsigned long long* dsmall, const long long* dsel, int n_ph,
                        unsigned long long* out, cudaStream_t s) {
