@@ -102,7 +102,7 @@ void launch_emit_tiles(const int4*, const uint32_t*, int64_t, int64_t, int, cons
                        const int2*, unsigned int*, uint32_t*, const double*, const CamDev&,
                        cudaStream_t, const int* nd, unsigned long long cap);
 void launch_seg_sort(uint32_t*, const int2*, unsigned int*, int, unsigned long long,
-                     cudaStream_t);
+                     cudaStream_t, long long max_seg = -1);
 void launch_chunk_key(const float*, const float*, const float*, const float*, int64_t,
                       const CamDev&, double, const uint32_t*, int, double*, unsigned long long*,
                       uint32_t*, cudaStream_t);
@@ -706,7 +706,7 @@ int forward_impl(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
   NXS_CUDA(ensure_n<int2>(v->ranges_ph[0], n_tiles));
   NXS_CUDA(ensure_n<int32_t>(v->cum_ph[0], n_tiles));
   NXS_CUDA(ensure_n<uint32_t>(v->tile_cnt, n_tiles));
-  NXS_CUDA(ensure_n<uint32_t>(v->bin_pos, 4096));
+  NXS_CUDA(ensure_n<uint32_t>(v->bin_pos, 4096 * 32));  // (one cursor per 128-byte line)
   NXS_CUDA(v->ph_hist.ensure(4096 * sizeof(unsigned int)));
   NXS_CUDA(v->ph_sel.ensure(96 * sizeof(long long)));
   if (P == 0) {  // (P > 0: k_call_init below, in the pipeline)
@@ -1283,7 +1283,7 @@ retry_sort:
         NXS_LAUNCHED("emit_tiles");
         if (ph == 0) mark(v, 4, s);
         launch_seg_sort(v->pv_ph[ph].as<uint32_t>(), v->ranges_ph[ph].as<int2>(),
-                        v->tile_cnt.as<uint32_t>(), n_tiles, n_pairs, s);
+                        v->tile_cnt.as<uint32_t>(), n_tiles, n_pairs, s, (long long)max_seg);
         NXS_LAUNCHED("seg_sort");
         if (ph == 0) mark(v, 5, s);
       } else if (n_pairs > 0) {

@@ -295,6 +295,7 @@ __global__ void k_rank_of(const uint32_t* __restrict__ order, int64_t r0, int64_
 // never straddle a boundary) and concatenating the phases' sorted ranks is
 // exactly the full order.
 constexpr int PH_BINS = 4096;
+constexpr int BIN_STRIDE = 32;  // bin cursors, one per 128-byte line
 
 __global__ void k_key_hist(const uint32_t* __restrict__ key, int64_t P,
                            unsigned int* __restrict__ hist) {
@@ -350,8 +351,10 @@ __global__ void __launch_bounds__(1024) k_phase_select(const unsigned int* __res
 #pragma unroll
   for (int k = 0; k < PER; ++k) {
     cum[t * PER + k] = base + loc[k];
-    // each bin's first rank: the scatter's cursor (k_bin_scatter)
-    if (bin_pos) bin_pos[t * PER + k] = (unsigned int)(base + loc[k] - hist[t * PER + k]);
+    // each bin's first rank: the scatter's cursor (k_bin_scatter), one
+    // counter per 128-byte line so the scatter's atomics spread over L2
+    if (bin_pos)
+      bin_pos[(t * PER + k) * BIN_STRIDE] = (unsigned int)(base + loc[k] - hist[t * PER + k]);
   }
   __syncthreads();
   if (t < n_targets) {
@@ -386,66 +389,69 @@ __global__ void k_bin_scatter(const uint32_t* __restrict__ key, int64_t P, int l
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int b = (int)(key[i] >> 20);
-    if (b >= lo && b <= hi) order[atomicAdd(&bin_pos[b], 1u)] = (uint32_t)i;
+    if (b >= lo && b <= hi) order[atomicAdd(&bin_pos[b * BIN_STRIDE], 1u)] = (uint32_t)i;
   }
 }
 
-__device__ __forceinline__ bool depth_before(double da, uint32_t ia, double db, uint32_t ib) {
-  const bool na = !(da == da), nb = !(db == db);
-  if (na != nb) return nb;  // numbers before NaN
-  if (!na && da != db) return da < db;
-  return ia < ib;
+// exact depth order as one integer: monotone in the depth, -0 = +0, every
+// NaN last; ties (equal keys) go by index
+__device__ __forceinline__ unsigned long long depth_sortkey(double d) {
+  if (!(d == d)) return ~0ull;
+  return dkey(d == 0.0 ? 0.0 : d);
 }
 
-constexpr int BIN_THREADS = 256;
+constexpr int BIN_THREADS = 512;
 constexpr int BIN_MAX = 2048;  // longest bin sorted in shared memory
 __global__ void __launch_bounds__(BIN_THREADS)
     k_bin_sort(uint32_t* __restrict__ order, const double* __restrict__ depth,
                const unsigned int* __restrict__ hist, const unsigned int* __restrict__ bin_end,
                int lo, int hi, const long long* __restrict__ hi_dev,
                uint32_t* __restrict__ rank_out, unsigned long long* __restrict__ overflow) {
-  __shared__ double s_d[BIN_MAX];
+  __shared__ unsigned long long s_k[BIN_MAX];
   __shared__ uint32_t s_i[BIN_MAX];
   if (hi_dev) hi = (int)hi_dev[0];
   const int b = lo + blockIdx.x, tid = threadIdx.x;
   if (b > hi) return;
   const int n = (int)hist[b];
   if (n == 0) return;
-  const int start = (int)bin_end[b] - n;
+  const int start = (int)bin_end[b * BIN_STRIDE] - n;
   uint32_t* v = order + start;
   if (n > BIN_MAX) {
     if (tid == 0) atomicAdd(overflow, 1ull);
     return;
   }
-  if (n <= BIN_THREADS) {  // rank counting
-    uint32_t mi = 0u;
-    double md = 0.0;
-    if (tid < n) {
-      mi = v[tid];
-      md = depth[mi];
-      s_i[tid] = mi;
-      s_d[tid] = md;
-    }
+  for (int i = tid; i < n; i += BIN_THREADS) {
+    const uint32_t g = v[i];
+    s_i[i] = g;
+    s_k[i] = depth_sortkey(depth[g]);
+  }
+  if (n <= BIN_THREADS / 2) {
+    // rank counting: two threads per element (halves of the bin)
     __syncthreads();
-    if (tid < n) {
-      int pos = 0;
-      for (int j = 0; j < n; ++j) pos += depth_before(s_d[j], s_i[j], md, mi) ? 1 : 0;
+    const int e = tid >> 1, h = tid & 1;
+    const bool live = e < n;
+    const unsigned long long mk = live ? s_k[e] : 0ull;
+    const uint32_t mi = live ? s_i[e] : 0u;
+    int pos = 0;
+    if (live) {
+#pragma unroll 4
+      for (int j = h; j < n; j += 2) {
+        const unsigned long long kj = s_k[j];
+        pos += (kj < mk || (kj == mk && s_i[j] < mi)) ? 1 : 0;
+      }
+    }
+    pos += __shfl_xor_sync(0xffffffffu, pos, 1);
+    if (live && h == 0) {
       v[pos] = mi;
       if (rank_out) rank_out[mi] = (uint32_t)(start + pos);
     }
     return;
   }
-  int p2 = BIN_THREADS * 2;
+  int p2 = 512;
   while (p2 < n) p2 <<= 1;
-  for (int i = tid; i < p2; i += BIN_THREADS) {
-    if (i < n) {
-      const uint32_t g = v[i];
-      s_i[i] = g;
-      s_d[i] = depth[g];
-    } else {
-      s_i[i] = 0xffffffffu;
-      s_d[i] = __longlong_as_double(0x7ff8000000000000ll);  // NaN, index max: last
-    }
+  for (int i = n + tid; i < p2; i += BIN_THREADS) {
+    s_i[i] = 0xffffffffu;
+    s_k[i] = ~0ull;
   }
   __syncthreads();
   for (int size = 2; size <= p2; size <<= 1) {
@@ -453,11 +459,12 @@ __global__ void __launch_bounds__(BIN_THREADS)
       for (int i = tid; i < (p2 >> 1); i += BIN_THREADS) {
         const int a = 2 * i - (i & (stride - 1)), c = a + stride;
         const bool up = (a & size) == 0;
-        const double da = s_d[a], dc = s_d[c];
+        const unsigned long long ka = s_k[a], kc = s_k[c];
         const uint32_t ia = s_i[a], ic = s_i[c];
-        if (depth_before(dc, ic, da, ia) == up) {
-          s_d[a] = dc;
-          s_d[c] = da;
+        const bool c_first = kc < ka || (kc == ka && ic < ia);
+        if (c_first == up) {
+          s_k[a] = kc;
+          s_k[c] = ka;
           s_i[a] = ic;
           s_i[c] = ia;
         }
@@ -1112,6 +1119,7 @@ __global__ void __launch_bounds__(256)
 // the total (and whether it exceeds cap), the longest list; the counts are
 // reset to zero to serve as the emission cursors
 constexpr int TSCAN_THREADS = 1024;
+constexpr int TSCAN_STAGED = 32768;  // tiles staged in shared memory (128 KB)
 __global__ void __launch_bounds__(TSCAN_THREADS)
     k_tile_scan(unsigned int* __restrict__ tile_cnt, int n_tiles, int2* __restrict__ ranges,
                 unsigned long long* __restrict__ total, unsigned long long* __restrict__ maxseg,
@@ -1119,30 +1127,52 @@ __global__ void __launch_bounds__(TSCAN_THREADS)
   typedef cub::BlockScan<unsigned long long, TSCAN_THREADS> Scan;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ unsigned int s_max;
+  extern __shared__ unsigned int s_c[];  // staged counts, then exclusive offsets
+  const bool staged = n_tiles <= TSCAN_STAGED;
+  const int tid = threadIdx.x;
+  if (tid == 0) s_max = 0;
+  if (staged) {  // coalesced in, counts reset (they are the emission cursors)
+    for (int t = tid; t < n_tiles; t += TSCAN_THREADS) {
+      s_c[t] = tile_cnt[t];
+      tile_cnt[t] = 0u;
+    }
+    __syncthreads();
+  }
   const int per = (n_tiles + TSCAN_THREADS - 1) / TSCAN_THREADS;
-  const int lo = min(n_tiles, (int)threadIdx.x * per), hi = min(n_tiles, lo + per);
+  const int lo = min(n_tiles, tid * per), hi = min(n_tiles, lo + per);
   unsigned long long sum = 0;
   unsigned int mx = 0;
   for (int t = lo; t < hi; ++t) {
-    const unsigned int c = tile_cnt[t];
+    const unsigned int c = staged ? s_c[t] : tile_cnt[t];
     sum += c;
     mx = max(mx, c);
   }
-  if (threadIdx.x == 0) s_max = 0;
   unsigned long long off, all;
   Scan(tmp).ExclusiveSum(sum, off, all);
-  __syncthreads();
   atomicMax(&s_max, mx);
-  for (int t = lo; t < hi; ++t) {
-    const unsigned int c = tile_cnt[t];
+  if (staged) {
+    for (int t = lo; t < hi; ++t) {
+      const unsigned int c = s_c[t];
+      s_c[t] = (unsigned int)min(off, cap);
+      off += c;
+    }
+    __syncthreads();
     // (a device-sized buffer too small: lists clamped to it, the pass is
     // flagged and redone — no list may reach past the buffer meanwhile)
-    ranges[t] = make_int2((int)min(off, cap), (int)min(off + c, cap));
-    off += c;
-    tile_cnt[t] = 0u;
+    const unsigned int capped = (unsigned int)min(all, cap);
+    for (int t = tid; t < n_tiles; t += TSCAN_THREADS)
+      ranges[t] = make_int2((int)s_c[t], (int)(t + 1 < n_tiles ? s_c[t + 1] : capped));
+  } else {
+    __syncthreads();
+    for (int t = lo; t < hi; ++t) {
+      const unsigned int c = tile_cnt[t];
+      ranges[t] = make_int2((int)min(off, cap), (int)min(off + c, cap));
+      off += c;
+      tile_cnt[t] = 0u;
+    }
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     *total = all;
     *maxseg = s_max;
     if (overflow && (all > cap || (int)s_max > seg_max)) atomicAdd(overflow, 1ull);
@@ -1179,15 +1209,48 @@ __global__ void __launch_bounds__(256)
 // memory — rank counting for short lists, a bitonic network up to SEG_MAX;
 // zeroes the tile's cursor for the next phase
 constexpr int SEG_THREADS = 256;
+constexpr int SEG_WARP_MAX = 256;  // lists up to this long: one warp each
+// one warp per tile: lists of up to SEG_WARP_MAX by rank counting (a list
+// of <= 32 entirely in registers); zeroes every tile's cursor
+__global__ void __launch_bounds__(256)
+    k_seg_sort_warp(uint32_t* __restrict__ vals, const int2* __restrict__ ranges,
+                    unsigned int* __restrict__ cursor, int n_tiles, unsigned long long cap) {
+  __shared__ uint32_t s_k[8][SEG_WARP_MAX];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = blockIdx.x * 8 + w;
+  if (t >= n_tiles) return;
+  const int2 rg = ranges[t];
+  if (lane == 0) cursor[t] = 0u;
+  const int n = rg.y - rg.x;
+  if (n <= 1 || n > SEG_WARP_MAX || (unsigned long long)rg.y > cap) return;
+  uint32_t* v = vals + rg.x;
+  if (n <= 32) {
+    const uint32_t k = lane < n ? v[lane] : 0xffffffffu;
+    int pos = 0;
+    for (int j = 0; j < n; ++j) pos += __shfl_sync(0xffffffffu, k, j) < k ? 1 : 0;
+    if (lane < n) v[pos] = k;
+    return;
+  }
+  uint32_t* sk = s_k[w];
+  for (int i = lane; i < n; i += 32) sk[i] = v[i];
+  __syncwarp();
+  for (int i = lane; i < n; i += 32) {
+    const uint32_t k = sk[i];
+    int pos = 0;
+#pragma unroll 4
+    for (int j = 0; j < n; ++j) pos += sk[j] < k ? 1 : 0;
+    v[pos] = k;
+  }
+}
+// one block per tile for the longer lists (bitonic up to SEG_MAX)
 __global__ void __launch_bounds__(SEG_THREADS)
     k_seg_sort(uint32_t* __restrict__ vals, const int2* __restrict__ ranges,
                unsigned int* __restrict__ cursor, unsigned long long cap) {
   __shared__ uint32_t s_k[SEG_MAX];
   const int t = blockIdx.x, tid = threadIdx.x;
   const int2 rg = ranges[t];
-  if (tid == 0) cursor[t] = 0u;
   const int n = rg.y - rg.x;
-  if (n <= 1 || n > SEG_MAX || (unsigned long long)rg.y > cap) return;
+  if (n <= SEG_WARP_MAX || n > SEG_MAX || (unsigned long long)rg.y > cap) return;
   uint32_t* v = vals + rg.x;
   if (n <= SEG_THREADS) {
     const uint32_t k = tid < n ? v[tid] : 0u;
@@ -1236,8 +1299,15 @@ void launch_count_tiles(const int4* rects, const uint32_t* order, int64_t r0, in
 void launch_tile_scan(unsigned int* tile_cnt, int n_tiles, int2* ranges, unsigned long long* total,
                       unsigned long long* maxseg, unsigned long long cap,
                       unsigned long long* overflow, cudaStream_t s) {
-  k_tile_scan<<<1, TSCAN_THREADS, 0, s>>>(tile_cnt, n_tiles, ranges, total, maxseg, cap, overflow,
-                                          SEG_MAX);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_tile_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         TSCAN_STAGED * (int)sizeof(unsigned int));
+    attr = true;
+  }
+  const size_t dyn = n_tiles <= TSCAN_STAGED ? (size_t)n_tiles * sizeof(unsigned int) : 0;
+  k_tile_scan<<<1, TSCAN_THREADS, dyn, s>>>(tile_cnt, n_tiles, ranges, total, maxseg, cap,
+                                            overflow, SEG_MAX);
 }
 void launch_emit_tiles(const int4* rects, const uint32_t* order, int64_t r0, int64_t r1,
                        int tiles_x, const uint8_t* active, const int2* ranges,
@@ -1252,9 +1322,12 @@ void launch_emit_tiles(const int4* rects, const uint32_t* order, int64_t r0, int
         rects, order, r0, r1, tiles_x, active, ranges, cursor, vals, nd, cap, tq, cam);
 }
 void launch_seg_sort(uint32_t* vals, const int2* ranges, unsigned int* cursor, int n_tiles,
-                     unsigned long long cap, cudaStream_t s) {
+                     unsigned long long cap, cudaStream_t s, long long max_seg) {
   if (n_tiles <= 0) return;
-  k_seg_sort<<<n_tiles, SEG_THREADS, 0, s>>>(vals, ranges, cursor, cap);
+  k_seg_sort_warp<<<(n_tiles + 7) / 8, 256, 0, s>>>(vals, ranges, cursor, n_tiles, cap);
+  // (max_seg < 0: unknown on the host)
+  if (max_seg < 0 || max_seg > SEG_WARP_MAX)
+    k_seg_sort<<<n_tiles, SEG_THREADS, 0, s>>>(vals, ranges, cursor, cap);
 }
 
 // device-sized binning: total pair count of the scan, the capacity check,
