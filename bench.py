@@ -296,7 +296,9 @@ def main():
             "dtype": "f32",
             "data": "synthetic",
             "config": {
-                "workload": (f"C3: {a.gaussians} Gaussians (canonical synthetic scene, seed 5), "
+                "workload": (("C3: " if (a.gaussians, W, H) == (1_000_000, 1920, 1080) else
+                              "C5-like: " if a.gaussians >= 5_000_000 else "custom: ")
+                             + f"{a.gaussians} Gaussians (canonical synthetic scene, seed 5), "
                              f"{W}x{H}, {model.describe()}, "
                              + ("chunk_size=1 (global depth order), " if a.chunk_size == 1 else
                                 "chunk_size=None (exact per-pixel order), " if a.chunk_size is None

@@ -1244,13 +1244,14 @@ __global__ void __launch_bounds__(256)
 }
 // one block per tile for the longer lists (bitonic up to SEG_MAX)
 __global__ void __launch_bounds__(SEG_THREADS)
-    k_seg_sort(uint32_t* __restrict__ vals, const int2* __restrict__ ranges,
-               unsigned int* __restrict__ cursor, unsigned long long cap) {
+    k_seg_sort(uint32_t* __restrict__ vals, const int2* __restrict__ ranges, int n_tiles,
+               unsigned long long cap) {
   __shared__ uint32_t s_k[SEG_MAX];
-  const int t = blockIdx.x, tid = threadIdx.x;
+  const int tid = threadIdx.x;
+  for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
   const int2 rg = ranges[t];
   const int n = rg.y - rg.x;
-  if (n <= SEG_WARP_MAX || n > SEG_MAX || (unsigned long long)rg.y > cap) return;
+  if (n <= SEG_WARP_MAX || n > SEG_MAX || (unsigned long long)rg.y > cap) continue;
   uint32_t* v = vals + rg.x;
   if (n <= SEG_THREADS) {
     const uint32_t k = tid < n ? v[tid] : 0u;
@@ -1282,6 +1283,8 @@ __global__ void __launch_bounds__(SEG_THREADS)
     }
   }
   for (int i = tid; i < n; i += SEG_THREADS) v[i] = s_k[i];
+  __syncthreads();  // (s_k is reused by the block's next tile)
+  }
 }
 
 void launch_count_tiles(const int4* rects, const uint32_t* order, int64_t r0, int64_t r1,
@@ -1326,8 +1329,12 @@ void launch_seg_sort(uint32_t* vals, const int2* ranges, unsigned int* cursor, i
   if (n_tiles <= 0) return;
   k_seg_sort_warp<<<(n_tiles + 7) / 8, 256, 0, s>>>(vals, ranges, cursor, n_tiles, cap);
   // (max_seg < 0: unknown on the host)
-  if (max_seg < 0 || max_seg > SEG_WARP_MAX)
-    k_seg_sort<<<n_tiles, SEG_THREADS, 0, s>>>(vals, ranges, cursor, cap);
+  if (max_seg < 0 || max_seg > SEG_WARP_MAX) {  // a persistent grid: most tiles are short
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    k_seg_sort<<<std::min(n_tiles, sms * 4), SEG_THREADS, 0, s>>>(vals, ranges, n_tiles, cap);
+  }
 }
 
 // device-sized binning: total pair count of the scan, the capacity check,
