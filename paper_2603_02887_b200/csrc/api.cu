@@ -1509,7 +1509,9 @@ int backward_blend(nxs_view* v, const float* seed, cudaStream_t s) {
 // K5: moments -> gradients (null gradients: only clear the moments)
 int backward_chain(nxs_view* v, const nxs_scene* scene, float* g_centers, float* g_scales,
                    float* g_quats, float* g_opacities, float* g_sh, cudaStream_t s) {
-  launch_chain(scene->scales, scene->quats, v->C, v->P, v->idx_out.as<uint32_t>(),
+  // (the backward touches only processed ranks: [0, proj_end))
+  launch_chain(scene->scales, scene->quats, v->C,
+               v->proj_end > 0 ? std::min(v->proj_end, v->P) : v->P, v->idx_out.as<uint32_t>(),
                v->moments.as<double>(), v->touched.as<uint8_t>(), g_centers, g_scales, g_quats,
                g_opacities, g_sh, s);
   NXS_LAUNCHED("chain");

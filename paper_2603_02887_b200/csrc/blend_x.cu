@@ -25,15 +25,17 @@ namespace nxs {
 
 // pending entries per pixel: 16 for the chunked order (a chunk flush empties
 // the buffer; an overflow reruns with 32), 32 for the exact order
-constexpr int XBATCH = 64;   // list entries staged per batch
+// list entries staged per batch: 64 with the 16-entry buffer, 32 with the
+// 32-entry one (so that its alpha column still leaves two blocks per SM)
+__host__ __device__ constexpr int xbatch(int xb) { return xb <= 16 ? 64 : 32; }
 // records of the current and the previous batch stay staged (a ring of
-// 2*XBATCH): most commits are of recently tested entries
+// 2 batches): most commits are of recently tested entries
 // the 16-entry buffer also keeps each pending entry's alpha (no re-test at
 // commit); the 32-entry one re-tests so that two blocks still fit an SM
-constexpr bool keeps_alpha(int xb) { return xb <= 16; }
+__host__ __device__ constexpr bool keeps_alpha(int xb) { return xb <= 32; }
 constexpr size_t fwdx_smem(int xb) {
-  return sizeof(float4) * 2 * XBATCH * REC_F4 + sizeof(uint32_t) * 2 * XBATCH +
-         (sizeof(uint32_t) + sizeof(float) + sizeof(uint32_t)) * XBATCH +
+  return sizeof(float4) * 2 * xbatch(xb) * REC_F4 + sizeof(uint32_t) * 2 * xbatch(xb) +
+         (sizeof(uint32_t) + sizeof(float) + sizeof(uint32_t)) * xbatch(xb) +
          (sizeof(float) + sizeof(int) + (keeps_alpha(xb) ? sizeof(float) : 0)) * xb * TILE_PIX;
 }
 
@@ -123,15 +125,16 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
                   bool save, float* __restrict__ carry_t, int32_t* __restrict__ carry_r,
                   int32_t* __restrict__ carry_n, const float* __restrict__ end_bound,
                   unsigned long long* __restrict__ need_rank, Counters* __restrict__ cnt) {
+  constexpr int XBT = xbatch(XBUF);
   const int tile = blockIdx.x;
   if (active && !active[tile]) return;  // finished in an earlier depth phase
   extern __shared__ float4 smem_dyn[];
-  float4(*s_ring)[REC_F4] = reinterpret_cast<float4(*)[REC_F4]>(smem_dyn);  // [2*XBATCH]
-  uint32_t* s_ring_rank = reinterpret_cast<uint32_t*>(smem_dyn + 2 * XBATCH * REC_F4);
-  uint32_t* s_rank = s_ring_rank + 2 * XBATCH;
-  float* s_zlo = reinterpret_cast<float*>(s_rank + XBATCH);
-  uint32_t* s_chunk = reinterpret_cast<uint32_t*>(s_zlo + XBATCH);
-  float* bt = reinterpret_cast<float*>(s_chunk + XBATCH);    // [XBUF][TILE_PIX] pending t
+  float4(*s_ring)[REC_F4] = reinterpret_cast<float4(*)[REC_F4]>(smem_dyn);  // [2*XBT]
+  uint32_t* s_ring_rank = reinterpret_cast<uint32_t*>(smem_dyn + 2 * XBT * REC_F4);
+  uint32_t* s_rank = s_ring_rank + 2 * XBT;
+  float* s_zlo = reinterpret_cast<float*>(s_rank + XBT);
+  uint32_t* s_chunk = reinterpret_cast<uint32_t*>(s_zlo + XBT);
+  float* bt = reinterpret_cast<float*>(s_chunk + XBT);    // [XBUF][TILE_PIX] pending t
   int* bp = reinterpret_cast<int*>(bt + XBUF * TILE_PIX);     // [XBUF][TILE_PIX] list position
   float* ba = reinterpret_cast<float*>(bp + XBUF * TILE_PIX);  // [XBUF][TILE_PIX] alpha
 
@@ -185,8 +188,19 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
     // ranks as -1 - rank (their records are read from global memory)
     nb = carry_n[pix];
     for (int i = 0; i < nb; ++i) {
+      const int32_t rk = carry_r[(size_t)i * npix + pix];
       bt[i * TILE_PIX + tid] = carry_t[(size_t)i * npix + pix];
-      bp[i * TILE_PIX + tid] = -1 - carry_r[(size_t)i * npix + pix];
+      bp[i * TILE_PIX + tid] = -1 - rk;
+      if constexpr (keeps_alpha(XBUF)) {  // (the carry keeps t and rank only)
+        float4 r[REC_F4];
+        const float4* rec = records + (size_t)rk * REC_F4;
+#pragma unroll
+        for (int k = 0; k < REC_F4; ++k) r[k] = __ldg(rec + k);
+        TestOut t;
+        float tpk;
+        test_with_t(r, cam, px, py, pc, hnorm, cutoff, near_plane, t, tpk);  // valid when carried
+        ba[i * TILE_PIX + tid] = t.alpha;
+      }
     }
   }
   uint32_t cur_chunk = 0;  // chunk of the pending entries (chunked order)
@@ -211,8 +225,8 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
     constexpr int K0 = keeps_alpha(XBUF) ? 4 : 0, K1 = keeps_alpha(XBUF) ? 7 : REC_F4;
     uint32_t rank;
     if (pos >= ring_lo) {  // (carried entries have pos < 0 and take the global path)
-      const float4* rec = s_ring[pos % (2 * XBATCH)];
-      rank = s_ring_rank[pos % (2 * XBATCH)];
+      const float4* rec = s_ring[pos % (2 * XBT)];
+      rank = s_ring_rank[pos % (2 * XBT)];
 #pragma unroll
       for (int k = K0; k < K1; ++k) r[k] = rec[k];
     } else {
@@ -237,13 +251,13 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
   };
 
   const int2 rg = ranges[tile];
-  for (int base = rg.x; base < rg.y; base += XBATCH) {
-    const int n = min(XBATCH, rg.y - base);
+  for (int base = rg.x; base < rg.y; base += XBT) {
+    const int n = min(XBT, rg.y - base);
     __syncthreads();
     if (tid < n) {
       const uint32_t rk = pairs[base + tid];
       s_rank[tid] = rk;
-      s_ring_rank[(base + tid) % (2 * XBATCH)] = rk;
+      s_ring_rank[(base + tid) % (2 * XBT)] = rk;
       s_zlo[tid] = zlo_rank[rk];
       s_chunk[tid] = chunk > 0 ? rank_c[order[rk]] / (uint32_t)chunk : 0u;
     }
@@ -251,13 +265,13 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
     // stage this batch into the ring slot it maps to (positions are consecutive)
     for (int k = tid; k < n * REC_F4; k += TILE_PIX) {
       const int e = k >> 3, part = k & 7;
-      s_ring[(base + e) % (2 * XBATCH)][part] = records[(size_t)s_rank[e] * REC_F4 + part];
+      s_ring[(base + e) % (2 * XBT)][part] = records[(size_t)s_rank[e] * REC_F4 + part];
     }
-    ring_lo = max(rg.x, base - XBATCH);
+    ring_lo = max(rg.x, base - XBT);
     __syncthreads();
     if (!s.done) {
       for (int j = 0; j < n; ++j) {
-        const float4* s_rec_j = s_ring[(base + j) % (2 * XBATCH)];
+        const float4* s_rec_j = s_ring[(base + j) % (2 * XBT)];
         // every remaining entry has t >= bound: pending entries below it are
         // final; a new chunk makes every pending entry final
         const bool next_chunk = s_chunk[j] != cur_chunk;

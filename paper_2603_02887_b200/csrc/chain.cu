@@ -106,8 +106,10 @@ void launch_chain(const float* scales, const float* quats, int C, int64_t P, con
                   double* moments, uint8_t* touched, float* g_centers, float* g_scales,
                   float* g_quats, float* g_opac, float* g_sh, cudaStream_t s) {
   if (P == 0) return;
-  k_chain<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(scales, quats, C, P, order, moments, touched,
-                                                      g_centers, g_scales, g_quats, g_opac, g_sh);
+  // touched ranks lie below the processed ranks (P here): small blocks
+  // spread their fp64 work over every SM
+  k_chain<<<(unsigned)((P + 63) / 64), 64, 0, s>>>(scales, quats, C, P, order, moments, touched,
+                                                    g_centers, g_scales, g_quats, g_opac, g_sh);
 }
 
 }  // namespace nxs
