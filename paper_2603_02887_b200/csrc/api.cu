@@ -735,10 +735,14 @@ int forward_impl(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
     if (!(opts->flags & NXS_FLAG_FULL_BINNING) && opts->first_phase_ranks <= 0) {
       // this view's previous call reported the last rank its finished tiles
       // needed (host_small[30], copied behind that forward);
-      // a first phase covering it (plus headroom) avoids a second phase.
+      // a first phase covering it (plus headroom) avoids a second phase, and
+      // one no larger spares sorting, projecting and binning ranks no tile reads.
       // The hint only moves phase boundaries, never the result.
       const int64_t need = (int64_t)v->host_small[30];
-      if (need > 0 && need < P && need + 1 > r1) r1 = need + 1 + need / 8 + 4096;
+      if (need > 0 && need < P) {
+        const int64_t target = need + 1 + need / 16 + 1024;
+        r1 = need < r1 ? std::min(r1, target) : target;
+      }
       // device-sized phase-0 estimates that fell short: size exactly again
       if (need > 0 && v->est_n0 > 0 && need >= v->est_n0) v->est_n0 = 0;
     }
@@ -1071,7 +1075,7 @@ retry_sort:
       // cursors, per-tile sort by rank
       launch_count_tiles(v->rects.as<int4>(), v->idx_out.as<uint32_t>(), 0, cap0, cam.tiles_x,
                          v->active.as<uint8_t>(), nullptr, v->tile_cnt.as<uint32_t>(),
-                         exact ? nullptr : v->tq.as<double>(), cam, s, n_sel);
+                         v->tq.as<double>(), cam, s, n_sel);
       NXS_LAUNCHED("count_tiles");
       NXS_CUDA(ensure_n<int2>(v->ranges_ph[0], n_tiles));
       NXS_CUDA(ensure_n<int32_t>(v->cum_ph[1], n_tiles));
@@ -1083,7 +1087,7 @@ retry_sort:
       launch_emit_tiles(v->rects.as<int4>(), v->idx_out.as<uint32_t>(), 0, cap0, cam.tiles_x,
                         v->active.as<uint8_t>(), v->ranges_ph[0].as<int2>(),
                         v->tile_cnt.as<uint32_t>(), v->pv_ph[0].as<uint32_t>(),
-                        exact ? nullptr : v->tq.as<double>(), cam, s, n_sel,
+                        v->tq.as<double>(), cam, s, n_sel,
                         (unsigned long long)capp);
       NXS_LAUNCHED("emit_tiles");
       mark(v, 4, s);
@@ -1231,7 +1235,7 @@ retry_sort:
         // per-tile counts and one scan over the tiles: ranges, total, longest list
         launch_count_tiles(v->rects.as<int4>(), v->idx_out.as<uint32_t>(), r0, r1, cam.tiles_x,
                            v->active.as<uint8_t>(), ph > 0 ? n_active : nullptr,
-                           v->tile_cnt.as<uint32_t>(), exact ? nullptr : v->tq.as<double>(), cam,
+                           v->tile_cnt.as<uint32_t>(), v->tq.as<double>(), cam,
                            s);
         NXS_LAUNCHED("count_tiles");
         launch_tile_scan(v->tile_cnt.as<uint32_t>(), n_tiles, v->ranges_ph[ph].as<int2>(),
@@ -1279,7 +1283,7 @@ retry_sort:
         launch_emit_tiles(v->rects.as<int4>(), v->idx_out.as<uint32_t>(), r0, r1, cam.tiles_x,
                           v->active.as<uint8_t>(), v->ranges_ph[ph].as<int2>(),
                           v->tile_cnt.as<uint32_t>(), v->pv_ph[ph].as<uint32_t>(),
-                          exact ? nullptr : v->tq.as<double>(), cam, s, nullptr, n_pairs);
+                          v->tq.as<double>(), cam, s, nullptr, n_pairs);
         NXS_LAUNCHED("emit_tiles");
         if (ph == 0) mark(v, 4, s);
         launch_seg_sort(v->pv_ph[ph].as<uint32_t>(), v->ranges_ph[ph].as<int2>(),
@@ -1292,7 +1296,7 @@ retry_sort:
         NXS_CUDA(cudaMemsetAsync(v->tile_cnt.p, 0, (size_t)n_tiles * 4, s));
         launch_count_active(v->rects.as<int4>(), v->idx_out.as<uint32_t>(), r0, r1, cam.tiles_x,
                             v->active.as<uint8_t>(), nullptr, v->ntiles.as<unsigned long long>(),
-                            exact ? nullptr : v->tq.as<double>(), cam, s);
+                            v->tq.as<double>(), cam, s);
         NXS_LAUNCHED("count_active");
         size_t tbo = v->temp.cap;
         NXS_CUDA(cub::DeviceScan::ExclusiveSum(v->temp.p, tbo, v->ntiles.as<unsigned long long>(),
@@ -1310,7 +1314,7 @@ retry_sort:
         launch_emit_pairs(v->rects.as<int4>(), v->idx_out.as<uint32_t>(),
                           v->offsets.as<unsigned long long>(), r0, r1, cam.tiles_x,
                           v->active.as<uint8_t>(), v->pk_in.as<uint32_t>(), v->pv_in.as<uint32_t>(),
-                          exact ? nullptr : v->tq.as<double>(), cam, s);
+                          v->tq.as<double>(), cam, s);
         NXS_LAUNCHED("emit_pairs");
         if (ph == 0) mark(v, 4, s);
         size_t tb = v->temp.cap;
