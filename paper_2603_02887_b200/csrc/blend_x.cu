@@ -413,7 +413,11 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
 // K4x
 // ---------------------------------------------------------------------------
 constexpr int XRED_STRIDE = 36;
-constexpr size_t BWDX_SMEM = sizeof(float) * NMOM * XRED_STRIDE * (TILE_PIX / 2 / 32);
+// per warp: the transpose scratch, then two record slots (record + B frame,
+// 11 float4) — the next step's record streams in while this one is replayed
+constexpr int XREC_F4 = REC_F4 + 3;
+constexpr size_t BWDX_WARP_FLOATS = NMOM * XRED_STRIDE + 2 * XREC_F4 * 4;
+constexpr size_t BWDX_SMEM = sizeof(float) * BWDX_WARP_FLOATS * (TILE_PIX / 2 / 32);
 
 // Two pixels per thread (rows r and r + 8, a 128-thread block per tile, as
 // K4): each warp step serves the largest pending rank over its 64 pixels,
@@ -445,35 +449,66 @@ __global__ void __launch_bounds__(BWDX_THREADS)
     myseq[q] = seq + (inside ? (size_t)py * cam.W + px : 0);  // [slot][pixel]
     ptr[q] = st[q].last;  // commit index, back to front
   }
-  float* red = smem_red + (tid >> 5) * NMOM * XRED_STRIDE;
+  float* red = smem_red + (tid >> 5) * BWDX_WARP_FLOATS;
+  float4* wrec = reinterpret_cast<float4*>(red + NMOM * XRED_STRIDE);  // [2][XREC_F4]
   const float gam = (FAM == FAM_EXP) ? 1.0f : m.c;
   const float inv_f = (float)(1.0 / cam.f);
   const float Y0 = (float)SH_C0;
   unsigned long long ntest = 0, nent = 0;
-  int cur[2];
+  // each pixel's next commit (cur) and the one after it (nxt, prefetched a
+  // step ahead so its load latency hides behind a whole step)
+  int cur[2], nxt[2];
 #pragma unroll
-  for (int q = 0; q < 2; ++q) cur[q] = ptr[q] >= 0 ? myseq[q][(size_t)ptr[q] * npix] : -1;
+  for (int q = 0; q < 2; ++q) {
+    cur[q] = ptr[q] >= 0 ? myseq[q][(size_t)ptr[q] * npix] : -1;
+    nxt[q] = ptr[q] >= 1 ? myseq[q][(size_t)(ptr[q] - 1) * npix] : -1;
+  }
+  // lanes 0..10 copy one float4 each of a rank's record + B frame
+  auto fetch = [&](int rank, int b) {
+    if (lane < XREC_F4) {
+      const float4* src = lane < REC_F4 ? records + (size_t)rank * REC_F4 + lane
+                                        : bframe + (size_t)rank * 3 + (lane - REC_F4);
+      cp_async16(&wrec[b * XREC_F4 + lane], src);
+    }
+    cp_async_commit();
+  };
+  int wcur = __reduce_max_sync(0xffffffffu, max(cur[0], cur[1]));
+  int b = 0;
+  if (wcur >= 0) fetch(wcur, 0);
 
-  while (true) {
-    const int wcur = __reduce_max_sync(0xffffffffu, max(cur[0], cur[1]));
-    if (wcur < 0) break;
+  while (wcur >= 0) {
     if (COUNT && lane == 0) ++nent;
     const uint32_t rank = (uint32_t)wcur;  // warp-uniform
-    float4 rec[REC_F4], bf[3];
+    // this step's pixels advance; the next step's rank is known at once
+    bool mine[2];
+    int idx[2];
 #pragma unroll
-    for (int k = 0; k < REC_F4; ++k) rec[k] = __ldg(records + (size_t)rank * REC_F4 + k);
-#pragma unroll
-    for (int k = 0; k < 3; ++k) bf[k] = __ldg(bframe + (size_t)rank * 3 + k);
+    for (int q = 0; q < 2; ++q) {
+      mine[q] = cur[q] == wcur;
+      idx[q] = ptr[q];
+      if (mine[q]) {
+        --ptr[q];
+        cur[q] = nxt[q];
+        nxt[q] = ptr[q] >= 1 ? myseq[q][(size_t)(ptr[q] - 1) * npix] : -1;
+      }
+    }
+    const int wnext = __reduce_max_sync(0xffffffffu, max(cur[0], cur[1]));
+    if (wnext >= 0) {
+      fetch(wnext, b ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncwarp();
+    const float4* rec = wrec + b * XREC_F4;
+    const float4* bf = rec + REC_F4;
     float dm2[2] = {0.f, 0.f}, ux[2] = {0.f, 0.f}, uy[2] = {0.f, 0.f}, uz[2] = {0.f, 0.f};
     float dak[2] = {0.f, 0.f}, e0[2] = {0.f, 0.f}, e1[2] = {0.f, 0.f}, e2[2] = {0.f, 0.f};
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
-      if (cur[q] == wcur) {
-        bwd_pixel<FAM>(st[q], rec, bf, ptr[q], cam, m, cutoff, near_plane, inv_f, gam, dm2[q],
+      if (mine[q])
+        bwd_pixel<FAM>(st[q], rec, bf, idx[q], cam, m, cutoff, near_plane, inv_f, gam, dm2[q],
                        ux[q], uy[q], uz[q], dak[q], e0[q], e1[q], e2[q], ntest, COUNT);
-        --ptr[q];
-        cur[q] = ptr[q] >= 0 ? myseq[q][(size_t)ptr[q] * npix] : -1;
-      }
     }
     const PixelConst& pa = st[0].pc;
     const PixelConst& pb = st[1].pc;
@@ -517,6 +552,8 @@ __global__ void __launch_bounds__(BWDX_THREADS)
       }
     }
     __syncwarp();
+    wcur = wnext;
+    b ^= 1;
   }
 
   if (COUNT) {
