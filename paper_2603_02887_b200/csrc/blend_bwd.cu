@@ -85,6 +85,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 4)
   if (mylast >= 0) atomicMax(&s_maxlast, mylast);
   __syncthreads();
   const int vmax = s_maxlast + 1;  // virtual per-tile list positions [0, vmax) are replayed
+  // this warp's last live entry: the entries behind it skip the warp
+  const int wlast = __reduce_max_sync(0xffffffffu, mylast);
 
   // phases back to front, each phase's segment back to front, in batches of
   // BWD_BATCH virtual positions [base, hi); batch (ph, hi) -> the next one
@@ -152,7 +154,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 4)
     const uint32_t* s_rank = s_rank2[buf];
     if (COUNT) nent += n;
 
-      for (int j = n - 1; j >= 0; --j) {
+      for (int j = min(n - 1, wlast - base); j >= 0; --j) {
         const int idx = base + j;
         // both pixels' contributions as a few scalars each; zero when a
         // pixel does not contribute, so the moments need no separate zeroing

@@ -13,6 +13,7 @@
 //                                    render.py:116-121, primitives.py:45-64
 // The per-pixel test those records feed is in blend_fwd.cu.
 #include <algorithm>
+#include <cstdlib>
 
 #include <cub/block/block_radix_sort.cuh>
 #include <cub/block/block_scan.cuh>
@@ -152,9 +153,10 @@ __global__ void k_depth(const float* __restrict__ centers, const float* __restri
                         double* __restrict__ depth, unsigned long long* __restrict__ key64,
                         uint32_t* __restrict__ idx, unsigned long long* __restrict__ kminmax) {
   __shared__ unsigned long long s_min[8], s_max[8];
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long kmin = ~0ull, kmax = 0ull;
-  if (i < P) {
+  // grid-stride: few blocks, so few atomics on the two min/max words
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P;
+       i += (int64_t)gridDim.x * blockDim.x) {
     double b0 = (double)centers[3 * i + 0] - cam.o[0];
     double b1 = (double)centers[3 * i + 1] - cam.o[1];
     double b2 = (double)centers[3 * i + 2] - cam.o[2];
@@ -168,8 +170,8 @@ __global__ void k_depth(const float* __restrict__ centers, const float* __restri
       idx[i] = (uint32_t)i;
     }
     if (d == d) {
-      kmin = k;
-      kmax = k;
+      kmin = min(kmin, k);
+      kmax = max(kmax, k);
     }
   }
   for (int o = 16; o > 0; o >>= 1) {
@@ -1369,8 +1371,12 @@ void launch_depth(const float* centers, const float* scales, const float* quats,
                   double* depth, unsigned long long* key64, uint32_t* idx,
                   unsigned long long* kminmax, cudaStream_t s) {
   if (P == 0) return;
-  k_depth<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(centers, scales, quats, opacities, P, cam,
-                                                      cutoff, zmode, depth, key64, idx, kminmax);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned grid = (unsigned)std::min<int64_t>((P + 255) / 256, (int64_t)sms * 8);
+  k_depth<<<grid, 256, 0, s>>>(centers, scales, quats, opacities, P, cam, cutoff, zmode, depth,
+                               key64, idx, kminmax);
 }
 void launch_key32(const double* depth, int64_t P, const unsigned long long* kminmax,
                   uint32_t* key, cudaStream_t s) {
