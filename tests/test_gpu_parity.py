@@ -654,3 +654,47 @@ def test_device_sized_first_phase_matches_fresh_views():
                 np.testing.assert_allclose(g[k].cpu().numpy(), r_g[k].cpu().numpy(), rtol=1e-5,
                                            atol=1e-7 * float(r_g[k].abs().max()), err_msg=k)
             # (n_pairs may differ: the view's first phase follows its history)
+
+
+def test_first_phase_follows_the_views_history():
+    """A view whose camera needs more depth ranks than the default first
+    phase (P/32) sizes its next first phase from the last rank its finished
+    tiles needed: after a warm-up call it renders in one phase, with the same
+    images and gradients as a fresh view (which needs two)."""
+    import torch
+    from paper_2603_02887_b200 import _native, forward_backward_device
+    sc = O.round_scene_f32(O.canonical_scene(60_000, seed=5))
+    dev = _dev(sc)
+    cam = O.canonical_camera(320, 240, 3, 8)  # a view of the bench's 8-view set
+    seed = torch.as_tensor(O.canonical_seed(320, 240, 3), dtype=torch.float32).cuda()
+    model = MODELS["softplus_20"]
+    fresh = _native.View().set_timing(True)
+    r_out, r_g = forward_backward_device(fresh, dev, cam, model, np.zeros(3), seed)
+    fresh_phases = fresh.timings()["n_depth_phases"]
+    view = _native.View().set_timing(True)
+    for _ in range(4):
+        out, g = forward_backward_device(view, dev, cam, model, np.zeros(3), seed)
+        torch.cuda.synchronize()
+    assert fresh_phases >= 2
+    assert view.timings()["n_depth_phases"] == 1
+    for a, b in zip(r_out, out):
+        assert torch.equal(a, b)
+    for k in GRAD_FIELDS:
+        np.testing.assert_allclose(g[k].cpu().numpy(), r_g[k].cpu().numpy(), rtol=1e-5,
+                                   atol=1e-7 * float(r_g[k].abs().max()), err_msg=k)
+
+
+def test_phase_timing_is_opt_in():
+    from paper_2603_02887_b200 import _native, forward_device
+    from paper_2603_02887_b200._native import NxsError
+    sc = O.round_scene_f32(O.canonical_scene(2_000, seed=1))
+    dev = _dev(sc)
+    cam = O.canonical_camera(64, 48)
+    view = _native.View()
+    forward_device(view, dev, cam, MODELS["linear"], np.zeros(3))
+    with pytest.raises(NxsError):
+        view.timings()
+    view.set_timing(True)
+    forward_device(view, dev, cam, MODELS["linear"], np.zeros(3))
+    t = view.timings()
+    assert t["forward_total"] > 0 and t["n_depth_phases"] >= 1
