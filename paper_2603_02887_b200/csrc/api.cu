@@ -58,7 +58,6 @@ void launch_key_fixup(const uint32_t*, uint32_t*, const double*, int64_t, unsign
 void launch_rank_of(const uint32_t*, int64_t, uint32_t*, cudaStream_t);
 void launch_rank_of_range(const uint32_t*, int64_t, int64_t, uint32_t*, cudaStream_t,
                           const int* nd = nullptr);
-void launch_key_hist(const uint32_t*, int64_t, unsigned int*, cudaStream_t);
 void launch_phase_select(const unsigned int*, const int64_t*, int, int64_t, long long*,
                          cudaStream_t, int max_bin0 = -1, unsigned long long* overflow = nullptr,
                          unsigned int* bin_pos = nullptr, int* n_sel = nullptr);
@@ -70,12 +69,6 @@ void launch_project_ranks(const float*, const float*, const float*, const float*
                           int, int64_t, int64_t, const uint32_t*, const CamDev&, double, double,
                           int4*, float4*, float4*, unsigned long long*, double*, cudaStream_t,
                           const int* nd = nullptr);
-void launch_gather_keys_pad(uint32_t*, const uint32_t*, const int*, int64_t, uint32_t*,
-                            cudaStream_t);
-void launch_pairs_total(const unsigned long long*, const unsigned long long*, int64_t,
-                        unsigned long long, unsigned long long*, unsigned long long*,
-                        cudaStream_t);
-void launch_pad_keys(uint32_t*, int64_t, const unsigned long long*, cudaStream_t);
 void launch_gather_keys(const uint32_t*, const uint32_t*, int64_t, uint32_t*, cudaStream_t);
 void launch_clear_rects(const uint32_t*, int64_t, int64_t, int4*, cudaStream_t);
 void launch_iota(uint32_t*, int64_t, cudaStream_t);
@@ -791,33 +784,21 @@ retry_sort:
   if (async0) {
     // every buffer the device-sized phase 0 touches is sized up front: no
     // allocation may move a buffer once its pointer is in the captured graph
-    const int64_t cap0 = std::min<int64_t>(P, v->est_n0 + v->est_n0 / 8 + 2048);
     const int64_t capp = v->est_pairs + v->est_pairs / 8 + 8192;
-    const int tbits_pad = bits_for((uint32_t)n_tiles + 1);
-    size_t t_sort = 0, t_scan = 0, t_pairs = 0, t_sel = 0, t_full = 0;
+    // (the scratch the generic setup below sizes for a full sort / scan)
+    size_t t_scan = 0, t_sel = 0, t_full = 0;
     NXS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t_full, v->k32a.as<uint32_t>(),
                                              v->k32b.as<uint32_t>(), v->idx_in.as<uint32_t>(),
                                              v->idx_out.as<uint32_t>(), (int)P, 0, 32, s));
-    NXS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t_sort, v->k32c.as<uint32_t>(),
-                                             v->k32b.as<uint32_t>(), v->idx_in.as<uint32_t>(),
-                                             v->idx_out.as<uint32_t>(), (int)cap0, 0, 32, s));
     NXS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t_scan, v->ntiles.as<unsigned long long>(),
                                            v->offsets.as<unsigned long long>(), (int)P, s));
-    NXS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t_pairs, v->pk_in.as<uint32_t>(),
-                                             v->pk_out.as<uint32_t>(), v->pv_in.as<uint32_t>(),
-                                             v->pv_ph[0].as<uint32_t>(), (int)capp, 0, tbits_pad,
-                                             s));
     NXS_CUDA(cub::DeviceSelect::If(nullptr, t_sel, cub::CountingInputIterator<uint32_t>(0),
                                    v->idx_in.as<uint32_t>(), v->ph_sel.as<int>(), (int)P,
                                    BinRange{nullptr, 0, 0}, s));
-    NXS_CUDA(v->temp.ensure(std::max({t_full, t_sort, t_scan, t_pairs, t_sel})));
+    NXS_CUDA(v->temp.ensure(std::max({t_full, t_scan, t_sel})));
     NXS_CUDA(v->ph_hist.ensure(4096 * sizeof(unsigned int)));
     NXS_CUDA(v->ph_sel.ensure(96 * sizeof(long long)));
-    NXS_CUDA(ensure_n<uint32_t>(v->k32c, P));
     NXS_CUDA(ensure_n<uint32_t>(v->pv_ph[0], capp));
-    NXS_CUDA(ensure_n<uint32_t>(v->pk_in, capp));
-    NXS_CUDA(ensure_n<uint32_t>(v->pk_out, capp));
-    NXS_CUDA(ensure_n<uint32_t>(v->pv_in, capp));
     NXS_CUDA(ensure_n<int2>(v->ranges_ph[0], n_tiles));
     NXS_CUDA(ensure_n<int32_t>(v->cum_ph[0], n_tiles));
     NXS_CUDA(ensure_n<int32_t>(v->cum_ph[1], n_tiles));

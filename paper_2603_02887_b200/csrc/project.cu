@@ -215,7 +215,7 @@ __global__ void k_key32(const double* __restrict__ depth, int64_t P,
   key[i] = key32_of(depth[i], lo, 4294967294.0 / (hi - lo), spread);
 }
 // the same keys and, in one pass, their histogram over the top 12 bits
-// (k_key_hist's; hist is zeroed by k_call_init)
+// (the histogram of the lazy depth phases; hist is zeroed by k_call_init)
 constexpr int PH_BINS_ = 4096;
 __global__ void __launch_bounds__(1024)
     k_key32_hist(const double* __restrict__ depth, int64_t P,
@@ -299,18 +299,6 @@ __global__ void k_rank_of(const uint32_t* __restrict__ order, int64_t r0, int64_
 constexpr int PH_BINS = 4096;
 constexpr int BIN_STRIDE = 32;  // bin cursors, one per 128-byte line
 
-__global__ void k_key_hist(const uint32_t* __restrict__ key, int64_t P,
-                           unsigned int* __restrict__ hist) {
-  __shared__ unsigned int sh[PH_BINS];
-  for (int b = threadIdx.x; b < PH_BINS; b += blockDim.x) sh[b] = 0u;
-  __syncthreads();
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P;
-       i += (int64_t)gridDim.x * blockDim.x)
-    atomicAdd(&sh[key[i] >> 20], 1u);
-  __syncthreads();
-  for (int b = threadIdx.x; b < PH_BINS; b += blockDim.x)
-    if (sh[b]) atomicAdd(&hist[b], sh[b]);
-}
 
 // one block: inclusive scan of the histogram; for each target rank T_p the
 // first bin whose cumulative count reaches it.  out[2p] = last bin of phase
@@ -1078,7 +1066,7 @@ __global__ void __launch_bounds__(256)
                                         ((1u << KSUB) - 1u);
     if (hit) {
       const unsigned long long q = o + __popc(m & ((1u << sl) - 1u));
-      if (q < cap) {  // device-sized pair buffer too small: flagged by k_pairs_total
+      if (q < cap) {  // (the legacy path sizes the buffer exactly)
         keys[q] = (uint32_t)t;
         vals[q] = (uint32_t)r;
       }
@@ -1339,22 +1327,6 @@ void launch_seg_sort(uint32_t* vals, const int2* ranges, unsigned int* cursor, i
   }
 }
 
-// device-sized binning: total pair count of the scan, the capacity check,
-// and max-key padding of the pair buffer beyond it
-__global__ void k_pairs_total(const unsigned long long* __restrict__ offsets,
-                              const unsigned long long* __restrict__ counts, int64_t n,
-                              unsigned long long cap, unsigned long long* __restrict__ total,
-                              unsigned long long* __restrict__ overflow) {
-  const unsigned long long t = n > 0 ? offsets[n - 1] + counts[n - 1] : 0ull;
-  *total = t;
-  if (t > cap) atomicAdd(overflow, 1ull);
-}
-__global__ void k_pad_keys(uint32_t* __restrict__ keys, int64_t cap,
-                           const unsigned long long* __restrict__ total) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < cap && (unsigned long long)i >= *total) keys[i] = 0xffffffffu;
-}
-
 __global__ void k_tile_ranges(const uint32_t* __restrict__ keys, int64_t n,
                               int2* __restrict__ ranges) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1439,18 +1411,6 @@ __global__ void k_gather_keys(const uint32_t* __restrict__ idx, const uint32_t* 
                               int64_t n, uint32_t* __restrict__ out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = key[idx[i]];
-}
-__global__ void k_gather_keys_pad(uint32_t* __restrict__ idx, const uint32_t* __restrict__ key,
-                                  const int* __restrict__ nd, int64_t cap,
-                                  uint32_t* __restrict__ out) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= cap) return;
-  if (i < *nd) {
-    out[i] = key[idx[i]];
-  } else {  // padding: sorts after every real key (max key, max index)
-    out[i] = 0xffffffffu;
-    idx[i] = 0xffffffffu;
-  }
 }
 __global__ void k_clear_rects(const uint32_t* __restrict__ order, int64_t r0, int64_t r1,
                               int4* __restrict__ rects) {
@@ -1569,24 +1529,10 @@ void launch_project_ranks_z(const float* centers, const float* scales, const flo
       centers, scales, quats, opacities, sh, C, r0, r1, order, cam, cutoff, near_plane, o,
       nullptr);
 }
-void launch_gather_keys_pad(uint32_t* idx, const uint32_t* key, const int* nd, int64_t cap,
-                            uint32_t* out, cudaStream_t s) {
-  if (cap <= 0) return;
-  k_gather_keys_pad<<<(unsigned)((cap + 255) / 256), 256, 0, s>>>(idx, key, nd, cap, out);
-}
 void launch_clear_rects(const uint32_t* order, int64_t r0, int64_t r1, int4* rects,
                         cudaStream_t s) {
   if (r1 <= r0) return;
   k_clear_rects<<<(unsigned)((r1 - r0 + 255) / 256), 256, 0, s>>>(order, r0, r1, rects);
-}
-void launch_key_hist(const uint32_t* key, int64_t P, unsigned int* hist, cudaStream_t s) {
-  cudaMemsetAsync(hist, 0, PH_BINS * sizeof(unsigned int), s);
-  if (P == 0) return;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const unsigned grid = (unsigned)std::min<int64_t>((P + 1023) / 1024, (int64_t)sms * 2);
-  k_key_hist<<<grid, 1024, 0, s>>>(key, P, hist);
 }
 void launch_phase_select(const unsigned int* hist, const int64_t* targets, int n_targets,
                          int64_t P, long long* out, cudaStream_t s, int max_bin0,
@@ -1662,16 +1608,6 @@ void launch_emit_pairs(const int4* rects, const uint32_t* order, const unsigned 
   else
     k_emit_pairs<8><<<(unsigned)((r1 - r0 + 31) / 32), 256, 0, s>>>(
         rects, order, offsets, r0, r1, tiles_x, active, keys, vals, nd, cap, tq, cam);
-}
-void launch_pairs_total(const unsigned long long* offsets, const unsigned long long* counts,
-                        int64_t n, unsigned long long cap, unsigned long long* total,
-                        unsigned long long* overflow, cudaStream_t s) {
-  k_pairs_total<<<1, 1, 0, s>>>(offsets, counts, n, cap, total, overflow);
-}
-void launch_pad_keys(uint32_t* keys, int64_t cap, const unsigned long long* total,
-                     cudaStream_t s) {
-  if (cap <= 0) return;
-  k_pad_keys<<<(unsigned)((cap + 255) / 256), 256, 0, s>>>(keys, cap, total);
 }
 
 void launch_tile_ranges(const uint32_t* keys, int64_t n, int2* ranges, cudaStream_t s) {
