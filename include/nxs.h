@@ -129,6 +129,8 @@ typedef struct {
     int64_t n_tests_bwd;      /* pairs re-tested by the backward     [COUNT_EVENTS] */
     int64_t n_entries_bwd;    /* (tile, entry) pairs replayed        [COUNT_EVENTS] */
     int64_t n_overflow;       /* exact order: pending-buffer overflows (must be 0) */
+    int64_t n_launches;       /* kernels this view has launched so far (cumulative;
+                                 the ones replayed from its CUDA graph included) */
 } nxs_stats;
 
 typedef struct nxs_view nxs_view;

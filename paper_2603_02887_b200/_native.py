@@ -117,7 +117,7 @@ class AdamGroup(C.Structure):
 class Stats(C.Structure):
     _fields_ = [(n, C.c_int64) for n in (
         "n_gaussians", "n_visible", "n_pairs", "n_straddling", "n_tiles", "n_tests_fwd",
-        "n_composited", "n_tests_bwd", "n_entries_bwd", "n_overflow")]
+        "n_composited", "n_tests_bwd", "n_entries_bwd", "n_overflow", "n_launches")]
 
     def as_dict(self) -> dict:
         return {n: int(getattr(self, n)) for n, _ in self._fields_}

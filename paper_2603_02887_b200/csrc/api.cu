@@ -144,6 +144,7 @@ int fail(int code, const std::string& msg) {
 
 #define NXS_LAUNCHED(what)                                                             \
   do {                                                                                 \
+    ++v->stats.n_launches;                                                             \
     cudaError_t _e = cudaGetLastError();                                               \
     if (_e != cudaSuccess)                                                             \
       return fail(NXS_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(_e));    \
@@ -657,7 +658,11 @@ int forward_impl(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
 
   const int64_t npix = (int64_t)cam.W * cam.H;
   const int n_tiles = cam.tiles_x * cam.tiles_y;
-  v->stats = nxs_stats{};
+  {
+    const int64_t launched = v->stats.n_launches;  // (cumulative over calls)
+    v->stats = nxs_stats{};
+    v->stats.n_launches = launched;
+  }
   v->stats.n_gaussians = P;
   v->stats.n_tiles = n_tiles;
   const bool count = (opts->flags & NXS_FLAG_COUNT_EVENTS) != 0;
@@ -1075,6 +1080,7 @@ retry_sort:
       launch_seg_sort(v->pv_ph[0].as<uint32_t>(), v->ranges_ph[0].as<int2>(),
                       v->tile_cnt.as<uint32_t>(), n_tiles, (unsigned long long)capp, s);
       NXS_LAUNCHED("seg_sort");
+      ++v->stats.n_launches;  // (short and long lists: two kernels)
       mark(v, 5, s);
       mark(v, 6, s);
       if (v->ev_ok) rec_event(v, v->evp[0][3], s);
@@ -1270,6 +1276,7 @@ retry_sort:
         launch_seg_sort(v->pv_ph[ph].as<uint32_t>(), v->ranges_ph[ph].as<int2>(),
                         v->tile_cnt.as<uint32_t>(), n_tiles, n_pairs, s, (long long)max_seg);
         NXS_LAUNCHED("seg_sort");
+        if (max_seg > 256) ++v->stats.n_launches;  // (long lists: a second kernel)
         if (ph == 0) mark(v, 5, s);
       } else if (n_pairs > 0) {
         // a tile list longer than the per-tile sort takes: per-rank counts,
