@@ -93,9 +93,12 @@ void launch_tile_scan(unsigned int*, int, int2*, unsigned long long*, unsigned l
                       unsigned long long, unsigned long long*, cudaStream_t);
 void launch_emit_tiles(const int4*, const uint32_t*, int64_t, int64_t, int, const uint8_t*,
                        const int2*, unsigned int*, uint32_t*, const double*, const CamDev&,
-                       cudaStream_t, const int* nd, unsigned long long cap);
-void launch_seg_sort(uint32_t*, const int2*, unsigned int*, int, unsigned long long,
-                     cudaStream_t, long long max_seg = -1);
+                       cudaStream_t, const int* nd, unsigned long long cap,
+                       const unsigned int* base = nullptr, unsigned long long* overflow = nullptr);
+void launch_seg_sort(uint32_t*, int2*, unsigned int*, int, unsigned long long, cudaStream_t,
+                     long long max_seg = -1, const unsigned int* base = nullptr,
+                     unsigned long long* total = nullptr, unsigned long long* overflow = nullptr);
+void launch_make_bases(const int2*, int, unsigned int*, cudaStream_t);
 void launch_chunk_key(const float*, const float*, const float*, const float*, int64_t,
                       const CamDev&, double, const uint32_t*, int, double*, unsigned long long*,
                       uint32_t*, cudaStream_t);
@@ -206,6 +209,14 @@ struct nxs_view {
   // per tile: phase ranges and virtual offsets, activity
   Buf ranges_ph[MAX_PHASES], cum_ph[MAX_PHASES + 1], active, tile_cnt;
   Buf bin_pos;  // per depth-key bin: first rank, then the scatter cursor
+  // per-tile list capacities for the device-sized first phase (from the
+  // view's last exact phase 0): emission needs no count pass while they hold
+  Buf tile_base;
+  bool bases_valid = false;
+  int bases_ntiles = 0;
+  int64_t bases_bound = 0;  // >= base[n_tiles], the pair buffer it needs
+  bool async_bases = false;  // this call's device-sized pass uses them
+  int64_t bases_maxcap = 0;  // the largest per-tile capacity
   // per pixel: replay cache and the forward carry between phases
   Buf c_last, c_sat, c_tk, c_thi, c_tlo, c_P, c_ck, c_Pck, c_ek, c_th0;
   Buf r_rad, r_trem, r_count, r_sea, r_sa;
@@ -264,7 +275,7 @@ struct nxs_view {
   void for_each_buf(F f) {
     Buf* all[] = {&dkeys_in, &dkeys_out, &idx_in,  &idx_out, &records, &bframe, &rects,
                   &ntiles,   &offsets,   &moments, &touched, &pk_in,   &pk_out,  &pv_in,  &active,
-                  &tile_cnt, &bin_pos,
+                  &tile_cnt, &bin_pos, &tile_base,
                   &depth,    &k32a,      &k32b,    &k32c,    &rank_of, &rank_c, &zlo_rank, &seq, &ph_hist,
                   &ph_sel,   &tq,      &zlo64,  &xc_t, &xc_r, &xc_n,
                   &c_last,   &c_sat,     &c_tk,    &c_thi,   &c_tlo,   &c_P,    &c_ck,
@@ -789,7 +800,9 @@ retry_sort:
   if (async0) {
     // every buffer the device-sized phase 0 touches is sized up front: no
     // allocation may move a buffer once its pointer is in the captured graph
-    const int64_t capp = v->est_pairs + v->est_pairs / 8 + 8192;
+    v->async_bases = v->bases_valid && v->bases_ntiles == n_tiles && !getenv("NXS_NO_BASES");
+    const int64_t capp =
+        v->async_bases ? v->bases_bound : v->est_pairs + v->est_pairs / 8 + 8192;
     // (the scratch the generic setup below sizes for a full sort / scan)
     size_t t_scan = 0, t_sel = 0, t_full = 0;
     NXS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t_full, v->k32a.as<uint32_t>(),
@@ -907,7 +920,8 @@ retry_sort:
                             v->bin_pos.as<uint32_t>(), reinterpret_cast<int*>(dsel + 48));
         NXS_LAUNCHED("phase_select");
         v->async_cap0 = std::min<int64_t>(P, v->est_n0 + v->est_n0 / 8 + 2048);
-        v->async_capp = v->est_pairs + v->est_pairs / 8 + 8192;
+        v->async_capp =
+            v->async_bases ? v->bases_bound : v->est_pairs + v->est_pairs / 8 + 8192;
         R[0] = 0;
         R[1] = v->async_cap0;  // ranks phase 0 may occupy; later bounds come with the check
       }
@@ -1056,31 +1070,48 @@ retry_sort:
                            v->tq.as<double>(), s, n_sel);
       NXS_LAUNCHED("project_ranks");
       if (v->ev_ok) rec_event(v, v->evp[0][2], s);
-      // ---- tile-major binning: per-tile counts, one scan over the tiles
-      // (ranges, total vs capacity, longest list), emission at per-tile
-      // cursors, per-tile sort by rank
-      launch_count_tiles(v->rects.as<int4>(), v->idx_out.as<uint32_t>(), 0, cap0, cam.tiles_x,
-                         v->active.as<uint8_t>(), nullptr, v->tile_cnt.as<uint32_t>(),
-                         v->tq.as<double>(), cam, s, n_sel);
-      NXS_LAUNCHED("count_tiles");
       NXS_CUDA(ensure_n<int2>(v->ranges_ph[0], n_tiles));
       NXS_CUDA(ensure_n<int32_t>(v->cum_ph[1], n_tiles));
       NXS_CUDA(ensure_n<uint32_t>(v->pv_ph[0], capp));
-      mark(v, 3, s);
-      launch_tile_scan(v->tile_cnt.as<uint32_t>(), n_tiles, v->ranges_ph[0].as<int2>(),
-                       dsmall + 11, dsmall + 14, (unsigned long long)capp, dsmall + 10, s);
-      NXS_LAUNCHED("tile_scan");
-      launch_emit_tiles(v->rects.as<int4>(), v->idx_out.as<uint32_t>(), 0, cap0, cam.tiles_x,
-                        v->active.as<uint8_t>(), v->ranges_ph[0].as<int2>(),
-                        v->tile_cnt.as<uint32_t>(), v->pv_ph[0].as<uint32_t>(),
-                        v->tq.as<double>(), cam, s, n_sel,
-                        (unsigned long long)capp);
-      NXS_LAUNCHED("emit_tiles");
-      mark(v, 4, s);
-      launch_seg_sort(v->pv_ph[0].as<uint32_t>(), v->ranges_ph[0].as<int2>(),
-                      v->tile_cnt.as<uint32_t>(), n_tiles, (unsigned long long)capp, s);
-      NXS_LAUNCHED("seg_sort");
-      ++v->stats.n_launches;  // (short and long lists: two kernels)
+      if (v->async_bases) {
+        // ---- per-tile capacities of the view's last pass: emission at
+        // base + cursor (an exceeded capacity is flagged and the pass redone),
+        // the list sort writes the ranges and the pair total
+        mark(v, 3, s);
+        launch_emit_tiles(v->rects.as<int4>(), v->idx_out.as<uint32_t>(), 0, cap0, cam.tiles_x,
+                          v->active.as<uint8_t>(), nullptr, v->tile_cnt.as<uint32_t>(),
+                          v->pv_ph[0].as<uint32_t>(), v->tq.as<double>(), cam, s, n_sel,
+                          (unsigned long long)capp, v->tile_base.as<uint32_t>(), dsmall + 10);
+        NXS_LAUNCHED("emit_tiles");
+        mark(v, 4, s);
+        launch_seg_sort(v->pv_ph[0].as<uint32_t>(), v->ranges_ph[0].as<int2>(),
+                        v->tile_cnt.as<uint32_t>(), n_tiles, (unsigned long long)capp, s,
+                        v->bases_maxcap, v->tile_base.as<uint32_t>(), dsmall + 11, dsmall + 10);
+        NXS_LAUNCHED("seg_sort");
+        if (v->bases_maxcap > 256) ++v->stats.n_launches;  // (long lists: a second kernel)
+      } else {
+        // ---- tile-major binning: per-tile counts, one scan over the tiles
+        // (ranges, total vs capacity, longest list), emission at per-tile
+        // cursors, per-tile sort by rank
+        launch_count_tiles(v->rects.as<int4>(), v->idx_out.as<uint32_t>(), 0, cap0, cam.tiles_x,
+                           v->active.as<uint8_t>(), nullptr, v->tile_cnt.as<uint32_t>(),
+                           v->tq.as<double>(), cam, s, n_sel);
+        NXS_LAUNCHED("count_tiles");
+        mark(v, 3, s);
+        launch_tile_scan(v->tile_cnt.as<uint32_t>(), n_tiles, v->ranges_ph[0].as<int2>(),
+                         dsmall + 11, dsmall + 14, (unsigned long long)capp, dsmall + 10, s);
+        NXS_LAUNCHED("tile_scan");
+        launch_emit_tiles(v->rects.as<int4>(), v->idx_out.as<uint32_t>(), 0, cap0, cam.tiles_x,
+                          v->active.as<uint8_t>(), v->ranges_ph[0].as<int2>(),
+                          v->tile_cnt.as<uint32_t>(), v->pv_ph[0].as<uint32_t>(),
+                          v->tq.as<double>(), cam, s, n_sel, (unsigned long long)capp);
+        NXS_LAUNCHED("emit_tiles");
+        mark(v, 4, s);
+        launch_seg_sort(v->pv_ph[0].as<uint32_t>(), v->ranges_ph[0].as<int2>(),
+                        v->tile_cnt.as<uint32_t>(), n_tiles, (unsigned long long)capp, s);
+        NXS_LAUNCHED("seg_sort");
+        ++v->stats.n_launches;  // (short and long lists: two kernels)
+      }
       mark(v, 5, s);
       mark(v, 6, s);
       if (v->ev_ok) rec_event(v, v->evp[0][3], s);
@@ -1277,6 +1308,16 @@ retry_sort:
                         v->tile_cnt.as<uint32_t>(), n_tiles, n_pairs, s, (long long)max_seg);
         NXS_LAUNCHED("seg_sort");
         if (max_seg > 256) ++v->stats.n_launches;  // (long lists: a second kernel)
+        if (ph == 0 && v->lazy && !torder) {
+          // per-tile capacities for this view's next device-sized pass
+          NXS_CUDA(ensure_n<uint32_t>(v->tile_base, (int64_t)n_tiles + 1));
+          launch_make_bases(v->ranges_ph[0].as<int2>(), n_tiles, v->tile_base.as<uint32_t>(), s);
+          NXS_LAUNCHED("make_bases");
+          v->bases_valid = true;
+          v->bases_ntiles = n_tiles;
+          v->bases_bound = (int64_t)n_pairs + (int64_t)n_pairs / 8 + 8 * (int64_t)n_tiles + 1;
+          v->bases_maxcap = (int64_t)max_seg + (int64_t)max_seg / 8 + 8;
+        }
         if (ph == 0) mark(v, 5, s);
       } else if (n_pairs > 0) {
         // a tile list longer than the per-tile sort takes: per-rank counts,

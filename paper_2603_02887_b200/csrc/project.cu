@@ -1169,13 +1169,38 @@ __global__ void __launch_bounds__(TSCAN_THREADS)
   }
 }
 
+// per-tile list capacities for the view's next device-sized pass, from this
+// pass's phase-0 lists: cap_t = n_t + n_t/8 + 8, base = exclusive scan
+__global__ void __launch_bounds__(TSCAN_THREADS)
+    k_make_bases(const int2* __restrict__ ranges, int n_tiles, unsigned int* __restrict__ base) {
+  typedef cub::BlockScan<unsigned long long, TSCAN_THREADS> Scan;
+  __shared__ typename Scan::TempStorage tmp;
+  const int per = (n_tiles + TSCAN_THREADS - 1) / TSCAN_THREADS;
+  const int lo = min(n_tiles, (int)threadIdx.x * per), hi = min(n_tiles, lo + per);
+  auto cap_of = [&](int t) {
+    const int2 rg = ranges[t];
+    const unsigned int n = (unsigned int)(rg.y - rg.x);
+    return n + n / 8 + 8u;
+  };
+  unsigned long long sum = 0;
+  for (int t = lo; t < hi; ++t) sum += cap_of(t);
+  unsigned long long off, all;
+  Scan(tmp).ExclusiveSum(sum, off, all);
+  for (int t = lo; t < hi; ++t) {
+    base[t] = (unsigned int)off;
+    off += cap_of(t);
+  }
+  if (threadIdx.x == 0) base[n_tiles] = (unsigned int)all;
+}
+
 template <int KSUB>
 __global__ void __launch_bounds__(256)
     k_emit_tiles(const int4* __restrict__ rects, const uint32_t* __restrict__ order, int64_t r0,
                  int64_t r1, int tiles_x, const uint8_t* __restrict__ active,
                  const int2* __restrict__ ranges, unsigned int* __restrict__ cursor,
                  uint32_t* __restrict__ vals, const int* __restrict__ nd, unsigned long long cap,
-                 const double* __restrict__ tq, CamDev cam) {
+                 const double* __restrict__ tq, CamDev cam, const unsigned int* __restrict__ base,
+                 unsigned long long* __restrict__ overflow) {
   const int sl = threadIdx.x & (KSUB - 1);
   const int64_t r = r0 + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / KSUB;
   const int64_t rn = nd ? min(r1, r0 + (int64_t)*nd) : r1;
@@ -1189,8 +1214,14 @@ __global__ void __launch_bounds__(256)
     const int tx = rc.x + k % w, ty = rc.y + k / w;
     const int t = ty * tiles_x + tx;
     if (active[t] && tile_hit(tq, g, tx, ty, cam, inv_f)) {
-      const unsigned long long q = (unsigned long long)ranges[t].x + atomicAdd(&cursor[t], 1u);
-      if (q < cap) vals[q] = (uint32_t)r;  // (a device-sized buffer too small is flagged)
+      if (base) {  // per-tile capacities from the view's last call (no count pass)
+        const unsigned int q = atomicAdd(&cursor[t], 1u);
+        if (q < base[t + 1] - base[t]) vals[base[t] + q] = (uint32_t)r;
+        else atomicAdd(overflow, 1ull);  // (the pass is redone with exact counts)
+      } else {
+        const unsigned long long q = (unsigned long long)ranges[t].x + atomicAdd(&cursor[t], 1u);
+        if (q < cap) vals[q] = (uint32_t)r;  // (a device-sized buffer too small is flagged)
+      }
     }
   }
 }
@@ -1203,13 +1234,28 @@ constexpr int SEG_WARP_MAX = 256;  // lists up to this long: one warp each
 // one warp per tile: lists of up to SEG_WARP_MAX by rank counting (a list
 // of <= 32 entirely in registers); zeroes every tile's cursor
 __global__ void __launch_bounds__(256)
-    k_seg_sort_warp(uint32_t* __restrict__ vals, const int2* __restrict__ ranges,
-                    unsigned int* __restrict__ cursor, int n_tiles, unsigned long long cap) {
+    k_seg_sort_warp(uint32_t* __restrict__ vals, int2* __restrict__ ranges,
+                    unsigned int* __restrict__ cursor, int n_tiles, unsigned long long cap,
+                    const unsigned int* __restrict__ base, unsigned long long* __restrict__ total,
+                    unsigned long long* __restrict__ overflow) {
   __shared__ uint32_t s_k[8][SEG_WARP_MAX];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t = blockIdx.x * 8 + w;
   if (t >= n_tiles) return;
-  const int2 rg = ranges[t];
+  int2 rg;
+  if (base) {  // lists emitted at per-tile capacities: the range is [base, base + count)
+    const unsigned int b0 = base[t];
+    const int n0 = (int)min(cursor[t], base[t + 1] - b0);
+    rg = make_int2((int)b0, (int)b0 + n0);
+    __syncwarp();
+    if (lane == 0) {
+      ranges[t] = rg;
+      atomicAdd(total, (unsigned long long)n0);
+      if (n0 > SEG_MAX) atomicAdd(overflow, 1ull);
+    }
+  } else {
+    rg = ranges[t];
+  }
   if (lane == 0) cursor[t] = 0u;
   const int n = rg.y - rg.x;
   if (n <= 1 || n > SEG_WARP_MAX || (unsigned long long)rg.y > cap) return;
@@ -1305,19 +1351,28 @@ void launch_tile_scan(unsigned int* tile_cnt, int n_tiles, int2* ranges, unsigne
 void launch_emit_tiles(const int4* rects, const uint32_t* order, int64_t r0, int64_t r1,
                        int tiles_x, const uint8_t* active, const int2* ranges,
                        unsigned int* cursor, uint32_t* vals, const double* tq, const CamDev& cam,
-                       cudaStream_t s, const int* nd, unsigned long long cap) {
+                       cudaStream_t s, const int* nd, unsigned long long cap,
+                       const unsigned int* base, unsigned long long* overflow) {
   if (r1 <= r0) return;
   if (r1 - r0 <= 262144)
     k_emit_tiles<32><<<(unsigned)((r1 - r0 + 7) / 8), 256, 0, s>>>(
-        rects, order, r0, r1, tiles_x, active, ranges, cursor, vals, nd, cap, tq, cam);
+        rects, order, r0, r1, tiles_x, active, ranges, cursor, vals, nd, cap, tq, cam, base,
+        overflow);
   else
     k_emit_tiles<8><<<(unsigned)((r1 - r0 + 31) / 32), 256, 0, s>>>(
-        rects, order, r0, r1, tiles_x, active, ranges, cursor, vals, nd, cap, tq, cam);
+        rects, order, r0, r1, tiles_x, active, ranges, cursor, vals, nd, cap, tq, cam, base,
+        overflow);
 }
-void launch_seg_sort(uint32_t* vals, const int2* ranges, unsigned int* cursor, int n_tiles,
-                     unsigned long long cap, cudaStream_t s, long long max_seg) {
+void launch_make_bases(const int2* ranges, int n_tiles, unsigned int* base, cudaStream_t s) {
+  k_make_bases<<<1, TSCAN_THREADS, 0, s>>>(ranges, n_tiles, base);
+}
+void launch_seg_sort(uint32_t* vals, int2* ranges, unsigned int* cursor, int n_tiles,
+                     unsigned long long cap, cudaStream_t s, long long max_seg,
+                     const unsigned int* base, unsigned long long* total,
+                     unsigned long long* overflow) {
   if (n_tiles <= 0) return;
-  k_seg_sort_warp<<<(n_tiles + 7) / 8, 256, 0, s>>>(vals, ranges, cursor, n_tiles, cap);
+  k_seg_sort_warp<<<(n_tiles + 7) / 8, 256, 0, s>>>(vals, ranges, cursor, n_tiles, cap, base,
+                                                    total, overflow);
   // (max_seg < 0: unknown on the host)
   if (max_seg < 0 || max_seg > SEG_WARP_MAX) {  // a persistent grid: most tiles are short
     int dev = 0, sms = 148;
