@@ -161,11 +161,23 @@ __global__ void __launch_bounds__(BWD_THREADS, 4)
         float dm2[2] = {0.f, 0.f}, ux[2] = {0.f, 0.f}, uy[2] = {0.f, 0.f}, uz[2] = {0.f, 0.f};
         float dak[2] = {0.f, 0.f}, e0[2] = {0.f, 0.f}, e1[2] = {0.f, 0.f}, e2[2] = {0.f, 0.f};
         bool contrib = false;
+        if ((__float_as_int(s_rec[j][3].w) & (RF_GENERAL | RF_ANISO)) == 0) {  // block-uniform
+          PairOut po;
+          contrib = bwd_pair<FAM>(st[0], st[1], s_rec[j], s_bf[j], idx, m, cutoff, inv_f, gam, po,
+                                  ntest, COUNT);
+          if (contrib) {
+            dm2[0] = po.dm2.x, dm2[1] = po.dm2.y, ux[0] = po.ux.x, ux[1] = po.ux.y;
+            uy[0] = po.uy.x, uy[1] = po.uy.y, uz[0] = po.uz.x, uz[1] = po.uz.y;
+            dak[0] = po.dak.x, dak[1] = po.dak.y, e0[0] = po.e0.x, e0[1] = po.e0.y;
+            e1[0] = po.e1.x, e1[1] = po.e1.y, e2[0] = po.e2.x, e2[1] = po.e2.y;
+          }
+        } else {
 #pragma unroll
-        for (int q = 0; q < 2; ++q)
-          contrib |= bwd_pixel<FAM>(st[q], s_rec[j], s_bf[j], idx, cam, m, cutoff, near_plane,
-                                    inv_f, gam, dm2[q], ux[q], uy[q], uz[q], dak[q], e0[q], e1[q],
-                                    e2[q], ntest, COUNT);
+          for (int q = 0; q < 2; ++q)
+            contrib |= bwd_pixel<FAM>(st[q], s_rec[j], s_bf[j], idx, cam, m, cutoff, near_plane,
+                                      inv_f, gam, dm2[q], ux[q], uy[q], uz[q], dak[q], e0[q],
+                                      e1[q], e2[q], ntest, COUNT);
+        }
         if (__any_sync(0xffffffffu, contrib)) {
           // warp transpose-reduce through shared memory: lane r writes its
           // (two-pixel) moments down column r, lane k < 24 then sums row k

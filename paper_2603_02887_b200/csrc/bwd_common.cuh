@@ -123,6 +123,162 @@ __device__ __forceinline__ bool bwd_pixel(BwdPix& st, const float4* rec, const f
   return true;
 }
 
+// ---------------------------------------------------------------------------
+// Packed two-pixel step (Blackwell FFMA2/FADD2/FMUL2).  The global-order
+// backward gives each thread two pixels of the same column (rows r, r+8), so
+// every per-pixel fp32 operation of the common record kind (conic, not thin)
+// runs as one f32x2 instruction on the pair; record values enter as scalar
+// broadcast operands.  Each lane of an f32x2 op is the IEEE round-to-nearest
+// scalar op, so the ray-peak test and the emission stay bit-identical to the
+// forward's scalar code (blend_common.cuh); MUFU ops stay scalar.
+// ---------------------------------------------------------------------------
+struct F2 {
+  float x, y;
+};
+__device__ __forceinline__ F2 f2(float a) { return F2{a, a}; }
+#define NXS_F2OP3(name, op)                                                                  \
+  __device__ __forceinline__ F2 name(F2 a, F2 b) {                                          \
+    F2 d;                                                                                    \
+    asm("{.reg .b64 ra, rb, rd;\n mov.b64 ra, {%2,%3};\n mov.b64 rb, {%4,%5};\n " op        \
+        " rd, ra, rb;\n mov.b64 {%0,%1}, rd;}"                                              \
+        : "=f"(d.x), "=f"(d.y)                                                               \
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));                                           \
+    return d;                                                                                \
+  }
+NXS_F2OP3(add2, "add.rn.f32x2")
+NXS_F2OP3(sub2, "sub.rn.f32x2")
+NXS_F2OP3(mul2, "mul.rn.f32x2")
+#undef NXS_F2OP3
+__device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) {
+  F2 d;
+  asm("{.reg .b64 ra, rb, rc, rd;\n mov.b64 ra, {%2,%3};\n mov.b64 rb, {%4,%5};\n"
+      " mov.b64 rc, {%6,%7};\n fma.rn.f32x2 rd, ra, rb, rc;\n mov.b64 {%0,%1}, rd;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ F2 sel2(bool qa, bool qb, F2 v) {
+  return F2{qa ? v.x : 0.f, qb ? v.y : 0.f};
+}
+// packed df_add: (hi, lo) += a per lane, exactly (nxs_internal.cuh df_add)
+__device__ __forceinline__ void df_add2(F2& hi, F2& lo, F2 a) {
+  const F2 s = add2(hi, a);
+  const F2 bb = sub2(s, hi);
+  const F2 e = add2(sub2(hi, sub2(s, bb)), sub2(a, bb));
+  const F2 el = add2(e, lo);
+  const F2 s2 = add2(s, el);
+  lo = sub2(el, sub2(s2, s));
+  hi = s2;
+}
+
+// Outputs of one entry for the thread's two pixels (lane x: pixel a, y: b),
+// zero where a pixel does not replay the entry.
+struct PairOut {
+  F2 dm2, ux, uy, uz, dak, e0, e1, e2;
+};
+
+// Both pixels' contributions of a conic, non-thin record (rec[3].w flags
+// clear of RF_GENERAL | RF_ANISO); same results as two bwd_pixel calls.
+template <int FAM>
+__device__ __forceinline__ bool bwd_pair(BwdPix& A, BwdPix& B, const float4* rec, const float4* bf,
+                                         int idx, const ModelDev& m, float cutoff, float inv_f,
+                                         float gam, PairOut& o, unsigned long long& ntest,
+                                         bool count) {
+  const bool actA = idx <= A.last, actB = idx <= B.last;
+  if (!(actA || actB)) return false;
+  if (count) ntest += (unsigned)actA + (unsigned)actB;
+  const float4 r0 = rec[0], r1 = rec[1], r2 = rec[2], r3 = rec[3];
+  // ray-peak test (blend_common.cuh ray_peak_test), the column's pixels share x
+  const float ddx = __fsub_rn(__fsub_rn(A.pc.pxc, r0.x), r0.z);
+  const F2 pyc{A.pc.pyc, B.pc.pyc}, hy{A.pc.hy, B.pc.hy};
+  const F2 ddy = sub2(sub2(pyc, f2(r0.y)), f2(r0.w));
+  const F2 w = fma2(f2(r1.y), ddy, f2(ddx));
+  const F2 num = fma2(mul2(f2(r1.x), w), w, mul2(mul2(f2(r1.z), ddy), ddy));
+  const F2 u = add2(fma2(f2(r2.y), hy, f2(r2.z)), f2(A.pc.hx));
+  const F2 v = add2(hy, f2(r3.x));
+  const F2 D = fma2(mul2(f2(r2.x), u), u, fma2(mul2(f2(r2.w), v), v, f2(r3.y)));
+  const F2 lim = mul2(f2(r1.w), D);
+  bool okA = actA && !(num.x > lim.x), okB = actB && !(num.y > lim.y);
+  if (!(okA || okB)) return false;
+  const F2 rD{rcp_approx(D.x), rcp_approx(D.y)};
+  const F2 m2 = mul2(num, rD);
+  const F2 ek = mul2(f2(-0.72134752044448170368f), m2);
+  const F2 kern{ex2_approx(ek.x), ex2_approx(ek.y)};
+  const F2 araw = mul2(f2(r3.z), kern);
+  const F2 alpha{fminf(araw.x, ALPHA_MAX_F), fminf(araw.y, ALPHA_MAX_F)};
+  okA = okA && alpha.x >= cutoff;
+  okB = okB && alpha.y >= cutoff;
+  if (!(okA || okB)) return false;
+  // emission (blend_common.cuh emission); s.x·Y0 is the same for both pixels
+  const float Y0 = (float)SH_C0;
+  const F2 Y1{A.pc.Y1, B.pc.Y1}, Y2{A.pc.Y2, B.pc.Y2}, Y3{A.pc.Y3, B.pc.Y3};
+  const float4 s0 = rec[4], s1 = rec[5], s2 = rec[6];
+  const F2 c0 = fma2(f2(s0.w), Y3, fma2(f2(s0.z), Y2, fma2(f2(s0.y), Y1, f2(__fmul_rn(s0.x, Y0)))));
+  const F2 c1 = fma2(f2(s1.w), Y3, fma2(f2(s1.z), Y2, fma2(f2(s1.y), Y1, f2(__fmul_rn(s1.x, Y0)))));
+  const F2 c2 = fma2(f2(s2.w), Y3, fma2(f2(s2.z), Y2, fma2(f2(s2.y), Y1, f2(__fmul_rn(s2.x, Y0)))));
+  const F2 E0{fmaxf(c0.x, 0.f), fmaxf(c0.y, 0.f)};
+  const F2 E1{fmaxf(c1.x, 0.f), fmaxf(c1.y, 0.f)};
+  const F2 E2{fmaxf(c2.x, 0.f), fmaxf(c2.y, 0.f)};
+  // the saturating splat moves the loss only through its emission
+  const bool satA = okA && A.sat && idx == A.last, satB = okB && B.sat && idx == B.last;
+  const bool nA = okA && !satA, nB = okB && !satB;
+  const F2 s_0{A.s0, B.s0}, s_1{A.s1, B.s1}, s_2{A.s2, B.s2};
+  F2 ek0{A.ek0, B.ek0}, ek1{A.ek1, B.ek1}, ek2{A.ek2, B.ek2};
+  const F2 sdE = fma2(s_0, sub2(E0, ek0), fma2(s_1, sub2(E1, ek1), mul2(s_2, sub2(E2, ek2))));
+  // state in front of splat i, recovered back to front (normal pixels only)
+  F2 thi{A.thi, B.thi}, tlo{A.tlo, B.tlo};
+  if constexpr (FAM != FAM_EXP) {
+    F2 h = thi, l = tlo;
+    df_add2(h, l, F2{-alpha.x, -alpha.y});
+    if (nA) { A.thi = h.x; A.tlo = l.x; }
+    if (nB) { B.thi = h.y; B.tlo = l.y; }
+  }
+  if constexpr (IsPFam<FAM>::value) {
+    if (nA) A.P = (idx == A.ck) ? A.Pck : div_newton(A.P, __fsub_rn(1.0f, alpha.x));
+    if (nB) B.P = (idx == B.ck) ? B.Pck : div_newton(B.P, __fsub_rn(1.0f, alpha.y));
+  }
+  F2 fp;
+  const F2 g{weight_g<FAM>(m, A.thi, A.tlo, A.P, fp.x), weight_g<FAM>(m, B.thi, B.tlo, B.P, fp.y)};
+  const F2 wgt = mul2(alpha, g);
+  const F2 carry{A.carry, B.carry};
+  F2 da, nc;
+  if constexpr (IsPFam<FAM>::value) {
+    const F2 P{A.P, B.P};
+    da = fma2(sdE, g, mul2(mul2(f2(-gam), P), carry));
+    nc = fma2(sub2(f2(1.0f), alpha), carry, mul2(sdE, alpha));
+  } else {
+    da = fma2(sdE, g, carry);
+    nc = fma2(mul2(sdE, alpha), fp, carry);
+  }
+  if (nA) A.carry = nc.x;
+  if (nB) B.carry = nc.y;
+  if (satA) { A.ek0 = E0.x; A.ek1 = E1.x; A.ek2 = E2.x; }
+  if (satB) { B.ek0 = E0.y; B.ek1 = E1.y; B.ek2 = E2.y; }
+  // dE = s·w for normal pixels, s·T̄_k for the saturating one
+  const F2 wt{satA ? A.tk : wgt.x, satB ? B.tk : wgt.y};
+  const F2 dE0 = mul2(s_0, wt), dE1 = mul2(s_1, wt), dE2 = mul2(s_2, wt);
+  const F2 dae{(araw.x >= ALPHA_MAX_F) ? 0.f : da.x, (araw.y >= ALPHA_MAX_F) ? 0.f : da.y};
+  o.dm2 = sel2(nA, nB, mul2(mul2(f2(-0.5f), alpha), dae));
+  o.dak = sel2(nA, nB, mul2(dae, kern));
+  // whitened peak offset y = B̃ e, e = δ − ε h (bwd_pixel's conic branch)
+  const float dxn = ddx * inv_f;
+  const F2 dyn = mul2(ddy, f2(inv_f));
+  const F2 Ahx = mul2(f2(r2.x), u);
+  const F2 Ahy = fma2(f2(r2.x * r2.y), u, mul2(f2(r2.w), v));
+  const F2 eps = mul2(fma2(f2(dxn), Ahx, mul2(dyn, Ahy)), rD);
+  const F2 qx = fma2(eps, f2(-A.pc.hx), f2(dxn));
+  const F2 qy = fma2(eps, F2{-hy.x, -hy.y}, dyn);
+  // qz = −ε: the B̃ z-column enters negated
+  o.ux = sel2(nA, nB, fma2(f2(bf[0].x), qx, fma2(f2(bf[0].y), qy, mul2(f2(-bf[0].z), eps))));
+  o.uy = sel2(nA, nB, fma2(f2(bf[1].x), qx, fma2(f2(bf[1].y), qy, mul2(f2(-bf[1].z), eps))));
+  o.uz = sel2(nA, nB, fma2(f2(bf[2].x), qx, fma2(f2(bf[2].y), qy, mul2(f2(-bf[2].z), eps))));
+  // SH moments use dE_c·[E_c > 0] (render.py:340-341)
+  o.e0 = sel2(okA && c0.x > 0.f, okB && c0.y > 0.f, dE0);
+  o.e1 = sel2(okA && c1.x > 0.f, okB && c1.y > 0.f, dE1);
+  o.e2 = sel2(okA && c2.x > 0.f, okB && c2.y > 0.f, dE2);
+  return true;
+}
+
 __device__ __forceinline__ void bwd_load(BwdPix& st, const CamDev& cam, int px, int py,
                                          const PixCache& cache, const float* __restrict__ seed,
                                          float bg0, float bg1, float bg2) {
