@@ -15,6 +15,48 @@
 
 namespace nxs {
 
+// Packed f32x2 arithmetic (Blackwell FFMA2/FADD2/FMUL2): lane x and lane y
+// are each the IEEE round-to-nearest scalar op, so packed and scalar code
+// give bit-identical results; scalar operands broadcast without moves.
+struct F2 {
+  float x, y;
+};
+__device__ __forceinline__ F2 f2(float a) { return F2{a, a}; }
+#define NXS_F2OP3(name, op)                                                                  \
+  __device__ __forceinline__ F2 name(F2 a, F2 b) {                                          \
+    F2 d;                                                                                    \
+    asm("{.reg .b64 ra, rb, rd;\n mov.b64 ra, {%2,%3};\n mov.b64 rb, {%4,%5};\n " op        \
+        " rd, ra, rb;\n mov.b64 {%0,%1}, rd;}"                                              \
+        : "=f"(d.x), "=f"(d.y)                                                               \
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));                                           \
+    return d;                                                                                \
+  }
+NXS_F2OP3(add2, "add.rn.f32x2")
+NXS_F2OP3(sub2, "sub.rn.f32x2")
+NXS_F2OP3(mul2, "mul.rn.f32x2")
+#undef NXS_F2OP3
+__device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) {
+  F2 d;
+  asm("{.reg .b64 ra, rb, rc, rd;\n mov.b64 ra, {%2,%3};\n mov.b64 rb, {%4,%5};\n"
+      " mov.b64 rc, {%6,%7};\n fma.rn.f32x2 rd, ra, rb, rc;\n mov.b64 {%0,%1}, rd;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ F2 sel2(bool qa, bool qb, F2 v) {
+  return F2{qa ? v.x : 0.f, qb ? v.y : 0.f};
+}
+// packed df_add: (hi, lo) += a per lane, exactly (nxs_internal.cuh df_add)
+__device__ __forceinline__ void df_add2(F2& hi, F2& lo, F2 a) {
+  const F2 s = add2(hi, a);
+  const F2 bb = sub2(s, hi);
+  const F2 e = add2(sub2(hi, sub2(s, bb)), sub2(a, bb));
+  const F2 el = add2(e, lo);
+  const F2 s2 = add2(s, el);
+  lo = sub2(el, sub2(s2, s));
+  hi = s2;
+}
+
 struct PixelConst {
   float pxc, pyc;  // pixel centre (j + 0.5, i + 0.5)
   float hx, hy;    // normalised image coordinates ((j+0.5-cx)/f, (i+0.5-cy)/f)
@@ -137,6 +179,50 @@ __device__ __forceinline__ int emission(const float4& s0, const float4& s1, cons
   E1 = fmaxf(e1, 0.f);
   E2 = fmaxf(e2, 0.f);
   return mask;
+}
+
+// Packed ray-peak test of one record for a column's two pixels (a: lane x,
+// b: lane y; same px, so Δx is shared): the same rounded ops as
+// ray_peak_test, lane by lane.  ok_a/ok_b enter as "pixel still replays"
+// and leave as "pixel passes the test".
+struct TestOut2 {
+  float ddx;
+  F2 ddy, u, v, rD, kern, araw, alpha;
+};
+__device__ __forceinline__ void ray_peak_test2(const float4& r0, const float4& r1, const float4& r2,
+                                               const float4& r3, const PixelConst& pa,
+                                               const PixelConst& pb, float cutoff, TestOut2& o,
+                                               bool& ok_a, bool& ok_b) {
+  o.ddx = __fsub_rn(__fsub_rn(pa.pxc, r0.x), r0.z);
+  const F2 hy{pa.hy, pb.hy};
+  o.ddy = sub2(sub2(F2{pa.pyc, pb.pyc}, f2(r0.y)), f2(r0.w));
+  const F2 w = fma2(f2(r1.y), o.ddy, f2(o.ddx));
+  const F2 num = fma2(mul2(f2(r1.x), w), w, mul2(mul2(f2(r1.z), o.ddy), o.ddy));
+  o.u = add2(fma2(f2(r2.y), hy, f2(r2.z)), f2(pa.hx));
+  o.v = add2(hy, f2(r3.x));
+  const F2 D = fma2(mul2(f2(r2.x), o.u), o.u, fma2(mul2(f2(r2.w), o.v), o.v, f2(r3.y)));
+  const F2 lim = mul2(f2(r1.w), D);
+  ok_a = ok_a && !(num.x > lim.x);
+  ok_b = ok_b && !(num.y > lim.y);
+  if (!(ok_a || ok_b)) return;
+  o.rD = F2{rcp_approx(D.x), rcp_approx(D.y)};
+  const F2 ek = mul2(f2(-0.72134752044448170368f), mul2(num, o.rD));
+  o.kern = F2{ex2_approx(ek.x), ex2_approx(ek.y)};
+  o.araw = mul2(f2(r3.z), o.kern);
+  o.alpha = F2{fminf(o.araw.x, ALPHA_MAX_F), fminf(o.araw.y, ALPHA_MAX_F)};
+  ok_a = ok_a && o.alpha.x >= cutoff;
+  ok_b = ok_b && o.alpha.y >= cutoff;
+}
+
+// Packed emission (same rounded ops as emission); c = the unclamped sums.
+__device__ __forceinline__ void emission2(const float4& s0, const float4& s1, const float4& s2,
+                                          const PixelConst& pa, const PixelConst& pb, F2& c0,
+                                          F2& c1, F2& c2) {
+  const float Y0 = (float)SH_C0;
+  const F2 Y1{pa.Y1, pb.Y1}, Y2{pa.Y2, pb.Y2}, Y3{pa.Y3, pb.Y3};
+  c0 = fma2(f2(s0.w), Y3, fma2(f2(s0.z), Y2, fma2(f2(s0.y), Y1, f2(__fmul_rn(s0.x, Y0)))));
+  c1 = fma2(f2(s1.w), Y3, fma2(f2(s1.z), Y2, fma2(f2(s1.y), Y1, f2(__fmul_rn(s1.x, Y0)))));
+  c2 = fma2(f2(s2.w), Y3, fma2(f2(s2.z), Y2, fma2(f2(s2.y), Y1, f2(__fmul_rn(s2.x, Y0)))));
 }
 
 }  // namespace nxs

@@ -132,44 +132,6 @@ __device__ __forceinline__ bool bwd_pixel(BwdPix& st, const float4* rec, const f
 // scalar op, so the ray-peak test and the emission stay bit-identical to the
 // forward's scalar code (blend_common.cuh); MUFU ops stay scalar.
 // ---------------------------------------------------------------------------
-struct F2 {
-  float x, y;
-};
-__device__ __forceinline__ F2 f2(float a) { return F2{a, a}; }
-#define NXS_F2OP3(name, op)                                                                  \
-  __device__ __forceinline__ F2 name(F2 a, F2 b) {                                          \
-    F2 d;                                                                                    \
-    asm("{.reg .b64 ra, rb, rd;\n mov.b64 ra, {%2,%3};\n mov.b64 rb, {%4,%5};\n " op        \
-        " rd, ra, rb;\n mov.b64 {%0,%1}, rd;}"                                              \
-        : "=f"(d.x), "=f"(d.y)                                                               \
-        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));                                           \
-    return d;                                                                                \
-  }
-NXS_F2OP3(add2, "add.rn.f32x2")
-NXS_F2OP3(sub2, "sub.rn.f32x2")
-NXS_F2OP3(mul2, "mul.rn.f32x2")
-#undef NXS_F2OP3
-__device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) {
-  F2 d;
-  asm("{.reg .b64 ra, rb, rc, rd;\n mov.b64 ra, {%2,%3};\n mov.b64 rb, {%4,%5};\n"
-      " mov.b64 rc, {%6,%7};\n fma.rn.f32x2 rd, ra, rb, rc;\n mov.b64 {%0,%1}, rd;}"
-      : "=f"(d.x), "=f"(d.y)
-      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
-  return d;
-}
-__device__ __forceinline__ F2 sel2(bool qa, bool qb, F2 v) {
-  return F2{qa ? v.x : 0.f, qb ? v.y : 0.f};
-}
-// packed df_add: (hi, lo) += a per lane, exactly (nxs_internal.cuh df_add)
-__device__ __forceinline__ void df_add2(F2& hi, F2& lo, F2 a) {
-  const F2 s = add2(hi, a);
-  const F2 bb = sub2(s, hi);
-  const F2 e = add2(sub2(hi, sub2(s, bb)), sub2(a, bb));
-  const F2 el = add2(e, lo);
-  const F2 s2 = add2(s, el);
-  lo = sub2(el, sub2(s2, s));
-  hi = s2;
-}
 
 // Outputs of one entry for the thread's two pixels (lane x: pixel a, y: b),
 // zero where a pixel does not replay the entry.
@@ -187,35 +149,16 @@ __device__ __forceinline__ bool bwd_pair(BwdPix& A, BwdPix& B, const float4* rec
   const bool actA = idx <= A.last, actB = idx <= B.last;
   if (!(actA || actB)) return false;
   if (count) ntest += (unsigned)actA + (unsigned)actB;
-  const float4 r0 = rec[0], r1 = rec[1], r2 = rec[2], r3 = rec[3];
-  // ray-peak test (blend_common.cuh ray_peak_test), the column's pixels share x
-  const float ddx = __fsub_rn(__fsub_rn(A.pc.pxc, r0.x), r0.z);
-  const F2 pyc{A.pc.pyc, B.pc.pyc}, hy{A.pc.hy, B.pc.hy};
-  const F2 ddy = sub2(sub2(pyc, f2(r0.y)), f2(r0.w));
-  const F2 w = fma2(f2(r1.y), ddy, f2(ddx));
-  const F2 num = fma2(mul2(f2(r1.x), w), w, mul2(mul2(f2(r1.z), ddy), ddy));
-  const F2 u = add2(fma2(f2(r2.y), hy, f2(r2.z)), f2(A.pc.hx));
-  const F2 v = add2(hy, f2(r3.x));
-  const F2 D = fma2(mul2(f2(r2.x), u), u, fma2(mul2(f2(r2.w), v), v, f2(r3.y)));
-  const F2 lim = mul2(f2(r1.w), D);
-  bool okA = actA && !(num.x > lim.x), okB = actB && !(num.y > lim.y);
+  TestOut2 t;
+  bool okA = actA, okB = actB;
+  ray_peak_test2(rec[0], rec[1], rec[2], rec[3], A.pc, B.pc, cutoff, t, okA, okB);
   if (!(okA || okB)) return false;
-  const F2 rD{rcp_approx(D.x), rcp_approx(D.y)};
-  const F2 m2 = mul2(num, rD);
-  const F2 ek = mul2(f2(-0.72134752044448170368f), m2);
-  const F2 kern{ex2_approx(ek.x), ex2_approx(ek.y)};
-  const F2 araw = mul2(f2(r3.z), kern);
-  const F2 alpha{fminf(araw.x, ALPHA_MAX_F), fminf(araw.y, ALPHA_MAX_F)};
-  okA = okA && alpha.x >= cutoff;
-  okB = okB && alpha.y >= cutoff;
-  if (!(okA || okB)) return false;
-  // emission (blend_common.cuh emission); s.x·Y0 is the same for both pixels
-  const float Y0 = (float)SH_C0;
-  const F2 Y1{A.pc.Y1, B.pc.Y1}, Y2{A.pc.Y2, B.pc.Y2}, Y3{A.pc.Y3, B.pc.Y3};
-  const float4 s0 = rec[4], s1 = rec[5], s2 = rec[6];
-  const F2 c0 = fma2(f2(s0.w), Y3, fma2(f2(s0.z), Y2, fma2(f2(s0.y), Y1, f2(__fmul_rn(s0.x, Y0)))));
-  const F2 c1 = fma2(f2(s1.w), Y3, fma2(f2(s1.z), Y2, fma2(f2(s1.y), Y1, f2(__fmul_rn(s1.x, Y0)))));
-  const F2 c2 = fma2(f2(s2.w), Y3, fma2(f2(s2.z), Y2, fma2(f2(s2.y), Y1, f2(__fmul_rn(s2.x, Y0)))));
+  const F2 alpha = t.alpha, kern = t.kern, araw = t.araw, rD = t.rD, u = t.u, v = t.v;
+  const F2 ddy = t.ddy, hy{A.pc.hy, B.pc.hy};
+  const float ddx = t.ddx;
+  const float4 r2 = rec[2];
+  F2 c0, c1, c2;
+  emission2(rec[4], rec[5], rec[6], A.pc, B.pc, c0, c1, c2);
   const F2 E0{fmaxf(c0.x, 0.f), fmaxf(c0.y, 0.f)};
   const F2 E1{fmaxf(c1.x, 0.f), fmaxf(c1.y, 0.f)};
   const F2 E2{fmaxf(c2.x, 0.f), fmaxf(c2.y, 0.f)};
