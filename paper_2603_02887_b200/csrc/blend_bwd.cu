@@ -17,11 +17,13 @@
 // saturating splat only receives dE = s·T̄_k (render.py:313-314).  No
 // per-sample state is stored.
 //
-// Reduction: per list entry each warp transposes its 32 pixels' 24 moments
-// through shared memory (24 column stores, 8 row loads, 31 adds), lanes
-// 0..23 add into a per-entry shared accumulator, and after each batch the
-// block flushes the non-zero sums with one fp64 atomic each into the
-// per-rank moment buffer.
+// Reduction: per list entry each warp transposes its 32 lanes' 24 moments
+// (each lane's two pixels already summed) through shared memory as 12
+// moment-pair rows (12 eight-byte stores per lane); lanes 2p and 2p+1 sum
+// pair row p over lanes 0-15 and 16-31 with packed adds (8 row loads, 15
+// FADD2), swap halves with one shuffle, and add their moment into a
+// per-entry shared accumulator.  After each batch the block flushes the
+// non-zero sums with one fp64 atomic each into the per-rank moment buffer.
 #include "bwd_common.cuh"
 
 namespace nxs {
@@ -36,11 +38,13 @@ constexpr int BWD_THREADS = TILE_PIX / 2;
 constexpr int BWD_WARPS = BWD_THREADS / 32;
 
 // Shared-memory layout of one block (dynamic): staged records + B frames,
-// their ranks, per-entry moment accumulators, and one 24x36-float transpose
-// scratch per warp (row k = moment k of all 32 lanes; rows padded to 36
-// floats so the column stores and the 16-B row loads are conflict free).
-constexpr int RED_STRIDE = 36;
-constexpr int RED_WARP = NMOM * RED_STRIDE;  // floats per warp
+// their ranks, per-entry moment accumulators, and one 12x72-float transpose
+// scratch per warp (row p = moment pair (2p, 2p+1) of all 32 lanes, lanes
+// 16-31 shifted by 4 banks so the pair stores and the 16-B row loads are
+// conflict free).
+constexpr int RED_HALF = 36;                 // lanes 16-31's pairs start here (bank shift)
+constexpr int RED_ROW = 2 * RED_HALF;        // one row per moment pair
+constexpr int RED_WARP = (NMOM / 2) * RED_ROW;  // floats per warp
 // Records, B frames and ranks are double-buffered: the next batch streams
 // in with cp.async while the current one is replayed.
 constexpr size_t BWD_SMEM = 2 * (sizeof(float4) * BWD_BATCH * (REC_F4 + 3) +
@@ -179,46 +183,59 @@ __global__ void __launch_bounds__(BWD_THREADS, 4)
                                       e1[q], e2[q], ntest, COUNT);
         }
         if (__any_sync(0xffffffffu, contrib)) {
-          // warp transpose-reduce through shared memory: lane r writes its
-          // (two-pixel) moments down column r, lane k < 24 then sums row k
+          // warp transpose-reduce through shared memory (moment-pair rows)
           const PixelConst& pa = st[0].pc;
           const PixelConst& pb = st[1].pc;
           const float ax = dm2[0] * ux[0], ay = dm2[0] * uy[0], az = dm2[0] * uz[0];
           const float bx = dm2[1] * ux[1], by = dm2[1] * uy[1], bz = dm2[1] * uz[1];
-          float* col = red + lane;
-          col[0 * RED_STRIDE] = fmaf(ax, ux[0], bx * ux[1]);
-          col[1 * RED_STRIDE] = fmaf(ax, uy[0], bx * uy[1]);
-          col[2 * RED_STRIDE] = fmaf(ax, uz[0], bx * uz[1]);
-          col[3 * RED_STRIDE] = fmaf(ay, uy[0], by * uy[1]);
-          col[4 * RED_STRIDE] = fmaf(ay, uz[0], by * uz[1]);
-          col[5 * RED_STRIDE] = fmaf(az, uz[0], bz * uz[1]);
-          col[6 * RED_STRIDE] = ax + bx;
-          col[7 * RED_STRIDE] = ay + by;
-          col[8 * RED_STRIDE] = az + bz;
-          col[11 * RED_STRIDE] = dak[0] + dak[1];
-          col[12 * RED_STRIDE] = (e0[0] + e0[1]) * Y0;
-          col[13 * RED_STRIDE] = fmaf(e0[0], pa.Y1, e0[1] * pb.Y1);
-          col[14 * RED_STRIDE] = fmaf(e0[0], pa.Y2, e0[1] * pb.Y2);
-          col[15 * RED_STRIDE] = fmaf(e0[0], pa.Y3, e0[1] * pb.Y3);
-          col[16 * RED_STRIDE] = (e1[0] + e1[1]) * Y0;
-          col[17 * RED_STRIDE] = fmaf(e1[0], pa.Y1, e1[1] * pb.Y1);
-          col[18 * RED_STRIDE] = fmaf(e1[0], pa.Y2, e1[1] * pb.Y2);
-          col[19 * RED_STRIDE] = fmaf(e1[0], pa.Y3, e1[1] * pb.Y3);
-          col[20 * RED_STRIDE] = (e2[0] + e2[1]) * Y0;
-          col[21 * RED_STRIDE] = fmaf(e2[0], pa.Y1, e2[1] * pb.Y1);
-          col[22 * RED_STRIDE] = fmaf(e2[0], pa.Y2, e2[1] * pb.Y2);
-          col[23 * RED_STRIDE] = fmaf(e2[0], pa.Y3, e2[1] * pb.Y3);
+          // moment pairs (2p, 2p+1) as one 8-byte store; rows 9 and 10 are unused
+          float v[NMOM];
+          v[0] = fmaf(ax, ux[0], bx * ux[1]);
+          v[1] = fmaf(ax, uy[0], bx * uy[1]);
+          v[2] = fmaf(ax, uz[0], bx * uz[1]);
+          v[3] = fmaf(ay, uy[0], by * uy[1]);
+          v[4] = fmaf(ay, uz[0], by * uz[1]);
+          v[5] = fmaf(az, uz[0], bz * uz[1]);
+          v[6] = ax + bx;
+          v[7] = ay + by;
+          v[8] = az + bz;
+          v[9] = 0.f;
+          v[10] = 0.f;
+          v[11] = dak[0] + dak[1];
+          v[12] = (e0[0] + e0[1]) * Y0;
+          v[13] = fmaf(e0[0], pa.Y1, e0[1] * pb.Y1);
+          v[14] = fmaf(e0[0], pa.Y2, e0[1] * pb.Y2);
+          v[15] = fmaf(e0[0], pa.Y3, e0[1] * pb.Y3);
+          v[16] = (e1[0] + e1[1]) * Y0;
+          v[17] = fmaf(e1[0], pa.Y1, e1[1] * pb.Y1);
+          v[18] = fmaf(e1[0], pa.Y2, e1[1] * pb.Y2);
+          v[19] = fmaf(e1[0], pa.Y3, e1[1] * pb.Y3);
+          v[20] = (e2[0] + e2[1]) * Y0;
+          v[21] = fmaf(e2[0], pa.Y1, e2[1] * pb.Y1);
+          v[22] = fmaf(e2[0], pa.Y2, e2[1] * pb.Y2);
+          v[23] = fmaf(e2[0], pa.Y3, e2[1] * pb.Y3);
+          float2* col = reinterpret_cast<float2*>(red + (lane < 16 ? 2 * lane : RED_HALF + 2 * (lane - 16)));
+#pragma unroll
+          for (int q = 0; q < NMOM / 2; ++q) col[q * (RED_ROW / 2)] = make_float2(v[2 * q], v[2 * q + 1]);
           __syncwarp();
-          if (lane < NMOM && lane != 9 && lane != 10) {
-            const float4* row = reinterpret_cast<const float4*>(red + lane * RED_STRIDE);
-            const float4 a = row[0], b = row[1], c = row[2], d = row[3];
-            const float4 e = row[4], f = row[5], g = row[6], h = row[7];
-            const float sum = (((a.x + a.y) + (a.z + a.w)) + ((b.x + b.y) + (b.z + b.w))) +
-                              (((c.x + c.y) + (c.z + c.w)) + ((d.x + d.y) + (d.z + d.w))) +
-                              ((((e.x + e.y) + (e.z + e.w)) + ((f.x + f.y) + (f.z + f.w))) +
-                               (((g.x + g.y) + (g.z + g.w)) + ((h.x + h.y) + (h.z + h.w))));
-            if (sum != 0.f) atomicAdd(&s_acc[j * NMOM + lane], sum);
+          // lane 2p sums moments (2p, 2p+1) over lanes 0-15, lane 2p+1 over
+          // lanes 16-31 (packed adds), then each keeps its own moment and
+          // takes the partner's half of it
+          F2 part = f2(0.f);
+          if (lane < NMOM) {
+            const float4* row =
+                reinterpret_cast<const float4*>(red + (lane >> 1) * RED_ROW + (lane & 1) * RED_HALF);
+            F2 t[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float4 r = row[i];
+              t[i] = add2(F2{r.x, r.y}, F2{r.z, r.w});
+            }
+            part = add2(add2(add2(t[0], t[1]), add2(t[2], t[3])), add2(add2(t[4], t[5]), add2(t[6], t[7])));
           }
+          const float other = __shfl_xor_sync(0xffffffffu, (lane & 1) ? part.x : part.y, 1);
+          const float sum = ((lane & 1) ? part.y : part.x) + other;
+          if (lane < NMOM && sum != 0.f) atomicAdd(&s_acc[j * NMOM + lane], sum);
           __syncwarp();
         }
       }
