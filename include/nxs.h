@@ -206,8 +206,10 @@ int nxs_depth_order(nxs_view* view, int32_t* order, void* stream);
  * restatement (oracle/binning_oracle.c): tile rectangle per Gaussian in
  * storage order (P x int32[4] = tx0,ty0,tx1,ty1; empty = -1; Gaussians
  * outside the projected depth phases read empty), and the FIRST depth
- * phase's tile ranges (n_tiles x int32[2]) and sorted pair values; with
- * NXS_FLAG_FULL_BINNING that phase holds every rank (n_pairs ranks). */
+ * phase's tile ranges (n_tiles x int32[2]) and sorted pair values, lists
+ * compacted tile after tile (ranges index pair_ranks); with
+ * NXS_FLAG_FULL_BINNING that phase holds every rank (n_pairs ranks).
+ * Synchronises `stream` (an inspection call, not on the hot path). */
 int nxs_binning_export(nxs_view* view, int32_t* rects, int32_t* ranges,
                        int32_t* pair_ranks, void* stream);
 

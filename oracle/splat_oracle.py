@@ -518,25 +518,43 @@ def _backward_batch(scene, cam, model, bg, out, st, seed, grads, mass):
     w = np.stack([s[7] for s in slots])
     g, fp, gamma = weight_terms(variant, param, tau_b, prod_b)
     sdE = np.einsum("smc,mc->sm", E - e_k[None], seed)          # seed·(E_i - E_k)
+    want_mag = mass is not None
+    if want_mag:
+        # absolute evaluation of the same sums (|terms| summed, Higham's
+        # running-error scale): seed·(E_i - E_k) cancels, and so can the
+        # adjoint d_alpha = sdE·g + Θ; an fp32 evaluation is accurate to
+        # ~eps of these magnitudes, not of the cancelled result
+        sdE_m = np.einsum("smc,mc->sm", np.abs(E) + np.abs(e_k[None]), np.abs(seed))
     if gamma == 0.0:
         # Θ_i = Σ_{j>i, go} sdE_j α_j f'(τ̄_j)
         term = np.where(go, sdE * a * fp, 0.0)
         suffix = np.cumsum(term[::-1], axis=0)[::-1] - term
         d_al = np.where(go, sdE * g + suffix, 0.0)
+        if want_mag:
+            tm = np.where(go, sdE_m * a * np.abs(fp), 0.0)
+            sm = np.cumsum(tm[::-1], axis=0)[::-1] - tm
+            d_al_m = np.where(go, sdE_m * np.abs(g) + sm, 0.0)
     else:
         # γ/(1-α_i) Σ_{j>i, go} sdE_j α_j P_j
         term = np.where(go, sdE * a * prod_b, 0.0)
         suffix = np.cumsum(term[::-1], axis=0)[::-1] - term
         d_al = np.where(go, sdE * g - gamma * suffix / (1.0 - a), 0.0)
+        if want_mag:
+            tm = np.where(go, sdE_m * a * np.abs(prod_b), 0.0)
+            sm = np.cumsum(tm[::-1], axis=0)[::-1] - tm
+            d_al_m = np.where(go, sdE_m * np.abs(g) + abs(gamma) * sm / (1.0 - a), 0.0)
     d_em = np.where(go[..., None], seed[None] * (a * g)[..., None], 0.0)
     d_em = np.where(satn[..., None], seed[None] * w[..., None], d_em)
     # scatter to (row, pixel)
     d_alpha_rows = np.zeros((n_r, m))
     d_em_rows = np.zeros((n_r, m, 3))
+    d_alpha_m = np.zeros((n_r, m)) if want_mag else None
     for si, s in enumerate(slots):
         rows = s[0]
         d_alpha_rows[rows, cols] += d_al[si]
         d_em_rows[rows, cols] += d_em[si]
+        if want_mag:
+            d_alpha_m[rows, cols] += d_al_m[si]
     # chain, reference render.py:326-341
     d_alpha_rows = np.where(geo["clamped"], 0.0, d_alpha_rows)
     da = d_alpha_rows * geo["alpha"]
@@ -571,6 +589,26 @@ def _backward_batch(scene, cam, model, bg, out, st, seed, grads, mass):
         mass["scales"][ids] += np.linalg.norm(t_s, axis=2).sum(1)[:, None]
         mass["quats"][ids] += np.linalg.norm(t_q, axis=2).sum(1)[:, None]
         mass["sh"][ids] += np.abs(t_sh).sum(1)
+        # componentwise scale (S = Σ_px |per-pixel term| of
+        # that entry alone), each per-pixel term evaluated in absolute
+        # values: |d_alpha| from its own terms (above), and |R|·|Λu| /
+        # |J|·|diff|·|Λu| for the rotations that mix a term's components
+        # (a centre component that is small next to its siblings is a
+        # cancellation of the rotated offset, fp32-accurate only to ~eps of
+        # the terms).  DESIGN.md §6 gives the measured cases that need it.
+        d_alpha_m = np.where(geo["clamped"], 0.0, d_alpha_m)
+        da_m = d_alpha_m * geo["alpha"]
+        R_abs = np.abs(geo["R"])
+        us2_abs = np.abs(us2)
+        mass["opacities_c"][ids] += (d_alpha_m * geo["kernel"]).sum(1)
+        mass["centers_c"][ids] += (da_m[:, :, None] * np.einsum("rab,rmb->rma", R_abs,
+                                                                 us2_abs)).sum(1)
+        mass["scales_c"][ids] += (da_m[:, :, None] * np.abs(u * us2 / geo["s"][:, None, :])).sum(1)
+        tq_m = da_m[:, :, None] * np.einsum("rqab,rma,rmb->rmq", np.abs(J), np.abs(geo["diff"]),
+                                            us2_abs)
+        tq_m = tq_m + np.abs(qn)[:, None, :] * np.einsum("rq,rmq->rm", np.abs(qn), tq_m)[:, :, None]
+        mass["quats_c"][ids] += tq_m.sum(1)
+        mass["sh_c"][ids] += np.abs(t_sh).sum(1)
 
 
 def _zero_grads(scene):
@@ -594,7 +632,11 @@ def backward(scene, cam, model, background, fwd, seed, *, with_mass=False):
     if seed.shape[0] == cam.width * cam.height and len(fwd["pixels"]) != seed.shape[0]:
         seed = seed[fwd["pixels"]]
     grads = _zero_grads(scene)
-    mass = _zero_grads(scene) if with_mass else None
+    mass = None
+    if with_mass:
+        mass = _zero_grads(scene)
+        for k in ("centers", "scales", "quats", "opacities", "sh"):
+            mass[k + "_c"] = np.zeros_like(mass[k])
     for b, idx, out, st in fwd["_states"]:
         _backward_batch(scene, cam, model, bg, out, st, seed[idx], grads, mass)
     if with_mass:

@@ -99,6 +99,8 @@ void launch_seg_sort(uint32_t*, int2*, unsigned int*, int, unsigned long long, c
                      long long max_seg = -1, const unsigned int* base = nullptr,
                      unsigned long long* total = nullptr, unsigned long long* overflow = nullptr);
 void launch_make_bases(const int2*, int, unsigned int*, cudaStream_t);
+void launch_compact_lists(const uint32_t*, const int2*, const int*, int, uint32_t*, int2*,
+                          cudaStream_t);
 void launch_chunk_key(const float*, const float*, const float*, const float*, int64_t,
                       const CamDev&, double, const uint32_t*, int, double*, unsigned long long*,
                       uint32_t*, cudaStream_t);
@@ -1733,13 +1735,37 @@ int nxs_binning_export(nxs_view* v, int32_t* rects, int32_t* ranges, int32_t* pa
   if (v->P && (rc = complete_order(v, s)) != NXS_OK) return rc;
   if (rects && v->P)
     NXS_CUDA(cudaMemcpyAsync(rects, v->rects.p, (size_t)v->P * 16, cudaMemcpyDeviceToDevice, s));
-  if (v->n_phases < 1) return NXS_OK;
-  if (ranges)
-    NXS_CUDA(cudaMemcpyAsync(ranges, v->ranges_ph[0].p, (size_t)v->n_tiles * 8,
-                             cudaMemcpyDeviceToDevice, s));
-  if (pair_ranks && v->ph_pairs[0])
-    NXS_CUDA(cudaMemcpyAsync(pair_ranks, v->pv_ph[0].p, (size_t)v->ph_pairs[0] * 4,
-                             cudaMemcpyDeviceToDevice, s));
+  if (v->n_phases < 1 || (!ranges && !pair_ranks)) return NXS_OK;
+  // The first phase's lists may sit at per-tile capacities (device-sized
+  // pass) with gaps between them: export them compacted, tile after tile,
+  // with the ranges rewritten to the compact offsets.  (Synchronises s.)
+  const int T = v->n_tiles;
+  std::vector<int2> hr(T);
+  NXS_CUDA(cudaMemcpyAsync(hr.data(), v->ranges_ph[0].p, (size_t)T * sizeof(int2),
+                           cudaMemcpyDeviceToHost, s));
+  NXS_CUDA(cudaStreamSynchronize(s));
+  std::vector<int> off(T);
+  long long tot = 0;
+  for (int t = 0; t < T; ++t) {
+    off[t] = (int)tot;
+    tot += std::max(0, hr[t].y - hr[t].x);
+  }
+  if (tot != v->ph_pairs[0])
+    return fail(NXS_ERR_STATE, "tile lists do not add up to the phase's pair count");
+  int* d_off = nullptr;
+  NXS_CUDA(cudaMallocAsync((void**)&d_off, (size_t)std::max(T, 1) * sizeof(int), s));
+  cudaError_t e = cudaMemcpyAsync(d_off, off.data(), (size_t)T * sizeof(int),
+                                  cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) {
+    launch_compact_lists(v->pv_ph[0].as<uint32_t>(), v->ranges_ph[0].as<int2>(), d_off, T,
+                         reinterpret_cast<uint32_t*>(pair_ranks), reinterpret_cast<int2*>(ranges),
+                         s);
+    e = cudaGetLastError();
+  }
+  cudaFreeAsync(d_off, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // (off[] is host memory)
+  if (e != cudaSuccess) return fail(NXS_ERR_CUDA, std::string("binning export: ") +
+                                                      cudaGetErrorString(e));
   return NXS_OK;
 }
 

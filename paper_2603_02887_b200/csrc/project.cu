@@ -1366,6 +1366,25 @@ void launch_emit_tiles(const int4* rects, const uint32_t* order, int64_t r0, int
 void launch_make_bases(const int2* ranges, int n_tiles, unsigned int* base, cudaStream_t s) {
   k_make_bases<<<1, TSCAN_THREADS, 0, s>>>(ranges, n_tiles, base);
 }
+
+// Export: gather each tile's list [ranges[t].x, ranges[t].y) to the compact
+// offset dst_off[t] (lists laid out at per-tile capacities have gaps).
+__global__ void k_compact_lists(const uint32_t* __restrict__ src, const int2* __restrict__ ranges,
+                                const int* __restrict__ dst_off, int n_tiles,
+                                uint32_t* __restrict__ dst, int2* __restrict__ dst_ranges) {
+  const int t = blockIdx.x;
+  if (t >= n_tiles) return;
+  const int2 r = ranges[t];
+  const int o = dst_off[t], n = max(0, r.y - r.x);
+  if (threadIdx.x == 0 && dst_ranges) dst_ranges[t] = make_int2(o, o + n);
+  if (dst)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[o + i] = src[r.x + i];
+}
+void launch_compact_lists(const uint32_t* src, const int2* ranges, const int* dst_off,
+                          int n_tiles, uint32_t* dst, int2* dst_ranges, cudaStream_t s) {
+  if (n_tiles > 0)
+    k_compact_lists<<<n_tiles, 128, 0, s>>>(src, ranges, dst_off, n_tiles, dst, dst_ranges);
+}
 void launch_seg_sort(uint32_t* vals, int2* ranges, unsigned int* cursor, int n_tiles,
                      unsigned long long cap, cudaStream_t s, long long max_seg,
                      const unsigned int* base, unsigned long long* total,
