@@ -70,6 +70,9 @@ extern "C" {
 #define NXS_FLAG_FULL_BINNING 2    /* bin every rank in one phase (no progressive binning) */
 #define NXS_FLAG_XBUF32 4          /* chunked order: start with the 32-entry pending buffer
                                       (default 16, rerun with 32 on overflow) */
+#define NXS_FLAG_THETA0 8          /* also accumulate the reference cache's theta0
+                                      (render.py:213; only nxs_cache_export reads it, the
+                                      backward does not: off by default on the global order) */
 
 /* ordering: opts.chunk_size (reference render(..., chunk_size=), render.py:350-358)
  *   NXS_CHUNK_EXACT (None) or C >= count: one chunk, exact per-pixel t order

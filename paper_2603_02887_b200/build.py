@@ -46,9 +46,10 @@ def _stale() -> bool:
     return any(p.stat().st_mtime > t for p in _deps())
 
 
-def _compile(src: Path, objdir: Path, log: list) -> Path:
+def _compile(src: Path, objdir: Path, log: list, extra=()) -> Path:
     obj = objdir / (src.stem + ".o")
-    cmd = [NVCC, *ARCH, *COMMON, *PER_FILE.get(src.name, []), "-c", str(src), "-o", str(obj)]
+    cmd = [NVCC, *ARCH, *COMMON, *PER_FILE.get(src.name, []), *extra, "-c", str(src), "-o",
+           str(obj)]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log.append((src.name, res.stderr))
     if res.returncode != 0:
@@ -56,27 +57,33 @@ def _compile(src: Path, objdir: Path, log: list) -> Path:
     return obj
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, variant: str = "", defines=()) -> Path:
+    """Build lib/libnxs.so; ``variant`` builds lib/libnxs_<variant>.so with
+    extra ``-D`` defines instead (kernel experiments, loaded via NXS_LIB)."""
+    out = LIBDIR / f"libnxs_{variant}.so" if variant else LIB
+    if not variant and not force and not _stale():
         return LIB
-    objdir = PKG / "build_obj"
+    objdir = PKG / ("build_obj" + (f"_{variant}" if variant else ""))
     objdir.mkdir(exist_ok=True)
     LIBDIR.mkdir(exist_ok=True)
     log: list = []
+    extra = [f"-D{d}" for d in defines]
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, objdir, log), _sources()))
-    tmp = LIB.with_suffix(".so.tmp")
+        objs = list(ex.map(lambda s: _compile(s, objdir, log, extra), _sources()))
+    tmp = out.with_suffix(".so.tmp")
     cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs)]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stderr}")
-    os.replace(tmp, LIB)
+    os.replace(tmp, out)
     if verbose:
         for name, err in log:
             print(f"== {name}\n{err}")
-    return LIB
+    return out
 
 
 if __name__ == "__main__":
-    p = build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    var = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--variant=")), "")
+    defs = [a[2:] for a in sys.argv if a.startswith("-D")]
+    p = build(force="--force" in sys.argv, verbose="-v" in sys.argv, variant=var, defines=defs)
     print(p)

@@ -379,6 +379,8 @@ int make_camera(const nxs_camera* c, CamDev& cd) {
   cd.H = c->height;
   cd.tiles_x = (c->width + TILE - 1) / TILE;
   cd.tiles_y = (c->height + TILE - 1) / TILE;
+  cd.inv_f = 1.0 / c->focal;
+  for (int i = 0; i < 9; ++i) cd.Rf[i] = (float)c->rotation[i];
   return NXS_OK;
 }
 
@@ -1414,7 +1416,8 @@ retry_sort:
                v->cum_ph[ph].as<int32_t>(), v->cum_ph[ph + 1].as<int32_t>(),
                v->active.as<uint8_t>(), n_active, ph > 0, ph + 1 < n_ph, opts->max_splats,
                (float)opts->alpha_cutoff, opts->near_plane, {bgf[0], bgf[1], bgf[2]},
-               rgb, overdraw, residual, v->lazy ? dsmall + 12 : nullptr};
+               rgb, overdraw, residual, v->lazy ? dsmall + 12 : nullptr,
+               (opts->flags & NXS_FLAG_THETA0) != 0};
     launch_blend_fwd(count, n_tiles, fa, cam, md, v->cache(), v->resume(), cnt, s);
     g_ht.mark("fwd_enq");
     NXS_LAUNCHED("blend_fwd");
@@ -1710,8 +1713,11 @@ int nxs_cache_export(nxs_view* v, uint8_t* sat, float* e_k, float* t_k, float* t
   if (sat) NXS_CUDA(cudaMemcpyAsync(sat, v->c_sat.p, npix, cudaMemcpyDeviceToDevice, s));
   if (e_k) NXS_CUDA(cudaMemcpyAsync(e_k, v->c_ek.p, npix * 12, cudaMemcpyDeviceToDevice, s));
   if (t_k) NXS_CUDA(cudaMemcpyAsync(t_k, v->c_tk.p, npix * 4, cudaMemcpyDeviceToDevice, s));
-  if (theta0)
+  if (theta0) {
+    if (v->opts.chunk_size == 1 && !(v->opts.flags & NXS_FLAG_THETA0))
+      return fail(NXS_ERR_STATE, "theta0 was not accumulated: forward without NXS_FLAG_THETA0");
     NXS_CUDA(cudaMemcpyAsync(theta0, v->c_th0.p, npix * 12, cudaMemcpyDeviceToDevice, s));
+  }
   return NXS_OK;
 }
 

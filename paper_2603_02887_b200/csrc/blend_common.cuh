@@ -65,7 +65,7 @@ struct PixelConst {
 
 __device__ __forceinline__ PixelConst pixel_setup(const CamDev& cam, int px, int py) {
   PixelConst pc;
-  const double inv_f = 1.0 / cam.f;  // uniform across the block
+  const double inv_f = cam.inv_f;  // = 1.0 / cam.f, correctly rounded on the host
   const double hxd = ((double)px + 0.5 - cam.cx) * inv_f;
   const double hyd = ((double)py + 0.5 - cam.cy) * inv_f;
   pc.pxc = (float)px + 0.5f;
@@ -74,9 +74,9 @@ __device__ __forceinline__ PixelConst pixel_setup(const CamDev& cam, int px, int
   pc.hy = (float)hyd;
   // world direction = R (hx, hy, 1), normalised (primitives.py:192-203); the
   // SH basis only needs it to fp32 accuracy
-  const float dx = __fmaf_rn((float)cam.R[0], pc.hx, __fmaf_rn((float)cam.R[1], pc.hy, (float)cam.R[2]));
-  const float dy = __fmaf_rn((float)cam.R[3], pc.hx, __fmaf_rn((float)cam.R[4], pc.hy, (float)cam.R[5]));
-  const float dz = __fmaf_rn((float)cam.R[6], pc.hx, __fmaf_rn((float)cam.R[7], pc.hy, (float)cam.R[8]));
+  const float dx = __fmaf_rn(cam.Rf[0], pc.hx, __fmaf_rn(cam.Rf[1], pc.hy, cam.Rf[2]));
+  const float dy = __fmaf_rn(cam.Rf[3], pc.hx, __fmaf_rn(cam.Rf[4], pc.hy, cam.Rf[5]));
+  const float dz = __fmaf_rn(cam.Rf[6], pc.hx, __fmaf_rn(cam.Rf[7], pc.hy, cam.Rf[8]));
   const float inv = rsqrtf(__fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz))));
   pc.Y1 = (float)(-SH_C1) * (dy * inv);
   pc.Y2 = (float)SH_C1 * (dz * inv);
@@ -167,13 +167,13 @@ __device__ __forceinline__ bool general_test(const float4* rec, const CamDev& ca
   return (t > near_plane) && (o.alpha >= cutoff);
 }
 
-// E_c = max(Σ_k sh[c][k] Y_k, 0); returns the positivity mask bits.
+// E_c = max(Σ_k sh[c][k] Y_k, 0); returns the positivity mask bits.  The
+// record holds sh[c][0]·Y0 pre-multiplied (project.cu).
 __device__ __forceinline__ int emission(const float4& s0, const float4& s1, const float4& s2,
                                         const PixelConst& pc, float& E0, float& E1, float& E2) {
-  const float Y0 = (float)SH_C0;
-  float e0 = __fmaf_rn(s0.w, pc.Y3, __fmaf_rn(s0.z, pc.Y2, __fmaf_rn(s0.y, pc.Y1, __fmul_rn(s0.x, Y0))));
-  float e1 = __fmaf_rn(s1.w, pc.Y3, __fmaf_rn(s1.z, pc.Y2, __fmaf_rn(s1.y, pc.Y1, __fmul_rn(s1.x, Y0))));
-  float e2 = __fmaf_rn(s2.w, pc.Y3, __fmaf_rn(s2.z, pc.Y2, __fmaf_rn(s2.y, pc.Y1, __fmul_rn(s2.x, Y0))));
+  float e0 = __fmaf_rn(s0.w, pc.Y3, __fmaf_rn(s0.z, pc.Y2, __fmaf_rn(s0.y, pc.Y1, s0.x)));
+  float e1 = __fmaf_rn(s1.w, pc.Y3, __fmaf_rn(s1.z, pc.Y2, __fmaf_rn(s1.y, pc.Y1, s1.x)));
+  float e2 = __fmaf_rn(s2.w, pc.Y3, __fmaf_rn(s2.z, pc.Y2, __fmaf_rn(s2.y, pc.Y1, s2.x)));
   int mask = (e0 > 0.f ? 1 : 0) | (e1 > 0.f ? 2 : 0) | (e2 > 0.f ? 4 : 0);
   E0 = fmaxf(e0, 0.f);
   E1 = fmaxf(e1, 0.f);
@@ -218,11 +218,10 @@ __device__ __forceinline__ void ray_peak_test2(const float4& r0, const float4& r
 __device__ __forceinline__ void emission2(const float4& s0, const float4& s1, const float4& s2,
                                           const PixelConst& pa, const PixelConst& pb, F2& c0,
                                           F2& c1, F2& c2) {
-  const float Y0 = (float)SH_C0;
   const F2 Y1{pa.Y1, pb.Y1}, Y2{pa.Y2, pb.Y2}, Y3{pa.Y3, pb.Y3};
-  c0 = fma2(f2(s0.w), Y3, fma2(f2(s0.z), Y2, fma2(f2(s0.y), Y1, f2(__fmul_rn(s0.x, Y0)))));
-  c1 = fma2(f2(s1.w), Y3, fma2(f2(s1.z), Y2, fma2(f2(s1.y), Y1, f2(__fmul_rn(s1.x, Y0)))));
-  c2 = fma2(f2(s2.w), Y3, fma2(f2(s2.z), Y2, fma2(f2(s2.y), Y1, f2(__fmul_rn(s2.x, Y0)))));
+  c0 = fma2(f2(s0.w), Y3, fma2(f2(s0.z), Y2, fma2(f2(s0.y), Y1, f2(s0.x))));
+  c1 = fma2(f2(s1.w), Y3, fma2(f2(s1.z), Y2, fma2(f2(s1.y), Y1, f2(s1.x))));
+  c2 = fma2(f2(s2.w), Y3, fma2(f2(s2.z), Y2, fma2(f2(s2.y), Y1, f2(s2.x))));
 }
 
 }  // namespace nxs

@@ -16,14 +16,24 @@
 //     subtract its way back to every τ̄_i bit-exactly;
 //   * the per-pixel cache (last live position, τ̄_end, P_end, t_k, P
 //     checkpoint) is all the back-to-front backward needs.
+#include <type_traits>
+
 #include "blend_common.cuh"
 
 namespace nxs {
 
 constexpr int FWD_BATCH = 64;  // list entries per staged batch
+#ifdef NXS_FWD_PIPE
+constexpr bool FWD_PIPE = true;  // test entry j+1 ahead of compositing j
+#else
+constexpr bool FWD_PIPE = false;
+#endif
+#ifndef NXS_FWD_MINB
+#define NXS_FWD_MINB 3
+#endif
 
-template <int FAM, bool COUNT>
-__global__ void __launch_bounds__(TILE_PIX, 3)
+template <int FAM, bool COUNT, bool THETA>
+__global__ void __launch_bounds__(TILE_PIX, NXS_FWD_MINB)
     k_blend_fwd(const float4* __restrict__ records, const uint32_t* __restrict__ pairs,
                 const int2* __restrict__ ranges, const int32_t* __restrict__ cum_in,
                 int32_t* __restrict__ cum_out, uint8_t* __restrict__ active,
@@ -63,10 +73,12 @@ __global__ void __launch_bounds__(TILE_PIX, 3)
     rad2 = rs.rad[3 * pix + 2];
     Trem = rs.trem[pix];
     count = rs.count[pix];
-    sea0 = rs.sea[3 * pix + 0];
-    sea1 = rs.sea[3 * pix + 1];
-    sea2 = rs.sea[3 * pix + 2];
-    sa = rs.sa[pix];
+    if (THETA) {
+      sea0 = rs.sea[3 * pix + 0];
+      sea1 = rs.sea[3 * pix + 1];
+      sea2 = rs.sea[3 * pix + 2];
+      sa = rs.sa[pix];
+    }
     last = cache.last[pix];
     sat = cache.sat[pix] != 0;
     tk = cache.t_k[pix];
@@ -103,24 +115,38 @@ __global__ void __launch_bounds__(TILE_PIX, 3)
     } else {
       cp_async_wait<0>();
     }
-    __syncthreads();
+    // (the barrier also tells whether this batch holds a near-plane record:
+    // almost never, so the common walk carries no per-entry flag test)
+    const bool gen_batch =
+        __syncthreads_or(tid < n && (__float_as_int(s_rec[buf][tid][3].w) & RF_GENERAL));
     float4(*s_cur)[REC_F4] = s_rec[buf];
-    if (!done) {
-      for (int j = 0; j < n; ++j) {
-        if (COUNT) ++ntest;
-        TestOut t;
+    // One entry: the ray-peak test and emission (independent of the carry)
+    // of entry j+1 are computed before entry j is composited, so the two
+    // dependency chains interleave.
+    auto walk = [&](auto gen_tag) {
+      constexpr bool GEN = decltype(gen_tag)::value;
+      auto test = [&](int j, TestOut& t, float& E0, float& E1, float& E2) -> bool {
         bool ok;
-        if (__float_as_int(s_cur[j][3].w) & RF_GENERAL) {  // block-uniform branch
+        if (GEN && (__float_as_int(s_cur[j][3].w) & RF_GENERAL)) {  // block-uniform branch
           float gx, gy, gz, tpk;
           ok = general_test(s_cur[j], cam, px, py, cutoff, near_plane, t, gx, gy, gz, tpk);
         } else {
           ok = ray_peak_test(s_cur[j][0], s_cur[j][1], s_cur[j][2], s_cur[j][3], pc, cutoff, t);
         }
+        if (ok) emission(s_cur[j][4], s_cur[j][5], s_cur[j][6], pc, E0, E1, E2);
+        return ok;
+      };
+      TestOut tn;
+      float En0 = 0.f, En1 = 0.f, En2 = 0.f;
+      bool okn = FWD_PIPE ? test(0, tn, En0, En1, En2) : false;
+      for (int j = 0; j < n; ++j) {
+        if (COUNT) ++ntest;
+        if (!FWD_PIPE) okn = test(j, tn, En0, En1, En2);
+        const bool ok = okn;
+        const float alpha = tn.alpha, E0 = En0, E1 = En1, E2 = En2;
+        if (FWD_PIPE && j + 1 < n) okn = test(j + 1, tn, En0, En1, En2);
         if (!ok) continue;
         const int idx = vbase + base + j;
-        const float alpha = t.alpha;
-        float E0, E1, E2;
-        emission(s_cur[j][4], s_cur[j][5], s_cur[j][6], pc, E0, E1, E2);
         float fp;
         const float g = weight_g<FAM>(m, thi, tlo, P, fp);
         const float wr = alpha * g;
@@ -144,7 +170,7 @@ __global__ void __launch_bounds__(TILE_PIX, 3)
         rad0 = fmaf(wr, E0, rad0);
         rad1 = fmaf(wr, E1, rad1);
         rad2 = fmaf(wr, E2, rad2);
-        if (cb >= 1) {
+        if (THETA && cb >= 1) {
           sea0 = fmaf(alpha, E0, sea0);
           sea1 = fmaf(alpha, E1, sea1);
           sea2 = fmaf(alpha, E2, sea2);
@@ -172,6 +198,12 @@ __global__ void __launch_bounds__(TILE_PIX, 3)
           break;
         }
       }
+    };
+    if (!done) {
+      if (gen_batch)
+        walk(std::true_type{});
+      else
+        walk(std::false_type{});
     }
     // all threads are past buffer `buf` before the next iteration refills it
     if (__syncthreads_count(!done) == 0) break;
@@ -221,19 +253,23 @@ __global__ void __launch_bounds__(TILE_PIX, 3)
   cache.e_k[3 * pix + 0] = ek0;
   cache.e_k[3 * pix + 1] = ek1;
   cache.e_k[3 * pix + 2] = ek2;
-  cache.theta0[3 * pix + 0] = sea0 - ek0 * sa;  // render.py:213
-  cache.theta0[3 * pix + 1] = sea1 - ek1 * sa;
-  cache.theta0[3 * pix + 2] = sea2 - ek2 * sa;
+  if (THETA) {
+    cache.theta0[3 * pix + 0] = sea0 - ek0 * sa;  // render.py:213
+    cache.theta0[3 * pix + 1] = sea1 - ek1 * sa;
+    cache.theta0[3 * pix + 2] = sea2 - ek2 * sa;
+  }
   if (save && still > 0) {  // the tile continues in the next depth phase
     rs.rad[3 * pix + 0] = rad0;
     rs.rad[3 * pix + 1] = rad1;
     rs.rad[3 * pix + 2] = rad2;
     rs.trem[pix] = Trem;
     rs.count[pix] = count;
-    rs.sea[3 * pix + 0] = sea0;
-    rs.sea[3 * pix + 1] = sea1;
-    rs.sea[3 * pix + 2] = sea2;
-    rs.sa[pix] = sa;
+    if (THETA) {
+      rs.sea[3 * pix + 0] = sea0;
+      rs.sea[3 * pix + 1] = sea1;
+      rs.sea[3 * pix + 2] = sea2;
+      rs.sa[pix] = sa;
+    }
   }
 }
 
@@ -242,7 +278,8 @@ template <int FAM>
 static void launch_fwd_fam(bool count, int n_tiles, const FwdArgs& a, const CamDev& cam,
                            const ModelDev& m, const PixCache& cache, const PixResume& rs,
                            Counters* cnt, cudaStream_t s) {
-  auto k = count ? k_blend_fwd<FAM, true> : k_blend_fwd<FAM, false>;
+  auto k = count ? (a.theta0 ? k_blend_fwd<FAM, true, true> : k_blend_fwd<FAM, true, false>)
+                 : (a.theta0 ? k_blend_fwd<FAM, false, true> : k_blend_fwd<FAM, false, false>);
   k<<<n_tiles, TILE_PIX, 0, s>>>(a.records, a.pairs, a.ranges, a.cum_in, a.cum_out, a.active,
                                  a.n_active, a.resume, a.save, cam, m, a.max_splats, a.cutoff,
                                  a.near_plane, a.bg[0], a.bg[1], a.bg[2], a.rgb, a.overdraw,

@@ -211,10 +211,12 @@ __device__ __forceinline__ bool bwd_pair(BwdPix& A, BwdPix& B, const float4* rec
   const F2 eps = mul2(fma2(f2(dxn), Ahx, mul2(dyn, Ahy)), rD);
   const F2 qx = fma2(eps, f2(-A.pc.hx), f2(dxn));
   const F2 qy = fma2(eps, F2{-hy.x, -hy.y}, dyn);
-  // qz = −ε: the B̃ z-column enters negated
-  o.ux = sel2(nA, nB, fma2(f2(bf[0].x), qx, fma2(f2(bf[0].y), qy, mul2(f2(-bf[0].z), eps))));
-  o.uy = sel2(nA, nB, fma2(f2(bf[1].x), qx, fma2(f2(bf[1].y), qy, mul2(f2(-bf[1].z), eps))));
-  o.uz = sel2(nA, nB, fma2(f2(bf[2].x), qx, fma2(f2(bf[2].y), qy, mul2(f2(-bf[2].z), eps))));
+  // qz = −ε: the B̃ z-column enters negated.  Not masked: every moment of
+  // the offset carries the factor dm2, zero for a pixel that does not
+  // contribute, and the offset itself is finite (D > 0 for any pixel).
+  o.ux = fma2(f2(bf[0].x), qx, fma2(f2(bf[0].y), qy, mul2(f2(-bf[0].z), eps)));
+  o.uy = fma2(f2(bf[1].x), qx, fma2(f2(bf[1].y), qy, mul2(f2(-bf[1].z), eps)));
+  o.uz = fma2(f2(bf[2].x), qx, fma2(f2(bf[2].y), qy, mul2(f2(-bf[2].z), eps)));
   // SH moments use dE_c·[E_c > 0] (render.py:340-341)
   o.e0 = sel2(okA && c0.x > 0.f, okB && c0.y > 0.f, dE0);
   o.e1 = sel2(okA && c1.x > 0.f, okB && c1.y > 0.f, dE1);

@@ -47,6 +47,8 @@ struct CamDev {
   double f, cx, cy;
   int W, H;
   int tiles_x, tiles_y;
+  double inv_f;  // 1/f (IEEE, host): per-pixel setup without a double division
+  float Rf[9];   // R rounded to fp32 (the SH basis direction)
 };
 
 // model families
@@ -121,6 +123,7 @@ struct FwdArgs {
   // max over the tiles finishing in this pass of the last rank their list
   // needed (the view's first-phase hint for its next call), or null
   unsigned long long* need_rank;
+  bool theta0;  // accumulate the reference cache's theta0 (NXS_FLAG_THETA0)
 };
 
 // exact-order mode (K3x/K4x)

@@ -735,9 +735,11 @@ __device__ __forceinline__ void project_one(const GParams& prm, int64_t g, const
     rec[3] = make_float4((float)e, (float)gg, (float)opac,
                          __int_as_float(RF_CONIC | (smx > 4.0 * smn ? RF_ANISO : 0)));
   }
-  rec[4] = make_float4(shv[0], shv[1], shv[2], shv[3]);
-  rec[5] = make_float4(shv[4], shv[5], shv[6], shv[7]);
-  rec[6] = make_float4(shv[8], shv[9], shv[10], shv[11]);
+  // SH per channel; the DC coefficient is stored pre-multiplied by Y0 = C0
+  // (rounded once from fp64), so the per-pixel emission starts from it
+  rec[4] = make_float4((float)((double)shv[0] * SH_C0), shv[1], shv[2], shv[3]);
+  rec[5] = make_float4((float)((double)shv[4] * SH_C0), shv[5], shv[6], shv[7]);
+  rec[6] = make_float4((float)((double)shv[8] * SH_C0), shv[9], shv[10], shv[11]);
   // conic: t coefficients (A'b')·h of the exact-order mode, and b'_z (the
   // backward's cancellation-free peak offset)
   if (!general) rec[7] = make_float4((float)Ab[0], (float)Ab[1], (float)Ab[2], (float)bp[2]);

@@ -161,14 +161,19 @@ class _Stage:
         self.buf = torch.empty(n, dtype=dtype, pin_memory=True)
         self.ev = torch.cuda.Event()
         self.ev.record()
+        self.lock = threading.Lock()  # one host thread fills the buffer at a time
+
+
+_STAGES_LOCK = threading.Lock()
 
 
 def _stage(key, n, dtype) -> _Stage:
-    st = _STAGES.get(key)
-    if st is None or st.buf.numel() < n or st.buf.dtype != dtype:
-        st = _Stage(max(n, 1), dtype)
-        _STAGES[key] = st
-    return st
+    with _STAGES_LOCK:
+        st = _STAGES.get(key)
+        if st is None or st.buf.numel() < n or st.buf.dtype != dtype:
+            st = _Stage(max(n, 1), dtype)
+            _STAGES[key] = st
+        return st
 
 
 def _h2d_f32(a: np.ndarray, dev, key):
@@ -178,12 +183,13 @@ def _h2d_f32(a: np.ndarray, dev, key):
     n = src.numel()
     out = torch.empty(n, dtype=torch.float32, device=dev)
     st = _stage(("h2d", key), n, torch.float32)
-    st.ev.synchronize()  # the previous upload from this buffer has left it
-    for off in range(0, n, _PIECE):
-        end = min(n, off + _PIECE)
-        st.buf[off:end].copy_(src[off:end])
-        out[off:end].copy_(st.buf[off:end], non_blocking=True)
-    st.ev.record(torch.cuda.current_stream(dev))
+    with st.lock:
+        st.ev.synchronize()  # the previous upload from this buffer has left it
+        for off in range(0, n, _PIECE):
+            end = min(n, off + _PIECE)
+            st.buf[off:end].copy_(src[off:end])
+            out[off:end].copy_(st.buf[off:end], non_blocking=True)
+        st.ev.record(torch.cuda.current_stream(dev))
     return out.reshape(np.shape(a))
 
 
@@ -289,7 +295,7 @@ def _model_struct(model):
 
 
 def _forward_args(dev, camera, model, background, max_splats, alpha_cutoff, near, chunk_size,
-                  count_events, full_binning, first_phase_ranks, out):
+                  count_events, full_binning, first_phase_ranks, out, theta0=False):
     import torch
     chunk = _effective_chunk(chunk_size, dev.count)
     _check_mode(chunk)
@@ -302,7 +308,8 @@ def _forward_args(dev, camera, model, background, max_splats, alpha_cutoff, near
                torch.empty((H, W), dtype=torch.float32, device=d))
     bg = np.asarray(background, dtype=np.float64).reshape(3)
     flags = (_native.NXS_FLAG_COUNT_EVENTS if count_events else 0) | \
-        (_native.NXS_FLAG_FULL_BINNING if full_binning else 0)
+        (_native.NXS_FLAG_FULL_BINNING if full_binning else 0) | \
+        (_native.NXS_FLAG_THETA0 if theta0 else 0)
     opts = _native.make_opts(max_splats, alpha_cutoff, near, chunk, flags, first_phase_ranks)
     return _native.make_camera(camera), ms, opts, bg, out
 
@@ -320,12 +327,13 @@ def _raise_mapped(e):
 def forward_device(view, dev: DeviceScene, camera, model, background, *, max_splats=128,
                    alpha_cutoff=DEFAULT_ALPHA_CUTOFF, near=NEAR_PLANE, chunk_size=1,
                    count_events=False, full_binning=False, first_phase_ranks=0, out=None,
-                   stream=None):
+                   stream=None, theta0=False):
     """Forward render on the device; returns (rgb (H,W,3), overdraw (H,W)
-    int32, residual (H,W)) float32 CUDA tensors."""
+    int32, residual (H,W)) float32 CUDA tensors.  ``theta0`` also keeps the
+    reference cache's theta0 for :meth:`View.cache_export`."""
     cam, ms, opts, bg, out = _forward_args(dev, camera, model, background, max_splats,
                                            alpha_cutoff, near, chunk_size, count_events,
-                                           full_binning, first_phase_ranks, out)
+                                           full_binning, first_phase_ranks, out, theta0)
     try:
         view.forward(dev, cam, ms, opts, bg, out[0], out[1], out[2], stream=stream)
     except _native.NxsError as e:
@@ -351,6 +359,26 @@ def forward_backward_device(view, dev: DeviceScene, camera, model, background, s
     except _native.NxsError as e:
         _raise_mapped(e)
     return out, grads
+
+
+def _same_scene(arrs, dev: DeviceScene) -> bool:
+    """``arrs`` (host or device, any float dtype) equals the device scene at
+    the device precision (float32), field by field."""
+    import torch
+    n = dev.count
+    for name, shape in (("centers", (n, 3)), ("scales", (n, 3)), ("quats", (n, 4)),
+                        ("opacities", (n,)), ("sh", tuple(dev.sh.shape))):
+        x = getattr(arrs, name)
+        if isinstance(x, torch.Tensor):
+            t = x.to(device=dev.centers.device, dtype=torch.float32).reshape(shape)
+        else:
+            x = np.asarray(x)
+            if x.size != int(np.prod(shape)):
+                return False
+            t = _h2d_f32(x.reshape(shape), dev.centers.device, "cmp_" + name)
+        if not torch.equal(t, getattr(dev, name)):
+            return False
+    return True
 
 
 def zero_grads_device(dev: DeviceScene) -> dict:
@@ -499,7 +527,8 @@ def render_forward_cached(arrs, camera, model, background, *, max_splats: int = 
     view = _acquire_view()
     try:
         out = forward_device(view, dev, camera, model, background, max_splats=max_splats,
-                             alpha_cutoff=alpha_cutoff, near=near, chunk_size=chunk_size)
+                             alpha_cutoff=alpha_cutoff, near=near, chunk_size=chunk_size,
+                             theta0=True)
     except BaseException:
         _release_view(view)
         raise
@@ -526,8 +555,13 @@ def render_backward(arrs, camera, model, background, cache, seed_image, *,
         raise ValueError("render_backward settings must match the forward call")
     if len(arrs) != st.dev.count:
         raise ValueError("scene size differs from the forward call")
-    # the replay uses the forward's device scene (the cache describes it)
+    # The replay runs on the forward's projected scene (the cache describes
+    # that traversal); the reference recomputes the geometry from ``arrs``
+    # (render.py:437-442), so ``arrs`` must be the forward's scene.
     dev = st.dev
+    if arrs is not dev and not _same_scene(arrs, dev):
+        raise ValueError("render_backward: arrs differ from the scene of the forward call "
+                         "(the cache replays that forward's traversal)")
     H, W = int(camera.height), int(camera.width)
     seed = np.asarray(seed_image, dtype=np.float64).reshape(H, W, 3) if not isinstance(
         seed_image, torch.Tensor) else seed_image
