@@ -160,60 +160,62 @@ __global__ void __launch_bounds__(BWD_THREADS, 4)
 
       for (int j = min(n - 1, wlast - base); j >= 0; --j) {
         const int idx = base + j;
-        // both pixels' contributions as a few scalars each; zero when a
-        // pixel does not contribute, so the moments need no separate zeroing
-        float dm2[2] = {0.f, 0.f}, ux[2] = {0.f, 0.f}, uy[2] = {0.f, 0.f}, uz[2] = {0.f, 0.f};
-        float dak[2] = {0.f, 0.f}, e0[2] = {0.f, 0.f}, e1[2] = {0.f, 0.f}, e2[2] = {0.f, 0.f};
-        bool contrib = false;
+        // both pixels' contributions (lane x: pixel a, y: b), zero where a
+        // pixel does not contribute, so the moments need no separate masking
+        PairOut po;
+        bool contrib;
         if ((__float_as_int(s_rec[j][3].w) & (RF_GENERAL | RF_ANISO)) == 0) {  // block-uniform
-          PairOut po;
           contrib = bwd_pair<FAM>(st[0], st[1], s_rec[j], s_bf[j], idx, m, cutoff, inv_f, gam, po,
                                   ntest, COUNT);
-          if (contrib) {
-            dm2[0] = po.dm2.x, dm2[1] = po.dm2.y, ux[0] = po.ux.x, ux[1] = po.ux.y;
-            uy[0] = po.uy.x, uy[1] = po.uy.y, uz[0] = po.uz.x, uz[1] = po.uz.y;
-            dak[0] = po.dak.x, dak[1] = po.dak.y, e0[0] = po.e0.x, e0[1] = po.e0.y;
-            e1[0] = po.e1.x, e1[1] = po.e1.y, e2[0] = po.e2.x, e2[1] = po.e2.y;
-          }
         } else {
+          float dm2[2] = {0.f, 0.f}, ux[2] = {0.f, 0.f}, uy[2] = {0.f, 0.f}, uz[2] = {0.f, 0.f};
+          float dak[2] = {0.f, 0.f}, e0[2] = {0.f, 0.f}, e1[2] = {0.f, 0.f}, e2[2] = {0.f, 0.f};
+          contrib = false;
 #pragma unroll
           for (int q = 0; q < 2; ++q)
             contrib |= bwd_pixel<FAM>(st[q], s_rec[j], s_bf[j], idx, cam, m, cutoff, near_plane,
                                       inv_f, gam, dm2[q], ux[q], uy[q], uz[q], dak[q], e0[q],
                                       e1[q], e2[q], ntest, COUNT);
+          po.dm2 = F2{dm2[0], dm2[1]};
+          po.ux = F2{ux[0], ux[1]};
+          po.uy = F2{uy[0], uy[1]};
+          po.uz = F2{uz[0], uz[1]};
+          po.dak = F2{dak[0], dak[1]};
+          po.e0 = F2{e0[0], e0[1]};
+          po.e1 = F2{e1[0], e1[1]};
+          po.e2 = F2{e2[0], e2[1]};
         }
         if (__any_sync(0xffffffffu, contrib)) {
           // warp transpose-reduce through shared memory (moment-pair rows)
           const PixelConst& pa = st[0].pc;
           const PixelConst& pb = st[1].pc;
-          const float ax = dm2[0] * ux[0], ay = dm2[0] * uy[0], az = dm2[0] * uz[0];
-          const float bx = dm2[1] * ux[1], by = dm2[1] * uy[1], bz = dm2[1] * uz[1];
+          const F2 a = mul2(po.dm2, po.ux), b = mul2(po.dm2, po.uy), c = mul2(po.dm2, po.uz);
           // moment pairs (2p, 2p+1) as one 8-byte store; rows 9 and 10 are unused
           float v[NMOM];
-          v[0] = fmaf(ax, ux[0], bx * ux[1]);
-          v[1] = fmaf(ax, uy[0], bx * uy[1]);
-          v[2] = fmaf(ax, uz[0], bx * uz[1]);
-          v[3] = fmaf(ay, uy[0], by * uy[1]);
-          v[4] = fmaf(ay, uz[0], by * uz[1]);
-          v[5] = fmaf(az, uz[0], bz * uz[1]);
-          v[6] = ax + bx;
-          v[7] = ay + by;
-          v[8] = az + bz;
+          v[0] = fmaf(a.x, po.ux.x, a.y * po.ux.y);
+          v[1] = fmaf(a.x, po.uy.x, a.y * po.uy.y);
+          v[2] = fmaf(a.x, po.uz.x, a.y * po.uz.y);
+          v[3] = fmaf(b.x, po.uy.x, b.y * po.uy.y);
+          v[4] = fmaf(b.x, po.uz.x, b.y * po.uz.y);
+          v[5] = fmaf(c.x, po.uz.x, c.y * po.uz.y);
+          v[6] = a.x + a.y;
+          v[7] = b.x + b.y;
+          v[8] = c.x + c.y;
           v[9] = 0.f;
           v[10] = 0.f;
-          v[11] = dak[0] + dak[1];
-          v[12] = (e0[0] + e0[1]) * Y0;
-          v[13] = fmaf(e0[0], pa.Y1, e0[1] * pb.Y1);
-          v[14] = fmaf(e0[0], pa.Y2, e0[1] * pb.Y2);
-          v[15] = fmaf(e0[0], pa.Y3, e0[1] * pb.Y3);
-          v[16] = (e1[0] + e1[1]) * Y0;
-          v[17] = fmaf(e1[0], pa.Y1, e1[1] * pb.Y1);
-          v[18] = fmaf(e1[0], pa.Y2, e1[1] * pb.Y2);
-          v[19] = fmaf(e1[0], pa.Y3, e1[1] * pb.Y3);
-          v[20] = (e2[0] + e2[1]) * Y0;
-          v[21] = fmaf(e2[0], pa.Y1, e2[1] * pb.Y1);
-          v[22] = fmaf(e2[0], pa.Y2, e2[1] * pb.Y2);
-          v[23] = fmaf(e2[0], pa.Y3, e2[1] * pb.Y3);
+          v[11] = po.dak.x + po.dak.y;
+          v[12] = (po.e0.x + po.e0.y) * Y0;
+          v[13] = fmaf(po.e0.x, pa.Y1, po.e0.y * pb.Y1);
+          v[14] = fmaf(po.e0.x, pa.Y2, po.e0.y * pb.Y2);
+          v[15] = fmaf(po.e0.x, pa.Y3, po.e0.y * pb.Y3);
+          v[16] = (po.e1.x + po.e1.y) * Y0;
+          v[17] = fmaf(po.e1.x, pa.Y1, po.e1.y * pb.Y1);
+          v[18] = fmaf(po.e1.x, pa.Y2, po.e1.y * pb.Y2);
+          v[19] = fmaf(po.e1.x, pa.Y3, po.e1.y * pb.Y3);
+          v[20] = (po.e2.x + po.e2.y) * Y0;
+          v[21] = fmaf(po.e2.x, pa.Y1, po.e2.y * pb.Y1);
+          v[22] = fmaf(po.e2.x, pa.Y2, po.e2.y * pb.Y2);
+          v[23] = fmaf(po.e2.x, pa.Y3, po.e2.y * pb.Y3);
           float2* col = reinterpret_cast<float2*>(red + (lane < 16 ? 2 * lane : RED_HALF + 2 * (lane - 16)));
 #pragma unroll
           for (int q = 0; q < NMOM / 2; ++q) col[q * (RED_ROW / 2)] = make_float2(v[2 * q], v[2 * q + 1]);

@@ -147,12 +147,18 @@ __device__ __forceinline__ bool bwd_pair(BwdPix& A, BwdPix& B, const float4* rec
                                          float gam, PairOut& o, unsigned long long& ntest,
                                          bool count) {
   const bool actA = idx <= A.last, actB = idx <= B.last;
-  if (!(actA || actB)) return false;
+  if (!(actA || actB)) {
+    o = PairOut{};  // zero contributions (the warp's moments may still be formed)
+    return false;
+  }
   if (count) ntest += (unsigned)actA + (unsigned)actB;
   TestOut2 t;
   bool okA = actA, okB = actB;
   ray_peak_test2(rec[0], rec[1], rec[2], rec[3], A.pc, B.pc, cutoff, t, okA, okB);
-  if (!(okA || okB)) return false;
+  if (!(okA || okB)) {
+    o = PairOut{};
+    return false;
+  }
   const F2 alpha = t.alpha, kern = t.kern, araw = t.araw, rD = t.rD, u = t.u, v = t.v;
   const F2 ddy = t.ddy, hy{A.pc.hy, B.pc.hy};
   const float ddx = t.ddx;
@@ -166,7 +172,10 @@ __device__ __forceinline__ bool bwd_pair(BwdPix& A, BwdPix& B, const float4* rec
   const bool satA = okA && A.sat && idx == A.last, satB = okB && B.sat && idx == B.last;
   const bool nA = okA && !satA, nB = okB && !satB;
   const F2 s_0{A.s0, B.s0}, s_1{A.s1, B.s1}, s_2{A.s2, B.s2};
-  F2 ek0{A.ek0, B.ek0}, ek1{A.ek1, B.ek1}, ek2{A.ek2, B.ek2};
+  // E_k (the saturating splat's emission, else the background) comes from
+  // the forward's cache, bit-identical to this entry's emission on the
+  // saturating one (same rounded ops), so no per-entry update is needed
+  const F2 ek0{A.ek0, B.ek0}, ek1{A.ek1, B.ek1}, ek2{A.ek2, B.ek2};
   const F2 sdE = fma2(s_0, sub2(E0, ek0), fma2(s_1, sub2(E1, ek1), mul2(s_2, sub2(E2, ek2))));
   // state in front of splat i, recovered back to front (normal pixels only)
   F2 thi{A.thi, B.thi}, tlo{A.tlo, B.tlo};
@@ -195,14 +204,15 @@ __device__ __forceinline__ bool bwd_pair(BwdPix& A, BwdPix& B, const float4* rec
   }
   if (nA) A.carry = nc.x;
   if (nB) B.carry = nc.y;
-  if (satA) { A.ek0 = E0.x; A.ek1 = E1.x; A.ek2 = E2.x; }
-  if (satB) { B.ek0 = E0.y; B.ek1 = E1.y; B.ek2 = E2.y; }
   // dE = s·w for normal pixels, s·T̄_k for the saturating one
   const F2 wt{satA ? A.tk : wgt.x, satB ? B.tk : wgt.y};
   const F2 dE0 = mul2(s_0, wt), dE1 = mul2(s_1, wt), dE2 = mul2(s_2, wt);
-  const F2 dae{(araw.x >= ALPHA_MAX_F) ? 0.f : da.x, (araw.y >= ALPHA_MAX_F) ? 0.f : da.y};
-  o.dm2 = sel2(nA, nB, mul2(mul2(f2(-0.5f), alpha), dae));
-  o.dak = sel2(nA, nB, mul2(dae, kern));
+  // zero for a clamped alpha (render.py:329) and for a pixel that does not
+  // contribute (kern and alpha are finite there), so dm2 and dak need no mask
+  const F2 dae{(!nA || araw.x >= ALPHA_MAX_F) ? 0.f : da.x,
+               (!nB || araw.y >= ALPHA_MAX_F) ? 0.f : da.y};
+  o.dm2 = mul2(mul2(f2(-0.5f), alpha), dae);
+  o.dak = mul2(dae, kern);
   // whitened peak offset y = B̃ e, e = δ − ε h (bwd_pixel's conic branch)
   const float dxn = ddx * inv_f;
   const F2 dyn = mul2(ddy, f2(inv_f));
@@ -236,6 +246,9 @@ __device__ __forceinline__ void bwd_load(BwdPix& st, const CamDev& cam, int px, 
   st.P = 1.f;
   st.ck = -1;
   st.s0 = st.s1 = st.s2 = 0.f;
+  st.ek0 = bg0;
+  st.ek1 = bg1;
+  st.ek2 = bg2;
   if (px < cam.W && py < cam.H) {
     const int pix = py * cam.W + px;
     st.last = cache.last[pix];
@@ -249,10 +262,10 @@ __device__ __forceinline__ void bwd_load(BwdPix& st, const CamDev& cam, int px, 
     st.s0 = seed[3 * pix + 0];
     st.s1 = seed[3 * pix + 1];
     st.s2 = seed[3 * pix + 2];
+    st.ek0 = cache.e_k[3 * pix + 0];  // saturating splat's emission, else the background
+    st.ek1 = cache.e_k[3 * pix + 1];
+    st.ek2 = cache.e_k[3 * pix + 2];
   }
-  st.ek0 = bg0;
-  st.ek1 = bg1;
-  st.ek2 = bg2;
   st.carry = 0.f;  // Θ (τ-family) or U (P-family), seed-contracted
 }
 
