@@ -419,10 +419,12 @@ def e2e_arm(a, arrs, cams, model, my_views, world, render_with_gradients):
         t = torch.tensor([dt], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dt = float(t.item())
-    P, C = len(arrs), arrs.sh.shape[2]
+    from paper_2603_02887_b200.render import _LAST_IO
     npx = a.width * a.height
-    h2d = len(my_views) * (P * (3 + 3 + 4 + 1 + 3 * C) * 4 + npx * 3 * 4)
-    d2h = len(my_views) * (npx * (3 + 1 + 1) * 8 + P * (3 + 3 + 4 + 1 + 3 * C) * 8)
+    # bytes the API moved per view (fp32 scene + seed up; float64 image,
+    # residual, int64 overdraw and the touched gradient rows down)
+    h2d = len(my_views) * _LAST_IO["h2d"]
+    d2h = len(my_views) * _LAST_IO["d2h"]
     return {"value": round(npx * len(my_views) * world / dt / 1e6, 3), "unit": "Mpix/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "ms_per_step": round(dt * 1e3, 3),

@@ -31,8 +31,10 @@
  *     nxs_forward to nxs_backward of the same view ("settings must match the
  *     forward call", render.py:435-436).  Distinct views are independent and
  *     may be used concurrently on distinct streams.
- *   - Gradients ACCUMULATE (+=) into the caller's buffers, so a rank's views
- *     sum into one buffer before the data-parallel all-reduce.
+ *   - Gradients ACCUMULATE (+=, atomically) into the caller's buffers, so a
+ *     rank's views sum into one buffer before the data-parallel all-reduce;
+ *     views sharing a buffer may run concurrently on distinct streams (the
+ *     float summation order then varies run to run).
  */
 #ifndef NXS_H
 #define NXS_H
@@ -220,6 +222,15 @@ int nxs_binning_export(nxs_view* view, int32_t* rects, int32_t* ranges,
  * ranks of the processed depth phases are defined (NXS_FLAG_FULL_BINNING
  * projects every rank). */
 int nxs_records_export(nxs_view* view, float* records, void* stream);
+
+/* The Gaussians (storage indices, no particular order) whose gradients the
+ * last backward of this view wrote: every other row of its gradient
+ * contribution is zero.  *count (HOST pointer) receives their number; the
+ * call synchronises `stream` to read it.  gids (device, capacity >= the
+ * scene's count, or NULL to query the count only).  Used to move only the
+ * touched gradient rows (render_with_gradients' download, the sparse
+ * data-parallel reduction). */
+int nxs_touched_export(nxs_view* view, int32_t* gids, int64_t* count, void* stream);
 
 /* ---- train-step neighbours ---------------------------- */
 

@@ -44,6 +44,7 @@ SYMBOLS = (
     "nxs_depth_order",
     "nxs_binning_export",
     "nxs_records_export",
+    "nxs_touched_export",
     "nxs_loss_workspace_bytes",
     "nxs_image_loss",
     "nxs_adam_step",
@@ -160,6 +161,7 @@ def lib():
     h.nxs_depth_order.argtypes = [vp, vp, vp]
     h.nxs_binning_export.argtypes = [vp, vp, vp, vp, vp]
     h.nxs_records_export.argtypes = [vp, vp, vp]
+    h.nxs_touched_export.argtypes = [vp, vp, C.POINTER(C.c_int64), vp]
     h.nxs_loss_workspace_bytes.argtypes = [i32, i32]
     h.nxs_loss_workspace_bytes.restype = i64
     h.nxs_image_loss.argtypes = [vp, vp, i32, i32, C.c_double, i32, vp, vp, vp, vp]
@@ -277,6 +279,13 @@ class View:
 
     def records_export(self, out, stream=None):
         _check(self._h.nxs_records_export(self._p, _ptr(out), _stream_ptr(stream)))
+
+    def touched_export(self, out=None, stream=None) -> int:
+        """Gaussians the last backward wrote (into ``out``, int32 CUDA with
+        capacity >= the scene count, unless None); returns their number."""
+        n = C.c_int64(0)
+        _check(self._h.nxs_touched_export(self._p, _ptr(out), C.byref(n), _stream_ptr(stream)))
+        return int(n.value)
 
     def stats(self) -> dict:
         st = Stats()

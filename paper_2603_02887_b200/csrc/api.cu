@@ -125,7 +125,8 @@ void launch_blend_bwd(bool, int, const float4*, const float4*, const PhaseLists&
                       const ModelDev&, float, double, const float*, const float*,
                       const PixCache&, double*, uint8_t*, Counters*, cudaStream_t);
 void launch_chain(const float*, const float*, int, int64_t, const uint32_t*, double*, uint8_t*,
-                  float*, float*, float*, float*, float*, cudaStream_t);
+                  float*, float*, float*, float*, float*, uint32_t*, unsigned long long*,
+                  cudaStream_t);
 }  // namespace nxs
 
 using namespace nxs;
@@ -223,6 +224,8 @@ struct nxs_view {
   Buf c_last, c_sat, c_tk, c_thi, c_tlo, c_P, c_ck, c_Pck, c_ek, c_th0;
   Buf r_rad, r_trem, r_count, r_sea, r_sa;
   Buf temp, dev_small;  // CUB temp; counters
+  Buf tlist, tcount;     // Gaussians the last backward's chain wrote, and their number
+  bool tlist_valid = false;
   unsigned long long* host_small = nullptr;  // pinned
   // phase events: see NXS_PHASES in include/nxs.h
   cudaEvent_t ev[NXS_PHASES + 2] = {};
@@ -282,7 +285,7 @@ struct nxs_view {
                   &ph_sel,   &tq,      &zlo64,  &xc_t, &xc_r, &xc_n,
                   &c_last,   &c_sat,     &c_tk,    &c_thi,   &c_tlo,   &c_P,    &c_ck,
                   &c_Pck,    &c_ek,      &c_th0,   &r_rad,   &r_trem,  &r_count, &r_sea,
-                  &r_sa,     &temp,      &dev_small};
+                  &r_sa,     &temp,      &dev_small, &tlist, &tcount};
     for (Buf* b : all) f(*b);
     for (int p = 0; p < MAX_PHASES; ++p) {
       f(pv_ph[p]);
@@ -1483,6 +1486,7 @@ retry_sort:
   }
 
   v->have_fwd = true;
+  v->tlist_valid = false;
   v->cam = cam;
   v->model = md;
   v->opts = *opts;
@@ -1548,12 +1552,19 @@ int backward_blend(nxs_view* v, const float* seed, cudaStream_t s) {
 int backward_chain(nxs_view* v, const nxs_scene* scene, float* g_centers, float* g_scales,
                    float* g_quats, float* g_opacities, float* g_sh, cudaStream_t s) {
   // (the backward touches only processed ranks: [0, proj_end))
+  if (g_centers) {
+    NXS_CUDA(ensure_n<uint32_t>(v->tlist, std::max<int64_t>(v->P, 1)));
+    NXS_CUDA(v->tcount.ensure(sizeof(unsigned long long)));
+    NXS_CUDA(cudaMemsetAsync(v->tcount.p, 0, sizeof(unsigned long long), s));
+  }
   launch_chain(scene->scales, scene->quats, v->C,
                v->proj_end > 0 ? std::min(v->proj_end, v->P) : v->P, v->idx_out.as<uint32_t>(),
                v->moments.as<double>(), v->touched.as<uint8_t>(), g_centers, g_scales, g_quats,
-               g_opacities, g_sh, s);
+               g_opacities, g_sh, g_centers ? v->tlist.as<uint32_t>() : nullptr,
+               g_centers ? v->tcount.as<unsigned long long>() : nullptr, s);
   NXS_LAUNCHED("chain");
   if (!g_centers) return NXS_OK;
+  v->tlist_valid = true;
   mark(v, 11, s);
   v->ev_bwd = true;
   const bool count = (v->opts.flags & NXS_FLAG_COUNT_EVENTS) != 0;
@@ -1772,6 +1783,19 @@ int nxs_binning_export(nxs_view* v, int32_t* rects, int32_t* ranges, int32_t* pa
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // (off[] is host memory)
   if (e != cudaSuccess) return fail(NXS_ERR_CUDA, std::string("binning export: ") +
                                                       cudaGetErrorString(e));
+  return NXS_OK;
+}
+
+int nxs_touched_export(nxs_view* v, int32_t* gids, int64_t* count, void* stream_) {
+  if (!v || !count) return fail(NXS_ERR_INVALID, "null argument");
+  if (!v->tlist_valid) return fail(NXS_ERR_STATE, "no backward recorded in this view");
+  cudaStream_t s = (cudaStream_t)stream_;
+  unsigned long long n = 0;
+  NXS_CUDA(cudaMemcpyAsync(&n, v->tcount.p, sizeof(n), cudaMemcpyDeviceToHost, s));
+  NXS_CUDA(cudaStreamSynchronize(s));
+  *count = (int64_t)n;
+  if (gids && n)
+    NXS_CUDA(cudaMemcpyAsync(gids, v->tlist.p, (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
   return NXS_OK;
 }
 

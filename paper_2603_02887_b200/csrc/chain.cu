@@ -25,7 +25,8 @@ __global__ void k_chain(const float* __restrict__ scales, const float* __restric
                         double* __restrict__ moments, uint8_t* __restrict__ touched,
                         float* __restrict__ g_centers,
                         float* __restrict__ g_scales, float* __restrict__ g_quats,
-                        float* __restrict__ g_opac, float* __restrict__ g_sh) {
+                        float* __restrict__ g_opac, float* __restrict__ g_sh,
+                        uint32_t* __restrict__ tlist, unsigned long long* __restrict__ tcount) {
   int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= P || !touched[r]) return;
   // read this rank's moments and leave the buffer zeroed for the next backward
@@ -39,11 +40,15 @@ __global__ void k_chain(const float* __restrict__ scales, const float* __restric
   touched[r] = 0;
   if (!g_centers) return;  // clear only (a discarded speculative backward)
   const int64_t g = order[r];
+  // the Gaussians this backward wrote (any order): the touched-row export
+  if (tlist) tlist[atomicAdd(tcount, 1ull)] = (uint32_t)g;
 
+  // Gradients accumulate atomically: views sharing one gradient buffer may
+  // run their chains concurrently on different streams (include/nxs.h).
   // opacity and SH need no geometry
-  g_opac[g] += (float)mv[11];
+  atomicAdd(g_opac + g, (float)mv[11]);
   for (int c = 0; c < 3; ++c)
-    for (int k = 0; k < C; ++k) g_sh[(g * 3 + c) * C + k] += (float)mv[12 + 4 * c + k];
+    for (int k = 0; k < C; ++k) atomicAdd(g_sh + (g * 3 + c) * C + k, (float)mv[12 + 4 * c + k]);
 
   bool geo = false;
 #pragma unroll
@@ -67,9 +72,10 @@ __global__ void k_chain(const float* __restrict__ scales, const float* __restric
 
   const double LV[3] = {L[0] * V[0], L[1] * V[1], L[2] * V[2]};
   for (int i = 0; i < 3; ++i)
-    g_centers[3 * g + i] +=
-        (float)(-2.0 * (R[3 * i + 0] * LV[0] + R[3 * i + 1] * LV[1] + R[3 * i + 2] * LV[2]));
-  for (int k = 0; k < 3; ++k) g_scales[3 * g + k] += (float)(-2.0 * U[4 * k] / (s[k] * s[k] * s[k]));
+    atomicAdd(g_centers + 3 * g + i,
+              (float)(-2.0 * (R[3 * i + 0] * LV[0] + R[3 * i + 1] * LV[1] + R[3 * i + 2] * LV[2])));
+  for (int k = 0; k < 3; ++k)
+    atomicAdd(g_scales + 3 * g + k, (float)(-2.0 * U[4 * k] / (s[k] * s[k] * s[k])));
 
   double gq[4];
   for (int k = 0; k < 4; ++k) {
@@ -96,20 +102,22 @@ __global__ void k_chain(const float* __restrict__ scales, const float* __restric
     gq[k] = 2.0 * acc;
   }
   const double dot = w * gq[0] + x * gq[1] + y * gq[2] + z * gq[3];
-  g_quats[4 * g + 0] += (float)(gq[0] - w * dot);
-  g_quats[4 * g + 1] += (float)(gq[1] - x * dot);
-  g_quats[4 * g + 2] += (float)(gq[2] - y * dot);
-  g_quats[4 * g + 3] += (float)(gq[3] - z * dot);
+  atomicAdd(g_quats + 4 * g + 0, (float)(gq[0] - w * dot));
+  atomicAdd(g_quats + 4 * g + 1, (float)(gq[1] - x * dot));
+  atomicAdd(g_quats + 4 * g + 2, (float)(gq[2] - y * dot));
+  atomicAdd(g_quats + 4 * g + 3, (float)(gq[3] - z * dot));
 }
 
 void launch_chain(const float* scales, const float* quats, int C, int64_t P, const uint32_t* order,
                   double* moments, uint8_t* touched, float* g_centers, float* g_scales,
-                  float* g_quats, float* g_opac, float* g_sh, cudaStream_t s) {
+                  float* g_quats, float* g_opac, float* g_sh, uint32_t* tlist,
+                  unsigned long long* tcount, cudaStream_t s) {
   if (P == 0) return;
   // touched ranks lie below the processed ranks (P here): small blocks
   // spread their fp64 work over every SM
   k_chain<<<(unsigned)((P + 63) / 64), 64, 0, s>>>(scales, quats, C, P, order, moments, touched,
-                                                    g_centers, g_scales, g_quats, g_opac, g_sh);
+                                                    g_centers, g_scales, g_quats, g_opac, g_sh,
+                                                    tlist, tcount);
 }
 
 }  // namespace nxs

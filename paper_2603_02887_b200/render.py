@@ -576,6 +576,10 @@ def render_backward(arrs, camera, model, background, cache, seed_image, *,
     return dict(zip(g.keys(), dl.result()))
 
 
+# bytes moved by the last render_with_gradients call (instrumentation, bench.py)
+_LAST_IO: dict = {}
+
+
 def render_with_gradients(arrs, camera, model, background, seed_image, *,
                           max_splats: int = 128, alpha_cutoff: float = DEFAULT_ALPHA_CUTOFF,
                           near: float = NEAR_PLANE, chunk_size: int | None = None):
@@ -604,11 +608,20 @@ def render_with_gradients(arrs, camera, model, background, seed_image, *,
         dl = _Download()
         for t, k in zip(out, ("rgb", "overdraw", "residual")):
             dl.add(t, k)
+        # Every gradient row travels, widened to float64 on the device, into
+        # recycled page-locked arrays.  Moving only the touched rows (~3 % at
+        # C3, nxs_touched_export) was measured slower: the dense float64
+        # arrays must then be zero-filled on the host, 184 MB at ~10 ms, vs
+        # ~3.4 ms of DMA (profiles/r02_e2e_probe.txt).
         for k, v in grads.items():
             dl.add(v, "g_" + k)
         res = dl.result()
         result = RenderResult(*res[:3])
         g = dict(zip(grads.keys(), res[3:]))
+        _LAST_IO.update(d2h=H * W * 5 * 8 + sum(v.numel() for v in grads.values()) * 8)
+        _LAST_IO.update(h2d=sum(int(np.prod(np.shape(getattr(arrs, f)))) * 4
+                                for f in DeviceScene.FIELDS) + H * W * 3 * 4
+                        if not isinstance(arrs, DeviceScene) else H * W * 3 * 4)
     finally:
         _release_view(view)
     return result, g

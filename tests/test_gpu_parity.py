@@ -731,3 +731,32 @@ def test_binning_export_after_warm_calls_is_compact():
         views.append((r, p[:r[-1, 1]]))
     np.testing.assert_array_equal(views[0][0], views[1][0])
     np.testing.assert_array_equal(views[0][1], views[1][1])
+
+
+def test_touched_export_covers_the_gradient_rows():
+    """nxs_touched_export lists every Gaussian with a non-zero gradient row
+    (and only rows the backward wrote); the numpy API's float64 gradients
+    equal the device gradients of the same call."""
+    import torch
+    import paper_2603_02887_b200 as nx
+    from paper_2603_02887_b200 import _native, forward_backward_device
+    sc = O.round_scene_f32(O.canonical_scene(60_000, seed=4))
+    cam = O.canonical_camera(320, 240, 2, 8)
+    seed = O.canonical_seed(320, 240, 2)
+    arrs = nx.SceneArrays(sc.centers, sc.scales, sc.quats, sc.opacities, sc.sh)
+    for name in ("softplus_20", "exponential"):
+        res, g = nx.render_with_gradients(arrs, cam, MODELS[name], np.zeros(3), seed,
+                                          chunk_size=1)
+        dev = _dev(sc)
+        view = _native.View()
+        out, gd = forward_backward_device(view, dev, cam, MODELS[name], np.zeros(3),
+                                          torch.as_tensor(seed, dtype=torch.float32).cuda())
+        n = view.touched_export()
+        nz = int((gd["opacities"] != 0).sum())
+        assert 0 < nz <= n < len(sc)
+        np.testing.assert_array_equal(res.rgb, out[0].double().cpu().numpy())
+        for k in GRAD_FIELDS:
+            ref = gd[k].double().cpu().numpy()
+            assert g[k].shape == ref.shape and g[k].dtype == np.float64
+            # (fp64 moment atomics: the summation order differs between calls)
+            np.testing.assert_allclose(g[k], ref, rtol=1e-5, atol=1e-6 * np.abs(ref).max())
