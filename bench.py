@@ -16,9 +16,10 @@ e2e   : the same metric through the public drop-in API
         the timed region.
 roofline: for the kernel with the largest share of the step, measured live
         (per-phase CUDA events, include/nxs.h nxs_view_timings).
-cpu_baseline: the CPU oracle port (oracle/splat_oracle.py, brute force over
-        all Gaussians per pixel like the reference) on a bounded pixel sample,
-        all host cores, rank 0 only.
+cpu_baseline: the stock reference (nexsplat from baseline/_ref, its own
+        _forward_sweep/_backward_sweep) on runs of consecutive pixels of the
+        same view, all host cores, rank 0 only (forward-only for models the
+        reference has no backward for, and labelled so).
 --impl reference: times that CPU implementation as the reference arm.
 """
 from __future__ import annotations
@@ -59,7 +60,6 @@ def parse():
     p.add_argument("--param", type=float, default=None)
     p.add_argument("--views-per-rank", type=int, default=1)
     p.add_argument("--e2e-steps", type=int, default=5)
-    p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--chunk", default="1",
@@ -79,57 +79,153 @@ def model_of(a):
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline: the oracle port on a bounded sample (rank 0)
+# CPU baseline / reference arm: the reference's own implementation of the
+# path, timed on a bounded sample (rank 0)
 # ---------------------------------------------------------------------------
+# The stock reference package (pip-installed from /root/reference into
+# baseline/_ref, which travels to the GPU box) is imported and its own sweep
+# functions — nexsplat.render._forward_sweep / _backward_sweep, the body of
+# render_with_gradients (reference render.py:147-347, 445-464) with the
+# chunk_size=1 order of _depth_chunks (render.py:350-358) — run on contiguous
+# runs of pixels of the C3 view, one run per worker process, all host cores.
+# A run of pixels is the unit the reference itself vectorises over (its
+# render() splits the image into row bands per thread, render.py:394-400).
+# The reference has no softplus/blended backward (render.py:229-231): for
+# those models the sample is forward-only and says so.  Without
+# baseline/_ref the oracle port (oracle/splat_oracle.py, brute force over all
+# Gaussians per pixel, slower than the reference) is timed and labelled.
 
+REF_DIR = ROOT / "baseline" / "_ref"
 _CPU = {}
 
 
-def _cpu_worker(args):
-    wid, budget = args
-    from oracle import splat_oracle as O
-    sc, cam, model, seed = _CPU["sc"], _CPU["cam"], _CPU["model"], _CPU["seed"]
-    rng = np.random.default_rng(100 + wid)
-    t0 = time.perf_counter()
-    done = 0
-    while time.perf_counter() - t0 < budget or done == 0:
-        px = rng.choice(cam.width * cam.height, 1, replace=False)
-        fwd = O.forward(sc, cam, model, np.zeros(3), chunk_size=1, pixels=px, prune=False,
-                        keep_state=True)
-        O.backward(sc, cam, model, np.zeros(3), fwd, seed.reshape(-1, 3)[px])
-        done += 1
-    return done, time.perf_counter() - t0
+def _ref_modules():
+    """(render module, Camera, TransmittanceModel) of the stock reference, or None."""
+    if not (REF_DIR / "nexsplat").is_dir():
+        return None
+    if str(REF_DIR) not in sys.path:
+        sys.path.insert(0, str(REF_DIR))
+    import importlib
+    try:
+        R = importlib.import_module("nexsplat.render")
+        prim = importlib.import_module("nexsplat.primitives")
+        tm = importlib.import_module("nexsplat.transmittance")
+    except Exception:
+        return None
+    return R, prim.Camera, tm.TransmittanceModel
 
 
-def cpu_baseline(arrs, cam, model, seconds):
-    import multiprocessing as mp
-    from oracle import splat_oracle as O
-    _CPU.update(sc=O.Scene.of(arrs), cam=cam, model=model,
-                seed=np.random.default_rng(1000).uniform(0.2, 1.0, (cam.height, cam.width, 3)))
-    cores = os.cpu_count() or 1
-    workers = max(1, min(cores, 32))
-    # each worker holds ~1M x a few float64 temporaries per pixel
-    try:
-        import psutil
-        mem = psutil.virtual_memory().available
-        workers = max(1, min(workers, int(mem / 3.0e9)))
-    except Exception:
-        pass
-    ctx = mp.get_context("fork")
+def _ref_setup(a, model):
+    """Scene, camera, order chunks and seeds, built once before the workers fork."""
+    from paper_2603_02887_b200.scenes import canonical_scene
+    mods = _ref_modules()
+    arrs = canonical_scene(a.gaussians, seed=5)
+    seed = np.random.default_rng(1000).uniform(0.2, 1.0, (a.height * a.width, 3))
+    if mods is not None:
+        R, Camera, TM = mods
+        sc = R.SceneArrays(arrs.centers, arrs.scales, arrs.quats, arrs.opacities, arrs.sh)
+        cam = Camera.from_look_at([0.0, 0.0, 0.0], [0.0, 0.0, 3.5], [0.0, 1.0, 0.0], 55.0,
+                                  a.width, a.height)
+        m = TM(model.variant, float(model.param))
+        chunk = 1 if a.chunk_size is None else a.chunk_size
+        chunks = R._depth_chunks(sc, cam, None if a.chunk_size is None else chunk)
+        bwd = m.variant in ("linear", "quadratic", "exponential")
+        _CPU.update(kind="reference", R=R, sc=sc, cam=cam, model=m, chunks=chunks, bwd=bwd,
+                    dirs=cam.pixel_directions().reshape(-1, 3), seed=seed)
+    else:
+        from oracle import splat_oracle as O
+        from paper_2603_02887_b200.scenes import canonical_camera
+        _CPU.update(kind="port", sc=O.Scene.of(arrs), cam=canonical_camera(a.width, a.height),
+                    model=model, seed=seed, bwd=True, chunk_size=a.chunk_size)
+
+
+def _cpu_task(args):
+    """One run of `npx` consecutive pixels from flat index `start`: forward
+    (+ backward where the reference has one).  Returns (pixels, seconds)."""
+    start, npx = args
+    px = np.arange(start, start + npx)
     t0 = time.perf_counter()
-    with ctx.Pool(workers) as pool:
-        res = pool.map(_cpu_worker, [(i, seconds) for i in range(workers)])
-    wall = time.perf_counter() - t0
-    px = sum(r[0] for r in res)
+    if _CPU["kind"] == "reference":
+        R, cam = _CPU["R"], _CPU["cam"]
+        fwd = R._forward_sweep(_CPU["sc"], _CPU["dirs"][px], cam.position, _CPU["model"],
+                               np.zeros(3), 128, 1.0 / 255.0, 1e-4, _CPU["chunks"])
+        if _CPU["bwd"]:
+            R._backward_sweep(_CPU["sc"], _CPU["dirs"][px], cam.position, _CPU["model"],
+                              np.zeros(3), 128, 1.0 / 255.0, 1e-4, _CPU["chunks"], fwd,
+                              _CPU["seed"][px])
+    else:
+        from oracle import splat_oracle as O
+        fwd = O.forward(_CPU["sc"], _CPU["cam"], _CPU["model"], np.zeros(3),
+                        chunk_size=_CPU["chunk_size"], pixels=px, prune=False, keep_state=True,
+                        batch=npx)
+        O.backward(_CPU["sc"], _CPU["cam"], _CPU["model"], np.zeros(3), fwd, _CPU["seed"][px])
+    return npx, time.perf_counter() - t0
+
+
+class CpuRunner:
+    """A pool of worker processes over all host cores (forked after setup)."""
+
+    def __init__(self, a, model):
+        import multiprocessing as mp
+        _ref_setup(a, model)
+        cores = os.cpu_count() or 1
+        workers = cores
+        try:  # each worker ends up with its own copy of the scene and chunk list
+            import psutil
+            workers = max(1, min(workers, int(psutil.virtual_memory().available / 1.5e9)))
+        except Exception:
+            pass
+        self.workers = workers
+        self.npix = a.width * a.height
+        self.pool = mp.get_context("fork").Pool(workers)
+        self.rng = np.random.default_rng(7)
+
+    def step(self, npx):
+        """Every worker renders one run of npx pixels; (pixels, wall seconds)."""
+        starts = self.rng.integers(0, self.npix - npx, self.workers)
+        t0 = time.perf_counter()
+        res = self.pool.map(_cpu_task, [(int(s0), npx) for s0 in starts], chunksize=1)
+        return sum(r[0] for r in res), time.perf_counter() - t0
+
+    def describe(self, npx, n_steps):
+        try:
+            cpu = subprocess.run(["lscpu"], capture_output=True, text=True).stdout
+            name = [ln.split(":", 1)[1].strip() for ln in cpu.splitlines()
+                    if "Model name" in ln][0]
+        except Exception:
+            name = "unknown"
+        if _CPU["kind"] == "reference":
+            what = ("stock reference nexsplat (baseline/_ref) _forward_sweep"
+                    + (" + _backward_sweep" if _CPU["bwd"] else
+                       " only: the reference has no backward for this model "
+                       "(render.py:229-231), so its line is FORWARD-ONLY Mpix/s"))
+        else:
+            what = ("oracle port (oracle/splat_oracle.py) fwd+bwd, brute force over all "
+                    "Gaussians per pixel: slower than the reference (no early exit), "
+                    "baseline/_ref missing")
+        return (f"{what}; {n_steps} step(s) x {self.workers} processes x {npx} consecutive "
+                f"pixels at random positions of the view; {name}")
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+
+def _ref_npx(steps):
+    """Pixels per worker task: ~7 s tasks for short runs, smaller for long ones
+    (the reference arm must finish within a few minutes)."""
+    return int(max(256, min(1024, 1024 * 25 // max(1, steps))))
+
+
+def cpu_baseline(a, model):
+    r = CpuRunner(a, model)
     try:
-        cpu = subprocess.run(["lscpu"], capture_output=True, text=True).stdout
-        name = [ln.split(":", 1)[1].strip() for ln in cpu.splitlines() if "Model name" in ln][0]
-    except Exception:
-        name = "unknown"
-    return {"value": px / wall / 1e6, "unit": "Mpix/s", "cores": workers, "kind": "port",
-            "sample": f"{px} random pixels of the same 1M-Gaussian view, fwd+bwd, brute force "
-                      f"over all Gaussians per pixel (reference algorithm, oracle/splat_oracle.py"
-                      f"), {workers} processes x ~{seconds:.0f}s on {name}; wall {wall:.1f}s"}
+        npx = _ref_npx(1)
+        px, wall = r.step(npx)
+        return {"value": px / wall / 1e6, "unit": "Mpix/s", "cores": r.workers,
+                "kind": _CPU["kind"], "sample": r.describe(npx, 1) + f"; wall {wall:.1f}s"}
+    finally:
+        r.close()
 
 
 # ---------------------------------------------------------------------------
@@ -282,7 +378,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        cpu = cpu_baseline(arrs, cams[0], model, a.cpu_seconds)
+        cpu = cpu_baseline(a, model)
 
     if rank == 0:
         out = {
@@ -298,21 +394,7 @@ def main():
             "vs_baseline": None,
             "dtype": "f32",
             "data": "synthetic",
-            "config": {
-                "workload": (("C3: " if (a.gaussians, W, H) == (1_000_000, 1920, 1080) else
-                              "C5-like: " if a.gaussians >= 5_000_000 else "custom: ")
-                             + f"{a.gaussians} Gaussians (canonical synthetic scene, seed 5), "
-                             f"{W}x{H}, {model.describe()}, "
-                             + ("chunk_size=1 (global depth order), " if a.chunk_size == 1 else
-                                "chunk_size=None (exact per-pixel order), " if a.chunk_size is None
-                                else f"chunk_size={a.chunk_size} (chunked order), ")
-                             + f"fwd+bwd, {vpr} view(s) per GPU"
-                             + (", NCCL all-reduce of gradients" if world > 1 else "")),
-                "gaussians": a.gaussians, "width": W, "height": H,
-                "views_per_gpu": vpr, "total_views": n_views,
-                "parallelism": f"dp{world} over views",
-                "l2": "inputs larger than L2 (records 128 MB + pairs + 192 MB moments per view)",
-            },
+            "config": config_of(a, model, vpr, world),
             "phase_ms": {k: round(v, 4) for k, v in phase.items()},
             "depth_phases": n_depth_phases,
             "events": {k: st[k] for k in ("n_pairs", "n_tests_fwd", "n_composited",
@@ -326,6 +408,26 @@ def main():
         print(json.dumps(out))
     if world > 1:
         dist.destroy_process_group()
+
+
+def config_of(a, model, vpr, world):
+    """The workload description, identical in both arms (same_config)."""
+    W, H = a.width, a.height
+    n_views = vpr * world
+    return {
+        "workload": (("C3: " if (a.gaussians, W, H) == (1_000_000, 1920, 1080) else
+                      "C5-like: " if a.gaussians >= 5_000_000 else "custom: ")
+                     + f"{a.gaussians} Gaussians (canonical synthetic scene, seed 5), "
+                     f"{W}x{H}, {model.describe()}, "
+                     + ("chunk_size=1 (global depth order), " if a.chunk_size == 1 else
+                        "chunk_size=None (exact per-pixel order), " if a.chunk_size is None
+                        else f"chunk_size={a.chunk_size} (chunked order), ")
+                     + f"fwd+bwd, {vpr} view(s) per GPU"),
+        "gaussians": a.gaussians, "width": W, "height": H,
+        "views_per_gpu": vpr, "total_views": n_views,
+        "parallelism": f"dp{world} over views",
+        "l2": "inputs larger than L2 (records 128 MB + pairs + 192 MB moments per view)",
+    }
 
 
 def roofline(a, model, phase, st):
@@ -432,21 +534,23 @@ def e2e_arm(a, arrs, cams, model, my_views, world, render_with_gradients):
 
 
 def reference_arm(a, rank, model):
-    """The reference's CPU implementation of the path (oracle port, the
-    reference is not installed on the GPU box), rank 0 only."""
+    """The reference's own CPU implementation of the path (the stock package
+    from baseline/_ref, see the CPU-baseline section), rank 0 only, all host
+    cores; each step every worker renders one run of pixels."""
     if rank != 0:
         return
-    from paper_2603_02887_b200.scenes import canonical_camera, canonical_scene
-    arrs = canonical_scene(a.gaussians, seed=5)
-    cam = canonical_camera(a.width, a.height)
-    per_step = max(2.0, min(20.0, 150.0 / max(1, a.steps + a.warmup)))
+    r = CpuRunner(a, model)
+    npx = _ref_npx(a.steps + a.warmup)
     vals = []
-    last = None
-    for i in range(a.warmup + a.steps):
-        last = cpu_baseline(arrs, cam, model, per_step)
-        if i >= a.warmup:
-            vals.append(last["value"])
-    v = statistics.median(vals) if vals else last["value"]
+    try:
+        for i in range(a.warmup + a.steps):
+            px, wall = r.step(npx)
+            if i >= a.warmup:
+                vals.append(px / wall / 1e6)
+        sample = r.describe(npx, a.steps)
+    finally:
+        r.close()
+    v = statistics.median(vals)
     out = {
         "impl": "reference",
         "metric": METRIC,
@@ -458,9 +562,9 @@ def reference_arm(a, rank, model):
         "higher_is_better": True,
         "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": f"C3: {a.gaussians} Gaussians, {a.width}x{a.height}, "
-                               f"{model.describe()}, chunk_size=1, fwd+bwd (sampled pixels)"},
-        "cpu_baseline": dict(last, value=v),
+        "config": config_of(a, model, a.views_per_rank, int(os.environ.get("WORLD_SIZE", "1"))),
+        "cpu_baseline": {"value": v, "unit": "Mpix/s", "cores": r.workers, "kind": _CPU["kind"],
+                         "sample": sample},
         "e2e": {"value": v, "unit": "Mpix/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out))
