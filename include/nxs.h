@@ -24,13 +24,21 @@
  *   - All array pointers are DEVICE pointers (cudaMalloc / torch CUDA
  *     tensors) unless stated; the caller owns them.  Work is enqueued on
  *     `stream` (a cudaStream_t, NULL = legacy default stream).
- *   - nxs_forward synchronises `stream` once, to read the number of
- *     (tile, Gaussian) pairs it must sort; everything else is asynchronous.
- *   - A view (nxs_view) owns the per-view device workspace: projected
- *     records, tile lists and the per-pixel replay cache.  It persists from
- *     nxs_forward to nxs_backward of the same view ("settings must match the
- *     forward call", render.py:435-436).  Distinct views are independent and
- *     may be used concurrently on distinct streams.
+ *   - Host waits: a view's first call (and any call whose sizes outgrow the
+ *     previous one) reads phase and pair counts from the device between
+ *     kernels; from the second call on, the first depth phase is sized from
+ *     the view's history and runs without a host sync (its check is read
+ *     behind the forward).  nxs_forward_backward returns once that check
+ *     has been read; the waits poll an event (yielding the host thread).
+ *   - A view (nxs_view) owns the per-view device workspace (projected
+ *     records, tile lists, the per-pixel replay cache), allocated by the
+ *     library with cudaMalloc on the device that was current at
+ *     nxs_view_create; every call on the view makes that device current and
+ *     restores the caller's.  It persists from nxs_forward to nxs_backward
+ *     of the same view ("settings must match the forward call",
+ *     render.py:435-436).  Distinct views are independent and may be used
+ *     concurrently on distinct streams; nxs_view_destroy waits for the
+ *     view's device to drain.
  *   - Gradients ACCUMULATE (+=, atomically) into the caller's buffers, so a
  *     rank's views sum into one buffer before the data-parallel all-reduce;
  *     views sharing a buffer may run concurrently on distinct streams (the

@@ -19,6 +19,7 @@
 #include <string>
 #include <vector>
 #include <chrono>
+#include <thread>
 
 // NXS_HOST_TIMING=1: host-side time between points of one fused call,
 // printed to stderr (diagnostics only)
@@ -267,6 +268,12 @@ struct nxs_view {
   // small device->host reads that must not sit between two pipeline kernels
   // run on this stream, ordered after the work they read by ev_side
   cudaStream_t copy_stream = nullptr;
+  // first-phase hint: host_small[30] lands behind a forward on the side
+  // stream; the planner uses it only once ev_hint reports the copy complete
+  cudaEvent_t ev_hint = nullptr;
+  bool hint_pending = false;
+  unsigned long long hint = 0;
+  int device = 0;  // the CUDA device this view's workspace lives on
   cudaEvent_t ev_side = nullptr;
   bool capturing = false;
   int n_phases_plan = 0;       // planned depth phases of the last forward
@@ -304,6 +311,7 @@ struct nxs_view {
     if (gexec) cudaGraphExecDestroy(gexec);
     if (cap_stream) cudaStreamDestroy(cap_stream);
     if (copy_stream) cudaStreamDestroy(copy_stream);
+    if (ev_hint) cudaEventDestroy(ev_hint);
     if (ev_side) cudaEventDestroy(ev_side);
     if (ev_ok) {
       for (auto& e : ev) cudaEventDestroy(e);
@@ -407,6 +415,21 @@ struct CaptureGuard {
   }
 };
 
+// Makes the view's device current for the duration of a call (a view's
+// workspace, events and graph belong to the device it was created on) and
+// restores the caller's device afterwards.
+struct DevGuard {
+  int prev = -1;
+  explicit DevGuard(int dev) {
+    int cur = 0;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != dev && cudaSetDevice(dev) == cudaSuccess)
+      prev = cur;
+  }
+  ~DevGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 // Wait for the stream by polling an event: the syncs inside the pipeline
 // (pair counts, phase sizes) sit between kernels, and a blocking wait's
 // wake-up latency would leave the GPU idle; fall back to blocking if no
@@ -415,8 +438,7 @@ cudaError_t spin_sync(nxs_view* v, cudaStream_t s) {
   if (!v->ev_sync) return cudaStreamSynchronize(s);
   cudaError_t e = cudaEventRecord(v->ev_sync, s);
   if (e != cudaSuccess) return e;
-  while ((e = cudaEventQuery(v->ev_sync)) == cudaErrorNotReady) {
-  }
+  while ((e = cudaEventQuery(v->ev_sync)) == cudaErrorNotReady) std::this_thread::yield();
   return e;
 }
 
@@ -529,6 +551,7 @@ int nxs_view_create(nxs_view** out) {
     return fail(NXS_ERR_CUDA, "cudaHostAlloc failed (no CUDA device?)");
   }
   std::memset(v->host_small, 0, 32 * sizeof(unsigned long long));
+  cudaGetDevice(&v->device);
   v->ev_ok = true;
   for (auto& e : v->ev) v->ev_ok = v->ev_ok && cudaEventCreate(&e) == cudaSuccess;
   for (auto& row : v->evp)
@@ -540,6 +563,8 @@ int nxs_view_create(nxs_view** out) {
 }
 
 int nxs_view_destroy(nxs_view* view) {
+  if (!view) return NXS_OK;
+  DevGuard dg(view->device);
   delete view;
   return NXS_OK;
 }
@@ -616,8 +641,7 @@ int enqueue_async_check(nxs_view* v, int n_ph, cudaStream_t s) {
 
 int finish_async_check(nxs_view* v, bool& ok) {
   cudaError_t e;
-  while ((e = cudaEventQuery(v->ev_sync)) == cudaErrorNotReady) {
-  }
+  while ((e = cudaEventQuery(v->ev_sync)) == cudaErrorNotReady) std::this_thread::yield();
   NXS_CUDA(e);
   const int64_t n0 = (int64_t)(int)(uint32_t)v->host_small[24];
   const uint64_t pairs = v->host_small[26];
@@ -648,6 +672,7 @@ int forward_impl(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
   if (!v || !scene || !camera || !model || !opts || !background || !rgb || !overdraw ||
       !residual)
     return fail(NXS_ERR_INVALID, "null argument");
+  DevGuard dg(v->device);
   cudaStream_t s = (cudaStream_t)stream_;
   v->have_fwd = false;
   v->spec_pending = false;
@@ -754,7 +779,11 @@ int forward_impl(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
       // a first phase covering it (plus headroom) avoids a second phase, and
       // one no larger spares sorting, projecting and binning ranks no tile reads.
       // The hint only moves phase boundaries, never the result.
-      const int64_t need = (int64_t)v->host_small[30];
+      if (v->hint_pending && v->ev_hint && cudaEventQuery(v->ev_hint) == cudaSuccess) {
+        v->hint = v->host_small[30];
+        v->hint_pending = false;
+      }
+      const int64_t need = (int64_t)v->hint;
       if (need > 0 && need < P) {
         const int64_t target = need + 1 + need / 16 + 1024;
         r1 = need < r1 ? std::min(r1, target) : target;
@@ -796,7 +825,7 @@ int forward_impl(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
   if (std::getenv("NXS_DEBUG_PLAN"))
     std::fprintf(stderr, "plan P=%lld n_ph=%d R1=%lld async0=%d est_n0=%lld est_bin0=%d hint=%llu\n",
                  (long long)P, n_ph, (long long)R[1], (int)async0, (long long)v->est_n0,
-                 v->est_bin0, (unsigned long long)v->host_small[30]);
+                 v->est_bin0, (unsigned long long)v->hint);
   int64_t proc_end = 0;  // chunked lazy phases: ranks [0, proc_end) are processed
   bool phase_full[MAX_PHASES] = {false, false, false, false};  // lazy phase sorted on 32 bits
   int phase_shift[MAX_PHASES] = {0, 0, 0, 0};
@@ -1455,6 +1484,9 @@ retry_sort:
     NXS_CUDA(side_after(v, s, cs));
     NXS_CUDA(cudaMemcpyAsync(v->host_small + 30, dsmall + 12, sizeof(unsigned long long),
                              cudaMemcpyDeviceToHost, cs));
+    if (!v->ev_hint) NXS_CUDA(cudaEventCreateWithFlags(&v->ev_hint, cudaEventDisableTiming));
+    NXS_CUDA(cudaEventRecord(v->ev_hint, cs));
+    v->hint_pending = true;
   }
   v->ev_fwd = true;
   v->ev_bwd = false;
@@ -1594,6 +1626,8 @@ extern "C" {
 
 int nxs_backward(nxs_view* v, const nxs_scene* scene, const float* seed, float* g_centers,
                  float* g_scales, float* g_quats, float* g_opacities, float* g_sh, void* stream_) {
+  if (!v) return fail(NXS_ERR_INVALID, "null view");
+  DevGuard dg(v->device);
   int rc;
   if ((rc = check_backward_args(v, scene, seed, g_centers, g_scales, g_quats, g_opacities, g_sh)))
     return rc;
@@ -1612,6 +1646,8 @@ int nxs_forward_backward(nxs_view* v, const nxs_scene* scene, const nxs_camera* 
                          float* rgb, int32_t* overdraw, float* residual, const float* seed,
                          float* g_centers, float* g_scales, float* g_quats, float* g_opacities,
                          float* g_sh, void* stream_) {
+  if (!v) return fail(NXS_ERR_INVALID, "null view");
+  DevGuard dg(v->device);
   int rc;
   if ((rc = check_backward_args(v, scene, seed, g_centers, g_scales, g_quats, g_opacities, g_sh)))
     return rc;
@@ -1650,8 +1686,7 @@ int nxs_forward_backward(nxs_view* v, const nxs_scene* scene, const nxs_camera* 
       if ((rc = finish_async_check(v, ok))) return rc;
     } else {
       cudaError_t e;
-      while ((e = cudaEventQuery(v->ev_sync)) == cudaErrorNotReady) {
-      }
+      while ((e = cudaEventQuery(v->ev_sync)) == cudaErrorNotReady) std::this_thread::yield();
       NXS_CUDA(e);
     }
     v->spec_pending = false;
@@ -1718,6 +1753,7 @@ int nxs_view_timings(nxs_view* v, float* ms, int n) {
 int nxs_cache_export(nxs_view* v, uint8_t* sat, float* e_k, float* t_k, float* theta0,
                      void* stream_) {
   if (!v) return fail(NXS_ERR_INVALID, "null view");
+  DevGuard dg(v->device);
   if (!v->have_fwd) return fail(NXS_ERR_STATE, "no forward pass recorded in this view");
   cudaStream_t s = (cudaStream_t)stream_;
   const size_t npix = (size_t)v->cam.W * v->cam.H;
@@ -1734,6 +1770,7 @@ int nxs_cache_export(nxs_view* v, uint8_t* sat, float* e_k, float* t_k, float* t
 
 int nxs_depth_order(nxs_view* v, int32_t* order, void* stream_) {
   if (!v || !order) return fail(NXS_ERR_INVALID, "null argument");
+  DevGuard dg(v->device);
   if (!v->have_fwd) return fail(NXS_ERR_STATE, "no forward pass recorded in this view");
   if (v->P == 0) return NXS_OK;
   int rc;
@@ -1746,6 +1783,7 @@ int nxs_depth_order(nxs_view* v, int32_t* order, void* stream_) {
 int nxs_binning_export(nxs_view* v, int32_t* rects, int32_t* ranges, int32_t* pair_ranks,
                        void* stream_) {
   if (!v) return fail(NXS_ERR_INVALID, "null view");
+  DevGuard dg(v->device);
   if (!v->have_fwd) return fail(NXS_ERR_STATE, "no forward pass recorded in this view");
   cudaStream_t s = (cudaStream_t)stream_;
   int rc;
@@ -1788,6 +1826,7 @@ int nxs_binning_export(nxs_view* v, int32_t* rects, int32_t* ranges, int32_t* pa
 
 int nxs_touched_export(nxs_view* v, int32_t* gids, int64_t* count, void* stream_) {
   if (!v || !count) return fail(NXS_ERR_INVALID, "null argument");
+  DevGuard dg(v->device);
   if (!v->tlist_valid) return fail(NXS_ERR_STATE, "no backward recorded in this view");
   cudaStream_t s = (cudaStream_t)stream_;
   unsigned long long n = 0;
@@ -1801,6 +1840,7 @@ int nxs_touched_export(nxs_view* v, int32_t* gids, int64_t* count, void* stream_
 
 int nxs_records_export(nxs_view* v, float* records, void* stream_) {
   if (!v || !records) return fail(NXS_ERR_INVALID, "null argument");
+  DevGuard dg(v->device);
   if (!v->have_fwd) return fail(NXS_ERR_STATE, "no forward pass recorded in this view");
   if (v->P == 0) return NXS_OK;
   NXS_CUDA(cudaMemcpyAsync(records, v->records.p, (size_t)v->P * REC_F4 * 16,

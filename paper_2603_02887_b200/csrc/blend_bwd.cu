@@ -276,15 +276,14 @@ static void launch_bwd_fam(bool count, int n_tiles, const float4* records, const
                            float cutoff, double near_plane, const float* bg, const float* seed,
                            const PixCache& cache, double* moments, uint8_t* touched,
                            Counters* cnt, cudaStream_t s) {
-  static bool attr_set = false;  // host-side, once per instantiation
-  if (!attr_set) {
+  static unsigned long long attr_dev = 0;  // per instantiation and device
+  once_per_device(attr_dev, [] {
     for (auto k : {k_blend_bwd<FAM, true>, k_blend_bwd<FAM, false>}) {
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BWD_SMEM);
       cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
                            (int)cudaSharedmemCarveoutMaxShared);
     }
-    attr_set = true;
-  }
+  });
   auto k = count ? k_blend_bwd<FAM, true> : k_blend_bwd<FAM, false>;
   k<<<n_tiles, BWD_THREADS, BWD_SMEM, s>>>(records, bframe, lists, cam, m, cutoff, near_plane, bg[0],
                                         bg[1], bg[2], seed, cache, moments, touched, cnt);

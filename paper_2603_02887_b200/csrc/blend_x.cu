@@ -585,12 +585,11 @@ template <int FAM, int XB>
 static void launch_fwd_x_xb(bool count, int n_tiles, const FwdXArgs& a, const CamDev& cam,
                             const ModelDev& m, const PixCache& cache, const PixResume& rs,
                             Counters* cnt, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr_dev = 0;
+  once_per_device(attr_dev, [] {
     set_smem(k_blend_fwd_x<FAM, true, XB>, fwdx_smem(XB));
     set_smem(k_blend_fwd_x<FAM, false, XB>, fwdx_smem(XB));
-    attr = true;
-  }
+  });
   auto k = count ? k_blend_fwd_x<FAM, true, XB> : k_blend_fwd_x<FAM, false, XB>;
   k<<<n_tiles, TILE_PIX, fwdx_smem(XB), s>>>(
       a.records, a.pairs, a.ranges, a.zlo_rank, a.order, a.rank_c, a.chunk, cam, m, a.max_splats,
@@ -627,12 +626,11 @@ template <int FAM>
 static void launch_bwd_x_fam(bool count, int n_tiles, const BwdXArgs& a, const CamDev& cam,
                              const ModelDev& m, const PixCache& cache, Counters* cnt,
                              cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr_dev = 0;
+  once_per_device(attr_dev, [] {
     set_smem(k_blend_bwd_x<FAM, true>, BWDX_SMEM);
     set_smem(k_blend_bwd_x<FAM, false>, BWDX_SMEM);
-    attr = true;
-  }
+  });
   auto k = count ? k_blend_bwd_x<FAM, true> : k_blend_bwd_x<FAM, false>;
   k<<<n_tiles, BWDX_THREADS, BWDX_SMEM, s>>>(a.records, a.bframe, a.pairs, a.seq, a.max_splats, cam, m,
                                          a.cutoff, a.near_plane, a.bg[0], a.bg[1], a.bg[2],

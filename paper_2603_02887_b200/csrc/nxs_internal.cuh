@@ -14,7 +14,24 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <mutex>
+
 namespace nxs {
+
+// Host: run `f` once per (call site, CUDA device) — kernel attributes and
+// constant-memory uploads are per-device state.  `done` is the call site's
+// bit set of devices (device ids >= 64 share bit 63 and re-run every time).
+template <class F>
+inline void once_per_device(unsigned long long& done, F&& f) {
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev < 63 ? dev : 63);
+  std::lock_guard<std::mutex> lock(mu);
+  if ((done & bit) && dev < 63) return;
+  f();
+  done |= bit;
+}
 
 constexpr int TILE = 16;
 constexpr int TILE_PIX = TILE * TILE;  // 256 threads per tile block

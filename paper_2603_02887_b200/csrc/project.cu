@@ -1340,12 +1340,11 @@ void launch_count_tiles(const int4* rects, const uint32_t* order, int64_t r0, in
 void launch_tile_scan(unsigned int* tile_cnt, int n_tiles, int2* ranges, unsigned long long* total,
                       unsigned long long* maxseg, unsigned long long cap,
                       unsigned long long* overflow, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr_dev = 0;
+  once_per_device(attr_dev, [] {
     cudaFuncSetAttribute(k_tile_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          TSCAN_STAGED * (int)sizeof(unsigned int));
-    attr = true;
-  }
+  });
   const size_t dyn = n_tiles <= TSCAN_STAGED ? (size_t)n_tiles * sizeof(unsigned int) : 0;
   k_tile_scan<<<1, TSCAN_THREADS, dyn, s>>>(tile_cnt, n_tiles, ranges, total, maxseg, cap,
                                             overflow, SEG_MAX);

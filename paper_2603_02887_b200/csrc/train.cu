@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include "../../include/nxs.h"
+#include "nxs_internal.cuh"
 
 namespace nxs {
 int set_last_error(int code, const char* msg);  // api.cu
@@ -401,7 +402,7 @@ __global__ void __launch_bounds__(256) k_adam(AdamArgs a) {
   if ((threadIdx.x & 31) == 0 && bad) atomicAdd(a.nan_skips, (unsigned long long)bad);
 }
 
-bool g_win_ready = false;
+unsigned long long g_win_dev = 0;  // devices with the window and attributes set
 
 }  // namespace nxs_train
 
@@ -428,7 +429,8 @@ int nxs_image_loss(const float* rendered, const float* target, int32_t height, i
   if (with_ssim && (height < 2 * HALO + 1 || width < 2 * HALO + 1))
     return set_last_error(NXS_ERR_INVALID, "images must be at least 11 pixels on each side");
   cudaStream_t s = (cudaStream_t)stream;
-  if (!g_win_ready) {
+  bool win_ok = true;
+  nxs::once_per_device(g_win_dev, [&] {
     double w[11], sum = 0.0;
     for (int i = 0; i < 11; ++i) {
       const double r = (i - 5) / 1.5;
@@ -436,13 +438,15 @@ int nxs_image_loss(const float* rendered, const float* target, int32_t height, i
       sum += w[i];
     }
     for (double& x : w) x /= sum;
-    if (cudaMemcpyToSymbol(c_win, w, sizeof(w)) != cudaSuccess)
-      return nxs::set_last_error(NXS_ERR_CUDA, "window upload failed");
-    static const size_t sm1 = sizeof(double) * (2 * LS * LS + 5 * LS * LT);
-    static const size_t sm2 = sizeof(double) * (3 * LS * LS + 3 * LS * LT);
+    win_ok = cudaMemcpyToSymbol(c_win, w, sizeof(w)) == cudaSuccess;
+    const size_t sm1 = sizeof(double) * (2 * LS * LS + 5 * LS * LT);
+    const size_t sm2 = sizeof(double) * (3 * LS * LS + 3 * LS * LT);
     cudaFuncSetAttribute(k_loss_stats, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
     cudaFuncSetAttribute(k_loss_seed, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
-    g_win_ready = true;
+  });
+  if (!win_ok) {
+    g_win_dev = 0;
+    return nxs::set_last_error(NXS_ERR_CUDA, "window upload failed");
   }
   const dim3 grid((width + LT - 1) / LT, (height + LT - 1) / LT);
   const int nblk = (int)(grid.x * grid.y);
