@@ -65,6 +65,9 @@ def parse():
     p.add_argument("--chunk", default="1",
                    help="ordering: 1 = global depth order (default), none = exact per-pixel order, "
                         "C > 1 = chunked order")
+    p.add_argument("--adam", action="store_true",
+                   help="apply a bounded Adam step to the scene after every step (a moving "
+                        "scene, as in training: exercises the per-tile capacity refresh)")
     p.add_argument("--first-phase", type=int, default=0,
                    help="ranks binned in the first depth phase (0 = automatic)")
     return p.parse_args()
@@ -313,6 +316,17 @@ def main():
                               chunk_size=a.chunk_size)
     step = DataParallelStep(n_views, rank, world, grads, rv)
     my_views = step.views()
+    if a.adam:  # every step also moves the scene (lr of the reference optimizer's order)
+        from paper_2603_02887_b200.optim import AdamState, bounded_adam_step
+        params = {k: getattr(dev, k) for k in DeviceScene.FIELDS}
+        adam = AdamState.for_params(params)
+        lrs = {"centers": 1.6e-4, "scales": 5e-3, "quats": 1e-3, "opacities": 5e-2, "sh": 2.5e-3}
+        plain_step = step
+
+        def step():
+            g = plain_step()
+            bounded_adam_step(params, g.fields, adam, lrs)
+            return g
 
     for _ in range(a.warmup):
         step()
@@ -326,6 +340,7 @@ def main():
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = sum(rv.views[v].stats()["n_launches"] for v in my_views)
+    redo0 = sum(rv.views[v].stats()["n_redo"] for v in my_views)
     e0.record()
     for _ in range(a.steps):
         step()
@@ -333,6 +348,7 @@ def main():
     # hand-written kernels the library launched in the timed steps (counted
     # per enqueue; a captured phase-0 graph counts its kernels each call)
     n_launches = sum(rv.views[v].stats()["n_launches"] for v in my_views) - launches0
+    n_redo = sum(rv.views[v].stats()["n_redo"] for v in my_views) - redo0
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -402,6 +418,7 @@ def main():
             "roofline": roof,
             "clocks": ck,
             "gpu_launches": n_launches,
+            "redone_passes": n_redo,
             "e2e": e2e,
             "cpu_baseline": cpu,
         }
@@ -422,7 +439,8 @@ def config_of(a, model, vpr, world):
                      + ("chunk_size=1 (global depth order), " if a.chunk_size == 1 else
                         "chunk_size=None (exact per-pixel order), " if a.chunk_size is None
                         else f"chunk_size={a.chunk_size} (chunked order), ")
-                     + f"fwd+bwd, {vpr} view(s) per GPU"),
+                     + f"fwd+bwd, {vpr} view(s) per GPU"
+                     + (", + bounded Adam step on the scene per step" if a.adam else "")),
         "gaussians": a.gaussians, "width": W, "height": H,
         "views_per_gpu": vpr, "total_views": n_views,
         "parallelism": f"dp{world} over views",

@@ -54,7 +54,7 @@
 extern "C" {
 #endif
 
-#define NXS_ABI_VERSION 1
+#define NXS_ABI_VERSION 2
 
 /* status codes */
 #define NXS_OK 0
@@ -144,6 +144,10 @@ typedef struct {
     int64_t n_overflow;       /* exact order: pending-buffer overflows (must be 0) */
     int64_t n_launches;       /* kernels this view has launched so far (cumulative;
                                  the ones replayed from its CUDA graph included) */
+    int64_t n_redo;           /* passes redone so far (cumulative): a device-sized
+                                 first phase whose capacities were exceeded, a fused
+                                 call that needed more depth phases than speculated,
+                                 a chunked pass whose 16-entry buffer overflowed */
 } nxs_stats;
 
 typedef struct nxs_view nxs_view;

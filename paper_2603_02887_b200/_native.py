@@ -119,7 +119,7 @@ class AdamGroup(C.Structure):
 class Stats(C.Structure):
     _fields_ = [(n, C.c_int64) for n in (
         "n_gaussians", "n_visible", "n_pairs", "n_straddling", "n_tiles", "n_tests_fwd",
-        "n_composited", "n_tests_bwd", "n_entries_bwd", "n_overflow", "n_launches")]
+        "n_composited", "n_tests_bwd", "n_entries_bwd", "n_overflow", "n_launches", "n_redo")]
 
     def as_dict(self) -> dict:
         return {n: int(getattr(self, n)) for n, _ in self._fields_}
@@ -172,7 +172,7 @@ def lib():
         if name not in ("nxs_error_string", "nxs_last_error", "nxs_view_bytes",
                         "nxs_loss_workspace_bytes"):
             getattr(h, name).restype = C.c_int
-    if h.nxs_abi_version() != 1:
+    if h.nxs_abi_version() != 2:
         raise NativeLibraryError("libnxs ABI version mismatch")
     _lib = h
     return h

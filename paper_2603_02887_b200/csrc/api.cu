@@ -100,6 +100,8 @@ void launch_seg_sort(uint32_t*, int2*, unsigned int*, int, unsigned long long, c
                      long long max_seg = -1, const unsigned int* base = nullptr,
                      unsigned long long* total = nullptr, unsigned long long* overflow = nullptr);
 void launch_make_bases(const int2*, int, unsigned int*, cudaStream_t);
+void launch_refresh_bases(const int2*, int, unsigned int*, unsigned long long, unsigned int,
+                          cudaStream_t);
 void launch_compact_lists(const uint32_t*, const int2*, const int*, int, uint32_t*, int2*,
                           cudaStream_t);
 void launch_chunk_key(const float*, const float*, const float*, const float*, int64_t,
@@ -271,6 +273,8 @@ struct nxs_view {
   // first-phase hint: host_small[30] lands behind a forward on the side
   // stream; the planner uses it only once ev_hint reports the copy complete
   cudaEvent_t ev_hint = nullptr;
+  cudaEvent_t ev_bases = nullptr;  // the side-stream capacity refresh of the last call
+  bool bases_pending = false;
   bool hint_pending = false;
   unsigned long long hint = 0;
   int device = 0;  // the CUDA device this view's workspace lives on
@@ -312,6 +316,7 @@ struct nxs_view {
     if (cap_stream) cudaStreamDestroy(cap_stream);
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (ev_hint) cudaEventDestroy(ev_hint);
+    if (ev_bases) cudaEventDestroy(ev_bases);
     if (ev_side) cudaEventDestroy(ev_side);
     if (ev_ok) {
       for (auto& e : ev) cudaEventDestroy(e);
@@ -648,6 +653,7 @@ int finish_async_check(nxs_view* v, bool& ok) {
   ok = v->host_small[25] == 0 && n0 <= v->async_cap0 && (int64_t)pairs <= v->async_capp;
   v->async_pending = false;
   if (!ok) {
+    ++v->stats.n_redo;
     v->est_n0 = 0;  // the next pass sizes phase 0 exactly again
     return NXS_OK;
   }
@@ -674,6 +680,10 @@ int forward_impl(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
     return fail(NXS_ERR_INVALID, "null argument");
   DevGuard dg(v->device);
   cudaStream_t s = (cudaStream_t)stream_;
+  if (v->bases_pending) {  // the last call's side-stream capacity refresh
+    NXS_CUDA(cudaStreamWaitEvent(s, v->ev_bases, 0));
+    v->bases_pending = false;
+  }
   v->have_fwd = false;
   v->spec_pending = false;
   CamDev cam;
@@ -703,8 +713,10 @@ int forward_impl(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
   const int n_tiles = cam.tiles_x * cam.tiles_y;
   {
     const int64_t launched = v->stats.n_launches;  // (cumulative over calls)
+    const int64_t redone = v->stats.n_redo;
     v->stats = nxs_stats{};
     v->stats.n_launches = launched;
+    v->stats.n_redo = redone;
   }
   v->stats.n_gaussians = P;
   v->stats.n_tiles = n_tiles;
@@ -1482,6 +1494,18 @@ retry_sort:
   if (v->lazy) {  // the next call's first-phase hint (read without a sync)
     cudaStream_t cs;
     NXS_CUDA(side_after(v, s, cs));
+    if (v->async_bases) {
+      // the next call's per-tile capacities follow this pass's counts (a
+      // moving scene drifts from the exact pass's); one block on the side
+      // stream, off the pipeline — the next call waits for it (ev_bases)
+      launch_refresh_bases(v->ranges_ph[0].as<int2>(), n_tiles, v->tile_base.as<uint32_t>(),
+                           (unsigned long long)v->bases_bound,
+                           (unsigned int)std::min<int64_t>(v->bases_maxcap, 0xffffffffll), cs);
+      NXS_LAUNCHED("refresh_bases");
+      if (!v->ev_bases) NXS_CUDA(cudaEventCreateWithFlags(&v->ev_bases, cudaEventDisableTiming));
+      NXS_CUDA(cudaEventRecord(v->ev_bases, cs));
+      v->bases_pending = true;
+    }
     NXS_CUDA(cudaMemcpyAsync(v->host_small + 30, dsmall + 12, sizeof(unsigned long long),
                              cudaMemcpyDeviceToHost, cs));
     if (!v->ev_hint) NXS_CUDA(cudaEventCreateWithFlags(&v->ev_hint, cudaEventDisableTiming));
@@ -1499,6 +1523,7 @@ retry_sort:
     v->stats.n_overflow = (int64_t)v->host_small[7];
     if (v->host_small[7] > 0 && chunked && !(opts->flags & NXS_FLAG_XBUF32)) {
       // the small pending buffer overflowed: redo the pass with the large one
+      ++v->stats.n_redo;
       nxs_opts o2 = *opts;
       o2.flags |= NXS_FLAG_XBUF32;
       return nxs_forward(v, scene, camera, model, &o2, background, rgb, overdraw, residual,
@@ -1693,6 +1718,7 @@ int nxs_forward_backward(nxs_view* v, const nxs_scene* scene, const nxs_camera* 
     g_ht.mark("spin");
     if (!ok || (unsigned)v->host_small[3] != 0) {
       // more depth phases were needed: drop the moments, redo both passes
+      ++v->stats.n_redo;
       if ((rc = backward_chain(v, scene, nullptr, nullptr, nullptr, nullptr, nullptr, s)))
         return rc;
       v->phases_needed = 0;

@@ -1368,6 +1368,40 @@ void launch_make_bases(const int2* ranges, int n_tiles, unsigned int* base, cuda
   k_make_bases<<<1, TSCAN_THREADS, 0, s>>>(ranges, n_tiles, base);
 }
 
+// After a device-sized pass: re-derive the per-tile capacities from the
+// counts that pass found (a scene that moves between calls, e.g. under
+// Adam, drifts away from the exact pass's counts), each capped at the
+// host's longest-list bound and committed only when the total still fits
+// the pair buffer the host sized (`bound`); otherwise the old bases stay.
+__global__ void __launch_bounds__(TSCAN_THREADS)
+    k_refresh_bases(const int2* __restrict__ ranges, int n_tiles, unsigned int* __restrict__ base,
+                    unsigned long long bound, unsigned int maxcap) {
+  typedef cub::BlockScan<unsigned long long, TSCAN_THREADS> Scan;
+  __shared__ typename Scan::TempStorage tmp;
+  const int per = (n_tiles + TSCAN_THREADS - 1) / TSCAN_THREADS;
+  const int lo = min(n_tiles, (int)threadIdx.x * per), hi = min(n_tiles, lo + per);
+  auto cap_of = [&](int t) {
+    const int2 rg = ranges[t];
+    const unsigned int n = (unsigned int)max(0, rg.y - rg.x);
+    return min(n + n / 8 + 8u, maxcap);
+  };
+  unsigned long long sum = 0;
+  for (int t = lo; t < hi; ++t) sum += cap_of(t);
+  unsigned long long off, all;
+  Scan(tmp).ExclusiveSum(sum, off, all);
+  if (all > bound) return;  // (block-uniform)
+  __syncthreads();          // every thread has read its ranges before base moves
+  for (int t = lo; t < hi; ++t) {
+    base[t] = (unsigned int)off;
+    off += cap_of(t);
+  }
+  if (threadIdx.x == 0) base[n_tiles] = (unsigned int)all;
+}
+void launch_refresh_bases(const int2* ranges, int n_tiles, unsigned int* base,
+                          unsigned long long bound, unsigned int maxcap, cudaStream_t s) {
+  k_refresh_bases<<<1, TSCAN_THREADS, 0, s>>>(ranges, n_tiles, base, bound, maxcap);
+}
+
 // Export: gather each tile's list [ranges[t].x, ranges[t].y) to the compact
 // offset dst_off[t] (lists laid out at per-tile capacities have gaps).
 __global__ void k_compact_lists(const uint32_t* __restrict__ src, const int2* __restrict__ ranges,

@@ -21,7 +21,7 @@ def test_library_exports_every_header_symbol():
     h = _native.lib()
     for name in declared:
         assert hasattr(h, name), name
-    assert h.nxs_abi_version() == 1
+    assert h.nxs_abi_version() == 2
     assert h.nxs_error_string(-7).decode().startswith("exact-order pending buffer")
 
 
