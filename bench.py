@@ -65,6 +65,8 @@ def parse():
     p.add_argument("--chunk", default="1",
                    help="ordering: 1 = global depth order (default), none = exact per-pixel order, "
                         "C > 1 = chunked order")
+    p.add_argument("--deterministic", action="store_true",
+                   help="bit-reproducible gradients (NXS_FLAG_DETERMINISTIC)")
     p.add_argument("--adam", action="store_true",
                    help="apply a bounded Adam step to the scene after every step (a moving "
                         "scene, as in training: exercises the per-tile capacity refresh)")
@@ -313,7 +315,7 @@ def main():
     bg = np.zeros(3)
     grads = GradBuffer(len(arrs), arrs.sh.shape[2], device="cuda")
     rv = device_view_renderer(dev, model, bg, cams, seeds, first_phase_ranks=a.first_phase,
-                              chunk_size=a.chunk_size)
+                              chunk_size=a.chunk_size, deterministic=a.deterministic)
     step = DataParallelStep(n_views, rank, world, grads, rv)
     my_views = step.views()
     if a.adam:  # every step also moves the scene (lr of the reference optimizer's order)
@@ -440,7 +442,8 @@ def config_of(a, model, vpr, world):
                         "chunk_size=None (exact per-pixel order), " if a.chunk_size is None
                         else f"chunk_size={a.chunk_size} (chunked order), ")
                      + f"fwd+bwd, {vpr} view(s) per GPU"
-                     + (", + bounded Adam step on the scene per step" if a.adam else "")),
+                     + (", + bounded Adam step on the scene per step" if a.adam else "")
+                     + (", deterministic gradients" if a.deterministic else "")),
         "gaussians": a.gaussians, "width": W, "height": H,
         "views_per_gpu": vpr, "total_views": n_views,
         "parallelism": f"dp{world} over views",

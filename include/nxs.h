@@ -80,6 +80,12 @@ extern "C" {
 #define NXS_FLAG_FULL_BINNING 2    /* bin every rank in one phase (no progressive binning) */
 #define NXS_FLAG_XBUF32 4          /* chunked order: start with the 32-entry pending buffer
                                       (default 16, rerun with 32 on overflow) */
+#define NXS_FLAG_DETERMINISTIC 16  /* bit-reproducible gradients (SPEC "deterministic
+                                      partitioned reduction"): per (tile, list entry)
+                                      moment partials, summed per Gaussian in a fixed
+                                      tile order instead of atomics; global depth order
+                                      (chunk_size=1) only, else NXS_ERR_UNSUPPORTED at
+                                      the backward.  Costs shared memory (occupancy). */
 #define NXS_FLAG_THETA0 8          /* also accumulate the reference cache's theta0
                                       (render.py:213; only nxs_cache_export reads it, the
                                       backward does not: off by default on the global order) */

@@ -59,6 +59,7 @@ NXS_FLAG_COUNT_EVENTS = 1
 NXS_FLAG_FULL_BINNING = 2
 NXS_FLAG_XBUF32 = 4
 NXS_FLAG_THETA0 = 8
+NXS_FLAG_DETERMINISTIC = 16
 NXS_LOSS_SRGB_INPUT = 1
 
 

@@ -127,6 +127,8 @@ void launch_blend_fwd(bool, int, const FwdArgs&, const CamDev&, const ModelDev&,
 void launch_blend_bwd(bool, int, const float4*, const float4*, const PhaseLists&, const CamDev&,
                       const ModelDev&, float, double, const float*, const float*,
                       const PixCache&, double*, uint8_t*, Counters*, cudaStream_t);
+void launch_det_reduce(int64_t, const uint32_t*, const int4*, int, const PhaseLists&,
+                       const uint8_t*, double*, cudaStream_t);
 void launch_chain(const float*, const float*, int, int64_t, const uint32_t*, double*, uint8_t*,
                   float*, float*, float*, float*, float*, uint32_t*, unsigned long long*,
                   cudaStream_t);
@@ -228,6 +230,7 @@ struct nxs_view {
   Buf r_rad, r_trem, r_count, r_sea, r_sa;
   Buf temp, dev_small;  // CUB temp; counters
   Buf tlist, tcount;     // Gaussians the last backward's chain wrote, and their number
+  Buf partial;           // deterministic mode: per (tile, entry) moment partials
   bool tlist_valid = false;
   unsigned long long* host_small = nullptr;  // pinned
   // phase events: see NXS_PHASES in include/nxs.h
@@ -296,7 +299,7 @@ struct nxs_view {
                   &ph_sel,   &tq,      &zlo64,  &xc_t, &xc_r, &xc_n,
                   &c_last,   &c_sat,     &c_tk,    &c_thi,   &c_tlo,   &c_P,    &c_ck,
                   &c_Pck,    &c_ek,      &c_th0,   &r_rad,   &r_trem,  &r_count, &r_sea,
-                  &r_sa,     &temp,      &dev_small, &tlist, &tcount};
+                  &r_sa,     &temp,      &dev_small, &tlist, &tcount, &partial};
     for (Buf* b : all) f(*b);
     for (int p = 0; p < MAX_PHASES; ++p) {
       f(pv_ph[p]);
@@ -1582,6 +1585,10 @@ int backward_blend(nxs_view* v, const float* seed, cudaStream_t s) {
   const bool count = (v->opts.flags & NXS_FLAG_COUNT_EVENTS) != 0;
   unsigned long long* dsmall = v->dev_small.as<unsigned long long>();
   Counters* cnt = reinterpret_cast<Counters*>(dsmall + 1);
+  const bool det = (v->opts.flags & NXS_FLAG_DETERMINISTIC) != 0;
+  if (det && v->opts.chunk_size != 1)
+    return fail(NXS_ERR_UNSUPPORTED,
+                "deterministic gradients: global depth order (chunk_size=1) only");
   if (v->opts.chunk_size != 1) {
     BwdXArgs xa{v->records.as<float4>(), v->bframe.as<float4>(), v->pv_ph[0].as<uint32_t>(),
                 v->seq.as<int32_t>(), std::max(1, v->opts.max_splats),
@@ -1596,9 +1603,29 @@ int backward_blend(nxs_view* v, const float* seed, cudaStream_t s) {
     lists.ranges[p] = v->ranges_ph[p].as<int2>();
     lists.cum[p] = v->cum_ph[p].as<int32_t>();
   }
+  lists.partial = nullptr;
+  if (det) {  // partials per (tile, entry), reduced per rank in a fixed order
+    int64_t off = 0;
+    for (int p = 0; p < v->n_phases; ++p) {
+      lists.poff[p] = off;
+      off += (int64_t)(v->pv_ph[p].cap / sizeof(uint32_t));
+    }
+    NXS_CUDA(ensure_n<float>(v->partial, std::max<int64_t>(off, 1) * NMOM));
+    NXS_CUDA(cudaMemsetAsync(v->partial.p, 0, (size_t)off * NMOM * sizeof(float), s));
+    lists.partial = v->partial.as<float>();
+  }
   launch_blend_bwd(count, v->n_tiles, v->records.as<float4>(), v->bframe.as<float4>(), lists,
                    v->cam, v->model, (float)v->opts.alpha_cutoff, v->opts.near_plane, v->bg, seed,
                    v->cache(), v->moments.as<double>(), v->touched.as<uint8_t>(), cnt, s);
+  if (det) {
+    NXS_LAUNCHED("blend_bwd");
+    launch_det_reduce(v->proj_end > 0 ? std::min(v->proj_end, P) : P, v->idx_out.as<uint32_t>(),
+                      v->rects.as<int4>(), v->cam.tiles_x, lists, v->touched.as<uint8_t>(),
+                      v->moments.as<double>(), s);
+    NXS_LAUNCHED("det_reduce");
+    mark(v, 10, s);
+    return NXS_OK;
+  }
   }
   NXS_LAUNCHED("blend_bwd");
   mark(v, 10, s);

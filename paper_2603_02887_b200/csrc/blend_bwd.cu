@@ -47,11 +47,15 @@ constexpr int RED_ROW = 2 * RED_HALF;        // one row per moment pair
 constexpr int RED_WARP = (NMOM / 2) * RED_ROW;  // floats per warp
 // Records, B frames and ranks are double-buffered: the next batch streams
 // in with cp.async while the current one is replayed.
-constexpr size_t BWD_SMEM = 2 * (sizeof(float4) * BWD_BATCH * (REC_F4 + 3) +
-                                 sizeof(uint32_t) * BWD_BATCH) +
-                            sizeof(float) * BWD_BATCH * NMOM + sizeof(float) * RED_WARP * BWD_WARPS;
+// Deterministic mode keeps one accumulator row per warp (summed in warp order
+// at the flush) instead of shared float atomics from the four warps.
+__host__ __device__ constexpr int acc_rows(bool det) { return det ? BWD_WARPS : 1; }
+constexpr size_t bwd_smem(bool det) {
+  return 2 * (sizeof(float4) * BWD_BATCH * (REC_F4 + 3) + sizeof(uint32_t) * BWD_BATCH) +
+         sizeof(float) * BWD_BATCH * NMOM * acc_rows(det) + sizeof(float) * RED_WARP * BWD_WARPS;
+}
 
-template <int FAM, bool COUNT>
+template <int FAM, bool COUNT, bool DET>
 __global__ void __launch_bounds__(BWD_THREADS, 4)
     k_blend_bwd(const float4* __restrict__ records, const float4* __restrict__ bframe,
                 PhaseLists lists, CamDev cam, ModelDev m, float cutoff, double near_plane,
@@ -66,7 +70,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 4)
   uint32_t(*s_rank2)[BWD_BATCH] =
       reinterpret_cast<uint32_t(*)[BWD_BATCH]>(smem_dyn + 2 * BWD_BATCH * (REC_F4 + 3));
   float* s_acc = reinterpret_cast<float*>(s_rank2 + 2);
-  float* s_red = s_acc + BWD_BATCH * NMOM;
+  float* s_red = s_acc + BWD_BATCH * NMOM * acc_rows(DET);
   __shared__ int s_maxlast;
 
   const int tile = blockIdx.x;
@@ -149,7 +153,12 @@ __global__ void __launch_bounds__(BWD_THREADS, 4)
     const bool more = next_batch(nph, nhi);
     __syncthreads();  // every thread is past the previous batch's flush
     if (more) stage(buf ^ 1, nph, nhi);
-    for (int k = tid; k < n * NMOM; k += BWD_THREADS) s_acc[k] = 0.f;
+    if (DET) {
+      for (int w = 0; w < BWD_WARPS; ++w)
+        for (int k = tid; k < n * NMOM; k += BWD_THREADS) s_acc[w * BWD_BATCH * NMOM + k] = 0.f;
+    } else {
+      for (int k = tid; k < n * NMOM; k += BWD_THREADS) s_acc[k] = 0.f;
+    }
     if (more) cp_async_wait<1>();
     else cp_async_wait<0>();
     __syncthreads();
@@ -237,17 +246,38 @@ __global__ void __launch_bounds__(BWD_THREADS, 4)
           }
           const float other = __shfl_xor_sync(0xffffffffu, (lane & 1) ? part.x : part.y, 1);
           const float sum = ((lane & 1) ? part.y : part.x) + other;
-          if (lane < NMOM && sum != 0.f) atomicAdd(&s_acc[j * NMOM + lane], sum);
+          if (lane < NMOM && sum != 0.f) {
+            if (DET)  // this warp's own row: one writer per (entry, moment)
+              s_acc[((tid >> 5) * BWD_BATCH + j) * NMOM + lane] = sum;
+            else
+              atomicAdd(&s_acc[j * NMOM + lane], sum);
+          }
           __syncwarp();
         }
       }
       __syncthreads();
-      for (int k = tid; k < n * NMOM; k += BWD_THREADS) {
-        const float val = s_acc[k];
-        if (val != 0.f) {
-          const int e = k / NMOM;
-          atomicAdd(&moments[(size_t)s_rank[e] * NMOM + (k - e * NMOM)], (double)val);
-          touched[s_rank[e]] = 1;  // K5 reads (and re-zeroes) touched ranks only
+      if (DET) {
+        // fixed-order sum over the warps; one partial per (tile, entry):
+        // k_det_reduce adds them per rank in tile order
+        const int64_t slot0 = lists.poff[ph] + lists.ranges[ph][tile].x + (base - c0);
+        for (int k = tid; k < n * NMOM; k += BWD_THREADS) {
+          float val = s_acc[k];
+#pragma unroll
+          for (int w = 1; w < BWD_WARPS; ++w) val += s_acc[w * BWD_BATCH * NMOM + k];
+          if (val != 0.f) {
+            const int e = k / NMOM;
+            lists.partial[(slot0 + e) * NMOM + (k - e * NMOM)] = val;
+            touched[s_rank[e]] = 1;
+          }
+        }
+      } else {
+        for (int k = tid; k < n * NMOM; k += BWD_THREADS) {
+          const float val = s_acc[k];
+          if (val != 0.f) {
+            const int e = k / NMOM;
+            atomicAdd(&moments[(size_t)s_rank[e] * NMOM + (k - e * NMOM)], (double)val);
+            touched[s_rank[e]] = 1;  // K5 reads (and re-zeroes) touched ranks only
+          }
         }
       }
     ph = nph;
@@ -270,7 +300,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 4)
   }
 }
 
-template <int FAM>
+template <int FAM, bool DET>
 static void launch_bwd_fam(bool count, int n_tiles, const float4* records, const float4* bframe,
                            const PhaseLists& lists, const CamDev& cam, const ModelDev& m,
                            float cutoff, double near_plane, const float* bg, const float* seed,
@@ -278,15 +308,56 @@ static void launch_bwd_fam(bool count, int n_tiles, const float4* records, const
                            Counters* cnt, cudaStream_t s) {
   static unsigned long long attr_dev = 0;  // per instantiation and device
   once_per_device(attr_dev, [] {
-    for (auto k : {k_blend_bwd<FAM, true>, k_blend_bwd<FAM, false>}) {
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BWD_SMEM);
+    for (auto k : {k_blend_bwd<FAM, true, DET>, k_blend_bwd<FAM, false, DET>}) {
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd_smem(DET));
       cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
                            (int)cudaSharedmemCarveoutMaxShared);
     }
   });
-  auto k = count ? k_blend_bwd<FAM, true> : k_blend_bwd<FAM, false>;
-  k<<<n_tiles, BWD_THREADS, BWD_SMEM, s>>>(records, bframe, lists, cam, m, cutoff, near_plane, bg[0],
-                                        bg[1], bg[2], seed, cache, moments, touched, cnt);
+  auto k = count ? k_blend_bwd<FAM, true, DET> : k_blend_bwd<FAM, false, DET>;
+  k<<<n_tiles, BWD_THREADS, bwd_smem(DET), s>>>(records, bframe, lists, cam, m, cutoff, near_plane,
+                                               bg[0], bg[1], bg[2], seed, cache, moments, touched,
+                                               cnt);
+}
+
+// Deterministic moments: per touched rank, the (tile, entry) partials of
+// every tile of its rectangle (row-major tile order, phases in order), each
+// found by binary search in that tile's rank-sorted list, summed in fp64.
+__global__ void k_det_reduce(int64_t P, const uint32_t* __restrict__ order,
+                             const int4* __restrict__ rects, int tiles_x, PhaseLists lists,
+                             const uint8_t* __restrict__ touched, double* __restrict__ moments) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= P || !touched[r]) return;
+  const int4 rc = rects[order[r]];
+  double acc[NMOM];
+#pragma unroll
+  for (int m = 0; m < NMOM; ++m) acc[m] = 0.0;
+  for (int p = 0; p < lists.n; ++p)
+    for (int ty = rc.y; ty <= rc.w; ++ty)
+      for (int tx = rc.x; tx <= rc.z; ++tx) {
+        const int2 rg = lists.ranges[p][ty * tiles_x + tx];
+        int lo = rg.x, hi = rg.y;  // first position with rank >= r
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (lists.pairs[p][mid] < (uint32_t)r) lo = mid + 1;
+          else hi = mid;
+        }
+        if (lo >= rg.y || lists.pairs[p][lo] != (uint32_t)r) continue;
+        const float* q = lists.partial + (lists.poff[p] + lo) * NMOM;
+#pragma unroll
+        for (int m = 0; m < NMOM; ++m) acc[m] += (double)q[m];
+      }
+  double* mm = moments + r * NMOM;
+#pragma unroll
+  for (int m = 0; m < NMOM; ++m) mm[m] = acc[m];
+}
+
+void launch_det_reduce(int64_t P, const uint32_t* order, const int4* rects, int tiles_x,
+                       const PhaseLists& lists, const uint8_t* touched, double* moments,
+                       cudaStream_t s) {
+  if (P <= 0) return;
+  k_det_reduce<<<(unsigned)((P + 127) / 128), 128, 0, s>>>(P, order, rects, tiles_x, lists,
+                                                           touched, moments);
 }
 
 void launch_blend_bwd(bool count, int n_tiles, const float4* records, const float4* bframe,
@@ -295,9 +366,12 @@ void launch_blend_bwd(bool count, int n_tiles, const float4* records, const floa
                       const PixCache& cache, double* moments, uint8_t* touched, Counters* cnt,
                       cudaStream_t s) {
   if (n_tiles == 0) return;
-#define NXS_BWD(F) \
-  launch_bwd_fam<F>(count, n_tiles, records, bframe, lists, cam, m, cutoff, near_plane, bg, seed, \
-                    cache, moments, touched, cnt, s)
+#define NXS_BWD(F)                                                                            \
+  (lists.partial ? launch_bwd_fam<F, true>(count, n_tiles, records, bframe, lists, cam, m, cutoff, \
+                                           near_plane, bg, seed, cache, moments, touched, cnt, s) \
+                 : launch_bwd_fam<F, false>(count, n_tiles, records, bframe, lists, cam, m,      \
+                                            cutoff, near_plane, bg, seed, cache, moments, touched, \
+                                            cnt, s))
   switch (m.fam) {
     case FAM_EXP: NXS_BWD(FAM_EXP); break;
     case FAM_LIN: NXS_BWD(FAM_LIN); break;

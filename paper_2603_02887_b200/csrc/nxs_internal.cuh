@@ -117,6 +117,10 @@ struct PhaseLists {  // the per-tile virtual list = phase segments in order
   const int2* ranges[MAX_PHASES];     // per tile [start, end) in pairs[p]
   const int32_t* cum[MAX_PHASES];     // per tile virtual index of the segment start
   int n;
+  // deterministic gradients (NXS_FLAG_DETERMINISTIC): per (tile, entry)
+  // moment partials at partial[(poff[p] + index in pairs[p]) * NMOM + m]
+  float* partial;
+  int64_t poff[MAX_PHASES];
 };
 
 // arguments of one forward phase launch

@@ -123,7 +123,7 @@ class DataParallelStep:
 
 
 def device_view_renderer(dev_scene, model, background, cameras, seeds, *, chunk_size=1,
-                         max_splats=128, views=None, first_phase_ranks=0):
+                         max_splats=128, views=None, first_phase_ranks=0, deterministic=False):
     """Per-view fwd+bwd through libnxs on the current CUDA device.
     ``cameras[v]`` / ``seeds[v]`` (H,W,3 float32 CUDA) for view v; each view
     index gets its own persistent ``nxs_view`` workspace."""
@@ -139,7 +139,8 @@ def device_view_renderer(dev_scene, model, background, cameras, seeds, *, chunk_
         o, _ = forward_backward_device(views[v], dev_scene, cameras[v], model, background,
                                        seeds[v], grads.fields, chunk_size=chunk_size,
                                        max_splats=max_splats,
-                                       first_phase_ranks=first_phase_ranks, out=outs.get(v))
+                                       first_phase_ranks=first_phase_ranks, out=outs.get(v),
+                                       deterministic=deterministic)
         outs[v] = o
 
     render_view.views = views

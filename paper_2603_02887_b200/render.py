@@ -295,7 +295,8 @@ def _model_struct(model):
 
 
 def _forward_args(dev, camera, model, background, max_splats, alpha_cutoff, near, chunk_size,
-                  count_events, full_binning, first_phase_ranks, out, theta0=False):
+                  count_events, full_binning, first_phase_ranks, out, theta0=False,
+                  deterministic=False):
     import torch
     chunk = _effective_chunk(chunk_size, dev.count)
     _check_mode(chunk)
@@ -309,7 +310,8 @@ def _forward_args(dev, camera, model, background, max_splats, alpha_cutoff, near
     bg = np.asarray(background, dtype=np.float64).reshape(3)
     flags = (_native.NXS_FLAG_COUNT_EVENTS if count_events else 0) | \
         (_native.NXS_FLAG_FULL_BINNING if full_binning else 0) | \
-        (_native.NXS_FLAG_THETA0 if theta0 else 0)
+        (_native.NXS_FLAG_THETA0 if theta0 else 0) | \
+        (_native.NXS_FLAG_DETERMINISTIC if deterministic else 0)
     opts = _native.make_opts(max_splats, alpha_cutoff, near, chunk, flags, first_phase_ranks)
     return _native.make_camera(camera), ms, opts, bg, out
 
@@ -317,7 +319,7 @@ def _forward_args(dev, camera, model, background, max_splats, alpha_cutoff, near
 def _raise_mapped(e):
     if e.code == _native.NXS_ERR_OVERFLOW:
         raise RuntimeError(f"{e} (exact order could not be guaranteed)") from e
-    if e.code == _native.NXS_ERR_GEOMETRY:
+    if e.code in (_native.NXS_ERR_GEOMETRY, _native.NXS_ERR_UNSUPPORTED):
         raise NotImplementedError(str(e)) from e
     if e.code == _native.NXS_ERR_INVALID:
         raise ValueError(str(e)) from e
@@ -327,13 +329,16 @@ def _raise_mapped(e):
 def forward_device(view, dev: DeviceScene, camera, model, background, *, max_splats=128,
                    alpha_cutoff=DEFAULT_ALPHA_CUTOFF, near=NEAR_PLANE, chunk_size=1,
                    count_events=False, full_binning=False, first_phase_ranks=0, out=None,
-                   stream=None, theta0=False):
+                   stream=None, theta0=False, deterministic=False):
     """Forward render on the device; returns (rgb (H,W,3), overdraw (H,W)
     int32, residual (H,W)) float32 CUDA tensors.  ``theta0`` also keeps the
-    reference cache's theta0 for :meth:`View.cache_export`."""
+    reference cache's theta0 for :meth:`View.cache_export`;
+    ``deterministic`` makes the following backward bit-reproducible
+    (NXS_FLAG_DETERMINISTIC, chunk_size=1)."""
     cam, ms, opts, bg, out = _forward_args(dev, camera, model, background, max_splats,
                                            alpha_cutoff, near, chunk_size, count_events,
-                                           full_binning, first_phase_ranks, out, theta0)
+                                           full_binning, first_phase_ranks, out, theta0,
+                                           deterministic)
     try:
         view.forward(dev, cam, ms, opts, bg, out[0], out[1], out[2], stream=stream)
     except _native.NxsError as e:
@@ -344,13 +349,16 @@ def forward_device(view, dev: DeviceScene, camera, model, background, *, max_spl
 def forward_backward_device(view, dev: DeviceScene, camera, model, background, seed, grads=None,
                             *, max_splats=128, alpha_cutoff=DEFAULT_ALPHA_CUTOFF,
                             near=NEAR_PLANE, chunk_size=1, count_events=False,
-                            full_binning=False, first_phase_ranks=0, out=None, stream=None):
+                            full_binning=False, first_phase_ranks=0, out=None, stream=None,
+                            deterministic=False):
     """Forward render plus gradient accumulation for ``seed`` in one library
     call (``nxs_forward_backward``: the end-of-forward depth-phase check
-    overlaps the backward).  Returns ((rgb, overdraw, residual), grads)."""
+    overlaps the backward).  Returns ((rgb, overdraw, residual), grads).
+    ``deterministic``: bit-reproducible gradients (chunk_size=1)."""
     cam, ms, opts, bg, out = _forward_args(dev, camera, model, background, max_splats,
                                            alpha_cutoff, near, chunk_size, count_events,
-                                           full_binning, first_phase_ranks, out)
+                                           full_binning, first_phase_ranks, out,
+                                           deterministic=deterministic)
     if grads is None:
         grads = zero_grads_device(dev)
     try:

@@ -760,3 +760,36 @@ def test_touched_export_covers_the_gradient_rows():
             assert g[k].shape == ref.shape and g[k].dtype == np.float64
             # (fp64 moment atomics: the summation order differs between calls)
             np.testing.assert_allclose(g[k], ref, rtol=1e-5, atol=1e-6 * np.abs(ref).max())
+
+
+@pytest.mark.parametrize("name", ["softplus_20", "exponential"])
+def test_deterministic_gradients_are_bit_reproducible(name):
+    """NXS_FLAG_DETERMINISTIC (SPEC: deterministic partitioned reduction):
+    repeated backwards — fresh views, a warm view on its device-sized graph
+    path, multiple depth phases — give bit-identical gradients, equal to the
+    atomic path up to summation order."""
+    import torch
+    from paper_2603_02887_b200 import _native, forward_backward_device
+    sc = O.round_scene_f32(O.canonical_scene(60_000, seed=1))
+    cam = O.canonical_camera(320, 240, 1, 8)
+    seed = torch.as_tensor(O.canonical_seed(320, 240, 1), dtype=torch.float32).cuda()
+    dev = _dev(sc)
+    model = MODELS[name]
+    runs = []
+    warm = _native.View()
+    for first in (0, 0, 4096):
+        fresh = _native.View()
+        for view in (fresh, warm):
+            _, g = forward_backward_device(view, dev, cam, model, np.zeros(3), seed,
+                                           first_phase_ranks=first, deterministic=True)
+            runs.append({k: v.cpu().numpy() for k, v in g.items()})
+    _, ga = forward_backward_device(_native.View(), dev, cam, model, np.zeros(3), seed)
+    for r in runs[1:]:
+        for k in GRAD_FIELDS:
+            assert np.array_equal(r[k], runs[0][k]), k
+    for k in GRAD_FIELDS:
+        ref = ga[k].cpu().numpy()
+        np.testing.assert_allclose(runs[0][k], ref, rtol=1e-5, atol=1e-6 * np.abs(ref).max())
+    with pytest.raises(NotImplementedError):
+        forward_backward_device(_native.View(), dev, cam, model, np.zeros(3), seed,
+                                chunk_size=None, deterministic=True)
