@@ -65,6 +65,8 @@ def parse():
     p.add_argument("--chunk", default="1",
                    help="ordering: 1 = global depth order (default), none = exact per-pixel order, "
                         "C > 1 = chunked order")
+    p.add_argument("--pool", type=int, default=8,
+                   help="nxs_view workspaces per rank; the rank's views cycle through them")
     p.add_argument("--deterministic", action="store_true",
                    help="bit-reproducible gradients (NXS_FLAG_DETERMINISTIC)")
     p.add_argument("--adam", action="store_true",
@@ -310,12 +312,19 @@ def main():
         cams = [canonical_camera(W, H)]
     else:
         cams = [canonical_camera(W, H, v, n_views) for v in range(n_views)]
-    seeds = {v: torch.as_tensor(canonical_seed(W, H, v), dtype=torch.float32, device="cuda")
-             for v in range(n_views)}
+    # adjoint seeds: view v's own for up to 8 views, else cycled over 8
+    # (256 distinct 4K seed images would hold 25 GB)
+    seed_pool = [torch.as_tensor(canonical_seed(W, H, v), dtype=torch.float32, device="cuda")
+                 for v in range(min(n_views, 8))]
+
+    def seeds(v):
+        return seed_pool[v % len(seed_pool)]
+
     bg = np.zeros(3)
     grads = GradBuffer(len(arrs), arrs.sh.shape[2], device="cuda")
     rv = device_view_renderer(dev, model, bg, cams, seeds, first_phase_ranks=a.first_phase,
-                              chunk_size=a.chunk_size, deterministic=a.deterministic)
+                              chunk_size=a.chunk_size, deterministic=a.deterministic,
+                              pool=a.pool)
     step = DataParallelStep(n_views, rank, world, grads, rv)
     my_views = step.views()
     if a.adam:  # every step also moves the scene (lr of the reference optimizer's order)
@@ -341,16 +350,16 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches0 = sum(rv.views[v].stats()["n_launches"] for v in my_views)
-    redo0 = sum(rv.views[v].stats()["n_redo"] for v in my_views)
+    launches0 = sum(w.stats()["n_launches"] for w in rv.workspaces)
+    redo0 = sum(w.stats()["n_redo"] for w in rv.workspaces)
     e0.record()
     for _ in range(a.steps):
         step()
     e1.record()
     # hand-written kernels the library launched in the timed steps (counted
     # per enqueue; a captured phase-0 graph counts its kernels each call)
-    n_launches = sum(rv.views[v].stats()["n_launches"] for v in my_views) - launches0
-    n_redo = sum(rv.views[v].stats()["n_redo"] for v in my_views) - redo0
+    n_launches = sum(w.stats()["n_launches"] for w in rv.workspaces) - launches0
+    n_redo = sum(w.stats()["n_redo"] for w in rv.workspaces) - redo0
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -364,18 +373,18 @@ def main():
     mpix = W * H * n_views / (ms_step / 1e3) / 1e6
 
     # ---- per-phase device timings (same steps, events inside the library)
-    views = rv.views
-    for v in my_views:  # phase events only here (they cost the pipeline a few us)
-        views[v].set_timing(True)
+    wss = rv.workspaces
+    for w in wss:  # phase events only here (they cost the pipeline a few us)
+        w.set_timing(True)
     phase_tot = {}
     step()
     for _ in range(max(3, min(a.steps, 10))):
         step()
-        for v in my_views:
-            for k, x in views[v].timings().items():
+        for w in wss:  # each workspace's last call: one view's phases
+            for k, x in w.timings().items():
                 phase_tot[k] = phase_tot.get(k, 0.0) + x
     nprof = max(3, min(a.steps, 10))
-    phase = {k: x / nprof / max(1, len(my_views)) for k, x in phase_tot.items()}
+    phase = {k: x / nprof / max(1, len(wss)) for k, x in phase_tot.items()}
     n_depth_phases = phase.pop("n_depth_phases", None)
 
     # ---- event counts (instrumented run, not timed) for the blend roofline
@@ -383,7 +392,7 @@ def main():
     cview = _native.View()
     forward_device(cview, dev, cams[my_views[0]], model, bg, chunk_size=a.chunk_size,
                    count_events=True, first_phase_ranks=a.first_phase)
-    backward_device(cview, dev, seeds[my_views[0]])
+    backward_device(cview, dev, seeds(my_views[0]))
     st = cview.stats()
     cview.close()
 
@@ -530,6 +539,8 @@ def e2e_arm(a, arrs, cams, model, my_views, world, render_with_gradients):
                                            chunk_size=a.chunk_size)
         return res, g
 
+    if world > 1:
+        return e2e_dp(a, arrs, cams, model, my_views, world)
     one()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -537,21 +548,69 @@ def e2e_arm(a, arrs, cams, model, my_views, world, render_with_gradients):
         one()
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t0) / a.e2e_steps
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([dt], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dt = float(t.item())
     from paper_2603_02887_b200.render import _LAST_IO
     npx = a.width * a.height
     # bytes the API moved per view (fp32 scene + seed up; float64 image,
-    # residual, int64 overdraw and the touched gradient rows down)
+    # residual, int64 overdraw and gradients down)
     h2d = len(my_views) * _LAST_IO["h2d"]
     d2h = len(my_views) * _LAST_IO["d2h"]
     return {"value": round(npx * len(my_views) * world / dt / 1e6, 3), "unit": "Mpix/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "ms_per_step": round(dt * 1e3, 3),
             "api": f"render_with_gradients(numpy float64 SceneArrays, chunk_size={a.chunk_size})"}
+
+
+def e2e_dp(a, arrs, cams, model, my_views, world):
+    """N > 1 end to end through the data-parallel API: every step uploads the
+    scene (float64 host arrays -> fp32) and this rank's seeds from the host,
+    renders its views into the gradient buffer, all-reduces it across the
+    ranks (sparse, NCCL) and downloads the summed gradients to pinned host
+    memory.  Wall clock per step, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_2603_02887_b200 import DeviceScene
+    from paper_2603_02887_b200.dp import DataParallelStep, GradBuffer, device_view_renderer
+    from paper_2603_02887_b200.render import _h2d_f32
+    from paper_2603_02887_b200.scenes import canonical_seed
+    host_seeds = {v: canonical_seed(a.width, a.height, v) for v in my_views[:8]}
+    dev = DeviceScene.from_arrays(arrs)
+    seed_dev = {}
+    grads = GradBuffer(len(arrs), arrs.sh.shape[2], device="cuda")
+    out = torch.empty(grads.flat.numel(), dtype=torch.float32, pin_memory=True)
+    rv = device_view_renderer(dev, model, np.zeros(3), cams, lambda v: seed_dev[v % 8],
+                              chunk_size=a.chunk_size, pool=a.pool)
+    step = DataParallelStep(len(cams), int(os.environ.get("RANK", "0")), world, grads, rv)
+
+    def one():
+        for k in DeviceScene.FIELDS:  # upload the scene
+            x = getattr(arrs, k)
+            setattr(dev, k, _h2d_f32(np.asarray(x).reshape(tuple(getattr(dev, k).shape)),
+                                     dev.centers.device, "e2e_" + k))
+        for v, sd in host_seeds.items():
+            seed_dev[v % 8] = _h2d_f32(sd, dev.centers.device, f"e2e_seed{v % 8}")
+        g = step()
+        out.copy_(g.flat, non_blocking=True)
+        torch.cuda.synchronize()
+
+    one()
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(a.e2e_steps):
+        one()
+    dt = (time.perf_counter() - t0) / a.e2e_steps
+    t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dt = float(t.item())
+    npx = a.width * a.height
+    h2d = sum(int(np.prod(np.shape(getattr(arrs, k)))) * 4 for k in DeviceScene.FIELDS) \
+        + len(host_seeds) * npx * 3 * 4
+    d2h = grads.flat.numel() * 4
+    return {"value": round(npx * len(my_views) * world / dt / 1e6, 3), "unit": "Mpix/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "ms_per_step": round(dt * 1e3, 3),
+            "api": "DataParallelStep (device_view_renderer + sparse NCCL all-reduce) with the "
+                   "scene and seeds uploaded from host float64 arrays and the summed gradients "
+                   "downloaded, every step"}
 
 
 def reference_arm(a, rank, model):

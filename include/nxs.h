@@ -250,6 +250,46 @@ int nxs_records_export(nxs_view* view, float* records, void* stream);
  * data-parallel reduction). */
 int nxs_touched_export(nxs_view* view, int32_t* gids, int64_t* count, void* stream);
 
+/* Sizing history of a view — the estimates its device-sized first depth
+ * phase is planned from (ranks, pairs, key bins, the last rank its tiles
+ * needed, the speculated phase count) and the camera they belong to — as an
+ * opaque blob of nxs_view_history_bytes() bytes.  A caller that cycles many
+ * cameras through a few workspaces saves each camera's history after its
+ * call and loads it into the workspace before the next call of that camera,
+ * so every camera keeps the sync-free path.  Loading ends the workspace's
+ * last forward (no backward of it afterwards). */
+int64_t nxs_view_history_bytes(void);
+int nxs_view_history_save(nxs_view* view, void* blob);
+int nxs_view_history_load(nxs_view* view, const void* blob);
+
+/* ---- data-parallel gradient plumbing (no reference
+ * counterpart: the reference renders one view per iteration,
+ * optimizer.py:393-408) ------------------------------------------------
+ * A rank's gradient buffer `flat` is float32, n Gaussians, field after
+ * field: [centers (n,3) | scales (n,3) | quats (n,4) | opacities (n) |
+ * sh (n,3,C)] (paper_2603_02887_b200/dp.py GradBuffer); a Gaussian's row is
+ * 11 + 3C floats.  `mask` is one byte per Gaussian. */
+
+/* mask[g] = 1 for every Gaussian the view's last backward wrote (async,
+ * no host sync): the union over a rank's views is its touched set. */
+int nxs_touched_mark(nxs_view* view, uint8_t* mask, void* stream);
+
+/* Zero the rows of flagged Gaussians and clear their flags (the next step's
+ * clear touches only last step's rows, instead of the whole buffer). */
+int nxs_grads_zero_masked(float* flat, int64_t n, int32_t sh_coeffs, uint8_t* mask,
+                          void* stream);
+
+/* index[0..count) = flagged Gaussians, ascending; *count (HOST) — the call
+ * synchronises `stream` to read it (the collective needs the size). */
+int nxs_grads_select(const uint8_t* mask, int64_t n, int32_t* index, int64_t* count,
+                     void* stream);
+
+/* packed (count x (11+3C)) <- rows index[0..count) of flat, and back. */
+int nxs_grads_gather(const float* flat, int64_t n, int32_t sh_coeffs, const int32_t* index,
+                     int64_t count, float* packed, void* stream);
+int nxs_grads_scatter(float* flat, int64_t n, int32_t sh_coeffs, const int32_t* index,
+                      int64_t count, const float* packed, void* stream);
+
 /* ---- train-step neighbours ---------------------------- */
 
 /* Image loss (reference optimizer.py:128-152 loss(), :68-111 ssim(),

@@ -45,6 +45,14 @@ SYMBOLS = (
     "nxs_binning_export",
     "nxs_records_export",
     "nxs_touched_export",
+    "nxs_touched_mark",
+    "nxs_view_history_bytes",
+    "nxs_view_history_save",
+    "nxs_view_history_load",
+    "nxs_grads_zero_masked",
+    "nxs_grads_select",
+    "nxs_grads_gather",
+    "nxs_grads_scatter",
     "nxs_loss_workspace_bytes",
     "nxs_image_loss",
     "nxs_adam_step",
@@ -163,6 +171,15 @@ def lib():
     h.nxs_binning_export.argtypes = [vp, vp, vp, vp, vp]
     h.nxs_records_export.argtypes = [vp, vp, vp]
     h.nxs_touched_export.argtypes = [vp, vp, C.POINTER(C.c_int64), vp]
+    h.nxs_touched_mark.argtypes = [vp, vp, vp]
+    h.nxs_view_history_bytes.restype = i64
+    h.nxs_view_history_bytes.argtypes = []
+    h.nxs_view_history_save.argtypes = [vp, vp]
+    h.nxs_view_history_load.argtypes = [vp, vp]
+    h.nxs_grads_zero_masked.argtypes = [vp, i64, i32, vp, vp]
+    h.nxs_grads_select.argtypes = [vp, i64, vp, C.POINTER(C.c_int64), vp]
+    h.nxs_grads_gather.argtypes = [vp, i64, i32, vp, i64, vp, vp]
+    h.nxs_grads_scatter.argtypes = [vp, i64, i32, vp, i64, vp, vp]
     h.nxs_loss_workspace_bytes.argtypes = [i32, i32]
     h.nxs_loss_workspace_bytes.restype = i64
     h.nxs_image_loss.argtypes = [vp, vp, i32, i32, C.c_double, i32, vp, vp, vp, vp]
@@ -171,12 +188,34 @@ def lib():
                                       C.POINTER(C.c_double), vp, vp, vp, vp, vp, vp, vp, vp, vp]
     for name in SYMBOLS:
         if name not in ("nxs_error_string", "nxs_last_error", "nxs_view_bytes",
-                        "nxs_loss_workspace_bytes"):
+                        "nxs_loss_workspace_bytes", "nxs_view_history_bytes"):
             getattr(h, name).restype = C.c_int
     if h.nxs_abi_version() != 2:
         raise NativeLibraryError("libnxs ABI version mismatch")
     _lib = h
     return h
+
+
+def grads_zero_masked(flat, n, sh_coeffs, mask, stream=None):
+    _check(lib().nxs_grads_zero_masked(_ptr(flat), int(n), int(sh_coeffs), _ptr(mask),
+                                       _stream_ptr(stream)))
+
+
+def grads_select(mask, n, index, stream=None) -> int:
+    cnt = C.c_int64(0)
+    _check(lib().nxs_grads_select(_ptr(mask), int(n), _ptr(index), C.byref(cnt),
+                                  _stream_ptr(stream)))
+    return int(cnt.value)
+
+
+def grads_gather(flat, n, sh_coeffs, index, count, packed, stream=None):
+    _check(lib().nxs_grads_gather(_ptr(flat), int(n), int(sh_coeffs), _ptr(index), int(count),
+                                  _ptr(packed), _stream_ptr(stream)))
+
+
+def grads_scatter(flat, n, sh_coeffs, index, count, packed, stream=None):
+    _check(lib().nxs_grads_scatter(_ptr(flat), int(n), int(sh_coeffs), _ptr(index), int(count),
+                                   _ptr(packed), _stream_ptr(stream)))
 
 
 def _check(code: int):
@@ -280,6 +319,19 @@ class View:
 
     def records_export(self, out, stream=None):
         _check(self._h.nxs_records_export(self._p, _ptr(out), _stream_ptr(stream)))
+
+    def history_save(self) -> bytes:
+        """The view's sizing history (opaque; see nxs_view_history_save)."""
+        buf = C.create_string_buffer(int(self._h.nxs_view_history_bytes()))
+        _check(self._h.nxs_view_history_save(self._p, buf))
+        return buf.raw
+
+    def history_load(self, blob: bytes):
+        _check(self._h.nxs_view_history_load(self._p, C.c_char_p(blob)))
+
+    def touched_mark(self, mask, stream=None):
+        """mask[g] = 1 for the Gaussians the last backward wrote (async)."""
+        _check(self._h.nxs_touched_mark(self._p, _ptr(mask), _stream_ptr(stream)))
 
     def touched_export(self, out=None, stream=None) -> int:
         """Gaussians the last backward wrote (into ``out``, int32 CUDA with

@@ -127,6 +127,8 @@ void launch_blend_fwd(bool, int, const FwdArgs&, const CamDev&, const ModelDev&,
 void launch_blend_bwd(bool, int, const float4*, const float4*, const PhaseLists&, const CamDev&,
                       const ModelDev&, float, double, const float*, const float*,
                       const PixCache&, double*, uint8_t*, Counters*, cudaStream_t);
+void launch_touched_mark(const uint32_t*, const unsigned long long*, int64_t, uint8_t*,
+                         cudaStream_t);
 void launch_det_reduce(int64_t, const uint32_t*, const int4*, int, const PhaseLists&,
                        const uint8_t*, double*, cudaStream_t);
 void launch_chain(const float*, const float*, int, int64_t, const uint32_t*, double*, uint8_t*,
@@ -222,6 +224,7 @@ struct nxs_view {
   Buf tile_base;
   bool bases_valid = false;
   int bases_ntiles = 0;
+  CamDev bases_cam{};  // the camera the capacities were derived for
   int64_t bases_bound = 0;  // >= base[n_tiles], the pair buffer it needs
   bool async_bases = false;  // this call's device-sized pass uses them
   int64_t bases_maxcap = 0;  // the largest per-tile capacity
@@ -422,6 +425,14 @@ struct CaptureGuard {
     }
   }
 };
+
+inline bool same_camera(const CamDev& a, const CamDev& b) {
+  for (int i = 0; i < 3; ++i)
+    if (a.o[i] != b.o[i]) return false;
+  for (int i = 0; i < 9; ++i)
+    if (a.R[i] != b.R[i]) return false;
+  return a.f == b.f && a.cx == b.cx && a.cy == b.cy && a.W == b.W && a.H == b.H;
+}
 
 // Makes the view's device current for the duration of a call (a view's
 // workspace, events and graph belong to the device it was created on) and
@@ -657,6 +668,11 @@ int finish_async_check(nxs_view* v, bool& ok) {
   v->async_pending = false;
   if (!ok) {
     ++v->stats.n_redo;
+    if (std::getenv("NXS_DEBUG_PLAN"))
+      std::fprintf(stderr, "redo: device-sized pass flags=%llu n0=%lld/%lld pairs=%llu/%lld\n",
+                   (unsigned long long)v->host_small[25], (long long)n0,
+                   (long long)v->async_cap0, (unsigned long long)pairs,
+                   (long long)v->async_capp);
     v->est_n0 = 0;  // the next pass sizes phase 0 exactly again
     return NXS_OK;
   }
@@ -776,6 +792,11 @@ int forward_impl(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
   // ---- depth phases [R_p, R_{p+1}): R_1 = first phase, then x8.  The
   // chunked order cuts phases on chunk boundaries (nothing is pending
   // there); the exact order keeps per-pixel pending state: one phase.
+  // a view whose camera changed since its last call (a pooled workspace
+  // cycling the views of a step) sizes its device-sized pass from a nearby
+  // camera's counts: wider headroom (fewer redone passes)
+  const bool cam_moved = !same_camera(v->cam, cam);
+  const int64_t hdiv = cam_moved ? 4 : 8;
   int64_t R[MAX_PHASES + 1];
   int n_ph = 0;
   {
@@ -800,8 +821,9 @@ int forward_impl(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
       }
       const int64_t need = (int64_t)v->hint;
       if (need > 0 && need < P) {
-        const int64_t target = need + 1 + need / 16 + 1024;
-        r1 = need < r1 ? std::min(r1, target) : target;
+        const int64_t target = cam_moved ? need + need / 4 + 4096 : need + 1 + need / 16 + 1024;
+        // (a nearby camera's need is only a guess: never below the default)
+        r1 = cam_moved ? std::max(r1, target) : need < r1 ? std::min(r1, target) : target;
       }
       // device-sized phase-0 estimates that fell short: size exactly again
       if (need > 0 && v->est_n0 > 0 && need >= v->est_n0) v->est_n0 = 0;
@@ -835,8 +857,10 @@ int forward_impl(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
   const cudaStream_t s_caller = s;
   // device-sized phase 0 (no host sync before the first forward): needs
   // estimates from this view's previous call and a later phase to verify at
+  // (a new camera's depth-key histogram differs: its phase-0 bins and pair
+  // count are sized exactly, with host reads, rather than risk a redo)
   bool async0 = v->est_n0 > 0 && v->est_pairs >= 0 && v->est_bin0 >= 0 && n_ph >= 2 &&
-                spec_phase >= 0 && !chunked && !exact;
+                spec_phase >= 0 && !chunked && !exact && !cam_moved;
   if (std::getenv("NXS_DEBUG_PLAN"))
     std::fprintf(stderr, "plan P=%lld n_ph=%d R1=%lld async0=%d est_n0=%lld est_bin0=%d hint=%llu\n",
                  (long long)P, n_ph, (long long)R[1], (int)async0, (long long)v->est_n0,
@@ -851,9 +875,12 @@ retry_sort:
   if (async0) {
     // every buffer the device-sized phase 0 touches is sized up front: no
     // allocation may move a buffer once its pointer is in the captured graph
-    v->async_bases = v->bases_valid && v->bases_ntiles == n_tiles && !getenv("NXS_NO_BASES");
+    // per-tile capacities are camera-specific: a workspace shared by several
+    // views (dp.py pools them) falls back to the counting pass on a new camera
+    v->async_bases = v->bases_valid && v->bases_ntiles == n_tiles && same_camera(v->bases_cam, cam) &&
+                     !getenv("NXS_NO_BASES");
     const int64_t capp =
-        v->async_bases ? v->bases_bound : v->est_pairs + v->est_pairs / 8 + 8192;
+        v->async_bases ? v->bases_bound : v->est_pairs + v->est_pairs / hdiv + 8192 * (8 / hdiv);
     // (the scratch the generic setup below sizes for a full sort / scan)
     size_t t_scan = 0, t_sel = 0, t_full = 0;
     NXS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t_full, v->k32a.as<uint32_t>(),
@@ -965,14 +992,14 @@ retry_sort:
       if (async0) {
         // phase 0 sized from the previous call; the last bin it may use is
         // checked on the device (k_phase_select) and verified later
-        ph_bin[0] = std::min(4095, v->est_bin0 + 2);
+        ph_bin[0] = std::min(4095, v->est_bin0 + (cam_moved ? 8 : 2));
         launch_phase_select(v->ph_hist.as<unsigned int>(), reinterpret_cast<int64_t*>(dsel + 32),
                             n_ph - 1, P, dsel, s, ph_bin[0], dsmall + 10,
                             v->bin_pos.as<uint32_t>(), reinterpret_cast<int*>(dsel + 48));
         NXS_LAUNCHED("phase_select");
-        v->async_cap0 = std::min<int64_t>(P, v->est_n0 + v->est_n0 / 8 + 2048);
+        v->async_cap0 = std::min<int64_t>(P, v->est_n0 + v->est_n0 / hdiv + 2048 * (8 / hdiv));
         v->async_capp =
-            v->async_bases ? v->bases_bound : v->est_pairs + v->est_pairs / 8 + 8192;
+            v->async_bases ? v->bases_bound : v->est_pairs + v->est_pairs / hdiv + 8192 * (8 / hdiv);
         R[0] = 0;
         R[1] = v->async_cap0;  // ranks phase 0 may occupy; later bounds come with the check
       }
@@ -1366,6 +1393,7 @@ retry_sort:
           NXS_LAUNCHED("make_bases");
           v->bases_valid = true;
           v->bases_ntiles = n_tiles;
+          v->bases_cam = cam;
           v->bases_bound = (int64_t)n_pairs + (int64_t)n_pairs / 8 + 8 * (int64_t)n_tiles + 1;
           v->bases_maxcap = (int64_t)max_seg + (int64_t)max_seg / 8 + 8;
         }
@@ -1746,6 +1774,9 @@ int nxs_forward_backward(nxs_view* v, const nxs_scene* scene, const nxs_camera* 
     if (!ok || (unsigned)v->host_small[3] != 0) {
       // more depth phases were needed: drop the moments, redo both passes
       ++v->stats.n_redo;
+      if (std::getenv("NXS_DEBUG_PLAN"))
+        std::fprintf(stderr, "redo: speculation ok=%d active_tiles=%u phases_needed=%d\n",
+                     (int)ok, (unsigned)v->host_small[3], v->phases_needed);
       if ((rc = backward_chain(v, scene, nullptr, nullptr, nullptr, nullptr, nullptr, s)))
         return rc;
       v->phases_needed = 0;
@@ -1888,6 +1919,77 @@ int nxs_touched_export(nxs_view* v, int32_t* gids, int64_t* count, void* stream_
   *count = (int64_t)n;
   if (gids && n)
     NXS_CUDA(cudaMemcpyAsync(gids, v->tlist.p, (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
+  return NXS_OK;
+}
+
+// sizing history of a view (the device-sized first phase's estimates), so a
+// caller cycling many cameras through a few workspaces keeps each camera's
+struct ViewHistory {
+  uint32_t magic;
+  int32_t est_bin0, phases_needed, valid;
+  int64_t est_n0, est_pairs;
+  unsigned long long hint;
+  CamDev cam;
+};
+constexpr uint32_t HIST_MAGIC = 0x4e585348u;
+
+int64_t nxs_view_history_bytes(void) { return (int64_t)sizeof(ViewHistory); }
+
+int nxs_view_history_save(nxs_view* v, void* blob) {
+  if (!v || !blob) return fail(NXS_ERR_INVALID, "null argument");
+  DevGuard dg(v->device);
+  if (v->hint_pending && v->ev_hint) {  // the hint lands behind the last forward
+    NXS_CUDA(cudaEventSynchronize(v->ev_hint));
+    v->hint = v->host_small[30];
+    v->hint_pending = false;
+  }
+  ViewHistory h{};
+  h.magic = HIST_MAGIC;
+  h.valid = v->have_fwd ? 1 : 0;
+  h.est_n0 = v->est_n0;
+  h.est_pairs = v->est_pairs;
+  h.est_bin0 = v->est_bin0;
+  h.phases_needed = v->phases_needed;
+  h.hint = v->hint;
+  h.cam = v->cam;
+  std::memcpy(blob, &h, sizeof(h));
+  return NXS_OK;
+}
+
+int nxs_view_history_load(nxs_view* v, const void* blob) {
+  if (!v || !blob) return fail(NXS_ERR_INVALID, "null argument");
+  ViewHistory h;
+  std::memcpy(&h, blob, sizeof(h));
+  if (h.magic != HIST_MAGIC) return fail(NXS_ERR_INVALID, "not a view history blob");
+  DevGuard dg(v->device);
+  if (v->hint_pending && v->ev_hint) NXS_CUDA(cudaEventSynchronize(v->ev_hint));
+  v->hint_pending = false;
+  // the workspace now serves another camera: its last forward is gone
+  v->have_fwd = false;
+  v->tlist_valid = false;
+  if (!h.valid) {
+    v->est_n0 = 0;
+    v->hint = 0;
+    v->phases_needed = 0;
+    v->cam = CamDev{};
+    return NXS_OK;
+  }
+  v->est_n0 = h.est_n0;
+  v->est_pairs = h.est_pairs;
+  v->est_bin0 = h.est_bin0;
+  v->phases_needed = h.phases_needed;
+  v->hint = h.hint;
+  v->cam = h.cam;
+  return NXS_OK;
+}
+
+int nxs_touched_mark(nxs_view* v, uint8_t* mask, void* stream_) {
+  if (!v || !mask) return fail(NXS_ERR_INVALID, "null argument");
+  if (!v->tlist_valid) return fail(NXS_ERR_STATE, "no backward recorded in this view");
+  DevGuard dg(v->device);
+  launch_touched_mark(v->tlist.as<uint32_t>(), v->tcount.as<unsigned long long>(), v->P, mask,
+                      (cudaStream_t)stream_);
+  NXS_LAUNCHED("touched_mark");
   return NXS_OK;
 }
 
