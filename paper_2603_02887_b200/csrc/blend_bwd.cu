@@ -149,6 +149,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 4)
     const int c0 = lists.cum[ph][tile];
     const int base = max(c0, hi - BWD_BATCH);  // virtual
     const int n = hi - base;
+    NXS_CHECK(n > 0 && n <= BWD_BATCH && base >= c0);
     int nph = ph, nhi = hi;
     const bool more = next_batch(nph, nhi);
     __syncthreads();  // every thread is past the previous batch's flush
@@ -169,6 +170,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 4)
 
       for (int j = min(n - 1, wlast - base); j >= 0; --j) {
         const int idx = base + j;
+        NXS_CHECK(j >= 0 && j < n);
         // both pixels' contributions (lane x: pixel a, y: b), zero where a
         // pixel does not contribute, so the moments need no separate masking
         PairOut po;
@@ -260,6 +262,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 4)
         // fixed-order sum over the warps; one partial per (tile, entry):
         // k_det_reduce adds them per rank in tile order
         const int64_t slot0 = lists.poff[ph] + lists.ranges[ph][tile].x + (base - c0);
+        NXS_CHECK(lists.ranges[ph][tile].x + (base - c0) + n <= lists.ranges[ph][tile].y);
         for (int k = tid; k < n * NMOM; k += BWD_THREADS) {
           float val = s_acc[k];
 #pragma unroll

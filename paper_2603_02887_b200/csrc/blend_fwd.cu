@@ -98,6 +98,7 @@ __global__ void __launch_bounds__(TILE_PIX, NXS_FWD_MINB)
   const int vbase = cum_in[tile] - rg.x;  // list position -> virtual per-tile index
   auto stage = [&](int buf, int base) {
     const int n = min(FWD_BATCH, rg.y - base);
+    NXS_CHECK(n > 0 && n <= FWD_BATCH && base >= rg.x);
     for (int k = tid; k < n * REC_F4; k += TILE_PIX) {
       const int e = k >> 3, part = k & 7;
       cp_async16(&s_rec[buf][e][part], records + (size_t)pairs[base + e] * REC_F4 + part);

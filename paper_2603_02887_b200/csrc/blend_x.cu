@@ -217,6 +217,7 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
   int ring_lo = 0;  // list positions [ring_lo, current batch end) are staged
   auto commit_front = [&]() {
     const int slot = head * TILE_PIX + tid;
+    NXS_CHECK(nb > 0 && head >= 0 && head < XBUF);
     const int pos = bp[slot];
     head = (head + 1) & (XBUF - 1);
     --nb;
@@ -225,6 +226,7 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
     constexpr int K0 = keeps_alpha(XBUF) ? 4 : 0, K1 = keeps_alpha(XBUF) ? 7 : REC_F4;
     uint32_t rank;
     if (pos >= ring_lo) {  // (carried entries have pos < 0 and take the global path)
+      NXS_CHECK(pos >= ring_lo && pos < ring_lo + 2 * XBT);
       const float4* rec = s_ring[pos % (2 * XBT)];
       rank = s_ring_rank[pos % (2 * XBT)];
 #pragma unroll
@@ -246,6 +248,7 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
     }
     float E0, E1, E2;
     emission(r[4], r[5], r[6], pc, E0, E1, E2);
+    NXS_CHECK(s.count >= 0 && s.count < max_splats);
     myseq[(size_t)s.count * npix] = (int32_t)rank;
     composite<FAM>(s, m, max_splats, alpha, E0, E1, E2);
   };
@@ -253,6 +256,7 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
   const int2 rg = ranges[tile];
   for (int base = rg.x; base < rg.y; base += XBT) {
     const int n = min(XBT, rg.y - base);
+    NXS_CHECK(n > 0 && n <= XBT);
     __syncthreads();
     if (tid < n) {
       const uint32_t rk = pairs[base + tid];
@@ -319,6 +323,7 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
           --i;
         }
         const int f = (head + i) & (XBUF - 1);
+        NXS_CHECK(nb < XBUF && i >= 0 && i <= nb);
         bt[f * TILE_PIX + tid] = tpk;
         bp[f * TILE_PIX + tid] = pos;
         if constexpr (keeps_alpha(XBUF)) ba[f * TILE_PIX + tid] = t.alpha;
@@ -460,6 +465,7 @@ __global__ void __launch_bounds__(BWDX_THREADS)
   int cur[2], nxt[2];
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
+    NXS_CHECK(ptr[q] < max_splats);
     cur[q] = ptr[q] >= 0 ? myseq[q][(size_t)ptr[q] * npix] : -1;
     nxt[q] = ptr[q] >= 1 ? myseq[q][(size_t)(ptr[q] - 1) * npix] : -1;
   }

@@ -16,6 +16,18 @@
 
 #include <mutex>
 
+// NXS_CHECK(cond): device bounds checks of the blend kernels' shared-memory
+// rings, staged batches, commit sequences and list indices, compiled in by
+// the `checks` variant (python -m paper_2603_02887_b200.build --variant=checks
+// -DNXS_CHECKS); the GPU tests run against it (tools/checks_gpu.sh), in
+// place of compute-sanitizer, which this GPU pool does not allow.
+#ifdef NXS_CHECKS
+#include <cassert>
+#define NXS_CHECK(cond) assert(cond)
+#else
+#define NXS_CHECK(cond) ((void)0)
+#endif
+
 namespace nxs {
 
 // Host: run `f` once per (call site, CUDA device) — kernel attributes and
