@@ -325,6 +325,19 @@ typedef struct {
 } nxs_adam_group;
 int nxs_adam_step(const nxs_adam_group* groups, int64_t step, double lr_mult,
                   unsigned long long* nan_skips, void* stream);
+/* The same step in float64 (param / grad / m / v double): the numpy
+ * drop-in's float64 parameters update without a float32 round trip, like
+ * the reference optimizer (optimizer.py:173-204). */
+typedef struct {
+    double* param;
+    const double* grad;
+    double* m;
+    double* v;
+    int64_t count;
+    double lr;
+} nxs_adam_group_f64;
+int nxs_adam_step_f64(const nxs_adam_group_f64* groups, int64_t step, double lr_mult,
+                      unsigned long long* nan_skips, void* stream);
 
 /* ---- per-ray batched compositing --------------------- */
 

@@ -56,6 +56,7 @@ SYMBOLS = (
     "nxs_loss_workspace_bytes",
     "nxs_image_loss",
     "nxs_adam_step",
+    "nxs_adam_step_f64",
     "nxs_composite_batch",
 )
 
@@ -184,6 +185,7 @@ def lib():
     h.nxs_loss_workspace_bytes.restype = i64
     h.nxs_image_loss.argtypes = [vp, vp, i32, i32, C.c_double, i32, vp, vp, vp, vp]
     h.nxs_adam_step.argtypes = [C.POINTER(AdamGroup), i64, C.c_double, vp, vp]
+    h.nxs_adam_step_f64.argtypes = [C.POINTER(AdamGroup), i64, C.c_double, vp, vp]
     h.nxs_composite_batch.argtypes = [C.POINTER(Model), vp, vp, vp, i64, i64,
                                       C.POINTER(C.c_double), vp, vp, vp, vp, vp, vp, vp, vp, vp]
     for name in SYMBOLS:

@@ -328,78 +328,138 @@ __global__ void k_loss_final(const double* __restrict__ part, int nprep,
 // bounded Adam (optimizer.py:173-204): groups centers, scales, quats,
 // opacities, sh; non-finite gradients are dropped and counted
 // ---------------------------------------------------------------------------
+template <class T>
+struct AdamGroupT {
+  T* param;
+  const T* grad;
+  T* m;
+  T* v;
+  int64_t count;
+  double lr;
+};
+
+template <class T>
 struct AdamArgs {
-  nxs_adam_group g[5];
-  float b1, b2, omb1, omb2, inv_bc1, inv_bc2, eps, lr_mult;
+  AdamGroupT<T> g[5];
+  T b1, b2, omb1, omb2, inv_bc1, inv_bc2, eps, lr_mult;
   unsigned long long* nan_skips;
 };
 
-__device__ __forceinline__ float adam_one(const AdamArgs& a, float p, float gr, float& m,
-                                          float& v, float lr, unsigned& bad) {
+template <class T>
+__device__ __forceinline__ T adam_one(const AdamArgs<T>& a, T p, T gr, T& m, T& v, T lr,
+                                      unsigned& bad) {
   if (!isfinite(gr)) {
     ++bad;
-    gr = 0.f;
+    gr = T(0);
   }
   m = a.b1 * m + a.omb1 * gr;
   v = a.b2 * v + a.omb2 * gr * gr;
-  return p - lr * (m * a.inv_bc1) / (sqrtf(v * a.inv_bc2) + a.eps);
+  return p - lr * (m * a.inv_bc1) / (sqrt(v * a.inv_bc2) + a.eps);
 }
 
-__device__ __forceinline__ float clamp_group(int gi, float p) {
-  if (gi == 1) return fmaxf(p, 1e-6f);                                    // SCALE_MIN
-  if (gi == 3) return fminf(fmaxf(p, 1e-4f), (float)(1.0 - 1e-6));         // opacity bounds
+template <class T>
+__device__ __forceinline__ T clamp_group(int gi, T p) {
+  if (gi == 1) return p < T(1e-6) ? T(1e-6) : p;  // SCALE_MIN
+  if (gi == 3) {                                   // opacity bounds
+    const T hi = (T)(1.0 - 1e-6);
+    return p < T(1e-4) ? T(1e-4) : (p > hi ? hi : p);
+  }
   return p;
 }
 
-// one group per blockIdx.y; 16-B vectors (a quaternion row is one vector,
-// renormalised after its update), scalar tail
-__global__ void __launch_bounds__(256) k_adam(AdamArgs a) {
+// one group per blockIdx.y; fp32: 16-B vectors (a quaternion row is one
+// vector, renormalised after its update), scalar tail; fp64 (the numpy
+// drop-in's float64 parameters, updated without an fp32 round trip): scalar
+template <class T>
+__global__ void __launch_bounds__(256) k_adam(AdamArgs<T> a) {
   const int gi = blockIdx.y;
-  const nxs_adam_group& g = a.g[gi];
+  const AdamGroupT<T>& g = a.g[gi];
   if (!g.param || g.count <= 0) return;
-  const float lr = (float)g.lr * a.lr_mult;
+  const T lr = (T)g.lr * a.lr_mult;
   unsigned bad = 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool vec = ((reinterpret_cast<uintptr_t>(g.param) | reinterpret_cast<uintptr_t>(g.grad) |
-                     reinterpret_cast<uintptr_t>(g.m) | reinterpret_cast<uintptr_t>(g.v)) & 15) == 0;
-  const int64_t n4 = vec ? g.count / 4 : 0;
-  for (int64_t r = t0; r < n4; r += stride) {
-    float4 p = reinterpret_cast<const float4*>(g.param)[r];
-    const float4 gr = __ldcs(reinterpret_cast<const float4*>(g.grad) + r);
-    float4 m = reinterpret_cast<const float4*>(g.m)[r];
-    float4 v = reinterpret_cast<const float4*>(g.v)[r];
-    p.x = clamp_group(gi, adam_one(a, p.x, gr.x, m.x, v.x, lr, bad));
-    p.y = clamp_group(gi, adam_one(a, p.y, gr.y, m.y, v.y, lr, bad));
-    p.z = clamp_group(gi, adam_one(a, p.z, gr.z, m.z, v.z, lr, bad));
-    p.w = clamp_group(gi, adam_one(a, p.w, gr.w, m.w, v.w, lr, bad));
-    if (gi == 2) {  // quaternion row
-      const float n = sqrtf(p.x * p.x + p.y * p.y + p.z * p.z + p.w * p.w);
-      p.x /= n;
-      p.y /= n;
-      p.z /= n;
-      p.w /= n;
+  bool vec = false;
+  int64_t n4 = 0;
+  if constexpr (sizeof(T) == 4) {
+    vec = ((reinterpret_cast<uintptr_t>(g.param) | reinterpret_cast<uintptr_t>(g.grad) |
+            reinterpret_cast<uintptr_t>(g.m) | reinterpret_cast<uintptr_t>(g.v)) & 15) == 0;
+    n4 = vec ? g.count / 4 : 0;
+    for (int64_t r = t0; r < n4; r += stride) {
+      float4 p = reinterpret_cast<const float4*>(g.param)[r];
+      const float4 gr = __ldcs(reinterpret_cast<const float4*>(g.grad) + r);
+      float4 m = reinterpret_cast<const float4*>(g.m)[r];
+      float4 v = reinterpret_cast<const float4*>(g.v)[r];
+      p.x = clamp_group<T>(gi, adam_one<T>(a, p.x, gr.x, m.x, v.x, lr, bad));
+      p.y = clamp_group<T>(gi, adam_one<T>(a, p.y, gr.y, m.y, v.y, lr, bad));
+      p.z = clamp_group<T>(gi, adam_one<T>(a, p.z, gr.z, m.z, v.z, lr, bad));
+      p.w = clamp_group<T>(gi, adam_one<T>(a, p.w, gr.w, m.w, v.w, lr, bad));
+      if (gi == 2) {  // quaternion row
+        const float n = sqrtf(p.x * p.x + p.y * p.y + p.z * p.z + p.w * p.w);
+        p.x /= n;
+        p.y /= n;
+        p.z /= n;
+        p.w /= n;
+      }
+      reinterpret_cast<float4*>(g.param)[r] = p;
+      reinterpret_cast<float4*>(g.m)[r] = m;
+      reinterpret_cast<float4*>(g.v)[r] = v;
     }
-    reinterpret_cast<float4*>(g.param)[r] = p;
-    reinterpret_cast<float4*>(g.m)[r] = m;
-    reinterpret_cast<float4*>(g.v)[r] = v;
   }
-  if (gi == 2 && !vec) {  // unaligned quaternions: row by row
+  if (gi == 2 && !vec) {  // quaternions row by row
     for (int64_t r = t0; r < g.count / 4; r += stride) {
-      float q[4];
+      T q[4];
       for (int k = 0; k < 4; ++k) {
         const int64_t i = 4 * r + k;
-        q[k] = adam_one(a, g.param[i], g.grad[i], g.m[i], g.v[i], lr, bad);
+        q[k] = adam_one<T>(a, g.param[i], g.grad[i], g.m[i], g.v[i], lr, bad);
       }
-      const float n = sqrtf(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+      const T n = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
       for (int k = 0; k < 4; ++k) g.param[4 * r + k] = q[k] / n;
     }
   } else if (gi != 2) {
     for (int64_t i = 4 * n4 + t0; i < g.count; i += stride)
-      g.param[i] = clamp_group(gi, adam_one(a, g.param[i], g.grad[i], g.m[i], g.v[i], lr, bad));
+      g.param[i] = clamp_group<T>(gi, adam_one<T>(a, g.param[i], g.grad[i], g.m[i], g.v[i], lr,
+                                                  bad));
   }
   for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
   if ((threadIdx.x & 31) == 0 && bad) atomicAdd(a.nan_skips, (unsigned long long)bad);
+}
+
+template <class T, class G>
+int adam_step(const G* groups, int64_t step, double lr_mult, unsigned long long* nan_skips,
+              void* stream) {
+  if (!groups || !nan_skips || step < 1)
+    return nxs::set_last_error(NXS_ERR_INVALID, "null argument or step < 1");
+  AdamArgs<T> a;
+  int64_t most = 0;
+  for (int k = 0; k < 5; ++k) {
+    a.g[k] = AdamGroupT<T>{groups[k].param, groups[k].grad, groups[k].m, groups[k].v,
+                           groups[k].count, groups[k].lr};
+    if (a.g[k].param && (!a.g[k].grad || !a.g[k].m || !a.g[k].v))
+      return nxs::set_last_error(NXS_ERR_INVALID, "adam group without grad/m/v");
+    if (k == 2 && a.g[k].count % 4 != 0)
+      return nxs::set_last_error(NXS_ERR_INVALID, "quaternion count not a multiple of 4");
+    most = std::max<int64_t>(most, a.g[k].param ? a.g[k].count : 0);
+  }
+  const double b1 = 0.9, b2 = 0.999;  // ADAM_BETA1/2, optimizer.py:42-44
+  a.b1 = (T)b1;
+  a.b2 = (T)b2;
+  a.omb1 = (T)(1.0 - b1);
+  a.omb2 = (T)(1.0 - b2);
+  a.inv_bc1 = (T)(1.0 / (1.0 - std::pow(b1, (double)step)));
+  a.inv_bc2 = (T)(1.0 / (1.0 - std::pow(b2, (double)step)));
+  a.eps = (T)1e-8;
+  a.lr_mult = (T)lr_mult;
+  a.nan_skips = nan_skips;
+  if (most == 0) return NXS_OK;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t want = (most / 4 + 255) / 256;
+  const dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * 8)), 5);
+  k_adam<T><<<grid, 256, 0, (cudaStream_t)stream>>>(a);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? NXS_OK : nxs::set_last_error(NXS_ERR_CUDA, cudaGetErrorString(e));
 }
 
 unsigned long long g_win_dev = 0;  // devices with the window and attributes set
@@ -468,37 +528,12 @@ int nxs_image_loss(const float* rendered, const float* target, int32_t height, i
 
 int nxs_adam_step(const nxs_adam_group* groups, int64_t step, double lr_mult,
                   unsigned long long* nan_skips, void* stream) {
-  if (!groups || !nan_skips || step < 1)
-    return nxs::set_last_error(NXS_ERR_INVALID, "null argument or step < 1");
-  AdamArgs a;
-  int64_t most = 0;
-  for (int k = 0; k < 5; ++k) {
-    a.g[k] = groups[k];
-    if (a.g[k].param && (!a.g[k].grad || !a.g[k].m || !a.g[k].v))
-      return nxs::set_last_error(NXS_ERR_INVALID, "adam group without grad/m/v");
-    if (k == 2 && a.g[k].count % 4 != 0)
-      return nxs::set_last_error(NXS_ERR_INVALID, "quaternion count not a multiple of 4");
-    most = std::max<int64_t>(most, a.g[k].param ? a.g[k].count : 0);
-  }
-  const double b1 = 0.9, b2 = 0.999;  // ADAM_BETA1/2, optimizer.py:42-44
-  a.b1 = (float)b1;
-  a.b2 = (float)b2;
-  a.omb1 = (float)(1.0 - b1);
-  a.omb2 = (float)(1.0 - b2);
-  a.inv_bc1 = (float)(1.0 / (1.0 - std::pow(b1, (double)step)));
-  a.inv_bc2 = (float)(1.0 / (1.0 - std::pow(b2, (double)step)));
-  a.eps = 1e-8f;
-  a.lr_mult = (float)lr_mult;
-  a.nan_skips = nan_skips;
-  if (most == 0) return NXS_OK;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t want = (most / 4 + 255) / 256;
-  const dim3 grid((unsigned)std::min<int64_t>(want, (int64_t)sms * 8), 5);
-  k_adam<<<grid, 256, 0, (cudaStream_t)stream>>>(a);
-  const cudaError_t e = cudaGetLastError();
-  return e == cudaSuccess ? NXS_OK : nxs::set_last_error(NXS_ERR_CUDA, cudaGetErrorString(e));
+  return adam_step<float>(groups, step, lr_mult, nan_skips, stream);
+}
+
+int nxs_adam_step_f64(const nxs_adam_group_f64* groups, int64_t step, double lr_mult,
+                      unsigned long long* nan_skips, void* stream) {
+  return adam_step<double>(groups, step, lr_mult, nan_skips, stream);
 }
 
 }  // extern "C"

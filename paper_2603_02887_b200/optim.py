@@ -148,8 +148,9 @@ def psnr(a_linear, b_linear) -> float:
 
 @dataclass
 class AdamState:
-    """Adam moments (fp32 CUDA tensors) and counters; the non-finite
-    gradient count lives on the device until read."""
+    """Adam moments (CUDA tensors: float32 for device parameters, float64
+    for the numpy drop-in's float64 parameters) and counters; the
+    non-finite gradient count lives on the device until read."""
     m: dict
     v: dict
     step: int = 0
@@ -161,8 +162,9 @@ class AdamState:
         m, v = {}, {}
         for k, p in params.items():
             shape = tuple(p.shape)
-            m[k] = torch.zeros(shape, dtype=torch.float32, device="cuda")
-            v[k] = torch.zeros(shape, dtype=torch.float32, device="cuda")
+            dt = torch.float32 if _is_tensor(p) else torch.float64
+            m[k] = torch.zeros(shape, dtype=dt, device="cuda")
+            v[k] = torch.zeros(shape, dtype=dt, device="cuda")
         return cls(m=m, v=v)
 
     @property
@@ -174,13 +176,20 @@ def bounded_adam_step(params: dict, grads: dict, state: AdamState, lr: dict,
                       lr_mult: float = 1.0, stream=None) -> None:
     """One Adam step followed by projection onto parameter bounds (opacities
     clamped to [1e-4, 1 - 1e-6], scales floored at 1e-6, quaternions
-    renormalised); non-finite gradients are dropped and counted.  CUDA
-    tensor parameters are updated in place on the device; numpy parameters
-    round-trip through the device and are updated in place."""
+    renormalised); non-finite gradients are dropped and counted
+    (reference optimizer.py:173-204).  CUDA tensor parameters (float32) are
+    updated in place on the device; numpy parameters (the reference's
+    float64 arrays) are updated in float64 on the device — no float32 round
+    trip — and written back in place."""
     torch = _torch()
     unknown = set(params) - set(PARAM_GROUPS)
     if unknown:
         raise ValueError(f"unknown parameter groups {sorted(unknown)}")
+    kinds = {_is_tensor(p) for p in params.values()}
+    if len(kinds) > 1:
+        raise ValueError("parameters must be all CUDA tensors or all numpy arrays")
+    f64 = kinds == {False}
+    dt = torch.float64 if f64 else torch.float32
     state.step += 1
     if state._skips is None:
         state._skips = torch.zeros(1, dtype=torch.int64, device="cuda")
@@ -191,24 +200,28 @@ def bounded_adam_step(params: dict, grads: dict, state: AdamState, lr: dict,
         if key not in params:
             continue
         p = params[key]
-        if _is_tensor(p):
+        if not f64:
             if not (p.is_cuda and p.dtype == torch.float32 and p.is_contiguous()):
                 raise ValueError(f"{key}: device parameters must be contiguous fp32 CUDA tensors")
             pd = p
         else:
-            pd = _dev_image(np.asarray(p)).reshape(np.shape(p))
+            pd = torch.as_tensor(np.ascontiguousarray(p, dtype=np.float64)).to("cuda")
             host[key] = (p, pd)
         g = grads[key]
-        gd = (g.detach().to(torch.float32).contiguous() if _is_tensor(g)
-              else _dev_image(np.asarray(g)).reshape(np.shape(g)))
+        gd = (g.detach().to(device="cuda", dtype=dt).contiguous() if _is_tensor(g)
+              else torch.as_tensor(np.ascontiguousarray(g, dtype=np.float64)).to(
+                  device="cuda", dtype=dt))
+        gd = gd.reshape(tuple(pd.shape))
         m, v = state.m[key], state.v[key]
         if tuple(m.shape) != tuple(pd.shape) or tuple(gd.shape) != tuple(pd.shape):
             raise ValueError(f"{key}: parameter, gradient and moment shapes differ")
+        if m.dtype != dt:
+            raise ValueError(f"{key}: Adam moments are {m.dtype}, parameters need {dt}")
         keep += [pd, gd]
         groups[i] = _native.AdamGroup(pd.data_ptr(), gd.data_ptr(), m.data_ptr(), v.data_ptr(),
                                       int(pd.numel()), float(lr[key]))
-    _native._check(_native.lib().nxs_adam_step(groups, int(state.step), float(lr_mult),
-                                               state._skips.data_ptr(),
-                                               _native._stream_ptr(stream)))
+    step_fn = _native.lib().nxs_adam_step_f64 if f64 else _native.lib().nxs_adam_step
+    _native._check(step_fn(groups, int(state.step), float(lr_mult), state._skips.data_ptr(),
+                           _native._stream_ptr(stream)))
     for key, (p, pd) in host.items():
-        p[...] = pd.double().cpu().numpy()
+        p[...] = pd.cpu().numpy().reshape(np.shape(p))

@@ -75,13 +75,21 @@ def test_bounded_adam_matches_reference():
 
 
 def test_bounded_adam_numpy_params_in_place():
+    """numpy (float64) parameters update in float64 on the device
+    (nxs_adam_step_f64): the reference's own trajectory to ~1e-12, not to
+    float32 precision."""
     from paper_2603_02887_b200 import optim
     params = {k: TRAIN["p0_" + k].copy() for k in KEYS}
+    ids = {k: id(v) for k, v in params.items()}
     state = optim.AdamState.for_params(params)
-    grads = {k: TRAIN[f"g0_{k}"] for k in KEYS}
-    optim.bounded_adam_step(params, grads, state, LR, lr_mult=0.9)
-    for k in KEYS:
-        np.testing.assert_allclose(params[k], TRAIN[f"p1_{k}"], rtol=1e-5, atol=1e-6, err_msg=k)
+    for step in range(3):
+        grads = {k: TRAIN[f"g{step}_{k}"] for k in KEYS}
+        optim.bounded_adam_step(params, grads, state, LR, lr_mult=0.9)
+        for k in KEYS:
+            assert id(params[k]) == ids[k] and params[k].dtype == np.float64
+            np.testing.assert_allclose(params[k], TRAIN[f"p{step + 1}_{k}"], rtol=1e-11,
+                                       atol=1e-13, err_msg=k)
+    assert state.nan_skips == int(TRAIN["nan_skips"]) == 2
 
 
 def test_device_training_steps_reduce_the_loss():
