@@ -23,6 +23,13 @@
 
 namespace nxs {
 
+#ifdef NXS_XSTATS
+// debug statistics of the exact-order forward (variant build only):
+// [0] inserts, [1] shifted entries, [2] sum of pending count at insert,
+// [3] commits, [4] list entries tested, [5..36] histogram of pending at insert
+__device__ unsigned long long g_xstats[40];
+#endif
+
 // pending entries per pixel: 16 for the chunked order (a chunk flush empties
 // the buffer; an overflow reruns with 32), 32 for the exact order
 // list entries staged per batch: 64 with the 16-entry buffer, 32 with the
@@ -250,6 +257,9 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
     emission(r[4], r[5], r[6], pc, E0, E1, E2);
     NXS_CHECK(s.count >= 0 && s.count < max_splats);
     myseq[(size_t)s.count * npix] = (int32_t)rank;
+#ifdef NXS_XSTATS
+    atomicAdd(&g_xstats[3], 1ull);
+#endif
     composite<FAM>(s, m, max_splats, alpha, E0, E1, E2);
   };
 
@@ -324,6 +334,12 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
         }
         const int f = (head + i) & (XBUF - 1);
         NXS_CHECK(nb < XBUF && i >= 0 && i <= nb);
+#ifdef NXS_XSTATS
+        atomicAdd(&g_xstats[0], 1ull);
+        atomicAdd(&g_xstats[1], (unsigned long long)(nb - i));
+        atomicAdd(&g_xstats[2], (unsigned long long)nb);
+        atomicAdd(&g_xstats[5 + min(nb, 31)], 1ull);
+#endif
         bt[f * TILE_PIX + tid] = tpk;
         bp[f * TILE_PIX + tid] = pos;
         if constexpr (keeps_alpha(XBUF)) ba[f * TILE_PIX + tid] = t.alpha;
@@ -657,3 +673,9 @@ void launch_blend_bwd_x(bool count, int n_tiles, const BwdXArgs& a, const CamDev
 }
 
 }  // namespace nxs
+
+#ifdef NXS_XSTATS
+extern "C" int nxs_debug_xstats(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, nxs::g_xstats, sizeof(nxs::g_xstats)) == cudaSuccess ? 0 : -3;
+}
+#endif
