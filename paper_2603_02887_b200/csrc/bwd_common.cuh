@@ -189,8 +189,22 @@ __device__ __forceinline__ bool bwd_pair(BwdPix& A, BwdPix& B, const float4* rec
     if (nA) A.P = (idx == A.ck) ? A.Pck : div_newton(A.P, __fsub_rn(1.0f, alpha.x));
     if (nB) B.P = (idx == B.ck) ? B.Pck : div_newton(B.P, __fsub_rn(1.0f, alpha.y));
   }
-  F2 fp;
-  const F2 g{weight_g<FAM>(m, A.thi, A.tlo, A.P, fp.x), weight_g<FAM>(m, B.thi, B.tlo, B.P, fp.y)};
+  F2 fp, g;
+  if constexpr (FAM == FAM_SOFT) {
+    // weight_g<FAM_SOFT> on the pair (σ split by sign; MUFU ops per lane)
+    const F2 x = mul2(f2(m.c), sub2(sub2(f2(1.0f), F2{A.thi, B.thi}), F2{A.tlo, B.tlo}));
+    const F2 nx = mul2(F2{-fabsf(x.x), -fabsf(x.y)}, f2(1.4426950408889634f));
+    const F2 t{ex2_approx(nx.x), ex2_approx(nx.y)};
+    const F2 op = add2(f2(1.0f), t);
+    const F2 r{__fdividef(1.0f, op.x), __fdividef(1.0f, op.y)};
+    const F2 tr = mul2(t, r);
+    const F2 sig{x.x >= 0.f ? r.x : tr.x, x.y >= 0.f ? r.y : tr.y};
+    const F2 oms{x.x >= 0.f ? tr.x : r.x, x.y >= 0.f ? tr.y : r.y};
+    g = mul2(f2(m.K), sig);
+    fp = mul2(mul2(f2(-m.c), g), oms);
+  } else {
+    g = F2{weight_g<FAM>(m, A.thi, A.tlo, A.P, fp.x), weight_g<FAM>(m, B.thi, B.tlo, B.P, fp.y)};
+  }
   const F2 wgt = mul2(alpha, g);
   const F2 carry{A.carry, B.carry};
   F2 da, nc;
@@ -205,7 +219,8 @@ __device__ __forceinline__ bool bwd_pair(BwdPix& A, BwdPix& B, const float4* rec
   if (nA) A.carry = nc.x;
   if (nB) B.carry = nc.y;
   // dE = s·w for normal pixels, s·T̄_k for the saturating one
-  const F2 wt{satA ? A.tk : wgt.x, satB ? B.tk : wgt.y};
+  // (zero for a pixel that does not replay the entry: its dE vanish)
+  const F2 wt{satA ? A.tk : (okA ? wgt.x : 0.f), satB ? B.tk : (okB ? wgt.y : 0.f)};
   const F2 dE0 = mul2(s_0, wt), dE1 = mul2(s_1, wt), dE2 = mul2(s_2, wt);
   // zero for a clamped alpha (render.py:329) and for a pixel that does not
   // contribute (kern and alpha are finite there), so dm2 and dak need no mask
@@ -228,9 +243,9 @@ __device__ __forceinline__ bool bwd_pair(BwdPix& A, BwdPix& B, const float4* rec
   o.uy = fma2(f2(bf[1].x), qx, fma2(f2(bf[1].y), qy, mul2(f2(-bf[1].z), eps)));
   o.uz = fma2(f2(bf[2].x), qx, fma2(f2(bf[2].y), qy, mul2(f2(-bf[2].z), eps)));
   // SH moments use dE_c·[E_c > 0] (render.py:340-341)
-  o.e0 = sel2(okA && c0.x > 0.f, okB && c0.y > 0.f, dE0);
-  o.e1 = sel2(okA && c1.x > 0.f, okB && c1.y > 0.f, dE1);
-  o.e2 = sel2(okA && c2.x > 0.f, okB && c2.y > 0.f, dE2);
+  o.e0 = sel2(c0.x > 0.f, c0.y > 0.f, dE0);
+  o.e1 = sel2(c1.x > 0.f, c1.y > 0.f, dE1);
+  o.e2 = sel2(c2.x > 0.f, c2.y > 0.f, dE2);
   return true;
 }
 
