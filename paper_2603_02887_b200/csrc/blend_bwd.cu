@@ -55,8 +55,11 @@ constexpr size_t bwd_smem(bool det) {
          sizeof(float) * BWD_BATCH * NMOM * acc_rows(det) + sizeof(float) * RED_WARP * BWD_WARPS;
 }
 
+#ifndef NXS_BWD_MINB
+#define NXS_BWD_MINB 4
+#endif
 template <int FAM, bool COUNT, bool DET>
-__global__ void __launch_bounds__(BWD_THREADS, 4)
+__global__ void __launch_bounds__(BWD_THREADS, NXS_BWD_MINB)
     k_blend_bwd(const float4* __restrict__ records, const float4* __restrict__ bframe,
                 PhaseLists lists, CamDev cam, ModelDev m, float cutoff, double near_plane,
                 float bg0, float bg1, float bg2, const float* __restrict__ seed, PixCache cache,

@@ -141,9 +141,10 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
   uint32_t* s_rank = s_ring_rank + 2 * XBT;
   float* s_zlo = reinterpret_cast<float*>(s_rank + XBT);
   uint32_t* s_chunk = reinterpret_cast<uint32_t*>(s_zlo + XBT);
-  float* bt = reinterpret_cast<float*>(s_chunk + XBT);    // [XBUF][TILE_PIX] pending t
-  int* bp = reinterpret_cast<int*>(bt + XBUF * TILE_PIX);     // [XBUF][TILE_PIX] list position
-  float* ba = reinterpret_cast<float*>(bp + XBUF * TILE_PIX);  // [XBUF][TILE_PIX] alpha
+  // pending entries, [XBUF][TILE_PIX]: (t, list position) pairs moved as one
+  // 8-byte word, and alpha; each thread addresses its own column
+  float2* bq = reinterpret_cast<float2*>(s_chunk + XBT);
+  float* ba = reinterpret_cast<float*>(bq + XBUF * TILE_PIX);
 
   const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
   const int tid = threadIdx.x;
@@ -154,6 +155,8 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
   const int pix = py * cam.W + px;
   const size_t npix = (size_t)cam.W * cam.H;
   int32_t* myseq = seq + (inside ? pix : 0);  // [slot][pixel]: lanes read/write contiguously
+  float2* myq = bq + tid;
+  float* mya = ba + tid;
 
   FwdXPix s{};
   s.P = 1.f;
@@ -190,14 +193,14 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
   // pending entries: a ring of XBUF slots, ascending by (t, index) from the
   // head; new entries (lists are in z_lo order) usually append at the tail
   int nb = 0, head = 0;
+  float thead = __int_as_float(0x7f800000);  // t of the head entry (+inf when empty)
   if (resume && inside && carry_n && !s.done) {
     // pending entries carried over the phase end: list positions encode
     // ranks as -1 - rank (their records are read from global memory)
     nb = carry_n[pix];
     for (int i = 0; i < nb; ++i) {
       const int32_t rk = carry_r[(size_t)i * npix + pix];
-      bt[i * TILE_PIX + tid] = carry_t[(size_t)i * npix + pix];
-      bp[i * TILE_PIX + tid] = -1 - rk;
+      myq[i * TILE_PIX] = make_float2(carry_t[(size_t)i * npix + pix], __int_as_float(-1 - rk));
       if constexpr (keeps_alpha(XBUF)) {  // (the carry keeps t and rank only)
         float4 r[REC_F4];
         const float4* rec = records + (size_t)rk * REC_F4;
@@ -206,9 +209,10 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
         TestOut t;
         float tpk;
         test_with_t(r, cam, px, py, pc, hnorm, cutoff, near_plane, t, tpk);  // valid when carried
-        ba[i * TILE_PIX + tid] = t.alpha;
+        mya[i * TILE_PIX] = t.alpha;
       }
     }
+    if (nb > 0) thead = myq[0].x;
   }
   uint32_t cur_chunk = 0;  // chunk of the pending entries (chunked order)
   unsigned long long ntest = 0;
@@ -223,11 +227,12 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
   // emission re-reads the record's SH words (staged ring, else L1/L2)
   int ring_lo = 0;  // list positions [ring_lo, current batch end) are staged
   auto commit_front = [&]() {
-    const int slot = head * TILE_PIX + tid;
     NXS_CHECK(nb > 0 && head >= 0 && head < XBUF);
-    const int pos = bp[slot];
+    const int pos = __float_as_int(myq[head * TILE_PIX].y);
+    const float alpha_kept = mya[head * TILE_PIX];
     head = (head + 1) & (XBUF - 1);
     --nb;
+    thead = nb > 0 ? myq[head * TILE_PIX].x : __int_as_float(0x7f800000);
     // explicit shared / global branches (no generic loads)
     float4 r[REC_F4];
     constexpr int K0 = keeps_alpha(XBUF) ? 4 : 0, K1 = keeps_alpha(XBUF) ? 7 : REC_F4;
@@ -246,7 +251,7 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
     }
     float alpha;
     if constexpr (keeps_alpha(XBUF)) {
-      alpha = ba[slot];
+      alpha = alpha_kept;
     } else {
       TestOut t;
       float tpk;
@@ -290,7 +295,7 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
         // final; a new chunk makes every pending entry final
         const bool next_chunk = s_chunk[j] != cur_chunk;
         const float bound = s_zlo[j] * hnorm;
-        while (nb > 0 && (next_chunk || bt[head * TILE_PIX + tid] < bound)) {
+        while (nb > 0 && (next_chunk || thead < bound)) {
           commit_front();
           if (s.done) break;
         }
@@ -318,18 +323,17 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
         uint32_t gid_new = 0xffffffffu;
         while (i > 0) {
           const int e = (head + i - 1) & (XBUF - 1);
-          const float te = bt[e * TILE_PIX + tid];
-          bool later = te > tpk;  // the pending entry commits after the new one
-          if (te == tpk) {
+          const float2 qe = myq[e * TILE_PIX];
+          bool later = qe.x > tpk;  // the pending entry commits after the new one
+          if (qe.x == tpk) {
             if (gid_new == 0xffffffffu) gid_new = tie_key(s_rank[j]);
-            const int pe = bp[e * TILE_PIX + tid];
+            const int pe = __float_as_int(qe.y);
             later = tie_key(pe < 0 ? (uint32_t)(-1 - pe) : pairs[pe]) > gid_new;
           }
           if (!later) break;
           const int f = (head + i) & (XBUF - 1);
-          bt[f * TILE_PIX + tid] = te;
-          bp[f * TILE_PIX + tid] = bp[e * TILE_PIX + tid];
-          if constexpr (keeps_alpha(XBUF)) ba[f * TILE_PIX + tid] = ba[e * TILE_PIX + tid];
+          myq[f * TILE_PIX] = qe;
+          if constexpr (keeps_alpha(XBUF)) mya[f * TILE_PIX] = mya[e * TILE_PIX];
           --i;
         }
         const int f = (head + i) & (XBUF - 1);
@@ -340,9 +344,9 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
         atomicAdd(&g_xstats[2], (unsigned long long)nb);
         atomicAdd(&g_xstats[5 + min(nb, 31)], 1ull);
 #endif
-        bt[f * TILE_PIX + tid] = tpk;
-        bp[f * TILE_PIX + tid] = pos;
-        if constexpr (keeps_alpha(XBUF)) ba[f * TILE_PIX + tid] = t.alpha;
+        myq[f * TILE_PIX] = make_float2(tpk, __int_as_float(pos));
+        if constexpr (keeps_alpha(XBUF)) mya[f * TILE_PIX] = t.alpha;
+        if (i == 0) thead = tpk;
         ++nb;
       }
     }
@@ -353,13 +357,14 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
   // what lies in front of that phase's first z_lo; the rest is carried
   if (end_bound && save) {
     const float bound = *end_bound * hnorm;
-    while (nb > 0 && !s.done && bt[head * TILE_PIX + tid] < bound) commit_front();
+    while (nb > 0 && !s.done && thead < bound) commit_front();
     if (inside && !s.done) {
       carry_n[pix] = nb;
       for (int i = 0; i < nb; ++i) {
         const int e = (head + i) & (XBUF - 1);
-        const int pe = bp[e * TILE_PIX + tid];
-        carry_t[(size_t)i * npix + pix] = bt[e * TILE_PIX + tid];
+        const float2 qe = myq[e * TILE_PIX];
+        const int pe = __float_as_int(qe.y);
+        carry_t[(size_t)i * npix + pix] = qe.x;
         carry_r[(size_t)i * npix + pix] = pe < 0 ? -1 - pe : (int32_t)pairs[pe];
       }
     }
