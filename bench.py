@@ -503,9 +503,9 @@ def roofline(a, model, phase, st):
     r["frac"] = round(r["achieved"] / r["peak"], 4) if r["peak"] else None
     r["traffic"] = None
     # DRAM bytes and FP32-pipe utilisation of the blend kernels from the
-    # committed ncu capture of this workload (profiles/r01_blend_traffic.json)
+    # committed ncu capture of this workload (profiles/r02_blend_traffic.json)
     try:
-        cap = json.loads((ROOT / "profiles" / "r01_blend_traffic.json").read_text())
+        cap = json.loads((ROOT / "profiles" / "r02_blend_traffic.json").read_text())
         k = cap["per_step"]
         if dom == "blend (fwd+bwd)" and model.variant == "softplus" and a.chunk_size == 1 \
                 and a.gaussians == 1_000_000 and (a.width, a.height) == (1920, 1080):
@@ -513,7 +513,7 @@ def roofline(a, model, phase, st):
             r["traffic_unit"] = "bytes per step (fwd + bwd launches)"
             r["ncu_fma_pipe_pct"] = {n: v["fma_pipe_pct"] for n, v in k.items()}
             r["ncu_issue_active_pct"] = {n: v["issue_active_pct"] for n, v in k.items()}
-            r["ncu_source"] = "profiles/r01_blend_traffic.json"
+            r["ncu_source"] = "profiles/r02_blend_traffic.json"
     except Exception:
         pass
     r["share_of_step"] = round(shares[dom] / total, 3) if total else None

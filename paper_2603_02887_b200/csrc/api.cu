@@ -1924,6 +1924,7 @@ int nxs_touched_export(nxs_view* v, int32_t* gids, int64_t* count, void* stream_
 
 // sizing history of a view (the device-sized first phase's estimates), so a
 // caller cycling many cameras through a few workspaces keeps each camera's
+// sync-free device-sized first phase (nxs_view_history_save / _load)
 struct ViewHistory {
   uint32_t magic;
   int32_t est_bin0, phases_needed, valid;

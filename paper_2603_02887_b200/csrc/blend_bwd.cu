@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(BWD_THREADS, NXS_BWD_MINB)
   bwd_load(st[1], cam, px, py0 + TILE / 2, cache, seed, bg0, bg1, bg2);
   float* red = s_red + (tid >> 5) * RED_WARP;
   const float gam = (FAM == FAM_EXP) ? 1.0f : m.c;
-  const float inv_f = (float)(1.0 / cam.f);
+  const float inv_f = (float)cam.inv_f;
   const float Y0 = (float)SH_C0;
   unsigned long long ntest = 0, nent = 0;
 

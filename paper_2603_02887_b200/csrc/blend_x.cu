@@ -478,7 +478,7 @@ __global__ void __launch_bounds__(BWDX_THREADS)
   float* red = smem_red + (tid >> 5) * BWDX_WARP_FLOATS;
   float4* wrec = reinterpret_cast<float4*>(red + NMOM * XRED_STRIDE);  // [2][XREC_F4]
   const float gam = (FAM == FAM_EXP) ? 1.0f : m.c;
-  const float inv_f = (float)(1.0 / cam.f);
+  const float inv_f = (float)cam.inv_f;
   const float Y0 = (float)SH_C0;
   unsigned long long ntest = 0, nent = 0;
   // each pixel's next commit (cur) and the one after it (nxt, prefetched a

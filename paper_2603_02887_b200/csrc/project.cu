@@ -1021,7 +1021,7 @@ __global__ void __launch_bounds__(256)
     const int64_t g = order[r];
     const int4 rc = rects[g];
     if (rc.x >= 0) {
-      const double inv_f = 1.0 / cam.f;
+      const double inv_f = cam.inv_f;  // = 1.0 / cam.f (host, IEEE)
       const int w = rc.z - rc.x + 1, nt = w * (rc.w - rc.y + 1);
       for (int k = sl; k < nt; k += KSUB) {
         const int tx = rc.x + k % w, ty = rc.y + k / w;
@@ -1056,7 +1056,7 @@ __global__ void __launch_bounds__(256)
   const int nt = rc.x >= 0 ? w * (rc.w - rc.y + 1) : 0;
   int nmax = nt;  // the warp loops to its largest rect (ballots need every lane)
   for (int o = 16; o > 0; o >>= 1) nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
-  const double inv_f = 1.0 / cam.f;
+  const double inv_f = cam.inv_f;  // = 1.0 / cam.f (host, IEEE)
   unsigned long long o = nt > 0 ? offsets[r - r0] : 0ull;
   for (int base = 0; base < nmax; base += KSUB) {
     const int k = base + sl;
@@ -1098,7 +1098,7 @@ __global__ void __launch_bounds__(256)
   const int64_t g = order[r];
   const int4 rc = rects[g];
   if (rc.x < 0) return;
-  const double inv_f = 1.0 / cam.f;
+  const double inv_f = cam.inv_f;  // = 1.0 / cam.f (host, IEEE)
   const int w = rc.z - rc.x + 1, nt = w * (rc.w - rc.y + 1);
   for (int k = sl; k < nt; k += KSUB) {
     const int tx = rc.x + k % w, ty = rc.y + k / w;
@@ -1210,7 +1210,7 @@ __global__ void __launch_bounds__(256)
   const int64_t g = order[r];
   const int4 rc = rects[g];
   if (rc.x < 0) return;
-  const double inv_f = 1.0 / cam.f;
+  const double inv_f = cam.inv_f;  // = 1.0 / cam.f (host, IEEE)
   const int w = rc.z - rc.x + 1, nt = w * (rc.w - rc.y + 1);
   for (int k = sl; k < nt; k += KSUB) {
     const int tx = rc.x + k % w, ty = rc.y + k / w;
