@@ -240,12 +240,47 @@ def cpu_baseline(a, model):
 # ---------------------------------------------------------------------------
 
 class Clocks:
+    """SM clock and throttle reasons sampled DURING the timed region: an NVML
+    thread polling every ~2 ms (a C3 step is 0.5 ms, so a 30-step region
+    lasts ~16 ms — shorter than nvidia-smi's 100 ms period); nvidia-smi
+    -lms 100 as the fallback when NVML is unavailable."""
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4}
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu):
+        import threading
         self.p = None
+        self.samples = []
+        self.stop_ev = threading.Event()
+        self.th = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            idx = gpu
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            if vis and vis.split(",")[gpu].strip().isdigit():
+                idx = int(vis.split(",")[gpu])
+            h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+
+            def run():
+                while not self.stop_ev.is_set():
+                    try:
+                        self.samples.append(
+                            (pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+                             pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)))
+                    except Exception:
+                        pass
+                    time.sleep(0.002)
+
+            self.th = threading.Thread(target=run, daemon=True)
+            self.th.start()
+            return
+        except Exception:
+            self.th = None
         try:
             self.p = subprocess.Popen(
                 ["nvidia-smi", "-i", str(gpu), f"--query-gpu={self.Q}",
@@ -254,7 +289,21 @@ class Clocks:
         except Exception:
             self.p = None
 
+    def mark_start(self):
+        """Drop the samples taken before the timed region (NVML thread)."""
+        self.samples = []
+
     def stop(self):
+        if self.th is not None:
+            self.stop_ev.set()
+            self.th.join(timeout=1.0)
+            if not self.samples:
+                return None
+            reasons = sorted({n for _, r in self.samples for n, bit in self.REASONS.items()
+                              if r & bit})
+            return {"sm_mhz": statistics.median(c for c, _ in self.samples),
+                    "sm_max_mhz": self.mx, "reasons": reasons, "samples": len(self.samples),
+                    "source": "nvml"}
         if self.p is None:
             return None
         self.p.terminate()
@@ -276,7 +325,7 @@ class Clocks:
         if not sm:
             return None
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi"}
 
 
 # ---------------------------------------------------------------------------
@@ -350,6 +399,7 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks.mark_start()
     launches0 = sum(w.stats()["n_launches"] for w in rv.workspaces)
     redo0 = sum(w.stats()["n_redo"] for w in rv.workspaces)
     e0.record()

@@ -327,43 +327,61 @@ static void launch_bwd_fam(bool count, int n_tiles, const float4* records, const
 }
 
 // Deterministic moments: per touched rank, the (tile, entry) partials of
-// every tile of its rectangle (row-major tile order, phases in order), each
-// found by binary search in that tile's rank-sorted list, summed in fp64.
-__global__ void k_det_reduce(int64_t P, const uint32_t* __restrict__ order,
-                             const int4* __restrict__ rects, int tiles_x, PhaseLists lists,
-                             const uint8_t* __restrict__ touched, double* __restrict__ moments) {
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= P || !touched[r]) return;
+// every tile of its rectangle, summed in fp64 in a fixed order: one warp per
+// rank, lane l takes the rect's tiles l, l+32, ... (row-major; each found by
+// binary search in that tile's rank-sorted list, phases in order), then a
+// fixed shuffle tree adds the lanes.
+__global__ void __launch_bounds__(256)
+    k_det_reduce(int64_t P, const uint32_t* __restrict__ order, const int4* __restrict__ rects,
+                 int tiles_x, PhaseLists lists, const uint8_t* __restrict__ touched,
+                 double* __restrict__ moments) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (r >= P || !touched[r]) return;  // (warp-uniform)
   const int4 rc = rects[order[r]];
+  const int w = rc.z - rc.x + 1, nt = w * (rc.w - rc.y + 1);
   double acc[NMOM];
 #pragma unroll
   for (int m = 0; m < NMOM; ++m) acc[m] = 0.0;
   for (int p = 0; p < lists.n; ++p)
-    for (int ty = rc.y; ty <= rc.w; ++ty)
-      for (int tx = rc.x; tx <= rc.z; ++tx) {
-        const int2 rg = lists.ranges[p][ty * tiles_x + tx];
-        int lo = rg.x, hi = rg.y;  // first position with rank >= r
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (lists.pairs[p][mid] < (uint32_t)r) lo = mid + 1;
-          else hi = mid;
-        }
-        if (lo >= rg.y || lists.pairs[p][lo] != (uint32_t)r) continue;
-        const float* q = lists.partial + (lists.poff[p] + lo) * NMOM;
-#pragma unroll
-        for (int m = 0; m < NMOM; ++m) acc[m] += (double)q[m];
+    for (int k = lane; k < nt; k += 32) {
+      const int2 rg = lists.ranges[p][(rc.y + k / w) * tiles_x + rc.x + k % w];
+      int lo = rg.x, hi = rg.y;  // first position with rank >= r
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (lists.pairs[p][mid] < (uint32_t)r) lo = mid + 1;
+        else hi = mid;
       }
-  double* mm = moments + r * NMOM;
+      if (lo >= rg.y || lists.pairs[p][lo] != (uint32_t)r) continue;
+      const float4* q = reinterpret_cast<const float4*>(lists.partial + (lists.poff[p] + lo) * NMOM);
 #pragma unroll
-  for (int m = 0; m < NMOM; ++m) mm[m] = acc[m];
+      for (int i = 0; i < NMOM / 4; ++i) {
+        const float4 v = q[i];
+        acc[4 * i + 0] += (double)v.x;
+        acc[4 * i + 1] += (double)v.y;
+        acc[4 * i + 2] += (double)v.z;
+        acc[4 * i + 3] += (double)v.w;
+      }
+    }
+#pragma unroll
+  for (int m = 0; m < NMOM; ++m)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[m] += __shfl_xor_sync(0xffffffffu, acc[m], o);
+  if (lane < NMOM) {
+    double v = acc[0];
+#pragma unroll
+    for (int m = 1; m < NMOM; ++m)
+      if (lane == m) v = acc[m];
+    moments[r * NMOM + lane] = v;
+  }
 }
 
 void launch_det_reduce(int64_t P, const uint32_t* order, const int4* rects, int tiles_x,
                        const PhaseLists& lists, const uint8_t* touched, double* moments,
                        cudaStream_t s) {
   if (P <= 0) return;
-  k_det_reduce<<<(unsigned)((P + 127) / 128), 128, 0, s>>>(P, order, rects, tiles_x, lists,
-                                                           touched, moments);
+  k_det_reduce<<<(unsigned)((P * 32 + 255) / 256), 256, 0, s>>>(P, order, rects, tiles_x, lists,
+                                                               touched, moments);
 }
 
 void launch_blend_bwd(bool count, int n_tiles, const float4* records, const float4* bframe,
