@@ -65,6 +65,7 @@ __global__ void __launch_bounds__(BWD_THREADS, NXS_BWD_MINB)
                 float bg0, float bg1, float bg2, const float* __restrict__ seed, PixCache cache,
                 double* __restrict__ moments, uint8_t* __restrict__ touched,
                 Counters* __restrict__ cnt) {
+  nxs_pdl_enter();
   extern __shared__ float4 smem_dyn[];
   // [buffer][entry][part]
   float4(*s_rec2)[BWD_BATCH][REC_F4] = reinterpret_cast<float4(*)[BWD_BATCH][REC_F4]>(smem_dyn);
@@ -321,7 +322,7 @@ static void launch_bwd_fam(bool count, int n_tiles, const float4* records, const
     }
   });
   auto k = count ? k_blend_bwd<FAM, true, DET> : k_blend_bwd<FAM, false, DET>;
-  k<<<n_tiles, BWD_THREADS, bwd_smem(DET), s>>>(records, bframe, lists, cam, m, cutoff, near_plane,
+  nxs_launch(k, n_tiles, BWD_THREADS, bwd_smem(DET), s, records, bframe, lists, cam, m, cutoff, near_plane,
                                                bg[0], bg[1], bg[2], seed, cache, moments, touched,
                                                cnt);
 }
@@ -335,6 +336,7 @@ __global__ void __launch_bounds__(256)
     k_det_reduce(int64_t P, const uint32_t* __restrict__ order, const int4* __restrict__ rects,
                  int tiles_x, PhaseLists lists, const uint8_t* __restrict__ touched,
                  double* __restrict__ moments) {
+  nxs_pdl_enter();
   const int lane = threadIdx.x & 31;
   const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (r >= P || !touched[r]) return;  // (warp-uniform)
@@ -380,7 +382,7 @@ void launch_det_reduce(int64_t P, const uint32_t* order, const int4* rects, int 
                        const PhaseLists& lists, const uint8_t* touched, double* moments,
                        cudaStream_t s) {
   if (P <= 0) return;
-  k_det_reduce<<<(unsigned)((P * 32 + 255) / 256), 256, 0, s>>>(P, order, rects, tiles_x, lists,
+  nxs_launch(k_det_reduce, (unsigned)((P * 32 + 255) / 256), 256, 0, s, P, order, rects, tiles_x, lists,
                                                                touched, moments);
 }
 

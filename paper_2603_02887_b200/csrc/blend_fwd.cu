@@ -43,6 +43,7 @@ __global__ void __launch_bounds__(TILE_PIX, NXS_FWD_MINB)
                 float* __restrict__ rgb, int32_t* __restrict__ overdraw,
                 float* __restrict__ residual, PixCache cache, PixResume rs,
                 unsigned long long* __restrict__ need_rank, Counters* __restrict__ cnt) {
+  nxs_pdl_enter();
   const int tile = blockIdx.x;
   if (!active[tile]) return;  // every pixel of the tile finished in an earlier phase
   // two 64-entry record buffers: the next batch streams in (cp.async)
@@ -281,7 +282,7 @@ static void launch_fwd_fam(bool count, int n_tiles, const FwdArgs& a, const CamD
                            Counters* cnt, cudaStream_t s) {
   auto k = count ? (a.theta0 ? k_blend_fwd<FAM, true, true> : k_blend_fwd<FAM, true, false>)
                  : (a.theta0 ? k_blend_fwd<FAM, false, true> : k_blend_fwd<FAM, false, false>);
-  k<<<n_tiles, TILE_PIX, 0, s>>>(a.records, a.pairs, a.ranges, a.cum_in, a.cum_out, a.active,
+  nxs_launch(k, n_tiles, TILE_PIX, 0, s, a.records, a.pairs, a.ranges, a.cum_in, a.cum_out, a.active,
                                  a.n_active, a.resume, a.save, cam, m, a.max_splats, a.cutoff,
                                  a.near_plane, a.bg[0], a.bg[1], a.bg[2], a.rgb, a.overdraw,
                                  a.residual, cache, rs, a.need_rank, cnt);

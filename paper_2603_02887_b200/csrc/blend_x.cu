@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
                   bool save, float* __restrict__ carry_t, int32_t* __restrict__ carry_r,
                   int32_t* __restrict__ carry_n, const float* __restrict__ end_bound,
                   unsigned long long* __restrict__ need_rank, Counters* __restrict__ cnt) {
+  nxs_pdl_enter();
   constexpr int XBT = xbatch(XBUF);
   const int tile = blockIdx.x;
   if (active && !active[tile]) return;  // finished in an earlier depth phase
@@ -458,6 +459,7 @@ __global__ void __launch_bounds__(BWDX_THREADS)
                   float bg0, float bg1, float bg2, const float* __restrict__ seed,
                   PixCache cache, double* __restrict__ moments, uint8_t* __restrict__ touched,
                   Counters* __restrict__ cnt) {
+  nxs_pdl_enter();
   extern __shared__ float smem_red[];
   const int tile = blockIdx.x;
   const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
@@ -618,7 +620,7 @@ static void launch_fwd_x_xb(bool count, int n_tiles, const FwdXArgs& a, const Ca
     set_smem(k_blend_fwd_x<FAM, false, XB>, fwdx_smem(XB));
   });
   auto k = count ? k_blend_fwd_x<FAM, true, XB> : k_blend_fwd_x<FAM, false, XB>;
-  k<<<n_tiles, TILE_PIX, fwdx_smem(XB), s>>>(
+  nxs_launch(k, n_tiles, TILE_PIX, fwdx_smem(XB), s, 
       a.records, a.pairs, a.ranges, a.zlo_rank, a.order, a.rank_c, a.chunk, cam, m, a.max_splats,
       a.cutoff, a.near_plane, a.bg[0], a.bg[1], a.bg[2], a.rgb, a.overdraw, a.residual, cache, rs,
       a.seq, a.overflow, a.active, a.n_active, a.resume, a.save, a.carry_t, a.carry_r,
@@ -659,7 +661,7 @@ static void launch_bwd_x_fam(bool count, int n_tiles, const BwdXArgs& a, const C
     set_smem(k_blend_bwd_x<FAM, false>, BWDX_SMEM);
   });
   auto k = count ? k_blend_bwd_x<FAM, true> : k_blend_bwd_x<FAM, false>;
-  k<<<n_tiles, BWDX_THREADS, BWDX_SMEM, s>>>(a.records, a.bframe, a.pairs, a.seq, a.max_splats, cam, m,
+  nxs_launch(k, n_tiles, BWDX_THREADS, BWDX_SMEM, s, a.records, a.bframe, a.pairs, a.seq, a.max_splats, cam, m,
                                          a.cutoff, a.near_plane, a.bg[0], a.bg[1], a.bg[2],
                                          a.seed, cache, a.moments, a.touched, cnt);
 }

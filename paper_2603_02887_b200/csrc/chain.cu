@@ -27,6 +27,7 @@ __global__ void k_chain(const float* __restrict__ scales, const float* __restric
                         float* __restrict__ g_scales, float* __restrict__ g_quats,
                         float* __restrict__ g_opac, float* __restrict__ g_sh,
                         uint32_t* __restrict__ tlist, unsigned long long* __restrict__ tcount) {
+  nxs_pdl_enter();
   int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= P || !touched[r]) return;
   // read this rank's moments and leave the buffer zeroed for the next backward
@@ -115,7 +116,7 @@ void launch_chain(const float* scales, const float* quats, int C, int64_t P, con
   if (P == 0) return;
   // touched ranks lie below the processed ranks (P here): small blocks
   // spread their fp64 work over every SM
-  k_chain<<<(unsigned)((P + 63) / 64), 64, 0, s>>>(scales, quats, C, P, order, moments, touched,
+  nxs_launch(k_chain, (unsigned)((P + 63) / 64), 64, 0, s, scales, quats, C, P, order, moments, touched,
                                                     g_centers, g_scales, g_quats, g_opac, g_sh,
                                                     tlist, tcount);
 }

@@ -41,6 +41,7 @@ __host__ __device__ inline Layout layout_of(int64_t n, int C) {
 __global__ void k_touched_mark(const uint32_t* __restrict__ list,
                                const unsigned long long* __restrict__ count, int64_t n,
                                uint8_t* __restrict__ mask) {
+  nxs_pdl_enter();
   const unsigned long long m = *count;
   for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < m;
        i += (unsigned long long)gridDim.x * blockDim.x) {
@@ -52,6 +53,7 @@ __global__ void k_touched_mark(const uint32_t* __restrict__ list,
 // zero every flagged Gaussian's row (all five segments) and clear its flag
 __global__ void k_zero_masked(float* __restrict__ flat, int64_t n, int C,
                               uint8_t* __restrict__ mask) {
+  nxs_pdl_enter();
   const Layout L = layout_of(n, C);
   for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n;
        g += (int64_t)gridDim.x * blockDim.x) {
@@ -70,6 +72,7 @@ template <bool GATHER>
 __global__ void k_rows(float* __restrict__ flat, int64_t n, int C,
                        const int32_t* __restrict__ index, int64_t m,
                        float* __restrict__ packed) {
+  nxs_pdl_enter();
   const Layout L = layout_of(n, C);
   const int W = 11 + 3 * C;
   const int64_t total = m * W;
@@ -100,7 +103,7 @@ unsigned grid_for(int64_t work, int threads) {
 
 void launch_touched_mark(const uint32_t* list, const unsigned long long* count, int64_t n,
                          uint8_t* mask, cudaStream_t s) {
-  k_touched_mark<<<grid_for(std::min<int64_t>(n, 1 << 20), 256), 256, 0, s>>>(list, count, n,
+  nxs_launch(k_touched_mark, grid_for(std::min<int64_t>(n, 1 << 20), 256), 256, 0, s, list, count, n,
                                                                                mask);
 }
 
@@ -116,7 +119,7 @@ int nxs_grads_zero_masked(float* flat, int64_t n, int32_t sh_coeffs, uint8_t* ma
     return set_last_error(NXS_ERR_INVALID, "bad gradient buffer arguments");
   if (n == 0) return NXS_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  k_zero_masked<<<grid_for(n, 256), 256, 0, s>>>(flat, n, sh_coeffs, mask);
+  nxs_launch(k_zero_masked, grid_for(n, 256), 256, 0, s, flat, n, sh_coeffs, mask);
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? NXS_OK : set_last_error(NXS_ERR_CUDA, cudaGetErrorString(e));
 }
@@ -155,7 +158,7 @@ int nxs_grads_gather(const float* flat, int64_t n, int32_t sh_coeffs, const int3
     return set_last_error(NXS_ERR_INVALID, "bad gather arguments");
   if (count <= 0) return NXS_OK;
   const int W = 11 + 3 * sh_coeffs;
-  k_rows<true><<<grid_for(count * W, 256), 256, 0, (cudaStream_t)stream>>>(
+  nxs_launch(k_rows<true>, grid_for(count * W, 256), 256, 0, (cudaStream_t)stream, 
       const_cast<float*>(flat), n, sh_coeffs, index, count, packed);
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? NXS_OK : set_last_error(NXS_ERR_CUDA, cudaGetErrorString(e));
@@ -167,7 +170,7 @@ int nxs_grads_scatter(float* flat, int64_t n, int32_t sh_coeffs, const int32_t* 
     return set_last_error(NXS_ERR_INVALID, "bad scatter arguments");
   if (count <= 0) return NXS_OK;
   const int W = 11 + 3 * sh_coeffs;
-  k_rows<false><<<grid_for(count * W, 256), 256, 0, (cudaStream_t)stream>>>(
+  nxs_launch(k_rows<false>, grid_for(count * W, 256), 256, 0, (cudaStream_t)stream, 
       flat, n, sh_coeffs, index, count, const_cast<float*>(packed));
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? NXS_OK : set_last_error(NXS_ERR_CUDA, cudaGetErrorString(e));

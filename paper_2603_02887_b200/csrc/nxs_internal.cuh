@@ -14,7 +14,9 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <mutex>
+#include <utility>
 
 // NXS_CHECK(cond): device bounds checks of the blend kernels' shared-memory
 // rings, staged batches, commit sequences and list indices, compiled in by
@@ -29,6 +31,50 @@
 #endif
 
 namespace nxs {
+
+// Programmatic dependent launch (Hopper+/Blackwell): every library kernel
+// starts with nxs_pdl_enter() — it lets the next kernel of the stream begin
+// launching once all of this grid's blocks are running, then waits for the
+// previous kernel's completion (and memory) before touching anything — and
+// is launched by nxs_launch with the programmatic-serialization attribute,
+// so the launch latency and ramp of consecutive pipeline kernels overlap the
+// previous kernel's tail.  Opt-in (NXS_PDL=1): measured at C3 it made the
+// global-order step slower (0.530 -> 0.596 ms; the exact order 1 % faster),
+// so plain launches are the default (griddepcontrol.wait is then a no-op).
+__device__ __forceinline__ void nxs_pdl_enter() {
+#if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 900
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
+inline bool nxs_pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("NXS_PDL");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+inline void nxs_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t s, Args&&... args) {
+  if (nxs_pdl_enabled()) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  } else {
+    kern<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
+  }
+}
 
 // Host: run `f` once per (call site, CUDA device) — kernel attributes and
 // constant-memory uploads are per-device state.  `done` is the call site's

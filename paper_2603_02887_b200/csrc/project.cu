@@ -152,6 +152,7 @@ __global__ void k_depth(const float* __restrict__ centers, const float* __restri
                         int64_t P, CamDev cam, double cutoff, int zmode,
                         double* __restrict__ depth, unsigned long long* __restrict__ key64,
                         uint32_t* __restrict__ idx, unsigned long long* __restrict__ kminmax) {
+  nxs_pdl_enter();
   __shared__ unsigned long long s_min[8], s_max[8];
   unsigned long long kmin = ~0ull, kmax = 0ull;
   // grid-stride: few blocks, so few atomics on the two min/max words
@@ -208,6 +209,7 @@ __device__ __forceinline__ uint32_t key32_of(double d, double lo, double scale, 
 __global__ void k_key32(const double* __restrict__ depth, int64_t P,
                         const unsigned long long* __restrict__ kminmax,
                         uint32_t* __restrict__ key) {
+  nxs_pdl_enter();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P) return;
   const bool spread = kminmax[0] < kminmax[1];
@@ -221,6 +223,7 @@ __global__ void __launch_bounds__(1024)
     k_key32_hist(const double* __restrict__ depth, int64_t P,
                  const unsigned long long* __restrict__ kminmax, uint32_t* __restrict__ key,
                  unsigned int* __restrict__ hist) {
+  nxs_pdl_enter();
   __shared__ unsigned int sh[PH_BINS_];
   for (int b = threadIdx.x; b < PH_BINS_; b += blockDim.x) sh[b] = 0u;
   const bool spread = kminmax[0] < kminmax[1];
@@ -240,6 +243,7 @@ __global__ void __launch_bounds__(1024)
 // 64-bit keys of the fallback sort from the depths (lazy phases skip them in K0)
 __global__ void k_dkeys(const double* __restrict__ depth, int64_t P,
                         unsigned long long* __restrict__ key64) {
+  nxs_pdl_enter();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < P) key64[i] = dkey(depth[i]);
 }
@@ -253,6 +257,7 @@ __global__ void k_key_fixup(const uint32_t* __restrict__ key, uint32_t* __restri
                             const double* __restrict__ depth, int64_t P, int shift,
                             unsigned long long* __restrict__ overflow,
                             const int* __restrict__ nd) {
+  nxs_pdl_enter();
   if (nd) P = min(P, (int64_t)*nd);  // device-sized phase: real items only
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P) return;
@@ -285,6 +290,7 @@ __global__ void k_key_fixup(const uint32_t* __restrict__ key, uint32_t* __restri
 
 __global__ void k_rank_of(const uint32_t* __restrict__ order, int64_t r0, int64_t r1,
                           uint32_t* __restrict__ rank_of, const int* __restrict__ nd) {
+  nxs_pdl_enter();
   if (nd) r1 = min(r1, r0 + (int64_t)*nd);
   int64_t r = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r < r1) rank_of[order[r]] = (uint32_t)r;
@@ -311,6 +317,7 @@ __global__ void __launch_bounds__(1024) k_phase_select(const unsigned int* __res
                                                        unsigned long long* __restrict__ overflow,
                                                        unsigned int* __restrict__ bin_pos,
                                                        int* __restrict__ n_sel) {
+  nxs_pdl_enter();
   __shared__ unsigned long long cum[PH_BINS];
   __shared__ unsigned long long wsum[32];
   constexpr int PER = PH_BINS / 1024;
@@ -375,6 +382,7 @@ __global__ void __launch_bounds__(1024) k_phase_select(const unsigned int* __res
 __global__ void k_bin_scatter(const uint32_t* __restrict__ key, int64_t P, int lo, int hi,
                               const long long* __restrict__ hi_dev,
                               unsigned int* __restrict__ bin_pos, uint32_t* __restrict__ order) {
+  nxs_pdl_enter();
   if (hi_dev) hi = (int)hi_dev[0];
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -397,6 +405,7 @@ __global__ void __launch_bounds__(BIN_THREADS)
                const unsigned int* __restrict__ hist, const unsigned int* __restrict__ bin_end,
                int lo, int hi, const long long* __restrict__ hi_dev,
                uint32_t* __restrict__ rank_out, unsigned long long* __restrict__ overflow) {
+  nxs_pdl_enter();
   __shared__ unsigned long long s_k[BIN_MAX];
   __shared__ uint32_t s_i[BIN_MAX];
   if (hi_dev) hi = (int)hi_dev[0];
@@ -489,6 +498,7 @@ __global__ void k_chunk_key(const float* __restrict__ centers, const float* __re
                             const uint32_t* __restrict__ rank_c, int chunk,
                             double* __restrict__ zlo, unsigned long long* __restrict__ key64,
                             uint32_t* __restrict__ idx) {
+  nxs_pdl_enter();
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= P) return;
   const double z = z_lower(centers, scales, quats, opacities, g, cam, cutoff);
@@ -505,6 +515,7 @@ template <int THREADS, int ITEMS>
 __global__ void __launch_bounds__(THREADS)
     k_chunk_sort(const uint32_t* __restrict__ order_c, const double* __restrict__ zlo, int64_t P,
                  int chunk, uint32_t* __restrict__ order_out) {
+  nxs_pdl_enter();
   using Sort = cub::BlockRadixSort<uint32_t, THREADS, ITEMS, uint32_t>;
   __shared__ typename Sort::TempStorage tmp;
   const int64_t base = (int64_t)blockIdx.x * chunk;
@@ -788,6 +799,7 @@ __global__ void __launch_bounds__(PROJ_CHUNK)
               const float* __restrict__ sh, int C, int64_t P,
               const uint32_t* __restrict__ rank_of, CamDev cam, double cutoff,
               double near_plane, ProjOut out) {
+  nxs_pdl_enter();
   __shared__ ProjStage st[2];
   __shared__ ProjOutStage so;
   const int tid = threadIdx.x, lane = tid & 31, wbase = tid & ~31;
@@ -905,6 +917,7 @@ __global__ void __launch_bounds__(PROJ_CHUNK)
                     const float* __restrict__ sh, int C, int64_t r0, int64_t r1,
                     const uint32_t* __restrict__ order, CamDev cam, double cutoff,
                     double near_plane, ProjOut out, const int* __restrict__ nd) {
+  nxs_pdl_enter();
   __shared__ ProjOutStage so;
   if (nd) r1 = min(r1, r0 + (int64_t)*nd);
   const int tid = threadIdx.x, lane = tid & 31, wbase = tid & ~31;
@@ -1009,6 +1022,7 @@ __global__ void __launch_bounds__(256)
                    int64_t r0, int64_t r1, int tiles_x, const uint8_t* __restrict__ active,
                    const unsigned int* __restrict__ gate, unsigned long long* __restrict__ counts,
                    const int* __restrict__ nd, const double* __restrict__ tq, CamDev cam) {
+  nxs_pdl_enter();
   // later phases: nothing to count when the previous forward left no tile
   // active (the host then stops before reading the counts)
   if (gate && *gate == 0u) return;
@@ -1043,6 +1057,7 @@ __global__ void __launch_bounds__(256)
                  int tiles_x, const uint8_t* __restrict__ active, uint32_t* __restrict__ keys,
                  uint32_t* __restrict__ vals, const int* __restrict__ nd, unsigned long long cap,
                  const double* __restrict__ tq, CamDev cam) {
+  nxs_pdl_enter();
   if (nd) r1 = min(r1, r0 + (int64_t)*nd);
   const int lane = threadIdx.x & 31, sl = lane & (KSUB - 1), grp = lane / KSUB;
   const int64_t r = r0 + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / KSUB;
@@ -1090,6 +1105,7 @@ __global__ void __launch_bounds__(256)
                   int64_t r0, int64_t r1, int tiles_x, const uint8_t* __restrict__ active,
                   const unsigned int* __restrict__ gate, unsigned int* __restrict__ tile_cnt,
                   const int* __restrict__ nd, const double* __restrict__ tq, CamDev cam) {
+  nxs_pdl_enter();
   if (gate && *gate == 0u) return;
   const int sl = threadIdx.x & (KSUB - 1);
   const int64_t r = r0 + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / KSUB;
@@ -1116,6 +1132,7 @@ __global__ void __launch_bounds__(TSCAN_THREADS)
     k_tile_scan(unsigned int* __restrict__ tile_cnt, int n_tiles, int2* __restrict__ ranges,
                 unsigned long long* __restrict__ total, unsigned long long* __restrict__ maxseg,
                 unsigned long long cap, unsigned long long* __restrict__ overflow, int seg_max) {
+  nxs_pdl_enter();
   typedef cub::BlockScan<unsigned long long, TSCAN_THREADS> Scan;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ unsigned int s_max;
@@ -1175,6 +1192,7 @@ __global__ void __launch_bounds__(TSCAN_THREADS)
 // pass's phase-0 lists: cap_t = n_t + n_t/8 + 8, base = exclusive scan
 __global__ void __launch_bounds__(TSCAN_THREADS)
     k_make_bases(const int2* __restrict__ ranges, int n_tiles, unsigned int* __restrict__ base) {
+  nxs_pdl_enter();
   typedef cub::BlockScan<unsigned long long, TSCAN_THREADS> Scan;
   __shared__ typename Scan::TempStorage tmp;
   const int per = (n_tiles + TSCAN_THREADS - 1) / TSCAN_THREADS;
@@ -1203,6 +1221,7 @@ __global__ void __launch_bounds__(256)
                  uint32_t* __restrict__ vals, const int* __restrict__ nd, unsigned long long cap,
                  const double* __restrict__ tq, CamDev cam, const unsigned int* __restrict__ base,
                  unsigned long long* __restrict__ overflow) {
+  nxs_pdl_enter();
   const int sl = threadIdx.x & (KSUB - 1);
   const int64_t r = r0 + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / KSUB;
   const int64_t rn = nd ? min(r1, r0 + (int64_t)*nd) : r1;
@@ -1240,6 +1259,7 @@ __global__ void __launch_bounds__(256)
                     unsigned int* __restrict__ cursor, int n_tiles, unsigned long long cap,
                     const unsigned int* __restrict__ base, unsigned long long* __restrict__ total,
                     unsigned long long* __restrict__ overflow) {
+  nxs_pdl_enter();
   __shared__ uint32_t s_k[8][SEG_WARP_MAX];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t = blockIdx.x * 8 + w;
@@ -1284,6 +1304,7 @@ __global__ void __launch_bounds__(256)
 __global__ void __launch_bounds__(SEG_THREADS)
     k_seg_sort(uint32_t* __restrict__ vals, const int2* __restrict__ ranges, int n_tiles,
                unsigned long long cap) {
+  nxs_pdl_enter();
   __shared__ uint32_t s_k[SEG_MAX];
   const int tid = threadIdx.x;
   for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
@@ -1331,10 +1352,10 @@ void launch_count_tiles(const int4* rects, const uint32_t* order, int64_t r0, in
                         cudaStream_t s, const int* nd) {
   if (r1 <= r0) return;
   if (r1 - r0 <= 262144)
-    k_count_tiles<32><<<(unsigned)((r1 - r0 + 7) / 8), 256, 0, s>>>(
+    nxs_launch(k_count_tiles<32>, (unsigned)((r1 - r0 + 7) / 8), 256, 0, s, 
         rects, order, r0, r1, tiles_x, active, gate, tile_cnt, nd, tq, cam);
   else
-    k_count_tiles<8><<<(unsigned)((r1 - r0 + 31) / 32), 256, 0, s>>>(
+    nxs_launch(k_count_tiles<8>, (unsigned)((r1 - r0 + 31) / 32), 256, 0, s, 
         rects, order, r0, r1, tiles_x, active, gate, tile_cnt, nd, tq, cam);
 }
 void launch_tile_scan(unsigned int* tile_cnt, int n_tiles, int2* ranges, unsigned long long* total,
@@ -1346,7 +1367,7 @@ void launch_tile_scan(unsigned int* tile_cnt, int n_tiles, int2* ranges, unsigne
                          TSCAN_STAGED * (int)sizeof(unsigned int));
   });
   const size_t dyn = n_tiles <= TSCAN_STAGED ? (size_t)n_tiles * sizeof(unsigned int) : 0;
-  k_tile_scan<<<1, TSCAN_THREADS, dyn, s>>>(tile_cnt, n_tiles, ranges, total, maxseg, cap,
+  nxs_launch(k_tile_scan, 1, TSCAN_THREADS, dyn, s, tile_cnt, n_tiles, ranges, total, maxseg, cap,
                                             overflow, SEG_MAX);
 }
 void launch_emit_tiles(const int4* rects, const uint32_t* order, int64_t r0, int64_t r1,
@@ -1355,17 +1376,21 @@ void launch_emit_tiles(const int4* rects, const uint32_t* order, int64_t r0, int
                        cudaStream_t s, const int* nd, unsigned long long cap,
                        const unsigned int* base, unsigned long long* overflow) {
   if (r1 <= r0) return;
+#ifndef NXS_EMIT_KSUB
+#define NXS_EMIT_KSUB 32
+#endif
+  constexpr int KS = NXS_EMIT_KSUB;  // lanes per rank for a near phase (big rects)
   if (r1 - r0 <= 262144)
-    k_emit_tiles<32><<<(unsigned)((r1 - r0 + 7) / 8), 256, 0, s>>>(
+    nxs_launch(k_emit_tiles<KS>, (unsigned)((r1 - r0 + 256 / KS - 1) / (256 / KS)), 256, 0, s, 
         rects, order, r0, r1, tiles_x, active, ranges, cursor, vals, nd, cap, tq, cam, base,
         overflow);
   else
-    k_emit_tiles<8><<<(unsigned)((r1 - r0 + 31) / 32), 256, 0, s>>>(
+    nxs_launch(k_emit_tiles<8>, (unsigned)((r1 - r0 + 31) / 32), 256, 0, s, 
         rects, order, r0, r1, tiles_x, active, ranges, cursor, vals, nd, cap, tq, cam, base,
         overflow);
 }
 void launch_make_bases(const int2* ranges, int n_tiles, unsigned int* base, cudaStream_t s) {
-  k_make_bases<<<1, TSCAN_THREADS, 0, s>>>(ranges, n_tiles, base);
+  nxs_launch(k_make_bases, 1, TSCAN_THREADS, 0, s, ranges, n_tiles, base);
 }
 
 // After a device-sized pass: re-derive the per-tile capacities from the
@@ -1376,6 +1401,7 @@ void launch_make_bases(const int2* ranges, int n_tiles, unsigned int* base, cuda
 __global__ void __launch_bounds__(TSCAN_THREADS)
     k_refresh_bases(const int2* __restrict__ ranges, int n_tiles, unsigned int* __restrict__ base,
                     unsigned long long bound, unsigned int maxcap) {
+  nxs_pdl_enter();
   typedef cub::BlockScan<unsigned long long, TSCAN_THREADS> Scan;
   __shared__ typename Scan::TempStorage tmp;
   const int per = (n_tiles + TSCAN_THREADS - 1) / TSCAN_THREADS;
@@ -1399,7 +1425,7 @@ __global__ void __launch_bounds__(TSCAN_THREADS)
 }
 void launch_refresh_bases(const int2* ranges, int n_tiles, unsigned int* base,
                           unsigned long long bound, unsigned int maxcap, cudaStream_t s) {
-  k_refresh_bases<<<1, TSCAN_THREADS, 0, s>>>(ranges, n_tiles, base, bound, maxcap);
+  nxs_launch(k_refresh_bases, 1, TSCAN_THREADS, 0, s, ranges, n_tiles, base, bound, maxcap);
 }
 
 // Export: gather each tile's list [ranges[t].x, ranges[t].y) to the compact
@@ -1407,6 +1433,7 @@ void launch_refresh_bases(const int2* ranges, int n_tiles, unsigned int* base,
 __global__ void k_compact_lists(const uint32_t* __restrict__ src, const int2* __restrict__ ranges,
                                 const int* __restrict__ dst_off, int n_tiles,
                                 uint32_t* __restrict__ dst, int2* __restrict__ dst_ranges) {
+  nxs_pdl_enter();
   const int t = blockIdx.x;
   if (t >= n_tiles) return;
   const int2 r = ranges[t];
@@ -1418,26 +1445,27 @@ __global__ void k_compact_lists(const uint32_t* __restrict__ src, const int2* __
 void launch_compact_lists(const uint32_t* src, const int2* ranges, const int* dst_off,
                           int n_tiles, uint32_t* dst, int2* dst_ranges, cudaStream_t s) {
   if (n_tiles > 0)
-    k_compact_lists<<<n_tiles, 128, 0, s>>>(src, ranges, dst_off, n_tiles, dst, dst_ranges);
+    nxs_launch(k_compact_lists, n_tiles, 128, 0, s, src, ranges, dst_off, n_tiles, dst, dst_ranges);
 }
 void launch_seg_sort(uint32_t* vals, int2* ranges, unsigned int* cursor, int n_tiles,
                      unsigned long long cap, cudaStream_t s, long long max_seg,
                      const unsigned int* base, unsigned long long* total,
                      unsigned long long* overflow) {
   if (n_tiles <= 0) return;
-  k_seg_sort_warp<<<(n_tiles + 7) / 8, 256, 0, s>>>(vals, ranges, cursor, n_tiles, cap, base,
+  nxs_launch(k_seg_sort_warp, (n_tiles + 7) / 8, 256, 0, s, vals, ranges, cursor, n_tiles, cap, base,
                                                     total, overflow);
   // (max_seg < 0: unknown on the host)
   if (max_seg < 0 || max_seg > SEG_WARP_MAX) {  // a persistent grid: most tiles are short
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    k_seg_sort<<<std::min(n_tiles, sms * 4), SEG_THREADS, 0, s>>>(vals, ranges, n_tiles, cap);
+    nxs_launch(k_seg_sort, std::min(n_tiles, sms * 4), SEG_THREADS, 0, s, vals, ranges, n_tiles, cap);
   }
 }
 
 __global__ void k_tile_ranges(const uint32_t* __restrict__ keys, int64_t n,
                               int2* __restrict__ ranges) {
+  nxs_pdl_enter();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   uint32_t t = keys[i];
@@ -1456,13 +1484,13 @@ void launch_depth(const float* centers, const float* scales, const float* quats,
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const unsigned grid = (unsigned)std::min<int64_t>((P + 255) / 256, (int64_t)sms * 8);
-  k_depth<<<grid, 256, 0, s>>>(centers, scales, quats, opacities, P, cam, cutoff, zmode, depth,
+  nxs_launch(k_depth, grid, 256, 0, s, centers, scales, quats, opacities, P, cam, cutoff, zmode, depth,
                                key64, idx, kminmax);
 }
 void launch_key32(const double* depth, int64_t P, const unsigned long long* kminmax,
                   uint32_t* key, cudaStream_t s) {
   if (P == 0) return;
-  k_key32<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(depth, P, kminmax, key);
+  nxs_launch(k_key32, (unsigned)((P + 255) / 256), 256, 0, s, depth, P, kminmax, key);
 }
 void launch_key32_hist(const double* depth, int64_t P, const unsigned long long* kminmax,
                        uint32_t* key, unsigned int* hist, cudaStream_t s) {
@@ -1471,16 +1499,16 @@ void launch_key32_hist(const double* depth, int64_t P, const unsigned long long*
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const unsigned grid = (unsigned)std::min<int64_t>((P + 1023) / 1024, (int64_t)sms * 2);
-  k_key32_hist<<<grid, 1024, 0, s>>>(depth, P, kminmax, key, hist);
+  nxs_launch(k_key32_hist, grid, 1024, 0, s, depth, P, kminmax, key, hist);
 }
 void launch_dkeys(const double* depth, int64_t P, unsigned long long* key64, cudaStream_t s) {
   if (P == 0) return;
-  k_dkeys<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(depth, P, key64);
+  nxs_launch(k_dkeys, (unsigned)((P + 255) / 256), 256, 0, s, depth, P, key64);
 }
 void launch_key_fixup(const uint32_t* key, uint32_t* idx, const double* depth, int64_t P,
                       unsigned long long* overflow, cudaStream_t s, int shift, const int* nd) {
   if (P == 0) return;
-  k_key_fixup<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(key, idx, depth, P, shift, overflow,
+  nxs_launch(k_key_fixup, (unsigned)((P + 255) / 256), 256, 0, s, key, idx, depth, P, shift, overflow,
                                                           nd);
 }
 void launch_chunk_key(const float* centers, const float* scales, const float* quats,
@@ -1488,7 +1516,7 @@ void launch_chunk_key(const float* centers, const float* scales, const float* qu
                       const uint32_t* rank_c, int chunk, double* zlo, unsigned long long* key64,
                       uint32_t* idx, cudaStream_t s) {
   if (P == 0) return;
-  k_chunk_key<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(centers, scales, quats, opacities, P,
+  nxs_launch(k_chunk_key, (unsigned)((P + 255) / 256), 256, 0, s, centers, scales, quats, opacities, P,
                                                           cam, cutoff, rank_c, chunk, zlo, key64,
                                                           idx);
 }
@@ -1498,35 +1526,38 @@ bool launch_chunk_sort(const uint32_t* order_c, const double* zlo, int64_t P, in
   if (P == 0) return true;
   const unsigned grid = (unsigned)((P + chunk - 1) / chunk);
   if (chunk <= 128)
-    k_chunk_sort<128, 1><<<grid, 128, 0, s>>>(order_c, zlo, P, chunk, order_out);
+    nxs_launch(k_chunk_sort<128, 1>, grid, 128, 0, s, order_c, zlo, P, chunk, order_out);
   else if (chunk <= 512)
-    k_chunk_sort<128, 4><<<grid, 128, 0, s>>>(order_c, zlo, P, chunk, order_out);
+    nxs_launch(k_chunk_sort<128, 4>, grid, 128, 0, s, order_c, zlo, P, chunk, order_out);
   else if (chunk <= 2048)
-    k_chunk_sort<256, 8><<<grid, 256, 0, s>>>(order_c, zlo, P, chunk, order_out);
+    nxs_launch(k_chunk_sort<256, 8>, grid, 256, 0, s, order_c, zlo, P, chunk, order_out);
   else
     return false;
   return true;
 }
 void launch_rank_of(const uint32_t* order, int64_t P, uint32_t* rank_of, cudaStream_t s) {
   if (P == 0) return;
-  k_rank_of<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(order, 0, P, rank_of, nullptr);
+  nxs_launch(k_rank_of, (unsigned)((P + 255) / 256), 256, 0, s, order, 0, P, rank_of, nullptr);
 }
 void launch_rank_of_range(const uint32_t* order, int64_t r0, int64_t r1, uint32_t* rank_of,
                           cudaStream_t s, const int* nd) {
   if (r1 <= r0) return;
-  k_rank_of<<<(unsigned)((r1 - r0 + 255) / 256), 256, 0, s>>>(order, r0, r1, rank_of, nd);
+  nxs_launch(k_rank_of, (unsigned)((r1 - r0 + 255) / 256), 256, 0, s, order, r0, r1, rank_of, nd);
 }
 __global__ void k_gather_keys(const uint32_t* __restrict__ idx, const uint32_t* __restrict__ key,
                               int64_t n, uint32_t* __restrict__ out) {
+  nxs_pdl_enter();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = key[idx[i]];
 }
 __global__ void k_clear_rects(const uint32_t* __restrict__ order, int64_t r0, int64_t r1,
                               int4* __restrict__ rects) {
+  nxs_pdl_enter();
   const int64_t r = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r < r1) rects[order[r]] = make_int4(-1, -1, -1, -1);
 }
 __global__ void k_iota(uint32_t* __restrict__ a, int64_t n) {
+  nxs_pdl_enter();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) a[i] = (uint32_t)i;
 }
@@ -1536,6 +1567,7 @@ __global__ void k_iota(uint32_t* __restrict__ a, int64_t n) {
 __global__ void k_pack_check(const unsigned long long* __restrict__ dsmall,
                              const long long* __restrict__ dsel, int n_ph,
                              unsigned long long* __restrict__ out) {
+  nxs_pdl_enter();
   const int i = threadIdx.x;
   if (i >= 27) return;
   unsigned long long v = 0ull;
@@ -1558,6 +1590,7 @@ __global__ void k_call_init(unsigned long long* __restrict__ dsmall, uint8_t* __
                             unsigned int* __restrict__ tile_cnt, int n_tiles,
                             long long* __restrict__ dtgt, PhaseTargets tgt, int n_tgt,
                             unsigned int* __restrict__ hist) {
+  nxs_pdl_enter();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (hist && i < 4096) hist[i] = 0u;
   if (i < 16) dsmall[i] = (i == 6) ? ~0ull : 0ull;
@@ -1575,18 +1608,19 @@ void launch_call_init(unsigned long long* dsmall, uint8_t* active, int32_t* cum0
   PhaseTargets t{};
   for (int i = 0; i < n_tgt && i < 4; ++i) t.v[i] = tgt[i];
   const int n = std::max(n_tiles, 4096);
-  k_call_init<<<(n + 255) / 256, 256, 0, s>>>(dsmall, active, cum0, ranges0, tile_cnt, n_tiles, dtgt, t,
+  nxs_launch(k_call_init, (n + 255) / 256, 256, 0, s, dsmall, active, cum0, ranges0, tile_cnt, n_tiles, dtgt, t,
                                               std::min(n_tgt, 4), hist);
 }
 void launch_pack_check(const unsigned long long* dsmall, const long long* dsel, int n_ph,
                        unsigned long long* out, cudaStream_t s) {
-  k_pack_check<<<1, 32, 0, s>>>(dsmall, dsel, n_ph, out);
+  nxs_launch(k_pack_check, 1, 32, 0, s, dsmall, dsel, n_ph, out);
 }
 // exact order over depth phases: a lower bound of the depth key (z_lo) of
 // every Gaussian in the key bins after `bin` (the k_key32 map inverted, with
 // a relative safety margin; smaller is always safe), as float rounded down
 __global__ void k_phase_bound(const unsigned long long* __restrict__ kminmax, int bin,
                               float* __restrict__ out) {
+  nxs_pdl_enter();
   if (kminmax[0] < kminmax[1]) {
     const double lo = dkey_inv(kminmax[0]), hi = dkey_inv(kminmax[1]);
     const double step = (double)((unsigned long long)(bin + 1) << 20) / (4294967294.0 / (hi - lo));
@@ -1597,22 +1631,23 @@ __global__ void k_phase_bound(const unsigned long long* __restrict__ kminmax, in
   }
 }
 void launch_phase_bound(const unsigned long long* kminmax, int bin, float* out, cudaStream_t s) {
-  k_phase_bound<<<1, 1, 0, s>>>(kminmax, bin, out);
+  nxs_launch(k_phase_bound, 1, 1, 0, s, kminmax, bin, out);
 }
 void launch_iota(uint32_t* a, int64_t n, cudaStream_t s) {
   if (n <= 0) return;
-  k_iota<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a, n);
+  nxs_launch(k_iota, (unsigned)((n + 255) / 256), 256, 0, s, a, n);
 }
 void launch_gather_keys(const uint32_t* idx, const uint32_t* key, int64_t n, uint32_t* out,
                         cudaStream_t s) {
   if (n <= 0) return;
-  k_gather_keys<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(idx, key, n, out);
+  nxs_launch(k_gather_keys, (unsigned)((n + 255) / 256), 256, 0, s, idx, key, n, out);
 }
 // chunked lazy phases: z_lo of the Gaussians at ranks [r0, r1)
 __global__ void k_zlo_ranks(const float* __restrict__ centers, const float* __restrict__ scales,
                             const float* __restrict__ quats, const float* __restrict__ opacities,
                             const uint32_t* __restrict__ order, int64_t r0, int64_t r1,
                             CamDev cam, double cutoff, double* __restrict__ zlo) {
+  nxs_pdl_enter();
   const int64_t r = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= r1) return;
   const int64_t g = order[r];
@@ -1622,7 +1657,7 @@ void launch_zlo_ranks(const float* centers, const float* scales, const float* qu
                       const float* opacities, const uint32_t* order, int64_t r0, int64_t r1,
                       const CamDev& cam, double cutoff, double* zlo, cudaStream_t s) {
   if (r1 <= r0) return;
-  k_zlo_ranks<<<(unsigned)((r1 - r0 + 255) / 256), 256, 0, s>>>(centers, scales, quats,
+  nxs_launch(k_zlo_ranks, (unsigned)((r1 - r0 + 255) / 256), 256, 0, s, centers, scales, quats,
                                                                 opacities, order, r0, r1, cam,
                                                                 cutoff, zlo);
 }
@@ -1634,19 +1669,19 @@ void launch_project_ranks_z(const float* centers, const float* scales, const flo
                             double* tq, cudaStream_t s) {
   if (r1 <= r0) return;
   ProjOut o{zlo, zlo_rank, rects, records, bframe, straddle, tq};
-  k_project_ranks<<<(unsigned)((r1 - r0 + PROJ_CHUNK - 1) / PROJ_CHUNK), PROJ_CHUNK, 0, s>>>(
+  nxs_launch(k_project_ranks, (unsigned)((r1 - r0 + PROJ_CHUNK - 1) / PROJ_CHUNK), PROJ_CHUNK, 0, s, 
       centers, scales, quats, opacities, sh, C, r0, r1, order, cam, cutoff, near_plane, o,
       nullptr);
 }
 void launch_clear_rects(const uint32_t* order, int64_t r0, int64_t r1, int4* rects,
                         cudaStream_t s) {
   if (r1 <= r0) return;
-  k_clear_rects<<<(unsigned)((r1 - r0 + 255) / 256), 256, 0, s>>>(order, r0, r1, rects);
+  nxs_launch(k_clear_rects, (unsigned)((r1 - r0 + 255) / 256), 256, 0, s, order, r0, r1, rects);
 }
 void launch_phase_select(const unsigned int* hist, const int64_t* targets, int n_targets,
                          int64_t P, long long* out, cudaStream_t s, int max_bin0,
                          unsigned long long* overflow, unsigned int* bin_pos, int* n_sel) {
-  k_phase_select<<<1, 1024, 0, s>>>(hist, targets, n_targets, P, out, max_bin0, overflow,
+  nxs_launch(k_phase_select, 1, 1024, 0, s, hist, targets, n_targets, P, out, max_bin0, overflow,
                                     bin_pos, n_sel);
 }
 void launch_bin_scatter(const uint32_t* key, int64_t P, int lo, int hi, const long long* hi_dev,
@@ -1656,13 +1691,13 @@ void launch_bin_scatter(const uint32_t* key, int64_t P, int lo, int hi, const lo
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const unsigned grid = (unsigned)std::min<int64_t>((P + 255) / 256, (int64_t)sms * 8);
-  k_bin_scatter<<<grid, 256, 0, s>>>(key, P, lo, hi, hi_dev, bin_pos, order);
+  nxs_launch(k_bin_scatter, grid, 256, 0, s, key, P, lo, hi, hi_dev, bin_pos, order);
 }
 void launch_bin_sort(uint32_t* order, const double* depth, const unsigned int* hist,
                      const unsigned int* bin_end, int lo, int hi, const long long* hi_dev,
                      uint32_t* rank_out, unsigned long long* overflow, cudaStream_t s) {
   if (hi < lo) return;
-  k_bin_sort<<<hi - lo + 1, BIN_THREADS, 0, s>>>(order, depth, hist, bin_end, lo, hi, hi_dev,
+  nxs_launch(k_bin_sort, hi - lo + 1, BIN_THREADS, 0, s, order, depth, hist, bin_end, lo, hi, hi_dev,
                                                  rank_out, overflow);
 }
 void launch_project_ranks(const float* centers, const float* scales, const float* quats,
@@ -1673,7 +1708,7 @@ void launch_project_ranks(const float* centers, const float* scales, const float
                           const int* nd) {
   if (r1 <= r0) return;
   ProjOut o{nullptr, nullptr, rects, records, bframe, straddle, tq};
-  k_project_ranks<<<(unsigned)((r1 - r0 + PROJ_CHUNK - 1) / PROJ_CHUNK), PROJ_CHUNK, 0, s>>>(
+  nxs_launch(k_project_ranks, (unsigned)((r1 - r0 + PROJ_CHUNK - 1) / PROJ_CHUNK), PROJ_CHUNK, 0, s, 
       centers, scales, quats, opacities, sh, C, r0, r1, order, cam, cutoff, near_plane, o, nd);
 }
 
@@ -1689,7 +1724,7 @@ void launch_project(const float* centers, const float* scales, const float* quat
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t n_chunks = (P + PROJ_CHUNK - 1) / PROJ_CHUNK;
   const unsigned grid = (unsigned)std::min<int64_t>(n_chunks, (int64_t)sms * 8);
-  k_project<<<grid, PROJ_CHUNK, 0, s>>>(centers, scales, quats, opacities, sh, C, P, rank_of, cam,
+  nxs_launch(k_project, grid, PROJ_CHUNK, 0, s, centers, scales, quats, opacities, sh, C, P, rank_of, cam,
                                          cutoff, near_plane, o);
 }
 
@@ -1699,10 +1734,10 @@ void launch_count_active(const int4* rects, const uint32_t* order, int64_t r0, i
                          cudaStream_t s, const int* nd) {
   if (r1 <= r0) return;
   if (r1 - r0 <= 262144)
-    k_count_active<32><<<(unsigned)((r1 - r0 + 7) / 8), 256, 0, s>>>(
+    nxs_launch(k_count_active<32>, (unsigned)((r1 - r0 + 7) / 8), 256, 0, s, 
         rects, order, r0, r1, tiles_x, active, gate, counts, nd, tq, cam);
   else
-    k_count_active<8><<<(unsigned)((r1 - r0 + 31) / 32), 256, 0, s>>>(
+    nxs_launch(k_count_active<8>, (unsigned)((r1 - r0 + 31) / 32), 256, 0, s, 
         rects, order, r0, r1, tiles_x, active, gate, counts, nd, tq, cam);
 }
 
@@ -1712,16 +1747,16 @@ void launch_emit_pairs(const int4* rects, const uint32_t* order, const unsigned 
                        const int* nd, unsigned long long cap) {
   if (r1 <= r0) return;
   if (r1 - r0 <= 262144)
-    k_emit_pairs<32><<<(unsigned)((r1 - r0 + 7) / 8), 256, 0, s>>>(
+    nxs_launch(k_emit_pairs<32>, (unsigned)((r1 - r0 + 7) / 8), 256, 0, s, 
         rects, order, offsets, r0, r1, tiles_x, active, keys, vals, nd, cap, tq, cam);
   else
-    k_emit_pairs<8><<<(unsigned)((r1 - r0 + 31) / 32), 256, 0, s>>>(
+    nxs_launch(k_emit_pairs<8>, (unsigned)((r1 - r0 + 31) / 32), 256, 0, s, 
         rects, order, offsets, r0, r1, tiles_x, active, keys, vals, nd, cap, tq, cam);
 }
 
 void launch_tile_ranges(const uint32_t* keys, int64_t n, int2* ranges, cudaStream_t s) {
   if (n == 0) return;
-  k_tile_ranges<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(keys, n, ranges);
+  nxs_launch(k_tile_ranges, (unsigned)((n + 255) / 256), 256, 0, s, keys, n, ranges);
 }
 
 }  // namespace nxs
