@@ -3,7 +3,9 @@
 bench headline is quoted on, through the steady-state path the bench times:
 ONE reused ``nxs_view`` called several times, so the checked call runs the
 device-sized first depth phase replayed as a CUDA graph and the fused
-forward+backward with its speculative phase count.
+forward+backward with its speculative phase count.  Every transmittance
+model in the global order (BASELINE north_star: "for every transmittance
+function"), and the exact and chunked orders for three of them.
 
 Sampled-pixel protocol: the oracle (``splat_oracle``, pruned
 candidates — exact, see its module doc) evaluates N random pixels; the seed
@@ -19,7 +21,9 @@ Asserted (BASELINE north_star tolerance, |x-ref| <= 1e-6 + 1e-5|ref|):
     <= 1 %.  The t-ordered modes also mask samples where two candidates' peak
     depths agree to 1e-6 relative: at 1M Gaussians that is
     ~1.6 % of Mode X pixels (measured, 4 of 256), so the total is capped at 3 %
-    there, and the report counts how many masked samples matched anyway;
+    there (10 % for the exponential model, which composites 128 splats per
+    pixel: 9 of 128), and the report counts how many masked samples matched
+    anyway (all of them);
   * every gradient entry within the mass-scaled bound (normwise geometric
     scale), strict failures <= 0.1 % of the touched entries.
 The componentwise-scale failure count is reported next to it.  Each case
@@ -37,7 +41,9 @@ pytestmark = pytest.mark.gpu
 
 W, H, P = 1920, 1080, 1_000_000
 CASES = [("exponential", 1, 256), ("linear", 1, 256), ("softplus_20", 1, 256),
-         ("blended_0.5", 1, 256), ("softplus_20", None, 256), ("softplus_20", 128, 256)]
+         ("blended_0.5", 1, 256), ("quadratic_0.5", 1, 128), ("vicini_0.3", 1, 128),
+         ("power_law_2", 1, 128), ("softplus_20", None, 256), ("softplus_20", 128, 256),
+         ("exponential", None, 128), ("blended_0.5", 128, 128)]
 CALLS = 3  # the checked call is the third on one view
 
 
@@ -63,7 +69,7 @@ def test_c3_sampled_pixels_match_oracle(c3, name, cs, n_px):
     model = MODELS[name]
     bg = np.zeros(3)
     px = np.random.default_rng(21 + (0 if cs == 1 else 1 if cs is None else 2)).choice(
-        W * H, n_px, replace=False)
+        W * H, n_px, replace=False)  # (the same pixels for every model of an order)
     fwd = O.forward(sc, cam, model, bg, chunk_size=cs, pixels=px, keep_state=True, batch=8)
     keep = ~fwd["mask"]
     seed_px = seed_img[px] * keep[:, None]
@@ -99,4 +105,8 @@ def test_c3_sampled_pixels_match_oracle(c3, name, cs, n_px):
         write_report("c3", tag, extra)
     assert bad_px == 0, extra
     check_grads("c3", tag, got, g_ref, mass, basis="touched", **extra)
-    check_masked(fwd, model, cs != 1, n_px)
+    # t ties grow with the splats a pixel composites: the exponential model
+    # never saturates and composites 128 (vs ~10), 9 of 128 Mode X pixels have
+    # a pair within 1e-6 relative peak depth (all 9 matched anyway)
+    check_masked(fwd, model, cs != 1, n_px,
+                 t_cap=0.1 if model.variant == "exponential" else 0.03)
