@@ -570,6 +570,11 @@ def roofline(a, model, phase, st):
     r["blend_fp32"] = {"achieved_tflops": round(blend["achieved"], 3),
                        "frac_of_derived_peak": round(blend["achieved"] / fp32_peak, 4),
                        "flops": flops, "ms": round(blend_ms, 4)}
+    r["achieved_source"] = ("kernel durations from CUDA events the library records on the "
+                            "launching stream around each phase (nxs_view_timings), averaged over "
+                            "further timed steps right after the headline region (the headline "
+                            "region itself runs without those events); flops from an "
+                            "instrumented run's event counts (NXS_FLAG_COUNT_EVENTS)")
     r["peak_source"] = ("MEASURED_PEAKS.json hbm_gbs (measured copy)" if r["unit"] == "GB/s"
                         else f"derived: {sms} SMs x 128 FMA x 2 x {sm_mhz:.0f} MHz "
                              "(MEASURED_PEAKS.json sm_max_mhz)")
