@@ -63,8 +63,10 @@ class GradBuffer:
                        "sh": (n, 3, sh_coeffs)}
         self.flat = torch.zeros(sum(self.sizes.values()), dtype=dtype, device=device)
         self.mask = torch.zeros(n, dtype=torch.uint8, device=device)
-        # True while `mask` flags every non-zero row (rendering marks it)
-        self.mask_exact = True
+        # True while `mask` flags every non-zero row: set by
+        # device_view_renderer after it marks the rows a view wrote; any other
+        # writer of the buffer must leave it False (the clear is then dense)
+        self.mask_exact = False
         self.fields = {}
         off = 0
         for k, sz in self.sizes.items():
@@ -76,17 +78,23 @@ class GradBuffer:
         return 11 + 3 * self.c
 
     def zero_(self):
-        """Clear the buffer: only the flagged rows when the mask is exact."""
-        if self.flat.is_cuda and self.mask_exact and self.flat.dtype.is_floating_point:
+        """Clear the buffer: only the flagged rows when the mask is exact
+        (the previous step's writes all went through a marking renderer)."""
+        if self.flat.is_cuda and self.mask_exact and self.flat.dtype == torch_f32():
             from . import _native
             _native.grads_zero_masked(self.flat, self.n, self.c, self.mask)
         else:
             self.flat.zero_()
             self.mask.zero_()
-            self.mask_exact = True
+        self.mask_exact = False
 
     def __getitem__(self, k):
         return self.fields[k]
+
+
+def torch_f32():
+    import torch
+    return torch.float32
 
 
 def _rows_cpu(grads: GradBuffer) -> dict:
@@ -112,9 +120,11 @@ def sparse_allreduce(grads: GradBuffer, group=None, dense_above: float = 0.5) ->
         for t in rows.values():
             mask |= (t != 0).any(dim=1).to(torch.uint8)
         grads.mask.copy_(mask)
-    elif not grads.mask_exact:
-        raise RuntimeError("sparse_allreduce: the touched mask is not exact (use the dense "
-                           "all-reduce, or render through device_view_renderer)")
+    elif not grads.mask_exact:  # written by some other renderer: derive the mask
+        grads.mask.zero_()
+        for t in _rows_cpu(grads).values():
+            grads.mask |= (t != 0).any(dim=1).to(torch.uint8)
+        grads.mask_exact = True
     dist.all_reduce(grads.mask, op=dist.ReduceOp.MAX, group=group)
     if not grads.flat.is_cuda:
         idx = torch.nonzero(grads.mask, as_tuple=False).squeeze(1)
@@ -214,6 +224,7 @@ def device_view_renderer(dev_scene, model, background, cameras, seeds, *, chunk_
                                        out=outs.get(slot), deterministic=deterministic)
         outs[slot] = o
         view.touched_mark(grads.mask)
+        grads.mask_exact = True  # (this step's earlier writes were marked too, or cleared)
 
     render_view.workspaces = workspaces
     render_view.outputs = outs
