@@ -118,7 +118,7 @@ __device__ __forceinline__ bool test_with_t(const float4* rec, const CamDev& cam
   return true;
 }
 
-template <int FAM, bool COUNT, int XBUF>
+template <int FAM, bool COUNT, int XBUF, bool CH>
 __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
     k_blend_fwd_x(const float4* __restrict__ records, const uint32_t* __restrict__ pairs,
                   const int2* __restrict__ ranges, const float* __restrict__ zlo_rank,
@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
       s_rank[tid] = rk;
       s_ring_rank[(base + tid) % (2 * XBT)] = rk;
       s_zlo[tid] = zlo_rank[rk];
-      s_chunk[tid] = chunk > 0 ? rank_c[order[rk]] / (uint32_t)chunk : 0u;
+      if (CH) s_chunk[tid] = rank_c[order[rk]] / (uint32_t)chunk;
     }
     __syncthreads();
     // stage this batch into the ring slot it maps to (positions are consecutive)
@@ -294,7 +294,7 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
         const float4* s_rec_j = s_ring[(base + j) % (2 * XBT)];
         // every remaining entry has t >= bound: pending entries below it are
         // final; a new chunk makes every pending entry final
-        const bool next_chunk = s_chunk[j] != cur_chunk;
+        const bool next_chunk = CH && s_chunk[j] != cur_chunk;  // (exact order: one chunk)
         const float bound = s_zlo[j] * hnorm;
         while (nb > 0 && (next_chunk || thead < bound)) {
           commit_front();
@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
           dpos = base + j;
           break;
         }
-        cur_chunk = s_chunk[j];
+        if (CH) cur_chunk = s_chunk[j];
         if (COUNT) ++ntest;
         TestOut t;
         float tpk;
@@ -616,10 +616,14 @@ static void launch_fwd_x_xb(bool count, int n_tiles, const FwdXArgs& a, const Ca
                             Counters* cnt, cudaStream_t s) {
   static unsigned long long attr_dev = 0;
   once_per_device(attr_dev, [] {
-    set_smem(k_blend_fwd_x<FAM, true, XB>, fwdx_smem(XB));
-    set_smem(k_blend_fwd_x<FAM, false, XB>, fwdx_smem(XB));
+    set_smem(k_blend_fwd_x<FAM, true, XB, true>, fwdx_smem(XB));
+    set_smem(k_blend_fwd_x<FAM, false, XB, true>, fwdx_smem(XB));
+    set_smem(k_blend_fwd_x<FAM, true, XB, false>, fwdx_smem(XB));
+    set_smem(k_blend_fwd_x<FAM, false, XB, false>, fwdx_smem(XB));
   });
-  auto k = count ? k_blend_fwd_x<FAM, true, XB> : k_blend_fwd_x<FAM, false, XB>;
+  // (CH: chunked order; the exact order carries no chunk ids)
+  auto k = a.chunk > 0 ? (count ? k_blend_fwd_x<FAM, true, XB, true> : k_blend_fwd_x<FAM, false, XB, true>)
+                       : (count ? k_blend_fwd_x<FAM, true, XB, false> : k_blend_fwd_x<FAM, false, XB, false>);
   nxs_launch(k, n_tiles, TILE_PIX, fwdx_smem(XB), s, 
       a.records, a.pairs, a.ranges, a.zlo_rank, a.order, a.rank_c, a.chunk, cam, m, a.max_splats,
       a.cutoff, a.near_plane, a.bg[0], a.bg[1], a.bg[2], a.rgb, a.overdraw, a.residual, cache, rs,
