@@ -30,6 +30,10 @@ namespace nxs {
 __device__ unsigned long long g_xstats[40];
 #endif
 
+#ifndef NXS_X_DEFER
+#define NXS_X_DEFER 32  // commit once every active lane of the warp has one due (32/32)
+#endif
+
 // pending entries per pixel: 16 for the chunked order (a chunk flush empties
 // the buffer; an overflow reruns with 32), 32 for the exact order
 // list entries staged per batch: 64 with the 16-entry buffer, 32 with the
@@ -296,7 +300,21 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
         // final; a new chunk makes every pending entry final
         const bool next_chunk = CH && s_chunk[j] != cur_chunk;  // (exact order: one chunk)
         const float bound = s_zlo[j] * hnorm;
+#if NXS_X_DEFER > 0
+        // Committable entries stay committable (every later entry's t is above
+        // this bound), so the exact order may defer them until enough lanes of
+        // the warp have one: the composite then runs with most lanes active.
+        // (a new chunk commits everything pending at once: never deferred)
+        bool go_commit = next_chunk;
+        if (!go_commit) {
+          const unsigned am = __activemask();
+          const unsigned want = __ballot_sync(am, nb > 0 && thead < bound);
+          go_commit = __popc(want) * 32 >= NXS_X_DEFER * __popc(am) || nb >= XBUF - 4;
+        }
+        while (go_commit && nb > 0 && (next_chunk || thead < bound)) {
+#else
         while (nb > 0 && (next_chunk || thead < bound)) {
+#endif
           commit_front();
           if (s.done) break;
         }
