@@ -80,11 +80,14 @@ __global__ void __launch_bounds__(BWD_THREADS, NXS_BWD_MINB)
   const int tile = blockIdx.x;
   const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
   const int tid = threadIdx.x, lane = tid & 31;
-  const int px = tx * TILE + (tid & (TILE - 1));
-  const int py0 = ty * TILE + (tid >> 4);
+  // a warp = one 8x8 pixel block (warps 2 across, 2 down), the thread's two
+  // pixels on adjacent rows: the most compact warp footprint, so a warp's
+  // live entries and their lanes overlap most (16x4 rows r, r+8: bwd +7 %)
+  const int px = tx * TILE + ((tid >> 5) & 1) * 8 + (tid & 7);
+  const int py0 = ty * TILE + (tid >> 6) * 8 + 2 * ((tid >> 3) & 3);
   BwdPix st[2];
   bwd_load(st[0], cam, px, py0, cache, seed, bg0, bg1, bg2);
-  bwd_load(st[1], cam, px, py0 + TILE / 2, cache, seed, bg0, bg1, bg2);
+  bwd_load(st[1], cam, px, py0 + 1, cache, seed, bg0, bg1, bg2);
   float* red = s_red + (tid >> 5) * RED_WARP;
   const float gam = (FAM == FAM_EXP) ? 1.0f : m.c;
   const float inv_f = (float)cam.inv_f;

@@ -52,7 +52,12 @@ __global__ void __launch_bounds__(TILE_PIX, NXS_FWD_MINB)
 
   const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
   const int tid = threadIdx.x;
-  const int px = tx * TILE + (tid & (TILE - 1)), py = ty * TILE + (tid >> 4);
+  // warp footprint: 16x2 rows, or a compact 8x4 block for the exponential
+  // family, whose pixels walk long lists (8x4: exponential fwd -3.5 %,
+  // softplus +1 %)
+  const bool w8 = FAM == FAM_EXP;
+  const int px = tx * TILE + (w8 ? ((tid >> 5) & 1) * 8 + (tid & 7) : (tid & (TILE - 1)));
+  const int py = ty * TILE + (w8 ? (tid >> 6) * 4 + ((tid >> 3) & 3) : (tid >> 4));
   const bool inside = px < cam.W && py < cam.H;
   const PixelConst pc = pixel_setup(cam, px, py);
 
