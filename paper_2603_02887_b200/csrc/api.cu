@@ -218,6 +218,7 @@ struct nxs_view {
   Buf pk_in, pk_out, pv_in, pv_ph[MAX_PHASES];
   // per tile: phase ranges and virtual offsets, activity
   Buf ranges_ph[MAX_PHASES], cum_ph[MAX_PHASES + 1], active, tile_cnt;
+  Buf tile_last;  // per tile: max over its pixels' last list position (K3 -> K4)
   Buf bin_pos;  // per depth-key bin: first rank, then the scatter cursor
   // per-tile list capacities for the device-sized first phase (from the
   // view's last exact phase 0): emission needs no count pass while they hold
@@ -297,7 +298,7 @@ struct nxs_view {
   void for_each_buf(F f) {
     Buf* all[] = {&dkeys_in, &dkeys_out, &idx_in,  &idx_out, &records, &bframe, &rects,
                   &ntiles,   &offsets,   &moments, &touched, &pk_in,   &pk_out,  &pv_in,  &active,
-                  &tile_cnt, &bin_pos, &tile_base,
+                  &tile_cnt, &tile_last, &bin_pos, &tile_base,
                   &depth,    &k32a,      &k32b,    &k32c,    &rank_of, &rank_c, &zlo_rank, &seq, &ph_hist,
                   &ph_sel,   &tq,      &zlo64,  &xc_t, &xc_r, &xc_n,
                   &c_last,   &c_sat,     &c_tk,    &c_thi,   &c_tlo,   &c_P,    &c_ck,
@@ -778,6 +779,7 @@ int forward_impl(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
   NXS_CUDA(ensure_n<int2>(v->ranges_ph[0], n_tiles));
   NXS_CUDA(ensure_n<int32_t>(v->cum_ph[0], n_tiles));
   NXS_CUDA(ensure_n<uint32_t>(v->tile_cnt, n_tiles));
+  NXS_CUDA(ensure_n<int32_t>(v->tile_last, n_tiles));
   NXS_CUDA(ensure_n<uint32_t>(v->bin_pos, 4096 * 32));  // (one cursor per 128-byte line)
   NXS_CUDA(v->ph_hist.ensure(4096 * sizeof(unsigned int)));
   NXS_CUDA(v->ph_sel.ensure(96 * sizeof(long long)));
@@ -1492,7 +1494,7 @@ retry_sort:
                v->active.as<uint8_t>(), n_active, ph > 0, ph + 1 < n_ph, opts->max_splats,
                (float)opts->alpha_cutoff, opts->near_plane, {bgf[0], bgf[1], bgf[2]},
                rgb, overdraw, residual, v->lazy ? dsmall + 12 : nullptr,
-               (opts->flags & NXS_FLAG_THETA0) != 0};
+               (opts->flags & NXS_FLAG_THETA0) != 0, v->tile_last.as<int32_t>()};
     launch_blend_fwd(count, n_tiles, fa, cam, md, v->cache(), v->resume(), cnt, s);
     g_ht.mark("fwd_enq");
     NXS_LAUNCHED("blend_fwd");
@@ -1632,6 +1634,7 @@ int backward_blend(nxs_view* v, const float* seed, cudaStream_t s) {
     lists.cum[p] = v->cum_ph[p].as<int32_t>();
   }
   lists.partial = nullptr;
+  lists.tile_last = v->tile_last.as<int32_t>();  // written by every K3 pass of the tile
   if (det) {  // partials per (tile, entry), reduced per rank in a fixed order
     int64_t off = 0;
     for (int p = 0; p < v->n_phases; ++p) {

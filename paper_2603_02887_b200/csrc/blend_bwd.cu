@@ -86,22 +86,16 @@ __global__ void __launch_bounds__(BWD_THREADS, NXS_BWD_MINB)
   const int px = tx * TILE + ((tid >> 5) & 1) * 8 + (tid & 7);
   const int py0 = ty * TILE + (tid >> 6) * 8 + 2 * ((tid >> 3) & 3);
   BwdPix st[2];
-  bwd_load(st[0], cam, px, py0, cache, seed, bg0, bg1, bg2);
-  bwd_load(st[1], cam, px, py0 + 1, cache, seed, bg0, bg1, bg2);
   float* red = s_red + (tid >> 5) * RED_WARP;
   const float gam = (FAM == FAM_EXP) ? 1.0f : m.c;
   const float inv_f = (float)cam.inv_f;
   const float Y0 = (float)SH_C0;
   unsigned long long ntest = 0, nent = 0;
 
-  if (tid == 0) s_maxlast = -1;
-  __syncthreads();
-  const int mylast = max(st[0].last, st[1].last);
-  if (mylast >= 0) atomicMax(&s_maxlast, mylast);
-  __syncthreads();
-  const int vmax = s_maxlast + 1;  // virtual per-tile list positions [0, vmax) are replayed
-  // this warp's last live entry: the entries behind it skip the warp
-  const int wlast = __reduce_max_sync(0xffffffffu, mylast);
+  // virtual per-tile list positions [0, vmax) are replayed: the forward
+  // recorded the tile's largest, so the first batch streams in while the
+  // pixels' cache loads are in flight, with no block-wide max
+  const int vmax = lists.tile_last[tile] + 1;
 
   // phases back to front, each phase's segment back to front, in batches of
   // BWD_BATCH virtual positions [base, hi); batch (ph, hi) -> the next one
@@ -151,6 +145,18 @@ __global__ void __launch_bounds__(BWD_THREADS, NXS_BWD_MINB)
     }
   }
   if (have) stage(0, ph, hi);
+  bwd_load(st[0], cam, px, py0, cache, seed, bg0, bg1, bg2);
+  bwd_load(st[1], cam, px, py0 + 1, cache, seed, bg0, bg1, bg2);
+  const int mylast = max(st[0].last, st[1].last);
+  // this warp's last live entry: the entries behind it skip the warp
+  const int wlast = __reduce_max_sync(0xffffffffu, mylast);
+#ifdef NXS_CHECKS
+  if (tid == 0) s_maxlast = -1;
+  __syncthreads();
+  if (mylast >= 0) atomicMax(&s_maxlast, mylast);
+  __syncthreads();
+  NXS_CHECK(s_maxlast + 1 == vmax);
+#endif
   int buf = 0;
   while (have) {
     const int c0 = lists.cum[ph][tile];

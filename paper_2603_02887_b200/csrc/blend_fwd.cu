@@ -42,7 +42,8 @@ __global__ void __launch_bounds__(TILE_PIX, NXS_FWD_MINB)
                 int max_splats, float cutoff, double near_plane, float bg0, float bg1, float bg2,
                 float* __restrict__ rgb, int32_t* __restrict__ overdraw,
                 float* __restrict__ residual, PixCache cache, PixResume rs,
-                unsigned long long* __restrict__ need_rank, Counters* __restrict__ cnt) {
+                unsigned long long* __restrict__ need_rank, int32_t* __restrict__ tile_last,
+                Counters* __restrict__ cnt) {
   nxs_pdl_enter();
   const int tile = blockIdx.x;
   if (!active[tile]) return;  // every pixel of the tile finished in an earlier phase
@@ -216,12 +217,17 @@ __global__ void __launch_bounds__(TILE_PIX, NXS_FWD_MINB)
     if (__syncthreads_count(!done) == 0) break;
   }
   cp_async_wait<0>();
-  __shared__ int s_dpos;
-  if (tid == 0) s_dpos = -1;
+  __shared__ int s_dpos, s_last;
+  if (tid == 0) s_dpos = s_last = -1;
   const int still = __syncthreads_count(!done);
   if (still == 0 && need_rank && dpos >= 0) atomicMax(&s_dpos, dpos);
+  {  // the tile's last replayed position: K4 sizes its batches from it
+    const int wl = __reduce_max_sync(0xffffffffu, last);
+    if ((tid & 31) == 0 && wl >= 0) atomicMax(&s_last, wl);
+  }
   __syncthreads();
   if (tid == 0) {
+    tile_last[tile] = s_last;
     active[tile] = still > 0 ? 1 : 0;
     cum_out[tile] = cum_in[tile] + (rg.y - rg.x);
     if (still > 0) atomicAdd(n_active, 1u);
@@ -290,7 +296,7 @@ static void launch_fwd_fam(bool count, int n_tiles, const FwdArgs& a, const CamD
   nxs_launch(k, n_tiles, TILE_PIX, 0, s, a.records, a.pairs, a.ranges, a.cum_in, a.cum_out, a.active,
                                  a.n_active, a.resume, a.save, cam, m, a.max_splats, a.cutoff,
                                  a.near_plane, a.bg[0], a.bg[1], a.bg[2], a.rgb, a.overdraw,
-                                 a.residual, cache, rs, a.need_rank, cnt);
+                                 a.residual, cache, rs, a.need_rank, a.tile_last, cnt);
 }
 
 void launch_blend_fwd(bool count, int n_tiles, const FwdArgs& a, const CamDev& cam,

@@ -179,6 +179,8 @@ struct PhaseLists {  // the per-tile virtual list = phase segments in order
   // moment partials at partial[(poff[p] + index in pairs[p]) * NMOM + m]
   float* partial;
   int64_t poff[MAX_PHASES];
+  // per tile: the largest virtual position any pixel replays (K3 writes it)
+  const int32_t* tile_last;
 };
 
 // arguments of one forward phase launch
@@ -203,6 +205,7 @@ struct FwdArgs {
   // needed (the view's first-phase hint for its next call), or null
   unsigned long long* need_rank;
   bool theta0;  // accumulate the reference cache's theta0 (NXS_FLAG_THETA0)
+  int32_t* tile_last;  // per tile: max of its pixels' last (read by K4)
 };
 
 // exact-order mode (K3x/K4x)
