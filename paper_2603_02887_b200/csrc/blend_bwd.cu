@@ -75,7 +75,9 @@ __global__ void __launch_bounds__(BWD_THREADS, NXS_BWD_MINB)
       reinterpret_cast<uint32_t(*)[BWD_BATCH]>(smem_dyn + 2 * BWD_BATCH * (REC_F4 + 3));
   float* s_acc = reinterpret_cast<float*>(s_rank2 + 2);
   float* s_red = s_acc + BWD_BATCH * NMOM * acc_rows(DET);
-  __shared__ int s_maxlast;
+#ifdef NXS_CHECKS
+  __shared__ int s_maxlast;  // (checks the forward's per-tile last position)
+#endif
 
   const int tile = blockIdx.x;
   const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;

@@ -467,8 +467,8 @@ constexpr int XREC_F4 = REC_F4 + 3;
 constexpr size_t BWDX_WARP_FLOATS = NMOM * XRED_STRIDE + 2 * XREC_F4 * 4;
 constexpr size_t BWDX_SMEM = sizeof(float) * BWDX_WARP_FLOATS * (TILE_PIX / 2 / 32);
 
-// Two pixels per thread (rows r and r + 8, a 128-thread block per tile, as
-// K4): each warp step serves the largest pending rank over its 64 pixels,
+// Two pixels per thread (adjacent rows, a warp = one 8x8 block, a 128-thread
+// block per tile, as K4): each warp step serves the largest pending rank over its 64 pixels,
 // and a thread adds both of its pixels' moments before the warp reduction.
 constexpr int BWDX_THREADS = TILE_PIX / 2;
 

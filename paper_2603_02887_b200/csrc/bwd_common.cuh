@@ -125,7 +125,7 @@ __device__ __forceinline__ bool bwd_pixel(BwdPix& st, const float4* rec, const f
 
 // ---------------------------------------------------------------------------
 // Packed two-pixel step (Blackwell FFMA2/FADD2/FMUL2).  The global-order
-// backward gives each thread two pixels of the same column (rows r, r+8), so
+// backward gives each thread two pixels of the same column (adjacent rows), so
 // every per-pixel fp32 operation of the common record kind (conic, not thin)
 // runs as one f32x2 instruction on the pair; record values enter as scalar
 // broadcast operands.  Each lane of an f32x2 op is the IEEE round-to-nearest
