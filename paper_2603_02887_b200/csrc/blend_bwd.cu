@@ -55,6 +55,93 @@ constexpr size_t bwd_smem(bool det) {
          sizeof(float) * BWD_BATCH * NMOM * acc_rows(det) + sizeof(float) * RED_WARP * BWD_WARPS;
 }
 
+// Per list entry: each thread adds its two pixels' 24 moments, the warp
+// transposes them through `red` (12 moment-pair rows) and lane m < NMOM
+// returns moment m summed over the warp's 64 pixels.
+__device__ __forceinline__ float warp_moments(const PairOut& po, const PixelConst& pa,
+                                              const PixelConst& pb, float* red, int lane,
+                                              float Y0) {
+  // warp transpose-reduce through shared memory (moment-pair rows)
+  const F2 a = mul2(po.dm2, po.ux), b = mul2(po.dm2, po.uy), c = mul2(po.dm2, po.uz);
+  // moment pairs (2p, 2p+1) as one 8-byte store; rows 9 and 10 are unused
+  float v[NMOM];
+  v[0] = fmaf(a.x, po.ux.x, a.y * po.ux.y);
+  v[1] = fmaf(a.x, po.uy.x, a.y * po.uy.y);
+  v[2] = fmaf(a.x, po.uz.x, a.y * po.uz.y);
+  v[3] = fmaf(b.x, po.uy.x, b.y * po.uy.y);
+  v[4] = fmaf(b.x, po.uz.x, b.y * po.uz.y);
+  v[5] = fmaf(c.x, po.uz.x, c.y * po.uz.y);
+  v[6] = a.x + a.y;
+  v[7] = b.x + b.y;
+  v[8] = c.x + c.y;
+  v[9] = 0.f;
+  v[10] = 0.f;
+  v[11] = po.dak.x + po.dak.y;
+  v[12] = (po.e0.x + po.e0.y) * Y0;
+  v[13] = fmaf(po.e0.x, pa.Y1, po.e0.y * pb.Y1);
+  v[14] = fmaf(po.e0.x, pa.Y2, po.e0.y * pb.Y2);
+  v[15] = fmaf(po.e0.x, pa.Y3, po.e0.y * pb.Y3);
+  v[16] = (po.e1.x + po.e1.y) * Y0;
+  v[17] = fmaf(po.e1.x, pa.Y1, po.e1.y * pb.Y1);
+  v[18] = fmaf(po.e1.x, pa.Y2, po.e1.y * pb.Y2);
+  v[19] = fmaf(po.e1.x, pa.Y3, po.e1.y * pb.Y3);
+  v[20] = (po.e2.x + po.e2.y) * Y0;
+  v[21] = fmaf(po.e2.x, pa.Y1, po.e2.y * pb.Y1);
+  v[22] = fmaf(po.e2.x, pa.Y2, po.e2.y * pb.Y2);
+  v[23] = fmaf(po.e2.x, pa.Y3, po.e2.y * pb.Y3);
+  float2* col = reinterpret_cast<float2*>(red + (lane < 16 ? 2 * lane : RED_HALF + 2 * (lane - 16)));
+#pragma unroll
+  for (int q = 0; q < NMOM / 2; ++q) col[q * (RED_ROW / 2)] = make_float2(v[2 * q], v[2 * q + 1]);
+  __syncwarp();
+  // lane 2p sums moments (2p, 2p+1) over lanes 0-15, lane 2p+1 over
+  // lanes 16-31 (packed adds), then each keeps its own moment and
+  // takes the partner's half of it
+  F2 part = f2(0.f);
+  if (lane < NMOM) {
+    const float4* row =
+        reinterpret_cast<const float4*>(red + (lane >> 1) * RED_ROW + (lane & 1) * RED_HALF);
+    F2 t[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float4 r = row[i];
+      t[i] = add2(F2{r.x, r.y}, F2{r.z, r.w});
+    }
+    part = add2(add2(add2(t[0], t[1]), add2(t[2], t[3])), add2(add2(t[4], t[5]), add2(t[6], t[7])));
+  }
+  const float other = __shfl_xor_sync(0xffffffffu, (lane & 1) ? part.x : part.y, 1);
+  const float sum = ((lane & 1) ? part.y : part.x) + other;
+  return sum;
+}
+
+// Both pixels' contributions of list entry idx (lane x: pixel a, y: b), zero
+// where a pixel does not contribute, so the moments need no separate
+// masking: the packed pair step for conic non-thin records (uniform over the
+// warp: every lane reads the same record), else the scalar per-pixel path.
+template <int FAM, bool COUNT>
+__device__ __forceinline__ bool entry_step(BwdPix (&st)[2], const float4* rec, const float4* bf,
+                                           int idx, const CamDev& cam, const ModelDev& m,
+                                           float cutoff, double near_plane, float inv_f,
+                                           float gam, PairOut& po, unsigned long long& ntest) {
+  if ((__float_as_int(rec[3].w) & (RF_GENERAL | RF_ANISO)) == 0)
+    return bwd_pair<FAM>(st[0], st[1], rec, bf, idx, m, cutoff, inv_f, gam, po, ntest, COUNT);
+  float dm2[2] = {0.f, 0.f}, ux[2] = {0.f, 0.f}, uy[2] = {0.f, 0.f}, uz[2] = {0.f, 0.f};
+  float dak[2] = {0.f, 0.f}, e0[2] = {0.f, 0.f}, e1[2] = {0.f, 0.f}, e2[2] = {0.f, 0.f};
+  bool contrib = false;
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+    contrib |= bwd_pixel<FAM>(st[q], rec, bf, idx, cam, m, cutoff, near_plane, inv_f, gam, dm2[q],
+                              ux[q], uy[q], uz[q], dak[q], e0[q], e1[q], e2[q], ntest, COUNT);
+  po.dm2 = F2{dm2[0], dm2[1]};
+  po.ux = F2{ux[0], ux[1]};
+  po.uy = F2{uy[0], uy[1]};
+  po.uz = F2{uz[0], uz[1]};
+  po.dak = F2{dak[0], dak[1]};
+  po.e0 = F2{e0[0], e0[1]};
+  po.e1 = F2{e1[0], e1[1]};
+  po.e2 = F2{e2[0], e2[1]};
+  return contrib;
+}
+
 #ifndef NXS_BWD_MINB
 #define NXS_BWD_MINB 4
 #endif
@@ -189,80 +276,10 @@ __global__ void __launch_bounds__(BWD_THREADS, NXS_BWD_MINB)
         // both pixels' contributions (lane x: pixel a, y: b), zero where a
         // pixel does not contribute, so the moments need no separate masking
         PairOut po;
-        bool contrib;
-        if ((__float_as_int(s_rec[j][3].w) & (RF_GENERAL | RF_ANISO)) == 0) {  // block-uniform
-          contrib = bwd_pair<FAM>(st[0], st[1], s_rec[j], s_bf[j], idx, m, cutoff, inv_f, gam, po,
-                                  ntest, COUNT);
-        } else {
-          float dm2[2] = {0.f, 0.f}, ux[2] = {0.f, 0.f}, uy[2] = {0.f, 0.f}, uz[2] = {0.f, 0.f};
-          float dak[2] = {0.f, 0.f}, e0[2] = {0.f, 0.f}, e1[2] = {0.f, 0.f}, e2[2] = {0.f, 0.f};
-          contrib = false;
-#pragma unroll
-          for (int q = 0; q < 2; ++q)
-            contrib |= bwd_pixel<FAM>(st[q], s_rec[j], s_bf[j], idx, cam, m, cutoff, near_plane,
-                                      inv_f, gam, dm2[q], ux[q], uy[q], uz[q], dak[q], e0[q],
-                                      e1[q], e2[q], ntest, COUNT);
-          po.dm2 = F2{dm2[0], dm2[1]};
-          po.ux = F2{ux[0], ux[1]};
-          po.uy = F2{uy[0], uy[1]};
-          po.uz = F2{uz[0], uz[1]};
-          po.dak = F2{dak[0], dak[1]};
-          po.e0 = F2{e0[0], e0[1]};
-          po.e1 = F2{e1[0], e1[1]};
-          po.e2 = F2{e2[0], e2[1]};
-        }
+        const bool contrib = entry_step<FAM, COUNT>(st, s_rec[j], s_bf[j], idx, cam, m, cutoff,
+                                                    near_plane, inv_f, gam, po, ntest);
         if (__any_sync(0xffffffffu, contrib)) {
-          // warp transpose-reduce through shared memory (moment-pair rows)
-          const PixelConst& pa = st[0].pc;
-          const PixelConst& pb = st[1].pc;
-          const F2 a = mul2(po.dm2, po.ux), b = mul2(po.dm2, po.uy), c = mul2(po.dm2, po.uz);
-          // moment pairs (2p, 2p+1) as one 8-byte store; rows 9 and 10 are unused
-          float v[NMOM];
-          v[0] = fmaf(a.x, po.ux.x, a.y * po.ux.y);
-          v[1] = fmaf(a.x, po.uy.x, a.y * po.uy.y);
-          v[2] = fmaf(a.x, po.uz.x, a.y * po.uz.y);
-          v[3] = fmaf(b.x, po.uy.x, b.y * po.uy.y);
-          v[4] = fmaf(b.x, po.uz.x, b.y * po.uz.y);
-          v[5] = fmaf(c.x, po.uz.x, c.y * po.uz.y);
-          v[6] = a.x + a.y;
-          v[7] = b.x + b.y;
-          v[8] = c.x + c.y;
-          v[9] = 0.f;
-          v[10] = 0.f;
-          v[11] = po.dak.x + po.dak.y;
-          v[12] = (po.e0.x + po.e0.y) * Y0;
-          v[13] = fmaf(po.e0.x, pa.Y1, po.e0.y * pb.Y1);
-          v[14] = fmaf(po.e0.x, pa.Y2, po.e0.y * pb.Y2);
-          v[15] = fmaf(po.e0.x, pa.Y3, po.e0.y * pb.Y3);
-          v[16] = (po.e1.x + po.e1.y) * Y0;
-          v[17] = fmaf(po.e1.x, pa.Y1, po.e1.y * pb.Y1);
-          v[18] = fmaf(po.e1.x, pa.Y2, po.e1.y * pb.Y2);
-          v[19] = fmaf(po.e1.x, pa.Y3, po.e1.y * pb.Y3);
-          v[20] = (po.e2.x + po.e2.y) * Y0;
-          v[21] = fmaf(po.e2.x, pa.Y1, po.e2.y * pb.Y1);
-          v[22] = fmaf(po.e2.x, pa.Y2, po.e2.y * pb.Y2);
-          v[23] = fmaf(po.e2.x, pa.Y3, po.e2.y * pb.Y3);
-          float2* col = reinterpret_cast<float2*>(red + (lane < 16 ? 2 * lane : RED_HALF + 2 * (lane - 16)));
-#pragma unroll
-          for (int q = 0; q < NMOM / 2; ++q) col[q * (RED_ROW / 2)] = make_float2(v[2 * q], v[2 * q + 1]);
-          __syncwarp();
-          // lane 2p sums moments (2p, 2p+1) over lanes 0-15, lane 2p+1 over
-          // lanes 16-31 (packed adds), then each keeps its own moment and
-          // takes the partner's half of it
-          F2 part = f2(0.f);
-          if (lane < NMOM) {
-            const float4* row =
-                reinterpret_cast<const float4*>(red + (lane >> 1) * RED_ROW + (lane & 1) * RED_HALF);
-            F2 t[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const float4 r = row[i];
-              t[i] = add2(F2{r.x, r.y}, F2{r.z, r.w});
-            }
-            part = add2(add2(add2(t[0], t[1]), add2(t[2], t[3])), add2(add2(t[4], t[5]), add2(t[6], t[7])));
-          }
-          const float other = __shfl_xor_sync(0xffffffffu, (lane & 1) ? part.x : part.y, 1);
-          const float sum = ((lane & 1) ? part.y : part.x) + other;
+          const float sum = warp_moments(po, st[0].pc, st[1].pc, red, lane, Y0);
           if (lane < NMOM && sum != 0.f) {
             if (DET)  // this warp's own row: one writer per (entry, moment)
               s_acc[((tid >> 5) * BWD_BATCH + j) * NMOM + lane] = sum;
