@@ -59,9 +59,9 @@ void launch_key_fixup(const uint32_t*, uint32_t*, const double*, int64_t, unsign
 void launch_rank_of(const uint32_t*, int64_t, uint32_t*, cudaStream_t);
 void launch_rank_of_range(const uint32_t*, int64_t, int64_t, uint32_t*, cudaStream_t,
                           const int* nd = nullptr);
-void launch_phase_select(const unsigned int*, const int64_t*, int, int64_t, long long*,
-                         cudaStream_t, int max_bin0 = -1, unsigned long long* overflow = nullptr,
-                         unsigned int* bin_pos = nullptr, int* n_sel = nullptr);
+void launch_key32_hist_select(const double*, int64_t, const unsigned long long*, uint32_t*,
+                              unsigned int*, const int64_t*, int, long long*, int,
+                              unsigned long long*, unsigned int*, int*, cudaStream_t);
 void launch_bin_scatter(const uint32_t*, int64_t, int, int, const long long*, unsigned int*,
                         uint32_t*, cudaStream_t);
 void launch_bin_sort(uint32_t*, const double*, const unsigned int*, const unsigned int*, int, int,
@@ -84,8 +84,6 @@ void launch_pack_check(const unsigned long long*, const long long*, int, unsigne
                        cudaStream_t);
 void launch_call_init(unsigned long long*, uint8_t*, int32_t*, int2*, unsigned int*, int,
                       long long*, const int64_t*, int, unsigned int*, cudaStream_t);
-void launch_key32_hist(const double*, int64_t, const unsigned long long*, uint32_t*,
-                       unsigned int*, cudaStream_t);
 void launch_dkeys(const double*, int64_t, unsigned long long*, cudaStream_t);
 void launch_count_tiles(const int4*, const uint32_t*, int64_t, int64_t, int, const uint8_t*,
                         const unsigned int*, unsigned int*, const double*, const CamDev&,
@@ -754,7 +752,7 @@ int forward_impl(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
   NXS_CUDA(ensure_n<float4>(v->records, P * REC_F4));
   NXS_CUDA(ensure_n<float4>(v->bframe, P * 3));
   NXS_CUDA(ensure_n<int4>(v->rects, P));
-  NXS_CUDA(ensure_n<double>(v->tq, P * 10));
+  NXS_CUDA(ensure_n<double>(v->tq, P * 12));  // per rank: tile test + rect (project.cu TQ_STRIDE)
   NXS_CUDA(ensure_n<unsigned long long>(v->ntiles, P));
   NXS_CUDA(ensure_n<unsigned long long>(v->offsets, P));
   NXS_CUDA(ensure_n<uint8_t>(v->active, n_tiles));
@@ -781,7 +779,7 @@ int forward_impl(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
   NXS_CUDA(ensure_n<uint32_t>(v->tile_cnt, n_tiles));
   NXS_CUDA(ensure_n<int32_t>(v->tile_last, n_tiles));
   NXS_CUDA(ensure_n<uint32_t>(v->bin_pos, 4096 * 32));  // (one cursor per 128-byte line)
-  NXS_CUDA(v->ph_hist.ensure(4096 * sizeof(unsigned int)));
+  NXS_CUDA(v->ph_hist.ensure(4097 * sizeof(unsigned int)));  // bins + ticket
   NXS_CUDA(v->ph_sel.ensure(96 * sizeof(long long)));
   if (P == 0) {  // (P > 0: k_call_init below, in the pipeline)
     NXS_CUDA(cudaMemsetAsync(dsmall, 0, 16 * sizeof(unsigned long long), s));
@@ -894,7 +892,7 @@ retry_sort:
                                    v->idx_in.as<uint32_t>(), v->ph_sel.as<int>(), (int)P,
                                    BinRange{nullptr, 0, 0}, s));
     NXS_CUDA(v->temp.ensure(std::max({t_full, t_scan, t_sel})));
-    NXS_CUDA(v->ph_hist.ensure(4096 * sizeof(unsigned int)));
+    NXS_CUDA(v->ph_hist.ensure(4097 * sizeof(unsigned int)));  // bins + ticket
     NXS_CUDA(v->ph_sel.ensure(96 * sizeof(long long)));
     NXS_CUDA(ensure_n<uint32_t>(v->pv_ph[0], capp));
     NXS_CUDA(ensure_n<int2>(v->ranges_ph[0], n_tiles));
@@ -987,18 +985,20 @@ retry_sort:
           v->idx_out.as<uint32_t>(), (int)P, 0, 64, s));
     } else if (v->lazy) {
       // phase boundaries on whole key bins: one host sync for their ranks
-      launch_key32_hist(v->depth.as<double>(), P, dsmall + 6, v->k32a.as<uint32_t>(),
-                        v->ph_hist.as<unsigned int>(), s);
-      NXS_LAUNCHED("key32_hist");
+      // keys, their histogram and (last block) the phase selection, one launch
       long long* dsel = v->ph_sel.as<long long>();  // [32..) phase targets (k_call_init)
       if (async0) {
         // phase 0 sized from the previous call; the last bin it may use is
-        // checked on the device (k_phase_select) and verified later
+        // checked on the device (phase selection) and verified later
         ph_bin[0] = std::min(4095, v->est_bin0 + (cam_moved ? 8 : 2));
-        launch_phase_select(v->ph_hist.as<unsigned int>(), reinterpret_cast<int64_t*>(dsel + 32),
-                            n_ph - 1, P, dsel, s, ph_bin[0], dsmall + 10,
-                            v->bin_pos.as<uint32_t>(), reinterpret_cast<int*>(dsel + 48));
-        NXS_LAUNCHED("phase_select");
+      }
+      launch_key32_hist_select(v->depth.as<double>(), P, dsmall + 6, v->k32a.as<uint32_t>(),
+                               v->ph_hist.as<unsigned int>(), reinterpret_cast<int64_t*>(dsel + 32),
+                               n_ph - 1, dsel, async0 ? ph_bin[0] : -1,
+                               async0 ? dsmall + 10 : nullptr, v->bin_pos.as<uint32_t>(),
+                               async0 ? reinterpret_cast<int*>(dsel + 48) : nullptr, s);
+      NXS_LAUNCHED("key32_hist_select");
+      if (async0) {
         v->async_cap0 = std::min<int64_t>(P, v->est_n0 + v->est_n0 / hdiv + 2048 * (8 / hdiv));
         v->async_capp =
             v->async_bases ? v->bases_bound : v->est_pairs + v->est_pairs / hdiv + 8192 * (8 / hdiv);
@@ -1007,10 +1007,7 @@ retry_sort:
       }
     }
     if (v->lazy && !async0) {
-      long long* dsel = v->ph_sel.as<long long>();
-      launch_phase_select(v->ph_hist.as<unsigned int>(), reinterpret_cast<int64_t*>(dsel + 32),
-                          n_ph - 1, P, dsel, s, -1, nullptr, v->bin_pos.as<uint32_t>());
-      NXS_LAUNCHED("phase_select");
+      long long* dsel = v->ph_sel.as<long long>();  // (selected by k_key32_hist_select)
       long long* hsel = reinterpret_cast<long long*>(v->host_small + 16);
       NXS_CUDA(cudaMemcpyAsync(hsel, dsel, sizeof(long long) * 2 * n_ph, cudaMemcpyDeviceToHost,
                                s));

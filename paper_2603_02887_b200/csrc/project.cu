@@ -197,6 +197,81 @@ __global__ void k_depth(const float* __restrict__ centers, const float* __restri
   }
 }
 
+// K0, the centre-depth case (global and chunked orders): four Gaussians per
+// thread from three 16-byte loads of their centres, so every thread has its
+// whole input in flight at once (the one-per-thread grid-stride form waited
+// out a DRAM round trip per element: 11.9 -> ? us at 1M).  Same values as
+// k_depth.
+__global__ void k_depth4(const float4* __restrict__ centers4, int64_t P, CamDev cam,
+                         double* __restrict__ depth, unsigned long long* __restrict__ key64,
+                         uint32_t* __restrict__ idx, unsigned long long* __restrict__ kminmax) {
+  nxs_pdl_enter();
+  __shared__ unsigned long long s_min[8], s_max[8];
+  unsigned long long kmin = ~0ull, kmax = 0ull;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i0 = 4 * t;
+  if (i0 < P) {
+    float c[12];
+    const float* cf = reinterpret_cast<const float*>(centers4);
+    if (i0 + 4 <= P) {
+      const float4 a = centers4[3 * t], b = centers4[3 * t + 1], e = centers4[3 * t + 2];
+      c[0] = a.x; c[1] = a.y; c[2] = a.z; c[3] = a.w;
+      c[4] = b.x; c[5] = b.y; c[6] = b.z; c[7] = b.w;
+      c[8] = e.x; c[9] = e.y; c[10] = e.z; c[11] = e.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 12; ++k) c[k] = i0 * 3 + k < 3 * P ? cf[i0 * 3 + k] : 0.f;
+    }
+    double d[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double b0 = (double)c[3 * q + 0] - cam.o[0];
+      const double b1 = (double)c[3 * q + 1] - cam.o[1];
+      const double b2 = (double)c[3 * q + 2] - cam.o[2];
+      d[q] = dot3_compensated(b0, b1, b2, cam.R[2], cam.R[5], cam.R[8]);
+    }
+    if (i0 + 4 <= P) {
+      double2* d2 = reinterpret_cast<double2*>(depth + i0);
+      d2[0] = make_double2(d[0], d[1]);
+      d2[1] = make_double2(d[2], d[3]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (i0 + q >= P) break;
+      if (i0 + 4 > P) depth[i0 + q] = d[q];
+      const unsigned long long k = dkey(d[q]);
+      if (key64) {
+        key64[i0 + q] = k;
+        idx[i0 + q] = (uint32_t)(i0 + q);
+      }
+      if (d[q] == d[q]) {
+        kmin = min(kmin, k);
+        kmax = max(kmax, k);
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+    kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    s_min[w] = kmin;
+    s_max[w] = kmax;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
+      kmin = min(kmin, s_min[k]);
+      kmax = max(kmax, s_max[k]);
+    }
+    if (kmin <= kmax) {
+      atomicMin(&kminmax[0], kmin);
+      atomicMax(&kminmax[1], kmax);
+    }
+  }
+}
+
 // 32-bit monotone key: floor((d - dmin) * (2^32 - 2) / (dmax - dmin)); NaN last.
 // d1 < d2 implies key(d1) <= key(d2); equal keys are re-ordered by k_key_fixup.
 __device__ __forceinline__ uint32_t key32_of(double d, double lo, double scale, bool spread) {
@@ -215,30 +290,6 @@ __global__ void k_key32(const double* __restrict__ depth, int64_t P,
   const bool spread = kminmax[0] < kminmax[1];
   const double lo = dkey_inv(kminmax[0]), hi = dkey_inv(kminmax[1]);
   key[i] = key32_of(depth[i], lo, 4294967294.0 / (hi - lo), spread);
-}
-// the same keys and, in one pass, their histogram over the top 12 bits
-// (the histogram of the lazy depth phases; hist is zeroed by k_call_init)
-constexpr int PH_BINS_ = 4096;
-__global__ void __launch_bounds__(1024)
-    k_key32_hist(const double* __restrict__ depth, int64_t P,
-                 const unsigned long long* __restrict__ kminmax, uint32_t* __restrict__ key,
-                 unsigned int* __restrict__ hist) {
-  nxs_pdl_enter();
-  __shared__ unsigned int sh[PH_BINS_];
-  for (int b = threadIdx.x; b < PH_BINS_; b += blockDim.x) sh[b] = 0u;
-  const bool spread = kminmax[0] < kminmax[1];
-  const double lo = dkey_inv(kminmax[0]), hi = dkey_inv(kminmax[1]);
-  const double scale = 4294967294.0 / (hi - lo);
-  __syncthreads();
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t k = key32_of(depth[i], lo, scale, spread);
-    key[i] = k;
-    atomicAdd(&sh[k >> 20], 1u);
-  }
-  __syncthreads();
-  for (int b = threadIdx.x; b < PH_BINS_; b += blockDim.x)
-    if (sh[b]) atomicAdd(&hist[b], sh[b]);
 }
 // 64-bit keys of the fallback sort from the depths (lazy phases skip them in K0)
 __global__ void k_dkeys(const double* __restrict__ depth, int64_t P,
@@ -309,23 +360,22 @@ constexpr int BIN_STRIDE = 32;  // bin cursors, one per 128-byte line
 // one block: inclusive scan of the histogram; for each target rank T_p the
 // first bin whose cumulative count reaches it.  out[2p] = last bin of phase
 // p, out[2p+1] = its end rank; the last phase ends at bin PH_BINS-1, rank P.
-__global__ void __launch_bounds__(1024) k_phase_select(const unsigned int* __restrict__ hist,
-                                                       const int64_t* __restrict__ targets,
-                                                       int n_targets, int64_t P,
-                                                       long long* __restrict__ out,
-                                                       int max_bin0,
-                                                       unsigned long long* __restrict__ overflow,
-                                                       unsigned int* __restrict__ bin_pos,
-                                                       int* __restrict__ n_sel) {
-  nxs_pdl_enter();
-  __shared__ unsigned long long cum[PH_BINS];
-  __shared__ unsigned long long wsum[32];
+// (run by the last block of k_key32_hist_select; `hist` is read through L2:
+// the other blocks wrote it)
+__device__ __forceinline__ void phase_select_body(const unsigned int* __restrict__ hist,
+                                                  const int64_t* __restrict__ targets,
+                                                  int n_targets, int64_t P,
+                                                  long long* __restrict__ out, int max_bin0,
+                                                  unsigned long long* __restrict__ overflow,
+                                                  unsigned int* __restrict__ bin_pos,
+                                                  int* __restrict__ n_sel,
+                                                  unsigned long long* cum, unsigned long long* wsum) {
   constexpr int PER = PH_BINS / 1024;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   unsigned long long loc[PER], run = 0;
 #pragma unroll
   for (int k = 0; k < PER; ++k) {
-    run += hist[t * PER + k];
+    run += __ldcg(hist + t * PER + k);
     loc[k] = run;
   }
   unsigned long long x = run;
@@ -351,7 +401,7 @@ __global__ void __launch_bounds__(1024) k_phase_select(const unsigned int* __res
     // each bin's first rank: the scatter's cursor (k_bin_scatter), one
     // counter per 128-byte line so the scatter's atomics spread over L2
     if (bin_pos)
-      bin_pos[(t * PER + k) * BIN_STRIDE] = (unsigned int)(base + loc[k] - hist[t * PER + k]);
+      bin_pos[(t * PER + k) * BIN_STRIDE] = (unsigned int)(base + loc[k] - __ldcg(hist + t * PER + k));
   }
   __syncthreads();
   if (t < n_targets) {
@@ -374,8 +424,49 @@ __global__ void __launch_bounds__(1024) k_phase_select(const unsigned int* __res
   }
 }
 
+// The 32-bit keys (key32_of), their histogram over the top 12 bits and the
+// phase selection in one launch: every block adds its shared
+// histogram into `hist`, takes a ticket (hist[PH_BINS], zeroed by
+// k_call_init) and the last block runs the phase selection — one kernel
+// boundary and one single-block launch fewer on the pipeline's critical path.
+__global__ void __launch_bounds__(1024)
+    k_key32_hist_select(const double* __restrict__ depth, int64_t P,
+                        const unsigned long long* __restrict__ kminmax, uint32_t* __restrict__ key,
+                        unsigned int* __restrict__ hist, const int64_t* __restrict__ targets,
+                        int n_targets, long long* __restrict__ out, int max_bin0,
+                        unsigned long long* __restrict__ overflow,
+                        unsigned int* __restrict__ bin_pos, int* __restrict__ n_sel) {
+  nxs_pdl_enter();
+  __shared__ unsigned long long smem[PH_BINS];  // histogram (u32 view), then the scan
+  __shared__ unsigned long long wsum[32];
+  __shared__ bool s_last;
+  unsigned int* sh = reinterpret_cast<unsigned int*>(smem);
+  for (int b = threadIdx.x; b < PH_BINS; b += blockDim.x) sh[b] = 0u;
+  const bool spread = kminmax[0] < kminmax[1];
+  const double lo = dkey_inv(kminmax[0]), hi = dkey_inv(kminmax[1]);
+  const double scale = 4294967294.0 / (hi - lo);
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = key32_of(depth[i], lo, scale, spread);
+    key[i] = k;
+    atomicAdd(&sh[k >> 20], 1u);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < PH_BINS; b += blockDim.x)
+    if (sh[b]) atomicAdd(&hist[b], sh[b]);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&hist[PH_BINS], 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  phase_select_body(hist, targets, n_targets, P, out, max_bin0, overflow, bin_pos, n_sel, smem,
+                    wsum);
+}
+
 // ---- one depth phase in exact order without a global sort: the phase's
-// key bins are contiguous rank ranges (k_phase_select's bin_pos), each
+// key bins are contiguous rank ranges (the phase selection's bin_pos), each
 // Gaussian is scattered into its bin (any order), then each bin is sorted
 // exactly by (depth, index) — NaN last — in shared memory, which is the
 // order the 32-bit sort + fix-up produces.  Ranks are written alongside.
@@ -585,8 +676,15 @@ struct ProjOut {
   float4* records;              // per rank 8 x float4
   float4* bframe;               // per rank 3 x float4: rows of B (backward only)
   unsigned long long* straddle; // counter
-  double* tq;                   // per Gaussian: silhouette conic + an inside point (8)
+  double* tq;                   // per RANK: silhouette conic + an inside point, tile rect (TQ_STRIDE)
 };
+// per-rank tile-test slot: 10 doubles (conic, centre, 1/(2 Q00), 1/(2 Q11)),
+// then the tile rectangle as an int4 — the binning reads rank r's rect and
+// test data from one slot, without the order[r] -> rects[g] gather
+constexpr int TQ_STRIDE = 12;
+__device__ __forceinline__ int4 tq_rect(const double* tq, int64_t r) {
+  return *reinterpret_cast<const int4*>(tq + TQ_STRIDE * r + 10);
+}
 
 // K1: per rank r (Gaussian g = order[r]).
 // Per-Gaussian projection (g = storage index, r = depth rank), parameters
@@ -597,7 +695,7 @@ struct GParams {
   float shv[12];
 };
 
-__device__ __forceinline__ void project_one(const GParams& prm, int64_t g, const CamDev& cam,
+__device__ __forceinline__ void project_one(const GParams& prm, int64_t g, int64_t rk, const CamDev& cam,
                                             double cutoff, double near_plane, const ProjOut& out,
                                             float4* rec, float4* bf) {
   const float cx0 = prm.c0, cx1 = prm.c1, cx2 = prm.c2;
@@ -734,7 +832,7 @@ __device__ __forceinline__ void project_one(const GParams& prm, int64_t g, const
       if (ok && out.tq) {
         // exact tile test data: the silhouette conic q(X, Y) = Hᵀ Q H and
         // the projected centre (inside it: q = -r2m·D there)
-        double* t = out.tq + 10 * g;
+        double* t = out.tq + TQ_STRIDE * rk;
         t[0] = Q[0];
         t[1] = Q[1];
         t[2] = Q[4];
@@ -746,14 +844,14 @@ __device__ __forceinline__ void project_one(const GParams& prm, int64_t g, const
         t[8] = 0.5 / Q[0];
         t[9] = 0.5 / Q[4];
       } else if (out.tq) {
-        out.tq[10 * g] = __longlong_as_double(0x7ff8000000000000ll);  // NaN: no exact test
+        out.tq[TQ_STRIDE * rk] = __longlong_as_double(0x7ff8000000000000ll);  // NaN: no exact test
       }
     }
   }
 
   if (general) {
     rect = make_int4(0, 0, cam.tiles_x - 1, cam.tiles_y - 1);
-    if (out.tq) out.tq[10 * g] = __longlong_as_double(0x7ff8000000000000ll);  // every tile
+    if (out.tq) out.tq[TQ_STRIDE * rk] = __longlong_as_double(0x7ff8000000000000ll);  // every tile
     // world-frame A = R diag(s^-2) R^T, b = μ - o (render.py:116-121)
     double A[9];
 #pragma unroll
@@ -806,7 +904,8 @@ __device__ __forceinline__ void project_one(const GParams& prm, int64_t g, const
       bf[k] = make_float4((float)(bp[2] * M[0 + k] * ik), (float)(bp[2] * M[3 + k] * ik),
                           (float)(bp[2] * M[6 + k] * ik), (float)sk[k]);
   }
-  out.rects[g] = rect;  // storage order (coalesced); the binning gathers by rank
+  out.rects[g] = rect;  // storage order (coalesced; exports, the exact order's binning)
+  if (out.tq) *reinterpret_cast<int4*>(out.tq + TQ_STRIDE * rk + 10) = rect;
 }
 
 // K1: persistent blocks of 128 threads stream chunks of 128 Gaussians'
@@ -920,7 +1019,7 @@ __global__ void __launch_bounds__(PROJ_CHUNK)
 #pragma unroll
           for (int k = 0; k < 4; ++k) prm.shv[4 * c + k] = (k < C) ? sh[(g * 3 + c) * C + k] : 0.0f;
       }
-      project_one(prm, g, cam, cutoff, near_plane, out, so.rec[tid], so.bf[tid]);
+      project_one(prm, g, r, cam, cutoff, near_plane, out, so.rec[tid], so.bf[tid]);
       so.rank[tid] = r;
       if (out.zlo_rank) out.zlo_rank[r] = __double2float_rd(out.zlo[g]);
     } else {
@@ -987,7 +1086,7 @@ __global__ void __launch_bounds__(PROJ_CHUNK)
         prm.shv[4 * c + 1] = prm.shv[4 * c + 2] = prm.shv[4 * c + 3] = 0.0f;
       }
     }
-    project_one(prm, g, cam, cutoff, near_plane, out, so.rec[tid], so.bf[tid]);
+    project_one(prm, g, r, cam, cutoff, near_plane, out, so.rec[tid], so.bf[tid]);
     if (out.zlo_rank) out.zlo_rank[r] = __double2float_rd(out.zlo[g]);
     so.rank[tid] = r;
   } else {
@@ -1016,10 +1115,10 @@ __global__ void __launch_bounds__(PROJ_CHUNK)
 // every valid pixel lies strictly inside the margin ellipse (r2m).  fp64,
 // IEEE op by op (this file is built with --fmad=false), restated in
 // oracle/binning_oracle.c.
-__device__ __forceinline__ bool tile_hit(const double* __restrict__ tq, int64_t g, int tx, int ty,
+__device__ __forceinline__ bool tile_hit(const double* __restrict__ tq, int64_t r, int tx, int ty,
                                          const CamDev& cam, double inv_f) {
   if (!tq) return true;  // culling off (exact order: full binning, bbox tiles)
-  const double* t = tq + 10 * g;
+  const double* t = tq + TQ_STRIDE * r;
   const double q00 = t[0];
   if (!(q00 == q00)) return true;  // no exact test for this Gaussian
   const double q01 = t[1], q11 = t[2], q02 = t[3], q12 = t[4], q22 = t[5];
@@ -1069,14 +1168,13 @@ __global__ void __launch_bounds__(256)
   const bool live = r < rn;
   unsigned n = 0;
   if (live) {
-    const int64_t g = order[r];
-    const int4 rc = rects[g];
+    const int4 rc = tq ? tq_rect(tq, r) : rects[order[r]];
     if (rc.x >= 0) {
       const double inv_f = cam.inv_f;  // = 1.0 / cam.f (host, IEEE)
       const int w = rc.z - rc.x + 1, nt = w * (rc.w - rc.y + 1);
       for (int k = sl; k < nt; k += KSUB) {
         const int tx = rc.x + k % w, ty = rc.y + k / w;
-        n += (active[ty * tiles_x + tx] && tile_hit(tq, g, tx, ty, cam, inv_f)) ? 1u : 0u;
+        n += (active[ty * tiles_x + tx] && tile_hit(tq, r, tx, ty, cam, inv_f)) ? 1u : 0u;
       }
     }
   }
@@ -1098,12 +1196,8 @@ __global__ void __launch_bounds__(256)
   if (nd) r1 = min(r1, r0 + (int64_t)*nd);
   const int lane = threadIdx.x & 31, sl = lane & (KSUB - 1), grp = lane / KSUB;
   const int64_t r = r0 + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / KSUB;
-  int64_t g = 0;
   int4 rc = make_int4(-1, -1, -1, -1);
-  if (r < r1) {
-    g = order[r];
-    rc = rects[g];
-  }
+  if (r < r1) rc = tq ? tq_rect(tq, r) : rects[order[r]];
   const int w = rc.z - rc.x + 1;
   const int nt = rc.x >= 0 ? w * (rc.w - rc.y + 1) : 0;
   int nmax = nt;  // the warp loops to its largest rect (ballots need every lane)
@@ -1114,7 +1208,7 @@ __global__ void __launch_bounds__(256)
     const int k = base + sl;
     const int tx = rc.x + (w > 0 ? k % w : 0), ty = rc.y + (w > 0 ? k / w : 0);
     const int t = ty * tiles_x + tx;
-    const bool hit = k < nt && active[t] && tile_hit(tq, g, tx, ty, cam, inv_f);
+    const bool hit = k < nt && active[t] && tile_hit(tq, r, tx, ty, cam, inv_f);
     const unsigned m = KSUB == 32 ? __ballot_sync(0xffffffffu, hit)
                                   : (__ballot_sync(0xffffffffu, hit) >> (grp * KSUB)) &
                                         ((1u << KSUB) - 1u);
@@ -1148,15 +1242,14 @@ __global__ void __launch_bounds__(256)
   const int64_t r = r0 + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / KSUB;
   const int64_t rn = nd ? min(r1, r0 + (int64_t)*nd) : r1;
   if (r >= rn) return;
-  const int64_t g = order[r];
-  const int4 rc = rects[g];
+  const int4 rc = tq ? tq_rect(tq, r) : rects[order[r]];
   if (rc.x < 0) return;
   const double inv_f = cam.inv_f;  // = 1.0 / cam.f (host, IEEE)
   const int w = rc.z - rc.x + 1, nt = w * (rc.w - rc.y + 1);
   for (int k = sl; k < nt; k += KSUB) {
     const int tx = rc.x + k % w, ty = rc.y + k / w;
     const int t = ty * tiles_x + tx;
-    if (active[t] && tile_hit(tq, g, tx, ty, cam, inv_f)) atomicAdd(&tile_cnt[t], 1u);
+    if (active[t] && tile_hit(tq, r, tx, ty, cam, inv_f)) atomicAdd(&tile_cnt[t], 1u);
   }
 }
 
@@ -1263,15 +1356,14 @@ __global__ void __launch_bounds__(256)
   const int64_t r = r0 + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / KSUB;
   const int64_t rn = nd ? min(r1, r0 + (int64_t)*nd) : r1;
   if (r >= rn) return;
-  const int64_t g = order[r];
-  const int4 rc = rects[g];
+  const int4 rc = tq ? tq_rect(tq, r) : rects[order[r]];
   if (rc.x < 0) return;
   const double inv_f = cam.inv_f;  // = 1.0 / cam.f (host, IEEE)
   const int w = rc.z - rc.x + 1, nt = w * (rc.w - rc.y + 1);
   for (int k = sl; k < nt; k += KSUB) {
     const int tx = rc.x + k % w, ty = rc.y + k / w;
     const int t = ty * tiles_x + tx;
-    if (active[t] && tile_hit(tq, g, tx, ty, cam, inv_f)) {
+    if (active[t] && tile_hit(tq, r, tx, ty, cam, inv_f)) {
       if (base) {  // per-tile capacities from the view's last call (no count pass)
         const unsigned int q = atomicAdd(&cursor[t], 1u);
         if (q < base[t + 1] - base[t]) vals[base[t] + q] = (uint32_t)r;
@@ -1549,6 +1641,12 @@ void launch_depth(const float* centers, const float* scales, const float* quats,
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (!zmode && (reinterpret_cast<uintptr_t>(centers) & 15) == 0) {
+    const int64_t nt = (P + 3) / 4;
+    nxs_launch(k_depth4, (unsigned)((nt + 255) / 256), 256, 0, s,
+               reinterpret_cast<const float4*>(centers), P, cam, depth, key64, idx, kminmax);
+    return;
+  }
   const unsigned grid = (unsigned)std::min<int64_t>((P + 255) / 256, (int64_t)sms * 8);
   nxs_launch(k_depth, grid, 256, 0, s, centers, scales, quats, opacities, P, cam, cutoff, zmode, depth,
                                key64, idx, kminmax);
@@ -1557,15 +1655,6 @@ void launch_key32(const double* depth, int64_t P, const unsigned long long* kmin
                   uint32_t* key, cudaStream_t s) {
   if (P == 0) return;
   nxs_launch(k_key32, (unsigned)((P + 255) / 256), 256, 0, s, depth, P, kminmax, key);
-}
-void launch_key32_hist(const double* depth, int64_t P, const unsigned long long* kminmax,
-                       uint32_t* key, unsigned int* hist, cudaStream_t s) {
-  if (P == 0) return;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const unsigned grid = (unsigned)std::min<int64_t>((P + 1023) / 1024, (int64_t)sms * 2);
-  nxs_launch(k_key32_hist, grid, 1024, 0, s, depth, P, kminmax, key, hist);
 }
 void launch_dkeys(const double* depth, int64_t P, unsigned long long* key64, cudaStream_t s) {
   if (P == 0) return;
@@ -1658,7 +1747,7 @@ __global__ void k_call_init(unsigned long long* __restrict__ dsmall, uint8_t* __
                             unsigned int* __restrict__ hist) {
   nxs_pdl_enter();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (hist && i < 4096) hist[i] = 0u;
+  if (hist && i <= 4096) hist[i] = 0u;  // (bins and the k_key32_hist_select ticket)
   if (i < 16) dsmall[i] = (i == 6) ? ~0ull : 0ull;
   if (dtgt && i < n_tgt) dtgt[i] = tgt.v[i];
   if (i < n_tiles) {
@@ -1673,7 +1762,7 @@ void launch_call_init(unsigned long long* dsmall, uint8_t* active, int32_t* cum0
                       int n_tgt, unsigned int* hist, cudaStream_t s) {
   PhaseTargets t{};
   for (int i = 0; i < n_tgt && i < 4; ++i) t.v[i] = tgt[i];
-  const int n = std::max(n_tiles, 4096);
+  const int n = std::max(n_tiles, 4097);
   nxs_launch(k_call_init, (n + 255) / 256, 256, 0, s, dsmall, active, cum0, ranges0, tile_cnt, n_tiles, dtgt, t,
                                               std::min(n_tgt, 4), hist);
 }
@@ -1744,11 +1833,18 @@ void launch_clear_rects(const uint32_t* order, int64_t r0, int64_t r1, int4* rec
   if (r1 <= r0) return;
   nxs_launch(k_clear_rects, (unsigned)((r1 - r0 + 255) / 256), 256, 0, s, order, r0, r1, rects);
 }
-void launch_phase_select(const unsigned int* hist, const int64_t* targets, int n_targets,
-                         int64_t P, long long* out, cudaStream_t s, int max_bin0,
-                         unsigned long long* overflow, unsigned int* bin_pos, int* n_sel) {
-  nxs_launch(k_phase_select, 1, 1024, 0, s, hist, targets, n_targets, P, out, max_bin0, overflow,
-                                    bin_pos, n_sel);
+void launch_key32_hist_select(const double* depth, int64_t P, const unsigned long long* kminmax,
+                              uint32_t* key, unsigned int* hist, const int64_t* targets,
+                              int n_targets, long long* out, int max_bin0,
+                              unsigned long long* overflow, unsigned int* bin_pos, int* n_sel,
+                              cudaStream_t s) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned grid =
+      (unsigned)std::max<int64_t>(1, std::min<int64_t>((P + 1023) / 1024, (int64_t)sms * 2));
+  nxs_launch(k_key32_hist_select, grid, 1024, 0, s, depth, P, kminmax, key, hist, targets,
+             n_targets, out, max_bin0, overflow, bin_pos, n_sel);
 }
 void launch_bin_scatter(const uint32_t* key, int64_t P, int lo, int hi, const long long* hi_dev,
                         unsigned int* bin_pos, uint32_t* order, cudaStream_t s) {
