@@ -446,11 +446,29 @@ __global__ void __launch_bounds__(1024)
   const double lo = dkey_inv(kminmax[0]), hi = dkey_inv(kminmax[1]);
   const double scale = 4294967294.0 / (hi - lo);
   __syncthreads();
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t k = key32_of(depth[i], lo, scale, spread);
-    key[i] = k;
-    atomicAdd(&sh[k >> 20], 1u);
+  // four Gaussians per thread: two 16-B depth loads in flight, one 16-B key store
+  for (int64_t i0 = 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x); i0 < P;
+       i0 += 4 * (int64_t)gridDim.x * blockDim.x) {
+    if (i0 + 4 <= P) {
+      const double2 a = reinterpret_cast<const double2*>(depth + i0)[0];
+      const double2 b = reinterpret_cast<const double2*>(depth + i0)[1];
+      uint4 k;
+      k.x = key32_of(a.x, lo, scale, spread);
+      k.y = key32_of(a.y, lo, scale, spread);
+      k.z = key32_of(b.x, lo, scale, spread);
+      k.w = key32_of(b.y, lo, scale, spread);
+      *reinterpret_cast<uint4*>(key + i0) = k;
+      atomicAdd(&sh[k.x >> 20], 1u);
+      atomicAdd(&sh[k.y >> 20], 1u);
+      atomicAdd(&sh[k.z >> 20], 1u);
+      atomicAdd(&sh[k.w >> 20], 1u);
+    } else {
+      for (int64_t i = i0; i < P; ++i) {
+        const uint32_t k = key32_of(depth[i], lo, scale, spread);
+        key[i] = k;
+        atomicAdd(&sh[k >> 20], 1u);
+      }
+    }
   }
   __syncthreads();
   for (int b = threadIdx.x; b < PH_BINS; b += blockDim.x)
@@ -475,10 +493,23 @@ __global__ void k_bin_scatter(const uint32_t* __restrict__ key, int64_t P, int l
                               unsigned int* __restrict__ bin_pos, uint32_t* __restrict__ order) {
   nxs_pdl_enter();
   if (hi_dev) hi = (int)hi_dev[0];
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int b = (int)(key[i] >> 20);
-    if (b >= lo && b <= hi) order[atomicAdd(&bin_pos[b * BIN_STRIDE], 1u)] = (uint32_t)i;
+  // four keys per thread from one 16-B load (key is 16-B aligned)
+  for (int64_t i0 = 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x); i0 < P;
+       i0 += 4 * (int64_t)gridDim.x * blockDim.x) {
+    uint32_t k[4];
+    if (i0 + 4 <= P) {
+      const uint4 v = *reinterpret_cast<const uint4*>(key + i0);
+      k[0] = v.x; k[1] = v.y; k[2] = v.z; k[3] = v.w;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) k[q] = i0 + q < P ? key[i0 + q] : 0xffffffffu;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int b = (int)(k[q] >> 20);
+      if (i0 + q < P && b >= lo && b <= hi)
+        order[atomicAdd(&bin_pos[b * BIN_STRIDE], 1u)] = (uint32_t)(i0 + q);
+    }
   }
 }
 
@@ -1842,7 +1873,7 @@ void launch_key32_hist_select(const double* depth, int64_t P, const unsigned lon
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const unsigned grid =
-      (unsigned)std::max<int64_t>(1, std::min<int64_t>((P + 1023) / 1024, (int64_t)sms * 2));
+      (unsigned)std::max<int64_t>(1, std::min<int64_t>((P + 4095) / 4096, (int64_t)sms * 2));
   nxs_launch(k_key32_hist_select, grid, 1024, 0, s, depth, P, kminmax, key, hist, targets,
              n_targets, out, max_bin0, overflow, bin_pos, n_sel);
 }
@@ -1852,7 +1883,7 @@ void launch_bin_scatter(const uint32_t* key, int64_t P, int lo, int hi, const lo
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const unsigned grid = (unsigned)std::min<int64_t>((P + 255) / 256, (int64_t)sms * 8);
+  const unsigned grid = (unsigned)std::min<int64_t>((P + 1023) / 1024, (int64_t)sms * 8);
   nxs_launch(k_bin_scatter, grid, 256, 0, s, key, P, lo, hi, hi_dev, bin_pos, order);
 }
 void launch_bin_sort(uint32_t* order, const double* depth, const unsigned int* hist,
