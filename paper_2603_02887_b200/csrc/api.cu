@@ -270,6 +270,10 @@ struct nxs_view {
   int64_t est_n0 = 0, est_pairs = 0;
   int est_bin0 = -1;
   bool async_pending = false;  // phase 0 ran device-sized, not yet verified
+  // fused call, t-ordered modes: the forward's pending-buffer overflow count
+  // (host_small[28]) is read behind the backward instead of before it
+  bool defer_ovf = false, ovf_pending = false;
+  cudaEvent_t ev_ovf = nullptr;
   cudaGraphExec_t gexec = nullptr;  // the device-sized phase 0, replayed as one graph
   cudaStream_t cap_stream = nullptr;  // capture happens on this (non-default) stream
   // small device->host reads that must not sit between two pipeline kernels
@@ -321,6 +325,7 @@ struct nxs_view {
     if (cap_stream) cudaStreamDestroy(cap_stream);
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (ev_hint) cudaEventDestroy(ev_hint);
+    if (ev_ovf) cudaEventDestroy(ev_ovf);
     if (ev_bases) cudaEventDestroy(ev_bases);
     if (ev_side) cudaEventDestroy(ev_side);
     if (ev_ok) {
@@ -1545,7 +1550,18 @@ retry_sort:
   v->ev_fwd = true;
   v->ev_bwd = false;
   v->stats.n_pairs = total_pairs;
-  if (torder) {
+  v->ovf_pending = false;
+  if (torder && v->defer_ovf) {
+    // (nxs_forward_backward enqueues the backward first and checks this
+    // behind it: finish_ovf_check)
+    cudaStream_t cs;
+    NXS_CUDA(side_after(v, s, cs));
+    NXS_CUDA(cudaMemcpyAsync(v->host_small + 28, dsmall + 9, sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, cs));
+    if (!v->ev_ovf) NXS_CUDA(cudaEventCreateWithFlags(&v->ev_ovf, cudaEventDisableTiming));
+    NXS_CUDA(cudaEventRecord(v->ev_ovf, cs));
+    v->ovf_pending = true;
+  } else if (torder) {
     // pending-buffer overflow means the exact order was not guaranteed: report
     NXS_CUDA(cudaMemcpyAsync(v->host_small + 7, dsmall + 9, sizeof(unsigned long long),
                              cudaMemcpyDeviceToHost, s));
@@ -1734,10 +1750,13 @@ int nxs_forward_backward(nxs_view* v, const nxs_scene* scene, const nxs_camera* 
   cudaStream_t s = (cudaStream_t)stream_;
   g_ht.mark("start");
   // speculate that this view needs as many depth phases as its last call
+  // and, in the t-ordered modes, that no pending buffer overflowed
   const int spec = (v->ev_sync && v->phases_needed > 0) ? v->phases_needed : 0;
-  if ((rc = forward_impl(v, scene, camera, model, opts, background, rgb, overdraw, residual,
-                         stream_, spec)))
-    return rc;
+  v->defer_ovf = true;
+  rc = forward_impl(v, scene, camera, model, opts, background, rgb, overdraw, residual, stream_,
+                    spec);
+  v->defer_ovf = false;
+  if (rc) return rc;
   if (v->P == 0) return NXS_OK;
   const bool spec_check = v->spec_pending;
   const bool async_check = v->async_pending;
@@ -1760,6 +1779,26 @@ int nxs_forward_backward(nxs_view* v, const nxs_scene* scene, const nxs_camera* 
   g_ht.mark("check_enq");
   if ((rc = backward_blend(v, seed, s))) return rc;
   g_ht.mark("bwd_enq");
+  if (v->ovf_pending) {
+    v->ovf_pending = false;
+    NXS_CUDA(cudaEventSynchronize(v->ev_ovf));
+    v->stats.n_overflow = (int64_t)v->host_small[28];
+    if (v->host_small[28] > 0) {
+      // the order was not guaranteed: drop the moments; the chunked order
+      // reruns with the large buffer, the exact order reports (as nxs_forward)
+      ++v->stats.n_redo;
+      if ((rc = backward_chain(v, scene, nullptr, nullptr, nullptr, nullptr, nullptr, s)))
+        return rc;
+      if (spec_check && !async_check) NXS_CUDA(cudaEventSynchronize(v->ev_sync));  // (its copy lands first)
+      v->spec_pending = v->async_pending = false;
+      v->phases_needed = 0;
+      if ((rc = nxs_forward(v, scene, camera, model, opts, background, rgb, overdraw, residual,
+                            stream_)))
+        return rc;
+      if ((rc = backward_blend(v, seed, s))) return rc;
+      return backward_chain(v, scene, g_centers, g_scales, g_quats, g_opacities, g_sh, s);
+    }
+  }
   if (spec_check) {
     bool ok = true;
     if (async_check) {

@@ -500,6 +500,36 @@ def test_exact_order_pending_overflow_is_reported():
     arrs = nx.SceneArrays(sc.centers, sc.scales, sc.quats, sc.opacities, sc.sh)
     with pytest.raises(RuntimeError):
         nx.render(arrs, cam, MODELS["exponential"], np.zeros(3))
+    # the fused forward + backward reads the overflow count behind the
+    # backward (speculating none): it must still report, on a fresh and a warm view
+    seed = np.ones((16, 16, 3))
+    for _ in range(2):
+        with pytest.raises(RuntimeError, match="overflow"):
+            nx.render_with_gradients(arrs, cam, MODELS["exponential"], np.zeros(3), seed)
+
+
+def test_fused_chunked_rerun_with_large_pending_buffer():
+    """Chunked order, 24 entries pending at once in one chunk: the 16-entry
+    buffer overflows and the pass reruns with 32.  The fused call (overflow
+    read behind its speculative backward) must give the unfused results."""
+    import paper_2603_02887_b200 as nx
+    k = 24
+    cen = np.column_stack([np.zeros(k), np.zeros(k), np.linspace(12.0, 13.0, k)])
+    sc = O.Scene(cen, np.tile([0.3, 0.3, 3.0], (k, 1)), np.tile([1.0, 0, 0, 0], (k, 1)),
+                 np.full(k, 0.05), np.ones((k, 3, 1)))
+    cam = O.look_at([0, 0, 0], [0, 0, 1], [0, 1, 0], 40.0, 16, 16)
+    arrs = nx.SceneArrays(sc.centers, sc.scales, sc.quats, sc.opacities, sc.sh)
+    rng = np.random.default_rng(3)
+    seed = rng.uniform(0.2, 1.0, (16, 16, 3))
+    m = MODELS["exponential"]
+    res, cache = nx.render_forward_cached(arrs, cam, m, np.zeros(3), chunk_size=64)
+    ref = nx.render_backward(arrs, cam, m, np.zeros(3), cache, seed, chunk_size=64)
+    for _ in range(2):  # fresh view, then warm
+        r2, g2 = nx.render_with_gradients(arrs, cam, m, np.zeros(3), seed, chunk_size=64)
+        np.testing.assert_array_equal(r2.rgb, res.rgb)
+        np.testing.assert_array_equal(r2.overdraw, res.overdraw)
+        for key in ref:
+            np.testing.assert_allclose(g2[key], ref[key], rtol=1e-6, atol=1e-9)
 
 
 # ---------------------------------------------------------------------------
