@@ -23,11 +23,6 @@
 namespace nxs {
 
 constexpr int FWD_BATCH = 64;  // list entries per staged batch
-#ifdef NXS_FWD_PIPE
-constexpr bool FWD_PIPE = true;  // test entry j+1 ahead of compositing j
-#else
-constexpr bool FWD_PIPE = false;
-#endif
 #ifndef NXS_FWD_MINB
 #define NXS_FWD_MINB 3
 #endif
@@ -112,9 +107,80 @@ __global__ void __launch_bounds__(TILE_PIX, NXS_FWD_MINB)
     }
     cp_async_commit();
   };
+  int dpos = -1;  // list position of the entry that finished this pixel
+  // One list entry (record rj at list position lpos): the ray-peak test and,
+  // on a hit, the composite.  Returns true when the pixel is finished.
+  auto entry = [&](const float4* rj, int lpos, auto gen_tag) -> bool {
+    constexpr bool GEN = decltype(gen_tag)::value;
+    if (COUNT) ++ntest;
+    TestOut tn;
+    bool ok;
+    if (GEN && (__float_as_int(rj[3].w) & RF_GENERAL)) {  // (uniform over the block)
+      float gx, gy, gz, tpk;
+      ok = general_test(rj, cam, px, py, cutoff, near_plane, tn, gx, gy, gz, tpk);
+    } else {
+      ok = ray_peak_test(rj[0], rj[1], rj[2], rj[3], pc, cutoff, tn);
+    }
+    if (!ok) return false;
+    float E0, E1, E2;
+    emission(rj[4], rj[5], rj[6], pc, E0, E1, E2);
+    const float alpha = tn.alpha;
+    const int idx = vbase + lpos;
+    float fp;
+    const float g = weight_g<FAM>(m, thi, tlo, P, fp);
+    const float wr = alpha * g;
+    const bool satnow = (FAM == FAM_EXP) ? false : (wr >= Trem);
+    const int cb = count;
+    ++count;
+    last = idx;
+    if (satnow) {
+      rad0 = fmaf(Trem, E0, rad0);
+      rad1 = fmaf(Trem, E1, rad1);
+      rad2 = fmaf(Trem, E2, rad2);
+      ek0 = E0;
+      ek1 = E1;
+      ek2 = E2;
+      tk = Trem;
+      sat = true;
+      done = true;
+      dpos = lpos;
+      return true;
+    }
+    rad0 = fmaf(wr, E0, rad0);
+    rad1 = fmaf(wr, E1, rad1);
+    rad2 = fmaf(wr, E2, rad2);
+    if (THETA && cb >= 1) {
+      sea0 = fmaf(alpha, E0, sea0);
+      sea1 = fmaf(alpha, E1, sea1);
+      sea2 = fmaf(alpha, E2, sea2);
+      sa += alpha;
+    }
+    if constexpr (FAM != FAM_EXP) df_add(thi, tlo, alpha);
+    if constexpr (IsPFam<FAM>::value) {
+      const float Pn = __fmul_rn(P, __fsub_rn(1.0f, alpha));
+      if (Pn < P_FLOOR && ck < 0) {
+        ck = idx;
+        Pck = P;
+      }
+      P = Pn;
+    }
+    if constexpr (FAM == FAM_EXP) {
+      Trem = P;
+    } else if constexpr (FAM == FAM_BLEND) {
+      Trem = fmaf(1.0f - m.c, __fsub_rn(__fsub_rn(1.0f, thi), tlo), m.c * P);
+    } else {
+      Trem = __fsub_rn(Trem, wr);
+    }
+    if (count >= max_splats) {
+      done = true;
+      dpos = lpos;
+      return true;
+    }
+    return false;
+  };
+  {
   if (rg.x < rg.y) stage(0, rg.x);
   int buf = 0;
-  int dpos = -1;  // list position of the entry that finished this pixel
   for (int base = rg.x; base < rg.y; base += FWD_BATCH, buf ^= 1) {
     const int n = min(FWD_BATCH, rg.y - base);
     if (base + FWD_BATCH < rg.y) {
@@ -128,93 +194,18 @@ __global__ void __launch_bounds__(TILE_PIX, NXS_FWD_MINB)
     const bool gen_batch =
         __syncthreads_or(tid < n && (__float_as_int(s_rec[buf][tid][3].w) & RF_GENERAL));
     float4(*s_cur)[REC_F4] = s_rec[buf];
-    // One entry: the ray-peak test and emission (independent of the carry)
-    // of entry j+1 are computed before entry j is composited, so the two
-    // dependency chains interleave.
-    auto walk = [&](auto gen_tag) {
-      constexpr bool GEN = decltype(gen_tag)::value;
-      auto test = [&](int j, TestOut& t, float& E0, float& E1, float& E2) -> bool {
-        bool ok;
-        if (GEN && (__float_as_int(s_cur[j][3].w) & RF_GENERAL)) {  // block-uniform branch
-          float gx, gy, gz, tpk;
-          ok = general_test(s_cur[j], cam, px, py, cutoff, near_plane, t, gx, gy, gz, tpk);
-        } else {
-          ok = ray_peak_test(s_cur[j][0], s_cur[j][1], s_cur[j][2], s_cur[j][3], pc, cutoff, t);
-        }
-        if (ok) emission(s_cur[j][4], s_cur[j][5], s_cur[j][6], pc, E0, E1, E2);
-        return ok;
-      };
-      TestOut tn;
-      float En0 = 0.f, En1 = 0.f, En2 = 0.f;
-      bool okn = FWD_PIPE ? test(0, tn, En0, En1, En2) : false;
-      for (int j = 0; j < n; ++j) {
-        if (COUNT) ++ntest;
-        if (!FWD_PIPE) okn = test(j, tn, En0, En1, En2);
-        const bool ok = okn;
-        const float alpha = tn.alpha, E0 = En0, E1 = En1, E2 = En2;
-        if (FWD_PIPE && j + 1 < n) okn = test(j + 1, tn, En0, En1, En2);
-        if (!ok) continue;
-        const int idx = vbase + base + j;
-        float fp;
-        const float g = weight_g<FAM>(m, thi, tlo, P, fp);
-        const float wr = alpha * g;
-        const bool satnow = (FAM == FAM_EXP) ? false : (wr >= Trem);
-        const int cb = count;
-        ++count;
-        last = idx;
-        if (satnow) {
-          rad0 = fmaf(Trem, E0, rad0);
-          rad1 = fmaf(Trem, E1, rad1);
-          rad2 = fmaf(Trem, E2, rad2);
-          ek0 = E0;
-          ek1 = E1;
-          ek2 = E2;
-          tk = Trem;
-          sat = true;
-          done = true;
-          dpos = base + j;
-          break;
-        }
-        rad0 = fmaf(wr, E0, rad0);
-        rad1 = fmaf(wr, E1, rad1);
-        rad2 = fmaf(wr, E2, rad2);
-        if (THETA && cb >= 1) {
-          sea0 = fmaf(alpha, E0, sea0);
-          sea1 = fmaf(alpha, E1, sea1);
-          sea2 = fmaf(alpha, E2, sea2);
-          sa += alpha;
-        }
-        if constexpr (FAM != FAM_EXP) df_add(thi, tlo, alpha);
-        if constexpr (IsPFam<FAM>::value) {
-          const float Pn = __fmul_rn(P, __fsub_rn(1.0f, alpha));
-          if (Pn < P_FLOOR && ck < 0) {
-            ck = idx;
-            Pck = P;
-          }
-          P = Pn;
-        }
-        if constexpr (FAM == FAM_EXP) {
-          Trem = P;
-        } else if constexpr (FAM == FAM_BLEND) {
-          Trem = fmaf(1.0f - m.c, __fsub_rn(__fsub_rn(1.0f, thi), tlo), m.c * P);
-        } else {
-          Trem = __fsub_rn(Trem, wr);
-        }
-        if (count >= max_splats) {
-          done = true;
-          dpos = base + j;
-          break;
-        }
-      }
-    };
     if (!done) {
-      if (gen_batch)
-        walk(std::true_type{});
-      else
-        walk(std::false_type{});
+      if (gen_batch) {
+        for (int j = 0; j < n; ++j)
+          if (entry(s_cur[j], base + j, std::true_type{})) break;
+      } else {
+        for (int j = 0; j < n; ++j)
+          if (entry(s_cur[j], base + j, std::false_type{})) break;
+      }
     }
     // all threads are past buffer `buf` before the next iteration refills it
     if (__syncthreads_count(!done) == 0) break;
+  }
   }
   cp_async_wait<0>();
   __shared__ int s_dpos, s_last;

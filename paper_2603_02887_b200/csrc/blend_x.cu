@@ -277,102 +277,175 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
   };
 
   const int2 rg = ranges[tile];
-  for (int base = rg.x; base < rg.y; base += XBT) {
-    const int n = min(XBT, rg.y - base);
-    NXS_CHECK(n > 0 && n <= XBT);
-    __syncthreads();
-    if (tid < n) {
-      const uint32_t rk = pairs[base + tid];
-      s_rank[tid] = rk;
-      s_ring_rank[(base + tid) % (2 * XBT)] = rk;
-      s_zlo[tid] = zlo_rank[rk];
-      if (CH) s_chunk[tid] = rank_c[order[rk]] / (uint32_t)chunk;
-    }
-    __syncthreads();
-    // stage this batch into the ring slot it maps to (positions are consecutive)
-    for (int k = tid; k < n * REC_F4; k += TILE_PIX) {
-      const int e = k >> 3, part = k & 7;
-      s_ring[(base + e) % (2 * XBT)][part] = records[(size_t)s_rank[e] * REC_F4 + part];
-    }
-    ring_lo = max(rg.x, base - XBT);
-    __syncthreads();
-    if (!s.done) {
-      for (int j = 0; j < n; ++j) {
-        const float4* s_rec_j = s_ring[(base + j) % (2 * XBT)];
-        // every remaining entry has t >= bound: pending entries below it are
-        // final; a new chunk makes every pending entry final
-        const bool next_chunk = CH && s_chunk[j] != cur_chunk;  // (exact order: one chunk)
-        const float bound = s_zlo[j] * hnorm;
+  if constexpr (!CH && FAM == FAM_EXP) {
+  // exact order, exponential family (never saturates: every pixel walks
+  // ~128 composites deep, at its own pace): every warp walks the tile list
+  // on its own, reading each entry's rank, z_lo and record through L1 (the
+  // block's 8 warps share the lines) — no staged batches, so no block
+  // barrier between entries (fwd 10.56 -> 7.03 ms at C3; the saturating
+  // models, whose walks are short, keep the shared staged batches: linear /
+  // softplus / blended lose 12-14 % unstaged)
+  ring_lo = 0x7fffffff;  // (commits re-read their records the same way)
+  if (!s.done) {
+    uint32_t rk_next = rg.x < rg.y ? __ldg(pairs + rg.x) : 0u;
+    for (int pos = rg.x; pos < rg.y; ++pos) {
+      const uint32_t rk = rk_next;
+      if (pos + 1 < rg.y) rk_next = __ldg(pairs + pos + 1);
+      const float4* rec = records + (size_t)rk * REC_F4;
+      const float bound = __ldg(zlo_rank + rk) * hnorm;
 #if NXS_X_DEFER > 0
-        // Committable entries stay committable (every later entry's t is above
-        // this bound), so the exact order may defer them until enough lanes of
-        // the warp have one: the composite then runs with most lanes active.
-        // (a new chunk commits everything pending at once: never deferred)
-        bool go_commit = next_chunk;
-        if (!go_commit) {
-          const unsigned am = __activemask();
-          const unsigned want = __ballot_sync(am, nb > 0 && thead < bound);
-          go_commit = __popc(want) * 32 >= NXS_X_DEFER * __popc(am) || nb >= XBUF - 4;
-        }
-        while (go_commit && nb > 0 && (next_chunk || thead < bound)) {
+      bool go_commit;
+      {
+        const unsigned am = __activemask();
+        const unsigned want = __ballot_sync(am, nb > 0 && thead < bound);
+        go_commit = __popc(want) * 32 >= NXS_X_DEFER * __popc(am) || nb >= XBUF - 4;
+      }
+      while (go_commit && nb > 0 && thead < bound) {
 #else
-        while (nb > 0 && (next_chunk || thead < bound)) {
+      while (nb > 0 && thead < bound) {
 #endif
-          commit_front();
-          if (s.done) break;
-        }
+        commit_front();
+        if (s.done) break;
+      }
+      if (s.done) {
+        dpos = pos;
+        break;
+      }
+      if (COUNT) ++ntest;
+      TestOut t;
+      float tpk;
+      if (!test_with_t(rec, cam, px, py, pc, hnorm, cutoff, near_plane, t, tpk)) continue;
+      if (nb == XBUF) {
+        atomicAdd(overflow, 1ull);
+        commit_front();
         if (s.done) {
-          dpos = base + j;
+          dpos = pos;
           break;
         }
-        if (CH) cur_chunk = s_chunk[j];
-        if (COUNT) ++ntest;
-        TestOut t;
-        float tpk;
-        if (!test_with_t(s_rec_j, cam, px, py, pc, hnorm, cutoff, near_plane, t, tpk)) continue;
-        if (nb == XBUF) {
-          // overflow: the order is no longer guaranteed for this pixel
-          atomicAdd(overflow, 1ull);
-          commit_front();
+      }
+      int i = nb;
+      uint32_t gid_new = 0xffffffffu;
+      while (i > 0) {
+        const int e = (head + i - 1) & (XBUF - 1);
+        const float2 qe = myq[e * TILE_PIX];
+        bool later = qe.x > tpk;
+        if (qe.x == tpk) {
+          if (gid_new == 0xffffffffu) gid_new = tie_key(rk);
+          const int pe = __float_as_int(qe.y);
+          later = tie_key(pe < 0 ? (uint32_t)(-1 - pe) : pairs[pe]) > gid_new;
+        }
+        if (!later) break;
+        const int f = (head + i) & (XBUF - 1);
+        myq[f * TILE_PIX] = qe;
+        if constexpr (keeps_alpha(XBUF)) mya[f * TILE_PIX] = mya[e * TILE_PIX];
+        --i;
+      }
+      const int f = (head + i) & (XBUF - 1);
+      NXS_CHECK(nb < XBUF && i >= 0 && i <= nb);
+      myq[f * TILE_PIX] = make_float2(tpk, __int_as_float(pos));
+      if constexpr (keeps_alpha(XBUF)) mya[f * TILE_PIX] = t.alpha;
+      if (i == 0) thead = tpk;
+      ++nb;
+    }
+  }
+  } else {
+    for (int base = rg.x; base < rg.y; base += XBT) {
+      const int n = min(XBT, rg.y - base);
+      NXS_CHECK(n > 0 && n <= XBT);
+      __syncthreads();
+      if (tid < n) {
+        const uint32_t rk = pairs[base + tid];
+        s_rank[tid] = rk;
+        s_ring_rank[(base + tid) % (2 * XBT)] = rk;
+        s_zlo[tid] = zlo_rank[rk];
+        if (CH) s_chunk[tid] = rank_c[order[rk]] / (uint32_t)chunk;
+      }
+      __syncthreads();
+      // stage this batch into the ring slot it maps to (positions are consecutive)
+      for (int k = tid; k < n * REC_F4; k += TILE_PIX) {
+        const int e = k >> 3, part = k & 7;
+        s_ring[(base + e) % (2 * XBT)][part] = records[(size_t)s_rank[e] * REC_F4 + part];
+      }
+      ring_lo = max(rg.x, base - XBT);
+      __syncthreads();
+      if (!s.done) {
+        for (int j = 0; j < n; ++j) {
+          const float4* s_rec_j = s_ring[(base + j) % (2 * XBT)];
+          // every remaining entry has t >= bound: pending entries below it are
+          // final; a new chunk makes every pending entry final
+          const bool next_chunk = CH && s_chunk[j] != cur_chunk;  // (exact order: one chunk)
+          const float bound = s_zlo[j] * hnorm;
+  #if NXS_X_DEFER > 0
+          // Committable entries stay committable (every later entry's t is above
+          // this bound), so the exact order may defer them until enough lanes of
+          // the warp have one: the composite then runs with most lanes active.
+          // (a new chunk commits everything pending at once: never deferred)
+          bool go_commit = next_chunk;
+          if (!go_commit) {
+            const unsigned am = __activemask();
+            const unsigned want = __ballot_sync(am, nb > 0 && thead < bound);
+            go_commit = __popc(want) * 32 >= NXS_X_DEFER * __popc(am) || nb >= XBUF - 4;
+          }
+          while (go_commit && nb > 0 && (next_chunk || thead < bound)) {
+  #else
+          while (nb > 0 && (next_chunk || thead < bound)) {
+  #endif
+            commit_front();
+            if (s.done) break;
+          }
           if (s.done) {
             dpos = base + j;
             break;
           }
-        }
-        // insert (t, index) keeping the ring ascending from the head
-        const int pos = base + j;
-        int i = nb;
-        uint32_t gid_new = 0xffffffffu;
-        while (i > 0) {
-          const int e = (head + i - 1) & (XBUF - 1);
-          const float2 qe = myq[e * TILE_PIX];
-          bool later = qe.x > tpk;  // the pending entry commits after the new one
-          if (qe.x == tpk) {
-            if (gid_new == 0xffffffffu) gid_new = tie_key(s_rank[j]);
-            const int pe = __float_as_int(qe.y);
-            later = tie_key(pe < 0 ? (uint32_t)(-1 - pe) : pairs[pe]) > gid_new;
+          if (CH) cur_chunk = s_chunk[j];
+          if (COUNT) ++ntest;
+          TestOut t;
+          float tpk;
+          if (!test_with_t(s_rec_j, cam, px, py, pc, hnorm, cutoff, near_plane, t, tpk)) continue;
+          if (nb == XBUF) {
+            // overflow: the order is no longer guaranteed for this pixel
+            atomicAdd(overflow, 1ull);
+            commit_front();
+            if (s.done) {
+              dpos = base + j;
+              break;
+            }
           }
-          if (!later) break;
+          // insert (t, index) keeping the ring ascending from the head
+          const int pos = base + j;
+          int i = nb;
+          uint32_t gid_new = 0xffffffffu;
+          while (i > 0) {
+            const int e = (head + i - 1) & (XBUF - 1);
+            const float2 qe = myq[e * TILE_PIX];
+            bool later = qe.x > tpk;  // the pending entry commits after the new one
+            if (qe.x == tpk) {
+              if (gid_new == 0xffffffffu) gid_new = tie_key(s_rank[j]);
+              const int pe = __float_as_int(qe.y);
+              later = tie_key(pe < 0 ? (uint32_t)(-1 - pe) : pairs[pe]) > gid_new;
+            }
+            if (!later) break;
+            const int f = (head + i) & (XBUF - 1);
+            myq[f * TILE_PIX] = qe;
+            if constexpr (keeps_alpha(XBUF)) mya[f * TILE_PIX] = mya[e * TILE_PIX];
+            --i;
+          }
           const int f = (head + i) & (XBUF - 1);
-          myq[f * TILE_PIX] = qe;
-          if constexpr (keeps_alpha(XBUF)) mya[f * TILE_PIX] = mya[e * TILE_PIX];
-          --i;
+          NXS_CHECK(nb < XBUF && i >= 0 && i <= nb);
+  #ifdef NXS_XSTATS
+          atomicAdd(&g_xstats[0], 1ull);
+          atomicAdd(&g_xstats[1], (unsigned long long)(nb - i));
+          atomicAdd(&g_xstats[2], (unsigned long long)nb);
+          atomicAdd(&g_xstats[5 + min(nb, 31)], 1ull);
+  #endif
+          myq[f * TILE_PIX] = make_float2(tpk, __int_as_float(pos));
+          if constexpr (keeps_alpha(XBUF)) mya[f * TILE_PIX] = t.alpha;
+          if (i == 0) thead = tpk;
+          ++nb;
         }
-        const int f = (head + i) & (XBUF - 1);
-        NXS_CHECK(nb < XBUF && i >= 0 && i <= nb);
-#ifdef NXS_XSTATS
-        atomicAdd(&g_xstats[0], 1ull);
-        atomicAdd(&g_xstats[1], (unsigned long long)(nb - i));
-        atomicAdd(&g_xstats[2], (unsigned long long)nb);
-        atomicAdd(&g_xstats[5 + min(nb, 31)], 1ull);
-#endif
-        myq[f * TILE_PIX] = make_float2(tpk, __int_as_float(pos));
-        if constexpr (keeps_alpha(XBUF)) mya[f * TILE_PIX] = t.alpha;
-        if (i == 0) thead = tpk;
-        ++nb;
       }
+      if (__syncthreads_count(!s.done) == 0) break;
     }
-    if (__syncthreads_count(!s.done) == 0) break;
   }
   // end of the list: everything pending is final, in order (one chunk, the
   // end of a chunk, or the last depth phase) — or, with a later phase, only
