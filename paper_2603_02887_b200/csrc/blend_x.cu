@@ -277,22 +277,40 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
   };
 
   const int2 rg = ranges[tile];
-  if constexpr (!CH && FAM == FAM_EXP) {
-  // exact order, exponential family (never saturates: every pixel walks
-  // ~128 composites deep, at its own pace): every warp walks the tile list
-  // on its own, reading each entry's rank, z_lo and record through L1 (the
-  // block's 8 warps share the lines) — no staged batches, so no block
-  // barrier between entries (fwd 10.56 -> 7.03 ms at C3; the saturating
-  // models, whose walks are short, keep the shared staged batches: linear /
-  // softplus / blended lose 12-14 % unstaged)
+  if constexpr (!CH) {
+  // exact order: every warp walks the tile list on its own, reading each
+  // entry's rank, z_lo and test words through L1 (the block's 8 warps share
+  // the lines), software-pipelined in registers (ranks two entries ahead,
+  // the test words one ahead) — no staged batches, so no block barrier
+  // between entries: the warps' pending-buffer work is uneven, and the
+  // barriers made every warp wait for the slowest (softplus fwd 0.825 ->
+  // 0.745 ms, exponential 10.56 -> 5.94 ms at C3; unstaged without the
+  // prefetch was 12 % slower than staged for the saturating models)
   ring_lo = 0x7fffffff;  // (commits re-read their records the same way)
   if (!s.done) {
-    uint32_t rk_next = rg.x < rg.y ? __ldg(pairs + rg.x) : 0u;
+    // software pipeline: ranks two entries ahead, the test words and z_lo
+    // of the next entry one ahead (in registers)
+    auto ldrank = [&](int q) { return q < rg.y ? __ldg(pairs + q) : 0u; };
+    uint32_t rk_cur = ldrank(rg.x), rk_n1 = ldrank(rg.x + 1);
+    float4 c0, c1, c2, c3, c7;
+    float zc;
+    auto ldrec = [&](uint32_t r, float4& w0, float4& w1, float4& w2, float4& w3, float4& w7,
+                     float& z) {
+      const float4* g = records + (size_t)r * REC_F4;
+      w0 = __ldg(g + 0); w1 = __ldg(g + 1); w2 = __ldg(g + 2); w3 = __ldg(g + 3);
+      w7 = __ldg(g + 7);
+      z = __ldg(zlo_rank + r);
+    };
+    ldrec(rk_cur, c0, c1, c2, c3, c7, zc);
     for (int pos = rg.x; pos < rg.y; ++pos) {
-      const uint32_t rk = rk_next;
-      if (pos + 1 < rg.y) rk_next = __ldg(pairs + pos + 1);
-      const float4* rec = records + (size_t)rk * REC_F4;
-      const float bound = __ldg(zlo_rank + rk) * hnorm;
+      const uint32_t rk = rk_cur;
+      const float4 t0 = c0, t1 = c1, t2 = c2, t3 = c3, t7 = c7;
+      const float bound = zc * hnorm;
+      const uint32_t rk_n2 = ldrank(pos + 2);
+      if (pos + 1 < rg.y) ldrec(rk_n1, c0, c1, c2, c3, c7, zc);
+      rk_cur = rk_n1;
+      rk_n1 = rk_n2;
+      const float4* rec = records + (size_t)rk * REC_F4;  // (general records only)
 #if NXS_X_DEFER > 0
       bool go_commit;
       {
@@ -314,7 +332,14 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
       if (COUNT) ++ntest;
       TestOut t;
       float tpk;
-      if (!test_with_t(rec, cam, px, py, pc, hnorm, cutoff, near_plane, t, tpk)) continue;
+      bool okt;
+      if (__float_as_int(t3.w) & RF_GENERAL) {
+        okt = test_with_t(rec, cam, px, py, pc, hnorm, cutoff, near_plane, t, tpk);
+      } else {
+        okt = ray_peak_test(t0, t1, t2, t3, pc, cutoff, t);
+        tpk = hnorm * (__fmaf_rn(t7.x, pc.hx, __fmaf_rn(t7.y, pc.hy, t7.z)) * t.rD);
+      }
+      if (!okt) continue;
       if (nb == XBUF) {
         atomicAdd(overflow, 1ull);
         commit_front();
