@@ -249,6 +249,71 @@ __device__ __forceinline__ bool bwd_pair(BwdPix& A, BwdPix& B, const float4* rec
   return true;
 }
 
+// Warp transpose-reduce scratch: 12 moment-pair rows of 72 floats per warp
+// (row p = moments (2p, 2p+1) of all 32 lanes; lanes 16-31 shifted by 4
+// banks so the 8-byte pair stores and the 16-byte row loads are conflict free)
+constexpr int RED_HALF = 36;                    // lanes 16-31's pairs start here (bank shift)
+constexpr int RED_ROW = 2 * RED_HALF;           // one row per moment pair
+constexpr int RED_WARP = (NMOM / 2) * RED_ROW;  // floats per warp
+
+// Per list entry: each thread adds its two pixels' 24 moments, the warp
+// transposes them through `red` (12 moment-pair rows) and lane m < NMOM
+// returns moment m summed over the warp's 64 pixels.
+__device__ __forceinline__ float warp_moments(const PairOut& po, const PixelConst& pa,
+                                              const PixelConst& pb, float* red, int lane,
+                                              float Y0) {
+  // warp transpose-reduce through shared memory (moment-pair rows)
+  const F2 a = mul2(po.dm2, po.ux), b = mul2(po.dm2, po.uy), c = mul2(po.dm2, po.uz);
+  // moment pairs (2p, 2p+1) as one 8-byte store; rows 9 and 10 are unused
+  float v[NMOM];
+  v[0] = fmaf(a.x, po.ux.x, a.y * po.ux.y);
+  v[1] = fmaf(a.x, po.uy.x, a.y * po.uy.y);
+  v[2] = fmaf(a.x, po.uz.x, a.y * po.uz.y);
+  v[3] = fmaf(b.x, po.uy.x, b.y * po.uy.y);
+  v[4] = fmaf(b.x, po.uz.x, b.y * po.uz.y);
+  v[5] = fmaf(c.x, po.uz.x, c.y * po.uz.y);
+  v[6] = a.x + a.y;
+  v[7] = b.x + b.y;
+  v[8] = c.x + c.y;
+  v[9] = 0.f;
+  v[10] = 0.f;
+  v[11] = po.dak.x + po.dak.y;
+  v[12] = (po.e0.x + po.e0.y) * Y0;
+  v[13] = fmaf(po.e0.x, pa.Y1, po.e0.y * pb.Y1);
+  v[14] = fmaf(po.e0.x, pa.Y2, po.e0.y * pb.Y2);
+  v[15] = fmaf(po.e0.x, pa.Y3, po.e0.y * pb.Y3);
+  v[16] = (po.e1.x + po.e1.y) * Y0;
+  v[17] = fmaf(po.e1.x, pa.Y1, po.e1.y * pb.Y1);
+  v[18] = fmaf(po.e1.x, pa.Y2, po.e1.y * pb.Y2);
+  v[19] = fmaf(po.e1.x, pa.Y3, po.e1.y * pb.Y3);
+  v[20] = (po.e2.x + po.e2.y) * Y0;
+  v[21] = fmaf(po.e2.x, pa.Y1, po.e2.y * pb.Y1);
+  v[22] = fmaf(po.e2.x, pa.Y2, po.e2.y * pb.Y2);
+  v[23] = fmaf(po.e2.x, pa.Y3, po.e2.y * pb.Y3);
+  float2* col = reinterpret_cast<float2*>(red + (lane < 16 ? 2 * lane : RED_HALF + 2 * (lane - 16)));
+#pragma unroll
+  for (int q = 0; q < NMOM / 2; ++q) col[q * (RED_ROW / 2)] = make_float2(v[2 * q], v[2 * q + 1]);
+  __syncwarp();
+  // lane 2p sums moments (2p, 2p+1) over lanes 0-15, lane 2p+1 over
+  // lanes 16-31 (packed adds), then each keeps its own moment and
+  // takes the partner's half of it
+  F2 part = f2(0.f);
+  if (lane < NMOM) {
+    const float4* row =
+        reinterpret_cast<const float4*>(red + (lane >> 1) * RED_ROW + (lane & 1) * RED_HALF);
+    F2 t[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float4 r = row[i];
+      t[i] = add2(F2{r.x, r.y}, F2{r.z, r.w});
+    }
+    part = add2(add2(add2(t[0], t[1]), add2(t[2], t[3])), add2(add2(t[4], t[5]), add2(t[6], t[7])));
+  }
+  const float other = __shfl_xor_sync(0xffffffffu, (lane & 1) ? part.x : part.y, 1);
+  const float sum = ((lane & 1) ? part.y : part.x) + other;
+  return sum;
+}
+
 __device__ __forceinline__ void bwd_load(BwdPix& st, const CamDev& cam, int px, int py,
                                          const PixCache& cache, const float* __restrict__ seed,
                                          float bg0, float bg1, float bg2) {
