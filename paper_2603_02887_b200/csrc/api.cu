@@ -69,7 +69,8 @@ void launch_bin_sort(uint32_t*, const double*, const unsigned int*, const unsign
 void launch_project_ranks(const float*, const float*, const float*, const float*, const float*,
                           int, int64_t, int64_t, const uint32_t*, const CamDev&, double, double,
                           int4*, float4*, float4*, unsigned long long*, double*, cudaStream_t,
-                          const int* nd = nullptr);
+                          const int* nd = nullptr, uint32_t* live = nullptr,
+                          unsigned long long* n_live = nullptr);
 void launch_gather_keys(const uint32_t*, const uint32_t*, int64_t, uint32_t*, cudaStream_t);
 void launch_clear_rects(const uint32_t*, int64_t, int64_t, int4*, cudaStream_t);
 void launch_iota(uint32_t*, int64_t, cudaStream_t);
@@ -93,7 +94,8 @@ void launch_tile_scan(unsigned int*, int, int2*, unsigned long long*, unsigned l
 void launch_emit_tiles(const int4*, const uint32_t*, int64_t, int64_t, int, const uint8_t*,
                        const int2*, unsigned int*, uint32_t*, const double*, const CamDev&,
                        cudaStream_t, const int* nd, unsigned long long cap,
-                       const unsigned int* base = nullptr, unsigned long long* overflow = nullptr);
+                       const unsigned int* base = nullptr, unsigned long long* overflow = nullptr,
+                       const uint32_t* live = nullptr, const unsigned long long* n_live = nullptr);
 void launch_seg_sort(uint32_t*, int2*, unsigned int*, int, unsigned long long, cudaStream_t,
                      long long max_seg = -1, const unsigned int* base = nullptr,
                      unsigned long long* total = nullptr, unsigned long long* overflow = nullptr);
@@ -217,6 +219,7 @@ struct nxs_view {
   // per tile: phase ranges and virtual offsets, activity
   Buf ranges_ph[MAX_PHASES], cum_ph[MAX_PHASES + 1], active, tile_cnt;
   Buf tile_last;  // per tile: max over its pixels' last list position (K3 -> K4)
+  Buf live;       // device-sized phase 0: its ranks with a tile rectangle (count: dsmall[15])
   Buf bin_pos;  // per depth-key bin: first rank, then the scatter cursor
   // per-tile list capacities for the device-sized first phase (from the
   // view's last exact phase 0): emission needs no count pass while they hold
@@ -300,7 +303,7 @@ struct nxs_view {
   void for_each_buf(F f) {
     Buf* all[] = {&dkeys_in, &dkeys_out, &idx_in,  &idx_out, &records, &bframe, &rects,
                   &ntiles,   &offsets,   &moments, &touched, &pk_in,   &pk_out,  &pv_in,  &active,
-                  &tile_cnt, &tile_last, &bin_pos, &tile_base,
+                  &tile_cnt, &tile_last, &live, &bin_pos, &tile_base,
                   &depth,    &k32a,      &k32b,    &k32c,    &rank_of, &rank_c, &zlo_rank, &seq, &ph_hist,
                   &ph_sel,   &tq,      &zlo64,  &xc_t, &xc_r, &xc_n,
                   &c_last,   &c_sat,     &c_tk,    &c_thi,   &c_tlo,   &c_P,    &c_ck,
@@ -775,7 +778,8 @@ int forward_impl(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
   // dsmall: [0] straddle count, [1..4] event counters, [5] active tiles (u32),
   // [6] min depth key, [7] max depth key, [8] key-run overflow, [9] pending
   // overflow, [10]/[11] device-sized overflow/pairs, [12] last rank the
-  // finished tiles needed, [13]/[14] pair total / longest tile list
+  // finished tiles needed, [13]/[14] pair total / longest tile list, [15] ranks
+  // with a tile rectangle (device-sized phase 0: the emission list)
   unsigned long long* dsmall = v->dev_small.as<unsigned long long>();
   Counters* cnt = reinterpret_cast<Counters*>(dsmall + 1);
   unsigned int* n_active = reinterpret_cast<unsigned int*>(dsmall + 5);
@@ -900,6 +904,7 @@ retry_sort:
     NXS_CUDA(v->ph_hist.ensure(4097 * sizeof(unsigned int)));  // bins + ticket
     NXS_CUDA(v->ph_sel.ensure(96 * sizeof(long long)));
     NXS_CUDA(ensure_n<uint32_t>(v->pv_ph[0], capp));
+    NXS_CUDA(ensure_n<uint32_t>(v->live, P));
     NXS_CUDA(ensure_n<int2>(v->ranges_ph[0], n_tiles));
     NXS_CUDA(ensure_n<int32_t>(v->cum_ph[0], n_tiles));
     NXS_CUDA(ensure_n<int32_t>(v->cum_ph[1], n_tiles));
@@ -1149,7 +1154,8 @@ retry_sort:
                            scene->sh, C, 0, cap0, v->idx_out.as<uint32_t>(), cam,
                            opts->alpha_cutoff, opts->near_plane, v->rects.as<int4>(),
                            v->records.as<float4>(), v->bframe.as<float4>(), dsmall,
-                           v->tq.as<double>(), s, n_sel);
+                           v->tq.as<double>(), s, n_sel,
+                           v->async_bases ? v->live.as<uint32_t>() : nullptr, dsmall + 15);
       NXS_LAUNCHED("project_ranks");
       if (v->ev_ok) rec_event(v, v->evp[0][2], s);
       NXS_CUDA(ensure_n<int2>(v->ranges_ph[0], n_tiles));
@@ -1163,7 +1169,8 @@ retry_sort:
         launch_emit_tiles(v->rects.as<int4>(), v->idx_out.as<uint32_t>(), 0, cap0, cam.tiles_x,
                           v->active.as<uint8_t>(), nullptr, v->tile_cnt.as<uint32_t>(),
                           v->pv_ph[0].as<uint32_t>(), v->tq.as<double>(), cam, s, n_sel,
-                          (unsigned long long)capp, v->tile_base.as<uint32_t>(), dsmall + 10);
+                          (unsigned long long)capp, v->tile_base.as<uint32_t>(), dsmall + 10,
+                          v->live.as<uint32_t>(), dsmall + 15);
         NXS_LAUNCHED("emit_tiles");
         mark(v, 4, s);
         launch_seg_sort(v->pv_ph[0].as<uint32_t>(), v->ranges_ph[0].as<int2>(),

@@ -708,6 +708,10 @@ struct ProjOut {
   float4* bframe;               // per rank 3 x float4: rows of B (backward only)
   unsigned long long* straddle; // counter
   double* tq;                   // per RANK: silhouette conic + an inside point, tile rect (TQ_STRIDE)
+  // optional: the ranks with a tile rectangle, appended (any order), and
+  // their count — the emission then visits only those
+  uint32_t* live;
+  unsigned long long* n_live;
 };
 // per-rank tile-test slot: 10 doubles (conic, centre, 1/(2 Q00), 1/(2 Q11)),
 // then the tile rectangle as an int4 — the binning reads rank r's rect and
@@ -726,7 +730,7 @@ struct GParams {
   float shv[12];
 };
 
-__device__ __forceinline__ void project_one(const GParams& prm, int64_t g, int64_t rk, const CamDev& cam,
+__device__ __forceinline__ int4 project_one(const GParams& prm, int64_t g, int64_t rk, const CamDev& cam,
                                             double cutoff, double near_plane, const ProjOut& out,
                                             float4* rec, float4* bf) {
   const float cx0 = prm.c0, cx1 = prm.c1, cx2 = prm.c2;
@@ -937,6 +941,7 @@ __device__ __forceinline__ void project_one(const GParams& prm, int64_t g, int64
   }
   out.rects[g] = rect;  // storage order (coalesced; exports, the exact order's binning)
   if (out.tq) *reinterpret_cast<int4*>(out.tq + TQ_STRIDE * rk + 10) = rect;
+  return rect;
 }
 
 // K1: persistent blocks of 128 threads stream chunks of 128 Gaussians'
@@ -1089,6 +1094,7 @@ __global__ void __launch_bounds__(PROJ_CHUNK)
   if (nd) r1 = min(r1, r0 + (int64_t)*nd);
   const int tid = threadIdx.x, lane = tid & 31, wbase = tid & ~31;
   const int64_t r = r0 + (int64_t)blockIdx.x * PROJ_CHUNK + tid;
+  bool has_rect = false;
   if (r < r1) {
     const int64_t g = order[r];
     GParams prm;
@@ -1117,11 +1123,22 @@ __global__ void __launch_bounds__(PROJ_CHUNK)
         prm.shv[4 * c + 1] = prm.shv[4 * c + 2] = prm.shv[4 * c + 3] = 0.0f;
       }
     }
-    project_one(prm, g, r, cam, cutoff, near_plane, out, so.rec[tid], so.bf[tid]);
+    const int4 rect = project_one(prm, g, r, cam, cutoff, near_plane, out, so.rec[tid], so.bf[tid]);
     if (out.zlo_rank) out.zlo_rank[r] = __double2float_rd(out.zlo[g]);
     so.rank[tid] = r;
+    has_rect = rect.x >= 0;
   } else {
     so.rank[tid] = -1;
+  }
+  if (out.live) {  // warp-aggregated append of the ranks with a rectangle
+    const unsigned m = __ballot_sync(0xffffffffu, has_rect);
+    if (m) {
+      const int leader = __ffs(m) - 1;
+      unsigned long long at = 0;
+      if (lane == leader) at = atomicAdd(out.n_live, (unsigned long long)__popc(m));
+      at = __shfl_sync(0xffffffffu, at, leader);
+      if (has_rect) out.live[at + __popc(m & ((1u << lane) - 1u))] = (uint32_t)r;
+    }
   }
   __syncwarp();
 #pragma unroll
@@ -1381,12 +1398,20 @@ __global__ void __launch_bounds__(256)
                  const int2* __restrict__ ranges, unsigned int* __restrict__ cursor,
                  uint32_t* __restrict__ vals, const int* __restrict__ nd, unsigned long long cap,
                  const double* __restrict__ tq, CamDev cam, const unsigned int* __restrict__ base,
-                 unsigned long long* __restrict__ overflow) {
+                 unsigned long long* __restrict__ overflow, const uint32_t* __restrict__ live,
+                 const unsigned long long* __restrict__ n_live) {
   nxs_pdl_enter();
   const int sl = threadIdx.x & (KSUB - 1);
-  const int64_t r = r0 + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / KSUB;
-  const int64_t rn = nd ? min(r1, r0 + (int64_t)*nd) : r1;
-  if (r >= rn) return;
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / KSUB;
+  int64_t r;
+  if (live) {  // only the phase's ranks with a tile rectangle (k_project_ranks)
+    if (i >= (int64_t)*n_live) return;
+    r = live[i];
+  } else {
+    r = r0 + i;
+    const int64_t rn = nd ? min(r1, r0 + (int64_t)*nd) : r1;
+    if (r >= rn) return;
+  }
   const int4 rc = tq ? tq_rect(tq, r) : rects[order[r]];
   if (rc.x < 0) return;
   const double inv_f = cam.inv_f;  // = 1.0 / cam.f (host, IEEE)
@@ -1563,7 +1588,8 @@ void launch_emit_tiles(const int4* rects, const uint32_t* order, int64_t r0, int
                        int tiles_x, const uint8_t* active, const int2* ranges,
                        unsigned int* cursor, uint32_t* vals, const double* tq, const CamDev& cam,
                        cudaStream_t s, const int* nd, unsigned long long cap,
-                       const unsigned int* base, unsigned long long* overflow) {
+                       const unsigned int* base, unsigned long long* overflow,
+                       const uint32_t* live, const unsigned long long* n_live) {
   if (r1 <= r0) return;
 #ifndef NXS_EMIT_KSUB
 #define NXS_EMIT_KSUB 32
@@ -1572,11 +1598,11 @@ void launch_emit_tiles(const int4* rects, const uint32_t* order, int64_t r0, int
   if (r1 - r0 <= 262144)
     nxs_launch(k_emit_tiles<KS>, (unsigned)((r1 - r0 + 256 / KS - 1) / (256 / KS)), 256, 0, s, 
         rects, order, r0, r1, tiles_x, active, ranges, cursor, vals, nd, cap, tq, cam, base,
-        overflow);
+        overflow, live, n_live);
   else
     nxs_launch(k_emit_tiles<8>, (unsigned)((r1 - r0 + 31) / 32), 256, 0, s, 
         rects, order, r0, r1, tiles_x, active, ranges, cursor, vals, nd, cap, tq, cam, base,
-        overflow);
+        overflow, live, n_live);
 }
 void launch_make_bases(const int2* ranges, int n_tiles, unsigned int* base, cudaStream_t s) {
   nxs_launch(k_make_bases, 1, TSCAN_THREADS, 0, s, ranges, n_tiles, base);
@@ -1898,9 +1924,9 @@ void launch_project_ranks(const float* centers, const float* scales, const float
                           const uint32_t* order, const CamDev& cam, double cutoff,
                           double near_plane, int4* rects, float4* records, float4* bframe,
                           unsigned long long* straddle, double* tq, cudaStream_t s,
-                          const int* nd) {
+                          const int* nd, uint32_t* live, unsigned long long* n_live) {
   if (r1 <= r0) return;
-  ProjOut o{nullptr, nullptr, rects, records, bframe, straddle, tq};
+  ProjOut o{nullptr, nullptr, rects, records, bframe, straddle, tq, live, n_live};
   nxs_launch(k_project_ranks, (unsigned)((r1 - r0 + PROJ_CHUNK - 1) / PROJ_CHUNK), PROJ_CHUNK, 0, s, 
       centers, scales, quats, opacities, sh, C, r0, r1, order, cam, cutoff, near_plane, o, nd);
 }
