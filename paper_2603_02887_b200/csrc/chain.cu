@@ -29,7 +29,22 @@ __global__ void k_chain(const float* __restrict__ scales, const float* __restric
                         uint32_t* __restrict__ tlist, unsigned long long* __restrict__ tcount) {
   nxs_pdl_enter();
   int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= P || !touched[r]) return;
+  const bool act = r < P && touched[r];
+  const int64_t g = act ? (int64_t)order[r] : 0;
+  if (tlist && g_centers) {
+    // the Gaussians this backward wrote (any order): the touched-row export,
+    // appended one atomic per warp (a per-Gaussian atomic on the one
+    // counter serialised the kernel)
+    const unsigned m = __ballot_sync(0xffffffffu, act);
+    if (m) {
+      const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+      unsigned long long at = 0;
+      if (lane == leader) at = atomicAdd(tcount, (unsigned long long)__popc(m));
+      at = __shfl_sync(0xffffffffu, at, leader);
+      if (act) tlist[at + __popc(m & ((1u << lane) - 1u))] = (uint32_t)g;
+    }
+  }
+  if (!act) return;
   // read this rank's moments and leave the buffer zeroed for the next backward
   double* mm = moments + r * NMOM;
   double mv[NMOM];
@@ -40,9 +55,6 @@ __global__ void k_chain(const float* __restrict__ scales, const float* __restric
   }
   touched[r] = 0;
   if (!g_centers) return;  // clear only (a discarded speculative backward)
-  const int64_t g = order[r];
-  // the Gaussians this backward wrote (any order): the touched-row export
-  if (tlist) tlist[atomicAdd(tcount, 1ull)] = (uint32_t)g;
 
   // Gradients accumulate atomically: views sharing one gradient buffer may
   // run their chains concurrently on different streams (include/nxs.h).
