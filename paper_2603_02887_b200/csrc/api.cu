@@ -1662,7 +1662,6 @@ int backward_blend(nxs_view* v, const float* seed, cudaStream_t s) {
       off += (int64_t)(v->pv_ph[p].cap / sizeof(uint32_t));
     }
     NXS_CUDA(ensure_n<float>(v->partial, std::max<int64_t>(off, 1) * NMOM));
-    NXS_CUDA(cudaMemsetAsync(v->partial.p, 0, (size_t)off * NMOM * sizeof(float), s));
     lists.partial = v->partial.as<float>();
   }
   launch_blend_bwd(count, v->n_tiles, v->records.as<float4>(), v->bframe.as<float4>(), lists,

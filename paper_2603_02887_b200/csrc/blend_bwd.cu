@@ -28,7 +28,9 @@
 
 namespace nxs {
 
-constexpr int BWD_BATCH = 64;  // list entries staged per batch
+// list entries staged per batch: 64, or 32 in deterministic mode (its four
+// per-warp accumulator rows would otherwise cost a block per SM)
+__host__ __device__ constexpr int bwd_batch(bool det) { return det ? 32 : 64; }
 
 // Two pixels per thread: a 128-thread block covers the 16x16 tile, thread t
 // owning pixels t (rows 0-7) and t+128 (rows 8-15).  Each thread sums its
@@ -48,8 +50,8 @@ constexpr int BWD_WARPS = BWD_THREADS / 32;
 // at the flush) instead of shared float atomics from the four warps.
 __host__ __device__ constexpr int acc_rows(bool det) { return det ? BWD_WARPS : 1; }
 constexpr size_t bwd_smem(bool det) {
-  return 2 * (sizeof(float4) * BWD_BATCH * (REC_F4 + 3) + sizeof(uint32_t) * BWD_BATCH) +
-         sizeof(float) * BWD_BATCH * NMOM * acc_rows(det) + sizeof(float) * RED_WARP * BWD_WARPS;
+  return 2 * (sizeof(float4) * bwd_batch(det) * (REC_F4 + 3) + sizeof(uint32_t) * bwd_batch(det)) +
+         sizeof(float) * bwd_batch(det) * NMOM * acc_rows(det) + sizeof(float) * RED_WARP * BWD_WARPS;
 }
 
 
@@ -93,6 +95,7 @@ __global__ void __launch_bounds__(BWD_THREADS, NXS_BWD_MINB)
                 double* __restrict__ moments, uint8_t* __restrict__ touched,
                 Counters* __restrict__ cnt) {
   nxs_pdl_enter();
+  constexpr int BWD_BATCH = bwd_batch(DET);
   extern __shared__ float4 smem_dyn[];
   // [buffer][entry][part]
   float4(*s_rec2)[BWD_BATCH][REC_F4] = reinterpret_cast<float4(*)[BWD_BATCH][REC_F4]>(smem_dyn);
@@ -239,11 +242,11 @@ __global__ void __launch_bounds__(BWD_THREADS, NXS_BWD_MINB)
           float val = s_acc[k];
 #pragma unroll
           for (int w = 1; w < BWD_WARPS; ++w) val += s_acc[w * BWD_BATCH * NMOM + k];
-          if (val != 0.f) {
-            const int e = k / NMOM;
-            lists.partial[(slot0 + e) * NMOM + (k - e * NMOM)] = val;
-            touched[s_rank[e]] = 1;
-          }
+          const int e = k / NMOM;
+          // every replayed entry's row is written (zeros too): k_det_reduce
+          // reads only positions below the tile's last, so no memset
+          lists.partial[(slot0 + e) * NMOM + (k - e * NMOM)] = val;
+          if (val != 0.f) touched[s_rank[e]] = 1;
         }
       } else {
         for (int k = tid; k < n * NMOM; k += BWD_THREADS) {
@@ -323,6 +326,9 @@ __global__ void __launch_bounds__(256)
         else hi = mid;
       }
       if (lo >= rg.y || lists.pairs[p][lo] != (uint32_t)r) continue;
+      // entries past the tile's last replayed position were not written
+      const int tile = (rc.y + k / w) * tiles_x + rc.x + k % w;
+      if (lists.cum[p][tile] + (lo - rg.x) > lists.tile_last[tile]) continue;
       const float4* q = reinterpret_cast<const float4*>(lists.partial + (lists.poff[p] + lo) * NMOM);
 #pragma unroll
       for (int i = 0; i < NMOM / 4; ++i) {
