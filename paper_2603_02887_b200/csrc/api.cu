@@ -570,13 +570,13 @@ int nxs_view_create(nxs_view** out) {
   if (!out) return fail(NXS_ERR_INVALID, "null output pointer");
   nxs_view* v = new (std::nothrow) nxs_view();
   if (!v) return fail(NXS_ERR_NOMEM, "host allocation failed");
-  if (cudaHostAlloc((void**)&v->host_small, 32 * sizeof(unsigned long long),
+  if (cudaHostAlloc((void**)&v->host_small, 64 * sizeof(unsigned long long),
                     cudaHostAllocDefault) != cudaSuccess) {
     delete v;
     cudaGetLastError();
     return fail(NXS_ERR_CUDA, "cudaHostAlloc failed (no CUDA device?)");
   }
-  std::memset(v->host_small, 0, 32 * sizeof(unsigned long long));
+  std::memset(v->host_small, 0, 64 * sizeof(unsigned long long));
   cudaGetDevice(&v->device);
   v->ev_ok = true;
   for (auto& e : v->ev) v->ev_ok = v->ev_ok && cudaEventCreate(&e) == cudaSuccess;
@@ -1348,19 +1348,18 @@ retry_sort:
         launch_tile_scan(v->tile_cnt.as<uint32_t>(), n_tiles, v->ranges_ph[ph].as<int2>(),
                          dsmall + 13, dsmall + 14, ~0ull, nullptr, s);
         NXS_LAUNCHED("tile_scan");
-        NXS_CUDA(cudaMemcpyAsync(v->host_small, dsmall + 13, 2 * sizeof(unsigned long long),
-                                 cudaMemcpyDeviceToHost, s));
-      } else {
-        NXS_CUDA(cudaMemsetAsync(v->host_small, 0, 2 * sizeof(unsigned long long), s));
       }
-      NXS_CUDA(cudaMemcpyAsync(v->host_small + 2, dsmall, sizeof(unsigned long long),
+      // one copy of the small device counters (pair total and longest list,
+      // straddle count, active tiles, key-run overflow) behind the counting
+      unsigned long long* mirror = v->host_small + 32;
+      NXS_CUDA(cudaMemcpyAsync(mirror, dsmall, 16 * sizeof(unsigned long long),
                                cudaMemcpyDeviceToHost, s));
-      NXS_CUDA(cudaMemcpyAsync(v->host_small + 3, n_active, sizeof(unsigned int),
-                               cudaMemcpyDeviceToHost, s));
-      if (ph == 0 || v->lazy)
-        NXS_CUDA(cudaMemcpyAsync(v->host_small + 6, dsmall + 8, sizeof(unsigned long long),
-                                 cudaMemcpyDeviceToHost, s));
       NXS_CUDA(spin_sync(v, s));
+      v->host_small[0] = nr > 0 ? mirror[13] : 0ull;
+      v->host_small[1] = nr > 0 ? mirror[14] : 0ull;
+      v->host_small[2] = mirror[0];
+      v->host_small[3] = (unsigned int)mirror[5];
+      if (ph == 0 || v->lazy) v->host_small[6] = mirror[8];
       if (v->lazy && v->host_small[6] != 0 && phase_shift[ph] > 0) {
         // a long run of equal truncated keys: redo this phase on all 32 bits
         phase_full[ph] = true;
