@@ -335,12 +335,15 @@ def test_dropin_api_shapes_and_cache():
     assert out.rgb.shape == (16, 24, 3)
 
 
-@pytest.mark.parametrize("name", ["exponential", "linear", "softplus_20", "blended_0.5"])
-def test_near_plane_straddlers_match_oracle(name):
+@pytest.mark.parametrize("name,chunk", [("exponential", 1), ("linear", 1), ("softplus_20", 1),
+                                        ("blended_0.5", 1), ("softplus_20", None),
+                                        ("exponential", None), ("linear", 8)])
+def test_near_plane_straddlers_match_oracle(name, chunk):
     """Gaussians whose cutoff ellipsoid crosses the near plane (some centred
     behind the camera) take the fp64 general path; forward and gradients
     must still match the reference semantics (render.py:122-134, incl. the
-    t > near test)."""
+    t > near test) — in the global order and in the t-ordered ones (the
+    exact order's per-warp list walk reads general records from memory)."""
     rng = np.random.default_rng(3)
     base = O.round_scene_f32(O.canonical_scene(300, seed=4))
     k = 6
@@ -358,16 +361,17 @@ def test_near_plane_straddlers_match_oracle(name):
     cam = O.canonical_camera(48, 40)
     bg = np.array([0.1, 0.05, 0.2], dtype=np.float32).astype(np.float64)
     model = MODELS[name]
-    fwd = O.forward(sc, cam, model, bg, chunk_size=1, keep_state=True)
+    fwd = O.forward(sc, cam, model, bg, chunk_size=chunk, keep_state=True)
     seed = O.canonical_seed(48, 40, 0).reshape(-1, 3).astype(np.float32).astype(np.float64) \
         * (~fwd["mask"])[:, None]
     g_ref, mass = O.backward(sc, cam, model, bg, fwd, seed, with_mass=True)
-    got = gpu_run(sc, cam, model, bg, seed=seed.reshape(40, 48, 3))
+    got = gpu_run(sc, cam, model, bg, seed=seed.reshape(40, 48, 3), chunk_size=chunk)
     assert got["stats"]["n_straddling"] >= 3
     bad, kept = check_forward(got, fwd, fwd["mask"], 40, 48)
     assert bad == 0, (bad, kept)
-    check_masked(fwd, model, False, 48 * 40)
-    check_grads("near_plane", name, got["grads"], g_ref, mass)
+    check_masked(fwd, model, chunk != 1, 48 * 40)
+    tag = name if chunk == 1 else f"{name}__{'none' if chunk is None else chunk}"
+    check_grads("near_plane", tag, got["grads"], g_ref, mass)
 
 
 @pytest.mark.parametrize("cs", [1, 128, None])
