@@ -1642,7 +1642,8 @@ int backward_blend(nxs_view* v, const float* seed, cudaStream_t s) {
     BwdXArgs xa{v->records.as<float4>(), v->bframe.as<float4>(), v->pv_ph[0].as<uint32_t>(),
                 v->seq.as<int32_t>(), std::max(1, v->opts.max_splats),
                 (float)v->opts.alpha_cutoff, v->opts.near_plane, {v->bg[0], v->bg[1], v->bg[2]},
-                seed, v->moments.as<double>(), v->touched.as<uint8_t>()};
+                seed, v->moments.as<double>(), v->touched.as<uint8_t>(),
+                !(v->opts.chunk_size > 1 && v->opts.chunk_size < v->P)};
     launch_blend_bwd_x(count, v->n_tiles, xa, v->cam, v->model, v->cache(), cnt, s);
   } else {
   PhaseLists lists{};

@@ -563,16 +563,20 @@ constexpr int XRED_STRIDE = 36;
 // 11 float4) — the next step's record streams in while this one is replayed
 constexpr int XREC_F4 = REC_F4 + 3;
 constexpr size_t BWDX_WARP_FLOATS = NMOM * XRED_STRIDE + 2 * XREC_F4 * 4;
-constexpr size_t BWDX_SMEM = sizeof(float) * BWDX_WARP_FLOATS * (TILE_PIX / 2 / 32);
+// (per block: one warp slot per warp; NP pixels per thread)
+constexpr size_t bwdx_smem(int np) { return sizeof(float) * BWDX_WARP_FLOATS * (TILE_PIX / np / 32); }
 
 // Two pixels per thread (adjacent rows, a warp = one 8x8 block, a 128-thread
 // block per tile, as K4): each warp step serves the largest pending rank over its 64 pixels,
 // and a thread adds both of its pixels' moments before the warp reduction.
-constexpr int BWDX_THREADS = TILE_PIX / 2;
+// The exact order runs one pixel per thread (256-thread blocks, a warp =
+// an 8x4 block: smaller warp footprints take fewer lock-step rank steps, and
+// 91 registers): exact-order bwd 0.715 -> 0.694 ms, exponential 8.19 ->
+// 7.89; the chunked order keeps two (its chunk-sorted sequences step
+// together better: 0.368 vs 0.405 ms).
 
-template <int FAM, bool COUNT>
-__global__ void __launch_bounds__(BWDX_THREADS)
-    k_blend_bwd_x(const float4* __restrict__ records, const float4* __restrict__ bframe,
+template <int FAM, bool COUNT, int XNP>
+__device__ __forceinline__ void bwd_x_body(const float4* __restrict__ records, const float4* __restrict__ bframe,
                   const uint32_t* __restrict__ pairs, const int32_t* __restrict__ seq,
                   int max_splats, CamDev cam, ModelDev m, float cutoff, double near_plane,
                   float bg0, float bg1, float bg2, const float* __restrict__ seed,
@@ -583,15 +587,17 @@ __global__ void __launch_bounds__(BWDX_THREADS)
   const int tile = blockIdx.x;
   const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
   const int tid = threadIdx.x, lane = tid & 31;
-  // a warp = one 8x8 pixel block, the thread's pixels on adjacent rows (as K4)
+  // a warp = one 8x8 pixel block, the thread's pixels on adjacent rows (as
+  // K4); with one pixel per thread an 8x4 block (as K3x)
   const int px = tx * TILE + ((tid >> 5) & 1) * 8 + (tid & 7),
-            py0 = ty * TILE + (tid >> 6) * 8 + 2 * ((tid >> 3) & 3);
-  BwdPix st[2];
-  const int32_t* myseq[2];
-  int ptr[2];
+            py0 = XNP == 2 ? ty * TILE + (tid >> 6) * 8 + 2 * ((tid >> 3) & 3)
+                           : ty * TILE + (tid >> 6) * 4 + ((tid >> 3) & 3);
+  BwdPix st[XNP];
+  const int32_t* myseq[XNP];
+  int ptr[XNP];
   const size_t npix = (size_t)cam.W * cam.H;
 #pragma unroll
-  for (int q = 0; q < 2; ++q) {
+  for (int q = 0; q < XNP; ++q) {
     const int py = py0 + q;
     bwd_load(st[q], cam, px, py, cache, seed, bg0, bg1, bg2);
     const bool inside = px < cam.W && py < cam.H;
@@ -606,9 +612,9 @@ __global__ void __launch_bounds__(BWDX_THREADS)
   unsigned long long ntest = 0, nent = 0;
   // each pixel's next commit (cur) and the one after it (nxt, prefetched a
   // step ahead so its load latency hides behind a whole step)
-  int cur[2], nxt[2];
+  int cur[XNP], nxt[XNP];
 #pragma unroll
-  for (int q = 0; q < 2; ++q) {
+  for (int q = 0; q < XNP; ++q) {
     NXS_CHECK(ptr[q] < max_splats);
     cur[q] = ptr[q] >= 0 ? myseq[q][(size_t)ptr[q] * npix] : -1;
     nxt[q] = ptr[q] >= 1 ? myseq[q][(size_t)(ptr[q] - 1) * npix] : -1;
@@ -622,7 +628,7 @@ __global__ void __launch_bounds__(BWDX_THREADS)
     }
     cp_async_commit();
   };
-  int wcur = __reduce_max_sync(0xffffffffu, max(cur[0], cur[1]));
+  int wcur = __reduce_max_sync(0xffffffffu, XNP == 2 ? max(cur[0], cur[XNP - 1]) : cur[0]);
   int b = 0;
   if (wcur >= 0) fetch(wcur, 0);
 
@@ -630,10 +636,10 @@ __global__ void __launch_bounds__(BWDX_THREADS)
     if (COUNT && lane == 0) ++nent;
     const uint32_t rank = (uint32_t)wcur;  // warp-uniform
     // this step's pixels advance; the next step's rank is known at once
-    bool mine[2];
-    int idx[2];
+    bool mine[XNP];
+    int idx[XNP];
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < XNP; ++q) {
       mine[q] = cur[q] == wcur;
       idx[q] = ptr[q];
       if (mine[q]) {
@@ -642,7 +648,7 @@ __global__ void __launch_bounds__(BWDX_THREADS)
         nxt[q] = ptr[q] >= 1 ? myseq[q][(size_t)(ptr[q] - 1) * npix] : -1;
       }
     }
-    const int wnext = __reduce_max_sync(0xffffffffu, max(cur[0], cur[1]));
+    const int wnext = __reduce_max_sync(0xffffffffu, XNP == 2 ? max(cur[0], cur[XNP - 1]) : cur[0]);
     if (wnext >= 0) {
       fetch(wnext, b ^ 1);
       cp_async_wait<1>();
@@ -652,41 +658,71 @@ __global__ void __launch_bounds__(BWDX_THREADS)
     __syncwarp();
     const float4* rec = wrec + b * XREC_F4;
     const float4* bf = rec + REC_F4;
-    float dm2[2] = {0.f, 0.f}, ux[2] = {0.f, 0.f}, uy[2] = {0.f, 0.f}, uz[2] = {0.f, 0.f};
-    float dak[2] = {0.f, 0.f}, e0[2] = {0.f, 0.f}, e1[2] = {0.f, 0.f}, e2[2] = {0.f, 0.f};
+    float dm2[XNP], ux[XNP], uy[XNP], uz[XNP], dak[XNP], e0[XNP], e1[XNP], e2[XNP];
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < XNP; ++q)
+      dm2[q] = ux[q] = uy[q] = uz[q] = dak[q] = e0[q] = e1[q] = e2[q] = 0.f;
+#pragma unroll
+    for (int q = 0; q < XNP; ++q) {
       if (mine[q])
         bwd_pixel<FAM>(st[q], rec, bf, idx[q], cam, m, cutoff, near_plane, inv_f, gam, dm2[q],
                        ux[q], uy[q], uz[q], dak[q], e0[q], e1[q], e2[q], ntest, COUNT);
     }
-    const PixelConst& pa = st[0].pc;
-    const PixelConst& pb = st[1].pc;
-    const float ax = dm2[0] * ux[0], ay = dm2[0] * uy[0], az = dm2[0] * uz[0];
-    const float bx = dm2[1] * ux[1], by = dm2[1] * uy[1], bz = dm2[1] * uz[1];
     float* col = red + lane;
-    col[0 * XRED_STRIDE] = fmaf(ax, ux[0], bx * ux[1]);
-    col[1 * XRED_STRIDE] = fmaf(ax, uy[0], bx * uy[1]);
-    col[2 * XRED_STRIDE] = fmaf(ax, uz[0], bx * uz[1]);
-    col[3 * XRED_STRIDE] = fmaf(ay, uy[0], by * uy[1]);
-    col[4 * XRED_STRIDE] = fmaf(ay, uz[0], by * uz[1]);
-    col[5 * XRED_STRIDE] = fmaf(az, uz[0], bz * uz[1]);
+    if constexpr (XNP == 1) {
+      const PixelConst& pa = st[0].pc;
+      const float ax = dm2[0] * ux[0], ay = dm2[0] * uy[0], az = dm2[0] * uz[0];
+      col[0 * XRED_STRIDE] = ax * ux[0];
+      col[1 * XRED_STRIDE] = ax * uy[0];
+      col[2 * XRED_STRIDE] = ax * uz[0];
+      col[3 * XRED_STRIDE] = ay * uy[0];
+      col[4 * XRED_STRIDE] = ay * uz[0];
+      col[5 * XRED_STRIDE] = az * uz[0];
+      col[6 * XRED_STRIDE] = ax;
+      col[7 * XRED_STRIDE] = ay;
+      col[8 * XRED_STRIDE] = az;
+      col[11 * XRED_STRIDE] = dak[0];
+      col[12 * XRED_STRIDE] = e0[0] * Y0;
+      col[13 * XRED_STRIDE] = e0[0] * pa.Y1;
+      col[14 * XRED_STRIDE] = e0[0] * pa.Y2;
+      col[15 * XRED_STRIDE] = e0[0] * pa.Y3;
+      col[16 * XRED_STRIDE] = e1[0] * Y0;
+      col[17 * XRED_STRIDE] = e1[0] * pa.Y1;
+      col[18 * XRED_STRIDE] = e1[0] * pa.Y2;
+      col[19 * XRED_STRIDE] = e1[0] * pa.Y3;
+      col[20 * XRED_STRIDE] = e2[0] * Y0;
+      col[21 * XRED_STRIDE] = e2[0] * pa.Y1;
+      col[22 * XRED_STRIDE] = e2[0] * pa.Y2;
+      col[23 * XRED_STRIDE] = e2[0] * pa.Y3;
+    } else {
+    const PixelConst& pa = st[0].pc;
+    const PixelConst& pb = st[XNP - 1].pc;
+    const float ax = dm2[0] * ux[0], ay = dm2[0] * uy[0], az = dm2[0] * uz[0];
+    const float bx = dm2[XNP - 1] * ux[XNP - 1], by = dm2[XNP - 1] * uy[XNP - 1],
+                bz = dm2[XNP - 1] * uz[XNP - 1];
+    col[0 * XRED_STRIDE] = fmaf(ax, ux[0], bx * ux[XNP - 1]);
+    col[1 * XRED_STRIDE] = fmaf(ax, uy[0], bx * uy[XNP - 1]);
+    col[2 * XRED_STRIDE] = fmaf(ax, uz[0], bx * uz[XNP - 1]);
+    col[3 * XRED_STRIDE] = fmaf(ay, uy[0], by * uy[XNP - 1]);
+    col[4 * XRED_STRIDE] = fmaf(ay, uz[0], by * uz[XNP - 1]);
+    col[5 * XRED_STRIDE] = fmaf(az, uz[0], bz * uz[XNP - 1]);
     col[6 * XRED_STRIDE] = ax + bx;
     col[7 * XRED_STRIDE] = ay + by;
     col[8 * XRED_STRIDE] = az + bz;
-    col[11 * XRED_STRIDE] = dak[0] + dak[1];
-    col[12 * XRED_STRIDE] = (e0[0] + e0[1]) * Y0;
-    col[13 * XRED_STRIDE] = fmaf(e0[0], pa.Y1, e0[1] * pb.Y1);
-    col[14 * XRED_STRIDE] = fmaf(e0[0], pa.Y2, e0[1] * pb.Y2);
-    col[15 * XRED_STRIDE] = fmaf(e0[0], pa.Y3, e0[1] * pb.Y3);
-    col[16 * XRED_STRIDE] = (e1[0] + e1[1]) * Y0;
-    col[17 * XRED_STRIDE] = fmaf(e1[0], pa.Y1, e1[1] * pb.Y1);
-    col[18 * XRED_STRIDE] = fmaf(e1[0], pa.Y2, e1[1] * pb.Y2);
-    col[19 * XRED_STRIDE] = fmaf(e1[0], pa.Y3, e1[1] * pb.Y3);
-    col[20 * XRED_STRIDE] = (e2[0] + e2[1]) * Y0;
-    col[21 * XRED_STRIDE] = fmaf(e2[0], pa.Y1, e2[1] * pb.Y1);
-    col[22 * XRED_STRIDE] = fmaf(e2[0], pa.Y2, e2[1] * pb.Y2);
-    col[23 * XRED_STRIDE] = fmaf(e2[0], pa.Y3, e2[1] * pb.Y3);
+    col[11 * XRED_STRIDE] = dak[0] + dak[XNP - 1];
+    col[12 * XRED_STRIDE] = (e0[0] + e0[XNP - 1]) * Y0;
+    col[13 * XRED_STRIDE] = fmaf(e0[0], pa.Y1, e0[XNP - 1] * pb.Y1);
+    col[14 * XRED_STRIDE] = fmaf(e0[0], pa.Y2, e0[XNP - 1] * pb.Y2);
+    col[15 * XRED_STRIDE] = fmaf(e0[0], pa.Y3, e0[XNP - 1] * pb.Y3);
+    col[16 * XRED_STRIDE] = (e1[0] + e1[XNP - 1]) * Y0;
+    col[17 * XRED_STRIDE] = fmaf(e1[0], pa.Y1, e1[XNP - 1] * pb.Y1);
+    col[18 * XRED_STRIDE] = fmaf(e1[0], pa.Y2, e1[XNP - 1] * pb.Y2);
+    col[19 * XRED_STRIDE] = fmaf(e1[0], pa.Y3, e1[XNP - 1] * pb.Y3);
+    col[20 * XRED_STRIDE] = (e2[0] + e2[XNP - 1]) * Y0;
+    col[21 * XRED_STRIDE] = fmaf(e2[0], pa.Y1, e2[XNP - 1] * pb.Y1);
+    col[22 * XRED_STRIDE] = fmaf(e2[0], pa.Y2, e2[XNP - 1] * pb.Y2);
+    col[23 * XRED_STRIDE] = fmaf(e2[0], pa.Y3, e2[XNP - 1] * pb.Y3);
+    }
     __syncwarp();
     if (lane < NMOM && lane != 9 && lane != 10) {
       const float4* row = reinterpret_cast<const float4*>(red + lane * XRED_STRIDE);
@@ -719,6 +755,27 @@ __global__ void __launch_bounds__(BWDX_THREADS)
       atomicAdd(&cnt->entries_bwd, s_cnt[1]);
     }
   }
+}
+
+// (the two block shapes as separate kernels so each gets its own register
+// budget: 91-103 registers at one pixel per thread, 128 at two)
+template <int FAM, bool COUNT>
+__global__ void __launch_bounds__(TILE_PIX, 1) k_blend_bwd_x1(const float4* __restrict__ records, const float4* __restrict__ bframe,
+                  const uint32_t* __restrict__ pairs, const int32_t* __restrict__ seq,
+                  int max_splats, CamDev cam, ModelDev m, float cutoff, double near_plane,
+                  float bg0, float bg1, float bg2, const float* __restrict__ seed,
+                  PixCache cache, double* __restrict__ moments, uint8_t* __restrict__ touched,
+                  Counters* __restrict__ cnt) {
+  bwd_x_body<FAM, COUNT, 1>(records, bframe, pairs, seq, max_splats, cam, m, cutoff, near_plane, bg0, bg1, bg2, seed, cache, moments, touched, cnt);
+}
+template <int FAM, bool COUNT>
+__global__ void __launch_bounds__(TILE_PIX / 2) k_blend_bwd_x2(const float4* __restrict__ records, const float4* __restrict__ bframe,
+                  const uint32_t* __restrict__ pairs, const int32_t* __restrict__ seq,
+                  int max_splats, CamDev cam, ModelDev m, float cutoff, double near_plane,
+                  float bg0, float bg1, float bg2, const float* __restrict__ seed,
+                  PixCache cache, double* __restrict__ moments, uint8_t* __restrict__ touched,
+                  Counters* __restrict__ cnt) {
+  bwd_x_body<FAM, COUNT, 2>(records, bframe, pairs, seq, max_splats, cam, m, cutoff, near_plane, bg0, bg1, bg2, seed, cache, moments, touched, cnt);
 }
 
 // ---------------------------------------------------------------------------
@@ -782,13 +839,17 @@ static void launch_bwd_x_fam(bool count, int n_tiles, const BwdXArgs& a, const C
                              cudaStream_t s) {
   static unsigned long long attr_dev = 0;
   once_per_device(attr_dev, [] {
-    set_smem(k_blend_bwd_x<FAM, true>, BWDX_SMEM);
-    set_smem(k_blend_bwd_x<FAM, false>, BWDX_SMEM);
+    set_smem(k_blend_bwd_x1<FAM, true>, bwdx_smem(1));
+    set_smem(k_blend_bwd_x1<FAM, false>, bwdx_smem(1));
+    set_smem(k_blend_bwd_x2<FAM, true>, bwdx_smem(2));
+    set_smem(k_blend_bwd_x2<FAM, false>, bwdx_smem(2));
   });
-  auto k = count ? k_blend_bwd_x<FAM, true> : k_blend_bwd_x<FAM, false>;
-  nxs_launch(k, n_tiles, BWDX_THREADS, BWDX_SMEM, s, a.records, a.bframe, a.pairs, a.seq, a.max_splats, cam, m,
-                                         a.cutoff, a.near_plane, a.bg[0], a.bg[1], a.bg[2],
-                                         a.seed, cache, a.moments, a.touched, cnt);
+  const int np = a.exact ? 1 : 2;
+  auto k = a.exact ? (count ? k_blend_bwd_x1<FAM, true> : k_blend_bwd_x1<FAM, false>)
+                   : (count ? k_blend_bwd_x2<FAM, true> : k_blend_bwd_x2<FAM, false>);
+  nxs_launch(k, n_tiles, TILE_PIX / np, bwdx_smem(np), s, a.records, a.bframe, a.pairs, a.seq,
+             a.max_splats, cam, m, a.cutoff, a.near_plane, a.bg[0], a.bg[1], a.bg[2], a.seed,
+             cache, a.moments, a.touched, cnt);
 }
 
 void launch_blend_bwd_x(bool count, int n_tiles, const BwdXArgs& a, const CamDev& cam,

@@ -253,6 +253,7 @@ struct BwdXArgs {
   const float* seed;
   double* moments;
   uint8_t* touched;
+  bool exact;  // exact order (one chunk): one pixel per thread, else two
 };
 
 struct Counters {
