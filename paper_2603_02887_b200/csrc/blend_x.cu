@@ -564,7 +564,7 @@ constexpr int XRED_STRIDE = 36;
 constexpr int XREC_F4 = REC_F4 + 3;
 constexpr size_t BWDX_WARP_FLOATS = NMOM * XRED_STRIDE + 2 * XREC_F4 * 4;
 // (per block: one warp slot per warp; NP pixels per thread)
-constexpr size_t bwdx_smem(int np) { return sizeof(float) * BWDX_WARP_FLOATS * (TILE_PIX / np / 32); }
+constexpr size_t bwdx_smem(int np) { return sizeof(float) * BWDX_WARP_FLOATS * (np == 1 ? 1 : TILE_PIX / np / 32); }
 
 // Two pixels per thread (adjacent rows, a warp = one 8x8 block, a 128-thread
 // block per tile, as K4): each warp step serves the largest pending rank over its 64 pixels,
@@ -581,12 +581,13 @@ __device__ __forceinline__ void bwd_x_body(const float4* __restrict__ records, c
                   int max_splats, CamDev cam, ModelDev m, float cutoff, double near_plane,
                   float bg0, float bg1, float bg2, const float* __restrict__ seed,
                   PixCache cache, double* __restrict__ moments, uint8_t* __restrict__ touched,
-                  Counters* __restrict__ cnt) {
+                  Counters* __restrict__ cnt, int tile, int wid) {
   nxs_pdl_enter();
   extern __shared__ float smem_red[];
-  const int tile = blockIdx.x;
   const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
-  const int tid = threadIdx.x, lane = tid & 31;
+  // (tid: the thread's index within the tile; its warp's shared slot is
+  // threadIdx.x >> 5 of this block)
+  const int lane = threadIdx.x & 31, tid = wid * 32 + lane;
   // a warp = one 8x8 pixel block, the thread's pixels on adjacent rows (as
   // K4); with one pixel per thread an 8x4 block (as K3x)
   const int px = tx * TILE + ((tid >> 5) & 1) * 8 + (tid & 7),
@@ -604,7 +605,7 @@ __device__ __forceinline__ void bwd_x_body(const float4* __restrict__ records, c
     myseq[q] = seq + (inside ? (size_t)py * cam.W + px : 0);  // [slot][pixel]
     ptr[q] = st[q].last;  // commit index, back to front
   }
-  float* red = smem_red + (tid >> 5) * BWDX_WARP_FLOATS;
+  float* red = smem_red + (threadIdx.x >> 5) * BWDX_WARP_FLOATS;
   float4* wrec = reinterpret_cast<float4*>(red + NMOM * XRED_STRIDE);  // [2][XREC_F4]
   const float gam = (FAM == FAM_EXP) ? 1.0f : m.c;
   const float inv_f = (float)cam.inv_f;
@@ -742,17 +743,12 @@ __device__ __forceinline__ void bwd_x_body(const float4* __restrict__ records, c
     b ^= 1;
   }
 
-  if (COUNT) {
-    __shared__ unsigned long long s_cnt[2];
-    __syncthreads();
-    if (tid == 0) s_cnt[0] = s_cnt[1] = 0;
-    __syncthreads();
-    atomicAdd(&s_cnt[0], ntest);
-    atomicAdd(&s_cnt[1], nent);
-    __syncthreads();
-    if (tid == 0) {
-      atomicAdd(&cnt->tests_bwd, s_cnt[0]);
-      atomicAdd(&cnt->entries_bwd, s_cnt[1]);
+  if (COUNT) {  // (per warp: the warps of a tile may be separate blocks)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ntest += __shfl_xor_sync(0xffffffffu, ntest, o);
+    if (lane == 0) {
+      atomicAdd(&cnt->tests_bwd, ntest);
+      atomicAdd(&cnt->entries_bwd, nent);
     }
   }
 }
@@ -760,13 +756,15 @@ __device__ __forceinline__ void bwd_x_body(const float4* __restrict__ records, c
 // (the two block shapes as separate kernels so each gets its own register
 // budget: 91-103 registers at one pixel per thread, 128 at two)
 template <int FAM, bool COUNT>
-__global__ void __launch_bounds__(TILE_PIX, 1) k_blend_bwd_x1(const float4* __restrict__ records, const float4* __restrict__ bframe,
+__global__ void __launch_bounds__(32, 1) k_blend_bwd_x1(const float4* __restrict__ records, const float4* __restrict__ bframe,
                   const uint32_t* __restrict__ pairs, const int32_t* __restrict__ seq,
                   int max_splats, CamDev cam, ModelDev m, float cutoff, double near_plane,
                   float bg0, float bg1, float bg2, const float* __restrict__ seed,
                   PixCache cache, double* __restrict__ moments, uint8_t* __restrict__ touched,
                   Counters* __restrict__ cnt) {
-  bwd_x_body<FAM, COUNT, 1>(records, bframe, pairs, seq, max_splats, cam, m, cutoff, near_plane, bg0, bg1, bg2, seed, cache, moments, touched, cnt);
+  // one warp per block (8 per tile): a warp that finishes its steps frees
+  // its slot at once instead of idling until its tile's slowest warp is done
+  bwd_x_body<FAM, COUNT, 1>(records, bframe, pairs, seq, max_splats, cam, m, cutoff, near_plane, bg0, bg1, bg2, seed, cache, moments, touched, cnt, blockIdx.x >> 3, blockIdx.x & 7);
 }
 template <int FAM, bool COUNT>
 __global__ void __launch_bounds__(TILE_PIX / 2) k_blend_bwd_x2(const float4* __restrict__ records, const float4* __restrict__ bframe,
@@ -775,7 +773,7 @@ __global__ void __launch_bounds__(TILE_PIX / 2) k_blend_bwd_x2(const float4* __r
                   float bg0, float bg1, float bg2, const float* __restrict__ seed,
                   PixCache cache, double* __restrict__ moments, uint8_t* __restrict__ touched,
                   Counters* __restrict__ cnt) {
-  bwd_x_body<FAM, COUNT, 2>(records, bframe, pairs, seq, max_splats, cam, m, cutoff, near_plane, bg0, bg1, bg2, seed, cache, moments, touched, cnt);
+  bwd_x_body<FAM, COUNT, 2>(records, bframe, pairs, seq, max_splats, cam, m, cutoff, near_plane, bg0, bg1, bg2, seed, cache, moments, touched, cnt, blockIdx.x, threadIdx.x >> 5);
 }
 
 // ---------------------------------------------------------------------------
@@ -847,7 +845,8 @@ static void launch_bwd_x_fam(bool count, int n_tiles, const BwdXArgs& a, const C
   const int np = a.exact ? 1 : 2;
   auto k = a.exact ? (count ? k_blend_bwd_x1<FAM, true> : k_blend_bwd_x1<FAM, false>)
                    : (count ? k_blend_bwd_x2<FAM, true> : k_blend_bwd_x2<FAM, false>);
-  nxs_launch(k, n_tiles, TILE_PIX / np, bwdx_smem(np), s, a.records, a.bframe, a.pairs, a.seq,
+  nxs_launch(k, np == 1 ? 8 * n_tiles : n_tiles, np == 1 ? 32 : TILE_PIX / 2, bwdx_smem(np), s,
+             a.records, a.bframe, a.pairs, a.seq,
              a.max_splats, cam, m, a.cutoff, a.near_plane, a.bg[0], a.bg[1], a.bg[2], a.seed,
              cache, a.moments, a.touched, cnt);
 }
