@@ -74,13 +74,14 @@ void launch_project_ranks(const float*, const float*, const float*, const float*
 void launch_gather_keys(const uint32_t*, const uint32_t*, int64_t, uint32_t*, cudaStream_t);
 void launch_clear_rects(const uint32_t*, int64_t, int64_t, int4*, cudaStream_t);
 void launch_iota(uint32_t*, int64_t, cudaStream_t);
-void launch_phase_bound(const unsigned long long*, int, float*, cudaStream_t);
+void launch_phase_bound(const unsigned long long*, int, float*, cudaStream_t,
+                        const long long* dbin = nullptr);
 void launch_zlo_ranks(const float*, const float*, const float*, const float*, const uint32_t*,
                       int64_t, int64_t, const CamDev&, double, double*, cudaStream_t);
 void launch_project_ranks_z(const float*, const float*, const float*, const float*, const float*,
                             int, int64_t, int64_t, const uint32_t*, const CamDev&, double, double,
                             const double*, float*, int4*, float4*, float4*, unsigned long long*,
-                            double*, cudaStream_t);
+                            double*, cudaStream_t, const int* nd = nullptr);
 void launch_pack_check(const unsigned long long*, const long long*, int, unsigned long long*,
                        cudaStream_t);
 void launch_call_init(unsigned long long*, uint8_t*, int32_t*, int2*, unsigned int*, int,
@@ -869,7 +870,7 @@ int forward_impl(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
   // (a new camera's depth-key histogram differs: its phase-0 bins and pair
   // count are sized exactly, with host reads, rather than risk a redo)
   bool async0 = v->est_n0 > 0 && v->est_pairs >= 0 && v->est_bin0 >= 0 && n_ph >= 2 &&
-                spec_phase >= 0 && !chunked && !exact && !cam_moved;
+                spec_phase >= 0 && !chunked && !cam_moved;
   if (std::getenv("NXS_DEBUG_PLAN"))
     std::fprintf(stderr, "plan P=%lld n_ph=%d R1=%lld async0=%d est_n0=%lld est_bin0=%d hint=%llu\n",
                  (long long)P, n_ph, (long long)R[1], (int)async0, (long long)v->est_n0,
@@ -913,6 +914,13 @@ retry_sort:
     NXS_CUDA(ensure_n<int32_t>(v->r_count, npix));
     NXS_CUDA(ensure_n<float>(v->r_sea, npix * 3));
     NXS_CUDA(ensure_n<float>(v->r_sa, npix));
+    if (exact) {  // the exact order's phase 0: sequences, z_lo per rank, pending carry
+      NXS_CUDA(ensure_n<int32_t>(v->seq, npix * std::max(1, opts->max_splats)));
+      NXS_CUDA(ensure_n<float>(v->zlo_rank, P));
+      NXS_CUDA(ensure_n<float>(v->xc_t, (int64_t)32 * npix));
+      NXS_CUDA(ensure_n<int32_t>(v->xc_r, (int64_t)32 * npix));
+      NXS_CUDA(ensure_n<int32_t>(v->xc_n, npix));
+    }
   }
   if (async0 && !getenv("NXS_NO_GRAPH")) {
     // record on the view's own stream (the caller's may be the legacy default
@@ -1097,6 +1105,30 @@ retry_sort:
   const int tbits = bits_for((uint32_t)std::max(n_tiles, 2));
   int64_t total_pairs = 0;
   int ph_done = 0;
+  // end the phase-0 capture (after its forward kernel) and launch the graph
+  auto end_capture = [&]() -> int {
+    cudaGraph_t g = nullptr;
+    cap.on = false;
+    v->capturing = false;
+    NXS_CUDA(cudaStreamEndCapture(s, &g));
+    s = s_caller;
+    cudaGraphExecUpdateResultInfo info;
+    if (!v->gexec || cudaGraphExecUpdate(v->gexec, g, &info) != cudaSuccess) {
+      cudaGetLastError();
+      if (v->gexec) cudaGraphExecDestroy(v->gexec);
+      v->gexec = nullptr;
+      const cudaError_t e = cudaGraphInstantiate(&v->gexec, g, 0);
+      if (e != cudaSuccess) {
+        cudaGraphDestroy(g);
+        v->gexec = nullptr;
+        return fail(NXS_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+      }
+    }
+    cudaGraphDestroy(g);
+    NXS_CUDA(cudaGraphLaunch(v->gexec, s));
+    g_ht.mark("graph");
+    return NXS_OK;
+  };
   for (int ph = 0; ph < n_ph; ++ph) {
     int64_t r0 = R[ph], r1 = R[ph + 1], nr = r1 - r0;
     if (v->ev_ok) rec_event(v, v->evp[ph][0], s);
@@ -1150,12 +1182,20 @@ retry_sort:
                       v->rank_of.as<uint32_t>(), dsmall + 10, s);
       NXS_LAUNCHED("bin_sort");
       if (v->ev_ok) rec_event(v, v->evp[0][1], s);
-      launch_project_ranks(scene->centers, scene->scales, scene->quats, scene->opacities,
-                           scene->sh, C, 0, cap0, v->idx_out.as<uint32_t>(), cam,
-                           opts->alpha_cutoff, opts->near_plane, v->rects.as<int4>(),
-                           v->records.as<float4>(), v->bframe.as<float4>(), dsmall,
-                           v->tq.as<double>(), s, n_sel,
-                           v->async_bases ? v->live.as<uint32_t>() : nullptr, dsmall + 15);
+      if (exact)  // (z_lo per rank too: the pending-buffer bounds)
+        launch_project_ranks_z(scene->centers, scene->scales, scene->quats, scene->opacities,
+                               scene->sh, C, 0, cap0, v->idx_out.as<uint32_t>(), cam,
+                               opts->alpha_cutoff, opts->near_plane, v->depth.as<double>(),
+                               v->zlo_rank.as<float>(), v->rects.as<int4>(),
+                               v->records.as<float4>(), v->bframe.as<float4>(), dsmall,
+                               v->tq.as<double>(), s, n_sel);
+      else
+        launch_project_ranks(scene->centers, scene->scales, scene->quats, scene->opacities,
+                             scene->sh, C, 0, cap0, v->idx_out.as<uint32_t>(), cam,
+                             opts->alpha_cutoff, opts->near_plane, v->rects.as<int4>(),
+                             v->records.as<float4>(), v->bframe.as<float4>(), dsmall,
+                             v->tq.as<double>(), s, n_sel,
+                             v->async_bases ? v->live.as<uint32_t>() : nullptr, dsmall + 15);
       NXS_LAUNCHED("project_ranks");
       if (v->ev_ok) rec_event(v, v->evp[0][2], s);
       NXS_CUDA(ensure_n<int2>(v->ranges_ph[0], n_tiles));
@@ -1472,7 +1512,9 @@ retry_sort:
         NXS_CUDA(ensure_n<int32_t>(v->xc_n, npix));
         if (ph + 1 < n_ph) {
           ebound = reinterpret_cast<float*>(v->ph_sel.as<long long>() + 90);
-          launch_phase_bound(dsmall + 6, ph_bin[ph], ebound, s);
+          // (a device-sized phase 0 ends at the selection's bin, dsel[0])
+          launch_phase_bound(dsmall + 6, ph_bin[ph], ebound, s,
+                             (async0 && ph == 0) ? v->ph_sel.as<long long>() : nullptr);
           NXS_LAUNCHED("phase_bound");
         }
       }
@@ -1492,6 +1534,10 @@ retry_sort:
       NXS_LAUNCHED("blend_fwd_x");
       if (v->ev_ok) rec_event(v, v->evp[ph][4], s);
       ph_done = ph + 1;
+      if (cap.on && ph == 0) {
+        const int erc = end_capture();
+        if (erc) return erc;
+      }
       continue;
     }
     // ---- K3 forward blend of this phase (tiles still active; phase 0's
@@ -1509,26 +1555,8 @@ retry_sort:
     if (v->ev_ok) rec_event(v, v->evp[ph][4], s);
     ph_done = ph + 1;
     if (cap.on && ph == 0) {
-      cudaGraph_t g = nullptr;
-      cap.on = false;
-      v->capturing = false;
-      NXS_CUDA(cudaStreamEndCapture(s, &g));
-      s = s_caller;
-      cudaGraphExecUpdateResultInfo info;
-      if (!v->gexec || cudaGraphExecUpdate(v->gexec, g, &info) != cudaSuccess) {
-        cudaGetLastError();
-        if (v->gexec) cudaGraphExecDestroy(v->gexec);
-        v->gexec = nullptr;
-        const cudaError_t e = cudaGraphInstantiate(&v->gexec, g, 0);
-        if (e != cudaSuccess) {
-          cudaGraphDestroy(g);
-          v->gexec = nullptr;
-          return fail(NXS_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
-        }
-      }
-      cudaGraphDestroy(g);
-      NXS_CUDA(cudaGraphLaunch(v->gexec, s));
-      g_ht.mark("graph");
+      const int erc = end_capture();
+      if (erc) return erc;
     }
   }
   mark(v, 7, s);
@@ -1795,7 +1823,14 @@ int nxs_forward_backward(nxs_view* v, const nxs_scene* scene, const nxs_camera* 
       ++v->stats.n_redo;
       if ((rc = backward_chain(v, scene, nullptr, nullptr, nullptr, nullptr, nullptr, s)))
         return rc;
-      if (spec_check && !async_check) NXS_CUDA(cudaEventSynchronize(v->ev_sync));  // (its copy lands first)
+      if (spec_check) {  // (the check's copies land before the rerun reuses their slots)
+        bool ok_unused = true;
+        if (async_check) {
+          if ((rc = finish_async_check(v, ok_unused))) return rc;
+        } else {
+          NXS_CUDA(cudaEventSynchronize(v->ev_sync));
+        }
+      }
       v->spec_pending = v->async_pending = false;
       v->phases_needed = 0;
       if ((rc = nxs_forward(v, scene, camera, model, opts, background, rgb, overdraw, residual,

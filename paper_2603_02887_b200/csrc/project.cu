@@ -1839,8 +1839,9 @@ void launch_pack_check(const unsigned long long* dsmall, const long long* dsel, 
 // every Gaussian in the key bins after `bin` (the k_key32 map inverted, with
 // a relative safety margin; smaller is always safe), as float rounded down
 __global__ void k_phase_bound(const unsigned long long* __restrict__ kminmax, int bin,
-                              float* __restrict__ out) {
+                              float* __restrict__ out, const long long* __restrict__ dbin) {
   nxs_pdl_enter();
+  if (dbin) bin = (int)dbin[0];  // (a device-sized phase: its last bin from the selection)
   if (kminmax[0] < kminmax[1]) {
     const double lo = dkey_inv(kminmax[0]), hi = dkey_inv(kminmax[1]);
     const double step = (double)((unsigned long long)(bin + 1) << 20) / (4294967294.0 / (hi - lo));
@@ -1850,8 +1851,9 @@ __global__ void k_phase_bound(const unsigned long long* __restrict__ kminmax, in
     *out = __int_as_float(0xff800000);  // -inf: nothing is final at the phase end
   }
 }
-void launch_phase_bound(const unsigned long long* kminmax, int bin, float* out, cudaStream_t s) {
-  nxs_launch(k_phase_bound, 1, 1, 0, s, kminmax, bin, out);
+void launch_phase_bound(const unsigned long long* kminmax, int bin, float* out, cudaStream_t s,
+                        const long long* dbin) {
+  nxs_launch(k_phase_bound, 1, 1, 0, s, kminmax, bin, out, dbin);
 }
 void launch_iota(uint32_t* a, int64_t n, cudaStream_t s) {
   if (n <= 0) return;
@@ -1886,12 +1888,11 @@ void launch_project_ranks_z(const float* centers, const float* scales, const flo
                             int64_t r1, const uint32_t* order, const CamDev& cam, double cutoff,
                             double near_plane, const double* zlo, float* zlo_rank, int4* rects,
                             float4* records, float4* bframe, unsigned long long* straddle,
-                            double* tq, cudaStream_t s) {
+                            double* tq, cudaStream_t s, const int* nd) {
   if (r1 <= r0) return;
   ProjOut o{zlo, zlo_rank, rects, records, bframe, straddle, tq};
   nxs_launch(k_project_ranks, (unsigned)((r1 - r0 + PROJ_CHUNK - 1) / PROJ_CHUNK), PROJ_CHUNK, 0, s, 
-      centers, scales, quats, opacities, sh, C, r0, r1, order, cam, cutoff, near_plane, o,
-      nullptr);
+      centers, scales, quats, opacities, sh, C, r0, r1, order, cam, cutoff, near_plane, o, nd);
 }
 void launch_clear_rects(const uint32_t* order, int64_t r0, int64_t r1, int4* rects,
                         cudaStream_t s) {
