@@ -77,7 +77,8 @@ void launch_iota(uint32_t*, int64_t, cudaStream_t);
 void launch_phase_bound(const unsigned long long*, int, float*, cudaStream_t,
                         const long long* dbin = nullptr);
 void launch_zlo_ranks(const float*, const float*, const float*, const float*, const uint32_t*,
-                      int64_t, int64_t, const CamDev&, double, double*, cudaStream_t);
+                      int64_t, int64_t, const CamDev&, double, double*, cudaStream_t,
+                      const int* nd = nullptr);
 void launch_project_ranks_z(const float*, const float*, const float*, const float*, const float*,
                             int, int64_t, int64_t, const uint32_t*, const CamDev&, double, double,
                             const double*, float*, int4*, float4*, float4*, unsigned long long*,
@@ -108,7 +109,10 @@ void launch_compact_lists(const uint32_t*, const int2*, const int*, int, uint32_
 void launch_chunk_key(const float*, const float*, const float*, const float*, int64_t,
                       const CamDev&, double, const uint32_t*, int, double*, unsigned long long*,
                       uint32_t*, cudaStream_t);
-bool launch_chunk_sort(const uint32_t*, const double*, int64_t, int, uint32_t*, cudaStream_t);
+bool launch_chunk_sort(const uint32_t*, const double*, int64_t, int, uint32_t*, cudaStream_t,
+                       const int* nd = nullptr);
+void launch_chunk_count(const int*, int64_t, int, int*, cudaStream_t);
+void launch_copy_u32(const uint32_t*, int64_t, const int*, uint32_t*, cudaStream_t);
 void launch_project(const float*, const float*, const float*, const float*, const float*, int,
                     int64_t, const uint32_t*, const CamDev&, double, double, const double*,
                     float*, int4*, float4*, float4*, unsigned long long*, double*, cudaStream_t);
@@ -274,6 +278,7 @@ struct nxs_view {
   int64_t est_n0 = 0, est_pairs = 0;
   int est_bin0 = -1;
   bool async_pending = false;  // phase 0 ran device-sized, not yet verified
+  int64_t async_chunk = 0;     // its chunk size (chunked order: whole chunks were projected)
   // fused call, t-ordered modes: the forward's pending-buffer overflow count
   // (host_small[28]) is read behind the backward instead of before it
   bool defer_ovf = false, ovf_pending = false;
@@ -693,6 +698,8 @@ int finish_async_check(nxs_view* v, bool& ok) {
   v->stats.n_pairs = (int64_t)pairs;
   v->stats.n_straddling = (int64_t)v->host_small[2];
   v->sorted_end = v->proj_end = n0;
+  if (v->async_chunk > 1 && n0 < v->P)  // (chunked: only whole chunks were projected)
+    v->proj_end = n0 / v->async_chunk * v->async_chunk;
   v->bin_done = (int)hsel[0];
   return NXS_OK;
 }
@@ -870,7 +877,7 @@ int forward_impl(nxs_view* v, const nxs_scene* scene, const nxs_camera* camera,
   // (a new camera's depth-key histogram differs: its phase-0 bins and pair
   // count are sized exactly, with host reads, rather than risk a redo)
   bool async0 = v->est_n0 > 0 && v->est_pairs >= 0 && v->est_bin0 >= 0 && n_ph >= 2 &&
-                spec_phase >= 0 && !chunked && !cam_moved;
+                spec_phase >= 0 && !cam_moved && (!chunked || opts->chunk_size <= 2048);
   if (std::getenv("NXS_DEBUG_PLAN"))
     std::fprintf(stderr, "plan P=%lld n_ph=%d R1=%lld async0=%d est_n0=%lld est_bin0=%d hint=%llu\n",
                  (long long)P, n_ph, (long long)R[1], (int)async0, (long long)v->est_n0,
@@ -914,9 +921,15 @@ retry_sort:
     NXS_CUDA(ensure_n<int32_t>(v->r_count, npix));
     NXS_CUDA(ensure_n<float>(v->r_sea, npix * 3));
     NXS_CUDA(ensure_n<float>(v->r_sa, npix));
-    if (exact) {  // the exact order's phase 0: sequences, z_lo per rank, pending carry
+    if (torder) {  // t-ordered phase 0: sequences, z_lo per rank, pending carry
       NXS_CUDA(ensure_n<int32_t>(v->seq, npix * std::max(1, opts->max_splats)));
       NXS_CUDA(ensure_n<float>(v->zlo_rank, P));
+    }
+    if (chunked) {  // chunk ids (centre-depth ranks), z_lo per Gaussian
+      NXS_CUDA(ensure_n<uint32_t>(v->rank_c, P));
+      NXS_CUDA(ensure_n<double>(v->zlo64, P));
+    }
+    if (exact) {
       NXS_CUDA(ensure_n<float>(v->xc_t, (int64_t)32 * npix));
       NXS_CUDA(ensure_n<int32_t>(v->xc_r, (int64_t)32 * npix));
       NXS_CUDA(ensure_n<int32_t>(v->xc_n, npix));
@@ -1144,6 +1157,7 @@ retry_sort:
         NXS_CUDA(cudaMemsetAsync(v->active.p, 1, (size_t)n_tiles, s));
         goto retry_sort;
       }
+      if (chunked) proc_end = v->proj_end;  // (the next phase starts at the partial chunk)
       total_pairs += v->ph_pairs[0];
       const long long* hsel = reinterpret_cast<const long long*>(v->host_small + 16);
       int m = 0;
@@ -1179,10 +1193,34 @@ retry_sort:
       NXS_LAUNCHED("bin_scatter");
       launch_bin_sort(v->idx_out.as<uint32_t>(), v->depth.as<double>(),
                       v->ph_hist.as<unsigned int>(), v->bin_pos.as<uint32_t>(), 0, ph_bin[0], dsel,
-                      v->rank_of.as<uint32_t>(), dsmall + 10, s);
+                      chunked ? v->rank_c.as<uint32_t>() : v->rank_of.as<uint32_t>(), dsmall + 10,
+                      s);
       NXS_LAUNCHED("bin_sort");
       if (v->ev_ok) rec_event(v, v->evp[0][1], s);
-      if (exact)  // (z_lo per rank too: the pending-buffer bounds)
+      if (chunked) {
+        // whole chunks of the selected Gaussians (the partial last one waits
+        // for the next phase): z_lo, per-chunk z_lo sort, ranks, projection
+        int* n_ch = reinterpret_cast<int*>(v->ph_sel.as<long long>() + 52);
+        launch_chunk_count(n_sel, P, opts->chunk_size, n_ch, s);
+        launch_zlo_ranks(scene->centers, scene->scales, scene->quats, scene->opacities,
+                         v->idx_out.as<uint32_t>(), 0, cap0, cam, opts->alpha_cutoff,
+                         v->zlo64.as<double>(), s, n_ch);
+        NXS_LAUNCHED("zlo_ranks");
+        launch_chunk_sort(v->idx_out.as<uint32_t>(), v->zlo64.as<double>(), cap0,
+                          (int)opts->chunk_size, v->idx_in.as<uint32_t>(), s, n_ch);
+        NXS_LAUNCHED("chunk_sort");
+        launch_copy_u32(v->idx_in.as<uint32_t>(), cap0, n_ch, v->idx_out.as<uint32_t>(), s);
+        launch_rank_of_range(v->idx_out.as<uint32_t>(), 0, cap0, v->rank_of.as<uint32_t>(), s,
+                             n_ch);
+        NXS_LAUNCHED("rank_of");
+        launch_project_ranks_z(scene->centers, scene->scales, scene->quats, scene->opacities,
+                               scene->sh, C, 0, cap0, v->idx_out.as<uint32_t>(), cam,
+                               opts->alpha_cutoff, opts->near_plane, v->zlo64.as<double>(),
+                               v->zlo_rank.as<float>(), v->rects.as<int4>(),
+                               v->records.as<float4>(), v->bframe.as<float4>(), dsmall,
+                               v->tq.as<double>(), s, n_ch);
+        n_sel = n_ch;  // the binning below takes the processed (whole-chunk) ranks
+      } else if (exact)  // (z_lo per rank too: the pending-buffer bounds)
         launch_project_ranks_z(scene->centers, scene->scales, scene->quats, scene->opacities,
                                scene->sh, C, 0, cap0, v->idx_out.as<uint32_t>(), cam,
                                opts->alpha_cutoff, opts->near_plane, v->depth.as<double>(),
@@ -1245,6 +1283,7 @@ retry_sort:
       mark(v, 6, s);
       if (v->ev_ok) rec_event(v, v->evp[0][3], s);
       v->async_pending = true;
+      v->async_chunk = chunked ? opts->chunk_size : 0;
       v->ph_pairs[0] = capp;  // capacity; the real count comes with the check
     } else {
       if (v->lazy) {

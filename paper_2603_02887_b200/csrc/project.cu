@@ -673,8 +673,10 @@ __global__ void k_chunk_key(const float* __restrict__ centers, const float* __re
 template <int THREADS, int ITEMS>
 __global__ void __launch_bounds__(THREADS)
     k_chunk_sort(const uint32_t* __restrict__ order_c, const double* __restrict__ zlo, int64_t P,
-                 int chunk, uint32_t* __restrict__ order_out) {
+                 int chunk, uint32_t* __restrict__ order_out, const int* __restrict__ nd) {
   nxs_pdl_enter();
+  if (nd) P = min(P, (int64_t)*nd);  // (a device-sized phase: its chunk-aligned rank count)
+  if ((int64_t)blockIdx.x * chunk >= P) return;
   using Sort = cub::BlockRadixSort<uint32_t, THREADS, ITEMS, uint32_t>;
   __shared__ typename Sort::TempStorage tmp;
   const int64_t base = (int64_t)blockIdx.x * chunk;
@@ -1742,15 +1744,15 @@ void launch_chunk_key(const float* centers, const float* scales, const float* qu
 }
 // false when the chunk is too large for one block (use the global sort)
 bool launch_chunk_sort(const uint32_t* order_c, const double* zlo, int64_t P, int chunk,
-                       uint32_t* order_out, cudaStream_t s) {
+                       uint32_t* order_out, cudaStream_t s, const int* nd) {
   if (P == 0) return true;
   const unsigned grid = (unsigned)((P + chunk - 1) / chunk);
   if (chunk <= 128)
-    nxs_launch(k_chunk_sort<128, 1>, grid, 128, 0, s, order_c, zlo, P, chunk, order_out);
+    nxs_launch(k_chunk_sort<128, 1>, grid, 128, 0, s, order_c, zlo, P, chunk, order_out, nd);
   else if (chunk <= 512)
-    nxs_launch(k_chunk_sort<128, 4>, grid, 128, 0, s, order_c, zlo, P, chunk, order_out);
+    nxs_launch(k_chunk_sort<128, 4>, grid, 128, 0, s, order_c, zlo, P, chunk, order_out, nd);
   else if (chunk <= 2048)
-    nxs_launch(k_chunk_sort<256, 8>, grid, 256, 0, s, order_c, zlo, P, chunk, order_out);
+    nxs_launch(k_chunk_sort<256, 8>, grid, 256, 0, s, order_c, zlo, P, chunk, order_out, nd);
   else
     return false;
   return true;
@@ -1868,20 +1870,47 @@ void launch_gather_keys(const uint32_t* idx, const uint32_t* key, int64_t n, uin
 __global__ void k_zlo_ranks(const float* __restrict__ centers, const float* __restrict__ scales,
                             const float* __restrict__ quats, const float* __restrict__ opacities,
                             const uint32_t* __restrict__ order, int64_t r0, int64_t r1,
-                            CamDev cam, double cutoff, double* __restrict__ zlo) {
+                            CamDev cam, double cutoff, double* __restrict__ zlo,
+                            const int* __restrict__ nd) {
   nxs_pdl_enter();
+  if (nd) r1 = min(r1, r0 + (int64_t)*nd);
   const int64_t r = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= r1) return;
   const int64_t g = order[r];
   zlo[g] = z_lower(centers, scales, quats, opacities, g, cam, cutoff);
 }
+// device-sized chunked phase 0: its chunk-aligned rank count (whole chunks of
+// the selected n Gaussians, or all P) and a copy of that many ranks
+__global__ void k_chunk_count(const int* __restrict__ n_sel, int64_t P, int chunk,
+                              int* __restrict__ out) {
+  const int64_t n = *n_sel;
+  *out = (int)(n >= P ? P : (n / chunk) * (int64_t)chunk);
+}
+__global__ void k_copy_u32(const uint32_t* __restrict__ src, int64_t n,
+                           const int* __restrict__ nd, uint32_t* __restrict__ dst) {
+  nxs_pdl_enter();
+  if (nd) n = min(n, (int64_t)*nd);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+void launch_chunk_count(const int* n_sel, int64_t P, int chunk, int* out, cudaStream_t s) {
+  nxs_launch(k_chunk_count, 1, 1, 0, s, n_sel, P, chunk, out);
+}
+void launch_copy_u32(const uint32_t* src, int64_t n, const int* nd, uint32_t* dst,
+                     cudaStream_t s) {
+  if (n <= 0) return;
+  nxs_launch(k_copy_u32, (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 8), 256, 0, s, src,
+             n, nd, dst);
+}
 void launch_zlo_ranks(const float* centers, const float* scales, const float* quats,
                       const float* opacities, const uint32_t* order, int64_t r0, int64_t r1,
-                      const CamDev& cam, double cutoff, double* zlo, cudaStream_t s) {
+                      const CamDev& cam, double cutoff, double* zlo, cudaStream_t s,
+                      const int* nd) {
   if (r1 <= r0) return;
   nxs_launch(k_zlo_ranks, (unsigned)((r1 - r0 + 255) / 256), 256, 0, s, centers, scales, quats,
                                                                 opacities, order, r0, r1, cam,
-                                                                cutoff, zlo);
+                                                                cutoff, zlo, nd);
 }
 void launch_project_ranks_z(const float* centers, const float* scales, const float* quats,
                             const float* opacities, const float* sh, int C, int64_t r0,
