@@ -649,11 +649,13 @@ def test_fused_forward_backward_matches_separate_calls():
                                        atol=1e-7 * float(r_g[k].abs().max()), err_msg=k)
 
 
-def test_device_sized_first_phase_matches_fresh_views():
+@pytest.mark.parametrize("chunk", [1, None, 64])
+def test_device_sized_first_phase_matches_fresh_views(chunk):
     """A view sizes its first depth phase from its previous call (no host
     sync before the first forward) and verifies behind it.  Repeated calls
     on one view — same camera, a camera needing more pairs, a larger scene,
-    a different model — must equal fresh-view results bit for bit."""
+    a different model — must equal fresh-view results bit for bit, in the
+    global, exact and chunked orders."""
     import torch
     from paper_2603_02887_b200 import (_native, backward_device, forward_backward_device,
                                        forward_device)
@@ -674,15 +676,16 @@ def test_device_sized_first_phase_matches_fresh_views():
         for dev, cam, name in plan:
             model = MODELS[name]
             ref_view = _native.View()
-            r_out = forward_device(ref_view, dev, cam, model, np.zeros(3))
+            r_out = forward_device(ref_view, dev, cam, model, np.zeros(3), chunk_size=chunk)
             r_g = backward_device(ref_view, dev, seed)
             if fused:
-                out, g = forward_backward_device(view, dev, cam, model, np.zeros(3), seed)
+                out, g = forward_backward_device(view, dev, cam, model, np.zeros(3), seed,
+                                                 chunk_size=chunk)
             else:
-                out = forward_device(view, dev, cam, model, np.zeros(3))
+                out = forward_device(view, dev, cam, model, np.zeros(3), chunk_size=chunk)
                 g = backward_device(view, dev, seed)
             for a, b in zip(r_out, out):
-                assert torch.equal(a, b), (fused, name)
+                assert torch.equal(a, b), (fused, name, chunk)
             for k in GRAD_FIELDS:
                 np.testing.assert_allclose(g[k].cpu().numpy(), r_g[k].cpu().numpy(), rtol=1e-5,
                                            atol=1e-7 * float(r_g[k].abs().max()), err_msg=k)
