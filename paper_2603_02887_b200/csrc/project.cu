@@ -1936,8 +1936,13 @@ void launch_key32_hist_select(const double* depth, int64_t P, const unsigned lon
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const unsigned grid =
-      (unsigned)std::max<int64_t>(1, std::min<int64_t>((P + 4095) / 4096, (int64_t)sms * 2));
+#ifndef NXS_HIST_GRID_DIV
+#define NXS_HIST_GRID_DIV 2
+#endif
+  // (each block flushes its whole shared histogram with global atomics:
+  // fewer, longer blocks trade key-pass parallelism for fewer flushes)
+  const unsigned grid = (unsigned)std::max<int64_t>(
+      1, std::min<int64_t>((P + 4095) / 4096, (int64_t)sms * 2 / NXS_HIST_GRID_DIV));
   nxs_launch(k_key32_hist_select, grid, 1024, 0, s, depth, P, kminmax, key, hist, targets,
              n_targets, out, max_bin0, overflow, bin_pos, n_sel);
 }
