@@ -350,22 +350,22 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
       }
       int i = nb;
       uint32_t gid_new = 0xffffffffu;
+      // slot pointers walked down the ring (no index arithmetic per shift)
+      int f = (head + nb) & (XBUF - 1);
       while (i > 0) {
-        const int e = (head + i - 1) & (XBUF - 1);
+        const int e = (f - 1) & (XBUF - 1);
         const float2 qe = myq[e * TILE_PIX];
-        bool later = qe.x > tpk;
+        if (!(qe.x >= tpk)) break;  // (NaN: stop, as before)
         if (qe.x == tpk) {
           if (gid_new == 0xffffffffu) gid_new = tie_key(rk);
           const int pe = __float_as_int(qe.y);
-          later = tie_key(pe < 0 ? (uint32_t)(-1 - pe) : pairs[pe]) > gid_new;
+          if (!(tie_key(pe < 0 ? (uint32_t)(-1 - pe) : pairs[pe]) > gid_new)) break;
         }
-        if (!later) break;
-        const int f = (head + i) & (XBUF - 1);
         myq[f * TILE_PIX] = qe;
         if constexpr (keeps_alpha(XBUF)) mya[f * TILE_PIX] = mya[e * TILE_PIX];
+        f = e;
         --i;
       }
-      const int f = (head + i) & (XBUF - 1);
       NXS_CHECK(nb < XBUF && i >= 0 && i <= nb);
       myq[f * TILE_PIX] = make_float2(tpk, __int_as_float(pos));
       if constexpr (keeps_alpha(XBUF)) mya[f * TILE_PIX] = t.alpha;
@@ -440,22 +440,23 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
           const int pos = base + j;
           int i = nb;
           uint32_t gid_new = 0xffffffffu;
+          // slot index walked down the ring (no index arithmetic per shift)
+          int f = (head + nb) & (XBUF - 1);
           while (i > 0) {
-            const int e = (head + i - 1) & (XBUF - 1);
+            const int e = (f - 1) & (XBUF - 1);
             const float2 qe = myq[e * TILE_PIX];
-            bool later = qe.x > tpk;  // the pending entry commits after the new one
+            // the pending entry commits after the new one: shift it
+            if (!(qe.x >= tpk)) break;
             if (qe.x == tpk) {
               if (gid_new == 0xffffffffu) gid_new = tie_key(s_rank[j]);
               const int pe = __float_as_int(qe.y);
-              later = tie_key(pe < 0 ? (uint32_t)(-1 - pe) : pairs[pe]) > gid_new;
+              if (!(tie_key(pe < 0 ? (uint32_t)(-1 - pe) : pairs[pe]) > gid_new)) break;
             }
-            if (!later) break;
-            const int f = (head + i) & (XBUF - 1);
             myq[f * TILE_PIX] = qe;
             if constexpr (keeps_alpha(XBUF)) mya[f * TILE_PIX] = mya[e * TILE_PIX];
+            f = e;
             --i;
           }
-          const int f = (head + i) & (XBUF - 1);
           NXS_CHECK(nb < XBUF && i >= 0 && i <= nb);
   #ifdef NXS_XSTATS
           atomicAdd(&g_xstats[0], 1ull);
