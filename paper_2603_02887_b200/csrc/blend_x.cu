@@ -234,6 +234,10 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
   // commit the smallest pending entry: its alpha was kept at insertion, the
   // emission re-reads the record's SH words (staged ring, else L1/L2)
   int ring_lo = 0;  // list positions [ring_lo, current batch end) are staged
+  // where a list position's rank is read: the pair list, or (exact order)
+  // the tile's ranks staged in shared memory, indexed from lbase
+  const uint32_t* lpairs = pairs;
+  int lbase = 0;
   auto commit_front = [&]() {
     NXS_CHECK(nb > 0 && head >= 0 && head < XBUF);
     const int pos = __float_as_int(myq[head * TILE_PIX].y);
@@ -252,7 +256,7 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
 #pragma unroll
       for (int k = K0; k < K1; ++k) r[k] = rec[k];
     } else {
-      rank = pos < 0 ? (uint32_t)(-1 - pos) : pairs[pos];
+      rank = pos < 0 ? (uint32_t)(-1 - pos) : lpairs[pos - lbase];
       const float4* rec = records + (size_t)rank * REC_F4;
 #pragma unroll
       for (int k = K0; k < K1; ++k) r[k] = __ldg(rec + k);
@@ -287,10 +291,23 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
   // 0.745 ms, exponential 10.56 -> 5.94 ms at C3; unstaged without the
   // prefetch was 12 % slower than staged for the saturating models)
   ring_lo = 0x7fffffff;  // (commits re-read their records the same way)
+  {
+    // the tile's ranks in shared memory (the staged ring's space, unused in
+    // this order) when they fit: one barrier, then every read is an LDS
+    constexpr int LIST_CAP = 2 * XBT * REC_F4 * 4;
+    const int nlist = rg.y - rg.x;
+    if (nlist <= LIST_CAP) {  // (block-uniform)
+      uint32_t* s_list = reinterpret_cast<uint32_t*>(smem_dyn);
+      for (int k = threadIdx.x; k < nlist; k += blockDim.x) s_list[k] = __ldg(pairs + rg.x + k);
+      __syncthreads();
+      lpairs = s_list;
+      lbase = rg.x;
+    }
+  }
   if (!s.done) {
     // software pipeline: ranks two entries ahead, the test words and z_lo
     // of the next entry one ahead (in registers)
-    auto ldrank = [&](int q) { return q < rg.y ? __ldg(pairs + q) : 0u; };
+    auto ldrank = [&](int q) { return q < rg.y ? lpairs[q - lbase] : 0u; };
     uint32_t rk_cur = ldrank(rg.x), rk_n1 = ldrank(rg.x + 1);
     float4 c0, c1, c2, c3, c7;
     float zc;
@@ -359,7 +376,7 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
         if (qe.x == tpk) {
           if (gid_new == 0xffffffffu) gid_new = tie_key(rk);
           const int pe = __float_as_int(qe.y);
-          if (!(tie_key(pe < 0 ? (uint32_t)(-1 - pe) : pairs[pe]) > gid_new)) break;
+          if (!(tie_key(pe < 0 ? (uint32_t)(-1 - pe) : lpairs[pe - lbase]) > gid_new)) break;
         }
         myq[f * TILE_PIX] = qe;
         if constexpr (keeps_alpha(XBUF)) mya[f * TILE_PIX] = mya[e * TILE_PIX];
