@@ -333,7 +333,8 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
       {
         const unsigned am = __activemask();
         const unsigned want = __ballot_sync(am, nb > 0 && thead < bound);
-        go_commit = __popc(want) * 32 >= NXS_X_DEFER * __popc(am) || nb >= XBUF - 4;
+        go_commit = (NXS_X_DEFER >= 32 ? want == am : __popc(want) * 32 >= NXS_X_DEFER * __popc(am)) ||
+                    nb >= XBUF - 4;
       }
       while (go_commit && nb > 0 && thead < bound) {
 #else
@@ -426,7 +427,8 @@ __global__ void __launch_bounds__(TILE_PIX, XBUF <= 16 ? 3 : 2)
           if (!go_commit) {
             const unsigned am = __activemask();
             const unsigned want = __ballot_sync(am, nb > 0 && thead < bound);
-            go_commit = __popc(want) * 32 >= NXS_X_DEFER * __popc(am) || nb >= XBUF - 4;
+            go_commit = (NXS_X_DEFER >= 32 ? want == am : __popc(want) * 32 >= NXS_X_DEFER * __popc(am)) ||
+                    nb >= XBUF - 4;
           }
           while (go_commit && nb > 0 && (next_chunk || thead < bound)) {
   #else
