@@ -586,14 +586,16 @@ constexpr size_t BWDX_WARP_FLOATS = NMOM * XRED_STRIDE + 2 * XREC_F4 * 4;
 // (per block: one warp slot per warp; NP pixels per thread)
 constexpr size_t bwdx_smem(int np) { return sizeof(float) * BWDX_WARP_FLOATS * (np == 1 ? 1 : TILE_PIX / np / 32); }
 
-// Two pixels per thread (adjacent rows, a warp = one 8x8 block, a 128-thread
-// block per tile, as K4): each warp step serves the largest pending rank over its 64 pixels,
-// and a thread adds both of its pixels' moments before the warp reduction.
-// The exact order runs one pixel per thread (256-thread blocks, a warp =
-// an 8x4 block: smaller warp footprints take fewer lock-step rank steps, and
-// 91 registers): exact-order bwd 0.715 -> 0.694 ms, exponential 8.19 ->
-// 7.89; the chunked order keeps two (its chunk-sorted sequences step
-// together better: 0.368 vs 0.405 ms).
+// Each warp step serves the largest pending rank over the warp's pixels; the
+// pixels whose entry it is take part, and the warp reduces their moments.
+// Chunked order (k_blend_bwd_x2): two pixels per thread (adjacent rows, a
+// warp = one 8x8 block, a 128-thread block per tile, as K4), a thread adding
+// both pixels' moments before the warp reduction.  Exact order
+// (k_blend_bwd_x1): one pixel per thread (a warp = an 8x4 block: smaller
+// footprints take fewer lock-step steps) and one warp per block, so a warp
+// that finishes its steps frees its slot at once (the warps of a tile share
+// nothing): exact-order bwd 0.715 -> 0.616 ms; the chunked order's warps
+// finish together and keep the two-pixel, four-warp blocks.
 
 template <int FAM, bool COUNT, int XNP>
 __device__ __forceinline__ void bwd_x_body(const float4* __restrict__ records, const float4* __restrict__ bframe,
