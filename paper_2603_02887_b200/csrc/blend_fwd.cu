@@ -22,7 +22,10 @@
 
 namespace nxs {
 
-constexpr int FWD_BATCH = 64;  // list entries per staged batch
+#ifndef NXS_FWD_BATCH
+#define NXS_FWD_BATCH 128
+#endif
+constexpr int FWD_BATCH = NXS_FWD_BATCH;  // list entries per staged batch
 #ifndef NXS_FWD_MINB
 #define NXS_FWD_MINB 3
 #endif
