@@ -778,7 +778,10 @@ __device__ __forceinline__ void bwd_x_body(const float4* __restrict__ records, c
 // (the two block shapes as separate kernels so each gets its own register
 // budget: 91-103 registers at one pixel per thread, 128 at two)
 template <int FAM, bool COUNT>
-__global__ void __launch_bounds__(32, 1) k_blend_bwd_x1(const float4* __restrict__ records, const float4* __restrict__ bframe,
+#ifndef NXS_X1_MINB
+#define NXS_X1_MINB 20  // (96 registers: 21 one-warp blocks per SM; 22+ spills)
+#endif
+__global__ void __launch_bounds__(32, NXS_X1_MINB) k_blend_bwd_x1(const float4* __restrict__ records, const float4* __restrict__ bframe,
                   const uint32_t* __restrict__ pairs, const int32_t* __restrict__ seq,
                   int max_splats, CamDev cam, ModelDev m, float cutoff, double near_plane,
                   float bg0, float bg1, float bg2, const float* __restrict__ seed,
