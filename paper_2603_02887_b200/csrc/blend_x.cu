@@ -594,7 +594,8 @@ constexpr size_t bwdx_smem(int np) { return sizeof(float) * BWDX_WARP_FLOATS * (
 // (k_blend_bwd_x1): one pixel per thread (a warp = an 8x4 block: smaller
 // footprints take fewer lock-step steps) and one warp per block, so a warp
 // that finishes its steps frees its slot at once (the warps of a tile share
-// nothing): exact-order bwd 0.715 -> 0.616 ms; the chunked order's warps
+// nothing): exact-order bwd 0.715 -> 0.616 ms, 0.566 with 20 blocks per SM
+// (NXS_X1_MINB); the chunked order's warps
 // finish together and keep the two-pixel, four-warp blocks.
 
 template <int FAM, bool COUNT, int XNP>
